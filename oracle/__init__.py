@@ -1,0 +1,126 @@
+"""fp64 CPU oracle for one bifurcated-attention decode step (arXiv 2403.08845).
+
+TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and the
+``cpu_baseline`` / ``--impl reference`` legs of ``bench.py`` may import this
+package.  The product package ``paper_2403_08845_b200`` never imports it and
+shares no code with it (see the header of ``oracle/oracle.c``).
+
+``oracle.c`` holds the arithmetic: the plain definition of generalized
+multi-query attention, Eq. 1-2, over the context KV
+replicated into each sample's cache, and the paper's bifurcated algorithm,
+Eq. 3-4, for the App. E.1 exactness invariant.  This module
+only marshals arguments (ctypes) and builds the library with gcc.
+
+Parity status: pinned (tests/test_oracle_pins.py) — no function here is
+"parity unpinned".
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+OR_BF16, OR_FP32 = 0, 1
+
+
+def build(force: bool = False) -> str:
+    """Compile oracle.c with gcc (-O2, OpenMP over rows, no CUDA)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        subprocess.check_call(
+            ["gcc", "-O2", "-fopenmp", "-shared", "-fPIC", "-Wall", "-o", _LIB, _SRC, "-lm"])
+    return _LIB
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        build()
+        lib = ctypes.CDLL(_LIB)
+        P = ctypes.c_void_p
+        I = ctypes.c_int
+        args = [I, I, I, I, I, I, I, ctypes.c_double, P, P, P, P, P, P, P, I, P, P, P, I]
+        lib.oracle_attn_decode_f64.argtypes = args
+        lib.oracle_attn_decode_f64.restype = I
+        lib.oracle_bifurcated_f64.argtypes = args
+        lib.oracle_bifurcated_f64.restype = I
+        lib.oracle_kv_read_elements.argtypes = [ctypes.c_int64] * 5 + [I]
+        lib.oracle_kv_read_elements.restype = ctypes.c_int64
+        _lib = lib
+    return _lib
+
+
+def _as_np(x):
+    """Accept numpy arrays or CPU torch tensors; bf16 becomes its uint16 bits."""
+    if isinstance(x, np.ndarray):
+        return np.ascontiguousarray(x)
+    import torch  # local import: the oracle itself does not need torch
+
+    x = x.detach().contiguous()
+    if x.is_cuda:
+        x = x.cpu()
+    if x.dtype == torch.bfloat16:
+        return x.view(torch.int16).numpy().view(np.uint16)
+    if x.dtype == torch.float32:
+        return x.numpy()
+    if x.dtype == torch.int32:
+        return x.numpy()
+    raise TypeError(f"oracle: unsupported dtype {x.dtype}")
+
+
+def _ptr(a):
+    return a.ctypes.data_as(ctypes.c_void_p) if a is not None else None
+
+
+def attn_decode(q, Kc, Vc, Kd, Vd, lens, *, scale, rows=None, weights=False,
+                nthreads=1, bifurcated=False):
+    """Run the oracle.
+
+    Shapes (row-major): q [b][h][d]; Kc, Vc [g][mc][d]; Kd, Vd [b][g][md_cap][d];
+    lens int32 [b].  dtype: bf16 (as uint16 bits / torch.bfloat16) or fp32.
+    ``scale`` is the logit scale (pass the exact fp32 value the GPU uses).
+    ``rows``: optional list of flat row indices i*h + j to compute.
+    Returns (out [nrows][d] f64, lse [nrows] f64, weights [nrows][mc+md_cap] or None).
+    """
+    qn, Kcn, Vcn, Kdn, Vdn = (_as_np(t) for t in (q, Kc, Vc, Kd, Vd))
+    lensn = np.ascontiguousarray(_as_np(lens).astype(np.int32))
+    b, h, d = qn.shape
+    g, mc, d2 = Kcn.shape
+    md_cap = Kdn.shape[2]
+    assert d2 == d and Kdn.shape[:2] == (b, g) and Kdn.shape[3] == d
+    assert Vcn.shape == Kcn.shape and Vdn.shape == Kdn.shape
+    if qn.dtype == np.uint16:
+        dtype = OR_BF16
+    elif qn.dtype == np.float32:
+        dtype = OR_FP32
+    else:
+        raise TypeError(qn.dtype)
+    for t in (Kcn, Vcn, Kdn, Vdn):
+        assert t.dtype == qn.dtype
+    if rows is None:
+        rows_np = None
+        nrows = b * h
+    else:
+        rows_np = np.ascontiguousarray(np.asarray(rows, dtype=np.int32))
+        nrows = int(rows_np.size)
+    out = np.zeros((nrows, d), dtype=np.float64)
+    lse = np.zeros((nrows,), dtype=np.float64)
+    w = np.zeros((nrows, mc + md_cap), dtype=np.float64) if weights else None
+    fn = _load().oracle_bifurcated_f64 if bifurcated else _load().oracle_attn_decode_f64
+    rc = fn(b, h, g, d, mc, md_cap, dtype, float(scale), _ptr(qn), _ptr(Kcn), _ptr(Vcn),
+            _ptr(Kdn), _ptr(Vdn), _ptr(lensn), _ptr(rows_np), nrows, _ptr(out), _ptr(lse),
+            _ptr(w), int(nthreads))
+    if rc != 0:
+        raise ValueError("oracle: invalid problem")
+    return out, lse, w
+
+
+def kv_read_elements(b, g, k, mc, md, bifurcated):
+    """Eq. 5-6: KV elements read per K or V tensor."""
+    return int(_load().oracle_kv_read_elements(b, g, k, mc, md, 1 if bifurcated else 0))
