@@ -1,0 +1,163 @@
+/*
+ * bifattn.h — C ABI of libbifattn.so: one incremental-decoding step of
+ * context-aware bifurcated attention (arXiv 2403.08845) on NVIDIA B200 (sm_100a).
+ *
+ * THE OPERATION (§4.2, Eq. 3-4; code App. E.3)
+ *   b samples share one prefill context.  For sample i in [0,b) and query head
+ *   j in [0,h), with group c = j / p, p = h / g (layout `bgpnk`):
+ *     S_c[t] = scale * <q[i,j,:], Kc[c,t,:]>             t in [0, mc)
+ *                 — "einsum(bgpnk, gm_ck)": Kc has no batch axis
+ *     S_d[t] = scale * <q[i,j,:], Kd[i,c,t,:]>           t in [0, lens[i])
+ *                 — "einsum(bgpnk, bgm_dk)"
+ *     w      = softmax(S_c ⊕ S_d)   ONE softmax over the joined row
+ *                 (cat, then softmax: PAPER.md:1159-1166)
+ *     out[i,j,:] = <w_c, Vc[c]> + <w_d, Vd[i,c]>          (Eq. 4)
+ *     lse[i,j]   = ln sum_t exp(S_t)                      (natural log)
+ *   This equals ordinary generalized multi-query attention over the replicated
+ *   cache K = Kc ⊕ Kd[i] (proof App. E.1).
+ *   The device computes the joint softmax as a log-sum-exp merge of per-split
+ *   partials (m, l, o), which is the same function in exact arithmetic.
+ *
+ * LAYOUT — all tensors row-major and contiguous, all in ONE dtype (prob->dtype):
+ *   q    [b][h][d]             query of this step (n = 1 token per sample)
+ *   Kc,Vc[g][mc][d]            the single shared context cache ("compact shape
+ *                               1hm_ck or simply hm_ck")
+ *   Kd,Vd[b][g][md_cap][d]     per-sample decode caches, preallocated to md_cap;
+ *                               positions [0, lens[i]) of sample i are valid
+ *   lens int32 [b]  (device)   valid decode length per sample; values are
+ *                               clamped to [0, md_cap] on the device (a device
+ *                               cannot report errors synchronously)
+ *   out  [b][h][d]             result, rounded to nearest-even in the dtype
+ *   lse  float32 [b][h]        optional (NULL = not written)
+ *
+ * OWNERSHIP — the caller owns every buffer (PyTorch allocates them) and keeps
+ *   them alive until the work on `stream` has finished.  The library never
+ *   allocates or frees device memory per call; it caches per-device attributes
+ *   and kernel attributes under a mutex.
+ *
+ * EXECUTION — every call is asynchronous on `stream` (a cudaStream_t passed as
+ *   void*; NULL = legacy default stream), reentrant, and CUDA-graph capturable
+ *   (no host synchronisation, no allocation, lens read on the device).
+ *
+ * ERRORS — host-side checks only; a call returns BA_OK (0) or a negative code
+ *   and launches nothing on error.  There is NO CPU fallback: without an sm_100
+ *   device every compute call returns BA_ENODEV.
+ */
+#ifndef BIFATTN_H
+#define BIFATTN_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum { BA_BF16 = 0, BA_FP32 = 1 } ba_dtype_t;
+
+enum {
+  BA_OK = 0,
+  BA_EINVAL = -1,     /* bad shape: h % g != 0, b/h/g < 1, mc < 1, md_cap < 0, unsupported d */
+  BA_ENULL = -2,      /* a required pointer is NULL                                          */
+  BA_EALIGN = -3,     /* a tensor pointer is not 16-byte aligned                             */
+  BA_EWORKSPACE = -4, /* workspace NULL or smaller than ba_workspace_bytes()                */
+  BA_EDTYPE = -5,     /* dtype not BA_BF16 / BA_FP32                                         */
+  BA_ENODEV = -6,     /* no CUDA device of compute capability 10.x (sm_100a)                 */
+  BA_ECUDA = -7       /* a CUDA runtime call or kernel launch failed (see ba_last_cuda_error) */
+};
+
+/* flags (ba_problem_t.flags) */
+#define BA_FLAG_FORCE_FMA 0x1u /* route every branch through the CUDA-core FMA kernel
+                                  (tests use it to cover both kernel families)       */
+#define BA_FLAG_NO_PDL 0x2u    /* do not use programmatic dependent launch           */
+
+typedef struct {
+  int32_t b;        /* samples sharing the context, >= 1                                */
+  int32_t h;        /* query heads (rank-local when sharded), >= 1                      */
+  int32_t g;        /* KV groups (rank-local), >= 1, h % g == 0                         */
+  int32_t d;        /* head dim (k = v): 16, 32, 64, 128 or 256           */
+  int32_t mc;       /* shared context length, >= 1                                      */
+  int32_t md_cap;   /* decode-cache capacity = position stride of Kd/Vd, >= 0           */
+  ba_dtype_t dtype; /* dtype of q, Kc, Vc, Kd, Vd and out                               */
+  float scale;      /* logit scale; <= 0 means 1/sqrt(d) (the paper omits it: reading R1) */
+  uint32_t flags;   /* BA_FLAG_*; 0 for the default (fastest) path                      */
+} ba_problem_t;
+
+/* Bytes of device workspace bifurcated_attn_decode() needs (fp32 partials
+ * (m, l, o[d]) per output row and split, plus completion counters).  Returns 0
+ * for an invalid problem.  The workspace must be 16-byte aligned; its
+ * completion counters must be zero before the FIRST call (cudaMemset once);
+ * every call leaves them zero again, so it can be reused back to back on one
+ * stream without re-initialisation. */
+size_t ba_workspace_bytes(const ba_problem_t* prob);
+
+/* One decode step of bifurcated attention (see above).  Kc/Vc are read from
+ * HBM once for the whole batch; Kd/Vd once per sample.
+ *   prob              problem descriptor (host pointer)
+ *   q, Kc, Vc, Kd, Vd device pointers, layouts above, 16-byte aligned
+ *   lens              device int32 [b]
+ *   out               device [b][h][d]; must not alias any input
+ *   lse               device float32 [b][h] or NULL
+ *   workspace         device, >= ba_workspace_bytes(prob) bytes
+ *   stream            cudaStream_t (as void*)
+ * Returns BA_OK or a negative BA_E* code. */
+int bifurcated_attn_decode(const ba_problem_t* prob, const void* q, const void* Kc,
+                           const void* Vc, const void* Kd, const void* Vd,
+                           const int32_t* lens, void* out, float* lse, void* workspace,
+                           size_t workspace_bytes, void* stream);
+
+/* The same step with HOST inputs and outputs (end-to-end entry point): copies
+ * q, Kc, Vc, Kd, Vd, lens from host memory (pinned for async behaviour) into
+ * the caller-owned device buffers dq..dlens, runs bifurcated_attn_decode, and
+ * copies out (and lse if both hlse and dlse are non-NULL) back to host memory,
+ * all on `stream`.  Returns after enqueueing; synchronise the stream before
+ * reading hout. */
+int bifurcated_attn_decode_host(const ba_problem_t* prob, const void* hq, const void* hKc,
+                                const void* hVc, const void* hKd, const void* hVd,
+                                const int32_t* hlens, void* hout, float* hlse, void* dq,
+                                void* dKc, void* dVc, void* dKd, void* dVd, int32_t* dlens,
+                                void* dout, float* dlse, void* workspace,
+                                size_t workspace_bytes, void* stream);
+
+/* Non-bifurcated baseline ("K_c tensor is loaded b times"):
+ * ordinary generalized multi-query decode attention over a REPLICATED cache
+ *   K, V [b][g][mc + md_cap][d]   (context copied into every sample's cache)
+ * sample i attends to positions [0, mc + lens[i]).  Same kernels, no shared
+ * context branch.  Workspace: ba_workspace_bytes(prob). */
+int replicated_attn_decode(const ba_problem_t* prob, const void* q, const void* K,
+                           const void* V, const int32_t* lens, void* out, float* lse,
+                           void* workspace, size_t workspace_bytes, void* stream);
+
+/* Number of kernel launches one bifurcated_attn_decode() call makes for this
+ * problem on the current device (for the benchmark's launch count). <0 on error. */
+int ba_launches_per_call(const ba_problem_t* prob);
+
+/* Human-readable kernel plan for this problem (static string owned by the
+ * library, valid until the next call from the same thread). */
+const char* ba_plan_string(const ba_problem_t* prob);
+
+/* Name of kernel launch k (0-based, in launch order) of one call for this
+ * problem, e.g. "ctx_tc", "dec_fma", "merge" (static string), or NULL. */
+const char* ba_launch_name(const ba_problem_t* prob, int k);
+
+/* Instrumentation for the benchmark's per-kernel CUDA-event timing.  While
+ * set, launch k (< n) of every subsequent call made BY THIS THREAD is
+ * bracketed by cudaEventRecord(events[2k]) / cudaEventRecord(events[2k+1]) on
+ * the call's stream.  `events` are caller-created cudaEvent_t handles (as
+ * void*); the array must stay valid while set.  (NULL, 0) disables.  Recording
+ * events between launches serialises programmatic-dependent launches. */
+void ba_set_launch_events(void* const* events, int n);
+
+/* Message for a BA_* code (static string). */
+const char* ba_strerror(int code);
+
+/* The cudaError_t of the last BA_ECUDA on this thread (0 if none). */
+int ba_last_cuda_error(void);
+
+/* ABI version: 1. */
+int ba_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BIFATTN_H */

@@ -1,0 +1,269 @@
+"""B200-native bifurcated decode attention (arXiv 2403.08845).
+
+Thin Python binding over the C ABI of ``libbifattn.so`` (include/bifattn.h).
+It only marshals arguments: every step of the decode path runs in the CUDA
+kernels of ``csrc/``.  PyTorch provides device memory and streams.  There is
+no CPU fallback: if the library or an sm_100 device is missing, calls raise.
+
+Entry points mirror the C names:
+  bifurcated_attn_decode(q, Kc, Vc, Kd, Vd, lens, out=None, lse=None, ...)
+  bifurcated_attn_decode_host(...)   host tensors in, host result out (e2e)
+  replicated_attn_decode(q, K, V, lens, ...)   non-bifurcated baseline
+  ba_workspace_bytes(...), ba_launches_per_call(...), ba_plan_string(...)
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libbifattn.so")
+
+BA_BF16, BA_FP32 = 0, 1
+BA_FLAG_FORCE_FMA = 0x1
+BA_FLAG_NO_PDL = 0x2
+
+ERRORS = {0: "BA_OK", -1: "BA_EINVAL", -2: "BA_ENULL", -3: "BA_EALIGN", -4: "BA_EWORKSPACE",
+          -5: "BA_EDTYPE", -6: "BA_ENODEV", -7: "BA_ECUDA"}
+
+EXPORTED = ["ba_workspace_bytes", "bifurcated_attn_decode", "bifurcated_attn_decode_host",
+            "replicated_attn_decode", "ba_launches_per_call", "ba_plan_string", "ba_strerror",
+            "ba_last_cuda_error", "ba_version", "ba_launch_name", "ba_set_launch_events"]
+
+
+class BAProblem(ctypes.Structure):
+    _fields_ = [("b", ctypes.c_int32), ("h", ctypes.c_int32), ("g", ctypes.c_int32),
+                ("d", ctypes.c_int32), ("mc", ctypes.c_int32), ("md_cap", ctypes.c_int32),
+                ("dtype", ctypes.c_int32), ("scale", ctypes.c_float), ("flags", ctypes.c_uint32)]
+
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH):
+    """Load libbifattn.so (build it first with paper_2403_08845_b200._build)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise RuntimeError(
+            f"libbifattn.so not found at {path}: build it (python -m paper_2403_08845_b200._build);"
+            " there is no CPU fallback")
+    lib = ctypes.CDLL(path)
+    P = ctypes.c_void_p
+    pp = ctypes.POINTER(BAProblem)
+    lib.ba_workspace_bytes.argtypes = [pp]
+    lib.ba_workspace_bytes.restype = ctypes.c_size_t
+    lib.bifurcated_attn_decode.argtypes = [pp] + [P] * 9 + [ctypes.c_size_t, P]
+    lib.bifurcated_attn_decode.restype = ctypes.c_int
+    lib.bifurcated_attn_decode_host.argtypes = [pp] + [P] * 18 + [ctypes.c_size_t, P]
+    lib.bifurcated_attn_decode_host.restype = ctypes.c_int
+    lib.replicated_attn_decode.argtypes = [pp] + [P] * 7 + [ctypes.c_size_t, P]
+    lib.replicated_attn_decode.restype = ctypes.c_int
+    lib.ba_launches_per_call.argtypes = [pp]
+    lib.ba_launches_per_call.restype = ctypes.c_int
+    lib.ba_plan_string.argtypes = [pp]
+    lib.ba_plan_string.restype = ctypes.c_char_p
+    lib.ba_strerror.argtypes = [ctypes.c_int]
+    lib.ba_strerror.restype = ctypes.c_char_p
+    lib.ba_last_cuda_error.argtypes = []
+    lib.ba_last_cuda_error.restype = ctypes.c_int
+    lib.ba_launch_name.argtypes = [pp, ctypes.c_int]
+    lib.ba_launch_name.restype = ctypes.c_char_p
+    lib.ba_set_launch_events.argtypes = [ctypes.c_void_p, ctypes.c_int]
+    lib.ba_set_launch_events.restype = None
+    lib.ba_version.argtypes = []
+    lib.ba_version.restype = ctypes.c_int
+    _lib = lib
+    return lib
+
+
+class BifAttnError(RuntimeError):
+    def __init__(self, code: int, what: str):
+        lib = load_library()
+        msg = lib.ba_strerror(code).decode()
+        extra = ""
+        if code == -7:
+            extra = f" (cudaError {lib.ba_last_cuda_error()})"
+        super().__init__(f"{what}: {ERRORS.get(code, code)}: {msg}{extra}")
+        self.code = code
+
+
+def make_problem(b, h, g, d, mc, md_cap, dtype, scale: Optional[float] = None, flags: int = 0):
+    dt = {torch.bfloat16: BA_BF16, torch.float32: BA_FP32}.get(dtype, dtype)
+    return BAProblem(b, h, g, d, mc, md_cap, dt, float(scale) if scale else 0.0, flags)
+
+
+def _problem_from(q, Kc, Kd, scale, flags):
+    b, h, d = q.shape
+    g, mc, _ = Kc.shape
+    md_cap = Kd.shape[2]
+    return make_problem(b, h, g, d, mc, md_cap, q.dtype, scale, flags)
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+
+
+def _stream_handle(stream):
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def ba_workspace_bytes(prob: BAProblem) -> int:
+    return int(load_library().ba_workspace_bytes(ctypes.byref(prob)))
+
+
+def ba_launches_per_call(prob: BAProblem) -> int:
+    return int(load_library().ba_launches_per_call(ctypes.byref(prob)))
+
+
+def ba_plan_string(prob: BAProblem) -> str:
+    return load_library().ba_plan_string(ctypes.byref(prob)).decode()
+
+
+def ba_launch_names(prob: BAProblem):
+    lib = load_library()
+    names, k = [], 0
+    while True:
+        s = lib.ba_launch_name(ctypes.byref(prob), k)
+        if not s:
+            return names
+        names.append(s.decode())
+        k += 1
+
+
+class LaunchTimer:
+    """Per-kernel CUDA-event timing of the library's launches (instrumentation
+    for bench.py): records an event pair around every launch of every call made
+    while active, on the call's stream."""
+
+    def __init__(self, launches_per_call: int, calls: int):
+        self.L = launches_per_call
+        self.calls = calls
+        self.events = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                        for _ in range(self.L)] for _ in range(calls)]
+        self._arrays = []
+        for call in self.events:
+            arr = (ctypes.c_void_p * (2 * self.L))()
+            for k, (a, b) in enumerate(call):
+                arr[2 * k] = a.cuda_event
+                arr[2 * k + 1] = b.cuda_event
+            self._arrays.append(arr)
+
+    def arm(self, call: int):
+        load_library().ba_set_launch_events(self._arrays[call], self.L)
+
+    @staticmethod
+    def disarm():
+        load_library().ba_set_launch_events(None, 0)
+
+    def per_launch_ms(self):
+        """Mean duration (ms) of each launch index over all recorded calls."""
+        tot = [0.0] * self.L
+        for call in self.events:
+            for k, (a, b) in enumerate(call):
+                tot[k] += a.elapsed_time(b)
+        return [t / self.calls for t in tot]
+
+
+def alloc_workspace(prob: BAProblem, device) -> torch.Tensor:
+    """Zero-initialised workspace (the completion counters must start at 0)."""
+    n = ba_workspace_bytes(prob)
+    if n == 0:
+        raise BifAttnError(-1, "ba_workspace_bytes")
+    return torch.zeros(n, dtype=torch.uint8, device=device)
+
+
+def _check(ts, dtype, device):
+    for name, t in ts.items():
+        if t is None:
+            continue
+        if not t.is_cuda:
+            raise ValueError(f"{name} must be a CUDA tensor")
+        if t.device != device:
+            raise ValueError(f"{name} is on {t.device}, expected {device}")
+        if not t.is_contiguous():
+            raise ValueError(f"{name} must be contiguous")
+        if name != "lens" and t.dtype != dtype:
+            raise ValueError(f"{name} has dtype {t.dtype}, expected {dtype}")
+
+
+def bifurcated_attn_decode(q, Kc, Vc, Kd, Vd, lens, out=None, lse=None, *, scale=None,
+                           workspace=None, stream=None, flags=0):
+    """One bifurcated decode step on the GPU.  Shapes: q [b,h,d]; Kc,Vc [g,mc,d];
+    Kd,Vd [b,g,md_cap,d]; lens int32 [b].  Returns ``out`` [b,h,d]."""
+    lib = load_library()
+    _check(dict(q=q, Kc=Kc, Vc=Vc, Kd=Kd, Vd=Vd, lens=lens), q.dtype, q.device)
+    if lens.dtype != torch.int32:
+        raise ValueError("lens must be int32")
+    prob = _problem_from(q, Kc, Kd, scale, flags)
+    if out is None:
+        out = torch.empty_like(q)
+    if workspace is None:
+        workspace = alloc_workspace(prob, q.device)
+    rc = lib.bifurcated_attn_decode(ctypes.byref(prob), _ptr(q), _ptr(Kc), _ptr(Vc), _ptr(Kd),
+                                    _ptr(Vd), _ptr(lens), _ptr(out), _ptr(lse), _ptr(workspace),
+                                    workspace.numel(), _stream_handle(stream))
+    if rc != 0:
+        raise BifAttnError(rc, "bifurcated_attn_decode")
+    return out
+
+
+def bifurcated_attn_decode_host(hq, hKc, hVc, hKd, hVd, hlens, hout, dev, *, hlse=None,
+                                scale=None, stream=None, flags=0):
+    """End-to-end call: host (pinned) tensors in, host result out.  ``dev`` is a
+    dict of caller-owned device buffers {q,Kc,Vc,Kd,Vd,lens,out,lse,workspace}
+    (see make_device_buffers).  Enqueues H2D copies, the kernels and the D2H
+    copy on ``stream``; synchronise before reading ``hout``."""
+    lib = load_library()
+    prob = _problem_from(hq, hKc, hKd, scale, flags)
+    ws = dev["workspace"]
+    rc = lib.bifurcated_attn_decode_host(
+        ctypes.byref(prob), _ptr(hq), _ptr(hKc), _ptr(hVc), _ptr(hKd), _ptr(hVd), _ptr(hlens),
+        _ptr(hout), _ptr(hlse), _ptr(dev["q"]), _ptr(dev["Kc"]), _ptr(dev["Vc"]), _ptr(dev["Kd"]),
+        _ptr(dev["Vd"]), _ptr(dev["lens"]), _ptr(dev["out"]), _ptr(dev.get("lse")), _ptr(ws),
+        ws.numel(), _stream_handle(stream))
+    if rc != 0:
+        raise BifAttnError(rc, "bifurcated_attn_decode_host")
+    return hout
+
+
+def make_device_buffers(hq, hKc, hKd, device, with_lse=False, scale=None, flags=0):
+    prob = _problem_from(hq, hKc, hKd, scale, flags)
+    e = dict(q=torch.empty(hq.shape, dtype=hq.dtype, device=device),
+             Kc=torch.empty(hKc.shape, dtype=hq.dtype, device=device),
+             Vc=torch.empty(hKc.shape, dtype=hq.dtype, device=device),
+             Kd=torch.empty(hKd.shape, dtype=hq.dtype, device=device),
+             Vd=torch.empty(hKd.shape, dtype=hq.dtype, device=device),
+             lens=torch.empty(hq.shape[0], dtype=torch.int32, device=device),
+             out=torch.empty(hq.shape, dtype=hq.dtype, device=device),
+             workspace=alloc_workspace(prob, device))
+    if with_lse:
+        e["lse"] = torch.empty(hq.shape[0], hq.shape[1], dtype=torch.float32, device=device)
+    return e
+
+
+def replicated_attn_decode(q, K, V, lens, mc, out=None, lse=None, *, scale=None,
+                           workspace=None, stream=None, flags=0):
+    """Non-bifurcated baseline over the replicated cache K, V [b,g,mc+md_cap,d]:
+    sample i attends to positions [0, mc + lens[i])."""
+    lib = load_library()
+    _check(dict(q=q, K=K, V=V, lens=lens), q.dtype, q.device)
+    b, h, d = q.shape
+    g, M = K.shape[1], K.shape[2]
+    prob = make_problem(b, h, g, d, mc, M - mc, q.dtype, scale, flags)
+    if out is None:
+        out = torch.empty_like(q)
+    if workspace is None:
+        workspace = alloc_workspace(prob, q.device)
+    rc = lib.replicated_attn_decode(ctypes.byref(prob), _ptr(q), _ptr(K), _ptr(V), _ptr(lens),
+                                    _ptr(out), _ptr(lse), _ptr(workspace), workspace.numel(),
+                                    _stream_handle(stream))
+    if rc != 0:
+        raise BifAttnError(rc, "replicated_attn_decode")
+    return out

@@ -1,0 +1,432 @@
+// bifattn_api.cu — host side of the C ABI declared in include/bifattn.h:
+// validation, planning (splits, kernel choice), workspace layout, launches.
+//
+// Plan of one bifurcated step:
+//   1. context branch  — Kc/Vc read once for all b samples (Eq. 3-4 context rows,
+//      PAPER.md:254, :266): tcgen05 kernel (ctx_tc.cuh) when bf16, d = 128 and
+//      b*p >= 16 rows share the tile; otherwise the FMA kernel (fma_partial.cuh);
+//   2. decode branch   — Kd/Vd of each sample: FMA kernel;
+//   3. merge           — one log-sum-exp over all partials per row (merge.cuh).
+#include <mutex>
+#include <cstdio>
+#include <cstring>
+
+#include "../../include/bifattn.h"
+#include "common.cuh"
+#include "fma_partial.cuh"
+#include "merge.cuh"
+
+namespace {
+
+thread_local int g_last_cuda_error = 0;
+thread_local char g_plan_buf[512];
+thread_local void* const* g_events = nullptr;
+thread_local int g_nevents = 0;
+
+// Brackets launch k with the caller's timing events (ba_set_launch_events).
+struct LaunchRec {
+  cudaStream_t st;
+  int k = 0;
+  explicit LaunchRec(cudaStream_t s) : st(s) {}
+  void begin() {
+    if (g_events && k < g_nevents) cudaEventRecord((cudaEvent_t)g_events[2 * k], st);
+  }
+  int end() {
+    cudaError_t e = cudaGetLastError();
+    if (g_events && k < g_nevents) cudaEventRecord((cudaEvent_t)g_events[2 * k + 1], st);
+    ++k;
+    if (e != cudaSuccess) {
+      g_last_cuda_error = (int)e;
+      return BA_ECUDA;
+    }
+    return BA_OK;
+  }
+};
+
+struct DevInfo {
+  int sms = 0;
+  int major = 0;
+  bool ok = false;
+};
+
+std::mutex g_mu;
+DevInfo g_dev[64];
+bool g_dev_init[64];
+
+int device_info(DevInfo* out) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return BA_ENODEV;
+  }
+  if (dev < 0 || dev >= 64) return BA_ENODEV;
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (!g_dev_init[dev]) {
+    DevInfo di;
+    int major = 0, sms = 0;
+    if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+      cudaGetLastError();
+      return BA_ENODEV;
+    }
+    di.major = major;
+    di.sms = sms;
+    di.ok = (major == 10);
+    g_dev[dev] = di;
+    g_dev_init[dev] = true;
+  }
+  *out = g_dev[dev];
+  return out->ok ? BA_OK : BA_ENODEV;
+}
+
+inline int cdiv(long a, long b) { return (int)((a + b - 1) / b); }
+
+struct Plan {
+  int D = 0;
+  bool bf16 = false;
+  int elem = 0;
+  bool replicated = false;
+  // FMA context branch
+  int nsc = 0, ctx_chunk = 0, rb_c = 1, nrb_c = 0;
+  // FMA decode branch
+  int nsd = 0, dec_chunk = 0, rb_d = 1, nrb_d = 0;
+  int dec_stride = 0, dec_cap = 0, lens_offset = 0;
+  int S = 0, dec_slot0 = 0;
+  size_t off_o = 0, off_ml = 0, ws_bytes = 0;
+  int launches = 0;
+};
+
+int pick_rb(int rows) { return rows >= 4 ? 4 : (rows >= 2 ? 2 : 1); }
+
+int validate(const ba_problem_t* pr) {
+  if (!pr) return BA_ENULL;
+  if (pr->dtype != BA_BF16 && pr->dtype != BA_FP32) return BA_EDTYPE;
+  if (pr->b < 1 || pr->h < 1 || pr->g < 1 || pr->mc < 1 || pr->md_cap < 0) return BA_EINVAL;
+  if (pr->h % pr->g != 0) return BA_EINVAL;
+  const int d = pr->d;
+  if (d != 16 && d != 32 && d != 64 && d != 128 && d != 256) return BA_EINVAL;
+  // int32 index safety for the per-tensor element counts used in the kernels
+  const long long kd = (long long)pr->b * pr->g * ((long long)pr->md_cap + pr->mc) * d;
+  if (kd > (1ll << 40)) return BA_EINVAL;
+  return BA_OK;
+}
+
+// Plan for the bifurcated step (replicated == false) or the replicated baseline.
+int make_plan(const ba_problem_t* pr, int sms, bool replicated, Plan* pl) {
+  int rc = validate(pr);
+  if (rc) return rc;
+  Plan P;
+  P.D = pr->d;
+  P.bf16 = pr->dtype == BA_BF16;
+  P.elem = P.bf16 ? 2 : 4;
+  P.replicated = replicated;
+  const int b = pr->b, h = pr->h, g = pr->g, p = h / g;
+  const int target = 4 * sms;  // CTAs of 128 threads per launch (~4 per SM)
+  if (!replicated) {
+    // context branch, FMA kernel: rows R = b*p share each Kc tile
+    const int R = b * p;
+    P.rb_c = pick_rb(R);
+    P.nrb_c = cdiv(R, P.rb_c);
+    long items = (long)g * P.nrb_c;
+    int nsc = cdiv(target, items);
+    nsc = nsc < 1 ? 1 : nsc;
+    const int max_nsc = cdiv(pr->mc, 64);
+    if (nsc > max_nsc) nsc = max_nsc;
+    P.ctx_chunk = cdiv(cdiv(pr->mc, nsc), 32) * 32;
+    P.nsc = cdiv(pr->mc, P.ctx_chunk);
+    P.dec_stride = pr->md_cap;
+    P.dec_cap = pr->md_cap;
+    P.lens_offset = 0;
+  } else {
+    P.nsc = 0;
+    P.dec_stride = pr->mc + pr->md_cap;
+    P.dec_cap = pr->md_cap;
+    P.lens_offset = pr->mc;
+  }
+  const int maxlen = P.lens_offset + P.dec_cap;
+  P.rb_d = pick_rb(p);
+  P.nrb_d = cdiv(p, P.rb_d);
+  if (maxlen > 0) {
+    long items = (long)b * g * P.nrb_d;
+    int nsd = cdiv(target, items);
+    nsd = nsd < 1 ? 1 : nsd;
+    const int max_nsd = cdiv(maxlen, 64);
+    if (nsd > max_nsd) nsd = max_nsd;
+    P.dec_chunk = cdiv(cdiv(maxlen, nsd), 32) * 32;
+    P.nsd = cdiv(maxlen, P.dec_chunk);
+  } else {
+    P.nsd = 0;
+    P.dec_chunk = 32;
+  }
+  P.dec_slot0 = P.nsc;
+  P.S = P.nsc + P.nsd;
+  if (P.S < 1) P.S = 1;
+  const size_t rows = (size_t)b * h;
+  P.off_o = 0;
+  P.off_ml = rows * P.S * P.D * sizeof(float);
+  P.ws_bytes = P.off_ml + rows * P.S * 2 * sizeof(float);
+  P.ws_bytes = (P.ws_bytes + 255) & ~(size_t)255;
+  P.launches = (P.nsc > 0 ? 1 : 0) + (P.nsd > 0 ? 1 : 0) + 1;
+  *pl = P;
+  return BA_OK;
+}
+
+template <typename T, int D>
+int launch_fma_rb(int rb, int grid, const ba::FmaParams& fp, LaunchRec& rec) {
+  if (grid <= 0) return BA_OK;
+  cudaStream_t st = rec.st;
+  rec.begin();
+  switch (rb) {
+    case 1: ba::fma_partial_kernel<T, D, 1><<<grid, 128, 0, st>>>(fp); break;
+    case 2: ba::fma_partial_kernel<T, D, 2><<<grid, 128, 0, st>>>(fp); break;
+    default: ba::fma_partial_kernel<T, D, 4><<<grid, 128, 0, st>>>(fp); break;
+  }
+  return rec.end();
+}
+
+template <typename T, int D>
+int run_plan(const ba_problem_t* pr, const Plan& P, const void* q, const void* Kc,
+             const void* Vc, const void* Kd, const void* Vd, const int32_t* lens, void* out,
+             float* lse, void* ws, cudaStream_t st) {
+  const int b = pr->b, h = pr->h, g = pr->g, p = h / g;
+  float scale = pr->scale > 0.f ? pr->scale : 1.0f / sqrtf((float)D);
+  ba::FmaParams fp;
+  memset(&fp, 0, sizeof fp);
+  fp.q = q; fp.Kc = Kc; fp.Vc = Vc; fp.Kd = Kd; fp.Vd = Vd; fp.lens = lens;
+  fp.b = b; fp.h = h; fp.g = g; fp.p = p; fp.mc = pr->mc;
+  fp.dec_stride = P.dec_stride; fp.dec_cap = P.dec_cap; fp.lens_offset = P.lens_offset;
+  fp.scale_log2 = scale * ba::kLog2e;
+  fp.nsc = P.nsc; fp.nsd = P.nsd;
+  fp.ctx_chunk = P.ctx_chunk; fp.dec_chunk = P.dec_chunk;
+  fp.nrb_c = P.nrb_c; fp.nrb_d = P.nrb_d;
+  fp.S = P.S; fp.dec_slot0 = P.dec_slot0;
+  fp.ws_o = reinterpret_cast<float*>(static_cast<char*>(ws) + P.off_o);
+  fp.ws_ml = reinterpret_cast<float*>(static_cast<char*>(ws) + P.off_ml);
+  int rc;
+  LaunchRec rec(st);
+  // 1. context branch (FMA): items g * nsc * nrb_c
+  if (P.nsc > 0) {
+    ba::FmaParams f = fp;
+    f.n_ctx_items = g * P.nsc * P.nrb_c;
+    rc = launch_fma_rb<T, D>(P.rb_c, f.n_ctx_items, f, rec);
+    if (rc) return rc;
+  }
+  // 2. decode branch (FMA): items b * g * nsd * nrb_d
+  if (P.nsd > 0) {
+    ba::FmaParams f = fp;
+    f.n_ctx_items = 0;
+    rc = launch_fma_rb<T, D>(P.rb_d, b * g * P.nsd * P.nrb_d, f, rec);
+    if (rc) return rc;
+  }
+  // 3. merge
+  ba::MergeParams mp;
+  mp.ws_o = fp.ws_o;
+  mp.ws_ml = fp.ws_ml;
+  mp.rows = b * h;
+  mp.S = P.S;
+  mp.out = out;
+  mp.lse = lse;
+  const int warps_per_block = 8;
+  rec.begin();
+  ba::merge_kernel<T, D><<<cdiv(mp.rows, warps_per_block), 32 * warps_per_block, 0, st>>>(mp);
+  return rec.end();
+}
+
+template <typename T>
+int run_d(const ba_problem_t* pr, const Plan& P, const void* q, const void* Kc, const void* Vc,
+          const void* Kd, const void* Vd, const int32_t* lens, void* out, float* lse, void* ws,
+          cudaStream_t st) {
+  switch (pr->d) {
+    case 16: return run_plan<T, 16>(pr, P, q, Kc, Vc, Kd, Vd, lens, out, lse, ws, st);
+    case 32: return run_plan<T, 32>(pr, P, q, Kc, Vc, Kd, Vd, lens, out, lse, ws, st);
+    case 64: return run_plan<T, 64>(pr, P, q, Kc, Vc, Kd, Vd, lens, out, lse, ws, st);
+    case 128: return run_plan<T, 128>(pr, P, q, Kc, Vc, Kd, Vd, lens, out, lse, ws, st);
+    case 256: return run_plan<T, 256>(pr, P, q, Kc, Vc, Kd, Vd, lens, out, lse, ws, st);
+  }
+  return BA_EINVAL;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+int common_checks(const ba_problem_t* pr, const void* const* ptrs, int nptr, void* ws,
+                  size_t ws_bytes, size_t need) {
+  for (int k = 0; k < nptr; ++k) {
+    if (!ptrs[k]) return BA_ENULL;
+    if (!aligned16(ptrs[k])) return BA_EALIGN;
+  }
+  if (!ws || ws_bytes < need) return BA_EWORKSPACE;
+  if (!aligned16(ws)) return BA_EALIGN;
+  (void)pr;
+  return BA_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t ba_workspace_bytes(const ba_problem_t* prob) {
+  if (validate(prob) != BA_OK) return 0;
+  DevInfo di;
+  int sms = device_info(&di) == BA_OK ? di.sms : 148;
+  Plan a, r;
+  if (make_plan(prob, sms, false, &a) != BA_OK) return 0;
+  if (make_plan(prob, sms, true, &r) != BA_OK) return 0;
+  return a.ws_bytes > r.ws_bytes ? a.ws_bytes : r.ws_bytes;
+}
+
+int bifurcated_attn_decode(const ba_problem_t* prob, const void* q, const void* Kc,
+                           const void* Vc, const void* Kd, const void* Vd,
+                           const int32_t* lens, void* out, float* lse, void* workspace,
+                           size_t workspace_bytes, void* stream) {
+  int rc = validate(prob);
+  if (rc) return rc;
+  DevInfo di;
+  rc = device_info(&di);
+  if (rc) return rc;
+  Plan P;
+  rc = make_plan(prob, di.sms, false, &P);
+  if (rc) return rc;
+  const void* ptrs[] = {q, Kc, Vc, out, lens};
+  rc = common_checks(prob, ptrs, 5, workspace, workspace_bytes, ba_workspace_bytes(prob));
+  if (rc) return rc;
+  if (prob->md_cap > 0) {
+    if (!Kd || !Vd) return BA_ENULL;
+    if (!aligned16(Kd) || !aligned16(Vd)) return BA_EALIGN;
+  }
+  if (lse && (reinterpret_cast<uintptr_t>(lse) & 3u)) return BA_EALIGN;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (P.bf16)
+    return run_d<__nv_bfloat16>(prob, P, q, Kc, Vc, Kd, Vd, lens, out, lse, workspace, st);
+  return run_d<float>(prob, P, q, Kc, Vc, Kd, Vd, lens, out, lse, workspace, st);
+}
+
+int replicated_attn_decode(const ba_problem_t* prob, const void* q, const void* K,
+                           const void* V, const int32_t* lens, void* out, float* lse,
+                           void* workspace, size_t workspace_bytes, void* stream) {
+  int rc = validate(prob);
+  if (rc) return rc;
+  DevInfo di;
+  rc = device_info(&di);
+  if (rc) return rc;
+  Plan P;
+  rc = make_plan(prob, di.sms, true, &P);
+  if (rc) return rc;
+  const void* ptrs[] = {q, K, V, out, lens};
+  rc = common_checks(prob, ptrs, 5, workspace, workspace_bytes, ba_workspace_bytes(prob));
+  if (rc) return rc;
+  if (lse && (reinterpret_cast<uintptr_t>(lse) & 3u)) return BA_EALIGN;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (P.bf16)
+    return run_d<__nv_bfloat16>(prob, P, q, nullptr, nullptr, K, V, lens, out, lse, workspace, st);
+  return run_d<float>(prob, P, q, nullptr, nullptr, K, V, lens, out, lse, workspace, st);
+}
+
+int bifurcated_attn_decode_host(const ba_problem_t* prob, const void* hq, const void* hKc,
+                                const void* hVc, const void* hKd, const void* hVd,
+                                const int32_t* hlens, void* hout, float* hlse, void* dq,
+                                void* dKc, void* dVc, void* dKd, void* dVd, int32_t* dlens,
+                                void* dout, float* dlse, void* workspace,
+                                size_t workspace_bytes, void* stream) {
+  int rc = validate(prob);
+  if (rc) return rc;
+  if (!hq || !hKc || !hVc || !hlens || !hout) return BA_ENULL;
+  if (prob->md_cap > 0 && (!hKd || !hVd)) return BA_ENULL;
+  DevInfo di;
+  rc = device_info(&di);
+  if (rc) return rc;
+  const size_t e = prob->dtype == BA_BF16 ? 2 : 4;
+  const size_t d = prob->d;
+  const size_t nq = (size_t)prob->b * prob->h * d * e;
+  const size_t nc = (size_t)prob->g * prob->mc * d * e;
+  const size_t nd = (size_t)prob->b * prob->g * prob->md_cap * d * e;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  auto cp = [&](void* dst, const void* src, size_t n, cudaMemcpyKind k) -> int {
+    if (n == 0) return BA_OK;
+    if (!dst) return BA_ENULL;
+    cudaError_t ce = cudaMemcpyAsync(dst, src, n, k, st);
+    if (ce != cudaSuccess) {
+      g_last_cuda_error = (int)ce;
+      return BA_ECUDA;
+    }
+    return BA_OK;
+  };
+  if ((rc = cp(dq, hq, nq, cudaMemcpyHostToDevice))) return rc;
+  if ((rc = cp(dKc, hKc, nc, cudaMemcpyHostToDevice))) return rc;
+  if ((rc = cp(dVc, hVc, nc, cudaMemcpyHostToDevice))) return rc;
+  if ((rc = cp(dKd, hKd, nd, cudaMemcpyHostToDevice))) return rc;
+  if ((rc = cp(dVd, hVd, nd, cudaMemcpyHostToDevice))) return rc;
+  if ((rc = cp(dlens, hlens, (size_t)prob->b * sizeof(int32_t), cudaMemcpyHostToDevice)))
+    return rc;
+  rc = bifurcated_attn_decode(prob, dq, dKc, dVc, dKd, dVd, dlens, dout, dlse, workspace,
+                              workspace_bytes, stream);
+  if (rc) return rc;
+  if ((rc = cp(hout, dout, nq, cudaMemcpyDeviceToHost))) return rc;
+  if (hlse && dlse) {
+    if ((rc = cp(hlse, dlse, (size_t)prob->b * prob->h * sizeof(float), cudaMemcpyDeviceToHost)))
+      return rc;
+  }
+  return BA_OK;
+}
+
+int ba_launches_per_call(const ba_problem_t* prob) {
+  DevInfo di;
+  int sms = device_info(&di) == BA_OK ? di.sms : 148;
+  Plan P;
+  int rc = make_plan(prob, sms, false, &P);
+  return rc ? rc : P.launches;
+}
+
+const char* ba_plan_string(const ba_problem_t* prob) {
+  DevInfo di;
+  int sms = device_info(&di) == BA_OK ? di.sms : 148;
+  Plan P;
+  int rc = make_plan(prob, sms, false, &P);
+  if (rc) {
+    snprintf(g_plan_buf, sizeof g_plan_buf, "invalid (%d)", rc);
+    return g_plan_buf;
+  }
+  snprintf(g_plan_buf, sizeof g_plan_buf,
+           "ctx=fma(nsc=%d,chunk=%d,rb=%d) dec=fma(nsd=%d,chunk=%d,rb=%d) S=%d launches=%d "
+           "ws=%zu",
+           P.nsc, P.ctx_chunk, P.rb_c, P.nsd, P.dec_chunk, P.rb_d, P.S, P.launches, P.ws_bytes);
+  return g_plan_buf;
+}
+
+const char* ba_launch_name(const ba_problem_t* prob, int k) {
+  DevInfo di;
+  int sms = device_info(&di) == BA_OK ? di.sms : 148;
+  Plan P;
+  if (make_plan(prob, sms, false, &P) != BA_OK) return nullptr;
+  const char* names[4];
+  int n = 0;
+  if (P.nsc > 0) names[n++] = "ctx_fma";
+  if (P.nsd > 0) names[n++] = "dec_fma";
+  names[n++] = "merge";
+  return (k >= 0 && k < n) ? names[k] : nullptr;
+}
+
+void ba_set_launch_events(void* const* events, int n) {
+  g_events = n > 0 ? events : nullptr;
+  g_nevents = n > 0 ? n : 0;
+}
+
+const char* ba_strerror(int code) {
+  switch (code) {
+    case BA_OK: return "ok";
+    case BA_EINVAL: return "invalid problem shape";
+    case BA_ENULL: return "null pointer";
+    case BA_EALIGN: return "pointer not 16-byte aligned";
+    case BA_EWORKSPACE: return "workspace missing or too small";
+    case BA_EDTYPE: return "unsupported dtype";
+    case BA_ENODEV: return "no sm_100 CUDA device (there is no CPU fallback)";
+    case BA_ECUDA: return "CUDA error";
+  }
+  return "unknown error";
+}
+
+int ba_last_cuda_error(void) { return g_last_cuda_error; }
+
+int ba_version(void) { return 1; }
+
+}  // extern "C"

@@ -1,0 +1,68 @@
+// merge.cuh — join the per-split partials of one output row with one
+// log-sum-exp and write the normalised result (SURVEY §8(a) a3 + a6).
+//
+// Partials k = (m_k, l_k, o_k) with m_k the running max in log2 units,
+// l_k = sum 2^(s - m_k), o_k = sum 2^(s - m_k) v.  With M = max_k m_k:
+//   L = sum_k 2^(m_k - M) l_k ;  out = (sum_k 2^(m_k - M) o_k) / L
+//   lse = (M + log2 L) * ln 2
+// which is softmax over the concatenation S_c ⊕ S_d,
+// split at mc and summed (Eq. 4), in exact arithmetic.
+// Empty partials carry m = -inf, l = 0, o = 0 and drop out.
+#pragma once
+#include "common.cuh"
+
+namespace ba {
+
+struct MergeParams {
+  const float* ws_o;   // [rows][S][D]
+  const float* ws_ml;  // [rows][S][2]
+  int rows, S;
+  void* out;           // [rows][D] in T
+  float* lse;          // [rows] or null
+};
+
+template <typename T, int D>
+__global__ void __launch_bounds__(256) merge_kernel(const MergeParams P) {
+  constexpr int EPL = (D + 31) / 32;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= P.rows) return;
+  const float* ml = P.ws_ml + (size_t)warp * P.S * 2;
+  // max over slots
+  float M = kNegInf;
+  for (int k = lane; k < P.S; k += 32) M = fmaxf(M, ml[2 * k]);
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
+  const float Ms = (M == kNegInf) ? 0.f : M;
+  float acc[EPL];
+#pragma unroll
+  for (int e = 0; e < EPL; ++e) acc[e] = 0.f;
+  float L = 0.f;
+  const float* o = P.ws_o + (size_t)warp * P.S * D;
+  for (int k = 0; k < P.S; ++k) {
+    const float mk = ml[2 * k];
+    const float w = ex2(mk - Ms);
+    L = fmaf(w, ml[2 * k + 1], L);
+#pragma unroll
+    for (int e = 0; e < EPL; ++e) {
+      const int x = e * 32 + lane;
+      if (x < D) acc[e] = fmaf(w, o[(size_t)k * D + x], acc[e]);
+    }
+  }
+  const float invL = 1.f / L;
+#pragma unroll
+  for (int e = 0; e < EPL; ++e) {
+    const int x = e * 32 + lane;
+    if (x < D) {
+      const float v = acc[e] * invL;
+      if constexpr (sizeof(T) == 2) {
+        reinterpret_cast<__nv_bfloat16*>(P.out)[(size_t)warp * D + x] = __float2bfloat16_rn(v);
+      } else {
+        reinterpret_cast<float*>(P.out)[(size_t)warp * D + x] = v;
+      }
+    }
+  }
+  if (P.lse && lane == 0) P.lse[warp] = (M + lg2(L)) * kLn2;
+}
+
+}  // namespace ba

@@ -1,0 +1,187 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle,
+element by element, on seeded inputs.  Small problems span several tiles and a
+ragged tail and are checked on every row; BASELINE.json's full-size configs run
+in the launch configuration bench.py times and are checked on sampled rows."""
+import numpy as np
+import pytest
+import torch
+
+import paper_2403_08845_b200 as ba
+from synth import CONFIGS, Config, make_inputs, seed_for
+from tests.parity import compare, oracle_rows, sample_rows
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda:0"
+
+
+def run_gpu(inp, flags=0, with_lse=True):
+    q = inp.q.to(DEV)
+    lse = torch.empty(q.shape[0], q.shape[1], dtype=torch.float32, device=DEV) if with_lse else None
+    out = ba.bifurcated_attn_decode(q, inp.Kc.to(DEV), inp.Vc.to(DEV), inp.Kd.to(DEV),
+                                    inp.Vd.to(DEV), inp.lens.to(DEV), lse=lse, scale=inp.scale,
+                                    flags=flags)
+    torch.cuda.synchronize()
+    return out, lse
+
+
+SMALL = [
+    CONFIGS["tiny"],
+    Config("mha_small", "bf16", b=5, h=8, g=8, d=128, mc=1000, md=37),
+    Config("mha_rows16", "bf16", b=16, h=4, g=4, d=128, mc=777, md=50),
+    Config("mha_rows40", "bf16", b=40, h=2, g=2, d=128, mc=1290, md=33),
+    Config("gqa_small", "bf16", b=9, h=16, g=4, d=128, mc=513, md=21),
+    Config("mqa_small", "bf16", b=3, h=48, g=1, d=128, mc=300, md=20),
+    Config("d64", "bf16", b=6, h=4, g=2, d=64, mc=200, md=9),
+    Config("d256", "bf16", b=3, h=2, g=1, d=256, mc=130, md=5),
+    Config("d32_fp32", "fp32", b=3, h=6, g=3, d=32, mc=97, md=13),
+    Config("fp32_d128", "fp32", b=4, h=4, g=2, d=128, mc=300, md=17),
+    Config("mc1", "bf16", b=2, h=2, g=1, d=128, mc=1, md=3),
+    Config("md0", "bf16", b=4, h=4, g=4, d=128, mc=333, md=0),
+]
+
+
+@pytest.mark.parametrize("cfg", SMALL, ids=lambda c: c.name)
+@pytest.mark.parametrize("flags", [0, ba.BA_FLAG_FORCE_FMA], ids=["auto", "fma"])
+def test_small_all_rows(cfg, flags):
+    inp = make_inputs(cfg, seed_for(cfg.name), variant="ragged" if cfg.md > 0 else "normal")
+    out, lse = run_gpu(inp, flags)
+    ref, ref_lse = oracle_rows(inp)
+    compare(out, lse, ref, ref_lse, cfg.torch_dtype, cfg.name)
+
+
+@pytest.mark.parametrize("variant", ["normal", "peaky", "ctx_dom", "dec_dom", "planted_ctx",
+                                     "planted_dec", "equal", "ragged"])
+@pytest.mark.parametrize("cfg", [SMALL[2], SMALL[4], SMALL[5]], ids=lambda c: c.name)
+def test_stress_variants(cfg, variant):
+    inp = make_inputs(cfg, 7, variant=variant)
+    out, lse = run_gpu(inp)
+    ref, ref_lse = oracle_rows(inp)
+    compare(out, lse, ref, ref_lse, cfg.torch_dtype, f"{cfg.name}/{variant}")
+    if variant == "equal":
+        o = out.float()
+        assert torch.equal(o, o[:1].expand_as(o))
+
+
+def test_all_lens_zero_is_context_only():
+    cfg = Config("x", "bf16", b=17, h=4, g=2, d=128, mc=640, md=32)
+    inp = make_inputs(cfg, 8, lens=[0] * cfg.b)
+    out, lse = run_gpu(inp)
+    ref, ref_lse = oracle_rows(inp)
+    compare(out, lse, ref, ref_lse, cfg.torch_dtype, "lens0")
+
+
+def test_lens_clamped_to_cap():
+    cfg = Config("x", "bf16", b=4, h=2, g=2, d=128, mc=64, md=8)
+    inp = make_inputs(cfg, 9)
+    inp_big = make_inputs(cfg, 9, lens=[100, -5, 8, 3])
+    out, _ = run_gpu(inp_big)
+    ref_inp = make_inputs(cfg, 9, lens=[8, 0, 8, 3])
+    ref, ref_lse = oracle_rows(ref_inp)
+    compare(out, None, ref, None, cfg.torch_dtype, "clamp")
+    del inp
+
+
+def test_replicated_baseline_matches_oracle():
+    cfg = Config("x", "bf16", b=6, h=8, g=4, d=128, mc=300, md=40)
+    inp = make_inputs(cfg, 10, variant="ragged")
+    K = torch.cat([inp.Kc.unsqueeze(0).expand(cfg.b, -1, -1, -1), inp.Kd], dim=2).contiguous()
+    V = torch.cat([inp.Vc.unsqueeze(0).expand(cfg.b, -1, -1, -1), inp.Vd], dim=2).contiguous()
+    lse = torch.empty(cfg.b, cfg.h, device=DEV)
+    out = ba.replicated_attn_decode(inp.q.to(DEV), K.to(DEV), V.to(DEV), inp.lens.to(DEV),
+                                    cfg.mc, lse=lse, scale=inp.scale)
+    torch.cuda.synchronize()
+    ref, ref_lse = oracle_rows(inp)
+    compare(out, lse, ref, ref_lse, cfg.torch_dtype, "replicated")
+
+
+def test_host_entry_point_equals_device_call():
+    cfg = Config("x", "bf16", b=8, h=4, g=4, d=128, mc=500, md=30)
+    inp = make_inputs(cfg, 11)
+    out_dev, _ = run_gpu(inp, with_lse=False)
+    pin = lambda t: t.contiguous().pin_memory()
+    hq, hKc, hVc, hKd, hVd, hl = map(pin, (inp.q, inp.Kc, inp.Vc, inp.Kd, inp.Vd, inp.lens))
+    hout = torch.empty_like(hq).pin_memory()
+    dev = ba.make_device_buffers(hq, hKc, hKd, DEV)
+    ba.bifurcated_attn_decode_host(hq, hKc, hVc, hKd, hVd, hl, hout, dev, scale=inp.scale)
+    torch.cuda.synchronize()
+    assert torch.equal(hout, out_dev.cpu())
+
+
+def test_cuda_graph_capture_and_replay():
+    cfg = Config("x", "bf16", b=16, h=8, g=8, d=128, mc=1024, md=64)
+    inp = make_inputs(cfg, 12)
+    q, Kc, Vc, Kd, Vd, lens = (t.to(DEV) for t in (inp.q, inp.Kc, inp.Vc, inp.Kd, inp.Vd, inp.lens))
+    out = torch.empty_like(q)
+    prob = ba.make_problem(cfg.b, cfg.h, cfg.g, cfg.d, cfg.mc, cfg.md, q.dtype, inp.scale)
+    ws = ba.alloc_workspace(prob, DEV)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        ba.bifurcated_attn_decode(q, Kc, Vc, Kd, Vd, lens, out, workspace=ws, scale=inp.scale)
+    torch.cuda.synchronize()
+    ref_gpu = out.clone()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=s):
+        ba.bifurcated_attn_decode(q, Kc, Vc, Kd, Vd, lens, out, workspace=ws, scale=inp.scale)
+    out.zero_()
+    for _ in range(3):
+        graph.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref_gpu)
+    # lens change without recapture
+    lens.copy_(torch.tensor([5] * cfg.b, dtype=torch.int32))
+    graph.replay()
+    torch.cuda.synchronize()
+    inp.lens = lens.cpu()
+    ref, _ = oracle_rows(inp)
+    compare(out, None, ref, None, cfg.torch_dtype, "graph-lens")
+
+
+def test_repeated_calls_deterministic():
+    cfg = Config("x", "bf16", b=32, h=4, g=4, d=128, mc=2048, md=64)
+    inp = make_inputs(cfg, 13)
+    a, _ = run_gpu(inp)
+    b_, _ = run_gpu(inp)
+    assert torch.equal(a, b_)
+
+
+def test_misaligned_pointer_rejected():
+    cfg = Config("x", "bf16", b=2, h=2, g=2, d=128, mc=64, md=4)
+    inp = make_inputs(cfg, 14, device=DEV)
+    buf = torch.empty(inp.q.numel() + 8, dtype=torch.bfloat16, device=DEV)
+    qmis = buf[1:1 + inp.q.numel()].view_as(inp.q)
+    with pytest.raises(ba.BifAttnError) as e:
+        ba.bifurcated_attn_decode(qmis, inp.Kc, inp.Vc, inp.Kd, inp.Vd, inp.lens)
+    assert e.value.code == -3
+
+
+def test_small_workspace_rejected():
+    cfg = Config("x", "bf16", b=2, h=2, g=2, d=128, mc=64, md=4)
+    inp = make_inputs(cfg, 15, device=DEV)
+    ws = torch.zeros(64, dtype=torch.uint8, device=DEV)
+    with pytest.raises(ba.BifAttnError) as e:
+        ba.bifurcated_attn_decode(inp.q, inp.Kc, inp.Vc, inp.Kd, inp.Vd, inp.lens, workspace=ws)
+    assert e.value.code == -4
+
+
+# ---------------------------------------------------------------------------
+# BASELINE.json configs at full size, bench.py's launch configuration
+# ---------------------------------------------------------------------------
+FULL = ["mha7b_b16", "mha7b_b32", "gqa", "mqa", "long"]
+
+
+@pytest.mark.parametrize("name", FULL)
+def test_full_size_sampled_rows(name):
+    cfg = CONFIGS[name]
+    inp = make_inputs(cfg, seed_for(name), device=DEV)
+    lse = torch.empty(cfg.b, cfg.h, dtype=torch.float32, device=DEV)
+    out = ba.bifurcated_attn_decode(inp.q, inp.Kc, inp.Vc, inp.Kd, inp.Vd, inp.lens, lse=lse,
+                                    scale=inp.scale)
+    torch.cuda.synchronize()
+    rows = sample_rows(cfg.b, cfg.h, n=48 if name != "long" else 24)
+    ref, ref_lse = oracle_rows(inp, rows)
+    o = out.reshape(-1, cfg.d)[rows]
+    compare(o, lse.reshape(-1)[rows], ref, ref_lse, cfg.torch_dtype, name)
+    # properties that hold at any size: finite, and |out| bounded by max |V|
+    assert torch.isfinite(out.float()).all()
+    vmax = max(inp.Vc.float().abs().max().item(), inp.Vd.float().abs().max().item())
+    assert out.float().abs().max().item() <= vmax * (1 + 1e-2)
