@@ -59,7 +59,7 @@ def load_library(path: str = LIB_PATH):
     lib.ba_workspace_bytes.restype = ctypes.c_size_t
     lib.bifurcated_attn_decode.argtypes = [pp] + [P] * 9 + [ctypes.c_size_t, P]
     lib.bifurcated_attn_decode.restype = ctypes.c_int
-    lib.bifurcated_attn_decode_host.argtypes = [pp] + [P] * 18 + [ctypes.c_size_t, P]
+    lib.bifurcated_attn_decode_host.argtypes = [pp] + [P] * 17 + [ctypes.c_size_t, P]
     lib.bifurcated_attn_decode_host.restype = ctypes.c_int
     lib.replicated_attn_decode.argtypes = [pp] + [P] * 7 + [ctypes.c_size_t, P]
     lib.replicated_attn_decode.restype = ctypes.c_int
@@ -147,6 +147,12 @@ class LaunchTimer:
         self.calls = calls
         self.events = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                         for _ in range(self.L)] for _ in range(calls)]
+        # torch creates the CUDA event lazily on first record(): force creation
+        for call in self.events:
+            for a, b in call:
+                a.record()
+                b.record()
+        torch.cuda.synchronize()
         self._arrays = []
         for call in self.events:
             arr = (ctypes.c_void_p * (2 * self.L))()

@@ -13,6 +13,7 @@
 
 #include "../../include/bifattn.h"
 #include "common.cuh"
+#include "ctx_tc.cuh"
 #include "fma_partial.cuh"
 #include "merge.cuh"
 
@@ -87,6 +88,10 @@ struct Plan {
   bool bf16 = false;
   int elem = 0;
   bool replicated = false;
+  int ctx_mode = 0;  // 0 none (replicated baseline), 1 FMA kernel, 2 tcgen05 kernel
+  // tcgen05 context branch
+  int tc_N = 0, tc_nrc = 0, tc_ntile = 0, tc_G = 0, tc_nst = 0, tc_S = 0, tc_smem = 0;
+  long long tc_T = 0;
   // FMA context branch
   int nsc = 0, ctx_chunk = 0, rb_c = 1, nrb_c = 0;
   // FMA decode branch
@@ -123,9 +128,45 @@ int make_plan(const ba_problem_t* pr, int sms, bool replicated, Plan* pl) {
   P.replicated = replicated;
   const int b = pr->b, h = pr->h, g = pr->g, p = h / g;
   const int target = 4 * sms;  // CTAs of 128 threads per launch (~4 per SM)
-  if (!replicated) {
+  const int R = b * p;
+  int tcN = 0;
+  if (!replicated && P.bf16 && pr->d == 128 && R >= 16 && !(pr->flags & BA_FLAG_FORCE_FMA)) {
+    // tensor-core context branch: N = rows per chunk, a multiple of 16 and of p
+    static const int cands[] = {16, 32, 48, 64};  // > 64 spills registers (round 2)
+    int best_fit = 0, largest = 0;
+    for (int N : cands) {
+      if (N % p) continue;
+      largest = N;
+      if (!best_fit && N >= R) best_fit = N;
+    }
+    tcN = best_fit ? best_fit : largest;
+  }
+  if (tcN) {
+    P.ctx_mode = 2;
+    P.tc_N = tcN;
+    P.tc_nrc = cdiv(R, tcN);
+    P.tc_ntile = cdiv(pr->mc, 128);
+    P.tc_T = (long long)g * P.tc_nrc * P.tc_ntile;
+    P.tc_G = (int)(P.tc_T < sms ? P.tc_T : sms);
+    const int avail = 227 * 1024 - ba::ctx::smem_fixed(tcN);
+    P.tc_nst = avail / ba::ctx::kStageBytes;
+    if (P.tc_nst > 4) P.tc_nst = 4;
+    P.tc_smem = P.tc_nst * ba::ctx::kStageBytes + ba::ctx::smem_fixed(tcN);
+    // slots: the most CTAs any (group, row chunk) is split over
+    int smax = 1;
+    for (long long seg = 0; seg < (long long)g * P.tc_nrc; ++seg) {
+      const long long ff = seg * P.tc_ntile, fl = ff + P.tc_ntile - 1;
+      const int n = ba::ctx::owner(fl, P.tc_T, P.tc_G) - ba::ctx::owner(ff, P.tc_T, P.tc_G) + 1;
+      if (n > smax) smax = n;
+    }
+    P.tc_S = smax;
+    P.nsc = 0;
+    P.dec_stride = pr->md_cap;
+    P.dec_cap = pr->md_cap;
+    P.lens_offset = 0;
+  } else if (!replicated) {
     // context branch, FMA kernel: rows R = b*p share each Kc tile
-    const int R = b * p;
+    P.ctx_mode = 1;
     P.rb_c = pick_rb(R);
     P.nrb_c = cdiv(R, P.rb_c);
     long items = (long)g * P.nrb_c;
@@ -139,6 +180,7 @@ int make_plan(const ba_problem_t* pr, int sms, bool replicated, Plan* pl) {
     P.dec_cap = pr->md_cap;
     P.lens_offset = 0;
   } else {
+    P.ctx_mode = 0;
     P.nsc = 0;
     P.dec_stride = pr->mc + pr->md_cap;
     P.dec_cap = pr->md_cap;
@@ -159,15 +201,16 @@ int make_plan(const ba_problem_t* pr, int sms, bool replicated, Plan* pl) {
     P.nsd = 0;
     P.dec_chunk = 32;
   }
-  P.dec_slot0 = P.nsc;
-  P.S = P.nsc + P.nsd;
+  const int nctx_slots = P.ctx_mode == 2 ? P.tc_S : P.nsc;
+  P.dec_slot0 = nctx_slots;
+  P.S = nctx_slots + P.nsd;
   if (P.S < 1) P.S = 1;
   const size_t rows = (size_t)b * h;
   P.off_o = 0;
   P.off_ml = rows * P.S * P.D * sizeof(float);
   P.ws_bytes = P.off_ml + rows * P.S * 2 * sizeof(float);
   P.ws_bytes = (P.ws_bytes + 255) & ~(size_t)255;
-  P.launches = (P.nsc > 0 ? 1 : 0) + (P.nsd > 0 ? 1 : 0) + 1;
+  P.launches = (P.ctx_mode != 0 ? 1 : 0) + (P.nsd > 0 ? 1 : 0) + 1;
   *pl = P;
   return BA_OK;
 }
@@ -183,6 +226,93 @@ int launch_fma_rb(int rb, int grid, const ba::FmaParams& fp, LaunchRec& rec) {
     default: ba::fma_partial_kernel<T, D, 4><<<grid, 128, 0, st>>>(fp); break;
   }
   return rec.end();
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+    else
+      cudaGetLastError();
+  });
+  return fn;
+}
+
+// 3D bf16 tensor map with a 128-byte-swizzled box of (64, box1, box2).
+int make_tmap_3d(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64_t d2,
+                 uint64_t stride1_bytes, uint64_t stride2_bytes, uint32_t box1, uint32_t box2) {
+  EncodeTiledFn fn = get_encode_fn();
+  if (!fn) return BA_ECUDA;
+  cuuint64_t dims[3] = {d0, d1, d2};
+  cuuint64_t strides[2] = {stride1_bytes, stride2_bytes};
+  cuuint32_t box[3] = {64, box1, box2};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    g_last_cuda_error = 1000 + (int)r;
+    return BA_ECUDA;
+  }
+  return BA_OK;
+}
+
+template <int N>
+int launch_ctx_tc_n(const ba::CtxTcParams& cp, int smem, LaunchRec& rec) {
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [&] {
+    attr_err = cudaFuncSetAttribute(ba::ctx_tc_kernel<N>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  });
+  if (attr_err != cudaSuccess) {
+    g_last_cuda_error = (int)attr_err;
+    return BA_ECUDA;
+  }
+  rec.begin();
+  ba::ctx_tc_kernel<N><<<cp.G, ba::ctx::kThreads, smem, rec.st>>>(cp);
+  return rec.end();
+}
+
+int launch_ctx_tc(const ba_problem_t* pr, const Plan& P, const void* q, const void* Kc,
+                  const void* Vc, float* ws_o, float* ws_ml, float scale_log2, LaunchRec& rec) {
+  ba::CtxTcParams cp;
+  memset(&cp, 0, sizeof cp);
+  const int p = pr->h / pr->g;
+  const uint64_t d = 128;
+  int rc = make_tmap_3d(&cp.tmK, Kc, d, pr->mc, pr->g, d * 2, (uint64_t)pr->mc * d * 2, 128, 1);
+  if (!rc) rc = make_tmap_3d(&cp.tmV, Vc, d, pr->mc, pr->g, d * 2, (uint64_t)pr->mc * d * 2, 128, 1);
+  if (!rc)
+    rc = make_tmap_3d(&cp.tmQ, q, d, pr->h, pr->b, d * 2, (uint64_t)pr->h * d * 2, p, P.tc_N / p);
+  if (rc) return rc;
+  cp.b = pr->b; cp.h = pr->h; cp.g = pr->g; cp.p = p; cp.mc = pr->mc;
+  cp.nrc = P.tc_nrc; cp.ntile = P.tc_ntile; cp.T = P.tc_T; cp.G = P.tc_G; cp.nst = P.tc_nst;
+  cp.scale_log2 = scale_log2;
+  cp.S = P.S;
+  cp.ws_o = ws_o;
+  cp.ws_ml = ws_ml;
+  switch (P.tc_N) {
+    case 16: return launch_ctx_tc_n<16>(cp, P.tc_smem, rec);
+    case 32: return launch_ctx_tc_n<32>(cp, P.tc_smem, rec);
+    case 48: return launch_ctx_tc_n<48>(cp, P.tc_smem, rec);
+    case 64: return launch_ctx_tc_n<64>(cp, P.tc_smem, rec);
+    case 80: return launch_ctx_tc_n<80>(cp, P.tc_smem, rec);
+    case 96: return launch_ctx_tc_n<96>(cp, P.tc_smem, rec);
+    case 112: return launch_ctx_tc_n<112>(cp, P.tc_smem, rec);
+    case 128: return launch_ctx_tc_n<128>(cp, P.tc_smem, rec);
+  }
+  return BA_EINVAL;
 }
 
 template <typename T, int D>
@@ -205,8 +335,15 @@ int run_plan(const ba_problem_t* pr, const Plan& P, const void* q, const void* K
   fp.ws_ml = reinterpret_cast<float*>(static_cast<char*>(ws) + P.off_ml);
   int rc;
   LaunchRec rec(st);
-  // 1. context branch (FMA): items g * nsc * nrb_c
-  if (P.nsc > 0) {
+  // 1. context branch: tensor cores (bf16, d = 128, >= 16 rows) or FMA
+  if (P.ctx_mode == 2) {
+    if constexpr (sizeof(T) == 2 && D == 128) {
+      rc = launch_ctx_tc(pr, P, q, Kc, Vc, fp.ws_o, fp.ws_ml, fp.scale_log2, rec);
+      if (rc) return rc;
+    } else {
+      return BA_EINVAL;
+    }
+  } else if (P.ctx_mode == 1 && P.nsc > 0) {
     ba::FmaParams f = fp;
     f.n_ctx_items = g * P.nsc * P.nrb_c;
     rc = launch_fma_rb<T, D>(P.rb_c, f.n_ctx_items, f, rec);
@@ -225,6 +362,17 @@ int run_plan(const ba_problem_t* pr, const Plan& P, const void* q, const void* K
   mp.ws_ml = fp.ws_ml;
   mp.rows = b * h;
   mp.S = P.S;
+  mp.h = h;
+  mp.p = p;
+  mp.ctx_mode = P.ctx_mode;
+  mp.nsc = P.nsc;
+  mp.tc_N = P.tc_N;
+  mp.tc_nrc = P.tc_nrc;
+  mp.tc_ntile = P.tc_ntile;
+  mp.tc_G = P.tc_G;
+  mp.tc_T = P.tc_T;
+  mp.dec_slot0 = P.dec_slot0;
+  mp.nsd = P.nsd;
   mp.out = out;
   mp.lse = lse;
   const int warps_per_block = 8;
@@ -386,10 +534,15 @@ const char* ba_plan_string(const ba_problem_t* prob) {
     snprintf(g_plan_buf, sizeof g_plan_buf, "invalid (%d)", rc);
     return g_plan_buf;
   }
+  char ctxs[160];
+  if (P.ctx_mode == 2)
+    snprintf(ctxs, sizeof ctxs, "tc(N=%d,nrc=%d,tiles=%lld,ctas=%d,stages=%d,slots=%d,smem=%d)",
+             P.tc_N, P.tc_nrc, P.tc_T, P.tc_G, P.tc_nst, P.tc_S, P.tc_smem);
+  else
+    snprintf(ctxs, sizeof ctxs, "fma(nsc=%d,chunk=%d,rb=%d)", P.nsc, P.ctx_chunk, P.rb_c);
   snprintf(g_plan_buf, sizeof g_plan_buf,
-           "ctx=fma(nsc=%d,chunk=%d,rb=%d) dec=fma(nsd=%d,chunk=%d,rb=%d) S=%d launches=%d "
-           "ws=%zu",
-           P.nsc, P.ctx_chunk, P.rb_c, P.nsd, P.dec_chunk, P.rb_d, P.S, P.launches, P.ws_bytes);
+           "ctx=%s dec=fma(nsd=%d,chunk=%d,rb=%d) S=%d launches=%d ws=%zu", ctxs, P.nsd,
+           P.dec_chunk, P.rb_d, P.S, P.launches, P.ws_bytes);
   return g_plan_buf;
 }
 
@@ -400,7 +553,8 @@ const char* ba_launch_name(const ba_problem_t* prob, int k) {
   if (make_plan(prob, sms, false, &P) != BA_OK) return nullptr;
   const char* names[4];
   int n = 0;
-  if (P.nsc > 0) names[n++] = "ctx_fma";
+  if (P.ctx_mode == 2) names[n++] = "ctx_tc";
+  if (P.ctx_mode == 1) names[n++] = "ctx_fma";
   if (P.nsd > 0) names[n++] = "dec_fma";
   names[n++] = "merge";
   return (k >= 0 && k < n) ? names[k] : nullptr;

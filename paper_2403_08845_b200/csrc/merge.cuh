@@ -17,9 +17,28 @@ struct MergeParams {
   const float* ws_o;   // [rows][S][D]
   const float* ws_ml;  // [rows][S][2]
   int rows, S;
+  int h, p;
+  // context slots: mode 0 none, 1 fixed count nsc, 2 tensor-core split
+  int ctx_mode, nsc;
+  int tc_N, tc_nrc, tc_ntile, tc_G;
+  long long tc_T;
+  int dec_slot0, nsd;
   void* out;           // [rows][D] in T
   float* lse;          // [rows] or null
 };
+
+// Number of context partials written for output row gr.
+BA_DEVINL int ctx_slots_of_row(const MergeParams& P, int gr) {
+  if (P.ctx_mode == 0) return 0;
+  if (P.ctx_mode == 1) return P.nsc;
+  const int i = gr / P.h, j = gr % P.h;
+  const int c = j / P.p, r = i * P.p + (j % P.p);
+  const long long seg = (long long)c * P.tc_nrc + r / P.tc_N;
+  const long long ff = seg * P.tc_ntile, fl = ff + P.tc_ntile - 1;
+  const int klo = (int)(((ff + 1) * (long long)P.tc_G - 1) / P.tc_T);
+  const int khi = (int)(((fl + 1) * (long long)P.tc_G - 1) / P.tc_T);
+  return khi - klo + 1;
+}
 
 template <typename T, int D>
 __global__ void __launch_bounds__(256) merge_kernel(const MergeParams P) {
@@ -27,10 +46,13 @@ __global__ void __launch_bounds__(256) merge_kernel(const MergeParams P) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (warp >= P.rows) return;
+  const int nctx = ctx_slots_of_row(P, warp);
+  const int ntot = nctx + P.nsd;
+  // slot index of the k-th live partial
+  auto slot_of = [&](int k) { return k < nctx ? k : P.dec_slot0 + (k - nctx); };
   const float* ml = P.ws_ml + (size_t)warp * P.S * 2;
-  // max over slots
   float M = kNegInf;
-  for (int k = lane; k < P.S; k += 32) M = fmaxf(M, ml[2 * k]);
+  for (int k = lane; k < ntot; k += 32) M = fmaxf(M, ml[2 * slot_of(k)]);
 #pragma unroll
   for (int off = 16; off >= 1; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
   const float Ms = (M == kNegInf) ? 0.f : M;
@@ -39,14 +61,14 @@ __global__ void __launch_bounds__(256) merge_kernel(const MergeParams P) {
   for (int e = 0; e < EPL; ++e) acc[e] = 0.f;
   float L = 0.f;
   const float* o = P.ws_o + (size_t)warp * P.S * D;
-  for (int k = 0; k < P.S; ++k) {
-    const float mk = ml[2 * k];
-    const float w = ex2(mk - Ms);
-    L = fmaf(w, ml[2 * k + 1], L);
+  for (int k = 0; k < ntot; ++k) {
+    const int s = slot_of(k);
+    const float w = ex2(ml[2 * s] - Ms);
+    L = fmaf(w, ml[2 * s + 1], L);
 #pragma unroll
     for (int e = 0; e < EPL; ++e) {
       const int x = e * 32 + lane;
-      if (x < D) acc[e] = fmaf(w, o[(size_t)k * D + x], acc[e]);
+      if (x < D) acc[e] = fmaf(w, o[(size_t)s * D + x], acc[e]);
     }
   }
   const float invL = 1.f / L;
