@@ -1,0 +1,90 @@
+"""Multi-process (gloo, world_size 2, CPU) tests of the head-group sharding host
+logic: sharding the problem by KV group and all-gathering the output heads is
+bit-identical to the unsharded computation (groups are independent, Eq. 1
+PAPER.md:208).  The per-shard compute here is the oracle (no GPU in CI); on
+GPUs the same shard_inputs / gather_heads wrap the C ABI."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2403_08845_b200.dist import gather_heads, shard_bounds, shard_inputs
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, cfg_kw, seed, variant, q_out):
+    import oracle
+    from synth import Config, make_inputs
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        cfg = Config(**cfg_kw)
+        inp = make_inputs(cfg, seed, variant=variant)
+        ql, Kcl, Vcl, Kdl, Vdl = shard_inputs(inp.q, inp.Kc, inp.Vc, inp.Kd, inp.Vd, world, rank)
+        out, lse, _ = oracle.attn_decode(ql, Kcl, Vcl, Kdl, Vdl, inp.lens, scale=inp.scale)
+        out_t = torch.from_numpy(out).reshape(cfg.b, cfg.h // world, cfg.d)
+        full = gather_heads(out_t, world)
+        lse_t = torch.from_numpy(lse).reshape(cfg.b, cfg.h // world, 1)
+        full_lse = gather_heads(lse_t, world)
+        if rank == 0:
+            q_out.put((full.numpy(), full_lse.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("cfg_kw,variant", [
+    (dict(name="mha", dtype="bf16", b=3, h=8, g=8, d=32, mc=40, md=6), "ragged"),
+    (dict(name="gqa", dtype="bf16", b=4, h=8, g=2, d=16, mc=33, md=5), "normal"),
+    (dict(name="tiny", dtype="fp32", b=4, h=2, g=2, d=16, mc=32, md=4), "normal"),
+])
+def test_sharded_equals_unsharded(cfg_kw, variant):
+    import oracle
+    from synth import Config, make_inputs
+
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, cfg_kw, 5, variant, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    full, full_lse = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    cfg = Config(**cfg_kw)
+    inp = make_inputs(cfg, 5, variant=variant)
+    ref, ref_lse, _ = oracle.attn_decode(inp.q, inp.Kc, inp.Vc, inp.Kd, inp.Vd, inp.lens,
+                                         scale=inp.scale)
+    np.testing.assert_array_equal(full.reshape(-1, cfg.d), ref)
+    np.testing.assert_array_equal(full_lse.reshape(-1), ref_lse)
+
+
+def test_shard_bounds():
+    assert shard_bounds(32, 32, 8, 3) == (12, 16, 12, 16)
+    assert shard_bounds(32, 8, 4, 1) == (2, 4, 8, 16)
+    assert shard_bounds(64, 64, 2, 1) == (32, 64, 32, 64)
+    with pytest.raises(ValueError):
+        shard_bounds(48, 1, 2, 0)  # MQA: replicas only
+    # shards tile the heads exactly once
+    for world in (1, 2, 4, 8):
+        heads = []
+        for r in range(world):
+            g0, g1, h0, h1 = shard_bounds(32, 8, world, r) if 8 % world == 0 else (0, 0, 0, 0)
+            heads += list(range(h0, h1))
+        if 8 % world == 0:
+            assert heads == list(range(32))
