@@ -83,12 +83,14 @@ typedef struct {
   uint32_t flags;   /* BA_FLAG_*; 0 for the default (fastest) path                      */
 } ba_problem_t;
 
-/* Bytes of device workspace bifurcated_attn_decode() needs (fp32 partials
- * (m, l, o[d]) per output row and split, plus completion counters).  Returns 0
- * for an invalid problem.  The workspace must be 16-byte aligned; its
- * completion counters must be zero before the FIRST call (cudaMemset once);
- * every call leaves them zero again, so it can be reused back to back on one
- * stream without re-initialisation. */
+/* Bytes of device workspace bifurcated_attn_decode() / replicated_attn_decode()
+ * need: per-(group, row chunk) completion counters at offset 0, then fp32
+ * partials (m, l, o[d]) per output row and split.  Returns 0 for an invalid
+ * problem.  The workspace must be 16-byte aligned and ZEROED ONCE before its
+ * first use (cudaMemset); every completed call leaves the counters zero
+ * again, so one workspace serves any number of back-to-back calls (and CUDA
+ * graph replays) of the same problem on one stream.  Calls that may run
+ * concurrently need separate workspaces. */
 size_t ba_workspace_bytes(const ba_problem_t* prob);
 
 /* One decode step of bifurcated attention (see above).  Kc/Vc are read from

@@ -1,19 +1,22 @@
 // bifattn_api.cu — host side of the C ABI declared in include/bifattn.h:
 // validation, planning (splits, kernel choice), workspace layout, launches.
 //
-// Plan of one bifurcated step:
-//   1. context branch  — Kc/Vc read once for all b samples (Eq. 3-4 context rows,
-//      PAPER.md:254, :266): tcgen05 kernel (ctx_tc.cuh) when bf16, d = 128 and
-//      b*p >= 16 rows share the tile; otherwise the FMA kernel (fma_partial.cuh);
-//   2. decode branch   — Kd/Vd of each sample: FMA kernel;
-//   3. merge           — one log-sum-exp over all partials per row (merge.cuh).
+// Plans of one bifurcated step:
+//   TC  (bf16, d = 128, b*p >= 16 rows share the context tile): ONE persistent
+//       launch of bif_tc_kernel (bif_tc.cuh) — context tiles (Kc/Vc read once
+//       for all b samples, Eq. 3-4 context rows) and decode
+//       tiles (Kd/Vd per sample) stream through one
+//       TMA/tcgen05 pipeline; the last partial of each (group, row chunk) merges.
+//   FMA (fp32, other d, few rows): context FMA kernel + decode FMA kernel
+//       (fma_partial.cuh) + merge kernel (merge.cuh): three launches.
+// The replicated-KV baseline runs the same kernels with no context branch.
 #include <mutex>
 #include <cstdio>
 #include <cstring>
 
 #include "../../include/bifattn.h"
 #include "common.cuh"
-#include "ctx_tc.cuh"
+#include "bif_tc.cuh"
 #include "fma_partial.cuh"
 #include "merge.cuh"
 
@@ -88,10 +91,13 @@ struct Plan {
   bool bf16 = false;
   int elem = 0;
   bool replicated = false;
-  int ctx_mode = 0;  // 0 none (replicated baseline), 1 FMA kernel, 2 tcgen05 kernel
-  // tcgen05 context branch
-  int tc_N = 0, tc_nrc = 0, tc_ntile = 0, tc_G = 0, tc_nst = 0, tc_S = 0, tc_smem = 0;
-  long long tc_T = 0;
+  int ctx_mode = 0;  // 0 none (replicated baseline), 1 FMA kernel, 2 in the tcgen05 kernel
+  bool tc = false;   // single-launch tcgen05 plan
+  // tcgen05 plan
+  int tc_N = 0, tc_nrc = 0, tc_ntile_c = 0, tc_ntile_d = 0, tc_G = 0, tc_nst = 0;
+  int tc_Sc = 0, tc_Sd = 0, tc_smem = 0;
+  long long tc_Tc = 0, tc_T = 0;
+  size_t off_cnt = 0;
   // FMA context branch
   int nsc = 0, ctx_chunk = 0, rb_c = 1, nrb_c = 0;
   // FMA decode branch
@@ -101,6 +107,14 @@ struct Plan {
   size_t off_o = 0, off_ml = 0, ws_bytes = 0;
   int launches = 0;
 };
+
+// Completion counters live at the start of every plan's workspace, sized for
+// the most (group, row chunk) pairs any plan can use, so a call of any plan
+// leaves them zero for the next one.
+size_t counter_bytes(const ba_problem_t* pr) {
+  const long long chunks = (long long)pr->g * (((long long)pr->b * (pr->h / pr->g) + 15) / 16);
+  return ((size_t)chunks * sizeof(unsigned) + 255) & ~(size_t)255;
+}
 
 int pick_rb(int rows) { return rows >= 4 ? 4 : (rows >= 2 ? 2 : 1); }
 
@@ -130,9 +144,9 @@ int make_plan(const ba_problem_t* pr, int sms, bool replicated, Plan* pl) {
   const int target = 4 * sms;  // CTAs of 128 threads per launch (~4 per SM)
   const int R = b * p;
   int tcN = 0;
-  if (!replicated && P.bf16 && pr->d == 128 && R >= 16 && !(pr->flags & BA_FLAG_FORCE_FMA)) {
-    // tensor-core context branch: N = rows per chunk, a multiple of 16 and of p
-    static const int cands[] = {16, 32, 48, 64};  // > 64 spills registers (round 2)
+  if (P.bf16 && pr->d == 128 && R >= 16 && !(pr->flags & BA_FLAG_FORCE_FMA)) {
+    // tcgen05 plan: N = rows per chunk, a multiple of 16 and of p, >= p
+    static const int cands[] = {16, 32, 48, 64};  // > 64 spills softmax registers
     int best_fit = 0, largest = 0;
     for (int N : cands) {
       if (N % p) continue;
@@ -142,29 +156,50 @@ int make_plan(const ba_problem_t* pr, int sms, bool replicated, Plan* pl) {
     tcN = best_fit ? best_fit : largest;
   }
   if (tcN) {
-    P.ctx_mode = 2;
+    P.tc = true;
+    P.ctx_mode = replicated ? 0 : 2;
     P.tc_N = tcN;
     P.tc_nrc = cdiv(R, tcN);
-    P.tc_ntile = cdiv(pr->mc, 128);
-    P.tc_T = (long long)g * P.tc_nrc * P.tc_ntile;
-    P.tc_G = (int)(P.tc_T < sms ? P.tc_T : sms);
-    const int avail = 227 * 1024 - ba::ctx::smem_fixed(tcN);
-    P.tc_nst = avail / ba::ctx::kStageBytes;
-    if (P.tc_nst > 4) P.tc_nst = 4;
-    P.tc_smem = P.tc_nst * ba::ctx::kStageBytes + ba::ctx::smem_fixed(tcN);
-    // slots: the most CTAs any (group, row chunk) is split over
-    int smax = 1;
-    for (long long seg = 0; seg < (long long)g * P.tc_nrc; ++seg) {
-      const long long ff = seg * P.tc_ntile, fl = ff + P.tc_ntile - 1;
-      const int n = ba::ctx::owner(fl, P.tc_T, P.tc_G) - ba::ctx::owner(ff, P.tc_T, P.tc_G) + 1;
-      if (n > smax) smax = n;
-    }
-    P.tc_S = smax;
-    P.nsc = 0;
-    P.dec_stride = pr->md_cap;
+    P.dec_stride = replicated ? pr->mc + pr->md_cap : pr->md_cap;
     P.dec_cap = pr->md_cap;
-    P.lens_offset = 0;
-  } else if (!replicated) {
+    P.lens_offset = replicated ? pr->mc : 0;
+    P.tc_ntile_c = replicated ? 0 : cdiv(pr->mc, 128);
+    P.tc_ntile_d = cdiv(P.lens_offset + P.dec_cap, 128);
+    P.tc_Tc = (long long)g * P.tc_nrc * P.tc_ntile_c;
+    P.tc_T = P.tc_Tc + (long long)b * g * P.tc_ntile_d;
+    P.tc_G = (int)(P.tc_T < sms ? P.tc_T : sms);
+    const int avail = 227 * 1024 - ba::bif::smem_fixed(tcN);
+    P.tc_nst = avail / ba::bif::kStageBytes;
+    if (P.tc_nst > 4) P.tc_nst = 4;
+    P.tc_smem = P.tc_nst * ba::bif::kStageBytes + ba::bif::smem_fixed(tcN);
+    // slots: the most CTAs one context (c, rc) / decode (i, c) sequence is split over
+    auto parts = [&](long long ff, long long n) {
+      return ba::bif::owner(ff + n - 1, P.tc_T, P.tc_G) - ba::bif::owner(ff, P.tc_T, P.tc_G) + 1;
+    };
+    int sc = 0, sd = 0;
+    for (long long seg = 0; P.tc_ntile_c && seg < (long long)g * P.tc_nrc; ++seg) {
+      const int n = parts(seg * P.tc_ntile_c, P.tc_ntile_c);
+      if (n > sc) sc = n;
+    }
+    for (long long seg = 0; P.tc_ntile_d && seg < (long long)b * g; ++seg) {
+      const int n = parts(P.tc_Tc + seg * P.tc_ntile_d, P.tc_ntile_d);
+      if (n > sd) sd = n;
+    }
+    P.tc_Sc = sc;
+    P.tc_Sd = sd;
+    P.S = sc + sd;
+    if (P.S < 1) P.S = 1;
+    const size_t rows = (size_t)b * h;
+    P.off_cnt = 0;
+    P.off_o = counter_bytes(pr);
+    P.off_ml = P.off_o + rows * P.S * 128 * sizeof(float);
+    P.ws_bytes = P.off_ml + rows * P.S * 2 * sizeof(float);
+    P.ws_bytes = (P.ws_bytes + 255) & ~(size_t)255;
+    P.launches = 1;
+    *pl = P;
+    return BA_OK;
+  }
+  if (!replicated) {
     // context branch, FMA kernel: rows R = b*p share each Kc tile
     P.ctx_mode = 1;
     P.rb_c = pick_rb(R);
@@ -201,13 +236,12 @@ int make_plan(const ba_problem_t* pr, int sms, bool replicated, Plan* pl) {
     P.nsd = 0;
     P.dec_chunk = 32;
   }
-  const int nctx_slots = P.ctx_mode == 2 ? P.tc_S : P.nsc;
-  P.dec_slot0 = nctx_slots;
-  P.S = nctx_slots + P.nsd;
+  P.dec_slot0 = P.nsc;
+  P.S = P.nsc + P.nsd;
   if (P.S < 1) P.S = 1;
   const size_t rows = (size_t)b * h;
-  P.off_o = 0;
-  P.off_ml = rows * P.S * P.D * sizeof(float);
+  P.off_o = counter_bytes(pr);
+  P.off_ml = P.off_o + rows * P.S * P.D * sizeof(float);
   P.ws_bytes = P.off_ml + rows * P.S * 2 * sizeof(float);
   P.ws_bytes = (P.ws_bytes + 255) & ~(size_t)255;
   P.launches = (P.ctx_mode != 0 ? 1 : 0) + (P.nsd > 0 ? 1 : 0) + 1;
@@ -269,11 +303,11 @@ int make_tmap_3d(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uin
 }
 
 template <int N>
-int launch_ctx_tc_n(const ba::CtxTcParams& cp, int smem, LaunchRec& rec) {
+int launch_bif_tc_n(const ba::BifTcParams& bp, int smem, LaunchRec& rec) {
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [&] {
-    attr_err = cudaFuncSetAttribute(ba::ctx_tc_kernel<N>,
+    attr_err = cudaFuncSetAttribute(ba::bif_tc_kernel<N>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
   });
   if (attr_err != cudaSuccess) {
@@ -281,36 +315,51 @@ int launch_ctx_tc_n(const ba::CtxTcParams& cp, int smem, LaunchRec& rec) {
     return BA_ECUDA;
   }
   rec.begin();
-  ba::ctx_tc_kernel<N><<<cp.G, ba::ctx::kThreads, smem, rec.st>>>(cp);
+  ba::bif_tc_kernel<N><<<bp.G, ba::bif::kThreads, smem, rec.st>>>(bp);
   return rec.end();
 }
 
-int launch_ctx_tc(const ba_problem_t* pr, const Plan& P, const void* q, const void* Kc,
-                  const void* Vc, float* ws_o, float* ws_ml, float scale_log2, LaunchRec& rec) {
-  ba::CtxTcParams cp;
-  memset(&cp, 0, sizeof cp);
+// Single-launch tcgen05 step.  Replicated baseline: Kc = Vc = nullptr, Kd/Vd
+// are the replicated caches [b][g][mc+md_cap][d].
+int run_tc(const ba_problem_t* pr, const Plan& P, const void* q, const void* Kc, const void* Vc,
+           const void* Kd, const void* Vd, const int32_t* lens, void* out, float* lse, void* ws,
+           float scale_log2, cudaStream_t st) {
+  ba::BifTcParams bp;
+  memset(&bp, 0, sizeof bp);
   const int p = pr->h / pr->g;
   const uint64_t d = 128;
-  int rc = make_tmap_3d(&cp.tmK, Kc, d, pr->mc, pr->g, d * 2, (uint64_t)pr->mc * d * 2, 128, 1);
-  if (!rc) rc = make_tmap_3d(&cp.tmV, Vc, d, pr->mc, pr->g, d * 2, (uint64_t)pr->mc * d * 2, 128, 1);
-  if (!rc)
-    rc = make_tmap_3d(&cp.tmQ, q, d, pr->h, pr->b, d * 2, (uint64_t)pr->h * d * 2, p, P.tc_N / p);
+  int rc = BA_OK;
+  if (P.tc_Tc > 0) {
+    rc = make_tmap_3d(&bp.tmKc, Kc, d, pr->mc, pr->g, d * 2, (uint64_t)pr->mc * d * 2, 128, 1);
+    if (!rc) rc = make_tmap_3d(&bp.tmVc, Vc, d, pr->mc, pr->g, d * 2, (uint64_t)pr->mc * d * 2, 128, 1);
+    if (!rc) rc = make_tmap_3d(&bp.tmQc, q, d, pr->h, pr->b, d * 2, (uint64_t)pr->h * d * 2, p, P.tc_N / p);
+  }
+  if (!rc && P.tc_T > P.tc_Tc) {
+    const uint64_t ds = (uint64_t)P.dec_stride;
+    const uint64_t bg = (uint64_t)pr->b * pr->g;
+    rc = make_tmap_3d(&bp.tmKd, Kd, d, ds, bg, d * 2, ds * d * 2, 128, 1);
+    if (!rc) rc = make_tmap_3d(&bp.tmVd, Vd, d, ds, bg, d * 2, ds * d * 2, 128, 1);
+    if (!rc) rc = make_tmap_3d(&bp.tmQd, q, d, pr->h, pr->b, d * 2, (uint64_t)pr->h * d * 2, p, 1);
+  }
   if (rc) return rc;
-  cp.b = pr->b; cp.h = pr->h; cp.g = pr->g; cp.p = p; cp.mc = pr->mc;
-  cp.nrc = P.tc_nrc; cp.ntile = P.tc_ntile; cp.T = P.tc_T; cp.G = P.tc_G; cp.nst = P.tc_nst;
-  cp.scale_log2 = scale_log2;
-  cp.S = P.S;
-  cp.ws_o = ws_o;
-  cp.ws_ml = ws_ml;
+  bp.lens = lens;
+  bp.b = pr->b; bp.h = pr->h; bp.g = pr->g; bp.p = p; bp.mc = pr->mc;
+  bp.dec_cap = P.dec_cap; bp.lens_offset = P.lens_offset;
+  bp.nrc = P.tc_nrc; bp.ntile_c = P.tc_ntile_c; bp.ntile_d = P.tc_ntile_d;
+  bp.Tc = P.tc_Tc; bp.T = P.tc_T; bp.G = P.tc_G; bp.nst = P.tc_nst;
+  bp.scale_log2 = scale_log2;
+  bp.S = P.S; bp.Sc = P.tc_Sc;
+  bp.ws_o = reinterpret_cast<float*>(static_cast<char*>(ws) + P.off_o);
+  bp.ws_ml = reinterpret_cast<float*>(static_cast<char*>(ws) + P.off_ml);
+  bp.counters = reinterpret_cast<unsigned*>(static_cast<char*>(ws) + P.off_cnt);
+  bp.out = out;
+  bp.lse = lse;
+  LaunchRec rec(st);
   switch (P.tc_N) {
-    case 16: return launch_ctx_tc_n<16>(cp, P.tc_smem, rec);
-    case 32: return launch_ctx_tc_n<32>(cp, P.tc_smem, rec);
-    case 48: return launch_ctx_tc_n<48>(cp, P.tc_smem, rec);
-    case 64: return launch_ctx_tc_n<64>(cp, P.tc_smem, rec);
-    case 80: return launch_ctx_tc_n<80>(cp, P.tc_smem, rec);
-    case 96: return launch_ctx_tc_n<96>(cp, P.tc_smem, rec);
-    case 112: return launch_ctx_tc_n<112>(cp, P.tc_smem, rec);
-    case 128: return launch_ctx_tc_n<128>(cp, P.tc_smem, rec);
+    case 16: return launch_bif_tc_n<16>(bp, P.tc_smem, rec);
+    case 32: return launch_bif_tc_n<32>(bp, P.tc_smem, rec);
+    case 48: return launch_bif_tc_n<48>(bp, P.tc_smem, rec);
+    case 64: return launch_bif_tc_n<64>(bp, P.tc_smem, rec);
   }
   return BA_EINVAL;
 }
@@ -334,16 +383,14 @@ int run_plan(const ba_problem_t* pr, const Plan& P, const void* q, const void* K
   fp.ws_o = reinterpret_cast<float*>(static_cast<char*>(ws) + P.off_o);
   fp.ws_ml = reinterpret_cast<float*>(static_cast<char*>(ws) + P.off_ml);
   int rc;
+  if (P.tc) {
+    if constexpr (sizeof(T) == 2 && D == 128)
+      return run_tc(pr, P, q, Kc, Vc, Kd, Vd, lens, out, lse, ws, fp.scale_log2, st);
+    return BA_EINVAL;
+  }
   LaunchRec rec(st);
-  // 1. context branch: tensor cores (bf16, d = 128, >= 16 rows) or FMA
-  if (P.ctx_mode == 2) {
-    if constexpr (sizeof(T) == 2 && D == 128) {
-      rc = launch_ctx_tc(pr, P, q, Kc, Vc, fp.ws_o, fp.ws_ml, fp.scale_log2, rec);
-      if (rc) return rc;
-    } else {
-      return BA_EINVAL;
-    }
-  } else if (P.ctx_mode == 1 && P.nsc > 0) {
+  // 1. context branch (FMA)
+  if (P.ctx_mode == 1 && P.nsc > 0) {
     ba::FmaParams f = fp;
     f.n_ctx_items = g * P.nsc * P.nrb_c;
     rc = launch_fma_rb<T, D>(P.rb_c, f.n_ctx_items, f, rec);
@@ -366,11 +413,6 @@ int run_plan(const ba_problem_t* pr, const Plan& P, const void* q, const void* K
   mp.p = p;
   mp.ctx_mode = P.ctx_mode;
   mp.nsc = P.nsc;
-  mp.tc_N = P.tc_N;
-  mp.tc_nrc = P.tc_nrc;
-  mp.tc_ntile = P.tc_ntile;
-  mp.tc_G = P.tc_G;
-  mp.tc_T = P.tc_T;
   mp.dec_slot0 = P.dec_slot0;
   mp.nsd = P.nsd;
   mp.out = out;
@@ -534,15 +576,17 @@ const char* ba_plan_string(const ba_problem_t* prob) {
     snprintf(g_plan_buf, sizeof g_plan_buf, "invalid (%d)", rc);
     return g_plan_buf;
   }
-  char ctxs[160];
-  if (P.ctx_mode == 2)
-    snprintf(ctxs, sizeof ctxs, "tc(N=%d,nrc=%d,tiles=%lld,ctas=%d,stages=%d,slots=%d,smem=%d)",
-             P.tc_N, P.tc_nrc, P.tc_T, P.tc_G, P.tc_nst, P.tc_S, P.tc_smem);
+  if (P.tc)
+    snprintf(g_plan_buf, sizeof g_plan_buf,
+             "fused_tc(N=%d,nrc=%d,ctx_tiles=%lld,dec_tiles=%lld,ctas=%d,stages=%d,slots=%d+%d,"
+             "smem=%d) launches=1 ws=%zu",
+             P.tc_N, P.tc_nrc, P.tc_Tc, P.tc_T - P.tc_Tc, P.tc_G, P.tc_nst, P.tc_Sc, P.tc_Sd,
+             P.tc_smem, P.ws_bytes);
   else
-    snprintf(ctxs, sizeof ctxs, "fma(nsc=%d,chunk=%d,rb=%d)", P.nsc, P.ctx_chunk, P.rb_c);
-  snprintf(g_plan_buf, sizeof g_plan_buf,
-           "ctx=%s dec=fma(nsd=%d,chunk=%d,rb=%d) S=%d launches=%d ws=%zu", ctxs, P.nsd,
-           P.dec_chunk, P.rb_d, P.S, P.launches, P.ws_bytes);
+    snprintf(g_plan_buf, sizeof g_plan_buf,
+             "ctx=fma(nsc=%d,chunk=%d,rb=%d) dec=fma(nsd=%d,chunk=%d,rb=%d) S=%d launches=%d "
+             "ws=%zu",
+             P.nsc, P.ctx_chunk, P.rb_c, P.nsd, P.dec_chunk, P.rb_d, P.S, P.launches, P.ws_bytes);
   return g_plan_buf;
 }
 
@@ -553,10 +597,13 @@ const char* ba_launch_name(const ba_problem_t* prob, int k) {
   if (make_plan(prob, sms, false, &P) != BA_OK) return nullptr;
   const char* names[4];
   int n = 0;
-  if (P.ctx_mode == 2) names[n++] = "ctx_tc";
-  if (P.ctx_mode == 1) names[n++] = "ctx_fma";
-  if (P.nsd > 0) names[n++] = "dec_fma";
-  names[n++] = "merge";
+  if (P.tc) {
+    names[n++] = "fused_tc";
+  } else {
+    if (P.ctx_mode == 1) names[n++] = "ctx_fma";
+    if (P.nsd > 0) names[n++] = "dec_fma";
+    names[n++] = "merge";
+  }
   return (k >= 0 && k < n) ? names[k] : nullptr;
 }
 

@@ -18,10 +18,8 @@ struct MergeParams {
   const float* ws_ml;  // [rows][S][2]
   int rows, S;
   int h, p;
-  // context slots: mode 0 none, 1 fixed count nsc, 2 tensor-core split
+  // context slots: mode 0 none, 1 fixed count nsc
   int ctx_mode, nsc;
-  int tc_N, tc_nrc, tc_ntile, tc_G;
-  long long tc_T;
   int dec_slot0, nsd;
   void* out;           // [rows][D] in T
   float* lse;          // [rows] or null
@@ -29,15 +27,8 @@ struct MergeParams {
 
 // Number of context partials written for output row gr.
 BA_DEVINL int ctx_slots_of_row(const MergeParams& P, int gr) {
-  if (P.ctx_mode == 0) return 0;
-  if (P.ctx_mode == 1) return P.nsc;
-  const int i = gr / P.h, j = gr % P.h;
-  const int c = j / P.p, r = i * P.p + (j % P.p);
-  const long long seg = (long long)c * P.tc_nrc + r / P.tc_N;
-  const long long ff = seg * P.tc_ntile, fl = ff + P.tc_ntile - 1;
-  const int klo = (int)(((ff + 1) * (long long)P.tc_G - 1) / P.tc_T);
-  const int khi = (int)(((fl + 1) * (long long)P.tc_G - 1) / P.tc_T);
-  return khi - klo + 1;
+  (void)gr;
+  return P.ctx_mode == 1 ? P.nsc : 0;
 }
 
 template <typename T, int D>

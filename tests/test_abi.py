@@ -96,5 +96,5 @@ def test_no_gpu_means_enodev_not_fallback(lib):
 
 def test_plan_string_mentions_branches(lib):
     s = lib.ba_plan_string(ctypes.byref(_prob())).decode()
-    assert "ctx=" in s and "dec=" in s
+    assert "ctx" in s and "dec" in s
     assert lib.ba_launches_per_call(ctypes.byref(_prob())) >= 1
