@@ -8,10 +8,10 @@
 //   decode segments:   the p query rows of sample i, group c against a run of
 //                      128-position tiles of that sample's own Kd[i][c]/Vd[i][c]
 //                      (PAPER.md:255, :267), masked at lens[i];
-//   merge:             the last segment to finish a (group, row chunk) joins
-//                      all its partials with one log-sum-exp — the single
-//                      softmax over S_c ⊕ S_d split at mc
-//                      and summed (Eq. 4) — and writes out / lse.
+//   merge:             the last partial to arrive for (sample i, group c) joins
+//                      that row set's partials with one log-sum-exp — the
+//                      single softmax over S_c ⊕ S_d split
+//                      at mc and summed (Eq. 4) — and writes out / lse.
 // Each context tile is read from HBM once for all b samples.
 //
 // Tile math (swap-AB: query rows are few, positions many):
@@ -31,12 +31,15 @@
 // the exact tile max, rescale l and O^T (TMEM) and raise m_run.  Same softmax;
 // values stay <= 2^kTh.
 //
-// Work split: flat tile index f over [context tiles | decode tiles]:
-//   f <  Tc : ((c*nrc + rc)*ntile_c + t)        context tile t of (c, rc)
-//   f >= Tc : Tc + ((i*g + c)*ntile_d + t)      decode tile t of (i, c)
-// CTA k of G takes [k*T/G, (k+1)*T/G): every CTA streams the same number of
-// 64 KB tiles (+-1).  A maximal run of one (c, rc) or (i, c) is a segment and
-// writes one partial (m, l, o) per row to its workspace slot.
+// Work split: context tiles fc = (c*nrc + rc)*ntile_c + t in [0, Tc) and
+// decode tiles fd = (i*g + c)*ntile_d + t in [0, Td).  CTA k of G takes
+// context tiles [k*Tc/G, (k+1)*Tc/G) and then decode tiles [k*Td/G,
+// (k+1)*Td/G): every CTA streams the same number of 64 KB tiles (+-1 of each
+// kind), and all context partials land before the decode ones, so the last
+// arrival of a (sample, group) is usually its own decode segment.  A maximal
+// run of one (c, rc) or (i, c) is a segment and writes one partial (m, l, o)
+// per row to its workspace slot.  q and O^T are double buffered across
+// segments so a segment boundary costs no pipeline drain.
 #pragma once
 #include "common.cuh"
 #include "tc_ptx.cuh"
@@ -52,13 +55,13 @@ struct BifTcParams {
   int b, h, g, p, mc;
   int dec_cap, lens_offset;  // decode length = lens_offset + clamp(lens[i], 0, dec_cap)
   int nrc, ntile_c, ntile_d;
-  long long Tc, T;           // context tiles, all tiles
+  long long Tc, Td;          // context tiles, decode tiles
   int G, nst;
   float scale_log2;
   int S, Sc;                 // slots per row; decode slots start at Sc
   float* ws_o;               // [b*h][S][128]
   float* ws_ml;              // [b*h][S][2]
-  unsigned* counters;        // [g*nrc] arrivals per (group, row chunk); self-resetting
+  unsigned* counters;        // [b*g] arrivals per (sample, group); self-resetting
   void* out;                 // [b][h][128] bf16
   float* lse;                // [b][h] or null
 };
@@ -74,11 +77,12 @@ __host__ __device__ constexpr int p_atom(int N) { return (N % 64 == 0) ? 64 : ((
 __host__ __device__ constexpr int p_layout(int N) {
   return p_atom(N) == 64 ? tc::kSw128 : (p_atom(N) == 32 ? tc::kSw64 : tc::kSw32);
 }
-__host__ __device__ constexpr int tmem_cols(int N) {
-  return 3 * N <= 32 ? 32 : 3 * N <= 64 ? 64 : 3 * N <= 128 ? 128 : 3 * N <= 256 ? 256 : 512;
+__host__ __device__ constexpr int tmem_cols(int N) {  // 2 S^T slots + 2 O^T buffers
+  return 4 * N <= 32 ? 32 : 4 * N <= 64 ? 64 : 4 * N <= 128 ? 128 : 4 * N <= 256 ? 256 : 512;
 }
-// dynamic smem besides the stages: q (256N) + 2 P buffers (512N) + scratch + barriers + align
-__host__ __device__ constexpr int smem_fixed(int N) { return 3 * 256 * N + 4096 + 1024 + 512 + 1024; }
+// dynamic smem besides the stages: 2 q buffers + 2 P buffers (256N each) + scratch (40N) +
+// barriers (512) + alignment slack (1024)
+__host__ __device__ constexpr int smem_fixed(int N) { return 4 * 256 * N + 40 * N + 512 + 1024; }
 
 // CTA owning flat tile f when T tiles are split over G CTAs as [kT/G, (k+1)T/G)
 __host__ __device__ inline int owner(long long f, long long T, int G) {
@@ -91,8 +95,7 @@ struct Seg {
   int t0, ntiles;  // first tile, tiles in this CTA's part of the segment
   int L;           // valid positions of the whole sequence
   int slot;        // workspace slot of this CTA's partial
-  int counter;     // merge counter index (c*nrc + rc of the rows)
-  long long next;  // flat index after this segment part
+  long long next;  // flat index (CTA work order) after this segment part
 };
 
 BA_DEVINL int dec_len(const BifTcParams& P, int i) {
@@ -101,12 +104,31 @@ BA_DEVINL int dec_len(const BifTcParams& P, int i) {
   return P.lens_offset + L;
 }
 
+// This CTA's work is the concatenation [context range | decode range]; the
+// "work index" w runs over it: w < nc -> context tile fc0 + w, else decode
+// tile fd0 + (w - nc).
+struct Range {
+  long long fc0, fc1, fd0, fd1;
+  BA_DEVINL long long n() const { return (fc1 - fc0) + (fd1 - fd0); }
+};
+BA_DEVINL Range my_range(const BifTcParams& P) {
+  Range r;
+  const long long k = blockIdx.x, G = P.G;
+  r.fc0 = k * P.Tc / G;
+  r.fc1 = (k + 1) * P.Tc / G;
+  r.fd0 = k * P.Td / G;
+  r.fd1 = (k + 1) * P.Td / G;
+  return r;
+}
+
 template <int N>
-BA_DEVINL Seg seg_at(const BifTcParams& P, long long f, long long f1) {
+BA_DEVINL Seg seg_at(const BifTcParams& P, const Range& rg, long long w) {
   Seg s;
-  if (f < P.Tc) {
+  const long long nc = rg.fc1 - rg.fc0;
+  if (w < nc) {
+    const long long f = rg.fc0 + w;
     const long long seg = f / P.ntile_c;
-    const long long fend = (seg + 1) * P.ntile_c < f1 ? (seg + 1) * P.ntile_c : f1;
+    const long long fend = min((seg + 1) * P.ntile_c, rg.fc1);
     s.dec = false;
     s.c = (int)(seg / P.nrc);
     s.rc = (int)(seg % P.nrc);
@@ -114,14 +136,13 @@ BA_DEVINL Seg seg_at(const BifTcParams& P, long long f, long long f1) {
     s.t0 = (int)(f - seg * P.ntile_c);
     s.ntiles = (int)(fend - f);
     s.L = P.mc;
-    s.slot = (int)blockIdx.x - owner(seg * P.ntile_c, P.T, P.G);
-    s.counter = (int)seg;
-    s.next = fend;
+    s.slot = (int)blockIdx.x - owner(seg * P.ntile_c, P.Tc, P.G);
+    s.next = w + (fend - f);
   } else {
-    const long long fd = f - P.Tc;
-    const long long seg = fd / P.ntile_d;  // i*g + c
-    const long long base = P.Tc + seg * P.ntile_d;
-    const long long fend = base + P.ntile_d < f1 ? base + P.ntile_d : f1;
+    const long long f = rg.fd0 + (w - nc);
+    const long long seg = f / P.ntile_d;  // i*g + c
+    const long long base = seg * P.ntile_d;
+    const long long fend = min(base + P.ntile_d, rg.fd1);
     s.dec = true;
     s.i = (int)(seg / P.g);
     s.c = (int)(seg % P.g);
@@ -129,24 +150,23 @@ BA_DEVINL Seg seg_at(const BifTcParams& P, long long f, long long f1) {
     s.t0 = (int)(f - base);
     s.ntiles = (int)(fend - f);
     s.L = dec_len(P, s.i);
-    s.slot = P.Sc + (int)blockIdx.x - owner(base, P.T, P.G);
-    s.counter = s.c * P.nrc + s.rc;
-    s.next = fend;
+    s.slot = P.Sc + (int)blockIdx.x - owner(base, P.Td, P.G);
+    s.next = w + (fend - f);
   }
   return s;
 }
 
-// Number of partials (context, decode) for the rows of counter (c, rc), and
-// expected arrivals at the counter.
+// Partials written for the rows of (sample i, group c): context segments of
+// its row chunk + decode segments of (i, c).
 BA_DEVINL int ctx_parts(const BifTcParams& P, int c, int rc) {
   if (P.Tc == 0) return 0;
   const long long ff = ((long long)c * P.nrc + rc) * P.ntile_c;
-  return owner(ff + P.ntile_c - 1, P.T, P.G) - owner(ff, P.T, P.G) + 1;
+  return owner(ff + P.ntile_c - 1, P.Tc, P.G) - owner(ff, P.Tc, P.G) + 1;
 }
 BA_DEVINL int dec_parts(const BifTcParams& P, int i, int c) {
-  if (P.ntile_d == 0) return 0;
-  const long long ff = P.Tc + ((long long)i * P.g + c) * P.ntile_d;
-  return owner(ff + P.ntile_d - 1, P.T, P.G) - owner(ff, P.T, P.G) + 1;
+  if (P.Td == 0) return 0;
+  const long long ff = ((long long)i * P.g + c) * P.ntile_d;
+  return owner(ff + P.ntile_d - 1, P.Td, P.G) - owner(ff, P.Td, P.G) + 1;
 }
 }  // namespace bif
 
@@ -184,30 +204,33 @@ __global__ void __launch_bounds__(bif::kThreads, 1)
   constexpr uint32_t IDESC_QK = tc::idesc_bf16(128, N, 0, 0);
   constexpr uint32_t IDESC_PV = tc::idesc_bf16(128, N, 1, 1);
   constexpr uint32_t TMEM_COLS = tmem_cols(N);
-  static_assert(N % 16 == 0 && N >= 16 && N <= 128, "N");
+  constexpr int QB = 256 * N;  // bytes of one q buffer / one P buffer
+  static_assert(N % 16 == 0 && N >= 16 && N <= 64, "N");
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int NST = P.nst;
   uint8_t* sm_stage = smem;
-  uint8_t* sm_q = smem + NST * kStageBytes;
-  uint8_t* sm_p = sm_q + 256 * N;
-  float* sm_red = reinterpret_cast<float*>(sm_p + 2 * 256 * N);  // [4][128] col max (slow path)
-  float* sm_l = sm_red + 4 * 128;                               // [4][128] row sums (epilogue)
-  float* sm_mrun = sm_l + 4 * 128;                              // [2][128] running max
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sm_mrun + 256);
-  uint64_t* kv_full = bars;       // [8]
-  uint64_t* kv_empty = bars + 8;  // [8]
-  uint64_t* q_full = bars + 16;
-  uint64_t* q_empty = bars + 17;
-  uint64_t* s_full = bars + 18;   // [2]
-  uint64_t* s_free = bars + 20;   // [2]
-  uint64_t* p_full = bars + 22;   // [2]
-  uint64_t* p_empty = bars + 24;  // [2]
-  uint64_t* o_full = bars + 26;
-  uint64_t* o_empty = bars + 27;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 28);
-  int* sm_flag = reinterpret_cast<int*>(bars + 29);
+  uint8_t* sm_q = smem + NST * kStageBytes;  // 2 buffers
+  uint8_t* sm_p = sm_q + 2 * QB;             // 2 buffers
+  float* sm_red = reinterpret_cast<float*>(sm_p + 2 * QB);  // [4][N] col max (slow path)
+  float* sm_l = sm_red + 4 * N;                             // [4][N] row sums (epilogue)
+  float* sm_mrun = sm_l + 4 * N;                            // [2][N] running max
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm_mrun + 2 * N);
+  uint64_t* kv_full = bars;        // [8]
+  uint64_t* kv_empty = bars + 8;   // [8]
+  uint64_t* q_full = bars + 16;    // [2]
+  uint64_t* q_empty = bars + 18;   // [2]
+  uint64_t* s_full = bars + 20;    // [2]
+  uint64_t* s_free = bars + 22;    // [2]
+  uint64_t* p_full = bars + 24;    // [2]
+  uint64_t* p_empty = bars + 26;   // [2]
+  uint64_t* o_full = bars + 28;    // [2]
+  uint64_t* o_empty = bars + 30;   // [2]
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 32);
+  // merge list (count + samples, <= N/p + 1 ints) reuses the slow-path scratch:
+  // the epilogue never overlaps a slow path of the same CTA
+  int* sm_last = reinterpret_cast<int*>(sm_red);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -216,16 +239,16 @@ __global__ void __launch_bounds__(bif::kThreads, 1)
       tc::mbar_init(tc::smem_u32(&kv_full[s]), 1);
       tc::mbar_init(tc::smem_u32(&kv_empty[s]), 1);
     }
-    tc::mbar_init(tc::smem_u32(q_full), 1);
-    tc::mbar_init(tc::smem_u32(q_empty), 1);
     for (int s = 0; s < 2; ++s) {
+      tc::mbar_init(tc::smem_u32(&q_full[s]), 1);
+      tc::mbar_init(tc::smem_u32(&q_empty[s]), 1);
       tc::mbar_init(tc::smem_u32(&s_full[s]), 1);
       tc::mbar_init(tc::smem_u32(&s_free[s]), 8);
       tc::mbar_init(tc::smem_u32(&p_full[s]), 8);
       tc::mbar_init(tc::smem_u32(&p_empty[s]), 1);
+      tc::mbar_init(tc::smem_u32(&o_full[s]), 1);
+      tc::mbar_init(tc::smem_u32(&o_empty[s]), 8);
     }
-    tc::mbar_init(tc::smem_u32(o_full), 1);
-    tc::mbar_init(tc::smem_u32(o_empty), 8);
     tc::fence_mbar_init();
   }
   if (warp == 0 && lane == 0) {
@@ -241,8 +264,8 @@ __global__ void __launch_bounds__(bif::kThreads, 1)
     tc::tmem_relinquish();
   }
   if (warp >= 4) {
-    // rows of q beyond a decode segment's p keep finite (zero) values
-    for (int k = threadIdx.x - 128; k < 256 * N / 16; k += 256)
+    // q rows beyond a decode segment's p stay finite (zero) until overwritten
+    for (int k = threadIdx.x - 128; k < 2 * QB / 16; k += 256)
       reinterpret_cast<uint4*>(sm_q)[k] = make_uint4(0, 0, 0, 0);
     tc::fence_proxy_async_smem();
   }
@@ -250,12 +273,11 @@ __global__ void __launch_bounds__(bif::kThreads, 1)
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = *tmem_holder;
-  const uint32_t tS = tmem;          // S slots at columns [0,N), [N,2N)
-  const uint32_t tO = tmem + 2 * N;  // O^T at [2N, 3N)
+  const uint32_t tS = tmem;          // S^T slots at columns [0,N), [N,2N)
+  const uint32_t tO = tmem + 2 * N;  // O^T buffers at [2N,3N), [3N,4N)
 
-  const long long T = P.T;
-  const long long f0 = (long long)blockIdx.x * T / P.G;
-  const long long f1 = (long long)(blockIdx.x + 1) * T / P.G;
+  const Range rg = my_range(P);
+  const long long nw = rg.n();
 
   if (warp == 0) {
     // ============================ TMA producer ============================
@@ -263,18 +285,20 @@ __global__ void __launch_bounds__(bif::kThreads, 1)
       uint32_t tt = 0, sg = 0;
       const uint64_t pol_c = P.nrc == 1 ? tc::policy_evict_first() : tc::policy_evict_last();
       const uint64_t pol_d = tc::policy_evict_first();
-      for (long long f = f0; f < f1; ++sg) {
-        const Seg s = seg_at<N>(P, f, f1);
-        tc::mbar_wait(tc::smem_u32(q_empty), (sg & 1) ^ 1);
-        const uint32_t qb = tc::smem_u32(q_full);
+      for (long long w = 0; w < nw; ++sg) {
+        const Seg s = seg_at<N>(P, rg, w);
+        const uint32_t qbuf = sg & 1;
+        tc::mbar_wait(tc::smem_u32(&q_empty[qbuf]), ((sg >> 1) & 1) ^ 1);
+        const uint32_t qb = tc::smem_u32(&q_full[qbuf]);
+        const uint32_t qdst = tc::smem_u32(sm_q + qbuf * QB);
         if (!s.dec) {
           tc::mbar_arrive_expect_tx(qb, 2 * N * 128);
-          tc::tma_load_3d(tc::smem_u32(sm_q), &P.tmQc, qb, 0, s.c * P.p, s.rc * (N / P.p));
-          tc::tma_load_3d(tc::smem_u32(sm_q + N * 128), &P.tmQc, qb, 64, s.c * P.p, s.rc * (N / P.p));
+          tc::tma_load_3d(qdst, &P.tmQc, qb, 0, s.c * P.p, s.rc * (N / P.p));
+          tc::tma_load_3d(qdst + N * 128, &P.tmQc, qb, 64, s.c * P.p, s.rc * (N / P.p));
         } else {
           tc::mbar_arrive_expect_tx(qb, 2 * P.p * 128);
-          tc::tma_load_3d(tc::smem_u32(sm_q), &P.tmQd, qb, 0, s.c * P.p, s.i);
-          tc::tma_load_3d(tc::smem_u32(sm_q + N * 128), &P.tmQd, qb, 64, s.c * P.p, s.i);
+          tc::tma_load_3d(qdst, &P.tmQd, qb, 0, s.c * P.p, s.i);
+          tc::tma_load_3d(qdst + N * 128, &P.tmQd, qb, 64, s.c * P.p, s.i);
         }
         const CUtensorMap* mk = s.dec ? &P.tmKd : &P.tmKc;
         const CUtensorMap* mv = s.dec ? &P.tmVd : &P.tmVc;
@@ -292,56 +316,50 @@ __global__ void __launch_bounds__(bif::kThreads, 1)
           tc::tma_load_3d_hint(dst + 32768, mv, bar, 0, t * kBM, z, pol);
           tc::tma_load_3d_hint(dst + 49152, mv, bar, 64, t * kBM, z, pol);
         }
-        f = s.next;
+        w = s.next;
       }
     }
   } else if (warp == 1) {
     // ============================ MMA issuer ==============================
-    // Issues QK(u) as soon as its K tile and an S slot are ready and PV(v) as
-    // soon as P(v) is ready, whichever comes first (no PV waits on a TMA).
+    // QK(u) issues as soon as its K tile, q and an S slot are ready; PV(v) as
+    // soon as P(v) (and, for a segment's first tile, a free O buffer) is
+    // ready — whichever comes first.
     if (lane == 0) {
       const uint32_t q_addr = tc::smem_u32(sm_q);
       const uint32_t p_addr = tc::smem_u32(sm_p);
       uint32_t tt_qk = 0, u_qk = 0, u_pv = 0, sg_qk = 0, sg_pv = 0;
-      long long fq = f0, fp = f0;     // next tile for QK / PV
-      long long seg_end_q = f0, seg_end_p = f0;
-      bool q_ready = false;
-      bool pv_first = true;
-      uint32_t stage_of[4] = {0, 0, 0, 0};  // stage of unit u (ring of 4 >= in-flight units)
-      while (fp < f1) {
+      long long wq = 0, wp = 0, seg_end_q = 0, seg_end_p = 0;
+      bool q_ready = false, pv_first = true;
+      uint32_t stage_of[4] = {0, 0, 0, 0};
+      while (wp < nw) {
         bool progressed = false;
         // ---- QK ----
-        if (fq < f1 && u_qk - u_pv < 2) {
-          if (fq == seg_end_q) {
-            // new segment: need its q tile (and the previous segment's QKs are issued)
-            if (!q_ready) {
-              if (mbar_test(tc::smem_u32(q_full), sg_qk & 1)) {
-                q_ready = true;
-                const Seg s = seg_at<N>(P, fq, f1);
-                seg_end_q = s.next;
-              }
-            }
+        if (wq < nw && u_qk - u_pv < 2) {
+          if (!q_ready && mbar_test(tc::smem_u32(&q_full[sg_qk & 1]), (sg_qk >> 1) & 1)) {
+            q_ready = true;
+            seg_end_q = seg_at<N>(P, rg, wq).next;
           }
-          if (q_ready || fq < seg_end_q) {
+          if (q_ready) {
             const uint32_t st = tt_qk % NST;
             const uint32_t slot = u_qk & 1;
-            if (fq < seg_end_q && mbar_test(tc::smem_u32(&kv_full[st]), (tt_qk / NST) & 1) &&
+            if (mbar_test(tc::smem_u32(&kv_full[st]), (tt_qk / NST) & 1) &&
                 mbar_test(tc::smem_u32(&s_free[slot]), ((u_qk >> 1) & 1) ^ 1)) {
               tc::tc_fence_after();
               const uint32_t kbase = tc::smem_u32(sm_stage + st * kStageBytes);
+              const uint32_t qbase = q_addr + (sg_qk & 1) * QB;
 #pragma unroll
               for (int k = 0; k < 8; ++k) {
                 const uint64_t ad = tc::smem_desc(kbase + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024, tc::kSw128);
-                const uint64_t bd = tc::smem_desc(q_addr + (k >> 2) * (N * 128) + (k & 3) * 32, 16, 1024, tc::kSw128);
+                const uint64_t bd = tc::smem_desc(qbase + (k >> 2) * (N * 128) + (k & 3) * 32, 16, 1024, tc::kSw128);
                 tc::mma_bf16(tS + slot * N, ad, bd, IDESC_QK, k > 0 ? 1u : 0u);
               }
               tc::mma_commit(tc::smem_u32(&s_full[slot]));
               stage_of[u_qk & 3] = st;
-              ++fq;
+              ++wq;
               ++tt_qk;
               ++u_qk;
-              if (fq == seg_end_q) {
-                tc::mma_commit(tc::smem_u32(q_empty));  // q buffer reusable
+              if (wq == seg_end_q) {
+                tc::mma_commit(tc::smem_u32(&q_empty[sg_qk & 1]));  // q buffer reusable
                 q_ready = false;
                 ++sg_qk;
               }
@@ -352,31 +370,31 @@ __global__ void __launch_bounds__(bif::kThreads, 1)
         // ---- PV ----
         if (u_pv < u_qk) {
           const uint32_t slot = u_pv & 1;
-          if (fp == seg_end_p) {
-            const Seg s = seg_at<N>(P, fp, f1);
-            seg_end_p = s.next;
+          if (wp == seg_end_p) {
+            seg_end_p = seg_at<N>(P, rg, wp).next;
             pv_first = true;
           }
+          const uint32_t ob = sg_pv & 1;
           bool ok = mbar_test(tc::smem_u32(&p_full[slot]), (u_pv >> 1) & 1);
-          if (ok && pv_first) ok = mbar_test(tc::smem_u32(o_empty), (sg_pv & 1) ^ 1);
+          if (ok && pv_first) ok = mbar_test(tc::smem_u32(&o_empty[ob]), ((sg_pv >> 1) & 1) ^ 1);
           if (ok) {
             tc::tc_fence_after();
             const uint32_t st = stage_of[u_pv & 3];
             const uint32_t vbase = tc::smem_u32(sm_stage + st * kStageBytes + 32768);
-            const uint32_t pbase = p_addr + slot * 256 * N;
+            const uint32_t pbase = p_addr + slot * QB;
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
               const uint64_t ad = tc::smem_desc(vbase + k * 2048, 16384, 1024, tc::kSw128);
               const uint64_t bd = tc::smem_desc(pbase + k * 16 * PRB, PLBO, 8 * PRB, p_layout(N));
-              tc::mma_bf16(tO, ad, bd, IDESC_PV, (pv_first && k == 0) ? 0u : 1u);
+              tc::mma_bf16(tO + ob * N, ad, bd, IDESC_PV, (pv_first && k == 0) ? 0u : 1u);
             }
             tc::mma_commit(tc::smem_u32(&p_empty[slot]));
             tc::mma_commit(tc::smem_u32(&kv_empty[st]));
             pv_first = false;
-            ++fp;
+            ++wp;
             ++u_pv;
-            if (fp == seg_end_p) {
-              tc::mma_commit(tc::smem_u32(o_full));
+            if (wp == seg_end_p) {
+              tc::mma_commit(tc::smem_u32(&o_full[ob]));
               ++sg_pv;
             }
             progressed = true;
@@ -396,8 +414,10 @@ __global__ void __launch_bounds__(bif::kThreads, 1)
     const float sl2 = P.scale_log2;
     const int R = P.b * P.p;
     uint32_t u = 0, sg = 0, cur = 0;
-    for (long long f = f0; f < f1; ++sg) {
-      const Seg s = seg_at<N>(P, f, f1);
+    for (long long w = 0; w < nw; ++sg) {
+      const Seg s = seg_at<N>(P, rg, w);
+      const uint32_t ob = sg & 1;
+      const uint32_t tOb = tO + ob * N;
       float l_part[CPT];
 #pragma unroll
       for (int n = 0; n < CPT; ++n) l_part[n] = 0.f;
@@ -405,7 +425,7 @@ __global__ void __launch_bounds__(bif::kThreads, 1)
         const int t = s.t0 + j;
         const uint32_t slot = u & 1;
         const bool first = (j == 0);
-        const float* mrun = sm_mrun + cur * 128 + col0;
+        const float* mrun = sm_mrun + cur * N + col0;
         tc::mbar_wait(tc::smem_u32(&s_full[slot]), (u >> 1) & 1);
         tc::tc_fence_after();
         float x[CPT];
@@ -429,16 +449,16 @@ __global__ void __launch_bounds__(bif::kThreads, 1)
             float v = x[n];
 #pragma unroll
             for (int off = 16; off >= 1; off >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, off));
-            if (lane == (n & 31)) sm_red[quad * 128 + col0 + n] = v;
+            if (lane == (n & 31)) sm_red[quad * N + col0 + n] = v;
           }
           tc::named_bar_sync(2, 256);
-          float* mnext = sm_mrun + (cur ^ 1) * 128 + col0;
+          float* mnext = sm_mrun + (cur ^ 1) * N + col0;
 #pragma unroll
           for (int n = 0; n < CPT; ++n) {
             const int col = col0 + n;
             const float mref = first ? 0.f : mrun[n];
-            const float cm = fmaxf(fmaxf(sm_red[col], sm_red[128 + col]),
-                                   fmaxf(sm_red[256 + col], sm_red[384 + col]));
+            const float cm = fmaxf(fmaxf(sm_red[col], sm_red[N + col]),
+                                   fmaxf(sm_red[2 * N + col], sm_red[3 * N + col]));
             const float tmax = mref + cm;  // -inf if the whole column is masked
             const float mold = first ? kNegInf : mrun[n];
             const float mnew = fmaxf(mold, tmax);
@@ -454,7 +474,7 @@ __global__ void __launch_bounds__(bif::kThreads, 1)
 #pragma unroll
             for (int n = 0; n < CPT; n += 8) {
               uint32_t orr[8];
-              tc::tmem_ld<8>(tO + col0 + n + lane_addr, orr);
+              tc::tmem_ld<8>(tOb + col0 + n + lane_addr, orr);
               tc::tmem_ld_wait();
 #pragma unroll
               for (int e = 0; e < 8; ++e) {
@@ -462,7 +482,7 @@ __global__ void __launch_bounds__(bif::kThreads, 1)
                 const float a = (mn == kNegInf) ? 1.f : ex2(mo - mn);
                 orr[e] = __float_as_uint(__uint_as_float(orr[e]) * a);
               }
-              tc::tmem_st<8>(tO + col0 + n + lane_addr, orr);
+              tc::tmem_st<8>(tOb + col0 + n + lane_addr, orr);
             }
             tc::tmem_st_wait();
             tc::tc_fence_before();
@@ -470,18 +490,18 @@ __global__ void __launch_bounds__(bif::kThreads, 1)
           tc::named_bar_sync(2, 256);
           cur ^= 1;
         }
-        // ---- P = 2^x (bf16) into shared memory, per-position row sums ----
+        // ---- P = 2^x (bf16) into shared memory; row sums of the SAME bf16
+        //      values, so out = sum P v / sum P is a convex combination ----
         tc::mbar_wait(tc::smem_u32(&p_empty[slot]), ((u >> 1) & 1) ^ 1);
-        uint8_t* pbuf = sm_p + slot * 256 * N;
+        uint8_t* pbuf = sm_p + slot * QB;
 #pragma unroll
         for (int n = 0; n < CPT; n += 8) {
           uint32_t pk[4];
 #pragma unroll
           for (int e = 0; e < 8; e += 2) {
-            const float p0 = ex2(x[n + e]), p1 = ex2(x[n + e + 1]);
-            l_part[n + e] += p0;
-            l_part[n + e + 1] += p1;
-            pk[e / 2] = pack_bf16x2(p0, p1);
+            pk[e / 2] = pack_bf16x2(ex2(x[n + e]), ex2(x[n + e + 1]));
+            l_part[n + e] += bf16lo(pk[e / 2]);
+            l_part[n + e + 1] += bf16hi(pk[e / 2]);
           }
           const int col = col0 + n;
           uint32_t off = (uint32_t)((col / W) * PLBO + pos * PRB + (col % W) * 2);
@@ -498,15 +518,15 @@ __global__ void __launch_bounds__(bif::kThreads, 1)
         float v = l_part[n];
 #pragma unroll
         for (int off = 16; off >= 1; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-        if (lane == (n & 31)) sm_l[quad * 128 + col0 + n] = v;
+        if (lane == (n & 31)) sm_l[quad * N + col0 + n] = v;
       }
       const int nrows = s.dec ? P.p : N;
-      tc::mbar_wait(tc::smem_u32(o_full), sg & 1);
+      tc::mbar_wait(tc::smem_u32(&o_full[ob]), (sg >> 1) & 1);
       tc::tc_fence_after();
 #pragma unroll
       for (int n = 0; n < CPT; n += 8) {
         uint32_t orr[8];
-        tc::tmem_ld<8>(tO + col0 + n + lane_addr, orr);
+        tc::tmem_ld<8>(tOb + col0 + n + lane_addr, orr);
         tc::tmem_ld_wait();
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
@@ -523,9 +543,9 @@ __global__ void __launch_bounds__(bif::kThreads, 1)
       }
       tc::tc_fence_before();
       __syncwarp();
-      if (lane == 0) tc::mbar_arrive(tc::smem_u32(o_empty));
+      if (lane == 0) tc::mbar_arrive(tc::smem_u32(&o_empty[ob]));
       tc::named_bar_sync(2, 256);
-      if (sw < 4) {
+      if (sw < 2) {
         const int col = sw * 32 + lane;
         int gr = -1;
         if (!s.dec) {
@@ -535,45 +555,48 @@ __global__ void __launch_bounds__(bif::kThreads, 1)
           gr = s.i * P.h + s.c * P.p + col;
         }
         if (gr >= 0) {
-          const float L = sm_l[col] + sm_l[128 + col] + sm_l[256 + col] + sm_l[384 + col];
+          const float L = sm_l[col] + sm_l[N + col] + sm_l[2 * N + col] + sm_l[3 * N + col];
           float* ml = P.ws_ml + ((size_t)gr * P.S + s.slot) * 2;
-          ml[0] = sm_mrun[cur * 128 + col];
+          ml[0] = sm_mrun[cur * N + col];
           ml[1] = L;
         }
       }
-      // ---- arrive at the (group, row chunk) counter; the last arrival merges ----
+      // ---- arrive at the (sample, group) counters; the last arrival merges ----
       tc::named_bar_sync(2, 256);
-      const int cnt = s.counter;
-      const int cc = cnt / P.nrc, crc = cnt % P.nrc;
-      if (threadIdx.x == 128) {
-        int expected = ctx_parts(P, cc, crc);
-        const int i0 = crc * N / P.p;
-        const int i1 = min(P.b, (crc + 1) * N / P.p);
-        for (int i = i0; i < i1; ++i) expected += dec_parts(P, i, cc);
-        __threadfence();
-        const unsigned old = atomicAdd(&P.counters[cnt], 1u);
-        const int last = (old == (unsigned)(expected - 1));
-        if (last) {
+      const int i0 = s.dec ? s.i : s.rc * N / P.p;
+      const int i1 = s.dec ? s.i + 1 : min(P.b, (s.rc + 1) * N / P.p);
+      if (sw == 0) {
+        if (lane == 0) sm_last[0] = 0;
+        __syncwarp();
+        for (int i = i0 + lane; i < i1; i += 32) {
+          const int cidx = i * P.g + s.c;
+          const int expected = ctx_parts(P, s.c, (i * P.p) / N) + dec_parts(P, i, s.c);
           __threadfence();
-          P.counters[cnt] = 0u;  // self-reset for the next call
+          const unsigned old = atomicAdd(&P.counters[cidx], 1u);
+          if (old == (unsigned)(expected - 1)) {
+            __threadfence();
+            P.counters[cidx] = 0u;  // self-reset for the next call
+            const int k = atomicAdd(&sm_last[0], 1);
+            sm_last[1 + k] = i;
+          }
         }
-        *sm_flag = last;
       }
       tc::named_bar_sync(2, 256);
-      if (*sm_flag) {
+      const int nlast = sm_last[0];
+      if (nlast > 0) {
         __threadfence();
-        // one warp per row of the chunk: join context + decode partials
-        const int nctx = ctx_parts(P, cc, crc);
-        const int r0 = crc * N, r1 = min(R, (crc + 1) * N);
-        for (int r = r0 + sw; r < r1; r += 8) {
-          const int i = r / P.p;
-          const int gr = i * P.h + cc * P.p + (r % P.p);
-          const int ndec = dec_parts(P, i, cc);
+        // one warp per output row of the finished samples
+        for (int k = sw; k < nlast * P.p; k += 8) {
+          const int i = sm_last[1 + k / P.p];
+          const int jj = k % P.p;
+          const int gr = i * P.h + s.c * P.p + jj;
+          const int nctx = ctx_parts(P, s.c, (i * P.p) / N);
+          const int ndec = dec_parts(P, i, s.c);
           const float* ml = P.ws_ml + (size_t)gr * P.S * 2;
-          const float* ob = P.ws_o + (size_t)gr * P.S * kD;
+          const float* obuf = P.ws_o + (size_t)gr * P.S * kD;
           float M = kNegInf;
-          for (int k = lane; k < nctx + ndec; k += 32) {
-            const int sl = k < nctx ? k : P.Sc + (k - nctx);
+          for (int q = lane; q < nctx + ndec; q += 32) {
+            const int sl = q < nctx ? q : P.Sc + (q - nctx);
             M = fmaxf(M, __ldcg(ml + 2 * sl));
           }
 #pragma unroll
@@ -581,23 +604,24 @@ __global__ void __launch_bounds__(bif::kThreads, 1)
           const float Ms = (M == kNegInf) ? 0.f : M;
           float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
           float Lsum = 0.f;
-          for (int k = 0; k < nctx + ndec; ++k) {
-            const int sl = k < nctx ? k : P.Sc + (k - nctx);
-            const float w = ex2(__ldcg(ml + 2 * sl) - Ms);
-            Lsum = fmaf(w, __ldcg(ml + 2 * sl + 1), Lsum);
-            const float4 o4 = __ldcg(reinterpret_cast<const float4*>(ob + (size_t)sl * kD) + lane);
-            acc.x = fmaf(w, o4.x, acc.x);
-            acc.y = fmaf(w, o4.y, acc.y);
-            acc.z = fmaf(w, o4.z, acc.z);
-            acc.w = fmaf(w, o4.w, acc.w);
+          for (int q = 0; q < nctx + ndec; ++q) {
+            const int sl = q < nctx ? q : P.Sc + (q - nctx);
+            const float wgt = ex2(__ldcg(ml + 2 * sl) - Ms);
+            Lsum = fmaf(wgt, __ldcg(ml + 2 * sl + 1), Lsum);
+            const float4 o4 = __ldcg(reinterpret_cast<const float4*>(obuf + (size_t)sl * kD) + lane);
+            acc.x = fmaf(wgt, o4.x, acc.x);
+            acc.y = fmaf(wgt, o4.y, acc.y);
+            acc.z = fmaf(wgt, o4.z, acc.z);
+            acc.w = fmaf(wgt, o4.w, acc.w);
           }
           const float inv = 1.f / Lsum;
-          uint2 packed = make_uint2(pack_bf16x2(acc.x * inv, acc.y * inv), pack_bf16x2(acc.z * inv, acc.w * inv));
+          const uint2 packed = make_uint2(pack_bf16x2(acc.x * inv, acc.y * inv),
+                                          pack_bf16x2(acc.z * inv, acc.w * inv));
           *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(P.out) + (size_t)gr * kD + lane * 4) = packed;
           if (P.lse && lane == 0) P.lse[gr] = (M + lg2(Lsum)) * kLn2;
         }
       }
-      f = s.next;
+      w = s.next;
     }
   }
   tc::tc_fence_before();

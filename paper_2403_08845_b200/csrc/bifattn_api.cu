@@ -112,8 +112,8 @@ struct Plan {
 // the most (group, row chunk) pairs any plan can use, so a call of any plan
 // leaves them zero for the next one.
 size_t counter_bytes(const ba_problem_t* pr) {
-  const long long chunks = (long long)pr->g * (((long long)pr->b * (pr->h / pr->g) + 15) / 16);
-  return ((size_t)chunks * sizeof(unsigned) + 255) & ~(size_t)255;
+  const long long n = (long long)pr->b * pr->g;  // one per (sample, group)
+  return ((size_t)n * sizeof(unsigned) + 255) & ~(size_t)255;
 }
 
 int pick_rb(int rows) { return rows >= 4 ? 4 : (rows >= 2 ? 2 : 1); }
@@ -168,21 +168,22 @@ int make_plan(const ba_problem_t* pr, int sms, bool replicated, Plan* pl) {
     P.tc_Tc = (long long)g * P.tc_nrc * P.tc_ntile_c;
     P.tc_T = P.tc_Tc + (long long)b * g * P.tc_ntile_d;
     P.tc_G = (int)(P.tc_T < sms ? P.tc_T : sms);
+    const long long Td = P.tc_T - P.tc_Tc;
     const int avail = 227 * 1024 - ba::bif::smem_fixed(tcN);
     P.tc_nst = avail / ba::bif::kStageBytes;
     if (P.tc_nst > 4) P.tc_nst = 4;
     P.tc_smem = P.tc_nst * ba::bif::kStageBytes + ba::bif::smem_fixed(tcN);
     // slots: the most CTAs one context (c, rc) / decode (i, c) sequence is split over
-    auto parts = [&](long long ff, long long n) {
-      return ba::bif::owner(ff + n - 1, P.tc_T, P.tc_G) - ba::bif::owner(ff, P.tc_T, P.tc_G) + 1;
+    auto parts = [&](long long ff, long long n, long long T) {
+      return ba::bif::owner(ff + n - 1, T, P.tc_G) - ba::bif::owner(ff, T, P.tc_G) + 1;
     };
     int sc = 0, sd = 0;
     for (long long seg = 0; P.tc_ntile_c && seg < (long long)g * P.tc_nrc; ++seg) {
-      const int n = parts(seg * P.tc_ntile_c, P.tc_ntile_c);
+      const int n = parts(seg * P.tc_ntile_c, P.tc_ntile_c, P.tc_Tc);
       if (n > sc) sc = n;
     }
     for (long long seg = 0; P.tc_ntile_d && seg < (long long)b * g; ++seg) {
-      const int n = parts(P.tc_Tc + seg * P.tc_ntile_d, P.tc_ntile_d);
+      const int n = parts(seg * P.tc_ntile_d, P.tc_ntile_d, Td);
       if (n > sd) sd = n;
     }
     P.tc_Sc = sc;
@@ -346,7 +347,7 @@ int run_tc(const ba_problem_t* pr, const Plan& P, const void* q, const void* Kc,
   bp.b = pr->b; bp.h = pr->h; bp.g = pr->g; bp.p = p; bp.mc = pr->mc;
   bp.dec_cap = P.dec_cap; bp.lens_offset = P.lens_offset;
   bp.nrc = P.tc_nrc; bp.ntile_c = P.tc_ntile_c; bp.ntile_d = P.tc_ntile_d;
-  bp.Tc = P.tc_Tc; bp.T = P.tc_T; bp.G = P.tc_G; bp.nst = P.tc_nst;
+  bp.Tc = P.tc_Tc; bp.Td = P.tc_T - P.tc_Tc; bp.G = P.tc_G; bp.nst = P.tc_nst;
   bp.scale_log2 = scale_log2;
   bp.S = P.S; bp.Sc = P.tc_Sc;
   bp.ws_o = reinterpret_cast<float*>(static_cast<char*>(ws) + P.off_o);
