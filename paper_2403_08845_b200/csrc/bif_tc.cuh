@@ -88,6 +88,12 @@ __host__ __device__ constexpr int smem_fixed(int N) { return 4 * 256 * N + 40 * 
 __host__ __device__ inline int owner(long long f, long long T, int G) {
   return (int)(((f + 1) * (long long)G - 1) / T);
 }
+// Rank, among the distinct CTAs covering tiles [a, ...], of the CTA whose part
+// starts at tile f (f = a or a CTA range start).  With T >= G every CTA range
+// is non-empty; with T < G each CTA gets at most one tile.
+__host__ __device__ inline int part_rank(long long a, long long f, long long T, int G) {
+  return T >= G ? owner(f, T, G) - owner(a, T, G) : (int)(f - a);
+}
 
 struct Seg {
   bool dec;        // decode segment?
@@ -136,7 +142,7 @@ BA_DEVINL Seg seg_at(const BifTcParams& P, const Range& rg, long long w) {
     s.t0 = (int)(f - seg * P.ntile_c);
     s.ntiles = (int)(fend - f);
     s.L = P.mc;
-    s.slot = (int)blockIdx.x - owner(seg * P.ntile_c, P.Tc, P.G);
+    s.slot = part_rank(seg * P.ntile_c, f, P.Tc, P.G);
     s.next = w + (fend - f);
   } else {
     const long long f = rg.fd0 + (w - nc);
@@ -150,7 +156,7 @@ BA_DEVINL Seg seg_at(const BifTcParams& P, const Range& rg, long long w) {
     s.t0 = (int)(f - base);
     s.ntiles = (int)(fend - f);
     s.L = dec_len(P, s.i);
-    s.slot = P.Sc + (int)blockIdx.x - owner(base, P.Td, P.G);
+    s.slot = P.Sc + part_rank(base, f, P.Td, P.G);
     s.next = w + (fend - f);
   }
   return s;
@@ -161,12 +167,12 @@ BA_DEVINL Seg seg_at(const BifTcParams& P, const Range& rg, long long w) {
 BA_DEVINL int ctx_parts(const BifTcParams& P, int c, int rc) {
   if (P.Tc == 0) return 0;
   const long long ff = ((long long)c * P.nrc + rc) * P.ntile_c;
-  return owner(ff + P.ntile_c - 1, P.Tc, P.G) - owner(ff, P.Tc, P.G) + 1;
+  return part_rank(ff, ff + P.ntile_c - 1, P.Tc, P.G) + 1;
 }
 BA_DEVINL int dec_parts(const BifTcParams& P, int i, int c) {
   if (P.Td == 0) return 0;
   const long long ff = ((long long)i * P.g + c) * P.ntile_d;
-  return owner(ff + P.ntile_d - 1, P.Td, P.G) - owner(ff, P.Td, P.G) + 1;
+  return part_rank(ff, ff + P.ntile_d - 1, P.Td, P.G) + 1;
 }
 }  // namespace bif
 

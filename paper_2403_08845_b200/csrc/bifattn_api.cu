@@ -175,7 +175,7 @@ int make_plan(const ba_problem_t* pr, int sms, bool replicated, Plan* pl) {
     P.tc_smem = P.tc_nst * ba::bif::kStageBytes + ba::bif::smem_fixed(tcN);
     // slots: the most CTAs one context (c, rc) / decode (i, c) sequence is split over
     auto parts = [&](long long ff, long long n, long long T) {
-      return ba::bif::owner(ff + n - 1, T, P.tc_G) - ba::bif::owner(ff, T, P.tc_G) + 1;
+      return ba::bif::part_rank(ff, ff + n - 1, T, P.tc_G) + 1;
     };
     int sc = 0, sd = 0;
     for (long long seg = 0; P.tc_ntile_c && seg < (long long)g * P.tc_nrc; ++seg) {
