@@ -5,11 +5,13 @@
 //   context segments:  the R = b*p query rows of group c that share Kc[c] and
 //                      Vc[c] (no batch axis) against a run
 //                      of 128-position context tiles;
-//   decode segments:   the p query rows of sample i, group c against a run of
-//                      128-position tiles of that sample's own Kd[i][c]/Vd[i][c]
-//                      (PAPER.md:255, :267), masked at lens[i];
-//   merge:             the last partial to arrive for (sample i, group c) joins
-//                      that row set's partials with one log-sum-exp — the
+//   decode segments:   the same row chunk against the 128-position tiles of its
+//                      samples' own Kd[i][c]/Vd[i][c],
+//                      sample after sample; a tile of sample i only feeds the
+//                      p columns of sample i (others masked), positions masked
+//                      at lens[i];
+//   merge:             the last partial to arrive for a (group, row chunk)
+//                      joins its rows' partials with one log-sum-exp — the
 //                      single softmax over S_c ⊕ S_d split
 //                      at mc and summed (Eq. 4) — and writes out / lse.
 // Each context tile is read from HBM once for all b samples.
@@ -26,20 +28,20 @@
 // columns [half*CPT, half*CPT+CPT), half = (w-4)/4, CPT = N/2.
 //
 // Online softmax with a stale-max fast path: P = 2^(s*scale*log2e - m_run);
-// only when some logit exceeds m_run by more than kTh (CTA-wide vote,
-// bar.red.or) — and always on a segment's first tile — do the warps compute
-// the exact tile max, rescale l and O^T (TMEM) and raise m_run.  Same softmax;
-// values stay <= 2^kTh.
+// only when a valid logit exceeds m_run by more than kTh, or a column sees its
+// first valid logit (m_run unset), do the warps (CTA-wide vote, bar.red.or)
+// compute the exact tile max per column and raise m_run — rescaling l and
+// O^T (TMEM) only for columns whose max actually grew.  Same softmax; values
+// stay <= 2^kTh.
 //
 // Work split: context tiles fc = (c*nrc + rc)*ntile_c + t in [0, Tc) and
-// decode tiles fd = (i*g + c)*ntile_d + t in [0, Td).  CTA k of G takes
+// decode tiles fd = (c*b + i)*ntile_d + t in [0, Td).  CTA k of G takes
 // context tiles [k*Tc/G, (k+1)*Tc/G) and then decode tiles [k*Td/G,
 // (k+1)*Td/G): every CTA streams the same number of 64 KB tiles (+-1 of each
-// kind), and all context partials land before the decode ones, so the last
-// arrival of a (sample, group) is usually its own decode segment.  A maximal
-// run of one (c, rc) or (i, c) is a segment and writes one partial (m, l, o)
-// per row to its workspace slot.  q and O^T are double buffered across
-// segments so a segment boundary costs no pipeline drain.
+// kind).  A maximal run of tiles of one (c, rc) — context, or decode tiles of
+// the chunk's samples — is a segment and writes one partial (m, l, o) for
+// every row of the chunk to its workspace slot.  q and O^T are double
+// buffered across segments so a segment boundary costs no pipeline drain.
 #pragma once
 #include "common.cuh"
 #include "tc_ptx.cuh"
@@ -50,18 +52,18 @@ struct BifTcParams {
   CUtensorMap tmKc, tmVc;  // Kc/Vc as 3D (d, mc, g), box (64, 128, 1), SW128
   CUtensorMap tmQc;        // q as 3D (d, h, b), box (64, p, N/p), SW128
   CUtensorMap tmKd, tmVd;  // Kd/Vd as 3D (d, dec_stride, b*g), box (64, 128, 1)
-  CUtensorMap tmQd;        // q as 3D (d, h, b), box (64, p, 1)
   const int32_t* lens;
   int b, h, g, p, mc;
   int dec_cap, lens_offset;  // decode length = lens_offset + clamp(lens[i], 0, dec_cap)
   int nrc, ntile_c, ntile_d;
+  int spc;                   // samples per row chunk = N / p
   long long Tc, Td;          // context tiles, decode tiles
   int G, nst;
   float scale_log2;
   int S, Sc;                 // slots per row; decode slots start at Sc
   float* ws_o;               // [b*h][S][128]
   float* ws_ml;              // [b*h][S][2]
-  unsigned* counters;        // [b*g] arrivals per (sample, group); self-resetting
+  unsigned* counters;        // [g*nrc] arrivals per (group, row chunk); self-resetting
   void* out;                 // [b][h][128] bf16
   float* lse;                // [b][h] or null
 };
@@ -97,11 +99,11 @@ __host__ __device__ inline int part_rank(long long a, long long f, long long T, 
 
 struct Seg {
   bool dec;        // decode segment?
-  int c, rc, i;    // group, row chunk (context), sample (decode)
-  int t0, ntiles;  // first tile, tiles in this CTA's part of the segment
-  int L;           // valid positions of the whole sequence
+  int c, rc;       // group, row chunk
+  long long f;     // first flat tile (context or decode space) of this part
+  int ntiles;      // tiles in this CTA's part of the segment
   int slot;        // workspace slot of this CTA's partial
-  long long next;  // flat index (CTA work order) after this segment part
+  long long next;  // work index (CTA work order) after this segment part
 };
 
 BA_DEVINL int dec_len(const BifTcParams& P, int i) {
@@ -110,9 +112,8 @@ BA_DEVINL int dec_len(const BifTcParams& P, int i) {
   return P.lens_offset + L;
 }
 
-// This CTA's work is the concatenation [context range | decode range]; the
-// "work index" w runs over it: w < nc -> context tile fc0 + w, else decode
-// tile fd0 + (w - nc).
+// This CTA's work is the concatenation [context range | decode range]; work
+// index w < nc is context tile fc0 + w, else decode tile fd0 + (w - nc).
 struct Range {
   long long fc0, fc1, fd0, fd1;
   BA_DEVINL long long n() const { return (fc1 - fc0) + (fd1 - fd0); }
@@ -127,7 +128,15 @@ BA_DEVINL Range my_range(const BifTcParams& P) {
   return r;
 }
 
-template <int N>
+// First / one-past-last decode tile of chunk (c, rc).
+BA_DEVINL long long dec_chunk_begin(const BifTcParams& P, int c, int rc) {
+  return ((long long)c * P.b + (long long)rc * P.spc) * P.ntile_d;
+}
+BA_DEVINL long long dec_chunk_end(const BifTcParams& P, int c, int rc) {
+  const long long i1 = min((long long)P.b, (long long)(rc + 1) * P.spc);
+  return ((long long)c * P.b + i1) * P.ntile_d;
+}
+
 BA_DEVINL Seg seg_at(const BifTcParams& P, const Range& rg, long long w) {
   Seg s;
   const long long nc = rg.fc1 - rg.fc0;
@@ -138,41 +147,36 @@ BA_DEVINL Seg seg_at(const BifTcParams& P, const Range& rg, long long w) {
     s.dec = false;
     s.c = (int)(seg / P.nrc);
     s.rc = (int)(seg % P.nrc);
-    s.i = 0;
-    s.t0 = (int)(f - seg * P.ntile_c);
+    s.f = f;
     s.ntiles = (int)(fend - f);
-    s.L = P.mc;
     s.slot = part_rank(seg * P.ntile_c, f, P.Tc, P.G);
     s.next = w + (fend - f);
   } else {
     const long long f = rg.fd0 + (w - nc);
-    const long long seg = f / P.ntile_d;  // i*g + c
-    const long long base = seg * P.ntile_d;
-    const long long fend = min(base + P.ntile_d, rg.fd1);
+    const long long cb = f / P.ntile_d;  // c*b + i
     s.dec = true;
-    s.i = (int)(seg / P.g);
-    s.c = (int)(seg % P.g);
-    s.rc = (s.i * P.p) / N;
-    s.t0 = (int)(f - base);
+    s.c = (int)(cb / P.b);
+    s.rc = (int)((cb % P.b) / P.spc);
+    const long long a = dec_chunk_begin(P, s.c, s.rc);
+    const long long fend = min(dec_chunk_end(P, s.c, s.rc), rg.fd1);
+    s.f = f;
     s.ntiles = (int)(fend - f);
-    s.L = dec_len(P, s.i);
-    s.slot = P.Sc + part_rank(base, f, P.Td, P.G);
+    s.slot = P.Sc + part_rank(a, f, P.Td, P.G);
     s.next = w + (fend - f);
   }
   return s;
 }
 
-// Partials written for the rows of (sample i, group c): context segments of
-// its row chunk + decode segments of (i, c).
+// Partials written for the rows of chunk (c, rc).
 BA_DEVINL int ctx_parts(const BifTcParams& P, int c, int rc) {
   if (P.Tc == 0) return 0;
   const long long ff = ((long long)c * P.nrc + rc) * P.ntile_c;
   return part_rank(ff, ff + P.ntile_c - 1, P.Tc, P.G) + 1;
 }
-BA_DEVINL int dec_parts(const BifTcParams& P, int i, int c) {
+BA_DEVINL int dec_parts(const BifTcParams& P, int c, int rc) {
   if (P.Td == 0) return 0;
-  const long long ff = ((long long)i * P.g + c) * P.ntile_d;
-  return part_rank(ff, ff + P.ntile_d - 1, P.Td, P.G) + 1;
+  const long long a = dec_chunk_begin(P, c, rc), e = dec_chunk_end(P, c, rc);
+  return part_rank(a, e - 1, P.Td, P.G) + 1;
 }
 }  // namespace bif
 
@@ -234,9 +238,7 @@ __global__ void __launch_bounds__(bif::kThreads, 1)
   uint64_t* o_full = bars + 28;    // [2]
   uint64_t* o_empty = bars + 30;   // [2]
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 32);
-  // merge list (count + samples, <= N/p + 1 ints) reuses the slow-path scratch:
-  // the epilogue never overlaps a slow path of the same CTA
-  int* sm_last = reinterpret_cast<int*>(sm_red);
+  int* sm_flag = reinterpret_cast<int*>(bars + 33);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -263,17 +265,10 @@ __global__ void __launch_bounds__(bif::kThreads, 1)
     tc::prefetch_tmap(&P.tmQc);
     tc::prefetch_tmap(&P.tmKd);
     tc::prefetch_tmap(&P.tmVd);
-    tc::prefetch_tmap(&P.tmQd);
   }
   if (warp == 2) {
     tc::tmem_alloc(tc::smem_u32(tmem_holder), TMEM_COLS);
     tc::tmem_relinquish();
-  }
-  if (warp >= 4) {
-    // q rows beyond a decode segment's p stay finite (zero) until overwritten
-    for (int k = threadIdx.x - 128; k < 2 * QB / 16; k += 256)
-      reinterpret_cast<uint4*>(sm_q)[k] = make_uint4(0, 0, 0, 0);
-    tc::fence_proxy_async_smem();
   }
   tc::tc_fence_before();
   __syncthreads();
@@ -292,26 +287,27 @@ __global__ void __launch_bounds__(bif::kThreads, 1)
       const uint64_t pol_c = P.nrc == 1 ? tc::policy_evict_first() : tc::policy_evict_last();
       const uint64_t pol_d = tc::policy_evict_first();
       for (long long w = 0; w < nw; ++sg) {
-        const Seg s = seg_at<N>(P, rg, w);
+        const Seg s = seg_at(P, rg, w);
         const uint32_t qbuf = sg & 1;
         tc::mbar_wait(tc::smem_u32(&q_empty[qbuf]), ((sg >> 1) & 1) ^ 1);
         const uint32_t qb = tc::smem_u32(&q_full[qbuf]);
         const uint32_t qdst = tc::smem_u32(sm_q + qbuf * QB);
-        if (!s.dec) {
-          tc::mbar_arrive_expect_tx(qb, 2 * N * 128);
-          tc::tma_load_3d(qdst, &P.tmQc, qb, 0, s.c * P.p, s.rc * (N / P.p));
-          tc::tma_load_3d(qdst + N * 128, &P.tmQc, qb, 64, s.c * P.p, s.rc * (N / P.p));
-        } else {
-          tc::mbar_arrive_expect_tx(qb, 2 * P.p * 128);
-          tc::tma_load_3d(qdst, &P.tmQd, qb, 0, s.c * P.p, s.i);
-          tc::tma_load_3d(qdst + N * 128, &P.tmQd, qb, 64, s.c * P.p, s.i);
-        }
-        const CUtensorMap* mk = s.dec ? &P.tmKd : &P.tmKc;
-        const CUtensorMap* mv = s.dec ? &P.tmVd : &P.tmVc;
-        const int z = s.dec ? s.i * P.g + s.c : s.c;
-        const uint64_t pol = s.dec ? pol_d : pol_c;
+        tc::mbar_arrive_expect_tx(qb, 2 * N * 128);
+        tc::tma_load_3d(qdst, &P.tmQc, qb, 0, s.c * P.p, s.rc * P.spc);
+        tc::tma_load_3d(qdst + N * 128, &P.tmQc, qb, 64, s.c * P.p, s.rc * P.spc);
         for (int j = 0; j < s.ntiles; ++j, ++tt) {
-          const int t = s.t0 + j;
+          const long long f = s.f + j;
+          int t, z;
+          if (!s.dec) {
+            t = (int)(f % P.ntile_c);
+            z = s.c;
+          } else {
+            t = (int)(f % P.ntile_d);
+            z = (int)((f / P.ntile_d) % P.b) * P.g + s.c;  // i*g + c
+          }
+          const CUtensorMap* mk = s.dec ? &P.tmKd : &P.tmKc;
+          const CUtensorMap* mv = s.dec ? &P.tmVd : &P.tmVc;
+          const uint64_t pol = s.dec ? pol_d : pol_c;
           const int st = tt % NST;
           tc::mbar_wait(tc::smem_u32(&kv_empty[st]), ((tt / NST) & 1) ^ 1);
           const uint32_t bar = tc::smem_u32(&kv_full[st]);
@@ -343,7 +339,7 @@ __global__ void __launch_bounds__(bif::kThreads, 1)
         if (wq < nw && u_qk - u_pv < 2) {
           if (!q_ready && mbar_test(tc::smem_u32(&q_full[sg_qk & 1]), (sg_qk >> 1) & 1)) {
             q_ready = true;
-            seg_end_q = seg_at<N>(P, rg, wq).next;
+            seg_end_q = seg_at(P, rg, wq).next;
           }
           if (q_ready) {
             const uint32_t st = tt_qk % NST;
@@ -377,7 +373,7 @@ __global__ void __launch_bounds__(bif::kThreads, 1)
         if (u_pv < u_qk) {
           const uint32_t slot = u_pv & 1;
           if (wp == seg_end_p) {
-            seg_end_p = seg_at<N>(P, rg, wp).next;
+            seg_end_p = seg_at(P, rg, wp).next;
             pv_first = true;
           }
           const uint32_t ob = sg_pv & 1;
@@ -421,16 +417,35 @@ __global__ void __launch_bounds__(bif::kThreads, 1)
     const int R = P.b * P.p;
     uint32_t u = 0, sg = 0, cur = 0;
     for (long long w = 0; w < nw; ++sg) {
-      const Seg s = seg_at<N>(P, rg, w);
+      const Seg s = seg_at(P, rg, w);
       const uint32_t ob = sg & 1;
       const uint32_t tOb = tO + ob * N;
       float l_part[CPT];
 #pragma unroll
       for (int n = 0; n < CPT; ++n) l_part[n] = 0.f;
+      // running max of every column starts unset (-inf)
+      if (quad == 0 && lane == 0) {
+#pragma unroll
+        for (int n = 0; n < CPT; ++n) sm_mrun[cur * N + col0 + n] = kNegInf;
+      }
+      tc::named_bar_sync(2, 256);
       for (int j = 0; j < s.ntiles; ++j, ++u) {
-        const int t = s.t0 + j;
+        const long long f = s.f + j;
+        // valid columns [cv0, cv1) and positions [0, L) of this tile
+        int t, L, cv0, cv1;
+        if (!s.dec) {
+          t = (int)(f % P.ntile_c);
+          L = P.mc;
+          cv0 = 0;
+          cv1 = N;
+        } else {
+          t = (int)(f % P.ntile_d);
+          const int i = (int)((f / P.ntile_d) % P.b);
+          L = dec_len(P, i);
+          cv0 = i * P.p - s.rc * N;
+          cv1 = cv0 + P.p;
+        }
         const uint32_t slot = u & 1;
-        const bool first = (j == 0);
         const float* mrun = sm_mrun + cur * N + col0;
         tc::mbar_wait(tc::smem_u32(&s_full[slot]), (u >> 1) & 1);
         tc::tc_fence_after();
@@ -440,16 +455,19 @@ __global__ void __launch_bounds__(bif::kThreads, 1)
         tc::tc_fence_before();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(tc::smem_u32(&s_free[slot]));
-        const bool valid = t * kBM + pos < s.L;
-        float excess = kNegInf;
+        const bool vpos = t * kBM + pos < L;
+        bool need = false;
 #pragma unroll
         for (int n = 0; n < CPT; ++n) {
-          const float mref = first ? 0.f : mrun[n];
-          x[n] = valid ? fmaf(x[n], sl2, -mref) : kNegInf;
-          excess = fmaxf(excess, x[n]);
+          const int col = col0 + n;
+          const bool vc = vpos && col >= cv0 && col < cv1;
+          const float mo = mrun[n];
+          const float mref = (mo == kNegInf) ? 0.f : mo;
+          x[n] = vc ? fmaf(x[n], sl2, -mref) : kNegInf;
+          need |= vc && (mo == kNegInf || x[n] > kTh);
         }
-        if (tc::named_bar_or(1, 256, first || excess > kTh)) {
-          // ---- slow path: exact column max over the tile, new m_run, rescale ----
+        if (tc::named_bar_or(1, 256, need)) {
+          // ---- slow path: exact column max over the tile, new m_run ----
 #pragma unroll
           for (int n = 0; n < CPT; ++n) {
             float v = x[n];
@@ -459,21 +477,24 @@ __global__ void __launch_bounds__(bif::kThreads, 1)
           }
           tc::named_bar_sync(2, 256);
           float* mnext = sm_mrun + (cur ^ 1) * N + col0;
+          bool grew = false;
 #pragma unroll
           for (int n = 0; n < CPT; ++n) {
             const int col = col0 + n;
-            const float mref = first ? 0.f : mrun[n];
+            const float mo = mrun[n];
+            const float mref = (mo == kNegInf) ? 0.f : mo;
             const float cm = fmaxf(fmaxf(sm_red[col], sm_red[N + col]),
                                    fmaxf(sm_red[2 * N + col], sm_red[3 * N + col]));
-            const float tmax = mref + cm;  // -inf if the whole column is masked
-            const float mold = first ? kNegInf : mrun[n];
-            const float mnew = fmaxf(mold, tmax);
-            const float alpha = first ? 0.f : (mnew == kNegInf ? 1.f : ex2(mold - mnew));
+            const float mnew = fmaxf(mo, mref + cm);  // unchanged if the column had no valid logit
+            // l, O of a column are exactly 0 while its max is unset
+            const float alpha = (mo == kNegInf) ? 0.f : ex2(mo - mnew);
             l_part[n] *= alpha;
             x[n] = (mnew == kNegInf) ? kNegInf : x[n] + (mref - mnew);
+            grew |= (mo != kNegInf) && (mnew > mo);
             if (quad == 0 && lane == 0) mnext[n] = mnew;
           }
-          if (!first) {
+          if (tc::named_bar_or(1, 256, grew)) {
+            // O^T holds earlier tiles of this segment: wait for PV(u-1), rescale
             const uint32_t pv = u - 1;
             tc::mbar_wait(tc::smem_u32(&p_empty[pv & 1]), (pv >> 1) & 1);
             tc::tc_fence_after();
@@ -485,7 +506,7 @@ __global__ void __launch_bounds__(bif::kThreads, 1)
 #pragma unroll
               for (int e = 0; e < 8; ++e) {
                 const float mo = mrun[n + e], mn = mnext[n + e];
-                const float a = (mn == kNegInf) ? 1.f : ex2(mo - mn);
+                const float a = (mo == kNegInf) ? 0.f : ex2(mo - mn);
                 orr[e] = __float_as_uint(__uint_as_float(orr[e]) * a);
               }
               tc::tmem_st<8>(tOb + col0 + n + lane_addr, orr);
@@ -526,7 +547,6 @@ __global__ void __launch_bounds__(bif::kThreads, 1)
         for (int off = 16; off >= 1; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
         if (lane == (n & 31)) sm_l[quad * N + col0 + n] = v;
       }
-      const int nrows = s.dec ? P.p : N;
       tc::mbar_wait(tc::smem_u32(&o_full[ob]), (sg >> 1) & 1);
       tc::tc_fence_after();
 #pragma unroll
@@ -536,15 +556,11 @@ __global__ void __launch_bounds__(bif::kThreads, 1)
         tc::tmem_ld_wait();
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
-          const int col = col0 + n + e;
-          int gr = -1;
-          if (!s.dec) {
-            const int r = s.rc * N + col;
-            if (r < R) gr = (r / P.p) * P.h + s.c * P.p + (r % P.p);
-          } else if (col < nrows) {
-            gr = s.i * P.h + s.c * P.p + col;
+          const int r = s.rc * N + col0 + n + e;
+          if (r < R) {
+            const int gr = (r / P.p) * P.h + s.c * P.p + (r % P.p);
+            P.ws_o[((size_t)gr * P.S + s.slot) * kD + pos] = __uint_as_float(orr[e]);
           }
-          if (gr >= 0) P.ws_o[((size_t)gr * P.S + s.slot) * kD + pos] = __uint_as_float(orr[e]);
         }
       }
       tc::tc_fence_before();
@@ -553,51 +569,35 @@ __global__ void __launch_bounds__(bif::kThreads, 1)
       tc::named_bar_sync(2, 256);
       if (sw < 2) {
         const int col = sw * 32 + lane;
-        int gr = -1;
-        if (!s.dec) {
-          const int r = s.rc * N + col;
-          if (col < N && r < R) gr = (r / P.p) * P.h + s.c * P.p + (r % P.p);
-        } else if (col < nrows) {
-          gr = s.i * P.h + s.c * P.p + col;
-        }
-        if (gr >= 0) {
-          const float L = sm_l[col] + sm_l[N + col] + sm_l[2 * N + col] + sm_l[3 * N + col];
+        const int r = s.rc * N + col;
+        if (col < N && r < R) {
+          const int gr = (r / P.p) * P.h + s.c * P.p + (r % P.p);
+          const float Lr = sm_l[col] + sm_l[N + col] + sm_l[2 * N + col] + sm_l[3 * N + col];
           float* ml = P.ws_ml + ((size_t)gr * P.S + s.slot) * 2;
           ml[0] = sm_mrun[cur * N + col];
-          ml[1] = L;
+          ml[1] = Lr;
         }
       }
-      // ---- arrive at the (sample, group) counters; the last arrival merges ----
+      // ---- arrive at the (group, row chunk) counter; the last arrival merges ----
       tc::named_bar_sync(2, 256);
-      const int i0 = s.dec ? s.i : s.rc * N / P.p;
-      const int i1 = s.dec ? s.i + 1 : min(P.b, (s.rc + 1) * N / P.p);
-      if (sw == 0) {
-        if (lane == 0) sm_last[0] = 0;
-        __syncwarp();
-        for (int i = i0 + lane; i < i1; i += 32) {
-          const int cidx = i * P.g + s.c;
-          const int expected = ctx_parts(P, s.c, (i * P.p) / N) + dec_parts(P, i, s.c);
-          __threadfence();
-          const unsigned old = atomicAdd(&P.counters[cidx], 1u);
-          if (old == (unsigned)(expected - 1)) {
-            __threadfence();
-            P.counters[cidx] = 0u;  // self-reset for the next call
-            const int k = atomicAdd(&sm_last[0], 1);
-            sm_last[1 + k] = i;
-          }
-        }
-      }
-      tc::named_bar_sync(2, 256);
-      const int nlast = sm_last[0];
-      if (nlast > 0) {
+      const int cidx = s.c * P.nrc + s.rc;
+      const int nctx = ctx_parts(P, s.c, s.rc), ndec = dec_parts(P, s.c, s.rc);
+      if (threadIdx.x == 128) {
         __threadfence();
-        // one warp per output row of the finished samples
-        for (int k = sw; k < nlast * P.p; k += 8) {
-          const int i = sm_last[1 + k / P.p];
-          const int jj = k % P.p;
-          const int gr = i * P.h + s.c * P.p + jj;
-          const int nctx = ctx_parts(P, s.c, (i * P.p) / N);
-          const int ndec = dec_parts(P, i, s.c);
+        const unsigned old = atomicAdd(&P.counters[cidx], 1u);
+        const int last = old == (unsigned)(nctx + ndec - 1);
+        if (last) {
+          __threadfence();
+          P.counters[cidx] = 0u;  // self-reset for the next call
+        }
+        *sm_flag = last;
+      }
+      tc::named_bar_sync(2, 256);
+      if (*sm_flag) {
+        __threadfence();
+        const int r0 = s.rc * N, r1 = min(R, (s.rc + 1) * N);
+        for (int r = r0 + sw; r < r1; r += 8) {
+          const int gr = (r / P.p) * P.h + s.c * P.p + (r % P.p);
           const float* ml = P.ws_ml + (size_t)gr * P.S * 2;
           const float* obuf = P.ws_o + (size_t)gr * P.S * kD;
           float M = kNegInf;
@@ -610,10 +610,12 @@ __global__ void __launch_bounds__(bif::kThreads, 1)
           const float Ms = (M == kNegInf) ? 0.f : M;
           float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
           float Lsum = 0.f;
+#pragma unroll 4
           for (int q = 0; q < nctx + ndec; ++q) {
             const int sl = q < nctx ? q : P.Sc + (q - nctx);
-            const float wgt = ex2(__ldcg(ml + 2 * sl) - Ms);
-            Lsum = fmaf(wgt, __ldcg(ml + 2 * sl + 1), Lsum);
+            const float2 mlq = __ldcg(reinterpret_cast<const float2*>(ml) + sl);
+            const float wgt = ex2(mlq.x - Ms);
+            Lsum = fmaf(wgt, mlq.y, Lsum);
             const float4 o4 = __ldcg(reinterpret_cast<const float4*>(obuf + (size_t)sl * kD) + lane);
             acc.x = fmaf(wgt, o4.x, acc.x);
             acc.y = fmaf(wgt, o4.y, acc.y);

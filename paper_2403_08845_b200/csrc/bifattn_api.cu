@@ -10,6 +10,7 @@
 //   FMA (fp32, other d, few rows): context FMA kernel + decode FMA kernel
 //       (fma_partial.cuh) + merge kernel (merge.cuh): three launches.
 // The replicated-KV baseline runs the same kernels with no context branch.
+#include <algorithm>
 #include <mutex>
 #include <cstdio>
 #include <cstring>
@@ -112,7 +113,8 @@ struct Plan {
 // the most (group, row chunk) pairs any plan can use, so a call of any plan
 // leaves them zero for the next one.
 size_t counter_bytes(const ba_problem_t* pr) {
-  const long long n = (long long)pr->b * pr->g;  // one per (sample, group)
+  // one per (group, row chunk); row chunks are >= 16 rows (or >= p rows)
+  const long long n = (long long)pr->g * (((long long)pr->b * (pr->h / pr->g) + 15) / 16 + 1);
   return ((size_t)n * sizeof(unsigned) + 255) & ~(size_t)255;
 }
 
@@ -166,7 +168,7 @@ int make_plan(const ba_problem_t* pr, int sms, bool replicated, Plan* pl) {
     P.tc_ntile_c = replicated ? 0 : cdiv(pr->mc, 128);
     P.tc_ntile_d = cdiv(P.lens_offset + P.dec_cap, 128);
     P.tc_Tc = (long long)g * P.tc_nrc * P.tc_ntile_c;
-    P.tc_T = P.tc_Tc + (long long)b * g * P.tc_ntile_d;
+    P.tc_T = P.tc_Tc + (long long)g * b * P.tc_ntile_d;
     P.tc_G = (int)(P.tc_T < sms ? P.tc_T : sms);
     const long long Td = P.tc_T - P.tc_Tc;
     const int avail = 227 * 1024 - ba::bif::smem_fixed(tcN);
@@ -182,9 +184,14 @@ int make_plan(const ba_problem_t* pr, int sms, bool replicated, Plan* pl) {
       const int n = parts(seg * P.tc_ntile_c, P.tc_ntile_c, P.tc_Tc);
       if (n > sc) sc = n;
     }
-    for (long long seg = 0; P.tc_ntile_d && seg < (long long)b * g; ++seg) {
-      const int n = parts(seg * P.tc_ntile_d, P.tc_ntile_d, Td);
-      if (n > sd) sd = n;
+    const int spc = tcN / p;
+    for (int c = 0; P.tc_ntile_d && c < g; ++c) {
+      for (int rc = 0; rc < P.tc_nrc; ++rc) {
+        const long long a = ((long long)c * b + (long long)rc * spc) * P.tc_ntile_d;
+        const long long e = ((long long)c * b + std::min<long long>(b, (long long)(rc + 1) * spc)) * P.tc_ntile_d;
+        const int n = parts(a, e - a, Td);
+        if (n > sd) sd = n;
+      }
     }
     P.tc_Sc = sc;
     P.tc_Sd = sd;
@@ -340,13 +347,15 @@ int run_tc(const ba_problem_t* pr, const Plan& P, const void* q, const void* Kc,
     const uint64_t bg = (uint64_t)pr->b * pr->g;
     rc = make_tmap_3d(&bp.tmKd, Kd, d, ds, bg, d * 2, ds * d * 2, 128, 1);
     if (!rc) rc = make_tmap_3d(&bp.tmVd, Vd, d, ds, bg, d * 2, ds * d * 2, 128, 1);
-    if (!rc) rc = make_tmap_3d(&bp.tmQd, q, d, pr->h, pr->b, d * 2, (uint64_t)pr->h * d * 2, p, 1);
   }
+  if (!rc && P.tc_Tc == 0)  // replicated baseline: q map for the decode chunks
+    rc = make_tmap_3d(&bp.tmQc, q, d, pr->h, pr->b, d * 2, (uint64_t)pr->h * d * 2, p, P.tc_N / p);
   if (rc) return rc;
   bp.lens = lens;
   bp.b = pr->b; bp.h = pr->h; bp.g = pr->g; bp.p = p; bp.mc = pr->mc;
   bp.dec_cap = P.dec_cap; bp.lens_offset = P.lens_offset;
   bp.nrc = P.tc_nrc; bp.ntile_c = P.tc_ntile_c; bp.ntile_d = P.tc_ntile_d;
+  bp.spc = P.tc_N / p;
   bp.Tc = P.tc_Tc; bp.Td = P.tc_T - P.tc_Tc; bp.G = P.tc_G; bp.nst = P.tc_nst;
   bp.scale_log2 = scale_log2;
   bp.S = P.S; bp.Sc = P.tc_Sc;
