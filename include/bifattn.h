@@ -150,6 +150,13 @@ const char* ba_launch_name(const ba_problem_t* prob, int k);
  * events between launches serialises programmatic-dependent launches. */
 void ba_set_launch_events(void* const* events, int n);
 
+/* Instrumentation: while set, the fused tensor-core kernel launched by THIS
+ * thread writes up to 64 tagged %globaltimer stamps per CTA into dev_buf
+ * (device, uint64 [gridDim][64], zeroed by the caller): tag<<56 | time_ns,
+ * tags 1 start, 2/3 first tile of a context/decode segment, 4 segment end,
+ * 5/6 after the counter arrival (6 = this CTA merged), 7 done.  NULL disables. */
+void ba_set_trace_buffer(void* dev_buf);
+
 /* Message for a BA_* code (static string). */
 const char* ba_strerror(int code);
 

@@ -31,7 +31,8 @@ ERRORS = {0: "BA_OK", -1: "BA_EINVAL", -2: "BA_ENULL", -3: "BA_EALIGN", -4: "BA_
 
 EXPORTED = ["ba_workspace_bytes", "bifurcated_attn_decode", "bifurcated_attn_decode_host",
             "replicated_attn_decode", "ba_launches_per_call", "ba_plan_string", "ba_strerror",
-            "ba_last_cuda_error", "ba_version", "ba_launch_name", "ba_set_launch_events"]
+            "ba_last_cuda_error", "ba_version", "ba_launch_name", "ba_set_launch_events",
+            "ba_set_trace_buffer"]
 
 
 class BAProblem(ctypes.Structure):
@@ -75,6 +76,8 @@ def load_library(path: str = LIB_PATH):
     lib.ba_launch_name.restype = ctypes.c_char_p
     lib.ba_set_launch_events.argtypes = [ctypes.c_void_p, ctypes.c_int]
     lib.ba_set_launch_events.restype = None
+    lib.ba_set_trace_buffer.argtypes = [ctypes.c_void_p]
+    lib.ba_set_trace_buffer.restype = None
     lib.ba_version.argtypes = []
     lib.ba_version.restype = ctypes.c_int
     _lib = lib

@@ -66,6 +66,7 @@ struct BifTcParams {
   unsigned* counters;        // [g*nrc] arrivals per (group, row chunk); self-resetting
   void* out;                 // [b][h][128] bf16
   float* lse;                // [b][h] or null
+  unsigned long long* trace; // optional [G][kTraceSlots] globaltimer stamps (instrumentation)
 };
 
 namespace bif {
@@ -74,6 +75,7 @@ constexpr int kD = 128;
 constexpr int kBM = 128;            // positions per tile (MMA M)
 constexpr int kStageBytes = 65536;  // K tile 32 KB + V tile 32 KB
 constexpr float kTh = 8.0f;         // fast-path slack (log2 units)
+constexpr int kTraceSlots = 64;
 
 __host__ __device__ constexpr int p_atom(int N) { return (N % 64 == 0) ? 64 : ((N % 32 == 0) ? 32 : 16); }
 __host__ __device__ constexpr int p_layout(int N) {
@@ -189,6 +191,12 @@ BA_DEVINL void tmem_ld_cols2(uint32_t taddr, uint32_t* r) {
   for (; c + 16 <= CPT; c += 16) tc::tmem_ld<16>(taddr + c, r + c);
 #pragma unroll
   for (; c + 8 <= CPT; c += 8) tc::tmem_ld<8>(taddr + c, r + c);
+}
+
+BA_DEVINL unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
 }
 
 BA_DEVINL bool mbar_test(uint32_t bar, uint32_t parity) {
@@ -416,6 +424,12 @@ __global__ void __launch_bounds__(bif::kThreads, 1)
     const float sl2 = P.scale_log2;
     const int R = P.b * P.p;
     uint32_t u = 0, sg = 0, cur = 0;
+    unsigned long long* tr = P.trace ? P.trace + (size_t)blockIdx.x * kTraceSlots : nullptr;
+    int ntr = 0;
+    auto stamp = [&](unsigned long long tag) {
+      if (tr && threadIdx.x == 128 && ntr < kTraceSlots) tr[ntr++] = (gtimer() & 0x00ffffffffffffffull) | (tag << 56);
+    };
+    stamp(1);
     for (long long w = 0; w < nw; ++sg) {
       const Seg s = seg_at(P, rg, w);
       const uint32_t ob = sg & 1;
@@ -449,6 +463,7 @@ __global__ void __launch_bounds__(bif::kThreads, 1)
         const float* mrun = sm_mrun + cur * N + col0;
         tc::mbar_wait(tc::smem_u32(&s_full[slot]), (u >> 1) & 1);
         tc::tc_fence_after();
+        if (j == 0) stamp(s.dec ? 3 : 2);
         float x[CPT];
         tmem_ld_cols2<CPT>(tS + slot * N + col0 + lane_addr, reinterpret_cast<uint32_t*>(x));
         tc::tmem_ld_wait();
@@ -540,6 +555,7 @@ __global__ void __launch_bounds__(bif::kThreads, 1)
         if (lane == 0) tc::mbar_arrive(tc::smem_u32(&p_full[slot]));
       }
       // ------------------------- segment epilogue -------------------------
+      stamp(4);
 #pragma unroll
       for (int n = 0; n < CPT; ++n) {
         float v = l_part[n];
@@ -593,6 +609,7 @@ __global__ void __launch_bounds__(bif::kThreads, 1)
         *sm_flag = last;
       }
       tc::named_bar_sync(2, 256);
+      stamp(*sm_flag ? 6 : 5);
       if (*sm_flag) {
         __threadfence();
         const int r0 = s.rc * N, r1 = min(R, (s.rc + 1) * N);
@@ -631,6 +648,7 @@ __global__ void __launch_bounds__(bif::kThreads, 1)
       }
       w = s.next;
     }
+    stamp(7);
   }
   tc::tc_fence_before();
   __syncthreads();

@@ -25,6 +25,7 @@ namespace {
 
 thread_local int g_last_cuda_error = 0;
 thread_local char g_plan_buf[512];
+thread_local void* g_trace = nullptr;
 thread_local void* const* g_events = nullptr;
 thread_local int g_nevents = 0;
 
@@ -364,6 +365,7 @@ int run_tc(const ba_problem_t* pr, const Plan& P, const void* q, const void* Kc,
   bp.counters = reinterpret_cast<unsigned*>(static_cast<char*>(ws) + P.off_cnt);
   bp.out = out;
   bp.lse = lse;
+  bp.trace = static_cast<unsigned long long*>(g_trace);
   LaunchRec rec(st);
   switch (P.tc_N) {
     case 16: return launch_bif_tc_n<16>(bp, P.tc_smem, rec);
@@ -616,6 +618,8 @@ const char* ba_launch_name(const ba_problem_t* prob, int k) {
   }
   return (k >= 0 && k < n) ? names[k] : nullptr;
 }
+
+void ba_set_trace_buffer(void* dev_buf) { g_trace = dev_buf; }
 
 void ba_set_launch_events(void* const* events, int n) {
   g_events = n > 0 ? events : nullptr;
