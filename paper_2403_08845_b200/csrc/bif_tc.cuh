@@ -563,8 +563,10 @@ __global__ void __launch_bounds__(bif::kThreads, 1)
         for (int off = 16; off >= 1; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
         if (lane == (n & 31)) sm_l[quad * N + col0 + n] = v;
       }
+      stamp(8);
       tc::mbar_wait(tc::smem_u32(&o_full[ob]), (sg >> 1) & 1);
       tc::tc_fence_after();
+      stamp(9);
 #pragma unroll
       for (int n = 0; n < CPT; n += 8) {
         uint32_t orr[8];
@@ -583,6 +585,7 @@ __global__ void __launch_bounds__(bif::kThreads, 1)
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(tc::smem_u32(&o_empty[ob]));
       tc::named_bar_sync(2, 256);
+      stamp(10);
       if (sw < 2) {
         const int col = sw * 32 + lane;
         const int r = s.rc * N + col;
@@ -598,6 +601,7 @@ __global__ void __launch_bounds__(bif::kThreads, 1)
       tc::named_bar_sync(2, 256);
       const int cidx = s.c * P.nrc + s.rc;
       const int nctx = ctx_parts(P, s.c, s.rc), ndec = dec_parts(P, s.c, s.rc);
+      stamp(11);
       if (threadIdx.x == 128) {
         __threadfence();
         const unsigned old = atomicAdd(&P.counters[cidx], 1u);
