@@ -102,6 +102,7 @@ __host__ __device__ inline int part_rank(long long a, long long f, long long T, 
 struct Seg {
   bool dec;        // decode segment?
   int c, rc;       // group, row chunk
+  int t0, i0;      // first tile's position-tile index and (decode) sample
   long long f;     // first flat tile (context or decode space) of this part
   int ntiles;      // tiles in this CTA's part of the segment
   int slot;        // workspace slot of this CTA's partial
@@ -149,6 +150,8 @@ BA_DEVINL Seg seg_at(const BifTcParams& P, const Range& rg, long long w) {
     s.dec = false;
     s.c = (int)(seg / P.nrc);
     s.rc = (int)(seg % P.nrc);
+    s.t0 = (int)(f - seg * P.ntile_c);
+    s.i0 = 0;
     s.f = f;
     s.ntiles = (int)(fend - f);
     s.slot = part_rank(seg * P.ntile_c, f, P.Tc, P.G);
@@ -158,7 +161,9 @@ BA_DEVINL Seg seg_at(const BifTcParams& P, const Range& rg, long long w) {
     const long long cb = f / P.ntile_d;  // c*b + i
     s.dec = true;
     s.c = (int)(cb / P.b);
-    s.rc = (int)((cb % P.b) / P.spc);
+    s.i0 = (int)(cb % P.b);
+    s.rc = s.i0 / P.spc;
+    s.t0 = (int)(f - cb * P.ntile_d);
     const long long a = dec_chunk_begin(P, s.c, s.rc);
     const long long fend = min(dec_chunk_end(P, s.c, s.rc), rg.fd1);
     s.f = f;
@@ -210,6 +215,115 @@ BA_DEVINL bool mbar_test(uint32_t bar, uint32_t parity) {
   return ok != 0;
 }
 
+// Butterfly transpose-reduce over the 32 lanes of a warp: v[CPT] per lane
+// (CPT a power of two, 8..32) -> lane l holds in v[0] the max / sum of column
+// (l % CPT) over all 32 lanes.  CPT-1 shuffles + log2(32/CPT)*1 instead of
+// 5*CPT for independent column reductions.
+template <int CPT, bool kMax>
+BA_DEVINL void warp_col_reduce(float* v, int lane) {
+#pragma unroll
+  for (int w = CPT / 2; w >= 1; w >>= 1) {
+    // pair columns k and k+w: lanes with bit w set keep the upper half
+    const bool upper = lane & w;
+#pragma unroll
+    for (int k = 0; k < w; ++k) {
+      const float send = upper ? v[k] : v[k + w];
+      const float keep = upper ? v[k + w] : v[k];
+      const float got = __shfl_xor_sync(0xffffffffu, send, w);
+      v[k] = kMax ? fmaxf(keep, got) : keep + got;
+    }
+  }
+  // v[0] now holds column (lane % CPT) reduced over the lanes that share lane / CPT... finish
+#pragma unroll
+  for (int off = CPT; off < 32; off <<= 1) {
+    const float got = __shfl_xor_sync(0xffffffffu, v[0], off);
+    v[0] = kMax ? fmaxf(v[0], got) : v[0] + got;
+  }
+}
+template <int CPT>
+BA_DEVINL void warp_colmax(float* v, int lane) {
+  if constexpr ((CPT & (CPT - 1)) == 0 && CPT <= 32) {
+    warp_col_reduce<CPT, true>(v, lane);
+  } else {
+    // generic: reduce each column, lane n keeps column n
+    float keep = kNegInf;
+#pragma unroll
+    for (int n = 0; n < CPT; ++n) {
+      float a = v[n];
+#pragma unroll
+      for (int off = 16; off >= 1; off >>= 1) a = fmaxf(a, __shfl_xor_sync(0xffffffffu, a, off));
+      if (lane == (n & 31)) keep = a;
+    }
+    v[0] = keep;
+  }
+}
+template <int CPT>
+BA_DEVINL void warp_colsum(float* v, int lane) {
+  if constexpr ((CPT & (CPT - 1)) == 0 && CPT <= 32) {
+    warp_col_reduce<CPT, false>(v, lane);
+  } else {
+    float keep = 0.f;
+#pragma unroll
+    for (int n = 0; n < CPT; ++n) {
+      float a = v[n];
+#pragma unroll
+      for (int off = 16; off >= 1; off >>= 1) a += __shfl_xor_sync(0xffffffffu, a, off);
+      if (lane == (n & 31)) keep = a;
+    }
+    v[0] = keep;
+  }
+}
+
+// Join the partials of the rows listed in gr_tab[0..N) (one warp per row, 8
+// warps): context slots [0, nctx), decode slots [Sc, Sc + ndec).  Loads of up
+// to 8 slots are issued together so a row costs ~one L2 round trip per 8.
+BA_DEVINL void merge_rows(const BifTcParams& P, const int* gr_tab, int N, int nctx, int ndec,
+                          int sw, int lane) {
+  const int n = nctx + ndec;
+  for (int col = sw; col < N; col += 8) {
+    const int gr = gr_tab[col];
+    if (gr < 0) continue;
+    const float2* ml = reinterpret_cast<const float2*>(P.ws_ml) + (size_t)gr * P.S;
+    const float* obuf = P.ws_o + (size_t)gr * P.S * bif::kD;
+    float M = kNegInf;
+    for (int q = lane; q < n; q += 32) M = fmaxf(M, __ldcg(ml + (q < nctx ? q : P.Sc + q - nctx)).x);
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
+    const float Ms = (M == kNegInf) ? 0.f : M;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    float Lsum = 0.f;
+    for (int q0 = 0; q0 < n; q0 += 8) {
+      float2 mv[8];
+      float4 ov[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int q = q0 + k;
+        if (q < n) {
+          const int sl = q < nctx ? q : P.Sc + q - nctx;
+          mv[k] = __ldcg(ml + sl);
+          ov[k] = __ldcg(reinterpret_cast<const float4*>(obuf + (size_t)sl * bif::kD) + lane);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        if (q0 + k < n) {
+          const float wgt = ex2(mv[k].x - Ms);
+          Lsum = fmaf(wgt, mv[k].y, Lsum);
+          acc.x = fmaf(wgt, ov[k].x, acc.x);
+          acc.y = fmaf(wgt, ov[k].y, acc.y);
+          acc.z = fmaf(wgt, ov[k].z, acc.z);
+          acc.w = fmaf(wgt, ov[k].w, acc.w);
+        }
+      }
+    }
+    const float inv = 1.f / Lsum;
+    const uint2 packed = make_uint2(pack_bf16x2(acc.x * inv, acc.y * inv),
+                                    pack_bf16x2(acc.z * inv, acc.w * inv));
+    *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(P.out) + (size_t)gr * bif::kD + lane * 4) = packed;
+    if (P.lse && lane == 0) P.lse[gr] = (M + lg2(Lsum)) * kLn2;
+  }
+}
+
 template <int N>
 __global__ void __launch_bounds__(bif::kThreads, 1)
     bif_tc_kernel(const __grid_constant__ BifTcParams P) {
@@ -246,7 +360,7 @@ __global__ void __launch_bounds__(bif::kThreads, 1)
   uint64_t* o_full = bars + 28;    // [2]
   uint64_t* o_empty = bars + 30;   // [2]
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 32);
-  int* sm_flag = reinterpret_cast<int*>(bars + 33);
+  int* sm_flag = reinterpret_cast<int*>(bars + 33);  // [3]: last?, nctx, ndec
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -303,16 +417,10 @@ __global__ void __launch_bounds__(bif::kThreads, 1)
         tc::mbar_arrive_expect_tx(qb, 2 * N * 128);
         tc::tma_load_3d(qdst, &P.tmQc, qb, 0, s.c * P.p, s.rc * P.spc);
         tc::tma_load_3d(qdst + N * 128, &P.tmQc, qb, 64, s.c * P.p, s.rc * P.spc);
+        int t = s.t0, i = s.i0;
+        const int ntl = s.dec ? P.ntile_d : P.ntile_c;
         for (int j = 0; j < s.ntiles; ++j, ++tt) {
-          const long long f = s.f + j;
-          int t, z;
-          if (!s.dec) {
-            t = (int)(f % P.ntile_c);
-            z = s.c;
-          } else {
-            t = (int)(f % P.ntile_d);
-            z = (int)((f / P.ntile_d) % P.b) * P.g + s.c;  // i*g + c
-          }
+          const int z = s.dec ? i * P.g + s.c : s.c;  // TMA z: group, or sample*g + group
           const CUtensorMap* mk = s.dec ? &P.tmKd : &P.tmKc;
           const CUtensorMap* mv = s.dec ? &P.tmVd : &P.tmVc;
           const uint64_t pol = s.dec ? pol_d : pol_c;
@@ -325,6 +433,10 @@ __global__ void __launch_bounds__(bif::kThreads, 1)
           tc::tma_load_3d_hint(dst + 16384, mk, bar, 64, t * kBM, z, pol);
           tc::tma_load_3d_hint(dst + 32768, mv, bar, 0, t * kBM, z, pol);
           tc::tma_load_3d_hint(dst + 49152, mv, bar, 64, t * kBM, z, pol);
+          if (++t == ntl) {
+            t = 0;
+            ++i;
+          }
         }
         w = s.next;
       }
@@ -423,6 +535,8 @@ __global__ void __launch_bounds__(bif::kThreads, 1)
     const uint32_t lane_addr = (uint32_t)(quad * 32) << 16;
     const float sl2 = P.scale_log2;
     const int R = P.b * P.p;
+    int* sm_len = reinterpret_cast<int*>(sm_l);  // per-segment sample lengths (tile loop only)
+    int* sm_gr = reinterpret_cast<int*>(sm_red); // per-segment output rows (epilogue only)
     uint32_t u = 0, sg = 0, cur = 0;
     unsigned long long* tr = P.trace ? P.trace + (size_t)blockIdx.x * kTraceSlots : nullptr;
     int ntr = 0;
@@ -437,28 +551,23 @@ __global__ void __launch_bounds__(bif::kThreads, 1)
       float l_part[CPT];
 #pragma unroll
       for (int n = 0; n < CPT; ++n) l_part[n] = 0.f;
-      // running max of every column starts unset (-inf)
+      // running max of every column starts unset (-inf); decode lengths of the chunk's samples
       if (quad == 0 && lane == 0) {
 #pragma unroll
         for (int n = 0; n < CPT; ++n) sm_mrun[cur * N + col0 + n] = kNegInf;
       }
+      if (s.dec && sw * 32 + lane < P.spc) {
+        const int i = s.rc * P.spc + sw * 32 + lane;
+        sm_len[sw * 32 + lane] = i < P.b ? dec_len(P, i) : 0;
+      }
       tc::named_bar_sync(2, 256);
+      int t = s.t0, il = s.i0 - s.rc * P.spc;  // tile index, sample within the chunk
+      const int ntl = s.dec ? P.ntile_d : P.ntile_c;
       for (int j = 0; j < s.ntiles; ++j, ++u) {
-        const long long f = s.f + j;
         // valid columns [cv0, cv1) and positions [0, L) of this tile
-        int t, L, cv0, cv1;
-        if (!s.dec) {
-          t = (int)(f % P.ntile_c);
-          L = P.mc;
-          cv0 = 0;
-          cv1 = N;
-        } else {
-          t = (int)(f % P.ntile_d);
-          const int i = (int)((f / P.ntile_d) % P.b);
-          L = dec_len(P, i);
-          cv0 = i * P.p - s.rc * N;
-          cv1 = cv0 + P.p;
-        }
+        const int L = s.dec ? sm_len[il] : P.mc;
+        const int cv0 = s.dec ? il * P.p : 0;
+        const int cv1 = s.dec ? cv0 + P.p : N;
         const uint32_t slot = u & 1;
         const float* mrun = sm_mrun + cur * N + col0;
         tc::mbar_wait(tc::smem_u32(&s_full[slot]), (u >> 1) & 1);
@@ -482,13 +591,27 @@ __global__ void __launch_bounds__(bif::kThreads, 1)
           need |= vc && (mo == kNegInf || x[n] > kTh);
         }
         if (tc::named_bar_or(1, 256, need)) {
-          // ---- slow path: exact column max over the tile, new m_run ----
+          // ---- slow path: exact max of the tile's valid columns, new m_run ----
+          if (col0 < cv1 && col0 + CPT > cv0) {  // warp-uniform: this half has valid columns
+            if (cv1 - cv0 >= 16) {
+              // butterfly transpose-reduce: lane l ends with the max of column (l % CPT)
+              float v[CPT];
 #pragma unroll
-          for (int n = 0; n < CPT; ++n) {
-            float v = x[n];
+              for (int n = 0; n < CPT; ++n) v[n] = x[n];
+              warp_colmax<CPT>(v, lane);
+              if (lane < CPT) sm_red[quad * N + col0 + lane] = v[0];
+            } else {
 #pragma unroll
-            for (int off = 16; off >= 1; off >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, off));
-            if (lane == (n & 31)) sm_red[quad * N + col0 + n] = v;
+              for (int n = 0; n < CPT; ++n) {
+                const int col = col0 + n;
+                if (col >= cv0 && col < cv1) {
+                  float v = x[n];
+#pragma unroll
+                  for (int off = 16; off >= 1; off >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, off));
+                  if (lane == 0) sm_red[quad * N + col] = v;
+                }
+              }
+            }
           }
           tc::named_bar_sync(2, 256);
           float* mnext = sm_mrun + (cur ^ 1) * N + col0;
@@ -497,15 +620,18 @@ __global__ void __launch_bounds__(bif::kThreads, 1)
           for (int n = 0; n < CPT; ++n) {
             const int col = col0 + n;
             const float mo = mrun[n];
-            const float mref = (mo == kNegInf) ? 0.f : mo;
-            const float cm = fmaxf(fmaxf(sm_red[col], sm_red[N + col]),
-                                   fmaxf(sm_red[2 * N + col], sm_red[3 * N + col]));
-            const float mnew = fmaxf(mo, mref + cm);  // unchanged if the column had no valid logit
-            // l, O of a column are exactly 0 while its max is unset
-            const float alpha = (mo == kNegInf) ? 0.f : ex2(mo - mnew);
-            l_part[n] *= alpha;
-            x[n] = (mnew == kNegInf) ? kNegInf : x[n] + (mref - mnew);
-            grew |= (mo != kNegInf) && (mnew > mo);
+            float mnew = mo;
+            if (col >= cv0 && col < cv1) {
+              const float mref = (mo == kNegInf) ? 0.f : mo;
+              const float cm = fmaxf(fmaxf(sm_red[col], sm_red[N + col]),
+                                     fmaxf(sm_red[2 * N + col], sm_red[3 * N + col]));
+              mnew = fmaxf(mo, mref + cm);  // -inf stays if the column had no valid logit
+              // l and O of a column are exactly 0 while its max is unset
+              const float alpha = (mo == kNegInf) ? 0.f : ex2(mo - mnew);
+              l_part[n] *= alpha;
+              x[n] = (mnew == kNegInf) ? kNegInf : x[n] + (mref - mnew);
+              grew |= (mo != kNegInf) && (mnew > mo);
+            }
             if (quad == 0 && lane == 0) mnext[n] = mnew;
           }
           if (tc::named_bar_or(1, 256, grew)) {
@@ -553,16 +679,22 @@ __global__ void __launch_bounds__(bif::kThreads, 1)
         tc::fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(tc::smem_u32(&p_full[slot]));
+        if (++t == ntl) {
+          t = 0;
+          ++il;
+        }
       }
       // ------------------------- segment epilogue -------------------------
       stamp(4);
-#pragma unroll
-      for (int n = 0; n < CPT; ++n) {
-        float v = l_part[n];
-#pragma unroll
-        for (int off = 16; off >= 1; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-        if (lane == (n & 31)) sm_l[quad * N + col0 + n] = v;
+      // row sums over the 32 positions of this warp (lane l -> column l % CPT)
+      warp_colsum<CPT>(l_part, lane);
+      tc::named_bar_sync(2, 256);  // sm_len reads done; sm_red free
+      if (lane < CPT) sm_l[quad * N + col0 + lane] = l_part[0];
+      if (sw * 32 + lane < N) {
+        const int r = s.rc * N + sw * 32 + lane;
+        sm_gr[sw * 32 + lane] = r < R ? (r / P.p) * P.h + s.c * P.p + (r % P.p) : -1;
       }
+      tc::named_bar_sync(2, 256);
       stamp(8);
       tc::mbar_wait(tc::smem_u32(&o_full[ob]), (sg >> 1) & 1);
       tc::tc_fence_after();
@@ -574,81 +706,45 @@ __global__ void __launch_bounds__(bif::kThreads, 1)
         tc::tmem_ld_wait();
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
-          const int r = s.rc * N + col0 + n + e;
-          if (r < R) {
-            const int gr = (r / P.p) * P.h + s.c * P.p + (r % P.p);
-            P.ws_o[((size_t)gr * P.S + s.slot) * kD + pos] = __uint_as_float(orr[e]);
-          }
+          const int gr = sm_gr[col0 + n + e];
+          if (gr >= 0) P.ws_o[((size_t)gr * P.S + s.slot) * kD + pos] = __uint_as_float(orr[e]);
         }
       }
       tc::tc_fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(tc::smem_u32(&o_empty[ob]));
-      tc::named_bar_sync(2, 256);
-      stamp(10);
       if (sw < 2) {
         const int col = sw * 32 + lane;
-        const int r = s.rc * N + col;
-        if (col < N && r < R) {
-          const int gr = (r / P.p) * P.h + s.c * P.p + (r % P.p);
+        const int gr = col < N ? sm_gr[col] : -1;
+        if (gr >= 0) {
           const float Lr = sm_l[col] + sm_l[N + col] + sm_l[2 * N + col] + sm_l[3 * N + col];
-          float* ml = P.ws_ml + ((size_t)gr * P.S + s.slot) * 2;
-          ml[0] = sm_mrun[cur * N + col];
-          ml[1] = Lr;
+          float2* ml = reinterpret_cast<float2*>(P.ws_ml) + (size_t)gr * P.S + s.slot;
+          *ml = make_float2(sm_mrun[cur * N + col], Lr);
         }
       }
+      stamp(10);
       // ---- arrive at the (group, row chunk) counter; the last arrival merges ----
       tc::named_bar_sync(2, 256);
-      const int cidx = s.c * P.nrc + s.rc;
-      const int nctx = ctx_parts(P, s.c, s.rc), ndec = dec_parts(P, s.c, s.rc);
       stamp(11);
+      const int cidx = s.c * P.nrc + s.rc;
       if (threadIdx.x == 128) {
+        const int nparts = ctx_parts(P, s.c, s.rc) + dec_parts(P, s.c, s.rc);
         __threadfence();
         const unsigned old = atomicAdd(&P.counters[cidx], 1u);
-        const int last = old == (unsigned)(nctx + ndec - 1);
+        const int last = old == (unsigned)(nparts - 1);
         if (last) {
           __threadfence();
           P.counters[cidx] = 0u;  // self-reset for the next call
         }
-        *sm_flag = last;
+        sm_flag[0] = last;
+        sm_flag[1] = ctx_parts(P, s.c, s.rc);
+        sm_flag[2] = dec_parts(P, s.c, s.rc);
       }
       tc::named_bar_sync(2, 256);
-      stamp(*sm_flag ? 6 : 5);
-      if (*sm_flag) {
+      stamp(sm_flag[0] ? 6 : 5);
+      if (sm_flag[0]) {
         __threadfence();
-        const int r0 = s.rc * N, r1 = min(R, (s.rc + 1) * N);
-        for (int r = r0 + sw; r < r1; r += 8) {
-          const int gr = (r / P.p) * P.h + s.c * P.p + (r % P.p);
-          const float* ml = P.ws_ml + (size_t)gr * P.S * 2;
-          const float* obuf = P.ws_o + (size_t)gr * P.S * kD;
-          float M = kNegInf;
-          for (int q = lane; q < nctx + ndec; q += 32) {
-            const int sl = q < nctx ? q : P.Sc + (q - nctx);
-            M = fmaxf(M, __ldcg(ml + 2 * sl));
-          }
-#pragma unroll
-          for (int off = 16; off >= 1; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
-          const float Ms = (M == kNegInf) ? 0.f : M;
-          float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-          float Lsum = 0.f;
-#pragma unroll 4
-          for (int q = 0; q < nctx + ndec; ++q) {
-            const int sl = q < nctx ? q : P.Sc + (q - nctx);
-            const float2 mlq = __ldcg(reinterpret_cast<const float2*>(ml) + sl);
-            const float wgt = ex2(mlq.x - Ms);
-            Lsum = fmaf(wgt, mlq.y, Lsum);
-            const float4 o4 = __ldcg(reinterpret_cast<const float4*>(obuf + (size_t)sl * kD) + lane);
-            acc.x = fmaf(wgt, o4.x, acc.x);
-            acc.y = fmaf(wgt, o4.y, acc.y);
-            acc.z = fmaf(wgt, o4.z, acc.z);
-            acc.w = fmaf(wgt, o4.w, acc.w);
-          }
-          const float inv = 1.f / Lsum;
-          const uint2 packed = make_uint2(pack_bf16x2(acc.x * inv, acc.y * inv),
-                                          pack_bf16x2(acc.z * inv, acc.w * inv));
-          *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(P.out) + (size_t)gr * kD + lane * 4) = packed;
-          if (P.lse && lane == 0) P.lse[gr] = (M + lg2(Lsum)) * kLn2;
-        }
+        merge_rows(P, sm_gr, N, sm_flag[1], sm_flag[2], sw, lane);
       }
       w = s.next;
     }
