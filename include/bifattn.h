@@ -84,13 +84,11 @@ typedef struct {
 } ba_problem_t;
 
 /* Bytes of device workspace bifurcated_attn_decode() / replicated_attn_decode()
- * need: per-(group, row chunk) completion counters at offset 0, then fp32
- * partials (m, l, o[d]) per output row and split.  Returns 0 for an invalid
- * problem.  The workspace must be 16-byte aligned and ZEROED ONCE before its
- * first use (cudaMemset); every completed call leaves the counters zero
- * again, so one workspace serves any number of back-to-back calls (and CUDA
- * graph replays) of the same problem on one stream.  Calls that may run
- * concurrently need separate workspaces. */
+ * need: fp32 partials (m, l, o[d]) per output row and split.  Returns 0 for an
+ * invalid problem.  The workspace must be 16-byte aligned; it needs no
+ * initialisation and is fully rewritten by every call, so one workspace
+ * serves any number of back-to-back calls (and CUDA graph replays) on one
+ * stream.  Calls that may run concurrently need separate workspaces. */
 size_t ba_workspace_bytes(const ba_problem_t* prob);
 
 /* One decode step of bifurcated attention (see above).  Kc/Vc are read from

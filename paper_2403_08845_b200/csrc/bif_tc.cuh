@@ -1,38 +1,43 @@
-// bif_tc.cuh — the whole bifurcated decode step in ONE persistent launch on the
-// 5th-gen tensor cores (tcgen05 + TMEM + TMA), sm_100a.
+// bif_tc.cuh — one incremental-decoding step of context-aware bifurcated
+// attention on the 5th-gen tensor cores (tcgen05 + TMEM + TMA), sm_100a:
+// one persistent streaming kernel (bif_tc_kernel) + one small LSE-merge
+// kernel chained with programmatic dependent launch (bif_merge_kernel).
 //
 // What it computes (Eq. 3-4; App. E.3):
 //   context segments:  the R = b*p query rows of group c that share Kc[c] and
 //                      Vc[c] (no batch axis) against a run
-//                      of 128-position context tiles;
+//                      of 128-position context tiles — each context tile is
+//                      read from HBM once for all b samples;
 //   decode segments:   the same row chunk against the 128-position tiles of its
 //                      samples' own Kd[i][c]/Vd[i][c],
 //                      sample after sample; a tile of sample i only feeds the
 //                      p columns of sample i (others masked), positions masked
 //                      at lens[i];
-//   merge:             the last partial to arrive for a (group, row chunk)
-//                      joins its rows' partials with one log-sum-exp — the
-//                      single softmax over S_c ⊕ S_d split
-//                      at mc and summed (Eq. 4) — and writes out / lse.
-// Each context tile is read from HBM once for all b samples.
+//   merge:             every row's partials (m, l, o) joined with one
+//                      log-sum-exp — the single softmax over S_c ⊕ S_d
+//                       split at mc and summed (Eq. 4).
 //
 // Tile math (swap-AB: query rows are few, positions many):
-//   S^T[128 pos x N]  = K_tile[128 x d] . q_seg^T[d x N]      (M=128, K=d=128)
+//   S^T[128 pos x N]  = K_tile[128 x d] . q_chunk^T[d x N]    (M=128, K=d=128)
 //   O^T[d x N]       += V_tile^T[d x 128] . P^T[128 x N]       (M=d=128, K=128)
-// K/V tiles arrive by TMA (128B swizzle) in an NST-stage ring; S^T (double
-// buffered) and O^T live in TMEM; P (bf16) goes through shared memory.
+// K/V tiles arrive by TMA (128B swizzle) in an NST-stage ring; S^T (2 slots)
+// and O^T (2 buffers) live in TMEM; P (bf16) goes through shared memory.
 //
-// Warp roles (12 warps, 1 CTA per SM): 0 TMA producer, 1 MMA issuer (one
-// lane), 2 TMEM allocator, 3 idle, 4..11 softmax / epilogue / merge.  Softmax
-// warp w reads TMEM lanes 32*(w%4)... (positions; d in the epilogue) and
-// columns [half*CPT, half*CPT+CPT), half = (w-4)/4, CPT = N/2.
+// Warp roles (1 CTA per SM):
+//   warp 0            TMA producer (one lane)
+//   warp 1            MMA issuer (one lane): QK(u) when its K tile, q and an
+//                     S slot are ready; PV(v) when P(v) is — whichever first
+//   warp 2            TMEM allocator; warp 3 idle
+//   warps 4..4+4W-1   softmax (W warpgroups): warp w reads TMEM lanes
+//                     32*(w%4).. (= tile positions), CPT = N/W columns
+//   last 4 warps      epilogue: drains O^T of a finished segment from TMEM to
+//                     the workspace while the softmax warps run the next one
 //
 // Online softmax with a stale-max fast path: P = 2^(s*scale*log2e - m_run);
 // only when a valid logit exceeds m_run by more than kTh, or a column sees its
-// first valid logit (m_run unset), do the warps (CTA-wide vote, bar.red.or)
+// first valid logit (m_run unset), do the softmax warps (vote: bar.red.or)
 // compute the exact tile max per column and raise m_run — rescaling l and
-// O^T (TMEM) only for columns whose max actually grew.  Same softmax; values
-// stay <= 2^kTh.
+// O^T only for columns whose max actually grew.  Same softmax; P <= 2^kTh.
 //
 // Work split: context tiles fc = (c*nrc + rc)*ntile_c + t in [0, Tc) and
 // decode tiles fd = (c*b + i)*ntile_d + t in [0, Td).  CTA k of G takes
@@ -40,8 +45,8 @@
 // (k+1)*Td/G): every CTA streams the same number of 64 KB tiles (+-1 of each
 // kind).  A maximal run of tiles of one (c, rc) — context, or decode tiles of
 // the chunk's samples — is a segment and writes one partial (m, l, o) for
-// every row of the chunk to its workspace slot.  q and O^T are double
-// buffered across segments so a segment boundary costs no pipeline drain.
+// every row of the chunk to its workspace slot (context slots [0, Sc),
+// decode slots [Sc, S)).
 #pragma once
 #include "common.cuh"
 #include "tc_ptx.cuh"
@@ -55,6 +60,7 @@ struct BifTcParams {
   const int32_t* lens;
   int b, h, g, p, mc;
   int dec_cap, lens_offset;  // decode length = lens_offset + clamp(lens[i], 0, dec_cap)
+  int N;                     // rows per chunk (== template N)
   int nrc, ntile_c, ntile_d;
   int spc;                   // samples per row chunk = N / p
   long long Tc, Td;          // context tiles, decode tiles
@@ -63,19 +69,21 @@ struct BifTcParams {
   int S, Sc;                 // slots per row; decode slots start at Sc
   float* ws_o;               // [b*h][S][128]
   float* ws_ml;              // [b*h][S][2]
-  unsigned* counters;        // [g*nrc] arrivals per (group, row chunk); self-resetting
   void* out;                 // [b][h][128] bf16
   float* lse;                // [b][h] or null
   unsigned long long* trace; // optional [G][kTraceSlots] globaltimer stamps (instrumentation)
 };
 
 namespace bif {
-constexpr int kThreads = 384;
 constexpr int kD = 128;
 constexpr int kBM = 128;            // positions per tile (MMA M)
 constexpr int kStageBytes = 65536;  // K tile 32 KB + V tile 32 KB
 constexpr float kTh = 8.0f;         // fast-path slack (log2 units)
 constexpr int kTraceSlots = 64;
+
+// softmax warpgroups: keep columns per softmax thread <= 32
+__host__ __device__ constexpr int softmax_wgs(int N) { return N <= 32 ? 1 : 2; }
+__host__ __device__ constexpr int threads(int N) { return 32 * (8 + 4 * softmax_wgs(N)); }
 
 __host__ __device__ constexpr int p_atom(int N) { return (N % 64 == 0) ? 64 : ((N % 32 == 0) ? 32 : 16); }
 __host__ __device__ constexpr int p_layout(int N) {
@@ -84,9 +92,12 @@ __host__ __device__ constexpr int p_layout(int N) {
 __host__ __device__ constexpr int tmem_cols(int N) {  // 2 S^T slots + 2 O^T buffers
   return 4 * N <= 32 ? 32 : 4 * N <= 64 ? 64 : 4 * N <= 128 ? 128 : 4 * N <= 256 ? 256 : 512;
 }
-// dynamic smem besides the stages: 2 q buffers + 2 P buffers (256N each) + scratch (40N) +
-// barriers (512) + alignment slack (1024)
-__host__ __device__ constexpr int smem_fixed(int N) { return 4 * 256 * N + 40 * N + 512 + 1024; }
+// dynamic smem besides the stages: 2 q + 2 P buffers (256N B each), col-max
+// scratch [4][N], row sums [2][4][N], m_run [2][N], final m [2][N] (floats),
+// lengths [64] ints, barriers (512 B)
+__host__ __device__ constexpr int smem_fixed(int N) {
+  return 4 * 256 * N + 4 * (4 * N + 8 * N + 2 * N + 2 * N) + 256 + 512;
+}
 
 // CTA owning flat tile f when T tiles are split over G CTAs as [kT/G, (k+1)T/G)
 __host__ __device__ inline int owner(long long f, long long T, int G) {
@@ -132,12 +143,14 @@ BA_DEVINL Range my_range(const BifTcParams& P) {
 }
 
 // First / one-past-last decode tile of chunk (c, rc).
-BA_DEVINL long long dec_chunk_begin(const BifTcParams& P, int c, int rc) {
-  return ((long long)c * P.b + (long long)rc * P.spc) * P.ntile_d;
+__host__ __device__ inline long long dec_chunk_begin(long long b, long long spc, long long ntd,
+                                                     int c, int rc) {
+  return ((long long)c * b + (long long)rc * spc) * ntd;
 }
-BA_DEVINL long long dec_chunk_end(const BifTcParams& P, int c, int rc) {
-  const long long i1 = min((long long)P.b, (long long)(rc + 1) * P.spc);
-  return ((long long)c * P.b + i1) * P.ntile_d;
+__host__ __device__ inline long long dec_chunk_end(long long b, long long spc, long long ntd, int c,
+                                                   int rc) {
+  const long long i1 = (long long)(rc + 1) * spc < b ? (long long)(rc + 1) * spc : b;
+  return ((long long)c * b + i1) * ntd;
 }
 
 BA_DEVINL Seg seg_at(const BifTcParams& P, const Range& rg, long long w) {
@@ -164,8 +177,8 @@ BA_DEVINL Seg seg_at(const BifTcParams& P, const Range& rg, long long w) {
     s.i0 = (int)(cb % P.b);
     s.rc = s.i0 / P.spc;
     s.t0 = (int)(f - cb * P.ntile_d);
-    const long long a = dec_chunk_begin(P, s.c, s.rc);
-    const long long fend = min(dec_chunk_end(P, s.c, s.rc), rg.fd1);
+    const long long a = dec_chunk_begin(P.b, P.spc, P.ntile_d, s.c, s.rc);
+    const long long fend = min(dec_chunk_end(P.b, P.spc, P.ntile_d, s.c, s.rc), rg.fd1);
     s.f = f;
     s.ntiles = (int)(fend - f);
     s.slot = P.Sc + part_rank(a, f, P.Td, P.G);
@@ -175,20 +188,29 @@ BA_DEVINL Seg seg_at(const BifTcParams& P, const Range& rg, long long w) {
 }
 
 // Partials written for the rows of chunk (c, rc).
-BA_DEVINL int ctx_parts(const BifTcParams& P, int c, int rc) {
+__host__ __device__ inline int ctx_parts(const BifTcParams& P, int c, int rc) {
   if (P.Tc == 0) return 0;
   const long long ff = ((long long)c * P.nrc + rc) * P.ntile_c;
   return part_rank(ff, ff + P.ntile_c - 1, P.Tc, P.G) + 1;
 }
-BA_DEVINL int dec_parts(const BifTcParams& P, int c, int rc) {
+__host__ __device__ inline int dec_parts(const BifTcParams& P, int c, int rc) {
   if (P.Td == 0) return 0;
-  const long long a = dec_chunk_begin(P, c, rc), e = dec_chunk_end(P, c, rc);
+  const long long a = dec_chunk_begin(P.b, P.spc, P.ntile_d, c, rc);
+  const long long e = dec_chunk_end(P.b, P.spc, P.ntile_d, c, rc);
   return part_rank(a, e - 1, P.Td, P.G) + 1;
+}
+
+// output row of column col of chunk (c, rc), or -1 for padding
+BA_DEVINL int row_of(const BifTcParams& P, int c, int rc, int col) {
+  const int r = rc * P.N + col;
+  if (r >= P.b * P.p) return -1;
+  const int i = r / P.p;
+  return i * P.h + c * P.p + (r - i * P.p);
 }
 }  // namespace bif
 
 template <int CPT>
-BA_DEVINL void tmem_ld_cols2(uint32_t taddr, uint32_t* r) {
+BA_DEVINL void tmem_ld_cols(uint32_t taddr, uint32_t* r) {
   int c = 0;
 #pragma unroll
   for (; c + 32 <= CPT; c += 32) tc::tmem_ld<32>(taddr + c, r + c);
@@ -215,16 +237,14 @@ BA_DEVINL bool mbar_test(uint32_t bar, uint32_t parity) {
   return ok != 0;
 }
 
-// Butterfly transpose-reduce over the 32 lanes of a warp: v[CPT] per lane
-// (CPT a power of two, 8..32) -> lane l holds in v[0] the max / sum of column
-// (l % CPT) over all 32 lanes.  CPT-1 shuffles + log2(32/CPT)*1 instead of
-// 5*CPT for independent column reductions.
+// Butterfly transpose-reduce over the 32 lanes of a warp: v[CPT] per lane ->
+// lane l holds in v[0] the max / sum of column (l % CPT) over all 32 lanes.
+// CPT-1 (+ log2(32/CPT)) shuffles instead of 5*CPT.  CPT a power of two <= 32.
 template <int CPT, bool kMax>
-BA_DEVINL void warp_col_reduce(float* v, int lane) {
+BA_DEVINL void warp_col_reduce_pow2(float* v, int lane) {
 #pragma unroll
   for (int w = CPT / 2; w >= 1; w >>= 1) {
-    // pair columns k and k+w: lanes with bit w set keep the upper half
-    const bool upper = lane & w;
+    const bool upper = lane & w;  // lanes with bit w set keep columns [w, 2w)
 #pragma unroll
     for (int k = 0; k < w; ++k) {
       const float send = upper ? v[k] : v[k + w];
@@ -233,102 +253,40 @@ BA_DEVINL void warp_col_reduce(float* v, int lane) {
       v[k] = kMax ? fmaxf(keep, got) : keep + got;
     }
   }
-  // v[0] now holds column (lane % CPT) reduced over the lanes that share lane / CPT... finish
 #pragma unroll
   for (int off = CPT; off < 32; off <<= 1) {
     const float got = __shfl_xor_sync(0xffffffffu, v[0], off);
     v[0] = kMax ? fmaxf(v[0], got) : v[0] + got;
   }
 }
-template <int CPT>
-BA_DEVINL void warp_colmax(float* v, int lane) {
-  if constexpr ((CPT & (CPT - 1)) == 0 && CPT <= 32) {
-    warp_col_reduce<CPT, true>(v, lane);
+template <int CPT, bool kMax>
+BA_DEVINL void warp_col_reduce(float* v, int lane) {
+  if constexpr ((CPT & (CPT - 1)) == 0) {
+    warp_col_reduce_pow2<CPT, kMax>(v, lane);
   } else {
-    // generic: reduce each column, lane n keeps column n
-    float keep = kNegInf;
+    float keep = kMax ? kNegInf : 0.f;
 #pragma unroll
     for (int n = 0; n < CPT; ++n) {
       float a = v[n];
 #pragma unroll
-      for (int off = 16; off >= 1; off >>= 1) a = fmaxf(a, __shfl_xor_sync(0xffffffffu, a, off));
-      if (lane == (n & 31)) keep = a;
+      for (int off = 16; off >= 1; off >>= 1) {
+        const float got = __shfl_xor_sync(0xffffffffu, a, off);
+        a = kMax ? fmaxf(a, got) : a + got;
+      }
+      if (lane == n) keep = a;
     }
     v[0] = keep;
-  }
-}
-template <int CPT>
-BA_DEVINL void warp_colsum(float* v, int lane) {
-  if constexpr ((CPT & (CPT - 1)) == 0 && CPT <= 32) {
-    warp_col_reduce<CPT, false>(v, lane);
-  } else {
-    float keep = 0.f;
-#pragma unroll
-    for (int n = 0; n < CPT; ++n) {
-      float a = v[n];
-#pragma unroll
-      for (int off = 16; off >= 1; off >>= 1) a += __shfl_xor_sync(0xffffffffu, a, off);
-      if (lane == (n & 31)) keep = a;
-    }
-    v[0] = keep;
-  }
-}
-
-// Join the partials of the rows listed in gr_tab[0..N) (one warp per row, 8
-// warps): context slots [0, nctx), decode slots [Sc, Sc + ndec).  Loads of up
-// to 8 slots are issued together so a row costs ~one L2 round trip per 8.
-BA_DEVINL void merge_rows(const BifTcParams& P, const int* gr_tab, int N, int nctx, int ndec,
-                          int sw, int lane) {
-  const int n = nctx + ndec;
-  for (int col = sw; col < N; col += 8) {
-    const int gr = gr_tab[col];
-    if (gr < 0) continue;
-    const float2* ml = reinterpret_cast<const float2*>(P.ws_ml) + (size_t)gr * P.S;
-    const float* obuf = P.ws_o + (size_t)gr * P.S * bif::kD;
-    float M = kNegInf;
-    for (int q = lane; q < n; q += 32) M = fmaxf(M, __ldcg(ml + (q < nctx ? q : P.Sc + q - nctx)).x);
-#pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
-    const float Ms = (M == kNegInf) ? 0.f : M;
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    float Lsum = 0.f;
-    for (int q0 = 0; q0 < n; q0 += 8) {
-      float2 mv[8];
-      float4 ov[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const int q = q0 + k;
-        if (q < n) {
-          const int sl = q < nctx ? q : P.Sc + q - nctx;
-          mv[k] = __ldcg(ml + sl);
-          ov[k] = __ldcg(reinterpret_cast<const float4*>(obuf + (size_t)sl * bif::kD) + lane);
-        }
-      }
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        if (q0 + k < n) {
-          const float wgt = ex2(mv[k].x - Ms);
-          Lsum = fmaf(wgt, mv[k].y, Lsum);
-          acc.x = fmaf(wgt, ov[k].x, acc.x);
-          acc.y = fmaf(wgt, ov[k].y, acc.y);
-          acc.z = fmaf(wgt, ov[k].z, acc.z);
-          acc.w = fmaf(wgt, ov[k].w, acc.w);
-        }
-      }
-    }
-    const float inv = 1.f / Lsum;
-    const uint2 packed = make_uint2(pack_bf16x2(acc.x * inv, acc.y * inv),
-                                    pack_bf16x2(acc.z * inv, acc.w * inv));
-    *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(P.out) + (size_t)gr * bif::kD + lane * 4) = packed;
-    if (P.lse && lane == 0) P.lse[gr] = (M + lg2(Lsum)) * kLn2;
   }
 }
 
 template <int N>
-__global__ void __launch_bounds__(bif::kThreads, 1)
+__global__ void __launch_bounds__(bif::threads(N), 1)
     bif_tc_kernel(const __grid_constant__ BifTcParams P) {
   using namespace bif;
-  constexpr int CPT = N / 2;
+  constexpr int SWG = softmax_wgs(N);        // softmax warpgroups
+  constexpr int NSW = 4 * SWG;               // softmax warps
+  constexpr int CPT = N / SWG;               // columns per softmax thread
+  constexpr int EPI0 = 4 + NSW;              // first epilogue warp
   constexpr int W = p_atom(N);
   constexpr int PRB = 2 * W;
   constexpr int PLBO = kBM * PRB;
@@ -337,18 +295,20 @@ __global__ void __launch_bounds__(bif::kThreads, 1)
   constexpr uint32_t IDESC_PV = tc::idesc_bf16(128, N, 1, 1);
   constexpr uint32_t TMEM_COLS = tmem_cols(N);
   constexpr int QB = 256 * N;  // bytes of one q buffer / one P buffer
-  static_assert(N % 16 == 0 && N >= 16 && N <= 64, "N");
+  static_assert(N % 16 == 0 && N >= 16 && N <= 64 && CPT % 8 == 0 && CPT <= 32, "N");
 
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(1024) uint8_t smem[];
+  if (threadIdx.x == 0 && (reinterpret_cast<uintptr_t>(smem) & 1023)) __trap();  // SW128 needs 1 KB
   const int NST = P.nst;
   uint8_t* sm_stage = smem;
   uint8_t* sm_q = smem + NST * kStageBytes;  // 2 buffers
   uint8_t* sm_p = sm_q + 2 * QB;             // 2 buffers
   float* sm_red = reinterpret_cast<float*>(sm_p + 2 * QB);  // [4][N] col max (slow path)
-  float* sm_l = sm_red + 4 * N;                             // [4][N] row sums (epilogue)
-  float* sm_mrun = sm_l + 4 * N;                            // [2][N] running max
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sm_mrun + 2 * N);
+  float* sm_l = sm_red + 4 * N;                             // [2][4][N] row sums per O buffer
+  float* sm_mrun = sm_l + 8 * N;                            // [2][N] running max
+  float* sm_mfin = sm_mrun + 2 * N;                         // [2][N] final max per O buffer
+  int* sm_len = reinterpret_cast<int*>(sm_mfin + 2 * N);    // [64] decode lengths of the chunk
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm_len + 64);
   uint64_t* kv_full = bars;        // [8]
   uint64_t* kv_empty = bars + 8;   // [8]
   uint64_t* q_full = bars + 16;    // [2]
@@ -357,10 +317,11 @@ __global__ void __launch_bounds__(bif::kThreads, 1)
   uint64_t* s_free = bars + 22;    // [2]
   uint64_t* p_full = bars + 24;    // [2]
   uint64_t* p_empty = bars + 26;   // [2]
-  uint64_t* o_full = bars + 28;    // [2]
-  uint64_t* o_empty = bars + 30;   // [2]
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 32);
-  int* sm_flag = reinterpret_cast<int*>(bars + 33);  // [3]: last?, nctx, ndec
+  uint64_t* o_full = bars + 28;    // [2]  last PV of a segment done
+  uint64_t* o_empty = bars + 30;   // [2]  epilogue drained the O buffer
+  uint64_t* e_full = bars + 32;    // [2]  softmax wrote row sums / final max
+  uint64_t* e_empty = bars + 34;   // [2]  epilogue consumed them
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 36);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -373,11 +334,13 @@ __global__ void __launch_bounds__(bif::kThreads, 1)
       tc::mbar_init(tc::smem_u32(&q_full[s]), 1);
       tc::mbar_init(tc::smem_u32(&q_empty[s]), 1);
       tc::mbar_init(tc::smem_u32(&s_full[s]), 1);
-      tc::mbar_init(tc::smem_u32(&s_free[s]), 8);
-      tc::mbar_init(tc::smem_u32(&p_full[s]), 8);
+      tc::mbar_init(tc::smem_u32(&s_free[s]), NSW);
+      tc::mbar_init(tc::smem_u32(&p_full[s]), NSW);
       tc::mbar_init(tc::smem_u32(&p_empty[s]), 1);
       tc::mbar_init(tc::smem_u32(&o_full[s]), 1);
-      tc::mbar_init(tc::smem_u32(&o_empty[s]), 8);
+      tc::mbar_init(tc::smem_u32(&o_empty[s]), 4);
+      tc::mbar_init(tc::smem_u32(&e_full[s]), NSW);
+      tc::mbar_init(tc::smem_u32(&e_empty[s]), 4);
     }
     tc::fence_mbar_init();
   }
@@ -395,6 +358,8 @@ __global__ void __launch_bounds__(bif::kThreads, 1)
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
+  // let the dependent merge kernel get launched early (it waits for our completion)
+  pdl_launch_dependents();
   const uint32_t tmem = *tmem_holder;
   const uint32_t tS = tmem;          // S^T slots at columns [0,N), [N,2N)
   const uint32_t tO = tmem + 2 * N;  // O^T buffers at [2N,3N), [3N,4N)
@@ -417,13 +382,13 @@ __global__ void __launch_bounds__(bif::kThreads, 1)
         tc::mbar_arrive_expect_tx(qb, 2 * N * 128);
         tc::tma_load_3d(qdst, &P.tmQc, qb, 0, s.c * P.p, s.rc * P.spc);
         tc::tma_load_3d(qdst + N * 128, &P.tmQc, qb, 64, s.c * P.p, s.rc * P.spc);
-        int t = s.t0, i = s.i0;
+        const CUtensorMap* mk = s.dec ? &P.tmKd : &P.tmKc;
+        const CUtensorMap* mv = s.dec ? &P.tmVd : &P.tmVc;
+        const uint64_t pol = s.dec ? pol_d : pol_c;
         const int ntl = s.dec ? P.ntile_d : P.ntile_c;
+        int t = s.t0, i = s.i0;
         for (int j = 0; j < s.ntiles; ++j, ++tt) {
           const int z = s.dec ? i * P.g + s.c : s.c;  // TMA z: group, or sample*g + group
-          const CUtensorMap* mk = s.dec ? &P.tmKd : &P.tmKc;
-          const CUtensorMap* mv = s.dec ? &P.tmVd : &P.tmVc;
-          const uint64_t pol = s.dec ? pol_d : pol_c;
           const int st = tt % NST;
           tc::mbar_wait(tc::smem_u32(&kv_empty[st]), ((tt / NST) & 1) ^ 1);
           const uint32_t bar = tc::smem_u32(&kv_full[st]);
@@ -443,9 +408,6 @@ __global__ void __launch_bounds__(bif::kThreads, 1)
     }
   } else if (warp == 1) {
     // ============================ MMA issuer ==============================
-    // QK(u) issues as soon as its K tile, q and an S slot are ready; PV(v) as
-    // soon as P(v) (and, for a segment's first tile, a free O buffer) is
-    // ready — whichever comes first.
     if (lane == 0) {
       const uint32_t q_addr = tc::smem_u32(sm_q);
       const uint32_t p_addr = tc::smem_u32(sm_p);
@@ -525,18 +487,14 @@ __global__ void __launch_bounds__(bif::kThreads, 1)
         if (!progressed) __nanosleep(20);
       }
     }
-  } else if (warp >= 4) {
-    // ================= softmax + epilogue + merge (8 warps) =================
+  } else if (warp >= 4 && warp < EPI0) {
+    // ========================= softmax (NSW warps) ==========================
     const int sw = warp - 4;
     const int quad = warp & 3;
-    const int half = sw >> 2;
-    const int col0 = half * CPT;
+    const int col0 = (sw >> 2) * CPT;
     const int pos = quad * 32 + lane;
     const uint32_t lane_addr = (uint32_t)(quad * 32) << 16;
     const float sl2 = P.scale_log2;
-    const int R = P.b * P.p;
-    int* sm_len = reinterpret_cast<int*>(sm_l);  // per-segment sample lengths (tile loop only)
-    int* sm_gr = reinterpret_cast<int*>(sm_red); // per-segment output rows (epilogue only)
     uint32_t u = 0, sg = 0, cur = 0;
     unsigned long long* tr = P.trace ? P.trace + (size_t)blockIdx.x * kTraceSlots : nullptr;
     int ntr = 0;
@@ -551,7 +509,7 @@ __global__ void __launch_bounds__(bif::kThreads, 1)
       float l_part[CPT];
 #pragma unroll
       for (int n = 0; n < CPT; ++n) l_part[n] = 0.f;
-      // running max of every column starts unset (-inf); decode lengths of the chunk's samples
+      // running max of every column starts unset (-inf); decode lengths of the chunk
       if (quad == 0 && lane == 0) {
 #pragma unroll
         for (int n = 0; n < CPT; ++n) sm_mrun[cur * N + col0 + n] = kNegInf;
@@ -560,7 +518,7 @@ __global__ void __launch_bounds__(bif::kThreads, 1)
         const int i = s.rc * P.spc + sw * 32 + lane;
         sm_len[sw * 32 + lane] = i < P.b ? dec_len(P, i) : 0;
       }
-      tc::named_bar_sync(2, 256);
+      tc::named_bar_sync(2, 32 * NSW);
       int t = s.t0, il = s.i0 - s.rc * P.spc;  // tile index, sample within the chunk
       const int ntl = s.dec ? P.ntile_d : P.ntile_c;
       for (int j = 0; j < s.ntiles; ++j, ++u) {
@@ -574,7 +532,7 @@ __global__ void __launch_bounds__(bif::kThreads, 1)
         tc::tc_fence_after();
         if (j == 0) stamp(s.dec ? 3 : 2);
         float x[CPT];
-        tmem_ld_cols2<CPT>(tS + slot * N + col0 + lane_addr, reinterpret_cast<uint32_t*>(x));
+        tmem_ld_cols<CPT>(tS + slot * N + col0 + lane_addr, reinterpret_cast<uint32_t*>(x));
         tc::tmem_ld_wait();
         tc::tc_fence_before();
         __syncwarp();
@@ -590,15 +548,14 @@ __global__ void __launch_bounds__(bif::kThreads, 1)
           x[n] = vc ? fmaf(x[n], sl2, -mref) : kNegInf;
           need |= vc && (mo == kNegInf || x[n] > kTh);
         }
-        if (tc::named_bar_or(1, 256, need)) {
+        if (tc::named_bar_or(1, 32 * NSW, need)) {
           // ---- slow path: exact max of the tile's valid columns, new m_run ----
-          if (col0 < cv1 && col0 + CPT > cv0) {  // warp-uniform: this half has valid columns
-            if (cv1 - cv0 >= 16) {
-              // butterfly transpose-reduce: lane l ends with the max of column (l % CPT)
+          if (col0 < cv1 && col0 + CPT > cv0) {  // warp-uniform: this warp has valid columns
+            if (cv1 - cv0 >= CPT) {
               float v[CPT];
 #pragma unroll
               for (int n = 0; n < CPT; ++n) v[n] = x[n];
-              warp_colmax<CPT>(v, lane);
+              warp_col_reduce<CPT, true>(v, lane);
               if (lane < CPT) sm_red[quad * N + col0 + lane] = v[0];
             } else {
 #pragma unroll
@@ -613,7 +570,7 @@ __global__ void __launch_bounds__(bif::kThreads, 1)
               }
             }
           }
-          tc::named_bar_sync(2, 256);
+          tc::named_bar_sync(2, 32 * NSW);
           float* mnext = sm_mrun + (cur ^ 1) * N + col0;
           bool grew = false;
 #pragma unroll
@@ -634,7 +591,7 @@ __global__ void __launch_bounds__(bif::kThreads, 1)
             }
             if (quad == 0 && lane == 0) mnext[n] = mnew;
           }
-          if (tc::named_bar_or(1, 256, grew)) {
+          if (tc::named_bar_or(1, 32 * NSW, grew)) {
             // O^T holds earlier tiles of this segment: wait for PV(u-1), rescale
             const uint32_t pv = u - 1;
             tc::mbar_wait(tc::smem_u32(&p_empty[pv & 1]), (pv >> 1) & 1);
@@ -655,7 +612,7 @@ __global__ void __launch_bounds__(bif::kThreads, 1)
             tc::tmem_st_wait();
             tc::tc_fence_before();
           }
-          tc::named_bar_sync(2, 256);
+          tc::named_bar_sync(2, 32 * NSW);
           cur ^= 1;
         }
         // ---- P = 2^x (bf16) into shared memory; row sums of the SAME bf16
@@ -684,71 +641,58 @@ __global__ void __launch_bounds__(bif::kThreads, 1)
           ++il;
         }
       }
-      // ------------------------- segment epilogue -------------------------
+      // ---- hand the segment's row sums / max to the epilogue warps ----
       stamp(4);
-      // row sums over the 32 positions of this warp (lane l -> column l % CPT)
-      warp_colsum<CPT>(l_part, lane);
-      tc::named_bar_sync(2, 256);  // sm_len reads done; sm_red free
-      if (lane < CPT) sm_l[quad * N + col0 + lane] = l_part[0];
-      if (sw * 32 + lane < N) {
-        const int r = s.rc * N + sw * 32 + lane;
-        sm_gr[sw * 32 + lane] = r < R ? (r / P.p) * P.h + s.c * P.p + (r % P.p) : -1;
-      }
-      tc::named_bar_sync(2, 256);
-      stamp(8);
+      warp_col_reduce<CPT, false>(l_part, lane);  // lane l: column l of this warp, over 32 positions
+      tc::mbar_wait(tc::smem_u32(&e_empty[ob]), ((sg >> 1) & 1) ^ 1);
+      if (lane < CPT) sm_l[(ob * 4 + quad) * N + col0 + lane] = l_part[0];
+      if (quad == 0 && lane < CPT) sm_mfin[ob * N + col0 + lane] = sm_mrun[cur * N + col0 + lane];
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(tc::smem_u32(&e_full[ob]));
+      tc::named_bar_sync(2, 32 * NSW);  // sm_mrun / sm_len reads of this segment done
+      w = s.next;
+    }
+    stamp(7);
+  } else if (warp >= EPI0) {
+    // ===================== epilogue warpgroup (4 warps) =====================
+    // O^T lanes are d = 32*(warp%4) + lane; columns are the chunk's rows.
+    const int quad = warp & 3;
+    const int d = quad * 32 + lane;
+    const int et = threadIdx.x - 32 * EPI0;  // 0..127
+    const uint32_t lane_addr = (uint32_t)(quad * 32) << 16;
+    uint32_t sg = 0;
+    for (long long w = 0; w < nw; ++sg) {
+      const Seg s = seg_at(P, rg, w);
+      const uint32_t ob = sg & 1;
       tc::mbar_wait(tc::smem_u32(&o_full[ob]), (sg >> 1) & 1);
       tc::tc_fence_after();
-      stamp(9);
 #pragma unroll
-      for (int n = 0; n < CPT; n += 8) {
-        uint32_t orr[8];
-        tc::tmem_ld<8>(tOb + col0 + n + lane_addr, orr);
+      for (int n = 0; n < N; n += 16) {
+        uint32_t orr[16];
+        tc::tmem_ld<16>(tO + ob * N + n + lane_addr, orr);
         tc::tmem_ld_wait();
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const int gr = sm_gr[col0 + n + e];
-          if (gr >= 0) P.ws_o[((size_t)gr * P.S + s.slot) * kD + pos] = __uint_as_float(orr[e]);
+        for (int e = 0; e < 16; ++e) {
+          const int gr = row_of(P, s.c, s.rc, n + e);
+          if (gr >= 0) P.ws_o[((size_t)gr * P.S + s.slot) * kD + d] = __uint_as_float(orr[e]);
         }
       }
       tc::tc_fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(tc::smem_u32(&o_empty[ob]));
-      if (sw < 2) {
-        const int col = sw * 32 + lane;
-        const int gr = col < N ? sm_gr[col] : -1;
+      tc::mbar_wait(tc::smem_u32(&e_full[ob]), (sg >> 1) & 1);
+      if (et < N) {
+        const int gr = row_of(P, s.c, s.rc, et);
         if (gr >= 0) {
-          const float Lr = sm_l[col] + sm_l[N + col] + sm_l[2 * N + col] + sm_l[3 * N + col];
-          float2* ml = reinterpret_cast<float2*>(P.ws_ml) + (size_t)gr * P.S + s.slot;
-          *ml = make_float2(sm_mrun[cur * N + col], Lr);
+          const float* lb = sm_l + ob * 4 * N;
+          const float Lr = lb[et] + lb[N + et] + lb[2 * N + et] + lb[3 * N + et];
+          reinterpret_cast<float2*>(P.ws_ml)[(size_t)gr * P.S + s.slot] = make_float2(sm_mfin[ob * N + et], Lr);
         }
       }
-      stamp(10);
-      // ---- arrive at the (group, row chunk) counter; the last arrival merges ----
-      tc::named_bar_sync(2, 256);
-      stamp(11);
-      const int cidx = s.c * P.nrc + s.rc;
-      if (threadIdx.x == 128) {
-        const int nparts = ctx_parts(P, s.c, s.rc) + dec_parts(P, s.c, s.rc);
-        __threadfence();
-        const unsigned old = atomicAdd(&P.counters[cidx], 1u);
-        const int last = old == (unsigned)(nparts - 1);
-        if (last) {
-          __threadfence();
-          P.counters[cidx] = 0u;  // self-reset for the next call
-        }
-        sm_flag[0] = last;
-        sm_flag[1] = ctx_parts(P, s.c, s.rc);
-        sm_flag[2] = dec_parts(P, s.c, s.rc);
-      }
-      tc::named_bar_sync(2, 256);
-      stamp(sm_flag[0] ? 6 : 5);
-      if (sm_flag[0]) {
-        __threadfence();
-        merge_rows(P, sm_gr, N, sm_flag[1], sm_flag[2], sw, lane);
-      }
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(tc::smem_u32(&e_empty[ob]));
       w = s.next;
     }
-    stamp(7);
   }
   tc::tc_fence_before();
   __syncthreads();
@@ -756,6 +700,60 @@ __global__ void __launch_bounds__(bif::kThreads, 1)
     tc::tc_fence_after();
     tc::tmem_dealloc(tmem, TMEM_COLS);
   }
+}
+
+// ----------------------------------------------------------------------------
+// LSE merge (PDL-chained after bif_tc_kernel): one warp per output row joins
+// its context partials [0, nctx) and decode partials [Sc, Sc + ndec).
+// ----------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) bif_merge_kernel(const __grid_constant__ BifTcParams P) {
+  pdl_wait();  // the streaming kernel's partials are complete and visible
+  const int gr = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (gr >= P.b * P.h) return;
+  const int i = gr / P.h, j = gr - (gr / P.h) * P.h;
+  const int c = j / P.p;
+  const int rc = (i * P.p + (j - c * P.p)) / P.N;
+  const int nctx = bif::ctx_parts(P, c, rc);
+  const int n = nctx + bif::dec_parts(P, c, rc);
+  const float2* ml = reinterpret_cast<const float2*>(P.ws_ml) + (size_t)gr * P.S;
+  const float* obuf = P.ws_o + (size_t)gr * P.S * bif::kD;
+  float M = kNegInf;
+  for (int q = lane; q < n; q += 32) M = fmaxf(M, __ldcg(ml + (q < nctx ? q : P.Sc + q - nctx)).x);
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
+  const float Ms = (M == kNegInf) ? 0.f : M;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  float Lsum = 0.f;
+  for (int q0 = 0; q0 < n; q0 += 8) {
+    float2 mv[8];
+    float4 ov[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int q = q0 + k;
+      if (q < n) {
+        const int sl = q < nctx ? q : P.Sc + q - nctx;
+        mv[k] = __ldcg(ml + sl);
+        ov[k] = __ldcg(reinterpret_cast<const float4*>(obuf + (size_t)sl * bif::kD) + lane);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      if (q0 + k < n) {
+        const float wgt = ex2(mv[k].x - Ms);
+        Lsum = fmaf(wgt, mv[k].y, Lsum);
+        acc.x = fmaf(wgt, ov[k].x, acc.x);
+        acc.y = fmaf(wgt, ov[k].y, acc.y);
+        acc.z = fmaf(wgt, ov[k].z, acc.z);
+        acc.w = fmaf(wgt, ov[k].w, acc.w);
+      }
+    }
+  }
+  const float inv = 1.f / Lsum;
+  const uint2 packed = make_uint2(pack_bf16x2(acc.x * inv, acc.y * inv),
+                                  pack_bf16x2(acc.z * inv, acc.w * inv));
+  *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(P.out) + (size_t)gr * bif::kD + lane * 4) = packed;
+  if (P.lse && lane == 0) P.lse[gr] = (M + lg2(Lsum)) * kLn2;
 }
 
 }  // namespace ba

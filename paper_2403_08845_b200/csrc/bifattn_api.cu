@@ -110,15 +110,6 @@ struct Plan {
   int launches = 0;
 };
 
-// Completion counters live at the start of every plan's workspace, sized for
-// the most (group, row chunk) pairs any plan can use, so a call of any plan
-// leaves them zero for the next one.
-size_t counter_bytes(const ba_problem_t* pr) {
-  // one per (group, row chunk); row chunks are >= 16 rows (or >= p rows)
-  const long long n = (long long)pr->g * (((long long)pr->b * (pr->h / pr->g) + 15) / 16 + 1);
-  return ((size_t)n * sizeof(unsigned) + 255) & ~(size_t)255;
-}
-
 int pick_rb(int rows) { return rows >= 4 ? 4 : (rows >= 2 ? 2 : 1); }
 
 int validate(const ba_problem_t* pr) {
@@ -172,7 +163,7 @@ int make_plan(const ba_problem_t* pr, int sms, bool replicated, Plan* pl) {
     P.tc_T = P.tc_Tc + (long long)g * b * P.tc_ntile_d;
     P.tc_G = (int)(P.tc_T < sms ? P.tc_T : sms);
     const long long Td = P.tc_T - P.tc_Tc;
-    const int avail = 227 * 1024 - ba::bif::smem_fixed(tcN);
+    const int avail = 227 * 1024 - ba::bif::smem_fixed(tcN);  // dynamic smem is 1 KB aligned
     P.tc_nst = avail / ba::bif::kStageBytes;
     if (P.tc_nst > 4) P.tc_nst = 4;
     P.tc_smem = P.tc_nst * ba::bif::kStageBytes + ba::bif::smem_fixed(tcN);
@@ -200,11 +191,11 @@ int make_plan(const ba_problem_t* pr, int sms, bool replicated, Plan* pl) {
     if (P.S < 1) P.S = 1;
     const size_t rows = (size_t)b * h;
     P.off_cnt = 0;
-    P.off_o = counter_bytes(pr);
+    P.off_o = 0;
     P.off_ml = P.off_o + rows * P.S * 128 * sizeof(float);
     P.ws_bytes = P.off_ml + rows * P.S * 2 * sizeof(float);
     P.ws_bytes = (P.ws_bytes + 255) & ~(size_t)255;
-    P.launches = 1;
+    P.launches = 2;
     *pl = P;
     return BA_OK;
   }
@@ -249,7 +240,7 @@ int make_plan(const ba_problem_t* pr, int sms, bool replicated, Plan* pl) {
   P.S = P.nsc + P.nsd;
   if (P.S < 1) P.S = 1;
   const size_t rows = (size_t)b * h;
-  P.off_o = counter_bytes(pr);
+  P.off_o = 0;
   P.off_ml = P.off_o + rows * P.S * P.D * sizeof(float);
   P.ws_bytes = P.off_ml + rows * P.S * 2 * sizeof(float);
   P.ws_bytes = (P.ws_bytes + 255) & ~(size_t)255;
@@ -312,7 +303,7 @@ int make_tmap_3d(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uin
 }
 
 template <int N>
-int launch_bif_tc_n(const ba::BifTcParams& bp, int smem, LaunchRec& rec) {
+int launch_bif_tc_n(const ba::BifTcParams& bp, int smem, uint32_t flags, LaunchRec& rec) {
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [&] {
@@ -324,12 +315,35 @@ int launch_bif_tc_n(const ba::BifTcParams& bp, int smem, LaunchRec& rec) {
     return BA_ECUDA;
   }
   rec.begin();
-  ba::bif_tc_kernel<N><<<bp.G, ba::bif::kThreads, smem, rec.st>>>(bp);
+  ba::bif_tc_kernel<N><<<bp.G, ba::bif::threads(N), smem, rec.st>>>(bp);
+  int rc = rec.end();
+  if (rc) return rc;
+  // LSE merge, chained with programmatic dependent launch: it is scheduled as
+  // the streaming kernel's CTAs retire and waits (griddepcontrol.wait) for
+  // its completion before reading the partials.
+  const int rows = bp.b * bp.h;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((rows + 7) / 8);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = rec.st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = (flags & BA_FLAG_NO_PDL) ? 0 : 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  rec.begin();
+  cudaError_t e = cudaLaunchKernelEx(&cfg, ba::bif_merge_kernel, bp);
+  if (e != cudaSuccess) {
+    g_last_cuda_error = (int)e;
+    rec.end();
+    return BA_ECUDA;
+  }
   return rec.end();
 }
 
-// Single-launch tcgen05 step.  Replicated baseline: Kc = Vc = nullptr, Kd/Vd
-// are the replicated caches [b][g][mc+md_cap][d].
+// tcgen05 step: streaming kernel + PDL-chained merge.  Replicated baseline:
+// Kc = Vc = nullptr, Kd/Vd are the replicated caches [b][g][mc+md_cap][d].
 int run_tc(const ba_problem_t* pr, const Plan& P, const void* q, const void* Kc, const void* Vc,
            const void* Kd, const void* Vd, const int32_t* lens, void* out, float* lse, void* ws,
            float scale_log2, cudaStream_t st) {
@@ -355,6 +369,7 @@ int run_tc(const ba_problem_t* pr, const Plan& P, const void* q, const void* Kc,
   bp.lens = lens;
   bp.b = pr->b; bp.h = pr->h; bp.g = pr->g; bp.p = p; bp.mc = pr->mc;
   bp.dec_cap = P.dec_cap; bp.lens_offset = P.lens_offset;
+  bp.N = P.tc_N;
   bp.nrc = P.tc_nrc; bp.ntile_c = P.tc_ntile_c; bp.ntile_d = P.tc_ntile_d;
   bp.spc = P.tc_N / p;
   bp.Tc = P.tc_Tc; bp.Td = P.tc_T - P.tc_Tc; bp.G = P.tc_G; bp.nst = P.tc_nst;
@@ -362,16 +377,15 @@ int run_tc(const ba_problem_t* pr, const Plan& P, const void* q, const void* Kc,
   bp.S = P.S; bp.Sc = P.tc_Sc;
   bp.ws_o = reinterpret_cast<float*>(static_cast<char*>(ws) + P.off_o);
   bp.ws_ml = reinterpret_cast<float*>(static_cast<char*>(ws) + P.off_ml);
-  bp.counters = reinterpret_cast<unsigned*>(static_cast<char*>(ws) + P.off_cnt);
   bp.out = out;
   bp.lse = lse;
   bp.trace = static_cast<unsigned long long*>(g_trace);
   LaunchRec rec(st);
   switch (P.tc_N) {
-    case 16: return launch_bif_tc_n<16>(bp, P.tc_smem, rec);
-    case 32: return launch_bif_tc_n<32>(bp, P.tc_smem, rec);
-    case 48: return launch_bif_tc_n<48>(bp, P.tc_smem, rec);
-    case 64: return launch_bif_tc_n<64>(bp, P.tc_smem, rec);
+    case 16: return launch_bif_tc_n<16>(bp, P.tc_smem, pr->flags, rec);
+    case 32: return launch_bif_tc_n<32>(bp, P.tc_smem, pr->flags, rec);
+    case 48: return launch_bif_tc_n<48>(bp, P.tc_smem, pr->flags, rec);
+    case 64: return launch_bif_tc_n<64>(bp, P.tc_smem, pr->flags, rec);
   }
   return BA_EINVAL;
 }
@@ -591,7 +605,7 @@ const char* ba_plan_string(const ba_problem_t* prob) {
   if (P.tc)
     snprintf(g_plan_buf, sizeof g_plan_buf,
              "fused_tc(N=%d,nrc=%d,ctx_tiles=%lld,dec_tiles=%lld,ctas=%d,stages=%d,slots=%d+%d,"
-             "smem=%d) launches=1 ws=%zu",
+             "smem=%d) launches=2 ws=%zu",
              P.tc_N, P.tc_nrc, P.tc_Tc, P.tc_T - P.tc_Tc, P.tc_G, P.tc_nst, P.tc_Sc, P.tc_Sd,
              P.tc_smem, P.ws_bytes);
   else
@@ -611,6 +625,7 @@ const char* ba_launch_name(const ba_problem_t* prob, int k) {
   int n = 0;
   if (P.tc) {
     names[n++] = "fused_tc";
+    names[n++] = "merge_tc";
   } else {
     if (P.ctx_mode == 1) names[n++] = "ctx_fma";
     if (P.nsd > 0) names[n++] = "dec_fma";
