@@ -83,7 +83,7 @@ constexpr int kTraceSlots = 64;
 
 // softmax warpgroups: keep columns per softmax thread <= 32
 __host__ __device__ constexpr int softmax_wgs(int N) { return N <= 32 ? 1 : 2; }
-__host__ __device__ constexpr int threads(int N) { return 32 * (8 + 4 * softmax_wgs(N)); }
+__host__ __device__ constexpr int threads(int swg) { return 32 * (8 + 4 * swg); }
 
 __host__ __device__ constexpr int p_atom(int N) { return (N % 64 == 0) ? 64 : ((N % 32 == 0) ? 32 : 16); }
 __host__ __device__ constexpr int p_layout(int N) {
@@ -279,11 +279,10 @@ BA_DEVINL void warp_col_reduce(float* v, int lane) {
   }
 }
 
-template <int N>
-__global__ void __launch_bounds__(bif::threads(N), 1)
+template <int N, int SWG>
+__global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
     bif_tc_kernel(const __grid_constant__ BifTcParams P) {
   using namespace bif;
-  constexpr int SWG = softmax_wgs(N);        // softmax warpgroups
   constexpr int NSW = 4 * SWG;               // softmax warps
   constexpr int CPT = N / SWG;               // columns per softmax thread
   constexpr int EPI0 = 4 + NSW;              // first epilogue warp

@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <mutex>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "../../include/bifattn.h"
@@ -302,12 +303,12 @@ int make_tmap_3d(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uin
   return BA_OK;
 }
 
-template <int N>
+template <int N, int SWG>
 int launch_bif_tc_n(const ba::BifTcParams& bp, int smem, uint32_t flags, LaunchRec& rec) {
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [&] {
-    attr_err = cudaFuncSetAttribute(ba::bif_tc_kernel<N>,
+    attr_err = cudaFuncSetAttribute(ba::bif_tc_kernel<N, SWG>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
   });
   if (attr_err != cudaSuccess) {
@@ -315,7 +316,7 @@ int launch_bif_tc_n(const ba::BifTcParams& bp, int smem, uint32_t flags, LaunchR
     return BA_ECUDA;
   }
   rec.begin();
-  ba::bif_tc_kernel<N><<<bp.G, ba::bif::threads(N), smem, rec.st>>>(bp);
+  ba::bif_tc_kernel<N, SWG><<<bp.G, ba::bif::threads(SWG), smem, rec.st>>>(bp);
   int rc = rec.end();
   if (rc) return rc;
   // LSE merge, chained with programmatic dependent launch: it is scheduled as
@@ -381,11 +382,19 @@ int run_tc(const ba_problem_t* pr, const Plan& P, const void* q, const void* Kc,
   bp.lse = lse;
   bp.trace = static_cast<unsigned long long*>(g_trace);
   LaunchRec rec(st);
-  switch (P.tc_N) {
-    case 16: return launch_bif_tc_n<16>(bp, P.tc_smem, pr->flags, rec);
-    case 32: return launch_bif_tc_n<32>(bp, P.tc_smem, pr->flags, rec);
-    case 48: return launch_bif_tc_n<48>(bp, P.tc_smem, pr->flags, rec);
-    case 64: return launch_bif_tc_n<64>(bp, P.tc_smem, pr->flags, rec);
+  // softmax warpgroups (override for experiments: BIFATTN_SWG=1|2)
+  static const int swg_env = [] {
+    const char* e = getenv("BIFATTN_SWG");
+    return e ? atoi(e) : 0;
+  }();
+  const int swg = (swg_env == 1 || swg_env == 2) ? swg_env : ba::bif::softmax_wgs(P.tc_N);
+  switch (P.tc_N * 4 + swg) {
+    case 16 * 4 + 1: return launch_bif_tc_n<16, 1>(bp, P.tc_smem, pr->flags, rec);
+    case 16 * 4 + 2: return launch_bif_tc_n<16, 2>(bp, P.tc_smem, pr->flags, rec);
+    case 32 * 4 + 1: return launch_bif_tc_n<32, 1>(bp, P.tc_smem, pr->flags, rec);
+    case 32 * 4 + 2: return launch_bif_tc_n<32, 2>(bp, P.tc_smem, pr->flags, rec);
+    case 48 * 4 + 2: return launch_bif_tc_n<48, 2>(bp, P.tc_smem, pr->flags, rec);
+    case 64 * 4 + 2: return launch_bif_tc_n<64, 2>(bp, P.tc_smem, pr->flags, rec);
   }
   return BA_EINVAL;
 }
