@@ -8,11 +8,12 @@
 //                      Vc[c] (no batch axis) against a run
 //                      of 128-position context tiles — each context tile is
 //                      read from HBM once for all b samples;
-//   decode segments:   the same row chunk against the 128-position tiles of its
-//                      samples' own Kd[i][c]/Vd[i][c],
-//                      sample after sample; a tile of sample i only feeds the
-//                      p columns of sample i (others masked), positions masked
-//                      at lens[i];
+//   decode segments:   the rows of sample i for a block of gpc = N/p groups
+//                      against the 128-position tiles of Kd[i][c]/Vd[i][c]
+//                      (PAPER.md:255, :267), group after group — i.e. in
+//                      memory order of the [b][g][md][d] cache; a tile of
+//                      group c only feeds the p columns of group c (others
+//                      masked), positions masked at lens[i];
 //   merge:             every row's partials (m, l, o) joined with one
 //                      log-sum-exp — the single softmax over S_c ⊕ S_d
 //                       split at mc and summed (Eq. 4).
@@ -40,12 +41,12 @@
 // O^T only for columns whose max actually grew.  Same softmax; P <= 2^kTh.
 //
 // Work split: context tiles fc = (c*nrc + rc)*ntile_c + t in [0, Tc) and
-// decode tiles fd = (c*b + i)*ntile_d + t in [0, Td).  CTA k of G takes
-// context tiles [k*Tc/G, (k+1)*Tc/G) and then decode tiles [k*Td/G,
-// (k+1)*Td/G): every CTA streams the same number of 64 KB tiles (+-1 of each
-// kind).  A maximal run of tiles of one (c, rc) — context, or decode tiles of
-// the chunk's samples — is a segment and writes one partial (m, l, o) for
-// every row of the chunk to its workspace slot (context slots [0, Sc),
+// decode tiles fd = (i*g + c)*ntile_d + t in [0, Td) (memory order).  CTA k
+// of G takes context tiles [k*Tc/G, (k+1)*Tc/G) and then decode tiles
+// [k*Td/G, (k+1)*Td/G): every CTA streams the same number of 64 KB tiles (+-1
+// of each kind).  A maximal run of tiles of one context chunk (c, rc) or one
+// decode chunk (i, cb) is a segment and writes one partial (m, l, o) for
+// every row of its chunk to its workspace slot (context slots [0, Sc),
 // decode slots [Sc, S)).
 #pragma once
 #include "common.cuh"
@@ -57,12 +58,15 @@ struct BifTcParams {
   CUtensorMap tmKc, tmVc;  // Kc/Vc as 3D (d, mc, g), box (64, 128, 1), SW128
   CUtensorMap tmQc;        // q as 3D (d, h, b), box (64, p, N/p), SW128
   CUtensorMap tmKd, tmVd;  // Kd/Vd as 3D (d, dec_stride, b*g), box (64, 128, 1)
+  CUtensorMap tmQd;        // q as 3D (d, h, b), box (64, min(N, h), 1), SW128
   const int32_t* lens;
   int b, h, g, p, mc;
   int dec_cap, lens_offset;  // decode length = lens_offset + clamp(lens[i], 0, dec_cap)
   int N;                     // rows per chunk (== template N)
   int nrc, ntile_c, ntile_d;
-  int spc;                   // samples per row chunk = N / p
+  int spc;                   // samples per context row chunk = N / p
+  int gpc, ndc;              // groups per decode chunk = N / p; decode chunks per sample
+  int qd_rows;               // rows of the decode q box = min(N, h)
   long long Tc, Td;          // context tiles, decode tiles
   int G, nst;
   float scale_log2;
@@ -82,7 +86,7 @@ constexpr float kTh = 8.0f;         // fast-path slack (log2 units)
 constexpr int kTraceSlots = 64;
 
 // softmax warpgroups: keep columns per softmax thread <= 32
-__host__ __device__ constexpr int softmax_wgs(int N) { return N <= 32 ? 1 : 2; }
+__host__ __device__ constexpr int softmax_wgs(int N) { return N > 0 ? 2 : 2; }  // measured: 2 beats 1 at N=16/32
 __host__ __device__ constexpr int threads(int swg) { return 32 * (8 + 4 * swg); }
 
 __host__ __device__ constexpr int p_atom(int N) { return (N % 64 == 0) ? 64 : ((N % 32 == 0) ? 32 : 16); }
@@ -112,9 +116,9 @@ __host__ __device__ inline int part_rank(long long a, long long f, long long T, 
 
 struct Seg {
   bool dec;        // decode segment?
-  int c, rc;       // group, row chunk
-  int t0, i0;      // first tile's position-tile index and (decode) sample
-  long long f;     // first flat tile (context or decode space) of this part
+  int c, rc;       // context: group, row chunk
+  int i, cb;       // decode: sample, group block (groups [cb*gpc, (cb+1)*gpc))
+  int t0, c0;      // first tile's position-tile index and (decode) group
   int ntiles;      // tiles in this CTA's part of the segment
   int slot;        // workspace slot of this CTA's partial
   long long next;  // work index (CTA work order) after this segment part
@@ -142,15 +146,15 @@ BA_DEVINL Range my_range(const BifTcParams& P) {
   return r;
 }
 
-// First / one-past-last decode tile of chunk (c, rc).
-__host__ __device__ inline long long dec_chunk_begin(long long b, long long spc, long long ntd,
-                                                     int c, int rc) {
-  return ((long long)c * b + (long long)rc * spc) * ntd;
+// First / one-past-last decode tile of chunk (i, cb).
+__host__ __device__ inline long long dec_chunk_begin(long long g, long long gpc, long long ntd,
+                                                     int i, int cb) {
+  return ((long long)i * g + (long long)cb * gpc) * ntd;
 }
-__host__ __device__ inline long long dec_chunk_end(long long b, long long spc, long long ntd, int c,
-                                                   int rc) {
-  const long long i1 = (long long)(rc + 1) * spc < b ? (long long)(rc + 1) * spc : b;
-  return ((long long)c * b + i1) * ntd;
+__host__ __device__ inline long long dec_chunk_end(long long g, long long gpc, long long ntd, int i,
+                                                   int cb) {
+  const long long c1 = (long long)(cb + 1) * gpc < g ? (long long)(cb + 1) * gpc : g;
+  return ((long long)i * g + c1) * ntd;
 }
 
 BA_DEVINL Seg seg_at(const BifTcParams& P, const Range& rg, long long w) {
@@ -163,23 +167,23 @@ BA_DEVINL Seg seg_at(const BifTcParams& P, const Range& rg, long long w) {
     s.dec = false;
     s.c = (int)(seg / P.nrc);
     s.rc = (int)(seg % P.nrc);
+    s.i = s.cb = 0;
     s.t0 = (int)(f - seg * P.ntile_c);
-    s.i0 = 0;
-    s.f = f;
+    s.c0 = s.c;
     s.ntiles = (int)(fend - f);
     s.slot = part_rank(seg * P.ntile_c, f, P.Tc, P.G);
     s.next = w + (fend - f);
   } else {
     const long long f = rg.fd0 + (w - nc);
-    const long long cb = f / P.ntile_d;  // c*b + i
+    const long long ic = f / P.ntile_d;  // i*g + c
     s.dec = true;
-    s.c = (int)(cb / P.b);
-    s.i0 = (int)(cb % P.b);
-    s.rc = s.i0 / P.spc;
-    s.t0 = (int)(f - cb * P.ntile_d);
-    const long long a = dec_chunk_begin(P.b, P.spc, P.ntile_d, s.c, s.rc);
-    const long long fend = min(dec_chunk_end(P.b, P.spc, P.ntile_d, s.c, s.rc), rg.fd1);
-    s.f = f;
+    s.i = (int)(ic / P.g);
+    s.c0 = (int)(ic % P.g);
+    s.cb = s.c0 / P.gpc;
+    s.c = s.rc = 0;
+    s.t0 = (int)(f - ic * P.ntile_d);
+    const long long a = dec_chunk_begin(P.g, P.gpc, P.ntile_d, s.i, s.cb);
+    const long long fend = min(dec_chunk_end(P.g, P.gpc, P.ntile_d, s.i, s.cb), rg.fd1);
     s.ntiles = (int)(fend - f);
     s.slot = P.Sc + part_rank(a, f, P.Td, P.G);
     s.next = w + (fend - f);
@@ -187,25 +191,29 @@ BA_DEVINL Seg seg_at(const BifTcParams& P, const Range& rg, long long w) {
   return s;
 }
 
-// Partials written for the rows of chunk (c, rc).
+// Partials written for context chunk (c, rc) / decode chunk (i, cb).
 __host__ __device__ inline int ctx_parts(const BifTcParams& P, int c, int rc) {
   if (P.Tc == 0) return 0;
   const long long ff = ((long long)c * P.nrc + rc) * P.ntile_c;
   return part_rank(ff, ff + P.ntile_c - 1, P.Tc, P.G) + 1;
 }
-__host__ __device__ inline int dec_parts(const BifTcParams& P, int c, int rc) {
+__host__ __device__ inline int dec_parts(const BifTcParams& P, int i, int cb) {
   if (P.Td == 0) return 0;
-  const long long a = dec_chunk_begin(P.b, P.spc, P.ntile_d, c, rc);
-  const long long e = dec_chunk_end(P.b, P.spc, P.ntile_d, c, rc);
+  const long long a = dec_chunk_begin(P.g, P.gpc, P.ntile_d, i, cb);
+  const long long e = dec_chunk_end(P.g, P.gpc, P.ntile_d, i, cb);
   return part_rank(a, e - 1, P.Td, P.G) + 1;
 }
 
-// output row of column col of chunk (c, rc), or -1 for padding
-BA_DEVINL int row_of(const BifTcParams& P, int c, int rc, int col) {
-  const int r = rc * P.N + col;
+// output row of column col of a segment's chunk, or -1 for padding
+BA_DEVINL int row_of(const BifTcParams& P, const Seg& s, int col) {
+  if (s.dec) {
+    const int j = s.cb * P.gpc * P.p + col;
+    return j < P.h ? s.i * P.h + j : -1;
+  }
+  const int r = s.rc * P.N + col;
   if (r >= P.b * P.p) return -1;
   const int i = r / P.p;
-  return i * P.h + c * P.p + (r - i * P.p);
+  return i * P.h + s.c * P.p + (r - i * P.p);
 }
 }  // namespace bif
 
@@ -349,6 +357,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
     tc::prefetch_tmap(&P.tmQc);
     tc::prefetch_tmap(&P.tmKd);
     tc::prefetch_tmap(&P.tmVd);
+    tc::prefetch_tmap(&P.tmQd);
   }
   if (warp == 2) {
     tc::tmem_alloc(tc::smem_u32(tmem_holder), TMEM_COLS);
@@ -378,16 +387,22 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
         tc::mbar_wait(tc::smem_u32(&q_empty[qbuf]), ((sg >> 1) & 1) ^ 1);
         const uint32_t qb = tc::smem_u32(&q_full[qbuf]);
         const uint32_t qdst = tc::smem_u32(sm_q + qbuf * QB);
-        tc::mbar_arrive_expect_tx(qb, 2 * N * 128);
-        tc::tma_load_3d(qdst, &P.tmQc, qb, 0, s.c * P.p, s.rc * P.spc);
-        tc::tma_load_3d(qdst + N * 128, &P.tmQc, qb, 64, s.c * P.p, s.rc * P.spc);
+        if (!s.dec) {
+          tc::mbar_arrive_expect_tx(qb, 2 * N * 128);
+          tc::tma_load_3d(qdst, &P.tmQc, qb, 0, s.c * P.p, s.rc * P.spc);
+          tc::tma_load_3d(qdst + N * 128, &P.tmQc, qb, 64, s.c * P.p, s.rc * P.spc);
+        } else {
+          tc::mbar_arrive_expect_tx(qb, 2 * P.qd_rows * 128);
+          tc::tma_load_3d(qdst, &P.tmQd, qb, 0, s.cb * P.gpc * P.p, s.i);
+          tc::tma_load_3d(qdst + N * 128, &P.tmQd, qb, 64, s.cb * P.gpc * P.p, s.i);
+        }
         const CUtensorMap* mk = s.dec ? &P.tmKd : &P.tmKc;
         const CUtensorMap* mv = s.dec ? &P.tmVd : &P.tmVc;
         const uint64_t pol = s.dec ? pol_d : pol_c;
         const int ntl = s.dec ? P.ntile_d : P.ntile_c;
-        int t = s.t0, i = s.i0;
+        int t = s.t0, cg = s.c0;
         for (int j = 0; j < s.ntiles; ++j, ++tt) {
-          const int z = s.dec ? i * P.g + s.c : s.c;  // TMA z: group, or sample*g + group
+          const int z = s.dec ? s.i * P.g + cg : s.c;  // TMA z: group, or sample*g + group
           const int st = tt % NST;
           tc::mbar_wait(tc::smem_u32(&kv_empty[st]), ((tt / NST) & 1) ^ 1);
           const uint32_t bar = tc::smem_u32(&kv_full[st]);
@@ -399,7 +414,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
           tc::tma_load_3d_hint(dst + 49152, mv, bar, 64, t * kBM, z, pol);
           if (++t == ntl) {
             t = 0;
-            ++i;
+            ++cg;
           }
         }
         w = s.next;
@@ -513,17 +528,13 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
 #pragma unroll
         for (int n = 0; n < CPT; ++n) sm_mrun[cur * N + col0 + n] = kNegInf;
       }
-      if (s.dec && sw * 32 + lane < P.spc) {
-        const int i = s.rc * P.spc + sw * 32 + lane;
-        sm_len[sw * 32 + lane] = i < P.b ? dec_len(P, i) : 0;
-      }
+      const int L = s.dec ? dec_len(P, s.i) : P.mc;  // valid positions of the sequence
       tc::named_bar_sync(2, 32 * NSW);
-      int t = s.t0, il = s.i0 - s.rc * P.spc;  // tile index, sample within the chunk
+      int t = s.t0, cl = s.c0 - s.cb * P.gpc;  // tile index, group within the decode chunk
       const int ntl = s.dec ? P.ntile_d : P.ntile_c;
       for (int j = 0; j < s.ntiles; ++j, ++u) {
-        // valid columns [cv0, cv1) and positions [0, L) of this tile
-        const int L = s.dec ? sm_len[il] : P.mc;
-        const int cv0 = s.dec ? il * P.p : 0;
+        // valid columns [cv0, cv1) of this tile
+        const int cv0 = s.dec ? cl * P.p : 0;
         const int cv1 = s.dec ? cv0 + P.p : N;
         const uint32_t slot = u & 1;
         const float* mrun = sm_mrun + cur * N + col0;
@@ -637,7 +648,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
         if (lane == 0) tc::mbar_arrive(tc::smem_u32(&p_full[slot]));
         if (++t == ntl) {
           t = 0;
-          ++il;
+          ++cl;
         }
       }
       // ---- hand the segment's row sums / max to the epilogue warps ----
@@ -648,7 +659,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
       if (quad == 0 && lane < CPT) sm_mfin[ob * N + col0 + lane] = sm_mrun[cur * N + col0 + lane];
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(tc::smem_u32(&e_full[ob]));
-      tc::named_bar_sync(2, 32 * NSW);  // sm_mrun / sm_len reads of this segment done
+      tc::named_bar_sync(2, 32 * NSW);  // sm_mrun reads of this segment done
       w = s.next;
     }
     stamp(7);
@@ -672,7 +683,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
         tc::tmem_ld_wait();
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
-          const int gr = row_of(P, s.c, s.rc, n + e);
+          const int gr = row_of(P, s, n + e);
           if (gr >= 0) P.ws_o[((size_t)gr * P.S + s.slot) * kD + d] = __uint_as_float(orr[e]);
         }
       }
@@ -681,7 +692,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
       if (lane == 0) tc::mbar_arrive(tc::smem_u32(&o_empty[ob]));
       tc::mbar_wait(tc::smem_u32(&e_full[ob]), (sg >> 1) & 1);
       if (et < N) {
-        const int gr = row_of(P, s.c, s.rc, et);
+        const int gr = row_of(P, s, et);
         if (gr >= 0) {
           const float* lb = sm_l + ob * 4 * N;
           const float Lr = lb[et] + lb[N + et] + lb[2 * N + et] + lb[3 * N + et];
@@ -714,7 +725,7 @@ __global__ void __launch_bounds__(256) bif_merge_kernel(const __grid_constant__ 
   const int c = j / P.p;
   const int rc = (i * P.p + (j - c * P.p)) / P.N;
   const int nctx = bif::ctx_parts(P, c, rc);
-  const int n = nctx + bif::dec_parts(P, c, rc);
+  const int n = nctx + bif::dec_parts(P, i, c / P.gpc);
   const float2* ml = reinterpret_cast<const float2*>(P.ws_ml) + (size_t)gr * P.S;
   const float* obuf = P.ws_o + (size_t)gr * P.S * bif::kD;
   float M = kNegInf;

@@ -177,11 +177,12 @@ int make_plan(const ba_problem_t* pr, int sms, bool replicated, Plan* pl) {
       const int n = parts(seg * P.tc_ntile_c, P.tc_ntile_c, P.tc_Tc);
       if (n > sc) sc = n;
     }
-    const int spc = tcN / p;
-    for (int c = 0; P.tc_ntile_d && c < g; ++c) {
-      for (int rc = 0; rc < P.tc_nrc; ++rc) {
-        const long long a = ((long long)c * b + (long long)rc * spc) * P.tc_ntile_d;
-        const long long e = ((long long)c * b + std::min<long long>(b, (long long)(rc + 1) * spc)) * P.tc_ntile_d;
+    const int gpc = tcN / p;  // groups per decode chunk
+    const int ndc = (g + gpc - 1) / gpc;
+    for (int i = 0; P.tc_ntile_d && i < b; ++i) {
+      for (int cb = 0; cb < ndc; ++cb) {
+        const long long a = ba::bif::dec_chunk_begin(g, gpc, P.tc_ntile_d, i, cb);
+        const long long e = ba::bif::dec_chunk_end(g, gpc, P.tc_ntile_d, i, cb);
         const int n = parts(a, e - a, Td);
         if (n > sd) sd = n;
       }
@@ -363,6 +364,9 @@ int run_tc(const ba_problem_t* pr, const Plan& P, const void* q, const void* Kc,
     const uint64_t bg = (uint64_t)pr->b * pr->g;
     rc = make_tmap_3d(&bp.tmKd, Kd, d, ds, bg, d * 2, ds * d * 2, 128, 1);
     if (!rc) rc = make_tmap_3d(&bp.tmVd, Vd, d, ds, bg, d * 2, ds * d * 2, 128, 1);
+    if (!rc)
+      rc = make_tmap_3d(&bp.tmQd, q, d, pr->h, pr->b, d * 2, (uint64_t)pr->h * d * 2,
+                        std::min(P.tc_N, pr->h), 1);
   }
   if (!rc && P.tc_Tc == 0)  // replicated baseline: q map for the decode chunks
     rc = make_tmap_3d(&bp.tmQc, q, d, pr->h, pr->b, d * 2, (uint64_t)pr->h * d * 2, p, P.tc_N / p);
@@ -373,6 +377,9 @@ int run_tc(const ba_problem_t* pr, const Plan& P, const void* q, const void* Kc,
   bp.N = P.tc_N;
   bp.nrc = P.tc_nrc; bp.ntile_c = P.tc_ntile_c; bp.ntile_d = P.tc_ntile_d;
   bp.spc = P.tc_N / p;
+  bp.gpc = P.tc_N / p;
+  bp.ndc = (pr->g + bp.gpc - 1) / bp.gpc;
+  bp.qd_rows = std::min(P.tc_N, pr->h);
   bp.Tc = P.tc_Tc; bp.Td = P.tc_T - P.tc_Tc; bp.G = P.tc_G; bp.nst = P.tc_nst;
   bp.scale_log2 = scale_log2;
   bp.S = P.S; bp.Sc = P.tc_Sc;

@@ -35,8 +35,10 @@ def simulate(b, h, g, mc, md, N, sms=148):
     tiles_seen = {}
     writes = {}
 
-    def dec_chunk(c, rc):
-        return (c * b + rc * spc) * ntd, (c * b + min(b, (rc + 1) * spc)) * ntd
+    gpc = N // p
+
+    def dec_chunk(i, cb):
+        return (i * g + cb * gpc) * ntd, (i * g + min(g, (cb + 1) * gpc)) * ntd
 
     for k in range(G):
         fc0, fc1 = k * Tc // G, (k + 1) * Tc // G
@@ -53,14 +55,14 @@ def simulate(b, h, g, mc, md, N, sms=148):
             f = fend
         f = fd0
         while f < fd1:
-            cb = f // ntd
-            c, rc = cb // b, (cb % b) // spc
-            a, e = dec_chunk(c, rc)
+            ic = f // ntd
+            i, cb = ic // g, (ic % g) // gpc
+            a, e = dec_chunk(i, cb)
             fend = min(e, fd1)
             for ff in range(f, fend):
-                i, t = (ff // ntd) % b, ff % ntd
-                tiles_seen.setdefault((("d", c, i, t), rc), []).append(k)
-            writes.setdefault((c, rc), []).append(("d", part_rank(a, f, Td, G)))
+                c, t = (ff // ntd) % g, ff % ntd
+                tiles_seen.setdefault((("d", c, i, t), 0), []).append(k)
+            writes.setdefault(("d", i, cb), []).append(("d", part_rank(a, f, Td, G)))
             f = fend
 
     def ctx_parts(c, rc):
@@ -69,10 +71,10 @@ def simulate(b, h, g, mc, md, N, sms=148):
         ff = (c * nrc + rc) * ntc
         return part_rank(ff, ff + ntc - 1, Tc, G) + 1
 
-    def dec_parts(c, rc):
+    def dec_parts(i, cb):
         if Td == 0:
             return 0
-        a, e = dec_chunk(c, rc)
+        a, e = dec_chunk(i, cb)
         return part_rank(a, e - 1, Td, G) + 1
 
     # every tile exactly once
@@ -83,14 +85,18 @@ def simulate(b, h, g, mc, md, N, sms=148):
     for c in range(g):
         for i in range(b):
             for t in range(ntd):
-                assert len(tiles_seen[(("d", c, i, t), i * p // N)]) == 1
+                assert len(tiles_seen[(("d", c, i, t), 0)]) == 1
     sc = sd = 0
-    for (c, rc), w in writes.items():
-        cs = sorted(s for kind, s in w if kind == "c")
-        ds = sorted(s for kind, s in w if kind == "d")
-        assert cs == list(range(ctx_parts(c, rc)))
-        assert ds == list(range(dec_parts(c, rc)))
-        sc, sd = max(sc, len(cs)), max(sd, len(ds))
+    for key, w in writes.items():
+        if key[0] == "d":
+            ds = sorted(s for kind, s in w)
+            assert ds == list(range(dec_parts(key[1], key[2])))
+            sd = max(sd, len(ds))
+        else:
+            c, rc = key
+            cs = sorted(s for kind, s in w)
+            assert cs == list(range(ctx_parts(c, rc)))
+            sc = max(sc, len(cs))
     return sc, sd
 
 
