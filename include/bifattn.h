@@ -149,10 +149,13 @@ const char* ba_launch_name(const ba_problem_t* prob, int k);
 void ba_set_launch_events(void* const* events, int n);
 
 /* Instrumentation: while set, the fused tensor-core kernel launched by THIS
- * thread writes up to 64 tagged %globaltimer stamps per CTA into dev_buf
- * (device, uint64 [gridDim][64], zeroed by the caller): tag<<56 | time_ns,
- * tags 1 start, 2/3 first tile of a context/decode segment, 4 segment end,
- * 5/6 after the counter arrival (6 = this CTA merged), 7 done.  NULL disables. */
+ * thread writes tagged %globaltimer stamps into dev_buf (device, uint64
+ * [gridDim][1024], zeroed by the caller), each tag<<56 | time_ns.  Per CTA:
+ * [0,256) softmax: 1 start, 2/3 first tile of a context/decode segment,
+ * 20 S ready, 21/22 fast/slow path, 23 P handed to MMA, 4 segment end,
+ * 7 done; [256,512) producer: 30 stage free (TMA issue) per tile;
+ * [512,768) MMA: 31 QK issued per tile; [768,1024) MMA: 32 PV issued.
+ * NULL disables. */
 void ba_set_trace_buffer(void* dev_buf);
 
 /* Message for a BA_* code (static string). */

@@ -83,7 +83,7 @@ constexpr int kD = 128;
 constexpr int kBM = 128;            // positions per tile (MMA M)
 constexpr int kStageBytes = 65536;  // K tile 32 KB + V tile 32 KB
 constexpr float kTh = 8.0f;         // fast-path slack (log2 units)
-constexpr int kTraceSlots = 64;
+constexpr int kTraceSlots = 1024;  // per CTA: 4 roles x 256 stamps
 
 // softmax warpgroups: keep columns per softmax thread <= 32
 __host__ __device__ constexpr int softmax_wgs(int N) { return N > 0 ? 2 : 2; }  // measured: 2 beats 1 at N=16/32
@@ -405,6 +405,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
           const int z = s.dec ? s.i * P.g + cg : s.c;  // TMA z: group, or sample*g + group
           const int st = tt % NST;
           tc::mbar_wait(tc::smem_u32(&kv_empty[st]), ((tt / NST) & 1) ^ 1);
+          if (P.trace && tt < 256) P.trace[(size_t)blockIdx.x * kTraceSlots + 256 + tt] = (gtimer() & 0x00ffffffffffffffull) | (30ull << 56);
           const uint32_t bar = tc::smem_u32(&kv_full[st]);
           tc::mbar_arrive_expect_tx(bar, kStageBytes);
           const uint32_t dst = tc::smem_u32(sm_stage + st * kStageBytes);
@@ -452,6 +453,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
                 tc::mma_bf16(tS + slot * N, ad, bd, IDESC_QK, k > 0 ? 1u : 0u);
               }
               tc::mma_commit(tc::smem_u32(&s_full[slot]));
+              if (P.trace && u_qk < 256) P.trace[(size_t)blockIdx.x * kTraceSlots + 512 + u_qk] = (gtimer() & 0x00ffffffffffffffull) | (31ull << 56);
               stage_of[u_qk & 3] = st;
               ++wq;
               ++tt_qk;
@@ -488,6 +490,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
             }
             tc::mma_commit(tc::smem_u32(&p_empty[slot]));
             tc::mma_commit(tc::smem_u32(&kv_empty[st]));
+            if (P.trace && u_pv < 256) P.trace[(size_t)blockIdx.x * kTraceSlots + 768 + u_pv] = (gtimer() & 0x00ffffffffffffffull) | (32ull << 56);
             pv_first = false;
             ++wp;
             ++u_pv;
@@ -513,7 +516,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
     unsigned long long* tr = P.trace ? P.trace + (size_t)blockIdx.x * kTraceSlots : nullptr;
     int ntr = 0;
     auto stamp = [&](unsigned long long tag) {
-      if (tr && threadIdx.x == 128 && ntr < kTraceSlots) tr[ntr++] = (gtimer() & 0x00ffffffffffffffull) | (tag << 56);
+      if (tr && threadIdx.x == 128 && ntr < 256) tr[ntr++] = (gtimer() & 0x00ffffffffffffffull) | (tag << 56);
     };
     stamp(1);
     for (long long w = 0; w < nw; ++sg) {
@@ -541,6 +544,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
         tc::mbar_wait(tc::smem_u32(&s_full[slot]), (u >> 1) & 1);
         tc::tc_fence_after();
         if (j == 0) stamp(s.dec ? 3 : 2);
+        stamp(20);
         float x[CPT];
         tmem_ld_cols<CPT>(tS + slot * N + col0 + lane_addr, reinterpret_cast<uint32_t*>(x));
         tc::tmem_ld_wait();
@@ -558,7 +562,9 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
           x[n] = vc ? fmaf(x[n], sl2, -mref) : kNegInf;
           need |= vc && (mo == kNegInf || x[n] > kTh);
         }
-        if (tc::named_bar_or(1, 32 * NSW, need)) {
+        const bool slow = tc::named_bar_or(1, 32 * NSW, need);
+        stamp(slow ? 22 : 21);
+        if (slow) {
           // ---- slow path: exact max of the tile's valid columns, new m_run ----
           if (col0 < cv1 && col0 + CPT > cv0) {  // warp-uniform: this warp has valid columns
             if (cv1 - cv0 >= CPT) {
@@ -646,6 +652,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
         tc::fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(tc::smem_u32(&p_full[slot]));
+        stamp(23);
         if (++t == ntl) {
           t = 0;
           ++cl;
