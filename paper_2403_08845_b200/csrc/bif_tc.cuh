@@ -405,7 +405,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
           const int z = s.dec ? s.i * P.g + cg : s.c;  // TMA z: group, or sample*g + group
           const int st = tt % NST;
           tc::mbar_wait(tc::smem_u32(&kv_empty[st]), ((tt / NST) & 1) ^ 1);
-          if (P.trace && tt < 256) P.trace[(size_t)blockIdx.x * kTraceSlots + 256 + tt] = (gtimer() & 0x00ffffffffffffffull) | (30ull << 56);
+          if (P.trace && tt < 128) P.trace[(size_t)blockIdx.x * kTraceSlots + 256 + tt] = (gtimer() & 0x00ffffffffffffffull) | (30ull << 56);
           const uint32_t bar = tc::smem_u32(&kv_full[st]);
           tc::mbar_arrive_expect_tx(bar, kStageBytes);
           const uint32_t dst = tc::smem_u32(sm_stage + st * kStageBytes);
@@ -430,6 +430,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
       long long wq = 0, wp = 0, seg_end_q = 0, seg_end_p = 0;
       bool q_ready = false, pv_first = true;
       uint32_t stage_of[4] = {0, 0, 0, 0};
+      uint32_t kvseen = 0xffffffffu;
       while (wp < nw) {
         bool progressed = false;
         // ---- QK ----
@@ -441,8 +442,12 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
           if (q_ready) {
             const uint32_t st = tt_qk % NST;
             const uint32_t slot = u_qk & 1;
-            if (mbar_test(tc::smem_u32(&kv_full[st]), (tt_qk / NST) & 1) &&
-                mbar_test(tc::smem_u32(&s_free[slot]), ((u_qk >> 1) & 1) ^ 1)) {
+            const bool kv_ok = mbar_test(tc::smem_u32(&kv_full[st]), (tt_qk / NST) & 1);
+            if (kv_ok && P.trace && u_qk < 128 && kvseen != u_qk) {
+              kvseen = u_qk;
+              P.trace[(size_t)blockIdx.x * kTraceSlots + 256 + 128 + u_qk] = (gtimer() & 0x00ffffffffffffffull) | (33ull << 56);
+            }
+            if (kv_ok && mbar_test(tc::smem_u32(&s_free[slot]), ((u_qk >> 1) & 1) ^ 1)) {
               tc::tc_fence_after();
               const uint32_t kbase = tc::smem_u32(sm_stage + st * kStageBytes);
               const uint32_t qbase = q_addr + (sg_qk & 1) * QB;

@@ -28,10 +28,12 @@ rel = (ts - t0) / 1e3
 for k in [int(x) for x in (sys.argv[2].split(",") if len(sys.argv) > 2 else ["0", "100"])]:
     print("=== CTA", k)
     sm = [(int(tags[k, j]), round(float(rel[k, j]), 2)) for j in range(256) if tags[k, j] != 0]
-    prod = [round(float(rel[k, 256 + j]), 2) for j in range(256) if tags[k, 256 + j] != 0]
+    prod = [round(float(rel[k, 256 + j]), 2) for j in range(128) if tags[k, 256 + j] != 0]
+    kvf = [round(float(rel[k, 384 + j]), 2) for j in range(128) if tags[k, 384 + j] != 0]
     qk = [round(float(rel[k, 512 + j]), 2) for j in range(256) if tags[k, 512 + j] != 0]
     pv = [round(float(rel[k, 768 + j]), 2) for j in range(256) if tags[k, 768 + j] != 0]
     print("softmax:", " ".join("%d@%.2f" % e for e in sm))
     print("tma_issue:", prod)
+    print("kv_landed(seen by MMA):", kvf)
     print("qk_issue:", qk)
     print("pv_issue:", pv)
