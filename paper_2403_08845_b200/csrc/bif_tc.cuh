@@ -591,7 +591,9 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
               }
             }
           }
+          stamp(24);
           tc::named_bar_sync(2, 32 * NSW);
+          stamp(25);
           float* mnext = sm_mrun + (cur ^ 1) * N + col0;
           bool grew = false;
 #pragma unroll
@@ -612,7 +614,10 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
             }
             if (quad == 0 && lane == 0) mnext[n] = mnew;
           }
-          if (tc::named_bar_or(1, 32 * NSW, grew)) {
+          stamp(26);
+          const bool grew_any = tc::named_bar_or(1, 32 * NSW, grew);
+          stamp(grew_any ? 28 : 27);
+          if (grew_any) {
             // O^T holds earlier tiles of this segment: wait for PV(u-1), rescale
             const uint32_t pv = u - 1;
             tc::mbar_wait(tc::smem_u32(&p_empty[pv & 1]), (pv >> 1) & 1);
@@ -634,8 +639,10 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
             tc::tc_fence_before();
           }
           tc::named_bar_sync(2, 32 * NSW);
+          stamp(29);
           cur ^= 1;
         }
+        stamp(35);
         // ---- P = 2^x (bf16) into shared memory; row sums of the SAME bf16
         //      values, so out = sum P v / sum P is a convex combination ----
         tc::mbar_wait(tc::smem_u32(&p_empty[slot]), ((u >> 1) & 1) ^ 1);
