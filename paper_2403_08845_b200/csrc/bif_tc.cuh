@@ -84,6 +84,7 @@ constexpr int kBM = 128;            // positions per tile (MMA M)
 constexpr int kStageBytes = 65536;  // K tile 32 KB + V tile 32 KB
 constexpr float kTh = 8.0f;         // fast-path slack (log2 units)
 constexpr int kTraceSlots = 1024;  // per CTA: 4 roles x 256 stamps
+constexpr int kNarrowP = 8;         // decode tiles with p <= 8 valid columns take the narrow path
 
 // softmax warpgroups: keep columns per softmax thread <= 32
 __host__ __device__ constexpr int softmax_wgs(int N) { return N > 0 ? 2 : 2; }  // measured: 2 beats 1 at N=16/32
@@ -540,6 +541,145 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
       tc::named_bar_sync(2, 32 * NSW);
       int t = s.t0, cl = s.c0 - s.cb * P.gpc;  // tile index, group within the decode chunk
       const int ntl = s.dec ? P.ntile_d : P.ntile_c;
+      if (s.dec && P.p <= kNarrowP) {
+        // ====== narrow decode path: a tile of group c feeds only its p columns ======
+        // Half-0 warps (one per TMEM lane quadrant) handle the p valid columns
+        // with an exact per-tile max; half-1 warps only keep the barriers.
+        const bool h0 = sw < 4;
+        float* nred = reinterpret_cast<float*>(sm_len);  // [2 slots][4 quads][kNarrowP]
+        // epilogue inputs for this O buffer start as "no contribution"
+        tc::mbar_wait(tc::smem_u32(&e_empty[ob]), ((sg >> 1) & 1) ^ 1);
+        for (int k = sw * 32 + lane; k < 5 * N; k += 32 * NSW) {
+          if (k < 4 * N) sm_l[ob * 4 * N + k] = 0.f;
+          else sm_mfin[ob * N + (k - 4 * N)] = kNegInf;
+        }
+        tc::named_bar_sync(2, 32 * NSW);
+        float m_g[kNarrowP], l_g[kNarrowP];
+#pragma unroll
+        for (int k = 0; k < kNarrowP; ++k) {
+          m_g[k] = kNegInf;
+          l_g[k] = 0.f;
+        }
+        for (int j = 0; j < s.ntiles; ++j, ++u) {
+          const int cv0 = cl * P.p;
+          const uint32_t slot = u & 1;
+          tc::mbar_wait(tc::smem_u32(&s_full[slot]), (u >> 1) & 1);
+          tc::tc_fence_after();
+          if (j == 0) stamp(3);
+          float xv[kNarrowP];
+          if (h0) {
+#pragma unroll
+            for (int k = 0; k < kNarrowP; ++k)
+              if (k < P.p) tc::tmem_ld<1>(tS + slot * N + cv0 + k + lane_addr, reinterpret_cast<uint32_t*>(&xv[k]));
+            tc::tmem_ld_wait();
+          }
+          tc::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive(tc::smem_u32(&s_free[slot]));
+          const bool vpos = t * kBM + pos < L;
+          if (h0) {
+#pragma unroll
+            for (int k = 0; k < kNarrowP; ++k) {
+              if (k < P.p) {
+                xv[k] = vpos ? xv[k] * sl2 : kNegInf;
+                float v = xv[k];
+#pragma unroll
+                for (int off = 16; off >= 1; off >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, off));
+                if (lane == 0) nred[(slot * 4 + quad) * kNarrowP + k] = v;
+              }
+            }
+          }
+          tc::named_bar_sync(2, 32 * NSW);
+          if (h0) {
+            float pv[kNarrowP], alpha[kNarrowP];
+            bool resc = false;
+#pragma unroll
+            for (int k = 0; k < kNarrowP; ++k) {
+              if (k < P.p) {
+                const float* nr = nred + slot * 4 * kNarrowP + k;
+                const float tmax = fmaxf(fmaxf(nr[0], nr[kNarrowP]), fmaxf(nr[2 * kNarrowP], nr[3 * kNarrowP]));
+                const float mo = m_g[k];
+                float mn = mo;
+                alpha[k] = 1.f;
+                if (mo == kNegInf) {
+                  mn = tmax;  // first valid tile of this column: exact max
+                } else if (tmax > mo + kTh) {
+                  mn = tmax;  // lazy rescale: only when P would exceed 2^kTh
+                  alpha[k] = ex2(mo - mn);
+                  l_g[k] *= alpha[k];
+                  resc = true;
+                }
+                m_g[k] = mn;
+                pv[k] = (mn == kNegInf) ? 0.f : ex2(xv[k] - mn);
+              }
+            }
+            if (resc) {  // uniform over half-0 warps (same shared values)
+              const uint32_t pvu = u - 1;
+              tc::mbar_wait(tc::smem_u32(&p_empty[pvu & 1]), (pvu >> 1) & 1);
+              tc::tc_fence_after();
+#pragma unroll
+              for (int k = 0; k < kNarrowP; ++k) {
+                if (k < P.p && alpha[k] != 1.f) {
+                  uint32_t o1;
+                  tc::tmem_ld<1>(tOb + cv0 + k + lane_addr, &o1);
+                  tc::tmem_ld_wait();
+                  o1 = __float_as_uint(__uint_as_float(o1) * alpha[k]);
+                  tc::tmem_st<1>(tOb + cv0 + k + lane_addr, &o1);
+                }
+              }
+              tc::tmem_st_wait();
+              tc::tc_fence_before();
+            }
+            // P row of this position: zeros except the p valid columns
+            tc::mbar_wait(tc::smem_u32(&p_empty[slot]), ((u >> 1) & 1) ^ 1);
+            uint8_t* pbuf = sm_p + slot * QB;
+#pragma unroll
+            for (int n = 0; n < N; n += 8) {
+              uint32_t off = (uint32_t)((n / W) * PLBO + pos * PRB + (n % W) * 2);
+              off ^= ((off >> 7) & PSWM) << 4;
+              *reinterpret_cast<uint4*>(pbuf + off) = make_uint4(0, 0, 0, 0);
+            }
+#pragma unroll
+            for (int k = 0; k < kNarrowP; ++k) {
+              if (k < P.p) {
+                const int col = cv0 + k;
+                const __nv_bfloat16 pb = __float2bfloat16_rn(pv[k]);
+                l_g[k] += __bfloat162float(pb);
+                uint32_t off = (uint32_t)((col / W) * PLBO + pos * PRB + (col % W) * 2);
+                off ^= ((off >> 7) & PSWM) << 4;
+                *reinterpret_cast<__nv_bfloat16*>(pbuf + off) = pb;
+              }
+            }
+            tc::fence_proxy_async_smem();
+          }
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive(tc::smem_u32(&p_full[slot]));
+          // end of this group's tiles (or of this segment part): flush its row sums / max
+          if (t == ntl - 1 || j == s.ntiles - 1) {
+            if (h0) {
+#pragma unroll
+              for (int k = 0; k < kNarrowP; ++k) {
+                if (k < P.p) {
+                  float v = l_g[k];
+#pragma unroll
+                  for (int off = 16; off >= 1; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+                  if (lane == 0) sm_l[(ob * 4 + quad) * N + cv0 + k] = v;
+                  if (lane == 0 && quad == 0) sm_mfin[ob * N + cv0 + k] = m_g[k];
+                  m_g[k] = kNegInf;
+                  l_g[k] = 0.f;
+                }
+              }
+            }
+          }
+          if (++t == ntl) {
+            t = 0;
+            ++cl;
+          }
+        }
+        stamp(4);
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(tc::smem_u32(&e_full[ob]));
+      } else {
       for (int j = 0; j < s.ntiles; ++j, ++u) {
         // valid columns [cv0, cv1) of this tile
         const int cv0 = s.dec ? cl * P.p : 0;
@@ -678,6 +818,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
       if (quad == 0 && lane < CPT) sm_mfin[ob * N + col0 + lane] = sm_mrun[cur * N + col0 + lane];
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(tc::smem_u32(&e_full[ob]));
+      }
       tc::named_bar_sync(2, 32 * NSW);  // sm_mrun reads of this segment done
       w = s.next;
     }

@@ -130,6 +130,10 @@ template <int N>
 BA_DEVINL void tmem_ld(uint32_t taddr, uint32_t* r);
 
 template <>
+BA_DEVINL void tmem_ld<1>(uint32_t taddr, uint32_t* r) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(r[0]) : "r"(taddr));
+}
+template <>
 BA_DEVINL void tmem_ld<8>(uint32_t taddr, uint32_t* r) {
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
@@ -160,6 +164,10 @@ BA_DEVINL void tmem_ld<32>(uint32_t taddr, uint32_t* r) {
 }
 template <int N>
 BA_DEVINL void tmem_st(uint32_t taddr, const uint32_t* r);
+template <>
+BA_DEVINL void tmem_st<1>(uint32_t taddr, const uint32_t* r) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(taddr), "r"(r[0]) : "memory");
+}
 template <>
 BA_DEVINL void tmem_st<8>(uint32_t taddr, const uint32_t* r) {
   asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(
