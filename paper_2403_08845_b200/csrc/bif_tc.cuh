@@ -313,8 +313,8 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
   uint8_t* sm_p = sm_q + 2 * QB;             // 2 buffers
   float* sm_red = reinterpret_cast<float*>(sm_p + 2 * QB);  // [4][N] col max (slow path)
   float* sm_l = sm_red + 4 * N;                             // [2][4][N] row sums per O buffer
-  float* sm_mrun = sm_l + 8 * N;                            // [2][N] running max
-  float* sm_mfin = sm_mrun + 2 * N;                         // [2][N] final max per O buffer
+  float* sm_mold = sm_l + 8 * N;                            // [N] running max before a slow path
+  float* sm_mfin = sm_mold + 2 * N;                         // [2][N] final max per O buffer
   int* sm_len = reinterpret_cast<int*>(sm_mfin + 2 * N);    // [64] decode lengths of the chunk
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm_len + 64);
   uint64_t* kv_full = bars;        // [8]
@@ -518,27 +518,22 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
     const int pos = quad * 32 + lane;
     const uint32_t lane_addr = (uint32_t)(quad * 32) << 16;
     const float sl2 = P.scale_log2;
-    uint32_t u = 0, sg = 0, cur = 0;
+    uint32_t u = 0, sg = 0;
     unsigned long long* tr = P.trace ? P.trace + (size_t)blockIdx.x * kTraceSlots : nullptr;
     int ntr = 0;
     auto stamp = [&](unsigned long long tag) {
       if (tr && threadIdx.x == 128 && ntr < 256) tr[ntr++] = (gtimer() & 0x00ffffffffffffffull) | (tag << 56);
     };
     stamp(1);
+    // valid positions of a segment's sequence; decode lengths are prefetched one
+    // segment ahead so no global-load latency sits on a segment boundary
+    auto seg_len = [&](const Seg& q) { return q.dec ? dec_len(P, q.i) : P.mc; };
+    int L = nw > 0 ? seg_len(seg_at(P, rg, 0)) : 0;
     for (long long w = 0; w < nw; ++sg) {
       const Seg s = seg_at(P, rg, w);
+      const int Ln = s.next < nw ? seg_len(seg_at(P, rg, s.next)) : 0;  // used next segment
       const uint32_t ob = sg & 1;
       const uint32_t tOb = tO + ob * N;
-      float l_part[CPT];
-#pragma unroll
-      for (int n = 0; n < CPT; ++n) l_part[n] = 0.f;
-      // running max of every column starts unset (-inf); decode lengths of the chunk
-      if (quad == 0 && lane == 0) {
-#pragma unroll
-        for (int n = 0; n < CPT; ++n) sm_mrun[cur * N + col0 + n] = kNegInf;
-      }
-      const int L = s.dec ? dec_len(P, s.i) : P.mc;  // valid positions of the sequence
-      tc::named_bar_sync(2, 32 * NSW);
       int t = s.t0, cl = s.c0 - s.cb * P.gpc;  // tile index, group within the decode chunk
       const int ntl = s.dec ? P.ntile_d : P.ntile_c;
       if (s.dec && P.p <= kNarrowP) {
@@ -547,13 +542,8 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
         // with an exact per-tile max; half-1 warps only keep the barriers.
         const bool h0 = sw < 4;
         float* nred = reinterpret_cast<float*>(sm_len);  // [2 slots][4 quads][kNarrowP]
-        // epilogue inputs for this O buffer start as "no contribution"
-        tc::mbar_wait(tc::smem_u32(&e_empty[ob]), ((sg >> 1) & 1) ^ 1);
-        for (int k = sw * 32 + lane; k < 5 * N; k += 32 * NSW) {
-          if (k < 4 * N) sm_l[ob * 4 * N + k] = 0.f;
-          else sm_mfin[ob * N + (k - 4 * N)] = kNegInf;
-        }
-        tc::named_bar_sync(2, 32 * NSW);
+        bool e_waited = false;
+        const int cfirst = cl;
         float m_g[kNarrowP], l_g[kNarrowP];
 #pragma unroll
         for (int k = 0; k < kNarrowP; ++k) {
@@ -591,20 +581,25 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
           }
           tc::named_bar_sync(2, 32 * NSW);
           if (h0) {
-            float pv[kNarrowP], alpha[kNarrowP];
+            float pv[kNarrowP], alpha[kNarrowP], tm[kNarrowP];
             bool resc = false;
 #pragma unroll
             for (int k = 0; k < kNarrowP; ++k) {
               if (k < P.p) {
                 const float* nr = nred + slot * 4 * kNarrowP + k;
-                const float tmax = fmaxf(fmaxf(nr[0], nr[kNarrowP]), fmaxf(nr[2 * kNarrowP], nr[3 * kNarrowP]));
+                tm[k] = fmaxf(fmaxf(nr[0], nr[kNarrowP]), fmaxf(nr[2 * kNarrowP], nr[3 * kNarrowP]));
+              }
+            }
+#pragma unroll
+            for (int k = 0; k < kNarrowP; ++k) {
+              if (k < P.p) {
                 const float mo = m_g[k];
                 float mn = mo;
                 alpha[k] = 1.f;
                 if (mo == kNegInf) {
-                  mn = tmax;  // first valid tile of this column: exact max
-                } else if (tmax > mo + kTh) {
-                  mn = tmax;  // lazy rescale: only when P would exceed 2^kTh
+                  mn = tm[k];  // first valid tile of this column: exact max
+                } else if (tm[k] > mo + kTh) {
+                  mn = tm[k];  // lazy rescale: only when P would exceed 2^kTh
                   alpha[k] = ex2(mo - mn);
                   l_g[k] *= alpha[k];
                   resc = true;
@@ -656,6 +651,10 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
           if (lane == 0) tc::mbar_arrive(tc::smem_u32(&p_full[slot]));
           // end of this group's tiles (or of this segment part): flush its row sums / max
           if (t == ntl - 1 || j == s.ntiles - 1) {
+            if (!e_waited) {  // the epilogue has consumed this buffer's previous segment
+              tc::mbar_wait(tc::smem_u32(&e_empty[ob]), ((sg >> 1) & 1) ^ 1);
+              e_waited = true;
+            }
             if (h0) {
 #pragma unroll
               for (int k = 0; k < kNarrowP; ++k) {
@@ -676,151 +675,161 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
             ++cl;
           }
         }
+        // columns of groups this segment part did not visit: no contribution
+        if (!e_waited) tc::mbar_wait(tc::smem_u32(&e_empty[ob]), ((sg >> 1) & 1) ^ 1);
+        {
+          const int vlo = cfirst * P.p;
+          const int vhi = (t == 0 ? cl : cl + 1) * P.p;  // one past the last visited column
+          for (int k = sw * 32 + lane; k < N; k += 32 * NSW) {
+            if (k < vlo || k >= vhi) {
+              sm_l[(ob * 4 + 0) * N + k] = 0.f;
+              sm_l[(ob * 4 + 1) * N + k] = 0.f;
+              sm_l[(ob * 4 + 2) * N + k] = 0.f;
+              sm_l[(ob * 4 + 3) * N + k] = 0.f;
+              sm_mfin[ob * N + k] = kNegInf;
+            }
+          }
+        }
         stamp(4);
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(tc::smem_u32(&e_full[ob]));
       } else {
-      for (int j = 0; j < s.ntiles; ++j, ++u) {
-        // valid columns [cv0, cv1) of this tile
-        const int cv0 = s.dec ? cl * P.p : 0;
-        const int cv1 = s.dec ? cv0 + P.p : N;
-        const uint32_t slot = u & 1;
-        const float* mrun = sm_mrun + cur * N + col0;
-        tc::mbar_wait(tc::smem_u32(&s_full[slot]), (u >> 1) & 1);
-        tc::tc_fence_after();
-        if (j == 0) stamp(s.dec ? 3 : 2);
-        stamp(20);
-        float x[CPT];
-        tmem_ld_cols<CPT>(tS + slot * N + col0 + lane_addr, reinterpret_cast<uint32_t*>(x));
-        tc::tmem_ld_wait();
-        tc::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive(tc::smem_u32(&s_free[slot]));
-        const bool vpos = t * kBM + pos < L;
-        bool need = false;
+        // ====== general path: every column of the tile may be valid ======
+        float l_part[CPT], mr[CPT];  // per-position row sums; running max per column
 #pragma unroll
         for (int n = 0; n < CPT; ++n) {
-          const int col = col0 + n;
-          const bool vc = vpos && col >= cv0 && col < cv1;
-          const float mo = mrun[n];
-          const float mref = (mo == kNegInf) ? 0.f : mo;
-          x[n] = vc ? fmaf(x[n], sl2, -mref) : kNegInf;
-          need |= vc && (mo == kNegInf || x[n] > kTh);
+          l_part[n] = 0.f;
+          mr[n] = kNegInf;
         }
-        const bool slow = tc::named_bar_or(1, 32 * NSW, need);
-        stamp(slow ? 22 : 21);
-        if (slow) {
-          // ---- slow path: exact max of the tile's valid columns, new m_run ----
-          if (col0 < cv1 && col0 + CPT > cv0) {  // warp-uniform: this warp has valid columns
-            if (cv1 - cv0 >= CPT) {
-              float v[CPT];
-#pragma unroll
-              for (int n = 0; n < CPT; ++n) v[n] = x[n];
-              warp_col_reduce<CPT, true>(v, lane);
-              if (lane < CPT) sm_red[quad * N + col0 + lane] = v[0];
-            } else {
-#pragma unroll
-              for (int n = 0; n < CPT; ++n) {
-                const int col = col0 + n;
-                if (col >= cv0 && col < cv1) {
-                  float v = x[n];
-#pragma unroll
-                  for (int off = 16; off >= 1; off >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, off));
-                  if (lane == 0) sm_red[quad * N + col] = v;
-                }
-              }
-            }
-          }
-          stamp(24);
-          tc::named_bar_sync(2, 32 * NSW);
-          stamp(25);
-          float* mnext = sm_mrun + (cur ^ 1) * N + col0;
-          bool grew = false;
+        for (int j = 0; j < s.ntiles; ++j, ++u) {
+          const int cv0 = s.dec ? cl * P.p : 0;
+          const int cv1 = s.dec ? cv0 + P.p : N;
+          const uint32_t slot = u & 1;
+          tc::mbar_wait(tc::smem_u32(&s_full[slot]), (u >> 1) & 1);
+          tc::tc_fence_after();
+          if (j == 0) stamp(s.dec ? 3 : 2);
+          float x[CPT];
+          tmem_ld_cols<CPT>(tS + slot * N + col0 + lane_addr, reinterpret_cast<uint32_t*>(x));
+          tc::tmem_ld_wait();
+          tc::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive(tc::smem_u32(&s_free[slot]));
+          const bool vpos = t * kBM + pos < L;
+          bool need = false;
 #pragma unroll
           for (int n = 0; n < CPT; ++n) {
             const int col = col0 + n;
-            const float mo = mrun[n];
-            float mnew = mo;
-            if (col >= cv0 && col < cv1) {
-              const float mref = (mo == kNegInf) ? 0.f : mo;
-              const float cm = fmaxf(fmaxf(sm_red[col], sm_red[N + col]),
-                                     fmaxf(sm_red[2 * N + col], sm_red[3 * N + col]));
-              mnew = fmaxf(mo, mref + cm);  // -inf stays if the column had no valid logit
-              // l and O of a column are exactly 0 while its max is unset
-              const float alpha = (mo == kNegInf) ? 0.f : ex2(mo - mnew);
-              l_part[n] *= alpha;
-              x[n] = (mnew == kNegInf) ? kNegInf : x[n] + (mref - mnew);
-              grew |= (mo != kNegInf) && (mnew > mo);
-            }
-            if (quad == 0 && lane == 0) mnext[n] = mnew;
+            const bool vc = vpos && col >= cv0 && col < cv1;
+            const float mref = (mr[n] == kNegInf) ? 0.f : mr[n];
+            x[n] = vc ? fmaf(x[n], sl2, -mref) : kNegInf;
+            need |= vc && (mr[n] == kNegInf || x[n] > kTh);
           }
-          stamp(26);
-          const bool grew_any = tc::named_bar_or(1, 32 * NSW, grew);
-          stamp(grew_any ? 28 : 27);
-          if (grew_any) {
-            // O^T holds earlier tiles of this segment: wait for PV(u-1), rescale
-            const uint32_t pv = u - 1;
-            tc::mbar_wait(tc::smem_u32(&p_empty[pv & 1]), (pv >> 1) & 1);
-            tc::tc_fence_after();
+          if (tc::named_bar_or(1, 32 * NSW, need)) {
+            // ---- slow path: exact max of the tile's valid columns, new running max ----
+            if (quad == 0 && lane == 0) {
 #pragma unroll
-            for (int n = 0; n < CPT; n += 8) {
-              uint32_t orr[8];
-              tc::tmem_ld<8>(tOb + col0 + n + lane_addr, orr);
-              tc::tmem_ld_wait();
+              for (int n = 0; n < CPT; ++n) sm_mold[col0 + n] = mr[n];
+            }
+            if (col0 < cv1 && col0 + CPT > cv0) {  // warp-uniform: this warp has valid columns
+              if (cv1 - cv0 >= CPT) {
+                float v[CPT];
 #pragma unroll
-              for (int e = 0; e < 8; ++e) {
-                const float mo = mrun[n + e], mn = mnext[n + e];
-                const float a = (mo == kNegInf) ? 0.f : ex2(mo - mn);
-                orr[e] = __float_as_uint(__uint_as_float(orr[e]) * a);
+                for (int n = 0; n < CPT; ++n) v[n] = x[n];
+                warp_col_reduce<CPT, true>(v, lane);
+                if (lane < CPT) sm_red[quad * N + col0 + lane] = v[0];
+              } else {
+#pragma unroll
+                for (int n = 0; n < CPT; ++n) {
+                  const int col = col0 + n;
+                  if (col >= cv0 && col < cv1) {
+                    float v = x[n];
+#pragma unroll
+                    for (int off = 16; off >= 1; off >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, off));
+                    if (lane == 0) sm_red[quad * N + col] = v;
+                  }
+                }
               }
-              tc::tmem_st<8>(tOb + col0 + n + lane_addr, orr);
             }
-            tc::tmem_st_wait();
-            tc::tc_fence_before();
-          }
-          tc::named_bar_sync(2, 32 * NSW);
-          stamp(29);
-          cur ^= 1;
-        }
-        stamp(35);
-        // ---- P = 2^x (bf16) into shared memory; row sums of the SAME bf16
-        //      values, so out = sum P v / sum P is a convex combination ----
-        tc::mbar_wait(tc::smem_u32(&p_empty[slot]), ((u >> 1) & 1) ^ 1);
-        uint8_t* pbuf = sm_p + slot * QB;
+            tc::named_bar_sync(2, 32 * NSW);
+            bool grew = false;
 #pragma unroll
-        for (int n = 0; n < CPT; n += 8) {
-          uint32_t pk[4];
+            for (int n = 0; n < CPT; ++n) {
+              const int col = col0 + n;
+              const float cm = (col >= cv0 && col < cv1)
+                                   ? fmaxf(fmaxf(sm_red[col], sm_red[N + col]), fmaxf(sm_red[2 * N + col], sm_red[3 * N + col]))
+                                   : kNegInf;
+              const float mo = mr[n];
+              const float mref = (mo == kNegInf) ? 0.f : mo;
+              const float mn = fmaxf(mo, mref + cm);  // unchanged if the column had no valid logit
+              // l and O of a column are exactly 0 while its max is unset
+              l_part[n] *= (mo == kNegInf) ? 0.f : ex2(mo - mn);
+              x[n] = (mn == kNegInf) ? kNegInf : x[n] + (mref - mn);
+              grew |= (mo != kNegInf) && (mn > mo);
+              mr[n] = mn;
+            }
+            // (the vote's barrier also orders these sm_red reads before later writes)
+            if (tc::named_bar_or(1, 32 * NSW, grew)) {
+              // O^T holds earlier tiles of this segment: wait for PV(u-1), rescale
+              const uint32_t pvu = u - 1;
+              tc::mbar_wait(tc::smem_u32(&p_empty[pvu & 1]), (pvu >> 1) & 1);
+              tc::tc_fence_after();
 #pragma unroll
-          for (int e = 0; e < 8; e += 2) {
-            pk[e / 2] = pack_bf16x2(ex2(x[n + e]), ex2(x[n + e + 1]));
-            l_part[n + e] += bf16lo(pk[e / 2]);
-            l_part[n + e + 1] += bf16hi(pk[e / 2]);
+              for (int n = 0; n < CPT; n += 8) {
+                uint32_t orr[8];
+                tc::tmem_ld<8>(tOb + col0 + n + lane_addr, orr);
+                tc::tmem_ld_wait();
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                  const float mo = sm_mold[col0 + n + e];
+                  const float a = (mo == kNegInf) ? 1.f : ex2(mo - mr[n + e]);
+                  orr[e] = __float_as_uint(__uint_as_float(orr[e]) * a);
+                }
+                tc::tmem_st<8>(tOb + col0 + n + lane_addr, orr);
+              }
+              tc::tmem_st_wait();
+              tc::tc_fence_before();
+            }
           }
-          const int col = col0 + n;
-          uint32_t off = (uint32_t)((col / W) * PLBO + pos * PRB + (col % W) * 2);
-          off ^= ((off >> 7) & PSWM) << 4;
-          *reinterpret_cast<uint4*>(pbuf + off) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+          // ---- P = 2^x (bf16) into shared memory; row sums of the SAME bf16
+          //      values, so out = sum P v / sum P is a convex combination ----
+          tc::mbar_wait(tc::smem_u32(&p_empty[slot]), ((u >> 1) & 1) ^ 1);
+          uint8_t* pbuf = sm_p + slot * QB;
+#pragma unroll
+          for (int n = 0; n < CPT; n += 8) {
+            uint32_t pk[4];
+#pragma unroll
+            for (int e = 0; e < 8; e += 2) {
+              pk[e / 2] = pack_bf16x2(ex2(x[n + e]), ex2(x[n + e + 1]));
+              l_part[n + e] += bf16lo(pk[e / 2]);
+              l_part[n + e + 1] += bf16hi(pk[e / 2]);
+            }
+            const int col = col0 + n;
+            uint32_t off = (uint32_t)((col / W) * PLBO + pos * PRB + (col % W) * 2);
+            off ^= ((off >> 7) & PSWM) << 4;
+            *reinterpret_cast<uint4*>(pbuf + off) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+          }
+          tc::fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive(tc::smem_u32(&p_full[slot]));
+          if (++t == ntl) {
+            t = 0;
+            ++cl;
+          }
         }
-        tc::fence_proxy_async_smem();
+        // ---- hand the segment's row sums / max to the epilogue warps ----
+        stamp(4);
+        warp_col_reduce<CPT, false>(l_part, lane);  // lane l: column l of this warp, over 32 positions
+        tc::mbar_wait(tc::smem_u32(&e_empty[ob]), ((sg >> 1) & 1) ^ 1);
+        if (lane < CPT) sm_l[(ob * 4 + quad) * N + col0 + lane] = l_part[0];
+        if (quad == 0 && lane == 0) {
+#pragma unroll
+          for (int n = 0; n < CPT; ++n) sm_mfin[ob * N + col0 + n] = mr[n];
+        }
         __syncwarp();
-        if (lane == 0) tc::mbar_arrive(tc::smem_u32(&p_full[slot]));
-        stamp(23);
-        if (++t == ntl) {
-          t = 0;
-          ++cl;
-        }
+        if (lane == 0) tc::mbar_arrive(tc::smem_u32(&e_full[ob]));
       }
-      // ---- hand the segment's row sums / max to the epilogue warps ----
-      stamp(4);
-      warp_col_reduce<CPT, false>(l_part, lane);  // lane l: column l of this warp, over 32 positions
-      tc::mbar_wait(tc::smem_u32(&e_empty[ob]), ((sg >> 1) & 1) ^ 1);
-      if (lane < CPT) sm_l[(ob * 4 + quad) * N + col0 + lane] = l_part[0];
-      if (quad == 0 && lane < CPT) sm_mfin[ob * N + col0 + lane] = sm_mrun[cur * N + col0 + lane];
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(tc::smem_u32(&e_full[ob]));
-      }
-      tc::named_bar_sync(2, 32 * NSW);  // sm_mrun reads of this segment done
       w = s.next;
+      L = Ln;
     }
     stamp(7);
   } else if (warp >= EPI0) {
