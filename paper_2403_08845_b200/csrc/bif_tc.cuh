@@ -708,6 +708,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
           tc::mbar_wait(tc::smem_u32(&s_full[slot]), (u >> 1) & 1);
           tc::tc_fence_after();
           if (j == 0) stamp(s.dec ? 3 : 2);
+          stamp(20);
           float x[CPT];
           tmem_ld_cols<CPT>(tS + slot * N + col0 + lane_addr, reinterpret_cast<uint32_t*>(x));
           tc::tmem_ld_wait();
@@ -724,7 +725,9 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
             x[n] = vc ? fmaf(x[n], sl2, -mref) : kNegInf;
             need |= vc && (mr[n] == kNegInf || x[n] > kTh);
           }
-          if (tc::named_bar_or(1, 32 * NSW, need)) {
+          const bool slowp = tc::named_bar_or(1, 32 * NSW, need);
+          stamp(slowp ? 22 : 21);
+          if (slowp) {
             // ---- slow path: exact max of the tile's valid columns, new running max ----
             if (quad == 0 && lane == 0) {
 #pragma unroll
@@ -750,7 +753,9 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
                 }
               }
             }
+            stamp(24);
             tc::named_bar_sync(2, 32 * NSW);
+            stamp(25);
             bool grew = false;
 #pragma unroll
             for (int n = 0; n < CPT; ++n) {
@@ -768,6 +773,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
               mr[n] = mn;
             }
             // (the vote's barrier also orders these sm_red reads before later writes)
+            stamp(26);
             if (tc::named_bar_or(1, 32 * NSW, grew)) {
               // O^T holds earlier tiles of this segment: wait for PV(u-1), rescale
               const uint32_t pvu = u - 1;
@@ -811,6 +817,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
           tc::fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) tc::mbar_arrive(tc::smem_u32(&p_full[slot]));
+          stamp(23);
           if (++t == ntl) {
             t = 0;
             ++cl;
