@@ -26,9 +26,10 @@
 //
 // Warp roles (1 CTA per SM):
 //   warp 0            TMA producer (one lane)
-//   warp 1            MMA issuer (one lane): QK(u) when its K tile, q and an
-//                     S slot are ready; PV(v) when P(v) is — whichever first
-//   warp 2            TMEM allocator; warp 3 idle
+//   warp 1            QK issuer (one lane): QK(u) when its K tile, q and an
+//                     S slot are ready
+//   warp 2            TMEM allocator
+//   warp 3            PV issuer (one lane): PV(u) when P(u) is ready
 //   warps 4..4+4W-1   softmax (W warpgroups): warp w reads TMEM lanes
 //                     32*(w%4).. (= tile positions), CPT = N/W columns
 //   last 4 warps      epilogue: drains O^T of a finished segment from TMEM to
@@ -423,91 +424,72 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
       }
     }
   } else if (warp == 1) {
-    // ============================ MMA issuer ==============================
+    // ========================== QK issuer (one lane) ==========================
+    // S^T(u) = K_tile(u) . q^T once the tile has landed and the softmax has
+    // released the S slot; blocking waits (no spinning on the SM's issue slots).
     if (lane == 0) {
       const uint32_t q_addr = tc::smem_u32(sm_q);
+      uint32_t u = 0, sg = 0;
+      for (long long w = 0; w < nw; ++sg) {
+        const Seg s = seg_at(P, rg, w);
+        const uint32_t qbase = q_addr + (sg & 1) * QB;
+        tc::mbar_wait(tc::smem_u32(&q_full[sg & 1]), (sg >> 1) & 1);
+        for (int j = 0; j < s.ntiles; ++j, ++u) {
+          const uint32_t st = u % NST;
+          const uint32_t slot = u & 1;
+          tc::mbar_wait(tc::smem_u32(&kv_full[st]), (u / NST) & 1);
+          if (P.trace && u < 128)
+            P.trace[(size_t)blockIdx.x * kTraceSlots + 256 + 128 + u] = (gtimer() & 0x00ffffffffffffffull) | (33ull << 56);
+          tc::mbar_wait(tc::smem_u32(&s_free[slot]), ((u >> 1) & 1) ^ 1);
+          tc::tc_fence_after();
+          const uint32_t kbase = tc::smem_u32(sm_stage + st * kStageBytes);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const uint64_t ad = tc::smem_desc(kbase + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024, tc::kSw128);
+            const uint64_t bd = tc::smem_desc(qbase + (k >> 2) * (N * 128) + (k & 3) * 32, 16, 1024, tc::kSw128);
+            tc::mma_bf16(tS + slot * N, ad, bd, IDESC_QK, k > 0 ? 1u : 0u);
+          }
+          tc::mma_commit(tc::smem_u32(&s_full[slot]));
+          if (P.trace && u < 256)
+            P.trace[(size_t)blockIdx.x * kTraceSlots + 512 + u] = (gtimer() & 0x00ffffffffffffffull) | (31ull << 56);
+        }
+        tc::mma_commit(tc::smem_u32(&q_empty[sg & 1]));  // q buffer reusable
+        w = s.next;
+      }
+    }
+  } else if (warp == 3) {
+    // ========================== PV issuer (one lane) ==========================
+    // O^T += V_tile^T . P^T once P(u) is in shared memory (and, for a
+    // segment's first tile, the epilogue has drained this O buffer).  Its
+    // commits release the P buffer and the K/V stage (QK(u) completed before
+    // the softmax could produce P(u)).
+    if (lane == 0) {
       const uint32_t p_addr = tc::smem_u32(sm_p);
-      uint32_t tt_qk = 0, u_qk = 0, u_pv = 0, sg_qk = 0, sg_pv = 0;
-      long long wq = 0, wp = 0, seg_end_q = 0, seg_end_p = 0;
-      bool q_ready = false, pv_first = true;
-      uint32_t stage_of[4] = {0, 0, 0, 0};
-      uint32_t kvseen = 0xffffffffu;
-      while (wp < nw) {
-        bool progressed = false;
-        // ---- QK ----
-        if (wq < nw && u_qk - u_pv < 2) {
-          if (!q_ready && mbar_test(tc::smem_u32(&q_full[sg_qk & 1]), (sg_qk >> 1) & 1)) {
-            q_ready = true;
-            seg_end_q = seg_at(P, rg, wq).next;
-          }
-          if (q_ready) {
-            const uint32_t st = tt_qk % NST;
-            const uint32_t slot = u_qk & 1;
-            const bool kv_ok = mbar_test(tc::smem_u32(&kv_full[st]), (tt_qk / NST) & 1);
-            if (kv_ok && P.trace && u_qk < 128 && kvseen != u_qk) {
-              kvseen = u_qk;
-              P.trace[(size_t)blockIdx.x * kTraceSlots + 256 + 128 + u_qk] = (gtimer() & 0x00ffffffffffffffull) | (33ull << 56);
-            }
-            if (kv_ok && mbar_test(tc::smem_u32(&s_free[slot]), ((u_qk >> 1) & 1) ^ 1)) {
-              tc::tc_fence_after();
-              const uint32_t kbase = tc::smem_u32(sm_stage + st * kStageBytes);
-              const uint32_t qbase = q_addr + (sg_qk & 1) * QB;
+      uint32_t u = 0, sg = 0;
+      for (long long w = 0; w < nw; ++sg) {
+        const Seg s = seg_at(P, rg, w);
+        const uint32_t ob = sg & 1;
+        tc::mbar_wait(tc::smem_u32(&o_empty[ob]), ((sg >> 1) & 1) ^ 1);
+        for (int j = 0; j < s.ntiles; ++j, ++u) {
+          const uint32_t st = u % NST;
+          const uint32_t slot = u & 1;
+          tc::mbar_wait(tc::smem_u32(&p_full[slot]), (u >> 1) & 1);
+          tc::tc_fence_after();
+          const uint32_t vbase = tc::smem_u32(sm_stage + st * kStageBytes + 32768);
+          const uint32_t pbase = p_addr + slot * QB;
 #pragma unroll
-              for (int k = 0; k < 8; ++k) {
-                const uint64_t ad = tc::smem_desc(kbase + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024, tc::kSw128);
-                const uint64_t bd = tc::smem_desc(qbase + (k >> 2) * (N * 128) + (k & 3) * 32, 16, 1024, tc::kSw128);
-                tc::mma_bf16(tS + slot * N, ad, bd, IDESC_QK, k > 0 ? 1u : 0u);
-              }
-              tc::mma_commit(tc::smem_u32(&s_full[slot]));
-              if (P.trace && u_qk < 256) P.trace[(size_t)blockIdx.x * kTraceSlots + 512 + u_qk] = (gtimer() & 0x00ffffffffffffffull) | (31ull << 56);
-              stage_of[u_qk & 3] = st;
-              ++wq;
-              ++tt_qk;
-              ++u_qk;
-              if (wq == seg_end_q) {
-                tc::mma_commit(tc::smem_u32(&q_empty[sg_qk & 1]));  // q buffer reusable
-                q_ready = false;
-                ++sg_qk;
-              }
-              progressed = true;
-            }
+          for (int k = 0; k < 8; ++k) {
+            const uint64_t ad = tc::smem_desc(vbase + k * 2048, 16384, 1024, tc::kSw128);
+            const uint64_t bd = tc::smem_desc(pbase + k * 16 * PRB, PLBO, 8 * PRB, p_layout(N));
+            tc::mma_bf16(tO + ob * N, ad, bd, IDESC_PV, (j == 0 && k == 0) ? 0u : 1u);
           }
+          tc::mma_commit(tc::smem_u32(&p_empty[slot]));
+          tc::mma_commit(tc::smem_u32(&kv_empty[st]));
+          if (P.trace && u < 256)
+            P.trace[(size_t)blockIdx.x * kTraceSlots + 768 + u] = (gtimer() & 0x00ffffffffffffffull) | (32ull << 56);
         }
-        // ---- PV ----
-        if (u_pv < u_qk) {
-          const uint32_t slot = u_pv & 1;
-          if (wp == seg_end_p) {
-            seg_end_p = seg_at(P, rg, wp).next;
-            pv_first = true;
-          }
-          const uint32_t ob = sg_pv & 1;
-          bool ok = mbar_test(tc::smem_u32(&p_full[slot]), (u_pv >> 1) & 1);
-          if (ok && pv_first) ok = mbar_test(tc::smem_u32(&o_empty[ob]), ((sg_pv >> 1) & 1) ^ 1);
-          if (ok) {
-            tc::tc_fence_after();
-            const uint32_t st = stage_of[u_pv & 3];
-            const uint32_t vbase = tc::smem_u32(sm_stage + st * kStageBytes + 32768);
-            const uint32_t pbase = p_addr + slot * QB;
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
-              const uint64_t ad = tc::smem_desc(vbase + k * 2048, 16384, 1024, tc::kSw128);
-              const uint64_t bd = tc::smem_desc(pbase + k * 16 * PRB, PLBO, 8 * PRB, p_layout(N));
-              tc::mma_bf16(tO + ob * N, ad, bd, IDESC_PV, (pv_first && k == 0) ? 0u : 1u);
-            }
-            tc::mma_commit(tc::smem_u32(&p_empty[slot]));
-            tc::mma_commit(tc::smem_u32(&kv_empty[st]));
-            if (P.trace && u_pv < 256) P.trace[(size_t)blockIdx.x * kTraceSlots + 768 + u_pv] = (gtimer() & 0x00ffffffffffffffull) | (32ull << 56);
-            pv_first = false;
-            ++wp;
-            ++u_pv;
-            if (wp == seg_end_p) {
-              tc::mma_commit(tc::smem_u32(&o_full[ob]));
-              ++sg_pv;
-            }
-            progressed = true;
-          }
-        }
-        if (!progressed) __nanosleep(20);
+        tc::mma_commit(tc::smem_u32(&o_full[ob]));
+        w = s.next;
       }
     }
   } else if (warp >= 4 && warp < EPI0) {
