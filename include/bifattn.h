@@ -158,6 +158,12 @@ void ba_set_launch_events(void* const* events, int n);
  * NULL disables. */
 void ba_set_trace_buffer(void* dev_buf);
 
+/* Work split of the tensor-core plan for this problem (bf16, d = 128): CTA k
+ * streams flat tiles [cs[k], cs[k+1]) of [context tiles | decode tiles]
+ * (128 positions each).  Writes min(cap, G + 1) entries to cs (nullable) and
+ * returns G, or 0 if the problem takes the CUDA-core plan, or a BA_E* code. */
+int ba_plan_ctas(const ba_problem_t* prob, int32_t* cs, int cap);
+
 /* Message for a BA_* code (static string). */
 const char* ba_strerror(int code);
 

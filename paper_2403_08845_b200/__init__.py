@@ -32,7 +32,7 @@ ERRORS = {0: "BA_OK", -1: "BA_EINVAL", -2: "BA_ENULL", -3: "BA_EALIGN", -4: "BA_
 EXPORTED = ["ba_workspace_bytes", "bifurcated_attn_decode", "bifurcated_attn_decode_host",
             "replicated_attn_decode", "ba_launches_per_call", "ba_plan_string", "ba_strerror",
             "ba_last_cuda_error", "ba_version", "ba_launch_name", "ba_set_launch_events",
-            "ba_set_trace_buffer"]
+            "ba_set_trace_buffer", "ba_plan_ctas"]
 
 
 class BAProblem(ctypes.Structure):
@@ -76,6 +76,8 @@ def load_library(path: str = LIB_PATH):
     lib.ba_launch_name.restype = ctypes.c_char_p
     lib.ba_set_launch_events.argtypes = [ctypes.c_void_p, ctypes.c_int]
     lib.ba_set_launch_events.restype = None
+    lib.ba_plan_ctas.argtypes = [pp, ctypes.c_void_p, ctypes.c_int]
+    lib.ba_plan_ctas.restype = ctypes.c_int
     lib.ba_set_trace_buffer.argtypes = [ctypes.c_void_p]
     lib.ba_set_trace_buffer.restype = None
     lib.ba_version.argtypes = []
@@ -178,6 +180,16 @@ class LaunchTimer:
             for k, (a, b) in enumerate(call):
                 tot[k] += a.elapsed_time(b)
         return [t / self.calls for t in tot]
+
+
+def ba_plan_ctas(prob: BAProblem):
+    """CTA range starts of the tensor-core plan ([] for the CUDA-core plan)."""
+    lib = load_library()
+    buf = (ctypes.c_int32 * 512)()
+    G = lib.ba_plan_ctas(ctypes.byref(prob), buf, 512)
+    if G < 0:
+        raise BifAttnError(G, "ba_plan_ctas")
+    return [int(buf[k]) for k in range(G + 1)] if G > 0 else []
 
 
 def alloc_workspace(prob: BAProblem, device) -> torch.Tensor:

@@ -41,19 +41,23 @@
 // compute the exact tile max per column and raise m_run — rescaling l and
 // O^T only for columns whose max actually grew.  Same softmax; P <= 2^kTh.
 //
-// Work split: context tiles fc = (c*nrc + rc)*ntile_c + t in [0, Tc) and
-// decode tiles fd = (i*g + c)*ntile_d + t in [0, Td) (memory order).  CTA k
-// of G takes context tiles [k*Tc/G, (k+1)*Tc/G) and then decode tiles
-// [k*Td/G, (k+1)*Td/G): every CTA streams the same number of 64 KB tiles (+-1
-// of each kind).  A maximal run of tiles of one context chunk (c, rc) or one
-// decode chunk (i, cb) is a segment and writes one partial (m, l, o) for
-// every row of its chunk to its workspace slot (context slots [0, Sc),
-// decode slots [Sc, S)).
+// Work split: flat tiles f in [0, Tc + Td): context tiles first,
+// f = (c*nrc + rc)*ntile_c + t, then decode tiles in Kd memory order,
+// f = Tc + (i*g + c)*ntile_d + t.  CTA k streams the contiguous range
+// [cs[k], cs[k+1]) planned on the host (bifattn_api.cu, plan_split): equal
+// 64 KB-tile counts, except that a range crossing into another chunk is
+// charged a segment-switch penalty and boundaries snap to chunk ends when
+// close.  A maximal run of tiles of one context chunk (c, rc) or one decode
+// chunk (i, cb) is a segment and writes one partial (m, l, o) for every row
+// of its chunk to its workspace slot (context slots [0, Sc), decode slots
+// [Sc, S)).
 #pragma once
 #include "common.cuh"
 #include "tc_ptx.cuh"
 
 namespace ba {
+
+constexpr int bif_max_ctas = 160;
 
 struct BifTcParams {
   CUtensorMap tmKc, tmVc;  // Kc/Vc as 3D (d, mc, g), box (64, 128, 1), SW128
@@ -70,6 +74,7 @@ struct BifTcParams {
   int qd_rows;               // rows of the decode q box = min(N, h)
   long long Tc, Td;          // context tiles, decode tiles
   int G, nst;
+  int cs[bif_max_ctas + 1];  // CTA k streams flat tiles [cs[k], cs[k+1]) of [context | decode]
   float scale_log2;
   int S, Sc;                 // slots per row; decode slots start at Sc
   float* ws_o;               // [b*h][S][128]
@@ -105,15 +110,19 @@ __host__ __device__ constexpr int smem_fixed(int N) {
   return 4 * 256 * N + 4 * (4 * N + 8 * N + 2 * N + 2 * N) + 256 + 512;
 }
 
-// CTA owning flat tile f when T tiles are split over G CTAs as [kT/G, (k+1)T/G)
-__host__ __device__ inline int owner(long long f, long long T, int G) {
-  return (int)(((f + 1) * (long long)G - 1) / T);
+// CTA owning flat tile f (the CTA ranges [cs[k], cs[k+1]) are non-empty and
+// cover [0, Tc + Td)): binary search of the start table.
+__host__ __device__ inline int owner(const int* cs, int G, long long f) {
+  int lo = 0, hi = G - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (cs[mid] <= f) lo = mid; else hi = mid - 1;
+  }
+  return lo;
 }
-// Rank, among the distinct CTAs covering tiles [a, ...], of the CTA whose part
-// starts at tile f (f = a or a CTA range start).  With T >= G every CTA range
-// is non-empty; with T < G each CTA gets at most one tile.
-__host__ __device__ inline int part_rank(long long a, long long f, long long T, int G) {
-  return T >= G ? owner(f, T, G) - owner(a, T, G) : (int)(f - a);
+// Number of CTAs that cover flat tiles [a, e) (e > a).
+__host__ __device__ inline int parts_of(const int* cs, int G, long long a, long long e) {
+  return owner(cs, G, e - 1) - owner(cs, G, a) + 1;
 }
 
 struct Seg {
@@ -132,19 +141,16 @@ BA_DEVINL int dec_len(const BifTcParams& P, int i) {
   return P.lens_offset + L;
 }
 
-// This CTA's work is the concatenation [context range | decode range]; work
-// index w < nc is context tile fc0 + w, else decode tile fd0 + (w - nc).
+// This CTA's work: flat tiles [f0, f1) of [context tiles | decode tiles];
+// work index w = f - f0.
 struct Range {
-  long long fc0, fc1, fd0, fd1;
-  BA_DEVINL long long n() const { return (fc1 - fc0) + (fd1 - fd0); }
+  long long f0, f1;
+  BA_DEVINL long long n() const { return f1 - f0; }
 };
 BA_DEVINL Range my_range(const BifTcParams& P) {
   Range r;
-  const long long k = blockIdx.x, G = P.G;
-  r.fc0 = k * P.Tc / G;
-  r.fc1 = (k + 1) * P.Tc / G;
-  r.fd0 = k * P.Td / G;
-  r.fd1 = (k + 1) * P.Td / G;
+  r.f0 = P.cs[blockIdx.x];
+  r.f1 = P.cs[blockIdx.x + 1];
   return r;
 }
 
@@ -161,11 +167,10 @@ __host__ __device__ inline long long dec_chunk_end(long long g, long long gpc, l
 
 BA_DEVINL Seg seg_at(const BifTcParams& P, const Range& rg, long long w) {
   Seg s;
-  const long long nc = rg.fc1 - rg.fc0;
-  if (w < nc) {
-    const long long f = rg.fc0 + w;
+  const long long f = rg.f0 + w;
+  if (f < P.Tc) {
     const long long seg = f / P.ntile_c;
-    const long long fend = min((seg + 1) * P.ntile_c, rg.fc1);
+    const long long fend = min((seg + 1) * P.ntile_c, rg.f1);
     s.dec = false;
     s.c = (int)(seg / P.nrc);
     s.rc = (int)(seg % P.nrc);
@@ -173,21 +178,21 @@ BA_DEVINL Seg seg_at(const BifTcParams& P, const Range& rg, long long w) {
     s.t0 = (int)(f - seg * P.ntile_c);
     s.c0 = s.c;
     s.ntiles = (int)(fend - f);
-    s.slot = part_rank(seg * P.ntile_c, f, P.Tc, P.G);
+    s.slot = (int)blockIdx.x - owner(P.cs, P.G, seg * P.ntile_c);
     s.next = w + (fend - f);
   } else {
-    const long long f = rg.fd0 + (w - nc);
-    const long long ic = f / P.ntile_d;  // i*g + c
+    const long long fd = f - P.Tc;
+    const long long ic = fd / P.ntile_d;  // i*g + c
     s.dec = true;
     s.i = (int)(ic / P.g);
     s.c0 = (int)(ic % P.g);
     s.cb = s.c0 / P.gpc;
     s.c = s.rc = 0;
-    s.t0 = (int)(f - ic * P.ntile_d);
-    const long long a = dec_chunk_begin(P.g, P.gpc, P.ntile_d, s.i, s.cb);
-    const long long fend = min(dec_chunk_end(P.g, P.gpc, P.ntile_d, s.i, s.cb), rg.fd1);
+    s.t0 = (int)(fd - ic * P.ntile_d);
+    const long long a = P.Tc + dec_chunk_begin(P.g, P.gpc, P.ntile_d, s.i, s.cb);
+    const long long fend = min(P.Tc + dec_chunk_end(P.g, P.gpc, P.ntile_d, s.i, s.cb), rg.f1);
     s.ntiles = (int)(fend - f);
-    s.slot = P.Sc + part_rank(a, f, P.Td, P.G);
+    s.slot = P.Sc + (int)blockIdx.x - owner(P.cs, P.G, a);
     s.next = w + (fend - f);
   }
   return s;
@@ -197,13 +202,13 @@ BA_DEVINL Seg seg_at(const BifTcParams& P, const Range& rg, long long w) {
 __host__ __device__ inline int ctx_parts(const BifTcParams& P, int c, int rc) {
   if (P.Tc == 0) return 0;
   const long long ff = ((long long)c * P.nrc + rc) * P.ntile_c;
-  return part_rank(ff, ff + P.ntile_c - 1, P.Tc, P.G) + 1;
+  return parts_of(P.cs, P.G, ff, ff + P.ntile_c);
 }
 __host__ __device__ inline int dec_parts(const BifTcParams& P, int i, int cb) {
   if (P.Td == 0) return 0;
-  const long long a = dec_chunk_begin(P.g, P.gpc, P.ntile_d, i, cb);
-  const long long e = dec_chunk_end(P.g, P.gpc, P.ntile_d, i, cb);
-  return part_rank(a, e - 1, P.Td, P.G) + 1;
+  const long long a = P.Tc + dec_chunk_begin(P.g, P.gpc, P.ntile_d, i, cb);
+  const long long e = P.Tc + dec_chunk_end(P.g, P.gpc, P.ntile_d, i, cb);
+  return parts_of(P.cs, P.G, a, e);
 }
 
 // output row of column col of a segment's chunk, or -1 for padding

@@ -12,6 +12,7 @@
 // The replicated-KV baseline runs the same kernels with no context branch.
 #include <algorithm>
 #include <mutex>
+#include <vector>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -100,6 +101,7 @@ struct Plan {
   int tc_N = 0, tc_nrc = 0, tc_ntile_c = 0, tc_ntile_d = 0, tc_G = 0, tc_nst = 0;
   int tc_Sc = 0, tc_Sd = 0, tc_smem = 0;
   long long tc_Tc = 0, tc_T = 0;
+  int tc_cs[ba::bif_max_ctas + 1];
   size_t off_cnt = 0;
   // FMA context branch
   int nsc = 0, ctx_chunk = 0, rb_c = 1, nrb_c = 0;
@@ -110,6 +112,51 @@ struct Plan {
   size_t off_o = 0, off_ml = 0, ws_bytes = 0;
   int launches = 0;
 };
+
+// Split the flat tile sequence [0, T) (chunk ends `ends`, increasing, last =
+// T) into G non-empty contiguous CTA ranges cs[0..G].  Each CTA gets about the
+// same cost = tiles + kSegPenalty per extra chunk it enters; a range stops at
+// a chunk end when the leftover budget could not pay for another segment.
+void plan_split(const std::vector<long long>& ends, long long T, int G, int* cs) {
+  static const double kSegPenalty = [] {
+    const char* e = getenv("BIFATTN_SEG_PENALTY");
+    return e ? atof(e) : 2.0;
+  }();
+  long long cur = 0;
+  size_t ci = 0;  // index of the chunk containing cur
+  for (int k = 0; k < G; ++k) {
+    cs[k] = (int)cur;
+    const int left = G - k;
+    if (left == 1) {
+      cur = T;
+      break;
+    }
+    // remaining virtual work: tiles + a penalty per remaining chunk start
+    const double vrem = (double)(T - cur) + kSegPenalty * (double)(ends.size() - ci - 1);
+    double budget = vrem / left;
+    const long long max_end = T - (left - 1);  // leave >= 1 tile per remaining CTA
+    long long start = cur;
+    while (cur < T) {
+      const long long r = ends[ci] - cur;
+      if ((double)r <= budget + 0.5) {
+        cur = ends[ci];
+        budget -= (double)r;
+        ++ci;
+        if (budget < kSegPenalty + 1.0) break;  // no room for another segment
+        budget -= kSegPenalty;
+      } else {
+        long long take = (long long)(budget + 0.5);
+        if (take < 1 && cur == start) take = 1;
+        cur += take;
+        break;
+      }
+    }
+    if (cur <= start) cur = start + 1;
+    if (cur > max_end) cur = max_end;
+    while (ci < ends.size() && ends[ci] <= cur) ++ci;
+  }
+  cs[G] = (int)T;
+}
 
 int pick_rb(int rows) { return rows >= 4 ? 4 : (rows >= 2 ? 2 : 1); }
 
@@ -162,30 +209,28 @@ int make_plan(const ba_problem_t* pr, int sms, bool replicated, Plan* pl) {
     P.tc_ntile_d = cdiv(P.lens_offset + P.dec_cap, 128);
     P.tc_Tc = (long long)g * P.tc_nrc * P.tc_ntile_c;
     P.tc_T = P.tc_Tc + (long long)g * b * P.tc_ntile_d;
-    P.tc_G = (int)(P.tc_T < sms ? P.tc_T : sms);
-    const long long Td = P.tc_T - P.tc_Tc;
+    const int gmax = sms < ba::bif_max_ctas ? sms : ba::bif_max_ctas;
+    P.tc_G = (int)(P.tc_T < gmax ? P.tc_T : gmax);
     const int avail = 227 * 1024 - ba::bif::smem_fixed(tcN);  // dynamic smem is 1 KB aligned
     P.tc_nst = avail / ba::bif::kStageBytes;
     if (P.tc_nst > 4) P.tc_nst = 4;
     P.tc_smem = P.tc_nst * ba::bif::kStageBytes + ba::bif::smem_fixed(tcN);
-    // slots: the most CTAs one context (c, rc) / decode (i, c) sequence is split over
-    auto parts = [&](long long ff, long long n, long long T) {
-      return ba::bif::part_rank(ff, ff + n - 1, T, P.tc_G) + 1;
-    };
-    int sc = 0, sd = 0;
-    for (long long seg = 0; P.tc_ntile_c && seg < (long long)g * P.tc_nrc; ++seg) {
-      const int n = parts(seg * P.tc_ntile_c, P.tc_ntile_c, P.tc_Tc);
-      if (n > sc) sc = n;
-    }
     const int gpc = tcN / p;  // groups per decode chunk
     const int ndc = (g + gpc - 1) / gpc;
-    for (int i = 0; P.tc_ntile_d && i < b; ++i) {
-      for (int cb = 0; cb < ndc; ++cb) {
-        const long long a = ba::bif::dec_chunk_begin(g, gpc, P.tc_ntile_d, i, cb);
-        const long long e = ba::bif::dec_chunk_end(g, gpc, P.tc_ntile_d, i, cb);
-        const int n = parts(a, e - a, Td);
-        if (n > sd) sd = n;
-      }
+    // chunk ends in the flat [context | decode] tile space
+    std::vector<long long> ends;
+    for (long long k = 0; P.tc_ntile_c && k < (long long)g * P.tc_nrc; ++k)
+      ends.push_back((k + 1) * P.tc_ntile_c);
+    for (int i = 0; P.tc_ntile_d && i < b; ++i)
+      for (int cb = 0; cb < ndc; ++cb)
+        ends.push_back(P.tc_Tc + ba::bif::dec_chunk_end(g, gpc, P.tc_ntile_d, i, cb));
+    plan_split(ends, P.tc_T, P.tc_G, P.tc_cs);
+    int sc = 0, sd = 0;
+    long long prev = 0;
+    for (size_t k = 0; k < ends.size(); ++k) {
+      const int n = ba::bif::parts_of(P.tc_cs, P.tc_G, prev, ends[k]);
+      if (prev < P.tc_Tc) sc = std::max(sc, n); else sd = std::max(sd, n);
+      prev = ends[k];
     }
     P.tc_Sc = sc;
     P.tc_Sd = sd;
@@ -381,6 +426,7 @@ int run_tc(const ba_problem_t* pr, const Plan& P, const void* q, const void* Kc,
   bp.ndc = (pr->g + bp.gpc - 1) / bp.gpc;
   bp.qd_rows = std::min(P.tc_N, pr->h);
   bp.Tc = P.tc_Tc; bp.Td = P.tc_T - P.tc_Tc; bp.G = P.tc_G; bp.nst = P.tc_nst;
+  memcpy(bp.cs, P.tc_cs, sizeof(int) * (P.tc_G + 1));
   bp.scale_log2 = scale_log2;
   bp.S = P.S; bp.Sc = P.tc_Sc;
   bp.ws_o = reinterpret_cast<float*>(static_cast<char*>(ws) + P.off_o);
@@ -651,6 +697,19 @@ const char* ba_launch_name(const ba_problem_t* prob, int k) {
 }
 
 void ba_set_trace_buffer(void* dev_buf) { g_trace = dev_buf; }
+
+int ba_plan_ctas(const ba_problem_t* prob, int32_t* cs, int cap) {
+  DevInfo di;
+  int sms = device_info(&di) == BA_OK ? di.sms : 148;
+  Plan P;
+  int rc = make_plan(prob, sms, false, &P);
+  if (rc) return rc;
+  if (!P.tc) return 0;
+  if (cs) {
+    for (int k = 0; k <= P.tc_G && k < cap; ++k) cs[k] = P.tc_cs[k];
+  }
+  return P.tc_G;
+}
 
 void ba_set_launch_events(void* const* events, int n) {
   g_events = n > 0 ? events : nullptr;
