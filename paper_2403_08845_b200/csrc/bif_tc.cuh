@@ -543,6 +543,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
           tc::mbar_wait(tc::smem_u32(&s_full[slot]), (u >> 1) & 1);
           tc::tc_fence_after();
           if (j == 0) stamp(3);
+          stamp(20);
           float xv[kNarrowP];
           if (h0) {
 #pragma unroll
@@ -636,6 +637,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
           }
           __syncwarp();
           if (lane == 0) tc::mbar_arrive(tc::smem_u32(&p_full[slot]));
+          stamp(23);
           // end of this group's tiles (or of this segment part): flush its row sums / max
           if (t == ntl - 1 || j == s.ntiles - 1) {
             if (!e_waited) {  // the epilogue has consumed this buffer's previous segment
