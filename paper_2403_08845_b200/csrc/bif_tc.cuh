@@ -701,6 +701,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
           float x[CPT];
           tmem_ld_cols<CPT>(tS + slot * N + col0 + lane_addr, reinterpret_cast<uint32_t*>(x));
           tc::tmem_ld_wait();
+          stamp(40);
           tc::tc_fence_before();
           __syncwarp();
           if (lane == 0) tc::mbar_arrive(tc::smem_u32(&s_free[slot]));
@@ -714,6 +715,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
             x[n] = vc ? fmaf(x[n], sl2, -mref) : kNegInf;
             need |= vc && (mr[n] == kNegInf || x[n] > kTh);
           }
+          stamp(41);
           const bool slowp = tc::named_bar_or(1, 32 * NSW, need);
           stamp(slowp ? 22 : 21);
           if (slowp) {
