@@ -82,6 +82,7 @@ struct BifTcParams {
   void* out;                 // [b][h][128] bf16
   float* lse;                // [b][h] or null
   unsigned long long* trace; // optional [G][kTraceSlots] globaltimer stamps (instrumentation)
+  int dbg_skip_softmax;      // experiment only: softmax warps skip all math (wrong results)
 };
 
 namespace bif {
@@ -554,6 +555,14 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
           tc::tc_fence_before();
           __syncwarp();
           if (lane == 0) tc::mbar_arrive(tc::smem_u32(&s_free[slot]));
+          if (P.dbg_skip_softmax) {
+            tc::mbar_wait(tc::smem_u32(&p_empty[slot]), ((u >> 1) & 1) ^ 1);
+            tc::fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(tc::smem_u32(&p_full[slot]));
+            if (++t == ntl) { t = 0; ++cl; }
+            continue;
+          }
           const bool vpos = t * kBM + pos < L;
           if (h0) {
 #pragma unroll
@@ -701,10 +710,17 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
           float x[CPT];
           tmem_ld_cols<CPT>(tS + slot * N + col0 + lane_addr, reinterpret_cast<uint32_t*>(x));
           tc::tmem_ld_wait();
-          stamp(40);
           tc::tc_fence_before();
           __syncwarp();
           if (lane == 0) tc::mbar_arrive(tc::smem_u32(&s_free[slot]));
+          if (P.dbg_skip_softmax) {
+            tc::mbar_wait(tc::smem_u32(&p_empty[slot]), ((u >> 1) & 1) ^ 1);
+            tc::fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(tc::smem_u32(&p_full[slot]));
+            if (++t == ntl) { t = 0; ++cl; }
+            continue;
+          }
           const bool vpos = t * kBM + pos < L;
           bool need = false;
 #pragma unroll
@@ -715,7 +731,6 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
             x[n] = vc ? fmaf(x[n], sl2, -mref) : kNegInf;
             need |= vc && (mr[n] == kNegInf || x[n] > kTh);
           }
-          stamp(41);
           const bool slowp = tc::named_bar_or(1, 32 * NSW, need);
           stamp(slowp ? 22 : 21);
           if (slowp) {
