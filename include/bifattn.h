@@ -84,11 +84,12 @@ typedef struct {
 } ba_problem_t;
 
 /* Bytes of device workspace bifurcated_attn_decode() / replicated_attn_decode()
- * need: fp32 partials (m, l, o[d]) per output row and split.  Returns 0 for an
- * invalid problem.  The workspace must be 16-byte aligned; it needs no
- * initialisation and is fully rewritten by every call, so one workspace
- * serves any number of back-to-back calls (and CUDA graph replays) on one
- * stream.  Calls that may run concurrently need separate workspaces. */
+ * need: a grid-barrier word pair at offset 0, then fp32 partials (m, l, o[d])
+ * per output row and split.  Returns 0 for an invalid problem.  The workspace
+ * must be 16-byte aligned and ZEROED ONCE before its first use (cudaMemset);
+ * every completed call leaves the barrier word reset, so one workspace serves
+ * any number of back-to-back calls (and CUDA graph replays) on one stream.
+ * Calls that may run concurrently need separate workspaces. */
 size_t ba_workspace_bytes(const ba_problem_t* prob);
 
 /* One decode step of bifurcated attention (see above).  Kc/Vc are read from
@@ -129,7 +130,8 @@ int replicated_attn_decode(const ba_problem_t* prob, const void* q, const void* 
                            void* workspace, size_t workspace_bytes, void* stream);
 
 /* Number of kernel launches one bifurcated_attn_decode() call makes for this
- * problem on the current device (for the benchmark's launch count). <0 on error. */
+ * problem on the current device (for the benchmark's launch count): 1 for the
+ * tensor-core plan (one cooperative launch), 3 for the CUDA-core plan. */
 int ba_launches_per_call(const ba_problem_t* prob);
 
 /* Human-readable kernel plan for this problem (static string owned by the

@@ -1,7 +1,7 @@
 // bif_tc.cuh — one incremental-decoding step of context-aware bifurcated
 // attention on the 5th-gen tensor cores (tcgen05 + TMEM + TMA), sm_100a:
-// one persistent streaming kernel (bif_tc_kernel) + one small LSE-merge
-// kernel chained with programmatic dependent launch (bif_merge_kernel).
+// ONE cooperative persistent kernel (bif_tc_kernel): stream + grid barrier +
+// LSE merge.
 //
 // What it computes (Eq. 3-4; App. E.3):
 //   context segments:  the R = b*p query rows of group c that share Kc[c] and
@@ -79,6 +79,7 @@ struct BifTcParams {
   int S, Sc;                 // slots per row; decode slots start at Sc
   float* ws_o;               // [b*h][S][128]
   float* ws_ml;              // [b*h][S][2]
+  unsigned* grid_ctr;        // grid barrier [count, generation] (self-resetting; zeroed once)
   void* out;                 // [b][h][128] bf16
   float* lse;                // [b][h] or null
   unsigned long long* trace; // optional [G][kTraceSlots] globaltimer stamps (instrumentation)
@@ -295,6 +296,56 @@ BA_DEVINL void warp_col_reduce(float* v, int lane) {
   }
 }
 
+// ----------------------------------------------------------------------------
+// LSE merge of one output row gr (one warp): join its context partials
+// [0, nctx) and decode partials [Sc, Sc + ndec) with one log-sum-exp.
+// ----------------------------------------------------------------------------
+BA_DEVINL void merge_row(const BifTcParams& P, int gr, int lane) {
+  const int i = gr / P.h, j = gr - (gr / P.h) * P.h;
+  const int c = j / P.p;
+  const int rc = (i * P.p + (j - c * P.p)) / P.N;
+  const int nctx = bif::ctx_parts(P, c, rc);
+  const int n = nctx + bif::dec_parts(P, i, c / P.gpc);
+  const float2* ml = reinterpret_cast<const float2*>(P.ws_ml) + (size_t)gr * P.S;
+  const float* obuf = P.ws_o + (size_t)gr * P.S * bif::kD;
+  float M = kNegInf;
+  for (int q = lane; q < n; q += 32) M = fmaxf(M, __ldcg(ml + (q < nctx ? q : P.Sc + q - nctx)).x);
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
+  const float Ms = (M == kNegInf) ? 0.f : M;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  float Lsum = 0.f;
+  for (int q0 = 0; q0 < n; q0 += 8) {
+    float2 mv[8];
+    float4 ov[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int q = q0 + k;
+      if (q < n) {
+        const int sl = q < nctx ? q : P.Sc + q - nctx;
+        mv[k] = __ldcg(ml + sl);
+        ov[k] = __ldcg(reinterpret_cast<const float4*>(obuf + (size_t)sl * bif::kD) + lane);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      if (q0 + k < n) {
+        const float wgt = ex2(mv[k].x - Ms);
+        Lsum = fmaf(wgt, mv[k].y, Lsum);
+        acc.x = fmaf(wgt, ov[k].x, acc.x);
+        acc.y = fmaf(wgt, ov[k].y, acc.y);
+        acc.z = fmaf(wgt, ov[k].z, acc.z);
+        acc.w = fmaf(wgt, ov[k].w, acc.w);
+      }
+    }
+  }
+  const float inv = 1.f / Lsum;
+  const uint2 packed = make_uint2(pack_bf16x2(acc.x * inv, acc.y * inv),
+                                  pack_bf16x2(acc.z * inv, acc.w * inv));
+  *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(P.out) + (size_t)gr * bif::kD + lane * 4) = packed;
+  if (P.lse && lane == 0) P.lse[gr] = (M + lg2(Lsum)) * kLn2;
+}
+
 template <int N, int SWG>
 __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
     bif_tc_kernel(const __grid_constant__ BifTcParams P) {
@@ -374,7 +425,10 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
-  // let the dependent merge kernel get launched early (it waits for our completion)
+  // programmatic dependent launch: the prologue above overlapped the previous
+  // kernel; wait for it before touching any global memory, and let the next
+  // launch start its own prologue
+  pdl_wait();
   pdl_launch_dependents();
   const uint32_t tmem = *tmem_holder;
   const uint32_t tS = tmem;          // S^T slots at columns [0,N), [N,2N)
@@ -892,60 +946,33 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
     tc::tc_fence_after();
     tc::tmem_dealloc(tmem, TMEM_COLS);
   }
-}
-
-// ----------------------------------------------------------------------------
-// LSE merge (PDL-chained after bif_tc_kernel): one warp per output row joins
-// its context partials [0, nctx) and decode partials [Sc, Sc + ndec).
-// ----------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) bif_merge_kernel(const __grid_constant__ BifTcParams P) {
-  pdl_wait();  // the streaming kernel's partials are complete and visible
-  const int gr = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (gr >= P.b * P.h) return;
-  const int i = gr / P.h, j = gr - (gr / P.h) * P.h;
-  const int c = j / P.p;
-  const int rc = (i * P.p + (j - c * P.p)) / P.N;
-  const int nctx = bif::ctx_parts(P, c, rc);
-  const int n = nctx + bif::dec_parts(P, i, c / P.gpc);
-  const float2* ml = reinterpret_cast<const float2*>(P.ws_ml) + (size_t)gr * P.S;
-  const float* obuf = P.ws_o + (size_t)gr * P.S * bif::kD;
-  float M = kNegInf;
-  for (int q = lane; q < n; q += 32) M = fmaxf(M, __ldcg(ml + (q < nctx ? q : P.Sc + q - nctx)).x);
-#pragma unroll
-  for (int off = 16; off >= 1; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
-  const float Ms = (M == kNegInf) ? 0.f : M;
-  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  float Lsum = 0.f;
-  for (int q0 = 0; q0 < n; q0 += 8) {
-    float2 mv[8];
-    float4 ov[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const int q = q0 + k;
-      if (q < n) {
-        const int sl = q < nctx ? q : P.Sc + q - nctx;
-        mv[k] = __ldcg(ml + sl);
-        ov[k] = __ldcg(reinterpret_cast<const float4*>(obuf + (size_t)sl * bif::kD) + lane);
-      }
+  // ---- grid-wide barrier (cooperative launch: all CTAs are resident), then
+  //      every CTA joins the partials of its share of the output rows ----
+  if (threadIdx.x == 0) {
+    // generation barrier: grid_ctr[0] counts arrivals (reset by the last
+    // arriver), grid_ctr[1] is the generation it then advances
+    unsigned gen;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(gen) : "l"(P.grid_ctr + 1) : "memory");
+    __threadfence();
+    const unsigned old = atomicAdd(P.grid_ctr, 1u);
+    if (old == (unsigned)P.G - 1u) {
+      P.grid_ctr[0] = 0u;
+      __threadfence();
+      atomicAdd(P.grid_ctr + 1, 1u);
+    } else {
+      unsigned g2;
+      do {
+        __nanosleep(64);
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(g2) : "l"(P.grid_ctr + 1) : "memory");
+      } while (g2 == gen);
     }
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      if (q0 + k < n) {
-        const float wgt = ex2(mv[k].x - Ms);
-        Lsum = fmaf(wgt, mv[k].y, Lsum);
-        acc.x = fmaf(wgt, ov[k].x, acc.x);
-        acc.y = fmaf(wgt, ov[k].y, acc.y);
-        acc.z = fmaf(wgt, ov[k].z, acc.z);
-        acc.w = fmaf(wgt, ov[k].w, acc.w);
-      }
-    }
+    __threadfence();
   }
-  const float inv = 1.f / Lsum;
-  const uint2 packed = make_uint2(pack_bf16x2(acc.x * inv, acc.y * inv),
-                                  pack_bf16x2(acc.z * inv, acc.w * inv));
-  *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(P.out) + (size_t)gr * bif::kD + lane * 4) = packed;
-  if (P.lse && lane == 0) P.lse[gr] = (M + lg2(Lsum)) * kLn2;
+  __syncthreads();
+  const int rows = P.b * P.h;
+  const int r0 = (int)((long long)blockIdx.x * rows / P.G);
+  const int r1 = (int)((long long)(blockIdx.x + 1) * rows / P.G);
+  for (int gr = r0 + warp; gr < r1; gr += (int)(blockDim.x >> 5)) merge_row(P, gr, lane);
 }
 
 }  // namespace ba

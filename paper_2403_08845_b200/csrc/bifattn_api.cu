@@ -237,12 +237,12 @@ int make_plan(const ba_problem_t* pr, int sms, bool replicated, Plan* pl) {
     P.S = sc + sd;
     if (P.S < 1) P.S = 1;
     const size_t rows = (size_t)b * h;
-    P.off_cnt = 0;
-    P.off_o = 0;
+    P.off_cnt = 0;                         // grid-barrier counter
+    P.off_o = 256;
     P.off_ml = P.off_o + rows * P.S * 128 * sizeof(float);
     P.ws_bytes = P.off_ml + rows * P.S * 2 * sizeof(float);
     P.ws_bytes = (P.ws_bytes + 255) & ~(size_t)255;
-    P.launches = 2;
+    P.launches = 1;
     *pl = P;
     return BA_OK;
   }
@@ -361,26 +361,23 @@ int launch_bif_tc_n(const ba::BifTcParams& bp, int smem, uint32_t flags, LaunchR
     g_last_cuda_error = (int)attr_err;
     return BA_ECUDA;
   }
-  rec.begin();
-  ba::bif_tc_kernel<N, SWG><<<bp.G, ba::bif::threads(SWG), smem, rec.st>>>(bp);
-  int rc = rec.end();
-  if (rc) return rc;
-  // LSE merge, chained with programmatic dependent launch: it is scheduled as
-  // the streaming kernel's CTAs retire and waits (griddepcontrol.wait) for
-  // its completion before reading the partials.
-  const int rows = bp.b * bp.h;
+  // one cooperative launch (all CTAs co-resident: the kernel ends with a grid
+  // barrier and the LSE merge); programmatic stream serialisation lets its
+  // prologue overlap the previous kernel on the stream
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((rows + 7) / 8);
-  cfg.blockDim = dim3(256);
-  cfg.dynamicSmemBytes = 0;
+  cfg.gridDim = dim3(bp.G);
+  cfg.blockDim = dim3(ba::bif::threads(SWG));
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = rec.st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = (flags & BA_FLAG_NO_PDL) ? 0 : 1;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = (flags & BA_FLAG_NO_PDL) ? 0 : 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   rec.begin();
-  cudaError_t e = cudaLaunchKernelEx(&cfg, ba::bif_merge_kernel, bp);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, ba::bif_tc_kernel<N, SWG>, bp);
   if (e != cudaSuccess) {
     g_last_cuda_error = (int)e;
     rec.end();
@@ -431,6 +428,7 @@ int run_tc(const ba_problem_t* pr, const Plan& P, const void* q, const void* Kc,
   bp.S = P.S; bp.Sc = P.tc_Sc;
   bp.ws_o = reinterpret_cast<float*>(static_cast<char*>(ws) + P.off_o);
   bp.ws_ml = reinterpret_cast<float*>(static_cast<char*>(ws) + P.off_ml);
+  bp.grid_ctr = reinterpret_cast<unsigned*>(static_cast<char*>(ws) + P.off_cnt);
   bp.out = out;
   bp.lse = lse;
   bp.trace = static_cast<unsigned long long*>(g_trace);
@@ -672,7 +670,7 @@ const char* ba_plan_string(const ba_problem_t* prob) {
   if (P.tc)
     snprintf(g_plan_buf, sizeof g_plan_buf,
              "fused_tc(N=%d,nrc=%d,ctx_tiles=%lld,dec_tiles=%lld,ctas=%d,stages=%d,slots=%d+%d,"
-             "smem=%d) launches=2 ws=%zu",
+             "smem=%d) launches=1 ws=%zu",
              P.tc_N, P.tc_nrc, P.tc_Tc, P.tc_T - P.tc_Tc, P.tc_G, P.tc_nst, P.tc_Sc, P.tc_Sd,
              P.tc_smem, P.ws_bytes);
   else
@@ -692,7 +690,6 @@ const char* ba_launch_name(const ba_problem_t* prob, int k) {
   int n = 0;
   if (P.tc) {
     names[n++] = "fused_tc";
-    names[n++] = "merge_tc";
   } else {
     if (P.ctx_mode == 1) names[n++] = "ctx_fma";
     if (P.nsd > 0) names[n++] = "dec_fma";
