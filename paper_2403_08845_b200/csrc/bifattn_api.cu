@@ -370,8 +370,12 @@ int launch_bif_tc_n(const ba::BifTcParams& bp, int smem, uint32_t flags, LaunchR
   cfg.dynamicSmemBytes = smem;
   cfg.stream = rec.st;
   cudaLaunchAttribute attr[2];
+  static const int no_coop = [] {  // experiment: plain launch (CTAs are resident anyway)
+    const char* e = getenv("BIFATTN_NO_COOP");
+    return e ? atoi(e) : 0;
+  }();
   attr[0].id = cudaLaunchAttributeCooperative;
-  attr[0].val.cooperative = 1;
+  attr[0].val.cooperative = no_coop ? 0 : 1;
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[1].val.programmaticStreamSerializationAllowed = (flags & BA_FLAG_NO_PDL) ? 0 : 1;
   cfg.attrs = attr;
