@@ -390,6 +390,10 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 36);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  auto tstamp = [&](int slot, unsigned long long tag) {
+    if (P.trace) P.trace[(size_t)blockIdx.x * kTraceSlots + slot] = (gtimer() & 0x00ffffffffffffffull) | (tag << 56);
+  };
+  if (threadIdx.x == 0) tstamp(250, 50);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < NST; ++s) {
@@ -430,6 +434,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
   // launch start its own prologue
   pdl_wait();
   pdl_launch_dependents();
+  if (threadIdx.x == 0) tstamp(254, 54);
   const uint32_t tmem = *tmem_holder;
   const uint32_t tS = tmem;          // S^T slots at columns [0,N), [N,2N)
   const uint32_t tO = tmem + 2 * N;  // O^T buffers at [2N,3N), [3N,4N)
@@ -942,6 +947,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
   }
   tc::tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) tstamp(251, 51);
   if (warp == 2) {
     tc::tc_fence_after();
     tc::tmem_dealloc(tmem, TMEM_COLS);
@@ -969,10 +975,13 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
     __threadfence();
   }
   __syncthreads();
+  if (threadIdx.x == 0) tstamp(252, 52);
   const int rows = P.b * P.h;
   const int r0 = (int)((long long)blockIdx.x * rows / P.G);
   const int r1 = (int)((long long)(blockIdx.x + 1) * rows / P.G);
   for (int gr = r0 + warp; gr < r1; gr += (int)(blockDim.x >> 5)) merge_row(P, gr, lane);
+  __syncthreads();
+  if (threadIdx.x == 0) tstamp(253, 53);
 }
 
 }  // namespace ba
