@@ -299,22 +299,16 @@ BA_DEVINL void warp_col_reduce(float* v, int lane) {
 // ----------------------------------------------------------------------------
 // LSE merge of one output row gr (one warp): join its context partials
 // [0, nctx) and decode partials [Sc, Sc + ndec) with one log-sum-exp.
+// (m is in log2 units; l and o are relative to 2^m.)
 // ----------------------------------------------------------------------------
-BA_DEVINL void merge_row(const BifTcParams& P, int gr, int lane) {
-  const int i = gr / P.h, j = gr - (gr / P.h) * P.h;
-  const int c = j / P.p;
-  const int rc = (i * P.p + (j - c * P.p)) / P.N;
-  const int nctx = bif::ctx_parts(P, c, rc);
-  const int n = nctx + bif::dec_parts(P, i, c / P.gpc);
+BA_DEVINL void merge_row(const BifTcParams& P, int gr, int lane, int nctx, int ndec) {
+  const int n = nctx + ndec;
   const float2* ml = reinterpret_cast<const float2*>(P.ws_ml) + (size_t)gr * P.S;
   const float* obuf = P.ws_o + (size_t)gr * P.S * bif::kD;
-  float M = kNegInf;
-  for (int q = lane; q < n; q += 32) M = fmaxf(M, __ldcg(ml + (q < nctx ? q : P.Sc + q - nctx)).x);
-#pragma unroll
-  for (int off = 16; off >= 1; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
-  const float Ms = (M == kNegInf) ? 0.f : M;
+  float M = kNegInf, Lsum = 0.f;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  float Lsum = 0.f;
+  // running-max merge over batches of 8 partials; every load of a batch is
+  // issued before any is used (one L2 round trip per batch)
   for (int q0 = 0; q0 < n; q0 += 8) {
     float2 mv[8];
     float4 ov[8];
@@ -327,6 +321,14 @@ BA_DEVINL void merge_row(const BifTcParams& P, int gr, int lane) {
         ov[k] = __ldcg(reinterpret_cast<const float4*>(obuf + (size_t)sl * bif::kD) + lane);
       }
     }
+    float Mb = M;
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (q0 + k < n) Mb = fmaxf(Mb, mv[k].x);
+    const float Ms = (Mb == kNegInf) ? 0.f : Mb;
+    const float a = (M == kNegInf) ? 0.f : ex2(M - Ms);
+    Lsum *= a;
+    acc.x *= a; acc.y *= a; acc.z *= a; acc.w *= a;
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       if (q0 + k < n) {
@@ -338,6 +340,7 @@ BA_DEVINL void merge_row(const BifTcParams& P, int gr, int lane) {
         acc.w = fmaf(wgt, ov[k].w, acc.w);
       }
     }
+    M = Mb;
   }
   const float inv = 1.f / Lsum;
   const uint2 packed = make_uint2(pack_bf16x2(acc.x * inv, acc.y * inv),
@@ -954,32 +957,46 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
   }
   // ---- grid-wide barrier (cooperative launch: all CTAs are resident), then
   //      every CTA joins the partials of its share of the output rows ----
+  // part counts of this CTA's merge rows (computed while waiting)
+  const int rows = P.b * P.h;
+  const int r0 = (int)((long long)blockIdx.x * rows / P.G);
+  const int r1 = (int)((long long)(blockIdx.x + 1) * rows / P.G);
+  const int nwarps = (int)(blockDim.x >> 5);
+  int my_gr = r0 + warp, my_nctx = 0, my_ndec = 0;
+  if (my_gr < r1) {
+    const int i = my_gr / P.h, j = my_gr - i * P.h;
+    const int c = j / P.p;
+    my_nctx = ctx_parts(P, c, (i * P.p + (j - c * P.p)) / P.N);
+    my_ndec = dec_parts(P, i, c / P.gpc);
+  }
   if (threadIdx.x == 0) {
     // generation barrier: grid_ctr[0] counts arrivals (reset by the last
     // arriver), grid_ctr[1] is the generation it then advances
     unsigned gen;
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(gen) : "l"(P.grid_ctr + 1) : "memory");
-    __threadfence();
-    const unsigned old = atomicAdd(P.grid_ctr, 1u);
+    unsigned old;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(P.grid_ctr) : "memory");
     if (old == (unsigned)P.G - 1u) {
-      P.grid_ctr[0] = 0u;
-      __threadfence();
-      atomicAdd(P.grid_ctr + 1, 1u);
+      asm volatile("st.relaxed.gpu.global.u32 [%0], 0;" ::"l"(P.grid_ctr) : "memory");
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(P.grid_ctr + 1) : "memory");
     } else {
       unsigned g2;
       do {
-        __nanosleep(64);
         asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(g2) : "l"(P.grid_ctr + 1) : "memory");
       } while (g2 == gen);
     }
-    __threadfence();
   }
   __syncthreads();
   if (threadIdx.x == 0) tstamp(252, 52);
-  const int rows = P.b * P.h;
-  const int r0 = (int)((long long)blockIdx.x * rows / P.G);
-  const int r1 = (int)((long long)(blockIdx.x + 1) * rows / P.G);
-  for (int gr = r0 + warp; gr < r1; gr += (int)(blockDim.x >> 5)) merge_row(P, gr, lane);
+  for (int gr = my_gr; gr < r1; gr += nwarps) {
+    if (gr != my_gr) {
+      const int i = gr / P.h, j = gr - i * P.h;
+      const int c = j / P.p;
+      my_nctx = ctx_parts(P, c, (i * P.p + (j - c * P.p)) / P.N);
+      my_ndec = dec_parts(P, i, c / P.gpc);
+    }
+    merge_row(P, gr, lane, my_nctx, my_ndec);
+  }
   __syncthreads();
   if (threadIdx.x == 0) tstamp(253, 53);
 }

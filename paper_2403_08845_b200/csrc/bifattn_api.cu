@@ -117,11 +117,21 @@ struct Plan {
 // T) into G non-empty contiguous CTA ranges cs[0..G].  Each CTA gets about the
 // same cost = tiles + kSegPenalty per extra chunk it enters; a range stops at
 // a chunk end when the leftover budget could not pay for another segment.
-void plan_split(const std::vector<long long>& ends, long long T, int G, int* cs) {
+void plan_split(const std::vector<long long>& ends, long long T, long long Tc, int G, int* cs) {
   static const double kSegPenalty = [] {
     const char* e = getenv("BIFATTN_SEG_PENALTY");
     return e ? atof(e) : 2.0;
   }();
+  // decode tiles (narrow softmax path) cost more than context tiles
+  static const double kDecCost = [] {
+    const char* e = getenv("BIFATTN_DEC_COST");
+    return e ? atof(e) : 1.1;
+  }();
+  // cost of tiles [a, b)
+  auto cost = [&](long long a, long long b) {
+    const long long c0 = std::min(b, Tc) - std::min(a, Tc);
+    return (double)c0 + kDecCost * (double)((b - a) - c0);
+  };
   long long cur = 0;
   size_t ci = 0;  // index of the chunk containing cur
   for (int k = 0; k < G; ++k) {
@@ -131,21 +141,22 @@ void plan_split(const std::vector<long long>& ends, long long T, int G, int* cs)
       cur = T;
       break;
     }
-    // remaining virtual work: tiles + a penalty per remaining chunk start
-    const double vrem = (double)(T - cur) + kSegPenalty * (double)(ends.size() - ci - 1);
+    // remaining virtual work: tile costs + a penalty per remaining chunk start
+    const double vrem = cost(cur, T) + kSegPenalty * (double)(ends.size() - ci - 1);
     double budget = vrem / left;
     const long long max_end = T - (left - 1);  // leave >= 1 tile per remaining CTA
     long long start = cur;
     while (cur < T) {
-      const long long r = ends[ci] - cur;
-      if ((double)r <= budget + 0.5) {
+      const double rc = cost(cur, ends[ci]);
+      if (rc <= budget + 0.5) {
+        budget -= rc;
         cur = ends[ci];
-        budget -= (double)r;
         ++ci;
         if (budget < kSegPenalty + 1.0) break;  // no room for another segment
         budget -= kSegPenalty;
       } else {
-        long long take = (long long)(budget + 0.5);
+        const double unit = cur < Tc ? 1.0 : kDecCost;
+        long long take = (long long)(budget / unit + 0.5);
         if (take < 1 && cur == start) take = 1;
         cur += take;
         break;
@@ -224,7 +235,7 @@ int make_plan(const ba_problem_t* pr, int sms, bool replicated, Plan* pl) {
     for (int i = 0; P.tc_ntile_d && i < b; ++i)
       for (int cb = 0; cb < ndc; ++cb)
         ends.push_back(P.tc_Tc + ba::bif::dec_chunk_end(g, gpc, P.tc_ntile_d, i, cb));
-    plan_split(ends, P.tc_T, P.tc_G, P.tc_cs);
+    plan_split(ends, P.tc_T, P.tc_Tc, P.tc_G, P.tc_cs);
     int sc = 0, sd = 0;
     long long prev = 0;
     for (size_t k = 0; k < ends.size(); ++k) {
