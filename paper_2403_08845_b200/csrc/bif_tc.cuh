@@ -83,7 +83,8 @@ struct BifTcParams {
   void* out;                 // [b][h][128] bf16
   float* lse;                // [b][h] or null
   unsigned long long* trace; // optional [G][kTraceSlots] globaltimer stamps (instrumentation)
-  int dbg_skip_softmax;      // experiment only: softmax warps skip all math (wrong results)
+  int dbg;                   // experiment bits (wrong results): 1 skip softmax math, 2 PV skips P_lo,
+                             // 4/8 general/narrow P write skips the PV(u-1) wait
 };
 
 namespace bif {
@@ -540,18 +541,21 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
         tc::mbar_wait(tc::smem_u32(&o_empty[ob]), ((sg >> 1) & 1) ^ 1);
         for (int j = 0; j < s.ntiles; ++j, ++u) {
           const uint32_t st = u % NST;
-          const uint32_t slot = u & 1;
-          tc::mbar_wait(tc::smem_u32(&p_full[slot]), (u >> 1) & 1);
+          tc::mbar_wait(tc::smem_u32(&p_full[0]), u & 1);
           tc::tc_fence_after();
           const uint32_t vbase = tc::smem_u32(sm_stage + st * kStageBytes + 32768);
-          const uint32_t pbase = p_addr + slot * QB;
+          // P = P_hi + P_lo (two bf16 parts): O^T += V^T P_hi^T + V^T P_lo^T
 #pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            const uint64_t ad = tc::smem_desc(vbase + k * 2048, 16384, 1024, tc::kSw128);
-            const uint64_t bd = tc::smem_desc(pbase + k * 16 * PRB, PLBO, 8 * PRB, p_layout(N));
-            tc::mma_bf16(tO + ob * N, ad, bd, IDESC_PV, (j == 0 && k == 0) ? 0u : 1u);
+          for (int part = 0; part < ((P.dbg & 2) ? 1 : 2); ++part) {
+            const uint32_t pbase = p_addr + part * QB;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              const uint64_t ad = tc::smem_desc(vbase + k * 2048, 16384, 1024, tc::kSw128);
+              const uint64_t bd = tc::smem_desc(pbase + k * 16 * PRB, PLBO, 8 * PRB, p_layout(N));
+              tc::mma_bf16(tO + ob * N, ad, bd, IDESC_PV, (j == 0 && part == 0 && k == 0) ? 0u : 1u);
+            }
           }
-          tc::mma_commit(tc::smem_u32(&p_empty[slot]));
+          tc::mma_commit(tc::smem_u32(&p_empty[0]));
           tc::mma_commit(tc::smem_u32(&kv_empty[st]));
           if (P.trace && u < 256)
             P.trace[(size_t)blockIdx.x * kTraceSlots + 768 + u] = (gtimer() & 0x00ffffffffffffffull) | (32ull << 56);
@@ -617,11 +621,11 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
           tc::tc_fence_before();
           __syncwarp();
           if (lane == 0) tc::mbar_arrive(tc::smem_u32(&s_free[slot]));
-          if (P.dbg_skip_softmax) {
-            tc::mbar_wait(tc::smem_u32(&p_empty[slot]), ((u >> 1) & 1) ^ 1);
+          if (P.dbg & 1) {
+            tc::mbar_wait(tc::smem_u32(&p_empty[0]), (u & 1) ^ 1);
             tc::fence_proxy_async_smem();
             __syncwarp();
-            if (lane == 0) tc::mbar_arrive(tc::smem_u32(&p_full[slot]));
+            if (lane == 0) tc::mbar_arrive(tc::smem_u32(&p_full[0]));
             if (++t == ntl) { t = 0; ++cl; }
             continue;
           }
@@ -668,8 +672,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
               }
             }
             if (resc) {  // uniform over half-0 warps (same shared values)
-              const uint32_t pvu = u - 1;
-              tc::mbar_wait(tc::smem_u32(&p_empty[pvu & 1]), (pvu >> 1) & 1);
+              tc::mbar_wait(tc::smem_u32(&p_empty[0]), (u & 1) ^ 1);  // PV(u-1) done
               tc::tc_fence_after();
 #pragma unroll
               for (int k = 0; k < kNarrowP; ++k) {
@@ -684,30 +687,32 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
               tc::tmem_st_wait();
               tc::tc_fence_before();
             }
-            // P row of this position: zeros except the p valid columns
-            tc::mbar_wait(tc::smem_u32(&p_empty[slot]), ((u >> 1) & 1) ^ 1);
-            uint8_t* pbuf = sm_p + slot * QB;
+            // P row of this position (hi and lo parts): zeros except the p valid columns
+            if (!(P.dbg & 8)) tc::mbar_wait(tc::smem_u32(&p_empty[0]), (u & 1) ^ 1);  // PV(u-1) done
 #pragma unroll
             for (int n = 0; n < N; n += 8) {
               uint32_t off = (uint32_t)((n / W) * PLBO + pos * PRB + (n % W) * 2);
               off ^= ((off >> 7) & PSWM) << 4;
-              *reinterpret_cast<uint4*>(pbuf + off) = make_uint4(0, 0, 0, 0);
+              *reinterpret_cast<uint4*>(sm_p + off) = make_uint4(0, 0, 0, 0);
+              *reinterpret_cast<uint4*>(sm_p + QB + off) = make_uint4(0, 0, 0, 0);
             }
 #pragma unroll
             for (int k = 0; k < kNarrowP; ++k) {
               if (k < P.p) {
                 const int col = cv0 + k;
-                const __nv_bfloat16 pb = __float2bfloat16_rn(pv[k]);
-                l_g[k] += __bfloat162float(pb);
+                const __nv_bfloat16 hi = __float2bfloat16_rn(pv[k]);
+                const __nv_bfloat16 lo = __float2bfloat16_rn(pv[k] - __bfloat162float(hi));
+                l_g[k] += pv[k];
                 uint32_t off = (uint32_t)((col / W) * PLBO + pos * PRB + (col % W) * 2);
                 off ^= ((off >> 7) & PSWM) << 4;
-                *reinterpret_cast<__nv_bfloat16*>(pbuf + off) = pb;
+                *reinterpret_cast<__nv_bfloat16*>(sm_p + off) = hi;
+                *reinterpret_cast<__nv_bfloat16*>(sm_p + QB + off) = lo;
               }
             }
             tc::fence_proxy_async_smem();
           }
           __syncwarp();
-          if (lane == 0) tc::mbar_arrive(tc::smem_u32(&p_full[slot]));
+          if (lane == 0) tc::mbar_arrive(tc::smem_u32(&p_full[0]));
           stamp(23);
           // end of this group's tiles (or of this segment part): flush its row sums / max
           if (t == ntl - 1 || j == s.ntiles - 1) {
@@ -775,11 +780,11 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
           tc::tc_fence_before();
           __syncwarp();
           if (lane == 0) tc::mbar_arrive(tc::smem_u32(&s_free[slot]));
-          if (P.dbg_skip_softmax) {
-            tc::mbar_wait(tc::smem_u32(&p_empty[slot]), ((u >> 1) & 1) ^ 1);
+          if (P.dbg & 1) {
+            tc::mbar_wait(tc::smem_u32(&p_empty[0]), (u & 1) ^ 1);
             tc::fence_proxy_async_smem();
             __syncwarp();
-            if (lane == 0) tc::mbar_arrive(tc::smem_u32(&p_full[slot]));
+            if (lane == 0) tc::mbar_arrive(tc::smem_u32(&p_full[0]));
             if (++t == ntl) { t = 0; ++cl; }
             continue;
           }
@@ -844,8 +849,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
             stamp(26);
             if (tc::named_bar_or(1, 32 * NSW, grew)) {
               // O^T holds earlier tiles of this segment: wait for PV(u-1), rescale
-              const uint32_t pvu = u - 1;
-              tc::mbar_wait(tc::smem_u32(&p_empty[pvu & 1]), (pvu >> 1) & 1);
+              tc::mbar_wait(tc::smem_u32(&p_empty[0]), (u & 1) ^ 1);  // PV(u-1) done
               tc::tc_fence_after();
 #pragma unroll
               for (int n = 0; n < CPT; n += 8) {
@@ -864,27 +868,29 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
               tc::tc_fence_before();
             }
           }
-          // ---- P = 2^x (bf16) into shared memory; row sums of the SAME bf16
-          //      values, so out = sum P v / sum P is a convex combination ----
-          tc::mbar_wait(tc::smem_u32(&p_empty[slot]), ((u >> 1) & 1) ^ 1);
-          uint8_t* pbuf = sm_p + slot * QB;
+          // ---- P = 2^x as two bf16 parts (P_hi + P_lo carries ~16 mantissa
+          //      bits) into shared memory; fp32 row sums ----
+          if (!(P.dbg & 4)) tc::mbar_wait(tc::smem_u32(&p_empty[0]), (u & 1) ^ 1);  // PV(u-1) done
 #pragma unroll
           for (int n = 0; n < CPT; n += 8) {
-            uint32_t pk[4];
+            uint32_t hk[4], lk[4];
 #pragma unroll
             for (int e = 0; e < 8; e += 2) {
-              pk[e / 2] = pack_bf16x2(ex2(x[n + e]), ex2(x[n + e + 1]));
-              l_part[n + e] += bf16lo(pk[e / 2]);
-              l_part[n + e + 1] += bf16hi(pk[e / 2]);
+              const float p0 = ex2(x[n + e]), p1 = ex2(x[n + e + 1]);
+              l_part[n + e] += p0;
+              l_part[n + e + 1] += p1;
+              hk[e / 2] = pack_bf16x2(p0, p1);
+              lk[e / 2] = pack_bf16x2(p0 - bf16lo(hk[e / 2]), p1 - bf16hi(hk[e / 2]));
             }
             const int col = col0 + n;
             uint32_t off = (uint32_t)((col / W) * PLBO + pos * PRB + (col % W) * 2);
             off ^= ((off >> 7) & PSWM) << 4;
-            *reinterpret_cast<uint4*>(pbuf + off) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+            *reinterpret_cast<uint4*>(sm_p + off) = make_uint4(hk[0], hk[1], hk[2], hk[3]);
+            *reinterpret_cast<uint4*>(sm_p + QB + off) = make_uint4(lk[0], lk[1], lk[2], lk[3]);
           }
           tc::fence_proxy_async_smem();
           __syncwarp();
-          if (lane == 0) tc::mbar_arrive(tc::smem_u32(&p_full[slot]));
+          if (lane == 0) tc::mbar_arrive(tc::smem_u32(&p_full[0]));
           stamp(23);
           if (++t == ntl) {
             t = 0;

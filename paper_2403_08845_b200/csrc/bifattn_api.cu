@@ -448,10 +448,10 @@ int run_tc(const ba_problem_t* pr, const Plan& P, const void* q, const void* Kc,
   bp.lse = lse;
   bp.trace = static_cast<unsigned long long*>(g_trace);
   static const int dbg_skip = [] {
-    const char* e = getenv("BIFATTN_DBG_SKIP_SOFTMAX");
+    const char* e = getenv("BIFATTN_DBG");
     return e ? atoi(e) : 0;
   }();
-  bp.dbg_skip_softmax = dbg_skip;
+  bp.dbg = dbg_skip;
   LaunchRec rec(st);
   // softmax warpgroups (override for experiments: BIFATTN_SWG=1|2)
   static const int swg_env = [] {
