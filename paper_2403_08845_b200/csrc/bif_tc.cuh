@@ -350,6 +350,41 @@ BA_DEVINL void merge_row(const BifTcParams& P, int gr, int lane, int nctx, int n
   if (P.lse && lane == 0) P.lse[gr] = (M + lg2(Lsum)) * kLn2;
 }
 
+// Cycle accounting for experiments (BIFATTN_PROF builds only): per-role
+// accumulators of where time goes, dumped into the trace buffer at exit.
+#ifdef BIFATTN_PROF
+BA_DEVINL unsigned long long prof_clock() {
+  unsigned long long c;
+  asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
+  return c;
+}
+struct Prof {
+  unsigned long long acc[8];
+  unsigned long long last;
+  __device__ Prof() : last(prof_clock()) {
+    for (int k = 0; k < 8; ++k) acc[k] = 0;
+  }
+  BA_DEVINL void mark(int k) {
+    const unsigned long long now = prof_clock();
+    acc[k] += now - last;
+    last = now;
+  }
+  BA_DEVINL void count(int k) { acc[k] += 1; }
+  BA_DEVINL void dump(unsigned long long* tr, int base) {
+    if (tr)
+      for (int k = 0; k < 8; ++k) tr[base + k] = acc[k];
+  }
+};
+constexpr bool kStamp = false;
+#else
+constexpr bool kStamp = true;
+struct Prof {
+  BA_DEVINL void mark(int) {}
+  BA_DEVINL void count(int) {}
+  BA_DEVINL void dump(unsigned long long*, int) {}
+};
+#endif
+
 template <int N, int SWG>
 __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
     bif_tc_kernel(const __grid_constant__ BifTcParams P) {
@@ -395,7 +430,10 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   auto tstamp = [&](int slot, unsigned long long tag) {
-    if (P.trace) P.trace[(size_t)blockIdx.x * kTraceSlots + slot] = (gtimer() & 0x00ffffffffffffffull) | (tag << 56);
+    if (kStamp && P.trace) P.trace[(size_t)blockIdx.x * kTraceSlots + slot] = (gtimer() & 0x00ffffffffffffffull) | (tag << 56);
+#ifdef BIFATTN_PROF
+    if (P.trace) P.trace[(size_t)blockIdx.x * kTraceSlots + 48 + (slot - 250)] = prof_clock();
+#endif
   };
   if (threadIdx.x == 0) tstamp(250, 50);
 
@@ -449,6 +487,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
   if (warp == 0) {
     // ============================ TMA producer ============================
     if (lane == 0) {
+      Prof pf;
       uint32_t tt = 0, sg = 0;
       const uint64_t pol_c = P.nrc == 1 ? tc::policy_evict_first() : tc::policy_evict_last();
       const uint64_t pol_d = tc::policy_evict_first();
@@ -456,6 +495,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
         const Seg s = seg_at(P, rg, w);
         const uint32_t qbuf = sg & 1;
         tc::mbar_wait(tc::smem_u32(&q_empty[qbuf]), ((sg >> 1) & 1) ^ 1);
+        pf.mark(0);
         const uint32_t qb = tc::smem_u32(&q_full[qbuf]);
         const uint32_t qdst = tc::smem_u32(sm_q + qbuf * QB);
         if (!s.dec) {
@@ -467,6 +507,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
           tc::tma_load_3d(qdst, &P.tmQd, qb, 0, s.cb * P.gpc * P.p, s.i);
           tc::tma_load_3d(qdst + N * 128, &P.tmQd, qb, 64, s.cb * P.gpc * P.p, s.i);
         }
+        pf.mark(1);
         const CUtensorMap* mk = s.dec ? &P.tmKd : &P.tmKc;
         const CUtensorMap* mv = s.dec ? &P.tmVd : &P.tmVc;
         const uint64_t pol = s.dec ? pol_d : pol_c;
@@ -476,7 +517,8 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
           const int z = s.dec ? s.i * P.g + cg : s.c;  // TMA z: group, or sample*g + group
           const int st = tt % NST;
           tc::mbar_wait(tc::smem_u32(&kv_empty[st]), ((tt / NST) & 1) ^ 1);
-          if (P.trace && tt < 128) P.trace[(size_t)blockIdx.x * kTraceSlots + 256 + tt] = (gtimer() & 0x00ffffffffffffffull) | (30ull << 56);
+          pf.mark(2);
+          if (kStamp && P.trace && tt < 128) P.trace[(size_t)blockIdx.x * kTraceSlots + 256 + tt] = (gtimer() & 0x00ffffffffffffffull) | (30ull << 56);
           const uint32_t bar = tc::smem_u32(&kv_full[st]);
           tc::mbar_arrive_expect_tx(bar, kStageBytes);
           const uint32_t dst = tc::smem_u32(sm_stage + st * kStageBytes);
@@ -484,6 +526,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
           tc::tma_load_3d_hint(dst + 16384, mk, bar, 64, t * kBM, z, pol);
           tc::tma_load_3d_hint(dst + 32768, mv, bar, 0, t * kBM, z, pol);
           tc::tma_load_3d_hint(dst + 49152, mv, bar, 64, t * kBM, z, pol);
+          pf.mark(3);
           if (++t == ntl) {
             t = 0;
             ++cg;
@@ -491,6 +534,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
         }
         w = s.next;
       }
+      pf.dump(P.trace ? P.trace + (size_t)blockIdx.x * kTraceSlots : nullptr, 16);
     }
   } else if (warp == 1) {
     // ========================== QK issuer (one lane) ==========================
@@ -498,18 +542,22 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
     // released the S slot; blocking waits (no spinning on the SM's issue slots).
     if (lane == 0) {
       const uint32_t q_addr = tc::smem_u32(sm_q);
+      Prof pf;
       uint32_t u = 0, sg = 0;
       for (long long w = 0; w < nw; ++sg) {
         const Seg s = seg_at(P, rg, w);
         const uint32_t qbase = q_addr + (sg & 1) * QB;
         tc::mbar_wait(tc::smem_u32(&q_full[sg & 1]), (sg >> 1) & 1);
+        pf.mark(0);
         for (int j = 0; j < s.ntiles; ++j, ++u) {
           const uint32_t st = u % NST;
           const uint32_t slot = u & 1;
           tc::mbar_wait(tc::smem_u32(&kv_full[st]), (u / NST) & 1);
-          if (P.trace && u < 128)
+          pf.mark(1);
+          if (kStamp && P.trace && u < 128)
             P.trace[(size_t)blockIdx.x * kTraceSlots + 256 + 128 + u] = (gtimer() & 0x00ffffffffffffffull) | (33ull << 56);
           tc::mbar_wait(tc::smem_u32(&s_free[slot]), ((u >> 1) & 1) ^ 1);
+          pf.mark(2);
           tc::tc_fence_after();
           const uint32_t kbase = tc::smem_u32(sm_stage + st * kStageBytes);
 #pragma unroll
@@ -519,12 +567,14 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
             tc::mma_bf16(tS + slot * N, ad, bd, IDESC_QK, k > 0 ? 1u : 0u);
           }
           tc::mma_commit(tc::smem_u32(&s_full[slot]));
-          if (P.trace && u < 256)
+          pf.mark(3);
+          if (kStamp && P.trace && u < 256)
             P.trace[(size_t)blockIdx.x * kTraceSlots + 512 + u] = (gtimer() & 0x00ffffffffffffffull) | (31ull << 56);
         }
         tc::mma_commit(tc::smem_u32(&q_empty[sg & 1]));  // q buffer reusable
         w = s.next;
       }
+      pf.dump(P.trace ? P.trace + (size_t)blockIdx.x * kTraceSlots : nullptr, 24);
     }
   } else if (warp == 3) {
     // ========================== PV issuer (one lane) ==========================
@@ -534,14 +584,17 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
     // the softmax could produce P(u)).
     if (lane == 0) {
       const uint32_t p_addr = tc::smem_u32(sm_p);
+      Prof pf;
       uint32_t u = 0, sg = 0;
       for (long long w = 0; w < nw; ++sg) {
         const Seg s = seg_at(P, rg, w);
         const uint32_t ob = sg & 1;
         tc::mbar_wait(tc::smem_u32(&o_empty[ob]), ((sg >> 1) & 1) ^ 1);
+        pf.mark(0);
         for (int j = 0; j < s.ntiles; ++j, ++u) {
           const uint32_t st = u % NST;
           tc::mbar_wait(tc::smem_u32(&p_full[0]), u & 1);
+          pf.mark(1);
           tc::tc_fence_after();
           const uint32_t vbase = tc::smem_u32(sm_stage + st * kStageBytes + 32768);
           // P = P_hi + P_lo (two bf16 parts): O^T += V^T P_hi^T + V^T P_lo^T
@@ -557,12 +610,14 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
           }
           tc::mma_commit(tc::smem_u32(&p_empty[0]));
           tc::mma_commit(tc::smem_u32(&kv_empty[st]));
-          if (P.trace && u < 256)
+          pf.mark(2);
+          if (kStamp && P.trace && u < 256)
             P.trace[(size_t)blockIdx.x * kTraceSlots + 768 + u] = (gtimer() & 0x00ffffffffffffffull) | (32ull << 56);
         }
         tc::mma_commit(tc::smem_u32(&o_full[ob]));
         w = s.next;
       }
+      pf.dump(P.trace ? P.trace + (size_t)blockIdx.x * kTraceSlots : nullptr, 32);
     }
   } else if (warp >= 4 && warp < EPI0) {
     // ========================= softmax (NSW warps) ==========================
@@ -576,9 +631,10 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
     unsigned long long* tr = P.trace ? P.trace + (size_t)blockIdx.x * kTraceSlots : nullptr;
     int ntr = 0;
     auto stamp = [&](unsigned long long tag) {
-      if (tr && threadIdx.x == 128 && ntr < 256) tr[ntr++] = (gtimer() & 0x00ffffffffffffffull) | (tag << 56);
+      if (kStamp && tr && threadIdx.x == 128 && ntr < 256) tr[ntr++] = (gtimer() & 0x00ffffffffffffffull) | (tag << 56);
     };
     stamp(1);
+    Prof pf;
     // valid positions of a segment's sequence; decode lengths are prefetched one
     // segment ahead so no global-load latency sits on a segment boundary
     auto seg_len = [&](const Seg& q) { return q.dec ? dec_len(P, q.i) : P.mc; };
@@ -607,7 +663,9 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
         for (int j = 0; j < s.ntiles; ++j, ++u) {
           const int cv0 = cl * P.p;
           const uint32_t slot = u & 1;
+          pf.mark(6);
           tc::mbar_wait(tc::smem_u32(&s_full[slot]), (u >> 1) & 1);
+          pf.mark(0);
           tc::tc_fence_after();
           if (j == 0) stamp(3);
           stamp(20);
@@ -621,6 +679,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
           tc::tc_fence_before();
           __syncwarp();
           if (lane == 0) tc::mbar_arrive(tc::smem_u32(&s_free[slot]));
+          pf.mark(1);
           if (P.dbg & 1) {
             tc::mbar_wait(tc::smem_u32(&p_empty[0]), (u & 1) ^ 1);
             tc::fence_proxy_async_smem();
@@ -643,6 +702,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
             }
           }
           tc::named_bar_sync(2, 32 * NSW);
+          pf.mark(2);
           if (h0) {
             float pv[kNarrowP], alpha[kNarrowP], tm[kNarrowP];
             bool resc = false;
@@ -688,7 +748,9 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
               tc::tc_fence_before();
             }
             // P row of this position (hi and lo parts): zeros except the p valid columns
+            pf.mark(3);
             if (!(P.dbg & 8)) tc::mbar_wait(tc::smem_u32(&p_empty[0]), (u & 1) ^ 1);  // PV(u-1) done
+            pf.mark(4);
 #pragma unroll
             for (int n = 0; n < N; n += 8) {
               uint32_t off = (uint32_t)((n / W) * PLBO + pos * PRB + (n % W) * 2);
@@ -713,6 +775,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
           }
           __syncwarp();
           if (lane == 0) tc::mbar_arrive(tc::smem_u32(&p_full[0]));
+          pf.mark(5);
           stamp(23);
           // end of this group's tiles (or of this segment part): flush its row sums / max
           if (t == ntl - 1 || j == s.ntiles - 1) {
@@ -770,7 +833,9 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
           const int cv0 = s.dec ? cl * P.p : 0;
           const int cv1 = s.dec ? cv0 + P.p : N;
           const uint32_t slot = u & 1;
+          pf.mark(6);
           tc::mbar_wait(tc::smem_u32(&s_full[slot]), (u >> 1) & 1);
+          pf.mark(0);
           tc::tc_fence_after();
           if (j == 0) stamp(s.dec ? 3 : 2);
           stamp(20);
@@ -780,6 +845,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
           tc::tc_fence_before();
           __syncwarp();
           if (lane == 0) tc::mbar_arrive(tc::smem_u32(&s_free[slot]));
+          pf.mark(1);
           if (P.dbg & 1) {
             tc::mbar_wait(tc::smem_u32(&p_empty[0]), (u & 1) ^ 1);
             tc::fence_proxy_async_smem();
@@ -799,6 +865,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
             need |= vc && (mr[n] == kNegInf || x[n] > kTh);
           }
           const bool slowp = tc::named_bar_or(1, 32 * NSW, need);
+          pf.mark(2);
           stamp(slowp ? 22 : 21);
           if (slowp) {
             // ---- slow path: exact max of the tile's valid columns, new running max ----
@@ -870,7 +937,9 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
           }
           // ---- P = 2^x as two bf16 parts (P_hi + P_lo carries ~16 mantissa
           //      bits) into shared memory; fp32 row sums ----
+          pf.mark(3);
           if (!(P.dbg & 4)) tc::mbar_wait(tc::smem_u32(&p_empty[0]), (u & 1) ^ 1);  // PV(u-1) done
+          pf.mark(4);
 #pragma unroll
           for (int n = 0; n < CPT; n += 8) {
             uint32_t hk[4], lk[4];
@@ -891,6 +960,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
           tc::fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) tc::mbar_arrive(tc::smem_u32(&p_full[0]));
+          pf.mark(5);
           stamp(23);
           if (++t == ntl) {
             t = 0;
@@ -913,6 +983,9 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
       L = Ln;
     }
     stamp(7);
+    pf.mark(6);
+    if (threadIdx.x == 128 || threadIdx.x == 256)
+      pf.dump(P.trace ? P.trace + (size_t)blockIdx.x * kTraceSlots : nullptr, threadIdx.x == 128 ? 0 : 8);
   } else if (warp >= EPI0) {
     // ===================== epilogue warpgroup (4 warps) =====================
     // O^T lanes are d = 32*(warp%4) + lane; columns are the chunk's rows.

@@ -1,0 +1,156 @@
+// Streaming ceiling micro-benchmark (experiment only, not part of the library):
+// 148 persistent CTAs stream [rows][128] bf16 K and V buffers tile by tile with
+// TMA (SW128 boxes of 64x128, like bif_tc), a ring of NST stages of SB boxes,
+// and a consumer that releases each stage after `hold` ns. Reports GB/s.
+// build: nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -o /tmp/exp_stream scripts/exp_stream.cu
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cstdio>
+#include <cstdlib>
+#include <cstdint>
+
+typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                             const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                             CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                             CUtensorMapFloatOOBfill);
+
+__device__ __forceinline__ uint32_t su32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, int c) {
+  asm volatile("mbarrier.init.shared.b64 [%0], %1;" ::"r"(su32(b)), "r"(c));
+}
+__device__ __forceinline__ void mbar_expect(uint64_t* b, uint32_t tx) {
+  asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(tx) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t par) {
+  asm volatile(
+      "{\n .reg .pred p;\n W: mbarrier.try_wait.parity.shared.b64 p, [%0], %1;\n @!p bra W;\n}" ::"r"(
+          su32(b)),
+      "r"(par)
+      : "memory");
+}
+__device__ __forceinline__ void tma2(uint32_t dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+      "l"((uint64_t)m), "r"(su32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+struct Args {
+  CUtensorMap tk, tv;
+  int tiles;     // 128-row tiles
+  int nst;       // stages
+  int sub;       // 16 KB boxes per stage
+  int hold_ns;   // consumer hold per stage
+  int split;     // 1: K and V released separately (K right away, V after hold)
+};
+
+__global__ void __launch_bounds__(64, 1) stream_kernel(const __grid_constant__ Args a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t full[16], empty[16];
+  const int G = gridDim.x, k = blockIdx.x;
+  const int t0 = (int)((long)a.tiles * k / G), t1 = (int)((long)a.tiles * (k + 1) / G);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < a.nst; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  __syncthreads();
+  // ring of nst stages, each `sub` boxes of 16 KB (box j of tile t: K lo, K hi, V lo, V hi)
+  const long b0 = 4L * t0, b1 = 4L * t1;
+  if (threadIdx.x == 0) {
+    int u = 0;
+    for (long bx = b0; bx < b1; ++u) {
+      const int s = u % a.nst;
+      if (u >= a.nst) mbar_wait(&empty[s], ((u / a.nst) - 1) & 1);
+      const int n = (int)min((long)a.sub, b1 - bx);
+      mbar_expect(&full[s], 16384u * n);
+      const uint32_t base = su32(smem) + s * 16384u * a.sub;
+      for (int j = 0; j < n; ++j, ++bx) {
+        const int t = (int)(bx >> 2), w = (int)(bx & 3);
+        tma2(base + j * 16384u, (w < 2) ? &a.tk : &a.tv, &full[s], (w & 1) * 64, t * 128);
+      }
+    }
+  } else if (threadIdx.x == 32) {
+    int u = 0;
+    for (long bx = b0; bx < b1; ++u) {
+      const int s = u % a.nst;
+      mbar_wait(&full[s], (u / a.nst) & 1);
+      if (a.hold_ns) {
+        uint64_t st;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(st));
+        uint64_t now = st;
+        while (now - st < (uint64_t)a.hold_ns) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+      }
+      mbar_arrive(&empty[s]);
+      bx += min((long)a.sub, b1 - bx);
+    }
+  }
+}
+
+int main(int argc, char** argv) {
+  const long MB = argc > 1 ? atol(argv[1]) : 268;
+  const int nst = argc > 2 ? atoi(argv[2]) : 3;
+  const int sub = argc > 3 ? atoi(argv[3]) : 4;
+  const int hold = argc > 4 ? atoi(argv[4]) : 0;
+  const int G = argc > 5 ? atoi(argv[5]) : 148;
+  const long rows = MB * 1000000L / 2 / 256 / 128 * 128;  // K and V each rows x 256 B
+  void *K[2], *V[2];
+  for (int j = 0; j < 2; ++j) {
+    cudaMalloc(&K[j], rows * 256);
+    cudaMalloc(&V[j], rows * 256);
+    cudaMemset(K[j], 0, rows * 256);
+    cudaMemset(V[j], 0, rows * 256);
+  }
+  EncodeFn enc;
+  cudaDriverEntryPointQueryResult q;
+  cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&enc, cudaEnableDefault, &q);
+  Args a[2] = {};
+  cuuint64_t dims[2] = {128, (cuuint64_t)rows};
+  cuuint64_t str[1] = {256};
+  cuuint32_t box[2] = {64, 128}, es[2] = {1, 1};
+  for (int j = 0; j < 2; ++j) {
+    enc(&a[j].tk, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, K[j], dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    enc(&a[j].tv, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, V[j], dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    a[j].tiles = (int)(rows / 128);
+    a[j].nst = nst;
+    a[j].sub = sub;
+    a[j].hold_ns = hold;
+  }
+  const int smem = nst * sub * 16384;
+  if (smem > 227 * 1024) { printf("{\"err\":\"smem\"}\n"); return 1; }
+  cudaFuncSetAttribute(stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  float best = 1e9, tot = 0;
+  const int it = 20;
+  for (int i = 0; i < it + 3; ++i) {  // one launch per event pair
+    cudaEventRecord(e0);
+    stream_kernel<<<G, 64, smem>>>(a[i & 1]);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (i >= 3) { best = ms < best ? ms : best; tot += ms; }
+  }
+  cudaEventRecord(e0);  // back to back
+  for (int i = 0; i < 40; ++i) stream_kernel<<<G, 64, smem>>>(a[i & 1]);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float bb;
+  cudaEventElapsedTime(&bb, e0, e1);
+  bb /= 40;
+  cudaError_t err = cudaGetLastError();
+  const double bytes = 2.0 * rows * 256;
+  printf("{\"MB\": %.1f, \"nst\": %d, \"sub\": %d, \"hold\": %d, \"G\": %d, \"us_best\": %.2f, \"us_mean\": %.2f, \"us_b2b\": %.2f, \"GBs_best\": %.1f, \"err\": \"%s\"}\n",
+         bytes / 1e6, nst, sub, hold, G, best * 1e3, tot / it * 1e3, bb * 1e3, bytes / (best * 1e-3) / 1e9,
+         cudaGetErrorString(err));
+  return 0;
+}
