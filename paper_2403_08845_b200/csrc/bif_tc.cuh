@@ -74,6 +74,7 @@ struct BifTcParams {
   int qd_rows;               // rows of the decode q box = min(N, h)
   long long Tc, Td;          // context tiles, decode tiles
   int G, nst;
+  int npb;                   // P buffer slots (1 or 2; each a P_hi, P_lo pair)
   int cs[bif_max_ctas + 1];  // CTA k streams flat tiles [cs[k], cs[k+1]) of [context | decode]
   float scale_log2;
   int S, Sc;                 // slots per row; decode slots start at Sc
@@ -83,7 +84,7 @@ struct BifTcParams {
   void* out;                 // [b][h][128] bf16
   float* lse;                // [b][h] or null
   unsigned long long* trace; // optional [G][kTraceSlots] globaltimer stamps (instrumentation)
-  int dbg;                   // experiment bits (wrong results): 1 skip softmax math, 2 PV skips P_lo,
+  int dbg;                   // experiment bits (wrong results): 1 skip softmax math,
                              // 4/8 general/narrow P write skips the PV(u-1) wait
 };
 
@@ -103,14 +104,15 @@ __host__ __device__ constexpr int p_atom(int N) { return (N % 64 == 0) ? 64 : ((
 __host__ __device__ constexpr int p_layout(int N) {
   return p_atom(N) == 64 ? tc::kSw128 : (p_atom(N) == 32 ? tc::kSw64 : tc::kSw32);
 }
-__host__ __device__ constexpr int tmem_cols(int N) {  // 2 S^T slots + 2 O^T buffers
-  return 4 * N <= 32 ? 32 : 4 * N <= 64 ? 64 : 4 * N <= 128 ? 128 : 4 * N <= 256 ? 256 : 512;
+// TMEM: 2 S^T slots (N columns) + 2 O^T buffers (2N: the P_hi and P_lo halves)
+__host__ __device__ constexpr int tmem_cols(int N) {
+  return 6 * N <= 32 ? 32 : 6 * N <= 64 ? 64 : 6 * N <= 128 ? 128 : 6 * N <= 256 ? 256 : 512;
 }
 // dynamic smem besides the stages: 2 q + 2 P buffers (256N B each), col-max
 // scratch [4][N], row sums [2][4][N], m_run [2][N], final m [2][N] (floats),
 // lengths [64] ints, barriers (512 B)
-__host__ __device__ constexpr int smem_fixed(int N) {
-  return 4 * 256 * N + 4 * (4 * N + 8 * N + 2 * N + 2 * N) + 256 + 512;
+__host__ __device__ constexpr int smem_fixed(int N, int npb) {
+  return (2 + 2 * npb) * 256 * N + 4 * (4 * N + 8 * N + 2 * N + 2 * N) + 256 + 512;
 }
 
 // CTA owning flat tile f (the CTA ranges [cs[k], cs[k+1]) are non-empty and
@@ -377,7 +379,11 @@ struct Prof {
 };
 constexpr bool kStamp = false;
 #else
-constexpr bool kStamp = true;
+#ifdef BIFATTN_TRACE
+constexpr bool kStamp = true;  // timeline stamps (experiment builds only)
+#else
+constexpr bool kStamp = false;
+#endif
 struct Prof {
   BA_DEVINL void mark(int) {}
   BA_DEVINL void count(int) {}
@@ -392,12 +398,13 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
   constexpr int NSW = 4 * SWG;               // softmax warps
   constexpr int CPT = N / SWG;               // columns per softmax thread
   constexpr int EPI0 = 4 + NSW;              // first epilogue warp
-  constexpr int W = p_atom(N);
+  constexpr int NP = 2 * N;                  // P / O^T width: [P_hi | P_lo] columns
+  constexpr int W = p_atom(NP);
   constexpr int PRB = 2 * W;
   constexpr int PLBO = kBM * PRB;
   constexpr int PSWM = W == 64 ? 7 : (W == 32 ? 3 : 1);
   constexpr uint32_t IDESC_QK = tc::idesc_bf16(128, N, 0, 0);
-  constexpr uint32_t IDESC_PV = tc::idesc_bf16(128, N, 1, 1);
+  constexpr uint32_t IDESC_PV = tc::idesc_bf16(128, NP, 1, 1);
   constexpr uint32_t TMEM_COLS = tmem_cols(N);
   constexpr int QB = 256 * N;  // bytes of one q buffer / one P buffer
   static_assert(N % 16 == 0 && N >= 16 && N <= 64 && CPT % 8 == 0 && CPT <= 32, "N");
@@ -407,8 +414,8 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
   const int NST = P.nst;
   uint8_t* sm_stage = smem;
   uint8_t* sm_q = smem + NST * kStageBytes;  // 2 buffers
-  uint8_t* sm_p = sm_q + 2 * QB;             // 2 buffers
-  float* sm_red = reinterpret_cast<float*>(sm_p + 2 * QB);  // [4][N] col max (slow path)
+  uint8_t* sm_p = sm_q + 2 * QB;             // npb slots of (P_hi, P_lo)
+  float* sm_red = reinterpret_cast<float*>(sm_p + 2 * P.npb * QB);  // [4][N] col max (slow path)
   float* sm_l = sm_red + 4 * N;                             // [2][4][N] row sums per O buffer
   float* sm_mold = sm_l + 8 * N;                            // [N] running max before a slow path
   float* sm_mfin = sm_mold + 2 * N;                         // [2][N] final max per O buffer
@@ -479,7 +486,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
   if (threadIdx.x == 0) tstamp(254, 54);
   const uint32_t tmem = *tmem_holder;
   const uint32_t tS = tmem;          // S^T slots at columns [0,N), [N,2N)
-  const uint32_t tO = tmem + 2 * N;  // O^T buffers at [2N,3N), [3N,4N)
+  const uint32_t tO = tmem + 2 * N;  // O^T buffers at [2N,4N), [4N,6N): O_hi | O_lo halves
 
   const Range rg = my_range(P);
   const long long nw = rg.n();
@@ -494,7 +501,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
       for (long long w = 0; w < nw; ++sg) {
         const Seg s = seg_at(P, rg, w);
         const uint32_t qbuf = sg & 1;
-        tc::mbar_wait(tc::smem_u32(&q_empty[qbuf]), ((sg >> 1) & 1) ^ 1);
+        if (P.dbg & 16384) tc::mbar_wait_sleep(tc::smem_u32(&q_empty[qbuf]), ((sg >> 1) & 1) ^ 1); else tc::mbar_wait(tc::smem_u32(&q_empty[qbuf]), ((sg >> 1) & 1) ^ 1);
         pf.mark(0);
         const uint32_t qb = tc::smem_u32(&q_full[qbuf]);
         const uint32_t qdst = tc::smem_u32(sm_q + qbuf * QB);
@@ -516,7 +523,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
         for (int j = 0; j < s.ntiles; ++j, ++tt) {
           const int z = s.dec ? s.i * P.g + cg : s.c;  // TMA z: group, or sample*g + group
           const int st = tt % NST;
-          tc::mbar_wait(tc::smem_u32(&kv_empty[st]), ((tt / NST) & 1) ^ 1);
+          tc::mbar_wait_sleep(tc::smem_u32(&kv_empty[st]), ((tt / NST) & 1) ^ 1);
           pf.mark(2);
           if (kStamp && P.trace && tt < 128) P.trace[(size_t)blockIdx.x * kTraceSlots + 256 + tt] = (gtimer() & 0x00ffffffffffffffull) | (30ull << 56);
           const uint32_t bar = tc::smem_u32(&kv_full[st]);
@@ -547,16 +554,16 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
       for (long long w = 0; w < nw; ++sg) {
         const Seg s = seg_at(P, rg, w);
         const uint32_t qbase = q_addr + (sg & 1) * QB;
-        tc::mbar_wait(tc::smem_u32(&q_full[sg & 1]), (sg >> 1) & 1);
+        if (P.dbg & 16384) tc::mbar_wait_sleep(tc::smem_u32(&q_full[sg & 1]), (sg >> 1) & 1); else tc::mbar_wait(tc::smem_u32(&q_full[sg & 1]), (sg >> 1) & 1);
         pf.mark(0);
         for (int j = 0; j < s.ntiles; ++j, ++u) {
           const uint32_t st = u % NST;
           const uint32_t slot = u & 1;
-          tc::mbar_wait(tc::smem_u32(&kv_full[st]), (u / NST) & 1);
+          tc::mbar_wait_sleep(tc::smem_u32(&kv_full[st]), (u / NST) & 1);
           pf.mark(1);
           if (kStamp && P.trace && u < 128)
             P.trace[(size_t)blockIdx.x * kTraceSlots + 256 + 128 + u] = (gtimer() & 0x00ffffffffffffffull) | (33ull << 56);
-          tc::mbar_wait(tc::smem_u32(&s_free[slot]), ((u >> 1) & 1) ^ 1);
+          if (P.dbg & 65536) tc::mbar_wait_sleep(tc::smem_u32(&s_free[slot]), ((u >> 1) & 1) ^ 1); else tc::mbar_wait(tc::smem_u32(&s_free[slot]), ((u >> 1) & 1) ^ 1);
           pf.mark(2);
           tc::tc_fence_after();
           const uint32_t kbase = tc::smem_u32(sm_stage + st * kStageBytes);
@@ -567,6 +574,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
             tc::mma_bf16(tS + slot * N, ad, bd, IDESC_QK, k > 0 ? 1u : 0u);
           }
           tc::mma_commit(tc::smem_u32(&s_full[slot]));
+          if (P.dbg & 1024) tc::mma_commit(tc::smem_u32(&kv_empty[st]));  // experiment: release at QK
           pf.mark(3);
           if (kStamp && P.trace && u < 256)
             P.trace[(size_t)blockIdx.x * kTraceSlots + 512 + u] = (gtimer() & 0x00ffffffffffffffull) | (31ull << 56);
@@ -589,27 +597,26 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
       for (long long w = 0; w < nw; ++sg) {
         const Seg s = seg_at(P, rg, w);
         const uint32_t ob = sg & 1;
-        tc::mbar_wait(tc::smem_u32(&o_empty[ob]), ((sg >> 1) & 1) ^ 1);
+        if (P.dbg & 16384) tc::mbar_wait_sleep(tc::smem_u32(&o_empty[ob]), ((sg >> 1) & 1) ^ 1); else tc::mbar_wait(tc::smem_u32(&o_empty[ob]), ((sg >> 1) & 1) ^ 1);
         pf.mark(0);
         for (int j = 0; j < s.ntiles; ++j, ++u) {
           const uint32_t st = u % NST;
-          tc::mbar_wait(tc::smem_u32(&p_full[0]), u & 1);
+          const uint32_t ps = P.npb == 2 ? (u & 1) : 0, ph = P.npb == 2 ? (u >> 1) : u;
+          tc::mbar_wait_sleep(tc::smem_u32(&p_full[ps]), ph & 1);
           pf.mark(1);
           tc::tc_fence_after();
           const uint32_t vbase = tc::smem_u32(sm_stage + st * kStageBytes + 32768);
-          // P = P_hi + P_lo (two bf16 parts): O^T += V^T P_hi^T + V^T P_lo^T
+          // P = P_hi + P_lo (two bf16 parts side by side): one MMA per K step
+          // gives [O_hi | O_lo]^T += V^T [P_hi | P_lo]^T, V read once
+          const uint32_t pbase = p_addr + 2 * ps * QB;
 #pragma unroll
-          for (int part = 0; part < ((P.dbg & 2) ? 1 : 2); ++part) {
-            const uint32_t pbase = p_addr + part * QB;
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
-              const uint64_t ad = tc::smem_desc(vbase + k * 2048, 16384, 1024, tc::kSw128);
-              const uint64_t bd = tc::smem_desc(pbase + k * 16 * PRB, PLBO, 8 * PRB, p_layout(N));
-              tc::mma_bf16(tO + ob * N, ad, bd, IDESC_PV, (j == 0 && part == 0 && k == 0) ? 0u : 1u);
-            }
+          for (int k = 0; k < ((P.dbg & 32) ? 0 : 8); ++k) {
+            const uint64_t ad = tc::smem_desc(vbase + k * 2048, 16384, 1024, tc::kSw128);
+            const uint64_t bd = tc::smem_desc(pbase + k * 16 * PRB, PLBO, 8 * PRB, p_layout(NP));
+            tc::mma_bf16(tO + ob * NP, ad, bd, IDESC_PV, (j == 0 && k == 0) ? 0u : 1u);
           }
-          tc::mma_commit(tc::smem_u32(&p_empty[0]));
-          tc::mma_commit(tc::smem_u32(&kv_empty[st]));
+          tc::mma_commit(tc::smem_u32(&p_empty[ps]));
+          if (!(P.dbg & 1024)) tc::mma_commit(tc::smem_u32(&kv_empty[st]));
           pf.mark(2);
           if (kStamp && P.trace && u < 256)
             P.trace[(size_t)blockIdx.x * kTraceSlots + 768 + u] = (gtimer() & 0x00ffffffffffffffull) | (32ull << 56);
@@ -643,7 +650,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
       const Seg s = seg_at(P, rg, w);
       const int Ln = s.next < nw ? seg_len(seg_at(P, rg, s.next)) : 0;  // used next segment
       const uint32_t ob = sg & 1;
-      const uint32_t tOb = tO + ob * N;
+      const uint32_t tOb = tO + ob * NP;
       int t = s.t0, cl = s.c0 - s.cb * P.gpc;  // tile index, group within the decode chunk
       const int ntl = s.dec ? P.ntile_d : P.ntile_c;
       if (s.dec && P.p <= kNarrowP) {
@@ -663,8 +670,10 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
         for (int j = 0; j < s.ntiles; ++j, ++u) {
           const int cv0 = cl * P.p;
           const uint32_t slot = u & 1;
+          const uint32_t ps = P.npb == 2 ? (u & 1) : 0, ph = P.npb == 2 ? (u >> 1) : u;  // P slot, its phase
           pf.mark(6);
-          tc::mbar_wait(tc::smem_u32(&s_full[slot]), (u >> 1) & 1);
+          if (P.dbg & 32768) tc::mbar_wait_sleep(tc::smem_u32(&s_full[slot]), (u >> 1) & 1);
+          else tc::mbar_wait(tc::smem_u32(&s_full[slot]), (u >> 1) & 1);
           pf.mark(0);
           tc::tc_fence_after();
           if (j == 0) stamp(3);
@@ -681,10 +690,10 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
           if (lane == 0) tc::mbar_arrive(tc::smem_u32(&s_free[slot]));
           pf.mark(1);
           if (P.dbg & 1) {
-            tc::mbar_wait(tc::smem_u32(&p_empty[0]), (u & 1) ^ 1);
+            tc::mbar_wait(tc::smem_u32(&p_empty[ps]), (ph & 1) ^ 1);
             tc::fence_proxy_async_smem();
             __syncwarp();
-            if (lane == 0) tc::mbar_arrive(tc::smem_u32(&p_full[0]));
+            if (lane == 0) tc::mbar_arrive(tc::smem_u32(&p_full[ps]));
             if (++t == ntl) { t = 0; ++cl; }
             continue;
           }
@@ -732,16 +741,19 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
               }
             }
             if (resc) {  // uniform over half-0 warps (same shared values)
-              tc::mbar_wait(tc::smem_u32(&p_empty[0]), (u & 1) ^ 1);  // PV(u-1) done
+              tc::mbar_wait(tc::smem_u32(&p_empty[(u - 1) % P.npb]), ((u - 1) / P.npb) & 1);  // PV(u-1) done
               tc::tc_fence_after();
 #pragma unroll
               for (int k = 0; k < kNarrowP; ++k) {
                 if (k < P.p && alpha[k] != 1.f) {
-                  uint32_t o1;
+                  uint32_t o1, o2;
                   tc::tmem_ld<1>(tOb + cv0 + k + lane_addr, &o1);
+                  tc::tmem_ld<1>(tOb + N + cv0 + k + lane_addr, &o2);
                   tc::tmem_ld_wait();
                   o1 = __float_as_uint(__uint_as_float(o1) * alpha[k]);
+                  o2 = __float_as_uint(__uint_as_float(o2) * alpha[k]);
                   tc::tmem_st<1>(tOb + cv0 + k + lane_addr, &o1);
+                  tc::tmem_st<1>(tOb + N + cv0 + k + lane_addr, &o2);
                 }
               }
               tc::tmem_st_wait();
@@ -749,14 +761,14 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
             }
             // P row of this position (hi and lo parts): zeros except the p valid columns
             pf.mark(3);
-            if (!(P.dbg & 8)) tc::mbar_wait(tc::smem_u32(&p_empty[0]), (u & 1) ^ 1);  // PV(u-1) done
+            if (!(P.dbg & 8)) tc::mbar_wait(tc::smem_u32(&p_empty[ps]), (ph & 1) ^ 1);  // PV(u-npb) done
+            uint8_t* const sm_pb = sm_p + 2 * ps * QB;
             pf.mark(4);
 #pragma unroll
-            for (int n = 0; n < N; n += 8) {
+            for (int n = 0; n < NP; n += 8) {
               uint32_t off = (uint32_t)((n / W) * PLBO + pos * PRB + (n % W) * 2);
               off ^= ((off >> 7) & PSWM) << 4;
-              *reinterpret_cast<uint4*>(sm_p + off) = make_uint4(0, 0, 0, 0);
-              *reinterpret_cast<uint4*>(sm_p + QB + off) = make_uint4(0, 0, 0, 0);
+              *reinterpret_cast<uint4*>(sm_pb + off) = make_uint4(0, 0, 0, 0);
             }
 #pragma unroll
             for (int k = 0; k < kNarrowP; ++k) {
@@ -767,14 +779,16 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
                 l_g[k] += pv[k];
                 uint32_t off = (uint32_t)((col / W) * PLBO + pos * PRB + (col % W) * 2);
                 off ^= ((off >> 7) & PSWM) << 4;
-                *reinterpret_cast<__nv_bfloat16*>(sm_p + off) = hi;
-                *reinterpret_cast<__nv_bfloat16*>(sm_p + QB + off) = lo;
+                uint32_t offl = (uint32_t)(((N + col) / W) * PLBO + pos * PRB + ((N + col) % W) * 2);
+                offl ^= ((offl >> 7) & PSWM) << 4;
+                *reinterpret_cast<__nv_bfloat16*>(sm_pb + off) = hi;
+                *reinterpret_cast<__nv_bfloat16*>(sm_pb + offl) = lo;
               }
             }
             tc::fence_proxy_async_smem();
           }
           __syncwarp();
-          if (lane == 0) tc::mbar_arrive(tc::smem_u32(&p_full[0]));
+          if (lane == 0) tc::mbar_arrive(tc::smem_u32(&p_full[ps]));
           pf.mark(5);
           stamp(23);
           // end of this group's tiles (or of this segment part): flush its row sums / max
@@ -829,12 +843,17 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
           l_part[n] = 0.f;
           mr[n] = kNegInf;
         }
+        // every column of this thread has a running max (uniform: mr is common
+        // to all positions); only a context segment gets there for all columns
+        bool all_set = false;
         for (int j = 0; j < s.ntiles; ++j, ++u) {
           const int cv0 = s.dec ? cl * P.p : 0;
           const int cv1 = s.dec ? cv0 + P.p : N;
           const uint32_t slot = u & 1;
+          const uint32_t ps = P.npb == 2 ? (u & 1) : 0, ph = P.npb == 2 ? (u >> 1) : u;  // P slot, its phase
           pf.mark(6);
-          tc::mbar_wait(tc::smem_u32(&s_full[slot]), (u >> 1) & 1);
+          if (P.dbg & 32768) tc::mbar_wait_sleep(tc::smem_u32(&s_full[slot]), (u >> 1) & 1);
+          else tc::mbar_wait(tc::smem_u32(&s_full[slot]), (u >> 1) & 1);
           pf.mark(0);
           tc::tc_fence_after();
           if (j == 0) stamp(s.dec ? 3 : 2);
@@ -847,24 +866,34 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
           if (lane == 0) tc::mbar_arrive(tc::smem_u32(&s_free[slot]));
           pf.mark(1);
           if (P.dbg & 1) {
-            tc::mbar_wait(tc::smem_u32(&p_empty[0]), (u & 1) ^ 1);
+            tc::mbar_wait(tc::smem_u32(&p_empty[ps]), (ph & 1) ^ 1);
             tc::fence_proxy_async_smem();
             __syncwarp();
-            if (lane == 0) tc::mbar_arrive(tc::smem_u32(&p_full[0]));
+            if (lane == 0) tc::mbar_arrive(tc::smem_u32(&p_full[ps]));
             if (++t == ntl) { t = 0; ++cl; }
             continue;
           }
-          const bool vpos = t * kBM + pos < L;
           bool need = false;
+          if (all_set && (t + 1) * kBM <= L) {
+            // fast path (warp-uniform): every column of this thread has its
+            // running max and every position of the tile is valid
 #pragma unroll
-          for (int n = 0; n < CPT; ++n) {
-            const int col = col0 + n;
-            const bool vc = vpos && col >= cv0 && col < cv1;
-            const float mref = (mr[n] == kNegInf) ? 0.f : mr[n];
-            x[n] = vc ? fmaf(x[n], sl2, -mref) : kNegInf;
-            need |= vc && (mr[n] == kNegInf || x[n] > kTh);
+            for (int n = 0; n < CPT; ++n) {
+              x[n] = fmaf(x[n], sl2, -mr[n]);
+              need |= x[n] > kTh;
+            }
+          } else {
+            const bool vpos = t * kBM + pos < L;
+#pragma unroll
+            for (int n = 0; n < CPT; ++n) {
+              const int col = col0 + n;
+              const bool vc = vpos && col >= cv0 && col < cv1;
+              const float mref = (mr[n] == kNegInf) ? 0.f : mr[n];
+              x[n] = vc ? fmaf(x[n], sl2, -mref) : kNegInf;
+              need |= vc && (mr[n] == kNegInf || x[n] > kTh);
+            }
           }
-          const bool slowp = tc::named_bar_or(1, 32 * NSW, need);
+          const bool slowp = (P.dbg & 4096) ? (bool)__any_sync(0xffffffffu, need) : tc::named_bar_or(1, 32 * NSW, need);
           pf.mark(2);
           stamp(slowp ? 22 : 21);
           if (slowp) {
@@ -912,24 +941,30 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
               grew |= (mo != kNegInf) && (mn > mo);
               mr[n] = mn;
             }
+            all_set = !s.dec;
+#pragma unroll
+            for (int n = 0; n < CPT; ++n) all_set = all_set && mr[n] != kNegInf;
             // (the vote's barrier also orders these sm_red reads before later writes)
             stamp(26);
             if (tc::named_bar_or(1, 32 * NSW, grew)) {
               // O^T holds earlier tiles of this segment: wait for PV(u-1), rescale
-              tc::mbar_wait(tc::smem_u32(&p_empty[0]), (u & 1) ^ 1);  // PV(u-1) done
+              tc::mbar_wait(tc::smem_u32(&p_empty[(u - 1) % P.npb]), ((u - 1) / P.npb) & 1);  // PV(u-1) done
               tc::tc_fence_after();
 #pragma unroll
               for (int n = 0; n < CPT; n += 8) {
-                uint32_t orr[8];
+                uint32_t orr[8], orl[8];
                 tc::tmem_ld<8>(tOb + col0 + n + lane_addr, orr);
+                tc::tmem_ld<8>(tOb + N + col0 + n + lane_addr, orl);
                 tc::tmem_ld_wait();
 #pragma unroll
                 for (int e = 0; e < 8; ++e) {
                   const float mo = sm_mold[col0 + n + e];
                   const float a = (mo == kNegInf) ? 1.f : ex2(mo - mr[n + e]);
                   orr[e] = __float_as_uint(__uint_as_float(orr[e]) * a);
+                  orl[e] = __float_as_uint(__uint_as_float(orl[e]) * a);
                 }
                 tc::tmem_st<8>(tOb + col0 + n + lane_addr, orr);
+                tc::tmem_st<8>(tOb + N + col0 + n + lane_addr, orl);
               }
               tc::tmem_st_wait();
               tc::tc_fence_before();
@@ -938,7 +973,8 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
           // ---- P = 2^x as two bf16 parts (P_hi + P_lo carries ~16 mantissa
           //      bits) into shared memory; fp32 row sums ----
           pf.mark(3);
-          if (!(P.dbg & 4)) tc::mbar_wait(tc::smem_u32(&p_empty[0]), (u & 1) ^ 1);  // PV(u-1) done
+          if (!(P.dbg & 4)) tc::mbar_wait(tc::smem_u32(&p_empty[ps]), (ph & 1) ^ 1);  // PV(u-npb) done
+          uint8_t* const sm_pb = sm_p + 2 * ps * QB;
           pf.mark(4);
 #pragma unroll
           for (int n = 0; n < CPT; n += 8) {
@@ -954,12 +990,16 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
             const int col = col0 + n;
             uint32_t off = (uint32_t)((col / W) * PLBO + pos * PRB + (col % W) * 2);
             off ^= ((off >> 7) & PSWM) << 4;
-            *reinterpret_cast<uint4*>(sm_p + off) = make_uint4(hk[0], hk[1], hk[2], hk[3]);
-            *reinterpret_cast<uint4*>(sm_p + QB + off) = make_uint4(lk[0], lk[1], lk[2], lk[3]);
+            uint32_t offl = (uint32_t)(((N + col) / W) * PLBO + pos * PRB + ((N + col) % W) * 2);
+            offl ^= ((offl >> 7) & PSWM) << 4;
+            if (!(P.dbg & 2048)) {
+              *reinterpret_cast<uint4*>(sm_pb + off) = make_uint4(hk[0], hk[1], hk[2], hk[3]);
+              *reinterpret_cast<uint4*>(sm_pb + offl) = make_uint4(lk[0], lk[1], lk[2], lk[3]);
+            }
           }
           tc::fence_proxy_async_smem();
           __syncwarp();
-          if (lane == 0) tc::mbar_arrive(tc::smem_u32(&p_full[0]));
+          if (lane == 0) tc::mbar_arrive(tc::smem_u32(&p_full[ps]));
           pf.mark(5);
           stamp(23);
           if (++t == ntl) {
@@ -997,23 +1037,27 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
     for (long long w = 0; w < nw; ++sg) {
       const Seg s = seg_at(P, rg, w);
       const uint32_t ob = sg & 1;
-      tc::mbar_wait(tc::smem_u32(&o_full[ob]), (sg >> 1) & 1);
+      if (P.dbg & 8192) tc::mbar_wait_sleep(tc::smem_u32(&o_full[ob]), (sg >> 1) & 1);
+      else tc::mbar_wait(tc::smem_u32(&o_full[ob]), (sg >> 1) & 1);
       tc::tc_fence_after();
 #pragma unroll
       for (int n = 0; n < N; n += 16) {
-        uint32_t orr[16];
-        tc::tmem_ld<16>(tO + ob * N + n + lane_addr, orr);
+        uint32_t orr[16], orl[16];
+        tc::tmem_ld<16>(tO + ob * NP + n + lane_addr, orr);
+        tc::tmem_ld<16>(tO + ob * NP + N + n + lane_addr, orl);
         tc::tmem_ld_wait();
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
           const int gr = row_of(P, s, n + e);
-          if (gr >= 0) P.ws_o[((size_t)gr * P.S + s.slot) * kD + d] = __uint_as_float(orr[e]);
+          if (gr >= 0)
+            P.ws_o[((size_t)gr * P.S + s.slot) * kD + d] = __uint_as_float(orr[e]) + __uint_as_float(orl[e]);
         }
       }
       tc::tc_fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(tc::smem_u32(&o_empty[ob]));
-      tc::mbar_wait(tc::smem_u32(&e_full[ob]), (sg >> 1) & 1);
+      if (P.dbg & 8192) tc::mbar_wait_sleep(tc::smem_u32(&e_full[ob]), (sg >> 1) & 1);
+      else tc::mbar_wait(tc::smem_u32(&e_full[ob]), (sg >> 1) & 1);
       if (et < N) {
         const int gr = row_of(P, s, et);
         if (gr >= 0) {

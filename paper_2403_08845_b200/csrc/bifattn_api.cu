@@ -98,7 +98,7 @@ struct Plan {
   int ctx_mode = 0;  // 0 none (replicated baseline), 1 FMA kernel, 2 in the tcgen05 kernel
   bool tc = false;   // single-launch tcgen05 plan
   // tcgen05 plan
-  int tc_N = 0, tc_nrc = 0, tc_ntile_c = 0, tc_ntile_d = 0, tc_G = 0, tc_nst = 0;
+  int tc_N = 0, tc_nrc = 0, tc_ntile_c = 0, tc_ntile_d = 0, tc_G = 0, tc_nst = 0, tc_npb = 1;
   int tc_Sc = 0, tc_Sd = 0, tc_smem = 0;
   long long tc_Tc = 0, tc_T = 0;
   int tc_cs[ba::bif_max_ctas + 1];
@@ -125,7 +125,7 @@ void plan_split(const std::vector<long long>& ends, long long T, long long Tc, i
   // decode tiles (narrow softmax path) cost more than context tiles
   static const double kDecCost = [] {
     const char* e = getenv("BIFATTN_DEC_COST");
-    return e ? atof(e) : 1.1;
+    return e ? atof(e) : 1.25;
   }();
   // cost of tiles [a, b)
   auto cost = [&](long long a, long long b) {
@@ -222,10 +222,20 @@ int make_plan(const ba_problem_t* pr, int sms, bool replicated, Plan* pl) {
     P.tc_T = P.tc_Tc + (long long)g * b * P.tc_ntile_d;
     const int gmax = sms < ba::bif_max_ctas ? sms : ba::bif_max_ctas;
     P.tc_G = (int)(P.tc_T < gmax ? P.tc_T : gmax);
-    const int avail = 227 * 1024 - ba::bif::smem_fixed(tcN);  // dynamic smem is 1 KB aligned
+    // P double-buffered when that keeps the K/V stage count (else one slot)
+    P.tc_npb = 2;
+    if ((227 * 1024 - ba::bif::smem_fixed(tcN, 2)) / ba::bif::kStageBytes <
+        (227 * 1024 - ba::bif::smem_fixed(tcN, 1)) / ba::bif::kStageBytes)
+      P.tc_npb = 1;
+    static const int npb_env = [] {  // experiment override: BIFATTN_NPB=1|2
+      const char* e = getenv("BIFATTN_NPB");
+      return e ? atoi(e) : 0;
+    }();
+    if (npb_env == 1 || npb_env == 2) P.tc_npb = npb_env;
+    const int avail = 227 * 1024 - ba::bif::smem_fixed(tcN, P.tc_npb);  // dynamic smem is 1 KB aligned
     P.tc_nst = avail / ba::bif::kStageBytes;
     if (P.tc_nst > 4) P.tc_nst = 4;
-    P.tc_smem = P.tc_nst * ba::bif::kStageBytes + ba::bif::smem_fixed(tcN);
+    P.tc_smem = P.tc_nst * ba::bif::kStageBytes + ba::bif::smem_fixed(tcN, P.tc_npb);
     const int gpc = tcN / p;  // groups per decode chunk
     const int ndc = (g + gpc - 1) / gpc;
     // chunk ends in the flat [context | decode] tile space
@@ -437,7 +447,7 @@ int run_tc(const ba_problem_t* pr, const Plan& P, const void* q, const void* Kc,
   bp.gpc = P.tc_N / p;
   bp.ndc = (pr->g + bp.gpc - 1) / bp.gpc;
   bp.qd_rows = std::min(P.tc_N, pr->h);
-  bp.Tc = P.tc_Tc; bp.Td = P.tc_T - P.tc_Tc; bp.G = P.tc_G; bp.nst = P.tc_nst;
+  bp.Tc = P.tc_Tc; bp.Td = P.tc_T - P.tc_Tc; bp.G = P.tc_G; bp.nst = P.tc_nst; bp.npb = P.tc_npb;
   memcpy(bp.cs, P.tc_cs, sizeof(int) * (P.tc_G + 1));
   bp.scale_log2 = scale_log2;
   bp.S = P.S; bp.Sc = P.tc_Sc;
@@ -458,12 +468,13 @@ int run_tc(const ba_problem_t* pr, const Plan& P, const void* q, const void* Kc,
     const char* e = getenv("BIFATTN_SWG");
     return e ? atoi(e) : 0;
   }();
-  const int swg = (swg_env == 1 || swg_env == 2) ? swg_env : ba::bif::softmax_wgs(P.tc_N);
+  const int swg = (swg_env == 1 || swg_env == 2 || (swg_env == 4 && P.tc_N == 32)) ? swg_env : ba::bif::softmax_wgs(P.tc_N);
   switch (P.tc_N * 4 + swg) {
     case 16 * 4 + 1: return launch_bif_tc_n<16, 1>(bp, P.tc_smem, pr->flags, rec);
     case 16 * 4 + 2: return launch_bif_tc_n<16, 2>(bp, P.tc_smem, pr->flags, rec);
     case 32 * 4 + 1: return launch_bif_tc_n<32, 1>(bp, P.tc_smem, pr->flags, rec);
     case 32 * 4 + 2: return launch_bif_tc_n<32, 2>(bp, P.tc_smem, pr->flags, rec);
+    case 32 * 4 + 4: return launch_bif_tc_n<32, 4>(bp, P.tc_smem, pr->flags, rec);
     case 48 * 4 + 2: return launch_bif_tc_n<48, 2>(bp, P.tc_smem, pr->flags, rec);
     case 64 * 4 + 2: return launch_bif_tc_n<64, 2>(bp, P.tc_smem, pr->flags, rec);
   }
@@ -684,10 +695,10 @@ const char* ba_plan_string(const ba_problem_t* prob) {
   }
   if (P.tc)
     snprintf(g_plan_buf, sizeof g_plan_buf,
-             "fused_tc(N=%d,nrc=%d,ctx_tiles=%lld,dec_tiles=%lld,ctas=%d,stages=%d,slots=%d+%d,"
-             "smem=%d) launches=1 ws=%zu",
-             P.tc_N, P.tc_nrc, P.tc_Tc, P.tc_T - P.tc_Tc, P.tc_G, P.tc_nst, P.tc_Sc, P.tc_Sd,
-             P.tc_smem, P.ws_bytes);
+             "fused_tc(N=%d,nrc=%d,ctx_tiles=%lld,dec_tiles=%lld,ctas=%d,stages=%d,pbuf=%d,"
+             "slots=%d+%d,smem=%d) launches=1 ws=%zu",
+             P.tc_N, P.tc_nrc, P.tc_Tc, P.tc_T - P.tc_Tc, P.tc_G, P.tc_nst, P.tc_npb, P.tc_Sc,
+             P.tc_Sd, P.tc_smem, P.ws_bytes);
   else
     snprintf(g_plan_buf, sizeof g_plan_buf,
              "ctx=fma(nsc=%d,chunk=%d,rb=%d) dec=fma(nsd=%d,chunk=%d,rb=%d) S=%d launches=%d "

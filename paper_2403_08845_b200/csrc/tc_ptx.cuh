@@ -37,6 +37,20 @@ BA_DEVINL void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
       : "memory");
 }
 // Wait until the phase with the given parity has completed.
+// Wait with a suspend-time hint: the thread may sleep until the phase
+// completes (or the hint expires) instead of re-polling, freeing issue slots
+// for the warps that do the math.  For waits off the critical path.
+BA_DEVINL void mbar_wait_sleep(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      " .reg .pred p;\n"
+      "WAITS_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      " @!p bra WAITS_%=;\n"
+      "}" ::"r"(bar),
+      "r"(parity), "r"(1000000u)
+      : "memory");
+}
 BA_DEVINL void mbar_wait(uint32_t bar, uint32_t parity) {
   asm volatile(
       "{\n"

@@ -15,6 +15,9 @@ import paper_2403_08845_b200 as ba
 from paper_2403_08845_b200 import _build
 
 
+DEC_COST = 1.25
+
+
 def owner(cs, f):
     lo, hi = 0, len(cs) - 2
     while lo < hi:
@@ -77,7 +80,9 @@ def model(b, h, g, mc, md, cs):
             sc = max(sc, parts)
         else:
             sd = max(sd, parts)
-    loads = [cs[k + 1] - cs[k] for k in range(G)]
+    # planner cost: decode tiles weigh DEC_COST (bifattn_api.cu, plan_split)
+    loads = [(min(cs[k + 1], Tc) - min(cs[k], Tc)) + DEC_COST * (max(cs[k + 1], Tc) - max(cs[k], Tc))
+             for k in range(G)]
     return N, sc, sd, loads
 
 
