@@ -448,6 +448,11 @@ int run_tc(const ba_problem_t* pr, const Plan& P, const void* q, const void* Kc,
   bp.ndc = (pr->g + bp.gpc - 1) / bp.gpc;
   bp.qd_rows = std::min(P.tc_N, pr->h);
   bp.Tc = P.tc_Tc; bp.Td = P.tc_T - P.tc_Tc; bp.G = P.tc_G; bp.nst = P.tc_nst; bp.npb = P.tc_npb;
+  static const int pf_env = [] {  // L2 prefetch distance (tiles; measured slower: off)
+    const char* e = getenv("BIFATTN_PF");
+    return e ? atoi(e) : 0;
+  }();
+  bp.pf_dist = pf_env;
   memcpy(bp.cs, P.tc_cs, sizeof(int) * (P.tc_G + 1));
   bp.scale_log2 = scale_log2;
   bp.S = P.S; bp.Sc = P.tc_Sc;

@@ -77,6 +77,14 @@ BA_DEVINL void tma_load_3d(uint32_t dst, const CUtensorMap* m, uint32_t bar, int
       "l"(reinterpret_cast<uint64_t>(m)), "r"(bar), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
 }
+// L2 prefetch of a 3-D box (no shared memory, no completion): warms L2 for a
+// later tma_load_3d of the same box.
+BA_DEVINL void tma_prefetch_3d(const CUtensorMap* m, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(
+                   reinterpret_cast<uint64_t>(m)),
+               "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
 BA_DEVINL void tma_load_3d_hint(uint32_t dst, const CUtensorMap* m, uint32_t bar, int c0, int c1,
                                 int c2, uint64_t policy) {
   asm volatile(

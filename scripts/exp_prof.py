@@ -11,6 +11,8 @@ from synth import CONFIGS, make_inputs
 
 name = sys.argv[1] if len(sys.argv) > 1 else "mha7b_b32"
 cfg = CONFIGS[name]
+if os.environ.get("EXP_MC"):
+    cfg = cfg.with_(mc=int(os.environ["EXP_MC"]), md=int(os.environ["EXP_MD"]))
 inp = make_inputs(cfg, 1, device="cuda")
 out = torch.empty_like(inp.q)
 prob = ba.make_problem(cfg.b, cfg.h, cfg.g, cfg.d, cfg.mc, cfg.md, cfg.torch_dtype, inp.scale)
