@@ -214,22 +214,48 @@ def _check(ts, dtype, device):
             raise ValueError(f"{name} has dtype {t.dtype}, expected {dtype}")
 
 
+_NAMES = ("q", "Kc", "Vc", "Kd", "Vd", "lens")
+_prob_cache = {}
+
+
+def _fast_check(ts, dtype, device):
+    """Per-call argument checks (the cheap common case; _check words the error)."""
+    for t in ts:
+        if not (t.is_cuda and t.device == device and t.is_contiguous()):
+            _check(dict(zip(_NAMES, ts)), dtype, device)
+    for t in ts[:5]:
+        if t.dtype != dtype:
+            _check(dict(zip(_NAMES, ts)), dtype, device)
+
+
+def _cached_problem(q, Kc, Kd, scale, flags):
+    key = (q.shape, Kc.shape, Kd.shape, q.dtype, scale, flags)
+    prob = _prob_cache.get(key)
+    if prob is None:
+        if len(_prob_cache) > 64:
+            _prob_cache.clear()
+        prob = _prob_cache[key] = _problem_from(q, Kc, Kd, scale, flags)
+    return prob
+
+
 def bifurcated_attn_decode(q, Kc, Vc, Kd, Vd, lens, out=None, lse=None, *, scale=None,
                            workspace=None, stream=None, flags=0):
     """One bifurcated decode step on the GPU.  Shapes: q [b,h,d]; Kc,Vc [g,mc,d];
     Kd,Vd [b,g,md_cap,d]; lens int32 [b].  Returns ``out`` [b,h,d]."""
-    lib = load_library()
-    _check(dict(q=q, Kc=Kc, Vc=Vc, Kd=Kd, Vd=Vd, lens=lens), q.dtype, q.device)
+    lib = _lib if _lib is not None else load_library()
+    _fast_check((q, Kc, Vc, Kd, Vd, lens), q.dtype, q.device)
     if lens.dtype != torch.int32:
         raise ValueError("lens must be int32")
-    prob = _problem_from(q, Kc, Kd, scale, flags)
+    prob = _cached_problem(q, Kc, Kd, scale, flags)
     if out is None:
         out = torch.empty_like(q)
     if workspace is None:
         workspace = alloc_workspace(prob, q.device)
-    rc = lib.bifurcated_attn_decode(ctypes.byref(prob), _ptr(q), _ptr(Kc), _ptr(Vc), _ptr(Kd),
-                                    _ptr(Vd), _ptr(lens), _ptr(out), _ptr(lse), _ptr(workspace),
-                                    workspace.numel(), _stream_handle(stream))
+    st = (stream if stream is not None else torch.cuda.current_stream()).cuda_stream
+    rc = lib.bifurcated_attn_decode(ctypes.byref(prob), q.data_ptr(), Kc.data_ptr(), Vc.data_ptr(),
+                                    Kd.data_ptr(), Vd.data_ptr(), lens.data_ptr(), out.data_ptr(),
+                                    lse.data_ptr() if lse is not None else None,
+                                    workspace.data_ptr(), workspace.numel(), st)
     if rc != 0:
         raise BifAttnError(rc, "bifurcated_attn_decode")
     return out

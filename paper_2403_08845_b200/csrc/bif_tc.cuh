@@ -76,6 +76,7 @@ struct BifTcParams {
   int G, nst;
   int npb;                   // P buffer slots (1 or 2; each a P_hi, P_lo pair)
   int pf_dist;               // L2 prefetch distance in tiles beyond the one being loaded (0: off)
+  int rot;                   // context segments start at tile (blockIdx*rot) mod length (0: in order)
   int cs[bif_max_ctas + 1];  // CTA k streams flat tiles [cs[k], cs[k+1]) of [context | decode]
   float scale_log2;
   int S, Sc;                 // slots per row; decode slots start at Sc
@@ -202,6 +203,13 @@ BA_DEVINL Seg seg_at(const BifTcParams& P, const Range& rg, long long w) {
     s.next = w + (fend - f);
   }
   return s;
+}
+
+// Tile streamed at step j of a context segment: the CTAs' streams start at
+// staggered offsets (rotation) so they do not walk the same DRAM pages in step.
+BA_DEVINL int ctx_tile(const BifTcParams& P, const Seg& s, int j) {
+  if (P.rot == 0 || s.ntiles <= 1) return s.t0 + j;
+  return s.t0 + (int)(((unsigned)j + (unsigned)blockIdx.x * (unsigned)P.rot) % (unsigned)s.ntiles);
 }
 
 // K/V box coordinates of the CTA's w-th tile: decode?, TMA z, tile index t.
@@ -540,6 +548,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
         int t = s.t0, cg = s.c0;
         for (int j = 0; j < s.ntiles; ++j, ++tt) {
           const int z = s.dec ? s.i * P.g + cg : s.c;  // TMA z: group, or sample*g + group
+          const int tl = s.dec ? t : ctx_tile(P, s, j);
           const int st = tt % NST;
           tc::mbar_wait_sleep(tc::smem_u32(&kv_empty[st]), ((tt / NST) & 1) ^ 1);
           pf.mark(2);
@@ -547,10 +556,10 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
           const uint32_t bar = tc::smem_u32(&kv_full[st]);
           tc::mbar_arrive_expect_tx(bar, kStageBytes);
           const uint32_t dst = tc::smem_u32(sm_stage + st * kStageBytes);
-          tc::tma_load_3d_hint(dst, mk, bar, 0, t * kBM, z, pol);
-          tc::tma_load_3d_hint(dst + 16384, mk, bar, 64, t * kBM, z, pol);
-          tc::tma_load_3d_hint(dst + 32768, mv, bar, 0, t * kBM, z, pol);
-          tc::tma_load_3d_hint(dst + 49152, mv, bar, 64, t * kBM, z, pol);
+          tc::tma_load_3d_hint(dst, mk, bar, 0, tl * kBM, z, pol);
+          tc::tma_load_3d_hint(dst + 16384, mk, bar, 64, tl * kBM, z, pol);
+          tc::tma_load_3d_hint(dst + 32768, mv, bar, 0, tl * kBM, z, pol);
+          tc::tma_load_3d_hint(dst + 49152, mv, bar, 64, tl * kBM, z, pol);
           // L2 prefetch pf_dist tiles ahead: more bytes in flight than the ring holds
           if (P.pf_dist > 0) {
             const long long wp = (long long)tt + P.pf_dist;
@@ -907,7 +916,8 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
             continue;
           }
           bool need = false;
-          if (all_set && (t + 1) * kBM <= L) {
+          const int tl = s.dec ? t : ctx_tile(P, s, j);
+          if (all_set && (tl + 1) * kBM <= L) {
             // fast path (warp-uniform): every column of this thread has its
             // running max and every position of the tile is valid
 #pragma unroll
@@ -916,7 +926,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
               need |= x[n] > kTh;
             }
           } else {
-            const bool vpos = t * kBM + pos < L;
+            const bool vpos = tl * kBM + pos < L;
 #pragma unroll
             for (int n = 0; n < CPT; ++n) {
               const int col = col0 + n;

@@ -352,7 +352,45 @@ EncodeTiledFn get_encode_fn() {
 }
 
 // 3D bf16 tensor map with a 128-byte-swizzled box of (64, box1, box2).
-int make_tmap_3d(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64_t d2,
+// Per-thread caches of plans and tensor maps: a decode loop calls with the
+// same problem (and usually the same buffers) every step, so planning and
+// cuTensorMapEncodeTiled are paid once (host cost per call, not GPU time).
+struct PlanKey {
+  ba_problem_t prob;
+  int sms;
+  bool replicated;
+};
+struct PlanEntry {
+  PlanKey key;
+  Plan plan;
+  bool valid = false;
+};
+thread_local PlanEntry g_plan_cache[4];
+thread_local int g_plan_next = 0;
+
+int cached_plan(const ba_problem_t* pr, int sms, bool replicated, const Plan** out) {
+  PlanKey k;
+  memset(&k, 0, sizeof k);
+  k.prob = *pr;
+  k.sms = sms;
+  k.replicated = replicated;
+  for (auto& e : g_plan_cache)
+    if (e.valid && memcmp(&e.key, &k, sizeof k) == 0) {
+      *out = &e.plan;
+      return BA_OK;
+    }
+  PlanEntry& e = g_plan_cache[g_plan_next];
+  g_plan_next = (g_plan_next + 1) & 3;
+  e.valid = false;
+  const int rc = make_plan(pr, sms, replicated, &e.plan);
+  if (rc) return rc;
+  e.key = k;
+  e.valid = true;
+  *out = &e.plan;
+  return BA_OK;
+}
+
+int encode_tmap_3d(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64_t d2,
                  uint64_t stride1_bytes, uint64_t stride2_bytes, uint32_t box1, uint32_t box2) {
   EncodeTiledFn fn = get_encode_fn();
   if (!fn) return BA_ECUDA;
@@ -367,6 +405,34 @@ int make_tmap_3d(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uin
     g_last_cuda_error = 1000 + (int)r;
     return BA_ECUDA;
   }
+  return BA_OK;
+}
+
+struct TmapEntry {
+  const void* base;
+  uint64_t d0, d1, d2, s1, s2;
+  uint32_t b1, b2;
+  CUtensorMap map;
+};
+thread_local TmapEntry g_tmap_cache[16];
+thread_local int g_tmap_n = 0, g_tmap_next = 0;
+
+int make_tmap_3d(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64_t d2,
+                 uint64_t stride1_bytes, uint64_t stride2_bytes, uint32_t box1, uint32_t box2) {
+  for (int k = 0; k < g_tmap_n; ++k) {
+    const TmapEntry& e = g_tmap_cache[k];
+    if (e.base == base && e.d0 == d0 && e.d1 == d1 && e.d2 == d2 && e.s1 == stride1_bytes &&
+        e.s2 == stride2_bytes && e.b1 == box1 && e.b2 == box2) {
+      *m = e.map;
+      return BA_OK;
+    }
+  }
+  const int rc = encode_tmap_3d(m, base, d0, d1, d2, stride1_bytes, stride2_bytes, box1, box2);
+  if (rc) return rc;
+  TmapEntry& e = g_tmap_cache[g_tmap_next];
+  g_tmap_next = (g_tmap_next + 1) & 15;
+  if (g_tmap_n < 16) ++g_tmap_n;
+  e = TmapEntry{base, d0, d1, d2, stride1_bytes, stride2_bytes, box1, box2, *m};
   return BA_OK;
 }
 
@@ -453,6 +519,11 @@ int run_tc(const ba_problem_t* pr, const Plan& P, const void* q, const void* Kc,
     return e ? atoi(e) : 0;
   }();
   bp.pf_dist = pf_env;
+  static const int rot_env = [] {  // context stream stagger (tiles per CTA index)
+    const char* e = getenv("BIFATTN_ROT");
+    return e ? atoi(e) : 0;
+  }();
+  bp.rot = rot_env;
   memcpy(bp.cs, P.tc_cs, sizeof(int) * (P.tc_G + 1));
   bp.scale_log2 = scale_log2;
   bp.S = P.S; bp.Sc = P.tc_Sc;
@@ -581,10 +652,10 @@ size_t ba_workspace_bytes(const ba_problem_t* prob) {
   if (validate(prob) != BA_OK) return 0;
   DevInfo di;
   int sms = device_info(&di) == BA_OK ? di.sms : 148;
-  Plan a, r;
-  if (make_plan(prob, sms, false, &a) != BA_OK) return 0;
-  if (make_plan(prob, sms, true, &r) != BA_OK) return 0;
-  return a.ws_bytes > r.ws_bytes ? a.ws_bytes : r.ws_bytes;
+  const Plan *a, *r;
+  if (cached_plan(prob, sms, false, &a) != BA_OK) return 0;
+  if (cached_plan(prob, sms, true, &r) != BA_OK) return 0;
+  return a->ws_bytes > r->ws_bytes ? a->ws_bytes : r->ws_bytes;
 }
 
 int bifurcated_attn_decode(const ba_problem_t* prob, const void* q, const void* Kc,
@@ -596,9 +667,10 @@ int bifurcated_attn_decode(const ba_problem_t* prob, const void* q, const void* 
   DevInfo di;
   rc = device_info(&di);
   if (rc) return rc;
-  Plan P;
-  rc = make_plan(prob, di.sms, false, &P);
+  const Plan* PP;
+  rc = cached_plan(prob, di.sms, false, &PP);
   if (rc) return rc;
+  const Plan P = *PP;  // copy: the cache may evict the entry below
   const void* ptrs[] = {q, Kc, Vc, out, lens};
   rc = common_checks(prob, ptrs, 5, workspace, workspace_bytes, ba_workspace_bytes(prob));
   if (rc) return rc;
@@ -621,9 +693,10 @@ int replicated_attn_decode(const ba_problem_t* prob, const void* q, const void* 
   DevInfo di;
   rc = device_info(&di);
   if (rc) return rc;
-  Plan P;
-  rc = make_plan(prob, di.sms, true, &P);
+  const Plan* PP;
+  rc = cached_plan(prob, di.sms, true, &PP);
   if (rc) return rc;
+  const Plan P = *PP;  // copy: the cache may evict the entry below
   const void* ptrs[] = {q, K, V, out, lens};
   rc = common_checks(prob, ptrs, 5, workspace, workspace_bytes, ba_workspace_bytes(prob));
   if (rc) return rc;

@@ -43,6 +43,9 @@ __device__ __forceinline__ void tma2(uint32_t dst, const CUtensorMap* m, uint64_
 
 struct Args {
   CUtensorMap tk, tv;
+  CUtensorMap pad_maps[4];  // size the parameter block like bif_tc's (experiment)
+  int pad_ints[170];
+  int tmem;                 // allocate/free TMEM like bif_tc
   int tiles;     // 128-row tiles
   int nst;       // stages
   int sub;       // 16 KB boxes per stage
@@ -50,9 +53,14 @@ struct Args {
   int split;     // 1: K and V released separately (K right away, V after hold)
 };
 
-__global__ void __launch_bounds__(64, 1) stream_kernel(const __grid_constant__ Args a) {
+__global__ void __launch_bounds__(512, 1) stream_kernel(const __grid_constant__ Args a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t full[16], empty[16];
+  __shared__ uint32_t tmem_holder;
+  if (a.tmem && threadIdx.x < 32) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&tmem_holder)), "r"(256));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
   const int G = gridDim.x, k = blockIdx.x;
   const int t0 = (int)((long)a.tiles * k / G), t1 = (int)((long)a.tiles * (k + 1) / G);
   if (threadIdx.x == 0) {
@@ -90,6 +98,9 @@ __global__ void __launch_bounds__(64, 1) stream_kernel(const __grid_constant__ A
       bx += min((long)a.sub, b1 - bx);
     }
   }
+  __syncthreads();
+  if (a.tmem && threadIdx.x < 32)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_holder), "r"(256));
 }
 
 int main(int argc, char** argv) {
@@ -98,6 +109,10 @@ int main(int argc, char** argv) {
   const int sub = argc > 3 ? atoi(argv[3]) : 4;
   const int hold = argc > 4 ? atoi(argv[4]) : 0;
   const int G = argc > 5 ? atoi(argv[5]) : 148;
+  const int nthr = argc > 6 ? atoi(argv[6]) : 64;
+  const int extra_smem = argc > 7 ? atoi(argv[7]) : 0;
+  const int use_tmem = argc > 8 ? atoi(argv[8]) : 0;
+  const int coop = argc > 9 ? atoi(argv[9]) : 0;
   const long rows = MB * 1000000L / 2 / 256 / 128 * 128;  // K and V each rows x 256 B
   void *K[2], *V[2];
   for (int j = 0; j < 2; ++j) {
@@ -122,10 +137,26 @@ int main(int argc, char** argv) {
     a[j].nst = nst;
     a[j].sub = sub;
     a[j].hold_ns = hold;
+    a[j].tmem = use_tmem;
   }
-  const int smem = nst * sub * 16384;
+  const int smem = nst * sub * 16384 + extra_smem;
   if (smem > 227 * 1024) { printf("{\"err\":\"smem\"}\n"); return 1; }
   cudaFuncSetAttribute(stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  auto launch = [&](const Args& arg) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(G);
+    cfg.blockDim = dim3(nthr);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = 0;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = coop & 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = (coop >> 1) & 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
+    cudaLaunchKernelEx(&cfg, stream_kernel, arg);
+  };
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
@@ -133,7 +164,7 @@ int main(int argc, char** argv) {
   const int it = 20;
   for (int i = 0; i < it + 3; ++i) {  // one launch per event pair
     cudaEventRecord(e0);
-    stream_kernel<<<G, 64, smem>>>(a[i & 1]);
+    launch(a[i & 1]);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     float ms;
@@ -141,7 +172,7 @@ int main(int argc, char** argv) {
     if (i >= 3) { best = ms < best ? ms : best; tot += ms; }
   }
   cudaEventRecord(e0);  // back to back
-  for (int i = 0; i < 40; ++i) stream_kernel<<<G, 64, smem>>>(a[i & 1]);
+  for (int i = 0; i < 40; ++i) launch(a[i & 1]);
   cudaEventRecord(e1);
   cudaEventSynchronize(e1);
   float bb;

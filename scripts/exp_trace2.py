@@ -3,10 +3,14 @@ import sys, os, json, ctypes
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import paper_2403_08845_b200 as ba
+if os.environ.get("EXP_LIB"):
+    ba.load_library(os.environ["EXP_LIB"])
 from synth import CONFIGS, make_inputs
 
 name = sys.argv[1] if len(sys.argv) > 1 else "mha7b_b32"
 cfg = CONFIGS[name]
+if os.environ.get("EXP_MC"):
+    cfg = cfg.with_(mc=int(os.environ["EXP_MC"]), md=int(os.environ["EXP_MD"]))
 inp = make_inputs(cfg, 1, device="cuda")
 out = torch.empty_like(inp.q)
 prob = ba.make_problem(cfg.b, cfg.h, cfg.g, cfg.d, cfg.mc, cfg.md, cfg.torch_dtype, inp.scale)
