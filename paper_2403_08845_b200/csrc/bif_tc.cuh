@@ -417,6 +417,14 @@ struct Prof {
 };
 #endif
 
+// Experiment bits (BifTcParams::dbg) exist only in BIFATTN_EXPERIMENTS builds;
+// the product kernel sees a constant 0 and carries none of their branches.
+#ifdef BIFATTN_EXPERIMENTS
+#define BIF_DBG (P.dbg)
+#else
+#define BIF_DBG 0
+#endif
+
 template <int N, int SWG>
 __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
     bif_tc_kernel(const __grid_constant__ BifTcParams P) {
@@ -527,7 +535,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
       for (long long w = 0; w < nw; ++sg) {
         const Seg s = seg_at(P, rg, w);
         const uint32_t qbuf = sg & 1;
-        if (P.dbg & 16384) tc::mbar_wait_sleep(tc::smem_u32(&q_empty[qbuf]), ((sg >> 1) & 1) ^ 1); else tc::mbar_wait(tc::smem_u32(&q_empty[qbuf]), ((sg >> 1) & 1) ^ 1);
+        if (BIF_DBG & 16384) tc::mbar_wait_sleep(tc::smem_u32(&q_empty[qbuf]), ((sg >> 1) & 1) ^ 1, BIF_DBG & 262144); else tc::mbar_wait(tc::smem_u32(&q_empty[qbuf]), ((sg >> 1) & 1) ^ 1);
         pf.mark(0);
         const uint32_t qb = tc::smem_u32(&q_full[qbuf]);
         const uint32_t qdst = tc::smem_u32(sm_q + qbuf * QB);
@@ -550,7 +558,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
           const int z = s.dec ? s.i * P.g + cg : s.c;  // TMA z: group, or sample*g + group
           const int tl = s.dec ? t : ctx_tile(P, s, j);
           const int st = tt % NST;
-          tc::mbar_wait_sleep(tc::smem_u32(&kv_empty[st]), ((tt / NST) & 1) ^ 1);
+          tc::mbar_wait_sleep(tc::smem_u32(&kv_empty[st]), ((tt / NST) & 1) ^ 1, BIF_DBG & 262144);
           pf.mark(2);
           if (kStamp && P.trace && tt < 128) P.trace[(size_t)blockIdx.x * kTraceSlots + 256 + tt] = (gtimer() & 0x00ffffffffffffffull) | (30ull << 56);
           const uint32_t bar = tc::smem_u32(&kv_full[st]);
@@ -596,16 +604,16 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
       for (long long w = 0; w < nw; ++sg) {
         const Seg s = seg_at(P, rg, w);
         const uint32_t qbase = q_addr + (sg & 1) * QB;
-        if (P.dbg & 16384) tc::mbar_wait_sleep(tc::smem_u32(&q_full[sg & 1]), (sg >> 1) & 1); else tc::mbar_wait(tc::smem_u32(&q_full[sg & 1]), (sg >> 1) & 1);
+        if (BIF_DBG & 16384) tc::mbar_wait_sleep(tc::smem_u32(&q_full[sg & 1]), (sg >> 1) & 1, BIF_DBG & 262144); else tc::mbar_wait(tc::smem_u32(&q_full[sg & 1]), (sg >> 1) & 1);
         pf.mark(0);
         for (int j = 0; j < s.ntiles; ++j, ++u) {
           const uint32_t st = u % NST;
           const uint32_t slot = u & 1;
-          tc::mbar_wait_sleep(tc::smem_u32(&kv_full[st]), (u / NST) & 1);
+          tc::mbar_wait_sleep(tc::smem_u32(&kv_full[st]), (u / NST) & 1, BIF_DBG & 262144);
           pf.mark(1);
           if (kStamp && P.trace && u < 128)
             P.trace[(size_t)blockIdx.x * kTraceSlots + 256 + 128 + u] = (gtimer() & 0x00ffffffffffffffull) | (33ull << 56);
-          if (P.dbg & 65536) tc::mbar_wait_sleep(tc::smem_u32(&s_free[slot]), ((u >> 1) & 1) ^ 1); else tc::mbar_wait(tc::smem_u32(&s_free[slot]), ((u >> 1) & 1) ^ 1);
+          if (BIF_DBG & 65536) tc::mbar_wait_sleep(tc::smem_u32(&s_free[slot]), ((u >> 1) & 1) ^ 1, BIF_DBG & 262144); else tc::mbar_wait(tc::smem_u32(&s_free[slot]), ((u >> 1) & 1) ^ 1);
           pf.mark(2);
           tc::tc_fence_after();
           const uint32_t kbase = tc::smem_u32(sm_stage + st * kStageBytes);
@@ -616,7 +624,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
             tc::mma_bf16(tS + slot * N, ad, bd, IDESC_QK, k > 0 ? 1u : 0u);
           }
           tc::mma_commit(tc::smem_u32(&s_full[slot]));
-          if (P.dbg & 1024) tc::mma_commit(tc::smem_u32(&kv_empty[st]));  // experiment: release at QK
+          if (BIF_DBG & 1024) tc::mma_commit(tc::smem_u32(&kv_empty[st]));  // experiment: release at QK
           pf.mark(3);
           if (kStamp && P.trace && u < 256)
             P.trace[(size_t)blockIdx.x * kTraceSlots + 512 + u] = (gtimer() & 0x00ffffffffffffffull) | (31ull << 56);
@@ -639,12 +647,12 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
       for (long long w = 0; w < nw; ++sg) {
         const Seg s = seg_at(P, rg, w);
         const uint32_t ob = sg & 1;
-        if (P.dbg & 16384) tc::mbar_wait_sleep(tc::smem_u32(&o_empty[ob]), ((sg >> 1) & 1) ^ 1); else tc::mbar_wait(tc::smem_u32(&o_empty[ob]), ((sg >> 1) & 1) ^ 1);
+        if (BIF_DBG & 16384) tc::mbar_wait_sleep(tc::smem_u32(&o_empty[ob]), ((sg >> 1) & 1) ^ 1, BIF_DBG & 262144); else tc::mbar_wait(tc::smem_u32(&o_empty[ob]), ((sg >> 1) & 1) ^ 1);
         pf.mark(0);
         for (int j = 0; j < s.ntiles; ++j, ++u) {
           const uint32_t st = u % NST;
           const uint32_t ps = P.npb == 2 ? (u & 1) : 0, ph = P.npb == 2 ? (u >> 1) : u;
-          tc::mbar_wait_sleep(tc::smem_u32(&p_full[ps]), ph & 1);
+          tc::mbar_wait_sleep(tc::smem_u32(&p_full[ps]), ph & 1, BIF_DBG & 262144);
           pf.mark(1);
           tc::tc_fence_after();
           const uint32_t vbase = tc::smem_u32(sm_stage + st * kStageBytes + 32768);
@@ -652,13 +660,13 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
           // gives [O_hi | O_lo]^T += V^T [P_hi | P_lo]^T, V read once
           const uint32_t pbase = p_addr + 2 * ps * QB;
 #pragma unroll
-          for (int k = 0; k < ((P.dbg & 32) ? 0 : 8); ++k) {
+          for (int k = 0; k < ((BIF_DBG & 32) ? 0 : 8); ++k) {
             const uint64_t ad = tc::smem_desc(vbase + k * 2048, 16384, 1024, tc::kSw128);
             const uint64_t bd = tc::smem_desc(pbase + k * 16 * PRB, PLBO, 8 * PRB, p_layout(NP));
             tc::mma_bf16(tO + ob * NP, ad, bd, IDESC_PV, (j == 0 && k == 0) ? 0u : 1u);
           }
           tc::mma_commit(tc::smem_u32(&p_empty[ps]));
-          if (!(P.dbg & 1024)) tc::mma_commit(tc::smem_u32(&kv_empty[st]));
+          if (!(BIF_DBG & 1024)) tc::mma_commit(tc::smem_u32(&kv_empty[st]));
           pf.mark(2);
           if (kStamp && P.trace && u < 256)
             P.trace[(size_t)blockIdx.x * kTraceSlots + 768 + u] = (gtimer() & 0x00ffffffffffffffull) | (32ull << 56);
@@ -714,7 +722,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
           const uint32_t slot = u & 1;
           const uint32_t ps = P.npb == 2 ? (u & 1) : 0, ph = P.npb == 2 ? (u >> 1) : u;  // P slot, its phase
           pf.mark(6);
-          if (P.dbg & 32768) tc::mbar_wait_sleep(tc::smem_u32(&s_full[slot]), (u >> 1) & 1);
+          if (BIF_DBG & 32768) tc::mbar_wait_sleep(tc::smem_u32(&s_full[slot]), (u >> 1) & 1, BIF_DBG & 262144);
           else tc::mbar_wait(tc::smem_u32(&s_full[slot]), (u >> 1) & 1);
           pf.mark(0);
           tc::tc_fence_after();
@@ -731,7 +739,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
           __syncwarp();
           if (lane == 0) tc::mbar_arrive(tc::smem_u32(&s_free[slot]));
           pf.mark(1);
-          if (P.dbg & 1) {
+          if (BIF_DBG & 1) {
             tc::mbar_wait(tc::smem_u32(&p_empty[ps]), (ph & 1) ^ 1);
             tc::fence_proxy_async_smem();
             __syncwarp();
@@ -803,7 +811,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
             }
             // P row of this position (hi and lo parts): zeros except the p valid columns
             pf.mark(3);
-            if (!(P.dbg & 8)) tc::mbar_wait(tc::smem_u32(&p_empty[ps]), (ph & 1) ^ 1);  // PV(u-npb) done
+            if (!(BIF_DBG & 8)) tc::mbar_wait(tc::smem_u32(&p_empty[ps]), (ph & 1) ^ 1);  // PV(u-npb) done
             uint8_t* const sm_pb = sm_p + 2 * ps * QB;
             pf.mark(4);
 #pragma unroll
@@ -894,7 +902,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
           const uint32_t slot = u & 1;
           const uint32_t ps = P.npb == 2 ? (u & 1) : 0, ph = P.npb == 2 ? (u >> 1) : u;  // P slot, its phase
           pf.mark(6);
-          if (P.dbg & 32768) tc::mbar_wait_sleep(tc::smem_u32(&s_full[slot]), (u >> 1) & 1);
+          if (BIF_DBG & 32768) tc::mbar_wait_sleep(tc::smem_u32(&s_full[slot]), (u >> 1) & 1, BIF_DBG & 262144);
           else tc::mbar_wait(tc::smem_u32(&s_full[slot]), (u >> 1) & 1);
           pf.mark(0);
           tc::tc_fence_after();
@@ -907,7 +915,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
           __syncwarp();
           if (lane == 0) tc::mbar_arrive(tc::smem_u32(&s_free[slot]));
           pf.mark(1);
-          if (P.dbg & 1) {
+          if (BIF_DBG & 1) {
             tc::mbar_wait(tc::smem_u32(&p_empty[ps]), (ph & 1) ^ 1);
             tc::fence_proxy_async_smem();
             __syncwarp();
@@ -936,7 +944,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
               need |= vc && (mr[n] == kNegInf || x[n] > kTh);
             }
           }
-          const bool slowp = (P.dbg & 4096) ? (bool)__any_sync(0xffffffffu, need) : tc::named_bar_or(1, 32 * NSW, need);
+          const bool slowp = (BIF_DBG & 4096) ? (bool)__any_sync(0xffffffffu, need) : tc::named_bar_or(1, 32 * NSW, need);
           pf.mark(2);
           stamp(slowp ? 22 : 21);
           if (slowp) pf.count(7);
@@ -1017,7 +1025,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
           // ---- P = 2^x as two bf16 parts (P_hi + P_lo carries ~16 mantissa
           //      bits) into shared memory; fp32 row sums ----
           pf.mark(3);
-          if (!(P.dbg & 4)) tc::mbar_wait(tc::smem_u32(&p_empty[ps]), (ph & 1) ^ 1);  // PV(u-npb) done
+          if (!(BIF_DBG & 4)) tc::mbar_wait(tc::smem_u32(&p_empty[ps]), (ph & 1) ^ 1);  // PV(u-npb) done
           uint8_t* const sm_pb = sm_p + 2 * ps * QB;
           pf.mark(4);
 #pragma unroll
@@ -1026,7 +1034,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
 #pragma unroll
             for (int e = 0; e < 8; e += 2) {
               float p0 = ex2(x[n + e]), p1 = ex2(x[n + e + 1]);
-              if (P.dbg & 131072) {  // experiment: twice the exp work
+              if (BIF_DBG & 131072) {  // experiment: twice the exp work
                 p0 = ex2(p0 * 1e-30f + x[n + e]);
                 p1 = ex2(p1 * 1e-30f + x[n + e + 1]);
               }
@@ -1040,7 +1048,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
             off ^= ((off >> 7) & PSWM) << 4;
             uint32_t offl = (uint32_t)(((N + col) / W) * PLBO + pos * PRB + ((N + col) % W) * 2);
             offl ^= ((offl >> 7) & PSWM) << 4;
-            if (!(P.dbg & 2048)) {
+            if (!(BIF_DBG & 2048)) {
               *reinterpret_cast<uint4*>(sm_pb + off) = make_uint4(hk[0], hk[1], hk[2], hk[3]);
               *reinterpret_cast<uint4*>(sm_pb + offl) = make_uint4(lk[0], lk[1], lk[2], lk[3]);
             }
@@ -1085,7 +1093,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
     for (long long w = 0; w < nw; ++sg) {
       const Seg s = seg_at(P, rg, w);
       const uint32_t ob = sg & 1;
-      if (P.dbg & 8192) tc::mbar_wait_sleep(tc::smem_u32(&o_full[ob]), (sg >> 1) & 1);
+      if (BIF_DBG & 8192) tc::mbar_wait_sleep(tc::smem_u32(&o_full[ob]), (sg >> 1) & 1, BIF_DBG & 262144);
       else tc::mbar_wait(tc::smem_u32(&o_full[ob]), (sg >> 1) & 1);
       tc::tc_fence_after();
       // output rows of the chunk's columns, stepped without divisions (row_of):
@@ -1103,11 +1111,16 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
       float* const wo = P.ws_o + (size_t)s.slot * kD + d;
       const size_t row_stride = (size_t)P.S * kD;
 #pragma unroll
-      for (int n = 0; n < N; n += 16) {
+      for (int n = 0; n < ((BIF_DBG & 524288) ? 0 : N); n += 16) {
         uint32_t orr[16], orl[16];
-        tc::tmem_ld<16>(tO + ob * NP + n + lane_addr, orr);
-        tc::tmem_ld<16>(tO + ob * NP + N + n + lane_addr, orl);
-        tc::tmem_ld_wait();
+        if (!(BIF_DBG & 2097152)) {
+          tc::tmem_ld<16>(tO + ob * NP + n + lane_addr, orr);
+          tc::tmem_ld<16>(tO + ob * NP + N + n + lane_addr, orl);
+          tc::tmem_ld_wait();
+        } else {
+#pragma unroll
+          for (int e = 0; e < 16; ++e) orr[e] = orl[e] = (uint32_t)e;
+        }
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
           const int col = n + e;
@@ -1121,13 +1134,13 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
               ++ri;
             }
           }
-          if (gr >= 0) wo[(size_t)gr * row_stride] = __uint_as_float(orr[e]) + __uint_as_float(orl[e]);
+          if (gr >= 0 && !(BIF_DBG & 1048576)) wo[(size_t)gr * row_stride] = __uint_as_float(orr[e]) + __uint_as_float(orl[e]);
         }
       }
       tc::tc_fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(tc::smem_u32(&o_empty[ob]));
-      if (P.dbg & 8192) tc::mbar_wait_sleep(tc::smem_u32(&e_full[ob]), (sg >> 1) & 1);
+      if (BIF_DBG & 8192) tc::mbar_wait_sleep(tc::smem_u32(&e_full[ob]), (sg >> 1) & 1, BIF_DBG & 262144);
       else tc::mbar_wait(tc::smem_u32(&e_full[ob]), (sg >> 1) & 1);
       if (et < N) {
         const int gr = row_of(P, s, et);

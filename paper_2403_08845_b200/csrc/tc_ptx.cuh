@@ -40,7 +40,12 @@ BA_DEVINL void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
 // Wait with a suspend-time hint: the thread may sleep until the phase
 // completes (or the hint expires) instead of re-polling, freeing issue slots
 // for the warps that do the math.  For waits off the critical path.
-BA_DEVINL void mbar_wait_sleep(uint32_t bar, uint32_t parity) {
+BA_DEVINL void mbar_wait(uint32_t bar, uint32_t parity);
+BA_DEVINL void mbar_wait_sleep(uint32_t bar, uint32_t parity, bool spin = false) {
+  if (spin) {
+    mbar_wait(bar, parity);
+    return;
+  }
   asm volatile(
       "{\n"
       " .reg .pred p;\n"
