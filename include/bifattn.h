@@ -33,7 +33,8 @@
  * OWNERSHIP — the caller owns every buffer (PyTorch allocates them) and keeps
  *   them alive until the work on `stream` has finished.  The library never
  *   allocates or frees device memory per call; it caches per-device attributes
- *   and kernel attributes under a mutex.
+ *   and kernel attributes under a mutex, and per host thread the last plans
+ *   (keyed by the problem) and TMA descriptors (keyed by pointer and shape).
  *
  * EXECUTION — every call is asynchronous on `stream` (a cudaStream_t passed as
  *   void*; NULL = legacy default stream), reentrant, and CUDA-graph capturable
