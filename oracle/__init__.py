@@ -50,6 +50,8 @@ def _load():
         lib.oracle_attn_decode_f64.restype = I
         lib.oracle_bifurcated_f64.argtypes = args
         lib.oracle_bifurcated_f64.restype = I
+        lib.oracle_attn_decode_multi_f64.argtypes = [I] + args
+        lib.oracle_attn_decode_multi_f64.restype = I
         lib.oracle_kv_read_elements.argtypes = [ctypes.c_int64] * 5 + [I]
         lib.oracle_kv_read_elements.restype = ctypes.c_int64
         _lib = lib
@@ -86,11 +88,18 @@ def attn_decode(q, Kc, Vc, Kd, Vd, lens, *, scale, rows=None, weights=False,
     lens int32 [b].  dtype: bf16 (as uint16 bits / torch.bfloat16) or fp32.
     ``scale`` is the logit scale (pass the exact fp32 value the GPU uses).
     ``rows``: optional list of flat row indices i*h + j to compute.
+    A 4-D q [b][h][n][d] is the multi-token step (oracle_attn_decode_multi_f64,
+    App. G): rows are (i*h + j)*n + k; ``bifurcated`` is not available there.
     Returns (out [nrows][d] f64, lse [nrows] f64, weights [nrows][mc+md_cap] or None).
     """
     qn, Kcn, Vcn, Kdn, Vdn = (_as_np(t) for t in (q, Kc, Vc, Kd, Vd))
     lensn = np.ascontiguousarray(_as_np(lens).astype(np.int32))
-    b, h, d = qn.shape
+    n = 1
+    if qn.ndim == 4:
+        b, h, n, d = qn.shape
+        assert not bifurcated, "the multi-token oracle is the plain definition only"
+    else:
+        b, h, d = qn.shape
     g, mc, d2 = Kcn.shape
     md_cap = Kdn.shape[2]
     assert d2 == d and Kdn.shape[:2] == (b, g) and Kdn.shape[3] == d
@@ -105,17 +114,20 @@ def attn_decode(q, Kc, Vc, Kd, Vd, lens, *, scale, rows=None, weights=False,
         assert t.dtype == qn.dtype
     if rows is None:
         rows_np = None
-        nrows = b * h
+        nrows = b * h * n
     else:
         rows_np = np.ascontiguousarray(np.asarray(rows, dtype=np.int32))
         nrows = int(rows_np.size)
     out = np.zeros((nrows, d), dtype=np.float64)
     lse = np.zeros((nrows,), dtype=np.float64)
     w = np.zeros((nrows, mc + md_cap), dtype=np.float64) if weights else None
-    fn = _load().oracle_bifurcated_f64 if bifurcated else _load().oracle_attn_decode_f64
-    rc = fn(b, h, g, d, mc, md_cap, dtype, float(scale), _ptr(qn), _ptr(Kcn), _ptr(Vcn),
-            _ptr(Kdn), _ptr(Vdn), _ptr(lensn), _ptr(rows_np), nrows, _ptr(out), _ptr(lse),
-            _ptr(w), int(nthreads))
+    tail = (float(scale), _ptr(qn), _ptr(Kcn), _ptr(Vcn), _ptr(Kdn), _ptr(Vdn), _ptr(lensn),
+            _ptr(rows_np), nrows, _ptr(out), _ptr(lse), _ptr(w), int(nthreads))
+    if qn.ndim == 4:
+        rc = _load().oracle_attn_decode_multi_f64(b, h, n, g, d, mc, md_cap, dtype, *tail)
+    else:
+        fn = _load().oracle_bifurcated_f64 if bifurcated else _load().oracle_attn_decode_f64
+        rc = fn(b, h, g, d, mc, md_cap, dtype, *tail)
     if rc != 0:
         raise ValueError("oracle: invalid problem")
     return out, lse, w

@@ -243,6 +243,83 @@ int oracle_bifurcated_f64(int b, int h, int g, int d, int mc, int md_cap, int dt
 }
 
 /*
+ * Multi-token step (App. G: n_g draft tokens decoded in one
+ * step, "with n_g replacing n"; SPEC.md:441-449 decode_multi: "intra-step causal
+ * masking (mask offset m_c+m_d)").  Plain masked attention, Eq. 1-2 over the
+ * replicated cache Kfull = Kc ⊕ Kd[i][0..L_i), L_i = clamp(lens[i], 0, md_cap),
+ * where the n query tokens of sample i sit at the last n cache positions
+ * P_k = mc + L_i - n + k (their K/V already appended, reading R3) and token k
+ * attends to the cache positions t <= P_k (causal mask).  Context positions
+ * (t < mc) are always visible.  q, out [b][h][n][d]; row = (i*h + j)*n + k.
+ * With n = 1 this is oracle_attn_decode_f64 exactly.
+ */
+int oracle_attn_decode_multi_f64(int b, int h, int n, int g, int d, int mc, int md_cap,
+                                 int dtype, double scale, const void *q, const void *Kc,
+                                 const void *Vc, const void *Kd, const void *Vd,
+                                 const int32_t *lens, const int32_t *rows, int nrows,
+                                 double *out, double *lse, double *weights, int nthreads) {
+  if (check(b, h, g, d, mc, md_cap, dtype) || n < 1) return -1;
+  if (!rows) nrows = b * h * n;
+  const int p = h / g;
+  const int Mcap = mc + md_cap;
+  int err = 0;
+  (void)nthreads;
+#pragma omp parallel for schedule(dynamic, 1) num_threads(nthreads > 0 ? nthreads : 1)
+  for (int r = 0; r < nrows; ++r) {
+    const int row = rows ? rows[r] : r;
+    const int k = row % n, ij = row / n;
+    const int i = ij / h, j = ij % h, c = j / p;
+    const int Li = dec_len(lens, i, md_cap);
+    const int M = mc + Li;
+    const long Pk = (long)mc + Li - n + k; /* this token's own cache position */
+    double *l = (double *)malloc(sizeof(double) * (size_t)(M > 0 ? M : 1));
+    if (!l || M < 1) {
+      free(l);
+#pragma omp atomic write
+      err = 1;
+      continue;
+    }
+    /* Logits over Kfull = Kc ⊕ Kd[i]; masked (weight 0) past the causal bound. */
+    int any = 0;
+    double mx = 0.0;
+    for (int t = 0; t < M; ++t) {
+      const int vis = t < mc || t <= Pk;
+      if (!vis) continue;
+      double acc = 0.0;
+      for (int x = 0; x < d; ++x) {
+        const double kv = t < mc ? widen(Kc, ((size_t)c * mc + t) * d + x, dtype)
+                                 : widen(Kd, (((size_t)i * g + c) * md_cap + (t - mc)) * d + x, dtype);
+        acc += widen(q, (((size_t)i * h + j) * n + k) * d + x, dtype) * kv;
+      }
+      l[t] = scale * acc;
+      if (!any || l[t] > mx) mx = l[t];
+      any = 1;
+    }
+    double Z = 0.0;
+    for (int t = 0; t < M; ++t) {
+      const int vis = t < mc || t <= Pk;
+      l[t] = vis ? exp(l[t] - mx) : 0.0;
+      Z += l[t];
+    }
+    for (int x = 0; x < d; ++x) {
+      double acc = 0.0;
+      for (int t = 0; t < M; ++t) {
+        if (l[t] == 0.0) continue;
+        const double vv = t < mc ? widen(Vc, ((size_t)c * mc + t) * d + x, dtype)
+                                 : widen(Vd, (((size_t)i * g + c) * md_cap + (t - mc)) * d + x, dtype);
+        acc += l[t] * vv;
+      }
+      out[(size_t)r * d + x] = acc / Z;
+    }
+    if (lse) lse[r] = mx + log(Z);
+    if (weights)
+      for (int t = 0; t < Mcap; ++t) weights[(size_t)r * Mcap + t] = t < M ? l[t] / Z : 0.0;
+    free(l);
+  }
+  return err ? -1 : 0;
+}
+
+/*
  * KV-read element counts of Eq. 5-6 (§4.3), per K or V
  * tensor, per layer:  naive  g*k*b*(mc+md);  bifurcated  g*k*(mc+b*md).
  */

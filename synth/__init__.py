@@ -78,12 +78,13 @@ class Inputs:
 
 def make_inputs(cfg: Config, seed: int, device="cpu", variant: str = "normal",
                 md_cap: Optional[int] = None, lens=None, scale: Optional[float] = None,
-                gen_dtype=torch.float32) -> Inputs:
+                gen_dtype=torch.float32, n_tok: int = 1) -> Inputs:
     """Seeded N(0,1) inputs shaped like ``cfg``.
 
     variant: "normal" | "peaky" (q*8) | "ctx_dom" (Kc*4) | "dec_dom" (Kd*4) |
              "ragged" (lens ~ U[0, md]) | "equal" (all samples identical q/Kd/Vd) |
              "planted_ctx" / "planted_dec" (one key per row made dominant).
+    n_tok > 1: a multi-token step, q [b][h][n_tok][d] (App. G draft tokens).
     """
     md_cap = cfg.md if md_cap is None else md_cap
     gen = torch.Generator(device=device)
@@ -93,7 +94,9 @@ def make_inputs(cfg: Config, seed: int, device="cpu", variant: str = "normal",
     def randn(*shape):
         return torch.randn(*shape, generator=gen, device=device, dtype=gen_dtype).to(dt)
 
-    q = randn(cfg.b, cfg.h, cfg.d)
+    q = randn(cfg.b, cfg.h, n_tok, cfg.d) if n_tok > 1 else randn(cfg.b, cfg.h, cfg.d)
+    if n_tok > 1 and variant.startswith("planted"):
+        raise ValueError("planted variants are single-token")
     Kc = randn(cfg.g, cfg.mc, cfg.d)
     Vc = randn(cfg.g, cfg.mc, cfg.d)
     Kd = randn(cfg.b, cfg.g, md_cap, cfg.d)
