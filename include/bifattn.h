@@ -19,7 +19,8 @@
  *   partials (m, l, o), which is the same function in exact arithmetic.
  *
  * LAYOUT — all tensors row-major and contiguous, all in ONE dtype (prob->dtype):
- *   q    [b][h][d]             query of this step (n = 1 token per sample)
+ *   q    [b][h][d]             query of this step (n = 1 token per sample;
+ *                               [b][h][n][d] for a multi-token step, below)
  *   Kc,Vc[g][mc][d]            the single shared context cache ("compact shape
  *                               1hm_ck or simply hm_ck")
  *   Kd,Vd[b][g][md_cap][d]     per-sample decode caches, preallocated to md_cap;
@@ -82,7 +83,21 @@ typedef struct {
   ba_dtype_t dtype; /* dtype of q, Kc, Vc, Kd, Vd and out                               */
   float scale;      /* logit scale; <= 0 means 1/sqrt(d) (the paper omits it: reading R1) */
   uint32_t flags;   /* BA_FLAG_*; 0 for the default (fastest) path                      */
+  int32_t n_tok;    /* query tokens per sample in this step (multi-token / speculative
+                       verification step, App. G PAPER.md:1219-1226 "with n_g replacing
+                       n"); 0 or 1 = the single-token step.  See MULTI-TOKEN below.    */
 } ba_problem_t;
+
+/* MULTI-TOKEN STEP (n_tok = n > 1):
+ *   q, out [b][h][n][d], lse [b][h][n]: token k of head j of sample i.
+ *   The n tokens' own K/V are the LAST n valid positions of the decode cache
+ *   (already appended, like the single-token step's current token, reading
+ *   R3), so token k sees every context position and the decode positions
+ *     t < lens[i] - (n - 1 - k)        (intra-step causal mask; SPEC.md:441-449
+ *                                       "mask offset m_c + m_d")
+ *   and none when that bound is <= 0.  Kc/Vc and Kd/Vd are still read once
+ *   per step for all n tokens (the I/O amortisation App. G describes).
+ *   n = 1 is exactly the single-token step. */
 
 /* Bytes of device workspace bifurcated_attn_decode() / replicated_attn_decode()
  * need: a grid-barrier word pair at offset 0, then fp32 partials (m, l, o[d])
@@ -173,7 +188,7 @@ const char* ba_strerror(int code);
 /* The cudaError_t of the last BA_ECUDA on this thread (0 if none). */
 int ba_last_cuda_error(void);
 
-/* ABI version: 1. */
+/* ABI version: 2 (2 added ba_problem_t.n_tok, the multi-token step). */
 int ba_version(void);
 
 #ifdef __cplusplus

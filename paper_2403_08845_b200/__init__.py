@@ -38,7 +38,8 @@ EXPORTED = ["ba_workspace_bytes", "bifurcated_attn_decode", "bifurcated_attn_dec
 class BAProblem(ctypes.Structure):
     _fields_ = [("b", ctypes.c_int32), ("h", ctypes.c_int32), ("g", ctypes.c_int32),
                 ("d", ctypes.c_int32), ("mc", ctypes.c_int32), ("md_cap", ctypes.c_int32),
-                ("dtype", ctypes.c_int32), ("scale", ctypes.c_float), ("flags", ctypes.c_uint32)]
+                ("dtype", ctypes.c_int32), ("scale", ctypes.c_float), ("flags", ctypes.c_uint32),
+                ("n_tok", ctypes.c_int32)]
 
 
 _lib = None
@@ -97,16 +98,21 @@ class BifAttnError(RuntimeError):
         self.code = code
 
 
-def make_problem(b, h, g, d, mc, md_cap, dtype, scale: Optional[float] = None, flags: int = 0):
+def make_problem(b, h, g, d, mc, md_cap, dtype, scale: Optional[float] = None, flags: int = 0,
+                 n_tok: int = 1):
     dt = {torch.bfloat16: BA_BF16, torch.float32: BA_FP32}.get(dtype, dtype)
-    return BAProblem(b, h, g, d, mc, md_cap, dt, float(scale) if scale else 0.0, flags)
+    return BAProblem(b, h, g, d, mc, md_cap, dt, float(scale) if scale else 0.0, flags, n_tok)
 
 
 def _problem_from(q, Kc, Kd, scale, flags):
-    b, h, d = q.shape
+    """q [b,h,d] (one token per sample) or [b,h,n,d] (multi-token step)."""
+    if q.dim() == 4:
+        b, h, n, d = q.shape
+    else:
+        (b, h, d), n = q.shape, 1
     g, mc, _ = Kc.shape
     md_cap = Kd.shape[2]
-    return make_problem(b, h, g, d, mc, md_cap, q.dtype, scale, flags)
+    return make_problem(b, h, g, d, mc, md_cap, q.dtype, scale, flags, n)
 
 
 def _ptr(t):
@@ -241,7 +247,10 @@ def _cached_problem(q, Kc, Kd, scale, flags):
 def bifurcated_attn_decode(q, Kc, Vc, Kd, Vd, lens, out=None, lse=None, *, scale=None,
                            workspace=None, stream=None, flags=0):
     """One bifurcated decode step on the GPU.  Shapes: q [b,h,d]; Kc,Vc [g,mc,d];
-    Kd,Vd [b,g,md_cap,d]; lens int32 [b].  Returns ``out`` [b,h,d]."""
+    Kd,Vd [b,g,md_cap,d]; lens int32 [b].  Returns ``out`` [b,h,d].
+    Multi-token step (n draft tokens per sample, include/bifattn.h MULTI-TOKEN):
+    q [b,h,n,d], out [b,h,n,d], lse [b,h,n]; token k sees the decode positions
+    t < lens[i] - (n - 1 - k)."""
     lib = _lib if _lib is not None else load_library()
     _fast_check((q, Kc, Vc, Kd, Vd, lens), q.dtype, q.device)
     if lens.dtype != torch.int32:
@@ -291,7 +300,7 @@ def make_device_buffers(hq, hKc, hKd, device, with_lse=False, scale=None, flags=
              out=torch.empty(hq.shape, dtype=hq.dtype, device=device),
              workspace=alloc_workspace(prob, device))
     if with_lse:
-        e["lse"] = torch.empty(hq.shape[0], hq.shape[1], dtype=torch.float32, device=device)
+        e["lse"] = torch.empty(hq.shape[:-1], dtype=torch.float32, device=device)
     return e
 
 
@@ -301,9 +310,12 @@ def replicated_attn_decode(q, K, V, lens, mc, out=None, lse=None, *, scale=None,
     sample i attends to positions [0, mc + lens[i])."""
     lib = load_library()
     _check(dict(q=q, K=K, V=V, lens=lens), q.dtype, q.device)
-    b, h, d = q.shape
+    if q.dim() == 4:
+        b, h, n, d = q.shape
+    else:
+        (b, h, d), n = q.shape, 1
     g, M = K.shape[1], K.shape[2]
-    prob = make_problem(b, h, g, d, mc, M - mc, q.dtype, scale, flags)
+    prob = make_problem(b, h, g, d, mc, M - mc, q.dtype, scale, flags, n)
     if out is None:
         out = torch.empty_like(q)
     if workspace is None:

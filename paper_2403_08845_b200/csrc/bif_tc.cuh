@@ -67,6 +67,8 @@ struct BifTcParams {
   const int32_t* lens;
   int b, h, g, p, mc;
   int dec_cap, lens_offset;  // decode length = lens_offset + clamp(lens[i], 0, dec_cap)
+  int ntok;                  // tokens per head (multi-token step): in-group row k sees decode
+                             // positions < max(L - (ntok - 1 - k % ntok), lens_offset)
   int N;                     // rows per chunk (== template N)
   int nrc, ntile_c, ntile_d;
   int spc;                   // samples per context row chunk = N / p
@@ -747,12 +749,14 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
             if (++t == ntl) { t = 0; ++cl; }
             continue;
           }
-          const bool vpos = t * kBM + pos < L;
+          const int tpos = t * kBM + pos;
           if (h0) {
 #pragma unroll
             for (int k = 0; k < kNarrowP; ++k) {
               if (k < P.p) {
-                xv[k] = vpos ? xv[k] * sl2 : kNegInf;
+                // multi-token step: the intra-step causal bound of token k % ntok
+                const int Lk = P.ntok > 1 ? max(L - (P.ntok - 1 - k % P.ntok), P.lens_offset) : L;
+                xv[k] = tpos < Lk ? xv[k] * sl2 : kNegInf;
                 float v = xv[k];
 #pragma unroll
                 for (int off = 16; off >= 1; off >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, off));
@@ -934,11 +938,14 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
               need |= x[n] > kTh;
             }
           } else {
-            const bool vpos = tl * kBM + pos < L;
+            const int tpos = tl * kBM + pos;
+            const bool vpos = tpos < L;
 #pragma unroll
             for (int n = 0; n < CPT; ++n) {
               const int col = col0 + n;
-              const bool vc = vpos && col >= cv0 && col < cv1;
+              bool vc = vpos && col >= cv0 && col < cv1;
+              if (s.dec && P.ntok > 1)  // intra-step causal bound of the column's token
+                vc = vc && tpos < max(L - (P.ntok - 1 - (col - cv0) % P.ntok), P.lens_offset);
               const float mref = (mr[n] == kNegInf) ? 0.f : mr[n];
               x[n] = vc ? fmaf(x[n], sl2, -mref) : kNegInf;
               need |= vc && (mr[n] == kNegInf || x[n] > kTh);

@@ -111,6 +111,7 @@ struct Plan {
   int S = 0, dec_slot0 = 0;
   size_t off_o = 0, off_ml = 0, ws_bytes = 0;
   int launches = 0;
+  int ntok = 1;  // query tokens per (sample, head) row group (multi-token step)
 };
 
 // Split the flat tile sequence [0, T) (chunk ends `ends`, increasing, last =
@@ -176,6 +177,8 @@ int validate(const ba_problem_t* pr) {
   if (pr->dtype != BA_BF16 && pr->dtype != BA_FP32) return BA_EDTYPE;
   if (pr->b < 1 || pr->h < 1 || pr->g < 1 || pr->mc < 1 || pr->md_cap < 0) return BA_EINVAL;
   if (pr->h % pr->g != 0) return BA_EINVAL;
+  if (pr->n_tok < 0 || pr->n_tok > 128 || (long long)pr->h * (pr->n_tok > 1 ? pr->n_tok : 1) > (1 << 20))
+    return BA_EINVAL;
   const int d = pr->d;
   if (d != 16 && d != 32 && d != 64 && d != 128 && d != 256) return BA_EINVAL;
   // int32 index safety for the per-tensor element counts used in the kernels
@@ -184,11 +187,24 @@ int validate(const ba_problem_t* pr) {
   return BA_OK;
 }
 
+// The kernels see a multi-token step (n_tok = n > 1) as h*n query rows per
+// sample in g groups (q [b][h][n][d] is [b][h*n][d]; the n tokens of a head are
+// adjacent rows of its group) plus the intra-step causal bound per row.
+inline int ntok_of(const ba_problem_t* pr) { return pr->n_tok > 1 ? pr->n_tok : 1; }
+inline ba_problem_t effective(const ba_problem_t* pr) {
+  ba_problem_t e = *pr;
+  e.h = pr->h * ntok_of(pr);
+  return e;
+}
+
 // Plan for the bifurcated step (replicated == false) or the replicated baseline.
-int make_plan(const ba_problem_t* pr, int sms, bool replicated, Plan* pl) {
-  int rc = validate(pr);
+int make_plan(const ba_problem_t* pr_in, int sms, bool replicated, Plan* pl) {
+  int rc = validate(pr_in);
   if (rc) return rc;
+  const ba_problem_t E = effective(pr_in);
+  const ba_problem_t* pr = &E;
   Plan P;
+  P.ntok = ntok_of(pr_in);
   P.D = pr->d;
   P.bf16 = pr->dtype == BA_BF16;
   P.elem = P.bf16 ? 2 : 4;
@@ -199,14 +215,25 @@ int make_plan(const ba_problem_t* pr, int sms, bool replicated, Plan* pl) {
   int tcN = 0;
   if (P.bf16 && pr->d == 128 && R >= 16 && !(pr->flags & BA_FLAG_FORCE_FMA)) {
     // tcgen05 plan: N = rows per chunk, a multiple of 16 and of p, >= p
-    static const int cands[] = {16, 32, 48, 64};  // > 64 spills softmax registers
-    int best_fit = 0, largest = 0;
+    // N = 48/64 spill softmax registers (128 per thread at 512 threads) and
+    // leave 2 K/V stages: measured 2x slower per tile than N = 32 (round-1
+    // N sweep), which beats them even with twice the context row chunks.  So
+    // the smallest legal N that covers min(R, 32) rows.
+    static const int cands[] = {16, 32, 48, 64};
+    const int want = R < 32 ? R : 32;
     for (int N : cands) {
       if (N % p) continue;
-      largest = N;
-      if (!best_fit && N >= R) best_fit = N;
+      if (!tcN) tcN = N;  // smallest legal
+      if (N >= want) {
+        tcN = N;
+        break;
+      }
     }
-    tcN = best_fit ? best_fit : largest;
+    static const int n_env = [] {  // experiment override: BIFATTN_N=16|32|48|64
+      const char* e = getenv("BIFATTN_N");
+      return e ? atoi(e) : 0;
+    }();
+    if (n_env && n_env % p == 0 && (n_env == 16 || n_env == 32 || n_env == 48 || n_env == 64)) tcN = n_env;
   }
   if (tcN) {
     P.tc = true;
@@ -506,7 +533,7 @@ int run_tc(const ba_problem_t* pr, const Plan& P, const void* q, const void* Kc,
   if (rc) return rc;
   bp.lens = lens;
   bp.b = pr->b; bp.h = pr->h; bp.g = pr->g; bp.p = p; bp.mc = pr->mc;
-  bp.dec_cap = P.dec_cap; bp.lens_offset = P.lens_offset;
+  bp.dec_cap = P.dec_cap; bp.lens_offset = P.lens_offset; bp.ntok = P.ntok;
   bp.N = P.tc_N;
   bp.nrc = P.tc_nrc; bp.ntile_c = P.tc_ntile_c; bp.ntile_d = P.tc_ntile_d;
   bp.spc = P.tc_N / p;
@@ -568,6 +595,7 @@ int run_plan(const ba_problem_t* pr, const Plan& P, const void* q, const void* K
   fp.q = q; fp.Kc = Kc; fp.Vc = Vc; fp.Kd = Kd; fp.Vd = Vd; fp.lens = lens;
   fp.b = b; fp.h = h; fp.g = g; fp.p = p; fp.mc = pr->mc;
   fp.dec_stride = P.dec_stride; fp.dec_cap = P.dec_cap; fp.lens_offset = P.lens_offset;
+  fp.ntok = P.ntok;
   fp.scale_log2 = scale * ba::kLog2e;
   fp.nsc = P.nsc; fp.nsd = P.nsd;
   fp.ctx_chunk = P.ctx_chunk; fp.dec_chunk = P.dec_chunk;
@@ -680,9 +708,10 @@ int bifurcated_attn_decode(const ba_problem_t* prob, const void* q, const void* 
   }
   if (lse && (reinterpret_cast<uintptr_t>(lse) & 3u)) return BA_EALIGN;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const ba_problem_t E = effective(prob);  // h*n query rows per sample
   if (P.bf16)
-    return run_d<__nv_bfloat16>(prob, P, q, Kc, Vc, Kd, Vd, lens, out, lse, workspace, st);
-  return run_d<float>(prob, P, q, Kc, Vc, Kd, Vd, lens, out, lse, workspace, st);
+    return run_d<__nv_bfloat16>(&E, P, q, Kc, Vc, Kd, Vd, lens, out, lse, workspace, st);
+  return run_d<float>(&E, P, q, Kc, Vc, Kd, Vd, lens, out, lse, workspace, st);
 }
 
 int replicated_attn_decode(const ba_problem_t* prob, const void* q, const void* K,
@@ -702,9 +731,10 @@ int replicated_attn_decode(const ba_problem_t* prob, const void* q, const void* 
   if (rc) return rc;
   if (lse && (reinterpret_cast<uintptr_t>(lse) & 3u)) return BA_EALIGN;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const ba_problem_t E = effective(prob);
   if (P.bf16)
-    return run_d<__nv_bfloat16>(prob, P, q, nullptr, nullptr, K, V, lens, out, lse, workspace, st);
-  return run_d<float>(prob, P, q, nullptr, nullptr, K, V, lens, out, lse, workspace, st);
+    return run_d<__nv_bfloat16>(&E, P, q, nullptr, nullptr, K, V, lens, out, lse, workspace, st);
+  return run_d<float>(&E, P, q, nullptr, nullptr, K, V, lens, out, lse, workspace, st);
 }
 
 int bifurcated_attn_decode_host(const ba_problem_t* prob, const void* hq, const void* hKc,
@@ -722,7 +752,7 @@ int bifurcated_attn_decode_host(const ba_problem_t* prob, const void* hq, const 
   if (rc) return rc;
   const size_t e = prob->dtype == BA_BF16 ? 2 : 4;
   const size_t d = prob->d;
-  const size_t nq = (size_t)prob->b * prob->h * d * e;
+  const size_t nq = (size_t)prob->b * prob->h * ntok_of(prob) * d * e;
   const size_t nc = (size_t)prob->g * prob->mc * d * e;
   const size_t nd = (size_t)prob->b * prob->g * prob->md_cap * d * e;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -748,7 +778,8 @@ int bifurcated_attn_decode_host(const ba_problem_t* prob, const void* hq, const 
   if (rc) return rc;
   if ((rc = cp(hout, dout, nq, cudaMemcpyDeviceToHost))) return rc;
   if (hlse && dlse) {
-    if ((rc = cp(hlse, dlse, (size_t)prob->b * prob->h * sizeof(float), cudaMemcpyDeviceToHost)))
+    if ((rc = cp(hlse, dlse, (size_t)prob->b * prob->h * ntok_of(prob) * sizeof(float),
+                  cudaMemcpyDeviceToHost)))
       return rc;
   }
   return BA_OK;
@@ -838,6 +869,6 @@ const char* ba_strerror(int code) {
 
 int ba_last_cuda_error(void) { return g_last_cuda_error; }
 
-int ba_version(void) { return 1; }
+int ba_version(void) { return 2; }
 
 }  // extern "C"

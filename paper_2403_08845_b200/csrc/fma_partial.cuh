@@ -35,6 +35,8 @@ struct FmaParams {
   int dec_stride;   // position stride of Kd/Vd (md_cap, or mc+md_cap for the replicated baseline)
   int dec_cap;      // clamp for lens[i]
   int lens_offset;  // decode valid length = lens_offset + clamp(lens[i], 0, dec_cap)
+  int ntok;         // tokens per head (multi-token step): token k of a row group sees
+                    // decode positions < max(L - (ntok - 1 - k), lens_offset)
   float scale_log2; // scale * log2(e)
   int nsc, nsd;     // context / decode splits per row (nsc = 0: no context branch)
   int ctx_chunk, dec_chunk;  // keys per split
@@ -110,6 +112,7 @@ __global__ void __launch_bounds__(128) fma_partial_kernel(const FmaParams P) {
   // ---- decode the work item --------------------------------------------
   int it = blockIdx.x;
   int c, r_begin, r_end, t0, t1, slot, row_base;  // rows r -> (r/p)*h + c*p + r%p
+  int dec_L = -1, dec_r0 = 0;  // decode item: valid length, first row of the sample
   const T* Kb;
   const T* Vb;
   if (it < P.n_ctx_items) {
@@ -135,6 +138,8 @@ __global__ void __launch_bounds__(128) fma_partial_kernel(const FmaParams P) {
     int L = P.lens[i];
     L = L < 0 ? 0 : (L > P.dec_cap ? P.dec_cap : L);
     L += P.lens_offset;
+    dec_L = L;
+    dec_r0 = i * P.p;
     r_begin = i * P.p + rb * RB;
     r_end = min(i * P.p + P.p, r_begin + RB);
     t0 = s * P.dec_chunk;
@@ -170,6 +175,17 @@ __global__ void __launch_bounds__(128) fma_partial_kernel(const FmaParams P) {
     }
   }
 
+  // per-row end of the valid keys: t1, or for a decode row the intra-step
+  // causal bound of its token (multi-token step; ntok = 1: t1)
+  int lim[RB];
+#pragma unroll
+  for (int r = 0; r < RB; ++r) {
+    lim[r] = t1;
+    if (dec_L >= 0 && P.ntok > 1) {
+      const int k = (r_begin + r - dec_r0) % P.ntok;
+      lim[r] = min(t1, max(dec_L - (P.ntok - 1 - k), P.lens_offset));
+    }
+  }
   float m[RB], l[RB], o[RB][NCH][LW];
 #pragma unroll
   for (int r = 0; r < RB; ++r) {
@@ -237,7 +253,7 @@ __global__ void __launch_bounds__(128) fma_partial_kernel(const FmaParams P) {
       float mx = m[r];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        if (tk[u] >= t1) s[u][r] = kNegInf;
+        if (tk[u] >= lim[r]) s[u][r] = kNegInf;
         mx = fmaxf(mx, s[u][r]);
       }
       const float ms = (mx == kNegInf) ? 0.f : mx;

@@ -28,6 +28,12 @@ def host_cores() -> int:
 def oracle_rows(inp, rows=None):
     """fp64 oracle on the given flat rows (i*h + j) of ``inp`` (tensors may be on
     the GPU: only the slices a row needs are copied to the host)."""
+    if inp.q.dim() == 4:  # multi-token step: all rows, on the host
+        assert rows is None
+        out, lse, _ = oracle.attn_decode(inp.q.cpu(), inp.Kc.cpu(), inp.Vc.cpu(), inp.Kd.cpu(),
+                                         inp.Vd.cpu(), inp.lens.cpu(), scale=inp.scale,
+                                         nthreads=host_cores())
+        return out, lse
     b, h, d = inp.q.shape
     g = inp.Kc.shape[0]
     p = h // g

@@ -30,11 +30,12 @@ def owner(cs, f):
 
 
 def pick_n(b, h, g):
-    """Rows per chunk: the smallest N in {16,32,48,64} with p | N and N >= b*p,
-    else the largest with p | N (the planner's rule, bifattn_api.cu)."""
+    """Rows per chunk: the smallest N in {16,32,48,64} with p | N and
+    N >= min(b*p, 32), else the largest with p | N (the planner's rule,
+    bifattn_api.cu: N = 48/64 spill softmax registers)."""
     p = h // g
     cands = [n for n in (16, 32, 48, 64) if n % p == 0]
-    fit = [n for n in cands if n >= b * p]
+    fit = [n for n in cands if n >= min(b * p, 32)]
     return fit[0] if fit else cands[-1]
 
 
