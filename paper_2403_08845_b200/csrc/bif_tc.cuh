@@ -41,8 +41,9 @@
 // compute the exact tile max per column and raise m_run — rescaling l and
 // O^T only for columns whose max actually grew.  Same softmax; P <= 2^kTh.
 //
-// Work split: flat tiles f in [0, Tc + Td): context tiles first,
-// f = (c*nrc + rc)*ntile_c + t, then decode tiles in Kd memory order,
+// Work split: flat tiles f in [0, Tc + Td): context tiles first, in units
+// (c, band, rc) of bw tiles (ctx_unit; one band = f = (c*nrc + rc)*ntile_c + t
+// when nrc = 1), then decode tiles in Kd memory order,
 // f = Tc + (i*g + c)*ntile_d + t.  CTA k streams the contiguous range
 // [cs[k], cs[k+1]) planned on the host (bifattn_api.cu, plan_split): equal
 // 64 KB-tile counts, except that a range crossing into another chunk is
@@ -71,6 +72,7 @@ struct BifTcParams {
                              // positions < max(L - (ntok - 1 - k % ntok), lens_offset)
   int N;                     // rows per chunk (== template N)
   int nrc, ntile_c, ntile_d;
+  int bw, nband;             // context band width (tiles) and bands per group (see seg_at)
   int spc;                   // samples per context row chunk = N / p
   int gpc, ndc;              // groups per decode chunk = N / p; decode chunks per sample
   int qd_rows;               // rows of the decode q box = min(N, h)
@@ -174,20 +176,57 @@ __host__ __device__ inline long long dec_chunk_end(long long g, long long gpc, l
   return ((long long)i * g + c1) * ntd;
 }
 
+// Context unit of flat context tile f: the context tiles of group c are cut
+// into bands of bw tiles (the last band may be narrower) and ordered
+// (c, band, rc, tile): the nrc row chunks of a band follow each other, so a
+// CTA re-reads a band's K/V while it is still in L2 (bw = ntile_c: one band,
+// the plain (c, rc, tile) order).  Returns the unit's first flat tile and
+// width; c, band, rc and the tile index within the group through the refs.
+__host__ __device__ inline long long ctx_unit(int nrc, int ntc, int bw, long long f, int& c,
+                                             int& band, int& rc, int& tg, int& wb) {
+  const long long GT = (long long)nrc * ntc;
+  c = (int)(f / GT);
+  const long long r = f - (long long)c * GT;
+  const int nfull = ntc / bw;
+  const long long full = (long long)nfull * nrc * bw;
+  long long base;
+  int tb;
+  if (r < full) {
+    band = (int)(r / ((long long)nrc * bw));
+    const long long rr = r - (long long)band * nrc * bw;
+    wb = bw;
+    rc = (int)(rr / bw);
+    tb = (int)(rr - (long long)rc * bw);
+    base = (long long)band * nrc * bw;
+  } else {
+    const long long r2 = r - full;
+    band = nfull;
+    wb = ntc - nfull * bw;
+    rc = (int)(r2 / wb);
+    tb = (int)(r2 - (long long)rc * wb);
+    base = full;
+  }
+  tg = band * bw + tb;
+  return (long long)c * GT + base + (long long)rc * wb;
+}
+
 BA_DEVINL Seg seg_at(const BifTcParams& P, const Range& rg, long long w) {
   Seg s;
   const long long f = rg.f0 + w;
   if (f < P.Tc) {
-    const long long seg = f / P.ntile_c;
-    const long long fend = min((seg + 1) * P.ntile_c, rg.f1);
+    int c, band, rc, tg, wb;
+    const long long u0 = ctx_unit(P.nrc, P.ntile_c, P.bw, f, c, band, rc, tg, wb);
+    const long long fend = min(u0 + wb, rg.f1);
     s.dec = false;
-    s.c = (int)(seg / P.nrc);
-    s.rc = (int)(seg % P.nrc);
+    s.c = c;
+    s.rc = rc;
     s.i = s.cb = 0;
-    s.t0 = (int)(f - seg * P.ntile_c);
+    s.t0 = tg;
     s.c0 = s.c;
     s.ntiles = (int)(fend - f);
-    s.slot = (int)blockIdx.x - owner(P.cs, P.G, seg * P.ntile_c);
+    // banded: the planner never splits a unit, slot = band; else the CTA's
+    // index among the CTAs that share the chunk
+    s.slot = P.nband > 1 ? band : (int)blockIdx.x - owner(P.cs, P.G, u0);
     s.next = w + (fend - f);
   } else {
     const long long fd = f - P.Tc;
@@ -218,10 +257,11 @@ BA_DEVINL int ctx_tile(const BifTcParams& P, const Seg& s, int j) {
 BA_DEVINL void tile_at(const BifTcParams& P, const Range& rg, long long w, bool& dec, int& z, int& t) {
   const long long f = rg.f0 + w;
   if (f < P.Tc) {
-    const long long seg = f / P.ntile_c;
+    int c, band, rc, tg, wb;
+    ctx_unit(P.nrc, P.ntile_c, P.bw, f, c, band, rc, tg, wb);
     dec = false;
-    z = (int)(seg / P.nrc);
-    t = (int)(f - seg * P.ntile_c);
+    z = c;
+    t = tg;
   } else {
     const long long fd = f - P.Tc;
     const long long ic = fd / P.ntile_d;  // i*g + c = the Kd/Vd map's z
@@ -234,6 +274,7 @@ BA_DEVINL void tile_at(const BifTcParams& P, const Range& rg, long long w, bool&
 // Partials written for context chunk (c, rc) / decode chunk (i, cb).
 __host__ __device__ inline int ctx_parts(const BifTcParams& P, int c, int rc) {
   if (P.Tc == 0) return 0;
+  if (P.nband > 1) return P.nband;  // one partial per band (units are never split)
   const long long ff = ((long long)c * P.nrc + rc) * P.ntile_c;
   return parts_of(P.cs, P.G, ff, ff + P.ntile_c);
 }

@@ -100,6 +100,7 @@ struct Plan {
   // tcgen05 plan
   int tc_N = 0, tc_nrc = 0, tc_ntile_c = 0, tc_ntile_d = 0, tc_G = 0, tc_nst = 0, tc_npb = 1;
   int tc_Sc = 0, tc_Sd = 0, tc_smem = 0;
+  int tc_bw = 0, tc_nband = 0;  // context band width (tiles), bands per group
   long long tc_Tc = 0, tc_T = 0;
   int tc_cs[ba::bif_max_ctas + 1];
   size_t off_cnt = 0;
@@ -118,7 +119,8 @@ struct Plan {
 // T) into G non-empty contiguous CTA ranges cs[0..G].  Each CTA gets about the
 // same cost = tiles + kSegPenalty per extra chunk it enters; a range stops at
 // a chunk end when the leftover budget could not pay for another segment.
-void plan_split(const std::vector<long long>& ends, long long T, long long Tc, int G, int* cs) {
+void plan_split(const std::vector<long long>& ends, long long T, long long Tc, int G, int* cs,
+                bool whole_ctx_units) {
   static const double kSegPenalty = [] {
     const char* e = getenv("BIFATTN_SEG_PENALTY");
     return e ? atof(e) : 2.0;
@@ -155,6 +157,14 @@ void plan_split(const std::vector<long long>& ends, long long T, long long Tc, i
         ++ci;
         if (budget < kSegPenalty + 1.0) break;  // no room for another segment
         budget -= kSegPenalty;
+      } else if (whole_ctx_units && cur < Tc) {
+        // banded context: units are never split (one partial slot per band);
+        // take the unit if at least half of it fits the budget
+        if (cur == start || budget >= 0.5 * rc) {
+          cur = ends[ci];
+          ++ci;
+        }
+        break;
       } else {
         const double unit = cur < Tc ? 1.0 : kDecCost;
         long long take = (long long)(budget / unit + 0.5);
@@ -265,20 +275,59 @@ int make_plan(const ba_problem_t* pr_in, int sms, bool replicated, Plan* pl) {
     P.tc_smem = P.tc_nst * ba::bif::kStageBytes + ba::bif::smem_fixed(tcN, P.tc_npb);
     const int gpc = tcN / p;  // groups per decode chunk
     const int ndc = (g + gpc - 1) / gpc;
-    // chunk ends in the flat [context | decode] tile space
-    std::vector<long long> ends;
-    for (long long k = 0; P.tc_ntile_c && k < (long long)g * P.tc_nrc; ++k)
-      ends.push_back((k + 1) * P.tc_ntile_c);
-    for (int i = 0; P.tc_ntile_d && i < b; ++i)
-      for (int cb = 0; cb < ndc; ++cb)
-        ends.push_back(P.tc_Tc + ba::bif::dec_chunk_end(g, gpc, P.tc_ntile_d, i, cb));
-    plan_split(ends, P.tc_T, P.tc_Tc, P.tc_G, P.tc_cs);
+    // context bands (ctx_unit, bif_tc.cuh): with several row chunks per group
+    // the context is cut into bands of bw tiles whose row-chunk passes follow
+    // each other (L2 re-reads instead of HBM); one band when nrc = 1
+    static const int bw_env = [] {  // experiment override: BIFATTN_BAND=<tiles>
+      const char* e = getenv("BIFATTN_BAND");
+      return e ? atoi(e) : 0;
+    }();
+    // Default: one band.  Measured (round 1, profiles/r01/band_sweep.txt): bands
+    // of 8/16/32 tiles were SLOWER on C3, C4, C5 and the 4-token C2b step —
+    // the re-reads already hit L2 where the context fits, and a multi-chunk
+    // tile pass is bound by the per-tile softmax, not by HBM.
+    int bw_try = P.tc_ntile_c;
+    if (P.tc_nrc > 1 && P.tc_ntile_c > 0 && bw_env > 0 && bw_env < P.tc_ntile_c) bw_try = bw_env;
     int sc = 0, sd = 0;
-    long long prev = 0;
-    for (size_t k = 0; k < ends.size(); ++k) {
-      const int n = ba::bif::parts_of(P.tc_cs, P.tc_G, prev, ends[k]);
-      if (prev < P.tc_Tc) sc = std::max(sc, n); else sd = std::max(sd, n);
-      prev = ends[k];
+    for (;;) {
+      P.tc_bw = bw_try;
+      P.tc_nband = P.tc_ntile_c ? cdiv(P.tc_ntile_c, P.tc_bw) : 0;
+      const bool banded = P.tc_nband > 1;
+      // unit ends in the flat [context | decode] tile space
+      std::vector<long long> ends;
+      for (int c = 0; P.tc_ntile_c && c < g; ++c) {
+        long long f = (long long)c * P.tc_nrc * P.tc_ntile_c;
+        for (int band = 0; band < P.tc_nband; ++band) {
+          const int wb = std::min(P.tc_bw, P.tc_ntile_c - band * P.tc_bw);
+          for (int r = 0; r < P.tc_nrc; ++r) {
+            f += wb;
+            ends.push_back(f);
+          }
+        }
+      }
+      for (int i = 0; P.tc_ntile_d && i < b; ++i)
+        for (int cb = 0; cb < ndc; ++cb)
+          ends.push_back(P.tc_Tc + ba::bif::dec_chunk_end(g, gpc, P.tc_ntile_d, i, cb));
+      plan_split(ends, P.tc_T, P.tc_Tc, P.tc_G, P.tc_cs, banded);
+      sc = sd = 0;
+      bool whole = true;
+      long long prev = 0;
+      for (size_t k = 0; k < ends.size(); ++k) {
+        const int n = ba::bif::parts_of(P.tc_cs, P.tc_G, prev, ends[k]);
+        if (prev < P.tc_Tc) {
+          whole = whole && n == 1;
+          sc = std::max(sc, n);
+        } else {
+          sd = std::max(sd, n);
+        }
+        prev = ends[k];
+      }
+      if (!banded) break;
+      if (whole) {
+        sc = P.tc_nband;  // one partial per band
+        break;
+      }
+      bw_try = P.tc_ntile_c;  // a unit got split (tiny problem): plain order
     }
     P.tc_Sc = sc;
     P.tc_Sd = sd;
@@ -536,6 +585,7 @@ int run_tc(const ba_problem_t* pr, const Plan& P, const void* q, const void* Kc,
   bp.dec_cap = P.dec_cap; bp.lens_offset = P.lens_offset; bp.ntok = P.ntok;
   bp.N = P.tc_N;
   bp.nrc = P.tc_nrc; bp.ntile_c = P.tc_ntile_c; bp.ntile_d = P.tc_ntile_d;
+  bp.bw = P.tc_bw > 0 ? P.tc_bw : 1; bp.nband = P.tc_nband;
   bp.spc = P.tc_N / p;
   bp.gpc = P.tc_N / p;
   bp.ndc = (pr->g + bp.gpc - 1) / bp.gpc;
@@ -804,9 +854,9 @@ const char* ba_plan_string(const ba_problem_t* prob) {
   }
   if (P.tc)
     snprintf(g_plan_buf, sizeof g_plan_buf,
-             "fused_tc(N=%d,nrc=%d,ctx_tiles=%lld,dec_tiles=%lld,ctas=%d,stages=%d,pbuf=%d,"
+             "fused_tc(N=%d,nrc=%d,band=%d,ctx_tiles=%lld,dec_tiles=%lld,ctas=%d,stages=%d,pbuf=%d,"
              "slots=%d+%d,smem=%d) launches=1 ws=%zu",
-             P.tc_N, P.tc_nrc, P.tc_Tc, P.tc_T - P.tc_Tc, P.tc_G, P.tc_nst, P.tc_npb, P.tc_Sc,
+             P.tc_N, P.tc_nrc, P.tc_bw, P.tc_Tc, P.tc_T - P.tc_Tc, P.tc_G, P.tc_nst, P.tc_npb, P.tc_Sc,
              P.tc_Sd, P.tc_smem, P.ws_bytes);
   else
     snprintf(g_plan_buf, sizeof g_plan_buf,

@@ -39,7 +39,9 @@ def pick_n(b, h, g):
     return fit[0] if fit else cands[-1]
 
 
-def model(b, h, g, mc, md, cs):
+def model(b, h, g, mc, md, cs, bw):
+    """Python model of seg_at / ctx_unit / ctx_parts / dec_parts (bif_tc.cuh)
+    over the planner's CTA table; bw = the plan's context band width."""
     p = h // g
     N = pick_n(b, h, g)
     R = b * p
@@ -52,29 +54,48 @@ def model(b, h, g, mc, md, cs):
     Td = g * b * ntd
     T = Tc + Td
     G = len(cs) - 1
+    nband = -(-ntc // bw)
+    banded = nband > 1
+    assert not banded or nrc > 1
     assert cs[0] == 0 and cs[-1] == T
     assert all(cs[k] < cs[k + 1] for k in range(G)), "empty CTA range"
-    # chunks: (kind, id, begin, end)
-    chunks = [("c", k, k * ntc, (k + 1) * ntc) for k in range(g * nrc)]
+    # units: (kind, chunk id, slot base, begin, end) in flat order (c, band, rc, tile)
+    chunks = []
+    f = 0
+    for c in range(g):
+        for band in range(nband):
+            wb = min(bw, ntc - band * bw)
+            for rc in range(nrc):
+                chunks.append(("c", (c, rc), band, f, f + wb))
+                f += wb
+    assert f == Tc
     for i in range(b if ntd else 0):
         for cb in range(ndc):
             a = Tc + (i * g + cb * gpc) * ntd
             e = Tc + (i * g + min(g, (cb + 1) * gpc)) * ntd
-            chunks.append(("d", (i, cb), a, e))
+            chunks.append(("d", (i, cb), 0, a, e))
     seen = [0] * T
     writes = {}
     for k in range(G):
         f = cs[k]
         while f < cs[k + 1]:
-            kind, cid, a, e = next(ch for ch in chunks if ch[2] <= f < ch[3])
+            kind, cid, band, a, e = next(ch for ch in chunks if ch[3] <= f < ch[4])
             fend = min(e, cs[k + 1])
             for ff in range(f, fend):
                 seen[ff] += 1
-            writes.setdefault((kind, cid), []).append(k - owner(cs, a))
+            if kind == "c" and banded:
+                assert a == f and fend == e, "a banded context unit was split"
+                writes.setdefault((kind, cid), []).append(band)
+            else:
+                writes.setdefault((kind, cid), []).append(k - owner(cs, a))
             f = fend
     assert all(x == 1 for x in seen)
     sc = sd = 0
-    for kind, cid, a, e in chunks:
+    for kind, cid, band, a, e in chunks:
+        if kind == "c" and banded:
+            assert sorted(writes[(kind, cid)]) == list(range(nband))
+            sc = nband
+            continue
         parts = owner(cs, e - 1) - owner(cs, a) + 1
         assert sorted(writes[(kind, cid)]) == list(range(parts))
         if kind == "c":
@@ -84,7 +105,7 @@ def model(b, h, g, mc, md, cs):
     # planner cost: decode tiles weigh DEC_COST (bifattn_api.cu, plan_split)
     loads = [(min(cs[k + 1], Tc) - min(cs[k], Tc)) + DEC_COST * (max(cs[k + 1], Tc) - max(cs[k], Tc))
              for k in range(G)]
-    return N, sc, sd, loads
+    return N, sc, sd, loads, banded
 
 
 SHAPES = [
@@ -103,15 +124,45 @@ def test_split_covers_every_tile_once_and_slots_match(shape):
     prob = ba.make_problem(b, h, g, 128, mc, md, 0)
     cs = ba.ba_plan_ctas(prob)
     assert cs, "tensor-core plan expected"
-    N, sc, sd, loads = model(b, h, g, mc, md, cs)
     plan = ba.ba_plan_string(prob)
-    m = re.search(r"N=(\d+).*slots=(\d+)\+(\d+)", plan)
+    m = re.search(r"N=(\d+).*band=(\d+).*slots=(\d+)\+(\d+)", plan)
     assert m, plan
-    assert (int(m.group(1)), int(m.group(2)), int(m.group(3))) == (N, sc, sd)
+    N, sc, sd, loads, banded = model(b, h, g, mc, md, cs, int(m.group(2)))
+    assert (int(m.group(1)), int(m.group(3)), int(m.group(4))) == (N, sc, sd)
     mean = sum(loads) / len(loads)
-    assert max(loads) <= mean + 3 + 0.1 * mean  # the segment penalty only trims loads
+    # the segment penalty only trims loads; whole banded units (8 tiles) add
+    # at most half a unit
+    assert max(loads) <= mean + 3 + 0.1 * mean + (4 if banded else 0)
 
 
 def test_fma_plan_has_no_cta_table():
     _build.build()
     assert ba.ba_plan_ctas(ba.make_problem(4, 2, 2, 16, 32, 4, 1)) == []
+
+
+def test_banded_context_split_in_subprocess():
+    """The banded context order (BIFATTN_BAND, experiment setting) keeps the
+    same invariants: whole units per CTA, one slot per band, every tile once."""
+    import json
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import json, re, paper_2403_08845_b200 as ba\n"
+        "out = []\n"
+        "for s in [(64, 32, 8, 16384, 512), (256, 64, 64, 4096, 256), (40, 2, 2, 1290, 33)]:\n"
+        "    pr = ba.make_problem(s[0], s[1], s[2], 128, s[3], s[4], 0)\n"
+        "    out.append([list(s), ba.ba_plan_ctas(pr), ba.ba_plan_string(pr)])\n"
+        "print(json.dumps(out))\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, BIFATTN_BAND="8", PYTHONPATH=root)
+    res = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                         check=True, cwd=root)
+    for (b, h, g, mc, md), cs, plan in json.loads(res.stdout.strip().splitlines()[-1]):
+        m = re.search(r"N=(\d+).*band=(\d+).*slots=(\d+)\+(\d+)", plan)
+        bw = int(m.group(2))
+        ntc = -(-mc // 128)
+        assert bw in (8, ntc), plan  # tiny problems fall back to one band
+        N, sc, sd, loads, banded = model(b, h, g, mc, md, cs, bw)
+        assert banded == (bw == 8) and (banded or b < 64)
+        assert (int(m.group(1)), int(m.group(3)), int(m.group(4))) == (N, sc, sd)
