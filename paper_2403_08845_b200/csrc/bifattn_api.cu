@@ -22,6 +22,7 @@
 #include "bif_tc.cuh"
 #include "fma_partial.cuh"
 #include "merge.cuh"
+#include "append.cuh"
 
 namespace {
 
@@ -115,20 +116,23 @@ struct Plan {
   int ntok = 1;  // query tokens per (sample, head) row group (multi-token step)
 };
 
+// bifurcated_attn_decode_append: this step's K/V rows and the lens update.
+struct AppendArgs {
+  const void* k_new;
+  const void* v_new;
+  int32_t* lens;  // updated in place after the step
+  int n;          // rows appended per (sample, group)
+};
+
 // Split the flat tile sequence [0, T) (chunk ends `ends`, increasing, last =
 // T) into G non-empty contiguous CTA ranges cs[0..G].  Each CTA gets about the
 // same cost = tiles + kSegPenalty per extra chunk it enters; a range stops at
 // a chunk end when the leftover budget could not pay for another segment.
 void plan_split(const std::vector<long long>& ends, long long T, long long Tc, int G, int* cs,
-                bool whole_ctx_units) {
+                bool whole_ctx_units, double kDecCost) {
   static const double kSegPenalty = [] {
     const char* e = getenv("BIFATTN_SEG_PENALTY");
     return e ? atof(e) : 2.0;
-  }();
-  // decode tiles (narrow softmax path) cost more than context tiles
-  static const double kDecCost = [] {
-    const char* e = getenv("BIFATTN_DEC_COST");
-    return e ? atof(e) : 1.25;
   }();
   // cost of tiles [a, b)
   auto cost = [&](long long a, long long b) {
@@ -288,6 +292,26 @@ int make_plan(const ba_problem_t* pr_in, int sms, bool replicated, Plan* pl) {
     // tile pass is bound by the per-tile softmax, not by HBM.
     int bw_try = P.tc_ntile_c;
     if (P.tc_nrc > 1 && P.tc_ntile_c > 0 && bw_env > 0 && bw_env < P.tc_ntile_c) bw_try = bw_env;
+    // Cost of a decode tile relative to a context tile pass, for balancing
+    // the CTA ranges.  Measured optima (round 1 sweeps, profiles/r01/
+    // deccost_sweep.txt): 1.7 at N = 16 (C2a), 1.25 at N = 32 (C2b and C5,
+    // whose 1 GB context is re-read from HBM by its 8 row chunks), 2.0 when
+    // several row chunks pass an L2-resident context (C3, the 4-token C2b
+    // step: the re-reads are L2 hits, cheaper than decode tiles from HBM),
+    // more for MQA's 128 passes over a 4 MB context (C4).
+    static const double dc_env = [] {
+      const char* e = getenv("BIFATTN_DEC_COST");
+      return e ? atof(e) : 0.0;
+    }();
+    // The re-reads hit L2 when the whole context fits in it, or when a chunk
+    // is about as long as a CTA's range, so that the nrc passes over a group
+    // run concurrently on neighbouring CTAs (not one after another in one CTA).
+    const double ctx_bytes = 2.0 * g * (double)pr->mc * pr->d * P.elem;
+    const bool l2_rereads = P.tc_nrc > 1 && (ctx_bytes <= 64.0 * (1 << 20) ||
+                                             1.5 * P.tc_ntile_c * P.tc_G >= (double)P.tc_T);
+    double dec_cost = tcN == 16 ? 1.7 : 1.25;
+    if (l2_rereads) dec_cost *= P.tc_nrc >= 32 ? 2.4 : 1.6;
+    if (dc_env > 0) dec_cost = dc_env;
     int sc = 0, sd = 0;
     for (;;) {
       P.tc_bw = bw_try;
@@ -308,7 +332,7 @@ int make_plan(const ba_problem_t* pr_in, int sms, bool replicated, Plan* pl) {
       for (int i = 0; P.tc_ntile_d && i < b; ++i)
         for (int cb = 0; cb < ndc; ++cb)
           ends.push_back(P.tc_Tc + ba::bif::dec_chunk_end(g, gpc, P.tc_ntile_d, i, cb));
-      plan_split(ends, P.tc_T, P.tc_Tc, P.tc_G, P.tc_cs, banded);
+      plan_split(ends, P.tc_T, P.tc_Tc, P.tc_G, P.tc_cs, banded, dec_cost);
       sc = sd = 0;
       bool whole = true;
       long long prev = 0;
@@ -557,7 +581,7 @@ int launch_bif_tc_n(const ba::BifTcParams& bp, int smem, uint32_t flags, LaunchR
 // Kc = Vc = nullptr, Kd/Vd are the replicated caches [b][g][mc+md_cap][d].
 int run_tc(const ba_problem_t* pr, const Plan& P, const void* q, const void* Kc, const void* Vc,
            const void* Kd, const void* Vd, const int32_t* lens, void* out, float* lse, void* ws,
-           float scale_log2, cudaStream_t st) {
+           float scale_log2, cudaStream_t st, const AppendArgs* ap) {
   ba::BifTcParams bp;
   memset(&bp, 0, sizeof bp);
   const int p = pr->h / pr->g;
@@ -581,6 +605,8 @@ int run_tc(const ba_problem_t* pr, const Plan& P, const void* q, const void* Kc,
     rc = make_tmap_3d(&bp.tmQc, q, d, pr->h, pr->b, d * 2, (uint64_t)pr->h * d * 2, p, P.tc_N / p);
   if (rc) return rc;
   bp.lens = lens;
+  bp.lens_add = ap ? ap->n : 0;
+  bp.lens_out = ap ? ap->lens : nullptr;
   bp.b = pr->b; bp.h = pr->h; bp.g = pr->g; bp.p = p; bp.mc = pr->mc;
   bp.dec_cap = P.dec_cap; bp.lens_offset = P.lens_offset; bp.ntok = P.ntok;
   bp.N = P.tc_N;
@@ -637,7 +663,8 @@ int run_tc(const ba_problem_t* pr, const Plan& P, const void* q, const void* Kc,
 template <typename T, int D>
 int run_plan(const ba_problem_t* pr, const Plan& P, const void* q, const void* Kc,
              const void* Vc, const void* Kd, const void* Vd, const int32_t* lens, void* out,
-             float* lse, void* ws, cudaStream_t st) {
+             float* lse, void* ws, cudaStream_t st,
+             const AppendArgs* ap) {
   const int b = pr->b, h = pr->h, g = pr->g, p = h / g;
   float scale = pr->scale > 0.f ? pr->scale : 1.0f / sqrtf((float)D);
   ba::FmaParams fp;
@@ -646,6 +673,29 @@ int run_plan(const ba_problem_t* pr, const Plan& P, const void* q, const void* K
   fp.b = b; fp.h = h; fp.g = g; fp.p = p; fp.mc = pr->mc;
   fp.dec_stride = P.dec_stride; fp.dec_cap = P.dec_cap; fp.lens_offset = P.lens_offset;
   fp.ntok = P.ntok;
+  fp.lens_add = ap ? ap->n : 0;
+  if (ap) {
+    // KV append (append.cuh) first; the next launch depends on it
+    ba::AppendParams a;
+    a.k_new = ap->k_new; a.v_new = ap->v_new; a.Kd = const_cast<void*>(Kd); a.Vd = const_cast<void*>(Vd);
+    a.lens = lens; a.b = b; a.g = g; a.n = ap->n; a.md_cap = P.dec_cap;
+    a.vec_per_row = D * (int)sizeof(T) / 16;
+    const long long tot = (long long)b * g * ap->n * a.vec_per_row;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)std::max(1ll, std::min((tot + 255) / 256, 4ll * 148)));
+    cfg.blockDim = dim3(256);
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = (pr->flags & BA_FLAG_NO_PDL) ? 0 : 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, ba::kv_append_kernel, a);
+    if (e != cudaSuccess) {
+      g_last_cuda_error = (int)e;
+      return BA_ECUDA;
+    }
+  }
   fp.scale_log2 = scale * ba::kLog2e;
   fp.nsc = P.nsc; fp.nsd = P.nsd;
   fp.ctx_chunk = P.ctx_chunk; fp.dec_chunk = P.dec_chunk;
@@ -656,7 +706,7 @@ int run_plan(const ba_problem_t* pr, const Plan& P, const void* q, const void* K
   int rc;
   if (P.tc) {
     if constexpr (sizeof(T) == 2 && D == 128)
-      return run_tc(pr, P, q, Kc, Vc, Kd, Vd, lens, out, lse, ws, fp.scale_log2, st);
+      return run_tc(pr, P, q, Kc, Vc, Kd, Vd, lens, out, lse, ws, fp.scale_log2, st, ap);
     return BA_EINVAL;
   }
   LaunchRec rec(st);
@@ -688,6 +738,10 @@ int run_plan(const ba_problem_t* pr, const Plan& P, const void* q, const void* K
   mp.nsd = P.nsd;
   mp.out = out;
   mp.lse = lse;
+  mp.lens_out = ap ? ap->lens : nullptr;
+  mp.b = b;
+  mp.lens_add = ap ? ap->n : 0;
+  mp.dec_cap = P.dec_cap;
   const int warps_per_block = 8;
   rec.begin();
   ba::merge_kernel<T, D><<<cdiv(mp.rows, warps_per_block), 32 * warps_per_block, 0, st>>>(mp);
@@ -697,13 +751,14 @@ int run_plan(const ba_problem_t* pr, const Plan& P, const void* q, const void* K
 template <typename T>
 int run_d(const ba_problem_t* pr, const Plan& P, const void* q, const void* Kc, const void* Vc,
           const void* Kd, const void* Vd, const int32_t* lens, void* out, float* lse, void* ws,
-          cudaStream_t st) {
+          cudaStream_t st,
+          const AppendArgs* ap = nullptr) {
   switch (pr->d) {
-    case 16: return run_plan<T, 16>(pr, P, q, Kc, Vc, Kd, Vd, lens, out, lse, ws, st);
-    case 32: return run_plan<T, 32>(pr, P, q, Kc, Vc, Kd, Vd, lens, out, lse, ws, st);
-    case 64: return run_plan<T, 64>(pr, P, q, Kc, Vc, Kd, Vd, lens, out, lse, ws, st);
-    case 128: return run_plan<T, 128>(pr, P, q, Kc, Vc, Kd, Vd, lens, out, lse, ws, st);
-    case 256: return run_plan<T, 256>(pr, P, q, Kc, Vc, Kd, Vd, lens, out, lse, ws, st);
+    case 16: return run_plan<T, 16>(pr, P, q, Kc, Vc, Kd, Vd, lens, out, lse, ws, st, ap);
+    case 32: return run_plan<T, 32>(pr, P, q, Kc, Vc, Kd, Vd, lens, out, lse, ws, st, ap);
+    case 64: return run_plan<T, 64>(pr, P, q, Kc, Vc, Kd, Vd, lens, out, lse, ws, st, ap);
+    case 128: return run_plan<T, 128>(pr, P, q, Kc, Vc, Kd, Vd, lens, out, lse, ws, st, ap);
+    case 256: return run_plan<T, 256>(pr, P, q, Kc, Vc, Kd, Vd, lens, out, lse, ws, st, ap);
   }
   return BA_EINVAL;
 }
@@ -762,6 +817,32 @@ int bifurcated_attn_decode(const ba_problem_t* prob, const void* q, const void* 
   if (P.bf16)
     return run_d<__nv_bfloat16>(&E, P, q, Kc, Vc, Kd, Vd, lens, out, lse, workspace, st);
   return run_d<float>(&E, P, q, Kc, Vc, Kd, Vd, lens, out, lse, workspace, st);
+}
+
+int bifurcated_attn_decode_append(const ba_problem_t* prob, const void* q, const void* k_new,
+                                  const void* v_new, const void* Kc, const void* Vc, void* Kd,
+                                  void* Vd, int32_t* lens, void* out, float* lse,
+                                  void* workspace, size_t workspace_bytes, void* stream) {
+  int rc = validate(prob);
+  if (rc) return rc;
+  if (prob->md_cap < 1) return BA_EINVAL;
+  DevInfo di;
+  rc = device_info(&di);
+  if (rc) return rc;
+  const Plan* PP;
+  rc = cached_plan(prob, di.sms, false, &PP);
+  if (rc) return rc;
+  const Plan P = *PP;
+  const void* ptrs[] = {q, Kc, Vc, Kd, Vd, out, lens, k_new, v_new};
+  rc = common_checks(prob, ptrs, 9, workspace, workspace_bytes, ba_workspace_bytes(prob));
+  if (rc) return rc;
+  if (lse && (reinterpret_cast<uintptr_t>(lse) & 3u)) return BA_EALIGN;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const ba_problem_t E = effective(prob);
+  const AppendArgs ap{k_new, v_new, lens, ntok_of(prob)};
+  if (P.bf16)
+    return run_d<__nv_bfloat16>(&E, P, q, Kc, Vc, Kd, Vd, lens, out, lse, workspace, st, &ap);
+  return run_d<float>(&E, P, q, Kc, Vc, Kd, Vd, lens, out, lse, workspace, st, &ap);
 }
 
 int replicated_attn_decode(const ba_problem_t* prob, const void* q, const void* K,

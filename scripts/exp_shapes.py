@@ -10,6 +10,8 @@ from synth import CONFIGS, make_inputs, alg_bytes
 base = CONFIGS[os.environ.get("EXP_CFG", "mha7b_b32")]
 shapes = [tuple(int(v) for v in a.split(",")) for a in sys.argv[1:]] or [(128, 256), (128, 512), (128, 1024), (128, 2048), (8192, 0), (16384, 0)]
 for mc, md in shapes:
+    if (mc, md) == (0, 0):  # the config's own shape
+        mc, md = base.mc, base.md
     cfg = base.with_(mc=mc, md=md)
     sets = [make_inputs(cfg, 1 + k, device="cuda") for k in range(2)]
     outs = [torch.empty_like(s.q) for s in sets]

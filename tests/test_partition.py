@@ -15,7 +15,12 @@ import paper_2403_08845_b200 as ba
 from paper_2403_08845_b200 import _build
 
 
-DEC_COST = 1.25
+def dec_cost(N, nrc, g, mc, ntc, G, T):
+    """The planner's decode-tile weight (bifattn_api.cu, make_plan)."""
+    dc = 1.7 if N == 16 else 1.25
+    if nrc > 1 and (2 * g * mc * 128 * 2 <= 64 * 2 ** 20 or 1.5 * ntc * G >= T):
+        dc *= 2.4 if nrc >= 32 else 1.6
+    return dc
 
 
 def owner(cs, f):
@@ -103,6 +108,7 @@ def model(b, h, g, mc, md, cs, bw):
         else:
             sd = max(sd, parts)
     # planner cost: decode tiles weigh DEC_COST (bifattn_api.cu, plan_split)
+    DEC_COST = dec_cost(N, nrc, g, mc, ntc, G, T)
     loads = [(min(cs[k + 1], Tc) - min(cs[k], Tc)) + DEC_COST * (max(cs[k + 1], Tc) - max(cs[k], Tc))
              for k in range(G)]
     return N, sc, sd, loads, banded
