@@ -123,6 +123,26 @@ int bifurcated_attn_decode(const ba_problem_t* prob, const void* q, const void* 
                            const int32_t* lens, void* out, float* lse, void* workspace,
                            size_t workspace_bytes, void* stream);
 
+/* KV append + attention of one decode step in one call (
+ * the per-step "+K_prev / +V_prev" cache write of PAPER.md Table 5 :982-987,
+ * SPEC.md:214-222).  With n = max(prob->n_tok, 1):
+ *   1. writes k_new, v_new [b][g][n][d] (this step's keys/values of the n
+ *      query tokens) into Kd, Vd at positions lens[i] .. lens[i] + n - 1
+ *      (lens clamped to [0, md_cap]; rows at positions >= md_cap are dropped);
+ *   2. runs the bifurcated step exactly as bifurcated_attn_decode with the
+ *      valid decode length min(lens[i] + n, md_cap) (the appended tokens see
+ *      themselves — reading R3 — and the multi-token causal bound applies);
+ *   3. stores lens[i] <- min(lens[i] + n, md_cap) on the device after every
+ *      read of lens, so the next step's call (or a CUDA-graph replay) needs
+ *      no host work.
+ * Two launches (append kernel, then the attention kernels chained by
+ * programmatic dependent launch).  Kd, Vd and lens are modified; k_new/v_new
+ * 16-byte aligned; md_cap >= 1.  Errors as bifurcated_attn_decode. */
+int bifurcated_attn_decode_append(const ba_problem_t* prob, const void* q, const void* k_new,
+                                  const void* v_new, const void* Kc, const void* Vc, void* Kd,
+                                  void* Vd, int32_t* lens, void* out, float* lse,
+                                  void* workspace, size_t workspace_bytes, void* stream);
+
 /* The same step with HOST inputs and outputs (end-to-end entry point): copies
  * q, Kc, Vc, Kd, Vd, lens from host memory (pinned for async behaviour) into
  * the caller-owned device buffers dq..dlens, runs bifurcated_attn_decode, and

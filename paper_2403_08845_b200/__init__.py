@@ -30,6 +30,7 @@ ERRORS = {0: "BA_OK", -1: "BA_EINVAL", -2: "BA_ENULL", -3: "BA_EALIGN", -4: "BA_
           -5: "BA_EDTYPE", -6: "BA_ENODEV", -7: "BA_ECUDA"}
 
 EXPORTED = ["ba_workspace_bytes", "bifurcated_attn_decode", "bifurcated_attn_decode_host",
+            "bifurcated_attn_decode_append",
             "replicated_attn_decode", "ba_launches_per_call", "ba_plan_string", "ba_strerror",
             "ba_last_cuda_error", "ba_version", "ba_launch_name", "ba_set_launch_events",
             "ba_set_trace_buffer", "ba_plan_ctas"]
@@ -63,6 +64,8 @@ def load_library(path: str = LIB_PATH):
     lib.bifurcated_attn_decode.restype = ctypes.c_int
     lib.bifurcated_attn_decode_host.argtypes = [pp] + [P] * 17 + [ctypes.c_size_t, P]
     lib.bifurcated_attn_decode_host.restype = ctypes.c_int
+    lib.bifurcated_attn_decode_append.argtypes = [pp] + [P] * 11 + [ctypes.c_size_t, P]
+    lib.bifurcated_attn_decode_append.restype = ctypes.c_int
     lib.replicated_attn_decode.argtypes = [pp] + [P] * 7 + [ctypes.c_size_t, P]
     lib.replicated_attn_decode.restype = ctypes.c_int
     lib.ba_launches_per_call.argtypes = [pp]
@@ -267,6 +270,36 @@ def bifurcated_attn_decode(q, Kc, Vc, Kd, Vd, lens, out=None, lse=None, *, scale
                                     workspace.data_ptr(), workspace.numel(), st)
     if rc != 0:
         raise BifAttnError(rc, "bifurcated_attn_decode")
+    return out
+
+
+def bifurcated_attn_decode_append(q, k_new, v_new, Kc, Vc, Kd, Vd, lens, out=None, lse=None, *,
+                                  scale=None, workspace=None, stream=None, flags=0):
+    """KV append + bifurcated decode step in one call (include/bifattn.h):
+    writes k_new/v_new [b,g,n,d] into Kd/Vd at lens[i].., attends with
+    lens + n, and advances ``lens`` (device int32) in place.  q [b,h,d]
+    (n = 1) or [b,h,n,d]."""
+    lib = _lib if _lib is not None else load_library()
+    _fast_check((q, Kc, Vc, Kd, Vd, lens), q.dtype, q.device)
+    _check(dict(k_new=k_new, v_new=v_new), q.dtype, q.device)
+    if lens.dtype != torch.int32:
+        raise ValueError("lens must be int32")
+    prob = _cached_problem(q, Kc, Kd, scale, flags)
+    n = max(prob.n_tok, 1)
+    exp = (Kd.shape[0], Kd.shape[1], n, Kd.shape[3])
+    if tuple(k_new.shape) != exp or tuple(v_new.shape) != exp:
+        raise ValueError(f"k_new/v_new must be {exp}")
+    if out is None:
+        out = torch.empty_like(q)
+    if workspace is None:
+        workspace = alloc_workspace(prob, q.device)
+    st = (stream if stream is not None else torch.cuda.current_stream()).cuda_stream
+    rc = lib.bifurcated_attn_decode_append(
+        ctypes.byref(prob), q.data_ptr(), k_new.data_ptr(), v_new.data_ptr(), Kc.data_ptr(),
+        Vc.data_ptr(), Kd.data_ptr(), Vd.data_ptr(), lens.data_ptr(), out.data_ptr(),
+        lse.data_ptr() if lse is not None else None, workspace.data_ptr(), workspace.numel(), st)
+    if rc != 0:
+        raise BifAttnError(rc, "bifurcated_attn_decode_append")
     return out
 
 

@@ -68,6 +68,9 @@ struct BifTcParams {
   const int32_t* lens;
   int b, h, g, p, mc;
   int dec_cap, lens_offset;  // decode length = lens_offset + clamp(lens[i], 0, dec_cap)
+  int lens_add;              // append+attend: lens[i] counts the cache BEFORE this step's n
+                             // appended rows; the step sees min(lens[i] + lens_add, dec_cap)
+  int32_t* lens_out;         // append+attend: lens updated in place after the step (or null)
   int ntok;                  // tokens per head (multi-token step): in-group row k sees decode
                              // positions < max(L - (ntok - 1 - k % ntok), lens_offset)
   int N;                     // rows per chunk (== template N)
@@ -149,6 +152,7 @@ struct Seg {
 BA_DEVINL int dec_len(const BifTcParams& P, int i) {
   int L = P.lens[i];
   L = L < 0 ? 0 : (L > P.dec_cap ? P.dec_cap : L);
+  L = min(L + P.lens_add, P.dec_cap);
   return P.lens_offset + L;
 }
 
@@ -1243,6 +1247,9 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
   }
   __syncthreads();
   if (threadIdx.x == 0) tstamp(252, 52);
+  // append+attend: every CTA has read lens (before the barrier); advance it
+  if (P.lens_out && blockIdx.x == 0)
+    for (int i = threadIdx.x; i < P.b; i += blockDim.x) P.lens_out[i] = dec_len(P, i) - P.lens_offset;
   for (int gr = my_gr; gr < r1; gr += nwarps) {
     if (gr != my_gr) {
       const int i = gr / P.h, j = gr - i * P.h;

@@ -35,6 +35,7 @@ struct FmaParams {
   int dec_stride;   // position stride of Kd/Vd (md_cap, or mc+md_cap for the replicated baseline)
   int dec_cap;      // clamp for lens[i]
   int lens_offset;  // decode valid length = lens_offset + clamp(lens[i], 0, dec_cap)
+  int lens_add;     // append+attend: valid decode length min(lens[i] + lens_add, dec_cap)
   int ntok;         // tokens per head (multi-token step): token k of a row group sees
                     // decode positions < max(L - (ntok - 1 - k), lens_offset)
   float scale_log2; // scale * log2(e)
@@ -137,6 +138,7 @@ __global__ void __launch_bounds__(128) fma_partial_kernel(const FmaParams P) {
     const int i = ic / P.g;
     int L = P.lens[i];
     L = L < 0 ? 0 : (L > P.dec_cap ? P.dec_cap : L);
+    L = min(L + P.lens_add, P.dec_cap);
     L += P.lens_offset;
     dec_L = L;
     dec_r0 = i * P.p;

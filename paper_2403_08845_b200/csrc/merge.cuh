@@ -23,6 +23,8 @@ struct MergeParams {
   int dec_slot0, nsd;
   void* out;           // [rows][D] in T
   float* lse;          // [rows] or null
+  int32_t* lens_out;   // append+attend: lens[i] <- min(clamp(lens[i]) + lens_add, dec_cap)
+  int b, lens_add, dec_cap;
 };
 
 // Number of context partials written for output row gr.
@@ -36,6 +38,13 @@ __global__ void __launch_bounds__(256) merge_kernel(const MergeParams P) {
   constexpr int EPL = (D + 31) / 32;
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
+  // append+attend: the partial kernels (earlier launches) have read lens
+  if (P.lens_out && blockIdx.x == 0)
+    for (int i = threadIdx.x; i < P.b; i += blockDim.x) {
+      int L = P.lens_out[i];
+      L = L < 0 ? 0 : (L > P.dec_cap ? P.dec_cap : L);
+      P.lens_out[i] = min(L + P.lens_add, P.dec_cap);
+    }
   if (warp >= P.rows) return;
   const int nctx = ctx_slots_of_row(P, warp);
   const int ntot = nctx + P.nsd;

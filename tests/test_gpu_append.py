@@ -1,0 +1,100 @@
+"""GPU parity of append + attend (include/bifattn.h
+bifurcated_attn_decode_append) through the C ABI.  The reference is the
+definition of the step: write k_new/v_new into the host copy of the decode
+cache at lens[i].. (Table 5 "+K_prev" rows, :982-987), advance lens by
+n, then the fp64 oracle.  Checked: the output and lse element by element, the
+device caches bit-exactly, lens advanced on the device, a sequence of steps
+driven only by the device-side lens (CUDA-graph replays), and both kernel
+families."""
+import pytest
+import torch
+
+import paper_2403_08845_b200 as ba
+from synth import Config, make_inputs
+from tests.parity import compare, oracle_rows
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda:0"
+
+
+def host_append(inp, k_new, v_new, n):
+    Kd, Vd, lens = inp.Kd.clone(), inp.Vd.clone(), inp.lens.clone()
+    cap = Kd.shape[2]
+    for i in range(Kd.shape[0]):
+        L = max(0, min(int(lens[i]), cap))
+        for k in range(n):
+            if L + k < cap:
+                Kd[i, :, L + k] = k_new[i, :, k]
+                Vd[i, :, L + k] = v_new[i, :, k]
+        lens[i] = min(L + n, cap)
+    return type(inp)(inp.q, inp.Kc, inp.Vc, Kd, Vd, lens, inp.scale)
+
+
+CASES = [
+    (Config("ap_mha", "bf16", b=16, h=8, g=8, d=128, mc=900, md=70), 1),
+    (Config("ap_gqa_n3", "bf16", b=6, h=16, g=4, d=128, mc=400, md=50), 3),
+    (Config("ap_fp32", "fp32", b=4, h=4, g=2, d=64, mc=100, md=20), 2),
+]
+
+
+@pytest.mark.parametrize("case", CASES, ids=lambda c: c[0].name)
+@pytest.mark.parametrize("flags", [0, ba.BA_FLAG_FORCE_FMA], ids=["auto", "fma"])
+def test_append_then_attend(case, flags):
+    cfg, n = case
+    inp = make_inputs(cfg, 41, variant="ragged", n_tok=n)
+    inp.lens[0] = cfg.md          # full cache: the appended rows are dropped
+    inp.lens[1] = cfg.md - 1      # partly dropped when n > 1
+    g = torch.Generator().manual_seed(5)
+    k_new = torch.randn(cfg.b, cfg.g, n, cfg.d, generator=g).to(cfg.torch_dtype)
+    v_new = torch.randn(cfg.b, cfg.g, n, cfg.d, generator=g).to(cfg.torch_dtype)
+    Kd, Vd, lens = inp.Kd.to(DEV), inp.Vd.to(DEV), inp.lens.to(DEV)
+    q = inp.q.to(DEV)
+    lse = torch.empty(q.shape[:-1], dtype=torch.float32, device=DEV)
+    out = ba.bifurcated_attn_decode_append(q, k_new.to(DEV), v_new.to(DEV), inp.Kc.to(DEV),
+                                           inp.Vc.to(DEV), Kd, Vd, lens, lse=lse,
+                                           scale=inp.scale, flags=flags)
+    torch.cuda.synchronize()
+    ref_inp = host_append(inp, k_new, v_new, n)
+    assert torch.equal(lens.cpu(), ref_inp.lens)
+    assert torch.equal(Kd.cpu(), ref_inp.Kd) and torch.equal(Vd.cpu(), ref_inp.Vd)
+    ref, ref_lse = oracle_rows(ref_inp)
+    compare(out, lse, ref, ref_lse, cfg.torch_dtype, f"append/{cfg.name}")
+
+
+def test_append_steps_in_a_cuda_graph():
+    """Four decode steps replayed from one captured graph: the device-side lens
+    advance drives the cache position; each step is checked."""
+    cfg = Config("x", "bf16", b=8, h=4, g=4, d=128, mc=500, md=40)
+    inp = make_inputs(cfg, 43, lens=[3, 0, 10, 37, 38, 39, 1, 20])
+    q, Kc, Vc = inp.q.to(DEV), inp.Kc.to(DEV), inp.Vc.to(DEV)
+    Kd, Vd, lens = inp.Kd.to(DEV), inp.Vd.to(DEV), inp.lens.to(DEV)
+    k_new = torch.empty(cfg.b, cfg.g, 1, cfg.d, dtype=torch.bfloat16, device=DEV)
+    v_new = torch.empty_like(k_new)
+    out = torch.empty_like(q)
+    prob = ba.make_problem(cfg.b, cfg.h, cfg.g, cfg.d, cfg.mc, cfg.md, q.dtype, inp.scale)
+    ws = ba.alloc_workspace(prob, DEV)
+    s = torch.cuda.Stream()
+    step = lambda: ba.bifurcated_attn_decode_append(q, k_new, v_new, Kc, Vc, Kd, Vd, lens, out,
+                                                    workspace=ws, scale=inp.scale, stream=s)
+    # capture on copies so that the capture itself does not advance the real state
+    snap = (Kd.clone(), Vd.clone(), lens.clone())
+    with torch.cuda.stream(s):
+        step()
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=s):
+        step()
+    Kd.copy_(snap[0]); Vd.copy_(snap[1]); lens.copy_(snap[2])
+    torch.cuda.synchronize()
+    host = inp
+    gen = torch.Generator().manual_seed(6)
+    for it in range(4):
+        kn = torch.randn(cfg.b, cfg.g, 1, cfg.d, generator=gen).to(torch.bfloat16)
+        vn = torch.randn(cfg.b, cfg.g, 1, cfg.d, generator=gen).to(torch.bfloat16)
+        k_new.copy_(kn); v_new.copy_(vn)
+        graph.replay()
+        torch.cuda.synchronize()
+        host = host_append(host, kn, vn, 1)
+        assert torch.equal(lens.cpu(), host.lens), it
+        ref, _ = oracle_rows(host)
+        compare(out, None, ref, None, cfg.torch_dtype, f"graph-step{it}")
