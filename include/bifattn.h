@@ -165,6 +165,21 @@ int replicated_attn_decode(const ba_problem_t* prob, const void* q, const void* 
                            const void* V, const int32_t* lens, void* out, float* lse,
                            void* workspace, size_t workspace_bytes, void* stream);
 
+/* Log-sum-exp join of partial results (the cross-GPU
+ * context split): out_parts [n_parts][rows][d] (dtype) and lse_parts float32
+ * [n_parts][rows] are n_parts results of the SAME rows, each the attention of
+ * a row over a disjoint slice of its keys (e.g. rank r's slice of the
+ * context, one rank also holding the decode part), with their natural-log
+ * LSE as written by bifurcated_attn_decode.  Writes the attention over the
+ * union of the slices (Eq. 4 "+", applied across slices):
+ *   M = max_k lse_k;  out = sum_k e^(lse_k - M) out_k / sum_k e^(lse_k - M);
+ *   lse = M + ln sum_k e^(lse_k - M)   (lse nullable).
+ * A part with lse = -inf contributes nothing.  Device pointers; d <= 256;
+ * one launch on `stream`.  The parts are rounded to the dtype before the
+ * join (bf16: one extra rounding per part). */
+int ba_lse_merge(int n_parts, int rows, int d, int dtype, const void* out_parts,
+                 const float* lse_parts, void* out, float* lse, void* stream);
+
 /* Number of kernel launches one bifurcated_attn_decode() call makes for this
  * problem on the current device (for the benchmark's launch count): 1 for the
  * tensor-core plan (one cooperative launch), 3 for the CUDA-core plan. */

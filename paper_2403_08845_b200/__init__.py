@@ -30,7 +30,7 @@ ERRORS = {0: "BA_OK", -1: "BA_EINVAL", -2: "BA_ENULL", -3: "BA_EALIGN", -4: "BA_
           -5: "BA_EDTYPE", -6: "BA_ENODEV", -7: "BA_ECUDA"}
 
 EXPORTED = ["ba_workspace_bytes", "bifurcated_attn_decode", "bifurcated_attn_decode_host",
-            "bifurcated_attn_decode_append",
+            "bifurcated_attn_decode_append", "ba_lse_merge",
             "replicated_attn_decode", "ba_launches_per_call", "ba_plan_string", "ba_strerror",
             "ba_last_cuda_error", "ba_version", "ba_launch_name", "ba_set_launch_events",
             "ba_set_trace_buffer", "ba_plan_ctas"]
@@ -66,6 +66,8 @@ def load_library(path: str = LIB_PATH):
     lib.bifurcated_attn_decode_host.restype = ctypes.c_int
     lib.bifurcated_attn_decode_append.argtypes = [pp] + [P] * 11 + [ctypes.c_size_t, P]
     lib.bifurcated_attn_decode_append.restype = ctypes.c_int
+    lib.ba_lse_merge.argtypes = [ctypes.c_int] * 4 + [P] * 5
+    lib.ba_lse_merge.restype = ctypes.c_int
     lib.replicated_attn_decode.argtypes = [pp] + [P] * 7 + [ctypes.c_size_t, P]
     lib.replicated_attn_decode.restype = ctypes.c_int
     lib.ba_launches_per_call.argtypes = [pp]
@@ -300,6 +302,27 @@ def bifurcated_attn_decode_append(q, k_new, v_new, Kc, Vc, Kd, Vd, lens, out=Non
         lse.data_ptr() if lse is not None else None, workspace.data_ptr(), workspace.numel(), st)
     if rc != 0:
         raise BifAttnError(rc, "bifurcated_attn_decode_append")
+    return out
+
+
+def lse_merge(out_parts, lse_parts, out=None, lse=None, *, stream=None):
+    """Join partial results over disjoint key slices (include/bifattn.h
+    ba_lse_merge): out_parts [n, ...rows..., d], lse_parts [n, ...rows...]."""
+    lib = _lib if _lib is not None else load_library()
+    n, d = out_parts.shape[0], out_parts.shape[-1]
+    rows = out_parts[0].numel() // d
+    _check(dict(out_parts=out_parts), out_parts.dtype, out_parts.device)
+    if lse_parts.dtype != torch.float32 or not lse_parts.is_contiguous() or \
+            lse_parts.numel() != n * rows:
+        raise ValueError("lse_parts must be contiguous float32 [n, rows]")
+    if out is None:
+        out = torch.empty(out_parts.shape[1:], dtype=out_parts.dtype, device=out_parts.device)
+    dt = {torch.bfloat16: BA_BF16, torch.float32: BA_FP32}[out_parts.dtype]
+    rc = lib.ba_lse_merge(n, rows, d, dt, out_parts.data_ptr(), lse_parts.data_ptr(),
+                          out.data_ptr(), lse.data_ptr() if lse is not None else None,
+                          _stream_handle(stream))
+    if rc != 0:
+        raise BifAttnError(rc, "ba_lse_merge")
     return out
 
 

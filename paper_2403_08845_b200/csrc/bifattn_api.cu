@@ -23,6 +23,7 @@
 #include "fma_partial.cuh"
 #include "merge.cuh"
 #include "append.cuh"
+#include "lse_merge.cuh"
 
 namespace {
 
@@ -912,6 +913,30 @@ int bifurcated_attn_decode_host(const ba_problem_t* prob, const void* hq, const 
     if ((rc = cp(hlse, dlse, (size_t)prob->b * prob->h * ntok_of(prob) * sizeof(float),
                   cudaMemcpyDeviceToHost)))
       return rc;
+  }
+  return BA_OK;
+}
+
+int ba_lse_merge(int n_parts, int rows, int d, int dtype, const void* out_parts,
+                 const float* lse_parts, void* out, float* lse, void* stream) {
+  if (n_parts < 1 || rows < 0 || d < 1 || d > 256) return BA_EINVAL;
+  if (dtype != BA_BF16 && dtype != BA_FP32) return BA_EDTYPE;
+  if (!out_parts || !lse_parts || !out) return BA_ENULL;
+  DevInfo di;
+  int rc = device_info(&di);
+  if (rc) return rc;
+  if (rows == 0) return BA_OK;
+  ba::LseMergeParams mp{out_parts, lse_parts, out, lse, n_parts, rows, d};
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int blocks = cdiv(rows, 8);
+  if (dtype == BA_BF16)
+    ba::lse_merge_kernel<__nv_bfloat16><<<blocks, 256, 0, st>>>(mp);
+  else
+    ba::lse_merge_kernel<float><<<blocks, 256, 0, st>>>(mp);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    g_last_cuda_error = (int)e;
+    return BA_ECUDA;
   }
   return BA_OK;
 }

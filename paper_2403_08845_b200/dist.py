@@ -68,3 +68,93 @@ def decode_sharded(q_local, Kc_local, Vc_local, Kd_local, Vd_local, lens, *, gat
         return out
     world = world or dist.get_world_size(group)
     return gather_heads(out, world, group)
+
+
+# ---------------------------------------------------------------------------
+# MQA / G > g: when the KV groups cannot be sharded
+# (g = 1, "the single head in K and V are duplicated across TP ranks",
+# PAPER.md:1014), split the work along the batch or along the context.
+# ---------------------------------------------------------------------------
+def batch_bounds(b: int, world: int, rank: int) -> Tuple[int, int]:
+    """Samples [i0, i1) of rank `rank` (contiguous, sizes differ by <= 1).
+    Each rank runs the whole step for its samples: the shared context is
+    read once PER GPU (still once for all of the rank's samples), the decode
+    caches are partitioned.  No collective inside attention."""
+    if world > b:
+        raise ValueError(f"batch split needs world ({world}) <= b ({b})")
+    return rank * b // world, (rank + 1) * b // world
+
+
+def shard_batch_inputs(q, Kd, Vd, lens, world: int, rank: int):
+    i0, i1 = batch_bounds(q.shape[0], world, rank)
+    return (q[i0:i1].contiguous(), Kd[i0:i1].contiguous(), Vd[i0:i1].contiguous(),
+            lens[i0:i1].contiguous())
+
+
+def gather_batch(out_local: torch.Tensor, b: int, world: int, group=None) -> torch.Tensor:
+    """All-gather per-rank outputs along the batch (uneven blocks allowed)."""
+    sizes = [batch_bounds(b, world, r)[1] - batch_bounds(b, world, r)[0] for r in range(world)]
+    mx = max(sizes)
+    pad = torch.zeros((mx,) + tuple(out_local.shape[1:]), dtype=out_local.dtype,
+                      device=out_local.device)
+    pad[: out_local.shape[0]] = out_local
+    buf = torch.empty((world,) + tuple(pad.shape), dtype=pad.dtype, device=pad.device)
+    if pad.is_cuda:
+        dist.all_gather_into_tensor(buf.view(-1), pad.view(-1), group=group)
+    else:
+        dist.all_gather(list(buf.unbind(0)), pad, group=group)
+    return torch.cat([buf[r, : sizes[r]] for r in range(world)], dim=0)
+
+
+def context_bounds(mc: int, world: int, rank: int) -> Tuple[int, int]:
+    """Context positions [t0, t1) of rank `rank` for the context split: the
+    shared context is cut into `world` contiguous slices (each >= 1
+    position); rank 0 also holds the decode caches."""
+    if world > mc:
+        raise ValueError(f"context split needs world ({world}) <= mc ({mc})")
+    return rank * mc // world, (rank + 1) * mc // world
+
+
+def split_context_inputs(Kc, Vc, Kd, Vd, lens, world: int, rank: int):
+    """Rank-local inputs of the context split: Kc/Vc[:, t0:t1]; rank 0 keeps
+    Kd/Vd and lens, the other ranks get an empty decode cache (md_cap = 0)."""
+    t0, t1 = context_bounds(Kc.shape[1], world, rank)
+    Kc_r, Vc_r = Kc[:, t0:t1].contiguous(), Vc[:, t0:t1].contiguous()
+    if rank == 0:
+        return Kc_r, Vc_r, Kd, Vd, lens
+    e = Kd[:, :, :0].contiguous()
+    return Kc_r, Vc_r, e, Vd[:, :, :0].contiguous(), torch.zeros_like(lens)
+
+
+def exchange_partials(out_local: torch.Tensor, lse_local: torch.Tensor, world: int, group=None):
+    """The one exchange of the context split: all-gather every rank's
+    normalised partial output and its LSE -> [world][...] (NCCL over NVLink)."""
+    ob = torch.empty((world,) + tuple(out_local.shape), dtype=out_local.dtype,
+                     device=out_local.device)
+    lb = torch.empty((world,) + tuple(lse_local.shape), dtype=lse_local.dtype,
+                     device=lse_local.device)
+    if out_local.is_cuda:
+        dist.all_gather_into_tensor(ob.view(-1), out_local.contiguous().view(-1), group=group)
+        dist.all_gather_into_tensor(lb.view(-1), lse_local.contiguous().view(-1), group=group)
+    else:
+        dist.all_gather(list(ob.unbind(0)), out_local.contiguous(), group=group)
+        dist.all_gather(list(lb.unbind(0)), lse_local.contiguous(), group=group)
+    return ob, lb
+
+
+def decode_context_split(q, Kc_r, Vc_r, Kd_r, Vd_r, lens_r, *, world: Optional[int] = None,
+                         group=None, scale=None, workspace=None, stream=None):
+    """Context split of one step across ranks (inputs from split_context_inputs):
+    each rank attends all rows to its context slice (+ the decode part on rank
+    0) through the C ABI, the ranks exchange (out, lse) once, and every rank
+    joins the partials with the LSE merge kernel (ba_lse_merge).  Returns the
+    full [b][h][d] output and [b][h] lse on every rank."""
+    from . import bifurcated_attn_decode, lse_merge
+
+    world = world or dist.get_world_size(group)
+    lse = torch.empty(q.shape[:-1], dtype=torch.float32, device=q.device)
+    out = bifurcated_attn_decode(q, Kc_r, Vc_r, Kd_r, Vd_r, lens_r, lse=lse, scale=scale,
+                                 workspace=workspace, stream=stream)
+    ob, lb = exchange_partials(out, lse, world, group)
+    full_lse = torch.empty_like(lse)
+    return lse_merge(ob, lb, lse=full_lse, stream=stream), full_lse

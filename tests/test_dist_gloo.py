@@ -88,3 +88,83 @@ def test_shard_bounds():
             heads += list(range(h0, h1))
         if 8 % world == 0:
             assert heads == list(range(32))
+
+
+# ---------------------------------------------------------------------------
+# batch split and context split (MQA, G > g)
+# ---------------------------------------------------------------------------
+def _worker_f3(rank, world, port, cfg_kw, seed, mode, q_out):
+    import oracle
+    from paper_2403_08845_b200.dist import (exchange_partials, gather_batch, shard_batch_inputs,
+                                            split_context_inputs)
+    from synth import Config, make_inputs
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        cfg = Config(**cfg_kw)
+        inp = make_inputs(cfg, seed, variant="ragged")
+        if mode == "batch":
+            ql, Kdl, Vdl, ll = shard_batch_inputs(inp.q, inp.Kd, inp.Vd, inp.lens, world, rank)
+            out, lse, _ = oracle.attn_decode(ql, inp.Kc, inp.Vc, Kdl, Vdl, ll, scale=inp.scale)
+            full = gather_batch(torch.from_numpy(out).reshape(ql.shape[0], cfg.h, cfg.d),
+                                cfg.b, world)
+            if rank == 0:
+                q_out.put((full.numpy(), None))
+        else:
+            Kc_r, Vc_r, Kd_r, Vd_r, l_r = split_context_inputs(inp.Kc, inp.Vc, inp.Kd, inp.Vd,
+                                                               inp.lens, world, rank)
+            out, lse, _ = oracle.attn_decode(inp.q, Kc_r, Vc_r, Kd_r, Vd_r, l_r, scale=inp.scale)
+            ob, lb = exchange_partials(torch.from_numpy(out), torch.from_numpy(lse), world)
+            if rank == 0:
+                q_out.put((ob.numpy(), lb.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("mode", ["batch", "context"])
+@pytest.mark.parametrize("world", [2, 3])
+def test_mqa_batch_and_context_split(mode, world):
+    """g = 1 cannot head-shard; the batch split (no collective) and the
+    context split (one exchange of (out, lse), then the LSE join of Eq. 4
+    across slices — here written out in numpy as the test's reference of the
+    ba_lse_merge kernel) both reproduce the unsplit oracle."""
+    import oracle
+    from synth import Config, make_inputs
+
+    cfg_kw = dict(name="mqa", dtype="bf16", b=5, h=6, g=1, d=16, mc=37, md=7)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_f3, args=(r, world, port, cfg_kw, 8, mode, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    a, b_ = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    cfg = Config(**cfg_kw)
+    inp = make_inputs(cfg, 8, variant="ragged")
+    ref, ref_lse, _ = oracle.attn_decode(inp.q, inp.Kc, inp.Vc, inp.Kd, inp.Vd, inp.lens,
+                                         scale=inp.scale)
+    if mode == "batch":
+        np.testing.assert_array_equal(a.reshape(-1, cfg.d), ref)
+        return
+    M = b_.max(axis=0)
+    w = np.exp(b_ - M)                          # [world][rows]
+    out = (w[..., None] * a).sum(0) / w.sum(0)[..., None]
+    np.testing.assert_allclose(out, ref, rtol=0, atol=1e-13)
+    np.testing.assert_allclose(M + np.log(w.sum(0)), ref_lse, rtol=0, atol=1e-12)
+
+
+def test_split_bounds():
+    from paper_2403_08845_b200.dist import batch_bounds, context_bounds
+    for world in (1, 2, 3, 8):
+        assert [i for r in range(world) for i in range(*batch_bounds(128, world, r))] == \
+            list(range(128))
+        assert [t for r in range(world) for t in range(*context_bounds(8192, world, r))] == \
+            list(range(8192))
+    with pytest.raises(ValueError):
+        context_bounds(3, 4, 0)
