@@ -217,7 +217,20 @@ __host__ __device__ inline long long ctx_unit(int nrc, int ntc, int bw, long lon
 BA_DEVINL Seg seg_at(const BifTcParams& P, const Range& rg, long long w) {
   Seg s;
   const long long f = rg.f0 + w;
-  if (f < P.Tc) {
+  if (f < P.Tc && P.nband <= 1) {
+    // one band: chunk (c, rc) = f / ntile_c (the common case, fewer divisions)
+    const long long seg = f / P.ntile_c;
+    const long long fend = min((seg + 1) * P.ntile_c, rg.f1);
+    s.dec = false;
+    s.c = (int)(seg / P.nrc);
+    s.rc = (int)(seg - (long long)s.c * P.nrc);
+    s.i = s.cb = 0;
+    s.t0 = (int)(f - seg * P.ntile_c);
+    s.c0 = s.c;
+    s.ntiles = (int)(fend - f);
+    s.slot = (int)blockIdx.x - owner(P.cs, P.G, seg * P.ntile_c);
+    s.next = w + (fend - f);
+  } else if (f < P.Tc) {
     int c, band, rc, tg, wb;
     const long long u0 = ctx_unit(P.nrc, P.ntile_c, P.bw, f, c, band, rc, tg, wb);
     const long long fend = min(u0 + wb, rg.f1);
@@ -472,7 +485,10 @@ struct Prof {
 #define BIF_DBG 0
 #endif
 
-template <int N, int SWG>
+// MT: multi-token step (P.ntok > 1) — the decode paths carry the per-column
+// intra-step causal bound; compiled out of the single-token kernel (it cost
+// ~1.5 us per C2b step in registers and issue slots).
+template <int N, int SWG, bool MT>
 __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
     bif_tc_kernel(const __grid_constant__ BifTcParams P) {
   using namespace bif;
@@ -800,7 +816,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
             for (int k = 0; k < kNarrowP; ++k) {
               if (k < P.p) {
                 // multi-token step: the intra-step causal bound of token k % ntok
-                const int Lk = P.ntok > 1 ? max(L - (P.ntok - 1 - k % P.ntok), P.lens_offset) : L;
+                const int Lk = MT ? max(L - (P.ntok - 1 - k % P.ntok), P.lens_offset) : L;
                 xv[k] = tpos < Lk ? xv[k] * sl2 : kNegInf;
                 float v = xv[k];
 #pragma unroll
@@ -989,7 +1005,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
             for (int n = 0; n < CPT; ++n) {
               const int col = col0 + n;
               bool vc = vpos && col >= cv0 && col < cv1;
-              if (s.dec && P.ntok > 1)  // intra-step causal bound of the column's token
+              if (MT && s.dec)  // intra-step causal bound of the column's token
                 vc = vc && tpos < max(L - (P.ntok - 1 - (col - cv0) % P.ntok), P.lens_offset);
               const float mref = (mr[n] == kNegInf) ? 0.f : mr[n];
               x[n] = vc ? fmaf(x[n], sl2, -mref) : kNegInf;

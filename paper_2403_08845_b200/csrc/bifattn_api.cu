@@ -537,12 +537,12 @@ int make_tmap_3d(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uin
   return BA_OK;
 }
 
-template <int N, int SWG>
+template <int N, int SWG, bool MT>
 int launch_bif_tc_n(const ba::BifTcParams& bp, int smem, uint32_t flags, LaunchRec& rec) {
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [&] {
-    attr_err = cudaFuncSetAttribute(ba::bif_tc_kernel<N, SWG>,
+    attr_err = cudaFuncSetAttribute(ba::bif_tc_kernel<N, SWG, MT>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
   });
   if (attr_err != cudaSuccess) {
@@ -569,7 +569,7 @@ int launch_bif_tc_n(const ba::BifTcParams& bp, int smem, uint32_t flags, LaunchR
   cfg.attrs = attr;
   cfg.numAttrs = 2;
   rec.begin();
-  cudaError_t e = cudaLaunchKernelEx(&cfg, ba::bif_tc_kernel<N, SWG>, bp);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, ba::bif_tc_kernel<N, SWG, MT>, bp);
   if (e != cudaSuccess) {
     g_last_cuda_error = (int)e;
     rec.end();
@@ -649,14 +649,23 @@ int run_tc(const ba_problem_t* pr, const Plan& P, const void* q, const void* Kc,
     return e ? atoi(e) : 0;
   }();
   const int swg = (swg_env == 1 || swg_env == 2 || (swg_env == 4 && P.tc_N == 32)) ? swg_env : ba::bif::softmax_wgs(P.tc_N);
+  if (P.ntok > 1) {  // multi-token kernels (MT): the default warpgroup split only
+    switch (P.tc_N) {
+      case 16: return launch_bif_tc_n<16, 2, true>(bp, P.tc_smem, pr->flags, rec);
+      case 32: return launch_bif_tc_n<32, 2, true>(bp, P.tc_smem, pr->flags, rec);
+      case 48: return launch_bif_tc_n<48, 2, true>(bp, P.tc_smem, pr->flags, rec);
+      case 64: return launch_bif_tc_n<64, 2, true>(bp, P.tc_smem, pr->flags, rec);
+    }
+    return BA_EINVAL;
+  }
   switch (P.tc_N * 4 + swg) {
-    case 16 * 4 + 1: return launch_bif_tc_n<16, 1>(bp, P.tc_smem, pr->flags, rec);
-    case 16 * 4 + 2: return launch_bif_tc_n<16, 2>(bp, P.tc_smem, pr->flags, rec);
-    case 32 * 4 + 1: return launch_bif_tc_n<32, 1>(bp, P.tc_smem, pr->flags, rec);
-    case 32 * 4 + 2: return launch_bif_tc_n<32, 2>(bp, P.tc_smem, pr->flags, rec);
-    case 32 * 4 + 4: return launch_bif_tc_n<32, 4>(bp, P.tc_smem, pr->flags, rec);
-    case 48 * 4 + 2: return launch_bif_tc_n<48, 2>(bp, P.tc_smem, pr->flags, rec);
-    case 64 * 4 + 2: return launch_bif_tc_n<64, 2>(bp, P.tc_smem, pr->flags, rec);
+    case 16 * 4 + 1: return launch_bif_tc_n<16, 1, false>(bp, P.tc_smem, pr->flags, rec);
+    case 16 * 4 + 2: return launch_bif_tc_n<16, 2, false>(bp, P.tc_smem, pr->flags, rec);
+    case 32 * 4 + 1: return launch_bif_tc_n<32, 1, false>(bp, P.tc_smem, pr->flags, rec);
+    case 32 * 4 + 2: return launch_bif_tc_n<32, 2, false>(bp, P.tc_smem, pr->flags, rec);
+    case 32 * 4 + 4: return launch_bif_tc_n<32, 4, false>(bp, P.tc_smem, pr->flags, rec);
+    case 48 * 4 + 2: return launch_bif_tc_n<48, 2, false>(bp, P.tc_smem, pr->flags, rec);
+    case 64 * 4 + 2: return launch_bif_tc_n<64, 2, false>(bp, P.tc_smem, pr->flags, rec);
   }
   return BA_EINVAL;
 }
