@@ -76,6 +76,8 @@ struct BifTcParams {
   int N;                     // rows per chunk (== template N)
   int nrc, ntile_c, ntile_d;
   int bw, nband;             // context band width (tiles) and bands per group (see seg_at)
+  int ext_ctx;               // > 0: the context branch ran in ctx_rows_kernel (ctx_rows.cuh),
+                             // which wrote ext_ctx context partials per row (slots [0, ext_ctx))
   int spc;                   // samples per context row chunk = N / p
   int gpc, ndc;              // groups per decode chunk = N / p; decode chunks per sample
   int qd_rows;               // rows of the decode q box = min(N, h)
@@ -290,6 +292,7 @@ BA_DEVINL void tile_at(const BifTcParams& P, const Range& rg, long long w, bool&
 
 // Partials written for context chunk (c, rc) / decode chunk (i, cb).
 __host__ __device__ inline int ctx_parts(const BifTcParams& P, int c, int rc) {
+  if (P.ext_ctx > 0) return P.ext_ctx;
   if (P.Tc == 0) return 0;
   if (P.nband > 1) return P.nband;  // one partial per band (units are never split)
   const long long ff = ((long long)c * P.nrc + rc) * P.ntile_c;

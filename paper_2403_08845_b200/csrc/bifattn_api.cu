@@ -24,6 +24,7 @@
 #include "merge.cuh"
 #include "append.cuh"
 #include "lse_merge.cuh"
+#include "ctx_rows.cuh"
 
 namespace {
 
@@ -103,6 +104,9 @@ struct Plan {
   int tc_N = 0, tc_nrc = 0, tc_ntile_c = 0, tc_ntile_d = 0, tc_G = 0, tc_nst = 0, tc_npb = 1;
   int tc_Sc = 0, tc_Sd = 0, tc_smem = 0;
   int tc_bw = 0, tc_nband = 0;  // context band width (tiles), bands per group
+  // rows-on-M context kernel (ctx_rows.cuh) for R = b*p >= 128 rows per group
+  bool ctx_rows = false;
+  int cr_nrb = 0, cr_ntile = 0, cr_tps = 0, cr_nsplit = 0, cr_items = 0, cr_grid = 0;
   long long tc_Tc = 0, tc_T = 0;
   int tc_cs[ba::bif_max_ctas + 1];
   size_t off_cnt = 0;
@@ -250,6 +254,41 @@ int make_plan(const ba_problem_t* pr_in, int sms, bool replicated, Plan* pl) {
     }();
     if (n_env && n_env % p == 0 && (n_env == 16 || n_env == 32 || n_env == 48 || n_env == 64)) tcN = n_env;
   }
+  static const int ctx_rows_env = [] {  // BIFATTN_CTX_ROWS=0 disables the rows-on-M kernel
+    const char* e = getenv("BIFATTN_CTX_ROWS");
+    return e ? atoi(e) : 1;
+  }();
+  // Rows-on-M context kernel when the swap-AB kernel's 32-row passes would
+  // re-read the context from HBM, or are very many (C4: 192 passes).  Where
+  // the 4-8 passes hit L2 (C3, the 4-token C2b step) the single fused launch
+  // measured faster (round 1: C3 105 vs 125 us; C5 2.7 -> 2.0 ms; C4 163 ->
+  // 127 us).
+  const double ctx_bytes_all = 2.0 * g * (double)pr->mc * pr->d * 2;
+  const int nrc32 = cdiv(R, 32);
+  const long long T32 = (long long)g * nrc32 * cdiv(pr->mc, 128) +
+                        (long long)g * pr->b * cdiv(pr->md_cap, 128);
+  const bool l2_hits32 = ctx_bytes_all <= 64.0 * (1 << 20) ||
+                         1.5 * cdiv(pr->mc, 128) * std::min(sms, ba::bif_max_ctas) >= (double)T32;
+  const bool want_rows = (pr->flags & BA_FLAG_CTX_ROWS) || ctx_rows_env == 2 || !l2_hits32 ||
+                         nrc32 >= 16;
+  if (tcN && !replicated && R >= 128 && ctx_rows_env && want_rows) {
+    // context branch on the rows-on-M kernel; the fused kernel streams only
+    // the decode tiles, so its N just has to hold p (smallest legal)
+    P.ctx_rows = true;
+    for (int N : {16, 32, 48, 64})
+      if (N % p == 0) {
+        tcN = N;
+        break;
+      }
+    P.cr_nrb = cdiv(R, 128);
+    P.cr_ntile = cdiv(pr->mc, 128);
+    int ns = cdiv(2 * sms, g * P.cr_nrb);  // ~2 items per SM
+    ns = std::max(1, std::min(ns, P.cr_ntile));
+    P.cr_tps = cdiv(P.cr_ntile, ns);
+    P.cr_nsplit = cdiv(P.cr_ntile, P.cr_tps);
+    P.cr_items = g * P.cr_nrb * P.cr_nsplit;
+    P.cr_grid = std::min(P.cr_items, sms);
+  }
   if (tcN) {
     P.tc = true;
     P.ctx_mode = replicated ? 0 : 2;
@@ -258,12 +297,13 @@ int make_plan(const ba_problem_t* pr_in, int sms, bool replicated, Plan* pl) {
     P.dec_stride = replicated ? pr->mc + pr->md_cap : pr->md_cap;
     P.dec_cap = pr->md_cap;
     P.lens_offset = replicated ? pr->mc : 0;
-    P.tc_ntile_c = replicated ? 0 : cdiv(pr->mc, 128);
+    P.tc_ntile_c = (replicated || P.ctx_rows) ? 0 : cdiv(pr->mc, 128);
     P.tc_ntile_d = cdiv(P.lens_offset + P.dec_cap, 128);
     P.tc_Tc = (long long)g * P.tc_nrc * P.tc_ntile_c;
     P.tc_T = P.tc_Tc + (long long)g * b * P.tc_ntile_d;
     const int gmax = sms < ba::bif_max_ctas ? sms : ba::bif_max_ctas;
     P.tc_G = (int)(P.tc_T < gmax ? P.tc_T : gmax);
+    if (P.tc_T == 0) P.tc_G = gmax;  // no tiles (ctx_rows, md_cap = 0): the merge only
     // P double-buffered when that keeps the K/V stage count (else one slot)
     P.tc_npb = 2;
     if ((227 * 1024 - ba::bif::smem_fixed(tcN, 2)) / ba::bif::kStageBytes <
@@ -314,7 +354,13 @@ int make_plan(const ba_problem_t* pr_in, int sms, bool replicated, Plan* pl) {
     if (l2_rereads) dec_cost *= P.tc_nrc >= 32 ? 2.4 : 1.6;
     if (dc_env > 0) dec_cost = dc_env;
     int sc = 0, sd = 0;
-    for (;;) {
+    for (; P.tc_T == 0;) {  // nothing to stream: empty ranges, merge only
+      for (int k = 0; k <= P.tc_G; ++k) P.tc_cs[k] = 0;
+      P.tc_bw = 1;
+      P.tc_nband = 0;
+      break;
+    }
+    for (; P.tc_T > 0;) {
       P.tc_bw = bw_try;
       P.tc_nband = P.tc_ntile_c ? cdiv(P.tc_ntile_c, P.tc_bw) : 0;
       const bool banded = P.tc_nband > 1;
@@ -354,6 +400,7 @@ int make_plan(const ba_problem_t* pr_in, int sms, bool replicated, Plan* pl) {
       }
       bw_try = P.tc_ntile_c;  // a unit got split (tiny problem): plain order
     }
+    if (P.ctx_rows) sc = P.cr_nsplit;  // context partials written by ctx_rows_kernel
     P.tc_Sc = sc;
     P.tc_Sd = sd;
     P.S = sc + sd;
@@ -364,7 +411,7 @@ int make_plan(const ba_problem_t* pr_in, int sms, bool replicated, Plan* pl) {
     P.off_ml = P.off_o + rows * P.S * 128 * sizeof(float);
     P.ws_bytes = P.off_ml + rows * P.S * 2 * sizeof(float);
     P.ws_bytes = (P.ws_bytes + 255) & ~(size_t)255;
-    P.launches = 1;
+    P.launches = P.ctx_rows ? 2 : 1;
     *pl = P;
     return BA_OK;
   }
@@ -629,6 +676,7 @@ int run_tc(const ba_problem_t* pr, const Plan& P, const void* q, const void* Kc,
   }();
   bp.rot = rot_env;
   memcpy(bp.cs, P.tc_cs, sizeof(int) * (P.tc_G + 1));
+  bp.ext_ctx = P.ctx_rows ? P.cr_nsplit : 0;
   bp.scale_log2 = scale_log2;
   bp.S = P.S; bp.Sc = P.tc_Sc;
   bp.ws_o = reinterpret_cast<float*>(static_cast<char*>(ws) + P.off_o);
@@ -643,6 +691,52 @@ int run_tc(const ba_problem_t* pr, const Plan& P, const void* q, const void* Kc,
   }();
   bp.dbg = dbg_skip;
   LaunchRec rec(st);
+  if (P.ctx_rows) {
+    // context branch, rows on M (ctx_rows.cuh); the fused launch below streams
+    // the decode tiles and joins these partials in its merge
+    ba::CtxRowsParams cp;
+    memset(&cp, 0, sizeof cp);
+    rc = make_tmap_3d(&cp.tmKc, Kc, d, pr->mc, pr->g, d * 2, (uint64_t)pr->mc * d * 2, 128, 1);
+    if (!rc) rc = make_tmap_3d(&cp.tmVc, Vc, d, pr->mc, pr->g, d * 2, (uint64_t)pr->mc * d * 2, 128, 1);
+    if (rc) return rc;
+    cp.q = q;
+    cp.b = pr->b; cp.h = pr->h; cp.g = pr->g; cp.p = p; cp.mc = pr->mc;
+    cp.R = pr->b * p; cp.nrb = P.cr_nrb;
+    cp.ntile = P.cr_ntile; cp.tps = P.cr_tps; cp.nsplit = P.cr_nsplit; cp.items = P.cr_items;
+    cp.scale_log2 = scale_log2;
+    cp.S = P.S;
+    cp.ws_o = bp.ws_o;
+    cp.ws_ml = bp.ws_ml;
+    static std::once_flag once;
+    static cudaError_t attr_err = cudaSuccess;
+    std::call_once(once, [&] {
+      attr_err = cudaFuncSetAttribute(ba::ctx_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      ba::ctxr::kSmem);
+    });
+    if (attr_err != cudaSuccess) {
+      g_last_cuda_error = (int)attr_err;
+      return BA_ECUDA;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(P.cr_grid);
+    cfg.blockDim = dim3(ba::ctxr::kThreads);
+    cfg.dynamicSmemBytes = ba::ctxr::kSmem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = (pr->flags & BA_FLAG_NO_PDL) ? 0 : 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    rec.begin();
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, ba::ctx_rows_kernel, cp);
+    if (e != cudaSuccess) {
+      g_last_cuda_error = (int)e;
+      rec.end();
+      return BA_ECUDA;
+    }
+    rc = rec.end();
+    if (rc) return rc;
+  }
   // softmax warpgroups (override for experiments: BIFATTN_SWG=1|2)
   static const int swg_env = [] {
     const char* e = getenv("BIFATTN_SWG");
@@ -967,7 +1061,13 @@ const char* ba_plan_string(const ba_problem_t* prob) {
     snprintf(g_plan_buf, sizeof g_plan_buf, "invalid (%d)", rc);
     return g_plan_buf;
   }
-  if (P.tc)
+  if (P.tc && P.ctx_rows)
+    snprintf(g_plan_buf, sizeof g_plan_buf,
+             "ctx_rows(blocks=%d,splits=%d,tiles/split=%d,items=%d,ctas=%d) + "
+             "dec_tc(N=%d,dec_tiles=%lld,ctas=%d,stages=%d,slots=%d+%d) launches=2 ws=%zu",
+             P.cr_nrb, P.cr_nsplit, P.cr_tps, P.cr_items, P.cr_grid, P.tc_N, P.tc_T, P.tc_G,
+             P.tc_nst, P.tc_Sc, P.tc_Sd, P.ws_bytes);
+  else if (P.tc)
     snprintf(g_plan_buf, sizeof g_plan_buf,
              "fused_tc(N=%d,nrc=%d,band=%d,ctx_tiles=%lld,dec_tiles=%lld,ctas=%d,stages=%d,pbuf=%d,"
              "slots=%d+%d,smem=%d) launches=1 ws=%zu",
@@ -988,7 +1088,10 @@ const char* ba_launch_name(const ba_problem_t* prob, int k) {
   if (make_plan(prob, sms, false, &P) != BA_OK) return nullptr;
   const char* names[4];
   int n = 0;
-  if (P.tc) {
+  if (P.tc && P.ctx_rows) {
+    names[n++] = "ctx_rows";
+    names[n++] = "dec_tc_merge";
+  } else if (P.tc) {
     names[n++] = "fused_tc";
   } else {
     if (P.ctx_mode == 1) names[n++] = "ctx_fma";

@@ -1,0 +1,314 @@
+// ctx_rows.cuh — the CONTEXT branch of the bifurcated step for wide row sets
+// (R = b*p >= 128 query rows per KV group: C3, C4, C5, multi-token steps),
+// rows on the MMA's M dimension (sm_100a tcgen05 + TMEM + TMA).
+//
+// What it computes (Eq. 3-4 context rows; "axis b does
+// not appear", :259): for a block of 128 of the R rows of group c and a range
+// of 128-position context tiles, the online-softmax partial
+//   m = running max of s*scale*log2e,  l = sum 2^(x - m),  o = sum 2^(x - m) Vc
+// written to the workspace context slot of the range; the fused kernel
+// (bif_tc.cuh) streams the decode branch and joins these partials with its
+// own in the LSE merge.  Each Kc/Vc tile is read once per 128-row block
+// (ceil(R/128) times instead of ceil(R/32) times by the swap-AB kernel).
+//
+// Tile math (rows on M):
+//   S[128 rows x 128 pos]  = Q_blk[128 x d] . K_tile^T       (A = Q, B = K, both K-major)
+//   O[128 rows x d]       += P_hi . V_tile + P_lo . V_tile   (A = P K-major, B = V MN-major)
+// One thread owns one row (TMEM lane = row): the row max, the stale-max test
+// and the O rescale are in-thread — no cross-warp vote.  P = P_hi + P_lo
+// (two bf16 parts, ~16 significant bits, reading R13) goes through shared
+// memory; both parts accumulate into the same fp32 O.
+//
+// Warps: 0 TMA producer (one lane), 1 MMA issuer (one lane), 2 TMEM
+// allocator, 3 idle, 4..7 softmax/epilogue (128 threads = 128 rows).
+#pragma once
+#include "common.cuh"
+#include "tc_ptx.cuh"
+
+namespace ba {
+
+struct CtxRowsParams {
+  CUtensorMap tmKc, tmVc;  // (d, mc, g), box (64, 128, 1), SW128
+  const void* q;           // [b][h][128] bf16 (rows of group c: (i, c*p + j))
+  int b, h, g, p, mc;
+  int R, nrb;              // rows per group, 128-row blocks per group
+  int ntile, tps, nsplit;  // context tiles, tiles per split, splits per (c, rb)
+  int items;               // g * nrb * nsplit
+  float scale_log2;
+  int S;                   // workspace slots per row (context slots [0, nsplit))
+  float* ws_o;             // [b*h][S][128]
+  float* ws_ml;            // [b*h][S][2]
+};
+
+namespace ctxr {
+constexpr int kStage = 65536;           // K tile 32 KB + V tile 32 KB
+constexpr int kNst = 2;                 // K/V stages
+constexpr int kQ = 2 * kStage;          // Q block (32 KB)
+constexpr int kP = kQ + 32768;          // P_hi (32 KB), P_lo (32 KB)
+constexpr int kBar = kP + 65536;        // barriers
+constexpr int kSmem = kBar + 256;
+constexpr float kTh = 8.0f;             // stale-max slack (log2 units), as bif_tc.cuh
+constexpr int kThreads = 256;
+
+// byte offset of 16-byte chunk `ch` (0..15) of row r in a 128-row x 128-col
+// bf16 K-major SW128 tile stored as two 64-column halves (the TMA box layout)
+BA_DEVINL uint32_t sw128_off(int r, int ch) {
+  return (uint32_t)((ch >> 3) * 16384 + r * 128 + (((ch & 7) ^ (r & 7)) << 4));
+}
+}  // namespace ctxr
+
+__global__ void __launch_bounds__(ctxr::kThreads, 1)
+    ctx_rows_kernel(const __grid_constant__ CtxRowsParams P) {
+  using namespace ctxr;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kBar);
+  uint64_t* kv_full = bars;       // [2]
+  uint64_t* kv_empty = bars + 2;  // [2]
+  uint64_t* s_full = bars + 4;    // [2]
+  uint64_t* s_free = bars + 6;    // [2]
+  uint64_t* q_full = bars + 8;
+  uint64_t* q_empty = bars + 9;
+  uint64_t* p_full = bars + 10;
+  uint64_t* p_empty = bars + 11;
+  uint64_t* o_full = bars + 12;
+  uint64_t* o_empty = bars + 13;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 14);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < 2; ++s) {
+      tc::mbar_init(tc::smem_u32(&kv_full[s]), 1);
+      tc::mbar_init(tc::smem_u32(&kv_empty[s]), 1);
+      tc::mbar_init(tc::smem_u32(&s_full[s]), 1);
+      tc::mbar_init(tc::smem_u32(&s_free[s]), 4);
+    }
+    tc::mbar_init(tc::smem_u32(q_full), 4);
+    tc::mbar_init(tc::smem_u32(q_empty), 1);
+    tc::mbar_init(tc::smem_u32(p_full), 4);
+    tc::mbar_init(tc::smem_u32(p_empty), 1);
+    tc::mbar_init(tc::smem_u32(o_full), 1);
+    tc::mbar_init(tc::smem_u32(o_empty), 4);
+    tc::fence_mbar_init();
+  }
+  if (warp == 0 && lane == 0) {
+    tc::prefetch_tmap(&P.tmKc);
+    tc::prefetch_tmap(&P.tmVc);
+  }
+  if (warp == 2) {
+    tc::tmem_alloc(tc::smem_u32(tmem_holder), 512);
+    tc::tmem_relinquish();
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  pdl_wait();
+  pdl_launch_dependents();
+  const uint32_t tmem = *tmem_holder;
+  const uint32_t tS = tmem;        // S buffers at columns [0,128), [128,256)
+  const uint32_t tO = tmem + 256;  // O at [256, 384)
+
+  // item k -> group c, row block rb, split s; its tiles [t0, t1)
+  auto item_of = [&](int k, int& c, int& rb, int& s, int& t0, int& t1) {
+    s = k % P.nsplit;
+    const int cr = k / P.nsplit;
+    rb = cr % P.nrb;
+    c = cr / P.nrb;
+    t0 = s * P.tps;
+    t1 = min(P.ntile, t0 + P.tps);
+  };
+
+  if (warp == 0) {
+    // ============================ TMA producer ============================
+    if (lane == 0) {
+      const uint64_t pol = tc::policy_evict_last();  // re-read by the other row blocks
+      uint32_t u = 0;
+      for (int k = blockIdx.x; k < P.items; k += gridDim.x) {
+        int c, rb, s, t0, t1;
+        item_of(k, c, rb, s, t0, t1);
+        for (int t = t0; t < t1; ++t, ++u) {
+          const int st = u & 1;
+          tc::mbar_wait_sleep(tc::smem_u32(&kv_empty[st]), ((u >> 1) & 1) ^ 1);
+          const uint32_t bar = tc::smem_u32(&kv_full[st]);
+          tc::mbar_arrive_expect_tx(bar, kStage);
+          const uint32_t dst = tc::smem_u32(smem + st * kStage);
+          tc::tma_load_3d_hint(dst, &P.tmKc, bar, 0, t * 128, c, pol);
+          tc::tma_load_3d_hint(dst + 16384, &P.tmKc, bar, 64, t * 128, c, pol);
+          tc::tma_load_3d_hint(dst + 32768, &P.tmVc, bar, 0, t * 128, c, pol);
+          tc::tma_load_3d_hint(dst + 49152, &P.tmVc, bar, 64, t * 128, c, pol);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ============================ MMA issuer ==============================
+    if (lane == 0) {
+      constexpr uint32_t IDESC_QK = tc::idesc_bf16(128, 128, 0, 0);
+      constexpr uint32_t IDESC_PV = tc::idesc_bf16(128, 128, 0, 1);
+      const uint32_t qbase = tc::smem_u32(smem + kQ);
+      const uint32_t pbase = tc::smem_u32(smem + kP);
+      uint32_t u = 0, it = 0;
+      // O += P(v) . V(v): both bf16 parts of P into the same accumulator
+      auto pv = [&](uint32_t v, bool first) {
+        tc::mbar_wait_sleep(tc::smem_u32(p_full), v & 1);
+        tc::tc_fence_after();
+        const uint32_t vb = tc::smem_u32(smem + (v & 1) * kStage + 32768);
+#pragma unroll
+        for (int part = 0; part < 2; ++part)
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const uint64_t ad = tc::smem_desc(pbase + part * 32768 + (k >> 2) * 16384 + (k & 3) * 32,
+                                              16, 1024, tc::kSw128);
+            const uint64_t bd = tc::smem_desc(vb + k * 2048, 16384, 1024, tc::kSw128);
+            tc::mma_bf16(tO, ad, bd, IDESC_PV, (first && part == 0 && k == 0) ? 0u : 1u);
+          }
+        tc::mma_commit(tc::smem_u32(p_empty));
+        tc::mma_commit(tc::smem_u32(&kv_empty[v & 1]));
+      };
+      for (int k = blockIdx.x; k < P.items; k += gridDim.x, ++it) {
+        int c, rb, s, t0, t1;
+        item_of(k, c, rb, s, t0, t1);
+        tc::mbar_wait_sleep(tc::smem_u32(q_full), it & 1);
+        const uint32_t u0 = u;
+        for (int t = t0; t < t1; ++t, ++u) {
+          tc::mbar_wait_sleep(tc::smem_u32(&kv_full[u & 1]), (u >> 1) & 1);
+          tc::mbar_wait_sleep(tc::smem_u32(&s_free[u & 1]), ((u >> 1) & 1) ^ 1);
+          tc::tc_fence_after();
+          const uint32_t kb = tc::smem_u32(smem + (u & 1) * kStage);
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            const uint64_t ad = tc::smem_desc(qbase + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024,
+                                              tc::kSw128);
+            const uint64_t bd = tc::smem_desc(kb + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024,
+                                              tc::kSw128);
+            tc::mma_bf16(tS + (u & 1) * 128, ad, bd, IDESC_QK, kk > 0 ? 1u : 0u);
+          }
+          tc::mma_commit(tc::smem_u32(&s_full[u & 1]));
+          if (t == t1 - 1) tc::mma_commit(tc::smem_u32(q_empty));  // Q block reusable
+          if (u > u0) pv(u - 1, u - 1 == u0);
+          else tc::mbar_wait_sleep(tc::smem_u32(o_empty), (it & 1) ^ 1);  // O drained
+        }
+        pv(u - 1, u - 1 == u0);
+        tc::mma_commit(tc::smem_u32(o_full));
+      }
+    }
+  } else if (warp >= 4) {
+    // ===================== softmax + epilogue (row per thread) =====================
+    const int quad = warp & 3;
+    const int r = quad * 32 + lane;                    // row in the block = TMEM lane
+    const uint32_t lane_addr = (uint32_t)(quad * 32) << 16;
+    const float sl2 = P.scale_log2;
+    uint8_t* const sq = smem + kQ;
+    uint8_t* const sp = smem + kP;
+    uint32_t u = 0, it = 0;
+    for (int k = blockIdx.x; k < P.items; k += gridDim.x, ++it) {
+      int c, rb, s, t0, t1;
+      item_of(k, c, rb, s, t0, t1);
+      const int rg = rb * 128 + r;                      // row within the group
+      const bool valid_row = rg < P.R;
+      const int gr = valid_row ? (rg / P.p) * P.h + c * P.p + rg % P.p : -1;
+      // ---- Q row -> shared memory (SW128, the TMA box layout) ----
+      tc::mbar_wait(tc::smem_u32(q_empty), (it & 1) ^ 1);
+      {
+        const uint4* src = reinterpret_cast<const uint4*>(P.q) + (size_t)(valid_row ? gr : 0) * 16;
+#pragma unroll
+        for (int ch = 0; ch < 16; ++ch) {
+          const uint4 v = valid_row ? __ldg(src + ch) : make_uint4(0, 0, 0, 0);
+          *reinterpret_cast<uint4*>(sq + sw128_off(r, ch)) = v;
+        }
+      }
+      tc::fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(tc::smem_u32(q_full));
+      float m = kNegInf, l = 0.f;
+      for (int t = t0; t < t1; ++t, ++u) {
+        tc::mbar_wait(tc::smem_u32(&s_full[u & 1]), (u >> 1) & 1);
+        tc::tc_fence_after();
+        float x[128];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          tc::tmem_ld<32>(tS + (u & 1) * 128 + q * 32 + lane_addr, reinterpret_cast<uint32_t*>(x) + q * 32);
+        tc::tmem_ld_wait();
+        tc::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(tc::smem_u32(&s_free[u & 1]));
+        // logits in log2 units; positions past mc masked (last tile only)
+        const int nvalid = min(128, P.mc - t * 128);
+        float mx = kNegInf;
+#pragma unroll
+        for (int i = 0; i < 128; ++i) {
+          x[i] = i < nvalid ? x[i] * sl2 : kNegInf;
+          mx = fmaxf(mx, x[i]);
+        }
+        // PV of the previous tile done: P buffer free and O quiescent
+        tc::mbar_wait(tc::smem_u32(p_empty), (u & 1) ^ 1);
+        if (m == kNegInf || mx > m + kTh) {
+          // raise the reference to the exact max; rescale l and this row of O
+          const float mn = mx;
+          if (m != kNegInf && t > t0) {
+            const float a = ex2(m - mn);
+            l *= a;
+            tc::tc_fence_after();
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+              uint32_t o[8];
+              tc::tmem_ld<8>(tO + q * 8 + lane_addr, o);
+              tc::tmem_ld_wait();
+#pragma unroll
+              for (int e = 0; e < 8; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * a);
+              tc::tmem_st<8>(tO + q * 8 + lane_addr, o);
+            }
+            tc::tmem_st_wait();
+            tc::tc_fence_before();
+          }
+          m = mn;
+        }
+        // P = 2^(x - m) as P_hi + P_lo (bf16) into shared memory, row r
+#pragma unroll
+        for (int ch = 0; ch < 16; ++ch) {
+          uint32_t hk[4], lk[4];
+#pragma unroll
+          for (int e = 0; e < 8; e += 2) {
+            const float p0 = ex2(x[ch * 8 + e] - m), p1 = ex2(x[ch * 8 + e + 1] - m);
+            l += p0 + p1;
+            hk[e / 2] = pack_bf16x2(p0, p1);
+            lk[e / 2] = pack_bf16x2(p0 - bf16lo(hk[e / 2]), p1 - bf16hi(hk[e / 2]));
+          }
+          const uint32_t off = sw128_off(r, ch);
+          *reinterpret_cast<uint4*>(sp + off) = make_uint4(hk[0], hk[1], hk[2], hk[3]);
+          *reinterpret_cast<uint4*>(sp + 32768 + off) = make_uint4(lk[0], lk[1], lk[2], lk[3]);
+        }
+        tc::fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(tc::smem_u32(p_full));
+      }
+      // ---- the item's partial: O row (relative to 2^m), m, l ----
+      tc::mbar_wait(tc::smem_u32(o_full), it & 1);
+      tc::tc_fence_after();
+      float* wo = valid_row ? P.ws_o + ((size_t)gr * P.S + s) * 128 : nullptr;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint32_t o[32];
+        tc::tmem_ld<32>(tO + q * 32 + lane_addr, o);
+        tc::tmem_ld_wait();
+        if (valid_row) {
+#pragma unroll
+          for (int e = 0; e < 32; e += 4)
+            *reinterpret_cast<float4*>(wo + q * 32 + e) =
+                make_float4(__uint_as_float(o[e]), __uint_as_float(o[e + 1]),
+                            __uint_as_float(o[e + 2]), __uint_as_float(o[e + 3]));
+        }
+      }
+      if (valid_row) reinterpret_cast<float2*>(P.ws_ml)[(size_t)gr * P.S + s] = make_float2(m, l);
+      tc::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(tc::smem_u32(o_empty));
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc::tc_fence_after();
+    tc::tmem_dealloc(tmem, 512);
+  }
+}
+
+}  // namespace ba

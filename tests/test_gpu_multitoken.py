@@ -17,6 +17,7 @@ DEV = "cuda:0"
 
 CASES = [
     (Config("mt_mha", "bf16", b=12, h=8, g=8, d=128, mc=700, md=40), 4),
+    (Config("mt_rows", "bf16", b=40, h=4, g=4, d=128, mc=333, md=20), 4),
     (Config("mt_mha_n2", "bf16", b=33, h=4, g=4, d=128, mc=300, md=130), 2),
     (Config("mt_gqa", "bf16", b=6, h=16, g=4, d=128, mc=513, md=77), 4),
     (Config("mt_p2n3", "bf16", b=5, h=4, g=2, d=128, mc=260, md=20), 3),
@@ -36,7 +37,8 @@ def _run(inp, flags=0):
 
 
 @pytest.mark.parametrize("case", CASES, ids=lambda c: f"{c[0].name}_n{c[1]}")
-@pytest.mark.parametrize("flags", [0, ba.BA_FLAG_FORCE_FMA], ids=["auto", "fma"])
+@pytest.mark.parametrize("flags", [0, ba.BA_FLAG_FORCE_FMA, ba.BA_FLAG_CTX_ROWS],
+                         ids=["auto", "fma", "rows"])
 @pytest.mark.parametrize("variant", ["ragged", "dec_dom"])
 def test_multi_token_all_rows(case, flags, variant):
     cfg, n = case

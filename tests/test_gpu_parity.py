@@ -37,11 +37,16 @@ SMALL = [
     Config("fp32_d128", "fp32", b=4, h=4, g=2, d=128, mc=300, md=17),
     Config("mc1", "bf16", b=2, h=2, g=1, d=128, mc=1, md=3),
     Config("md0", "bf16", b=4, h=4, g=4, d=128, mc=333, md=0),
+    # R = b*p >= 128: context branch on the rows-on-M kernel (ctx_rows.cuh)
+    Config("rows130", "bf16", b=130, h=2, g=2, d=128, mc=1000, md=20),
+    Config("gqa_rows300", "bf16", b=75, h=8, g=2, d=128, mc=700, md=30),
+    Config("rows128_md0", "bf16", b=64, h=4, g=2, d=128, mc=129, md=0),
 ]
 
 
 @pytest.mark.parametrize("cfg", SMALL, ids=lambda c: c.name)
-@pytest.mark.parametrize("flags", [0, ba.BA_FLAG_FORCE_FMA], ids=["auto", "fma"])
+@pytest.mark.parametrize("flags", [0, ba.BA_FLAG_FORCE_FMA, ba.BA_FLAG_CTX_ROWS],
+                         ids=["auto", "fma", "rows"])
 def test_small_all_rows(cfg, flags):
     inp = make_inputs(cfg, seed_for(cfg.name), variant="ragged" if cfg.md > 0 else "normal")
     out, lse = run_gpu(inp, flags)
@@ -51,10 +56,11 @@ def test_small_all_rows(cfg, flags):
 
 @pytest.mark.parametrize("variant", ["normal", "peaky", "ctx_dom", "dec_dom", "planted_ctx",
                                      "planted_dec", "equal", "ragged"])
-@pytest.mark.parametrize("cfg", [SMALL[2], SMALL[4], SMALL[5]], ids=lambda c: c.name)
-def test_stress_variants(cfg, variant):
+@pytest.mark.parametrize("cfg", [SMALL[2], SMALL[4], SMALL[5], SMALL[13]], ids=lambda c: c.name)
+@pytest.mark.parametrize("flags", [0, ba.BA_FLAG_CTX_ROWS], ids=["auto", "rows"])
+def test_stress_variants(cfg, variant, flags):
     inp = make_inputs(cfg, 7, variant=variant)
-    out, lse = run_gpu(inp)
+    out, lse = run_gpu(inp, flags)
     ref, ref_lse = oracle_rows(inp)
     compare(out, lse, ref, ref_lse, cfg.torch_dtype, f"{cfg.name}/{variant}")
     if variant == "equal":

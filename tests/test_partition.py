@@ -44,14 +44,16 @@ def pick_n(b, h, g):
     return fit[0] if fit else cands[-1]
 
 
-def model(b, h, g, mc, md, cs, bw):
+def model(b, h, g, mc, md, cs, bw, N=None, with_ctx=True):
     """Python model of seg_at / ctx_unit / ctx_parts / dec_parts (bif_tc.cuh)
-    over the planner's CTA table; bw = the plan's context band width."""
+    over the planner's CTA table; bw = the plan's context band width.  With
+    with_ctx=False (the context ran in ctx_rows_kernel) only decode tiles."""
     p = h // g
-    N = pick_n(b, h, g)
+    N = N or pick_n(b, h, g)
     R = b * p
     nrc = -(-R // N)
-    ntc = -(-mc // 128)
+    ntc = -(-mc // 128) if with_ctx else 0
+    bw = bw if with_ctx else 1
     ntd = -(-md // 128) if md else 0
     gpc = N // p
     ndc = -(-g // gpc)
@@ -59,7 +61,7 @@ def model(b, h, g, mc, md, cs, bw):
     Td = g * b * ntd
     T = Tc + Td
     G = len(cs) - 1
-    nband = -(-ntc // bw)
+    nband = -(-ntc // bw) if ntc else 0
     banded = nband > 1
     assert not banded or nrc > 1
     assert cs[0] == 0 and cs[-1] == T
@@ -131,6 +133,17 @@ def test_split_covers_every_tile_once_and_slots_match(shape):
     cs = ba.ba_plan_ctas(prob)
     assert cs, "tensor-core plan expected"
     plan = ba.ba_plan_string(prob)
+    if plan.startswith("ctx_rows"):
+        # context on the rows-on-M kernel: one partial per split; the fused
+        # launch streams decode tiles only (N = smallest multiple of 16 and p)
+        m = re.search(r"splits=(\d+).*dec_tc\(N=(\d+).*slots=(\d+)\+(\d+)", plan)
+        N = int(m.group(2))
+        assert N == min(n for n in (16, 32, 48, 64) if n % (h // g) == 0)
+        assert int(m.group(3)) == int(m.group(1))
+        if md:
+            _, _, sd, _, _ = model(b, h, g, mc, md, cs, 1, N=N, with_ctx=False)
+            assert sd == int(m.group(4))
+        return
     m = re.search(r"N=(\d+).*band=(\d+).*slots=(\d+)\+(\d+)", plan)
     assert m, plan
     N, sc, sd, loads, banded = model(b, h, g, mc, md, cs, int(m.group(2)))
@@ -161,7 +174,7 @@ def test_banded_context_split_in_subprocess():
         "    out.append([list(s), ba.ba_plan_ctas(pr), ba.ba_plan_string(pr)])\n"
         "print(json.dumps(out))\n")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, BIFATTN_BAND="8", PYTHONPATH=root)
+    env = dict(os.environ, BIFATTN_BAND="8", BIFATTN_CTX_ROWS="0", PYTHONPATH=root)
     res = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
                          check=True, cwd=root)
     for (b, h, g, mc, md), cs, plan in json.loads(res.stdout.strip().splitlines()[-1]):
