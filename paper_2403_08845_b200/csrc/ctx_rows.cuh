@@ -14,13 +14,15 @@
 // Tile math (rows on M):
 //   S[128 rows x 128 pos]  = Q_blk[128 x d] . K_tile^T       (A = Q, B = K, both K-major)
 //   O[128 rows x d]       += P_hi . V_tile + P_lo . V_tile   (A = P K-major, B = V MN-major)
-// One thread owns one row (TMEM lane = row): the row max, the stale-max test
-// and the O rescale are in-thread — no cross-warp vote.  P = P_hi + P_lo
+// Two threads own a row (TMEM lane = row, one per half of the positions):
+// the row max is a 2-way exchange, the stale-max test and the O rescale are
+// per row — no vote across the rows of a column as in the swap-AB kernel.  P = P_hi + P_lo
 // (two bf16 parts, ~16 significant bits, reading R13) goes through shared
 // memory; both parts accumulate into the same fp32 O.
 //
-// Warps: 0 TMA producer (one lane), 1 MMA issuer (one lane), 2 TMEM
-// allocator, 3 idle, 4..7 softmax/epilogue (128 threads = 128 rows).
+// Warps: 0 / 3 TMA producers of the K / V halves (one lane each), 1 MMA
+// issuer (one lane), 2 TMEM allocator, 4..11 softmax/epilogue: two threads
+// per row, each taking half of the tile's positions and of the O columns.
 #pragma once
 #include "common.cuh"
 #include "tc_ptx.cuh"
@@ -46,9 +48,10 @@ constexpr int kNst = 2;                 // K/V stages
 constexpr int kQ = 2 * kStage;          // Q block (32 KB)
 constexpr int kP = kQ + 32768;          // P_hi (32 KB), P_lo (32 KB)
 constexpr int kBar = kP + 65536;        // barriers
-constexpr int kSmem = kBar + 256;
+constexpr int kXch = kBar + 256;        // row-max exchange [2 tiles][2 halves][128 rows] floats
+constexpr int kSmem = kXch + 2048;      // 231680 <= 227 KB
 constexpr float kTh = 8.0f;             // stale-max slack (log2 units), as bif_tc.cuh
-constexpr int kThreads = 256;
+constexpr int kThreads = 384;
 
 // byte offset of 16-byte chunk `ch` (0..15) of row r in a 128-row x 128-col
 // bf16 K-major SW128 tile stored as two 64-column halves (the TMA box layout)
@@ -62,8 +65,10 @@ __global__ void __launch_bounds__(ctxr::kThreads, 1)
   using namespace ctxr;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kBar);
-  uint64_t* kv_full = bars;       // [2]
-  uint64_t* kv_empty = bars + 2;  // [2]
+  // K and V halves of a stage have their own barriers: K(u) is released by
+  // QK(u), V(u) by PV(u), so the next K load does not wait for the PV
+  uint64_t* k_full = bars;        // [2]
+  uint64_t* k_empty = bars + 2;   // [2]
   uint64_t* s_full = bars + 4;    // [2]
   uint64_t* s_free = bars + 6;    // [2]
   uint64_t* q_full = bars + 8;
@@ -72,22 +77,26 @@ __global__ void __launch_bounds__(ctxr::kThreads, 1)
   uint64_t* p_empty = bars + 11;
   uint64_t* o_full = bars + 12;
   uint64_t* o_empty = bars + 13;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 14);
+  uint64_t* v_full = bars + 14;   // [2]
+  uint64_t* v_empty = bars + 16;  // [2]
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 18);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < 2; ++s) {
-      tc::mbar_init(tc::smem_u32(&kv_full[s]), 1);
-      tc::mbar_init(tc::smem_u32(&kv_empty[s]), 1);
+      tc::mbar_init(tc::smem_u32(&k_full[s]), 1);
+      tc::mbar_init(tc::smem_u32(&k_empty[s]), 1);
+      tc::mbar_init(tc::smem_u32(&v_full[s]), 1);
+      tc::mbar_init(tc::smem_u32(&v_empty[s]), 1);
       tc::mbar_init(tc::smem_u32(&s_full[s]), 1);
-      tc::mbar_init(tc::smem_u32(&s_free[s]), 4);
+      tc::mbar_init(tc::smem_u32(&s_free[s]), 8);
     }
-    tc::mbar_init(tc::smem_u32(q_full), 4);
+    tc::mbar_init(tc::smem_u32(q_full), 8);
     tc::mbar_init(tc::smem_u32(q_empty), 1);
-    tc::mbar_init(tc::smem_u32(p_full), 4);
+    tc::mbar_init(tc::smem_u32(p_full), 8);
     tc::mbar_init(tc::smem_u32(p_empty), 1);
     tc::mbar_init(tc::smem_u32(o_full), 1);
-    tc::mbar_init(tc::smem_u32(o_empty), 4);
+    tc::mbar_init(tc::smem_u32(o_empty), 8);
     tc::fence_mbar_init();
   }
   if (warp == 0 && lane == 0) {
@@ -117,9 +126,13 @@ __global__ void __launch_bounds__(ctxr::kThreads, 1)
     t1 = min(P.ntile, t0 + P.tps);
   };
 
-  if (warp == 0) {
-    // ============================ TMA producer ============================
+  if (warp == 0 || warp == 3) {
+    // ==================== TMA producers: K (warp 0), V (warp 3) ====================
     if (lane == 0) {
+      const bool isk = warp == 0;
+      const CUtensorMap* map = isk ? &P.tmKc : &P.tmVc;
+      uint64_t* full = isk ? k_full : v_full;
+      uint64_t* empty = isk ? k_empty : v_empty;
       const uint64_t pol = tc::policy_evict_last();  // re-read by the other row blocks
       uint32_t u = 0;
       for (int k = blockIdx.x; k < P.items; k += gridDim.x) {
@@ -127,14 +140,12 @@ __global__ void __launch_bounds__(ctxr::kThreads, 1)
         item_of(k, c, rb, s, t0, t1);
         for (int t = t0; t < t1; ++t, ++u) {
           const int st = u & 1;
-          tc::mbar_wait_sleep(tc::smem_u32(&kv_empty[st]), ((u >> 1) & 1) ^ 1);
-          const uint32_t bar = tc::smem_u32(&kv_full[st]);
-          tc::mbar_arrive_expect_tx(bar, kStage);
-          const uint32_t dst = tc::smem_u32(smem + st * kStage);
-          tc::tma_load_3d_hint(dst, &P.tmKc, bar, 0, t * 128, c, pol);
-          tc::tma_load_3d_hint(dst + 16384, &P.tmKc, bar, 64, t * 128, c, pol);
-          tc::tma_load_3d_hint(dst + 32768, &P.tmVc, bar, 0, t * 128, c, pol);
-          tc::tma_load_3d_hint(dst + 49152, &P.tmVc, bar, 64, t * 128, c, pol);
+          tc::mbar_wait_sleep(tc::smem_u32(&empty[st]), ((u >> 1) & 1) ^ 1);
+          const uint32_t bar = tc::smem_u32(&full[st]);
+          tc::mbar_arrive_expect_tx(bar, kStage / 2);
+          const uint32_t dst = tc::smem_u32(smem + st * kStage + (isk ? 0 : 32768));
+          tc::tma_load_3d_hint(dst, map, bar, 0, t * 128, c, pol);
+          tc::tma_load_3d_hint(dst + 16384, map, bar, 64, t * 128, c, pol);
         }
       }
     }
@@ -148,6 +159,7 @@ __global__ void __launch_bounds__(ctxr::kThreads, 1)
       uint32_t u = 0, it = 0;
       // O += P(v) . V(v): both bf16 parts of P into the same accumulator
       auto pv = [&](uint32_t v, bool first) {
+        tc::mbar_wait_sleep(tc::smem_u32(&v_full[v & 1]), (v >> 1) & 1);
         tc::mbar_wait_sleep(tc::smem_u32(p_full), v & 1);
         tc::tc_fence_after();
         const uint32_t vb = tc::smem_u32(smem + (v & 1) * kStage + 32768);
@@ -161,7 +173,7 @@ __global__ void __launch_bounds__(ctxr::kThreads, 1)
             tc::mma_bf16(tO, ad, bd, IDESC_PV, (first && part == 0 && k == 0) ? 0u : 1u);
           }
         tc::mma_commit(tc::smem_u32(p_empty));
-        tc::mma_commit(tc::smem_u32(&kv_empty[v & 1]));
+        tc::mma_commit(tc::smem_u32(&v_empty[v & 1]));
       };
       for (int k = blockIdx.x; k < P.items; k += gridDim.x, ++it) {
         int c, rb, s, t0, t1;
@@ -169,7 +181,7 @@ __global__ void __launch_bounds__(ctxr::kThreads, 1)
         tc::mbar_wait_sleep(tc::smem_u32(q_full), it & 1);
         const uint32_t u0 = u;
         for (int t = t0; t < t1; ++t, ++u) {
-          tc::mbar_wait_sleep(tc::smem_u32(&kv_full[u & 1]), (u >> 1) & 1);
+          tc::mbar_wait_sleep(tc::smem_u32(&k_full[u & 1]), (u >> 1) & 1);
           tc::mbar_wait_sleep(tc::smem_u32(&s_free[u & 1]), ((u >> 1) & 1) ^ 1);
           tc::tc_fence_after();
           const uint32_t kb = tc::smem_u32(smem + (u & 1) * kStage);
@@ -182,6 +194,7 @@ __global__ void __launch_bounds__(ctxr::kThreads, 1)
             tc::mma_bf16(tS + (u & 1) * 128, ad, bd, IDESC_QK, kk > 0 ? 1u : 0u);
           }
           tc::mma_commit(tc::smem_u32(&s_full[u & 1]));
+          tc::mma_commit(tc::smem_u32(&k_empty[u & 1]));  // K(u) reusable
           if (t == t1 - 1) tc::mma_commit(tc::smem_u32(q_empty));  // Q block reusable
           if (u > u0) pv(u - 1, u - 1 == u0);
           else tc::mbar_wait_sleep(tc::smem_u32(o_empty), (it & 1) ^ 1);  // O drained
@@ -191,13 +204,19 @@ __global__ void __launch_bounds__(ctxr::kThreads, 1)
       }
     }
   } else if (warp >= 4) {
-    // ===================== softmax + epilogue (row per thread) =====================
+    // ============ softmax + epilogue: two threads per row (one per half) ============
+    // warps 4..7 (hf = 0) take positions [0, 64) and O columns [0, 64) of their
+    // rows, warps 8..11 (hf = 1) positions [64, 128) and O columns [64, 128);
+    // the two halves of a row agree on its running max through one 256-thread
+    // barrier per tile (double-buffered exchange slots).
+    const int hf = (warp - 4) >> 2;
     const int quad = warp & 3;
     const int r = quad * 32 + lane;                    // row in the block = TMEM lane
     const uint32_t lane_addr = (uint32_t)(quad * 32) << 16;
     const float sl2 = P.scale_log2;
     uint8_t* const sq = smem + kQ;
     uint8_t* const sp = smem + kP;
+    float* const sm_x = reinterpret_cast<float*>(smem + kXch);
     uint32_t u = 0, it = 0;
     for (int k = blockIdx.x; k < P.items; k += gridDim.x, ++it) {
       int c, rb, s, t0, t1;
@@ -205,12 +224,12 @@ __global__ void __launch_bounds__(ctxr::kThreads, 1)
       const int rg = rb * 128 + r;                      // row within the group
       const bool valid_row = rg < P.R;
       const int gr = valid_row ? (rg / P.p) * P.h + c * P.p + rg % P.p : -1;
-      // ---- Q row -> shared memory (SW128, the TMA box layout) ----
+      // ---- this half of the Q row -> shared memory (SW128, the TMA box layout) ----
       tc::mbar_wait(tc::smem_u32(q_empty), (it & 1) ^ 1);
       {
         const uint4* src = reinterpret_cast<const uint4*>(P.q) + (size_t)(valid_row ? gr : 0) * 16;
 #pragma unroll
-        for (int ch = 0; ch < 16; ++ch) {
+        for (int ch = 8 * hf; ch < 8 * hf + 8; ++ch) {
           const uint4 v = valid_row ? __ldg(src + ch) : make_uint4(0, 0, 0, 0);
           *reinterpret_cast<uint4*>(sq + sw128_off(r, ch)) = v;
         }
@@ -218,61 +237,64 @@ __global__ void __launch_bounds__(ctxr::kThreads, 1)
       tc::fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(tc::smem_u32(q_full));
-      float m = kNegInf, l = 0.f;
+      float m = kNegInf, l = 0.f;  // l: this half's share of the row sum
       for (int t = t0; t < t1; ++t, ++u) {
         tc::mbar_wait(tc::smem_u32(&s_full[u & 1]), (u >> 1) & 1);
         tc::tc_fence_after();
-        float x[128];
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-          tc::tmem_ld<32>(tS + (u & 1) * 128 + q * 32 + lane_addr, reinterpret_cast<uint32_t*>(x) + q * 32);
+        float x[64];
+        tc::tmem_ld<32>(tS + (u & 1) * 128 + hf * 64 + lane_addr, reinterpret_cast<uint32_t*>(x));
+        tc::tmem_ld<32>(tS + (u & 1) * 128 + hf * 64 + 32 + lane_addr, reinterpret_cast<uint32_t*>(x) + 32);
         tc::tmem_ld_wait();
         tc::tc_fence_before();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(tc::smem_u32(&s_free[u & 1]));
         // logits in log2 units; positions past mc masked (last tile only)
-        const int nvalid = min(128, P.mc - t * 128);
-        float mx = kNegInf;
+        const int nvalid = min(128, P.mc - t * 128) - hf * 64;
+        float mh = kNegInf;
 #pragma unroll
-        for (int i = 0; i < 128; ++i) {
+        for (int i = 0; i < 64; ++i) {
           x[i] = i < nvalid ? x[i] * sl2 : kNegInf;
-          mx = fmaxf(mx, x[i]);
+          mh = fmaxf(mh, x[i]);
         }
+        float* const xs = sm_x + (u & 1) * 256;
+        xs[hf * 128 + r] = mh;
+        tc::named_bar_sync(1, 256);
+        const float mx = fmaxf(mh, xs[(hf ^ 1) * 128 + r]);
         // PV of the previous tile done: P buffer free and O quiescent
         tc::mbar_wait(tc::smem_u32(p_empty), (u & 1) ^ 1);
         if (m == kNegInf || mx > m + kTh) {
-          // raise the reference to the exact max; rescale l and this row of O
+          // raise the reference to the exact max; rescale l and this half of the O row
           const float mn = mx;
           if (m != kNegInf && t > t0) {
             const float a = ex2(m - mn);
             l *= a;
             tc::tc_fence_after();
 #pragma unroll
-            for (int q = 0; q < 16; ++q) {
+            for (int q = 0; q < 8; ++q) {
               uint32_t o[8];
-              tc::tmem_ld<8>(tO + q * 8 + lane_addr, o);
+              tc::tmem_ld<8>(tO + hf * 64 + q * 8 + lane_addr, o);
               tc::tmem_ld_wait();
 #pragma unroll
               for (int e = 0; e < 8; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * a);
-              tc::tmem_st<8>(tO + q * 8 + lane_addr, o);
+              tc::tmem_st<8>(tO + hf * 64 + q * 8 + lane_addr, o);
             }
             tc::tmem_st_wait();
             tc::tc_fence_before();
           }
           m = mn;
         }
-        // P = 2^(x - m) as P_hi + P_lo (bf16) into shared memory, row r
+        // P = 2^(x - m) as P_hi + P_lo (bf16) into shared memory: this half's chunks
 #pragma unroll
-        for (int ch = 0; ch < 16; ++ch) {
+        for (int cc = 0; cc < 8; ++cc) {
           uint32_t hk[4], lk[4];
 #pragma unroll
           for (int e = 0; e < 8; e += 2) {
-            const float p0 = ex2(x[ch * 8 + e] - m), p1 = ex2(x[ch * 8 + e + 1] - m);
+            const float p0 = ex2(x[cc * 8 + e] - m), p1 = ex2(x[cc * 8 + e + 1] - m);
             l += p0 + p1;
             hk[e / 2] = pack_bf16x2(p0, p1);
             lk[e / 2] = pack_bf16x2(p0 - bf16lo(hk[e / 2]), p1 - bf16hi(hk[e / 2]));
           }
-          const uint32_t off = sw128_off(r, ch);
+          const uint32_t off = sw128_off(r, 8 * hf + cc);
           *reinterpret_cast<uint4*>(sp + off) = make_uint4(hk[0], hk[1], hk[2], hk[3]);
           *reinterpret_cast<uint4*>(sp + 32768 + off) = make_uint4(lk[0], lk[1], lk[2], lk[3]);
         }
@@ -283,11 +305,11 @@ __global__ void __launch_bounds__(ctxr::kThreads, 1)
       // ---- the item's partial: O row (relative to 2^m), m, l ----
       tc::mbar_wait(tc::smem_u32(o_full), it & 1);
       tc::tc_fence_after();
-      float* wo = valid_row ? P.ws_o + ((size_t)gr * P.S + s) * 128 : nullptr;
+      float* wo = valid_row ? P.ws_o + ((size_t)gr * P.S + s) * 128 + hf * 64 : nullptr;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < 2; ++q) {
         uint32_t o[32];
-        tc::tmem_ld<32>(tO + q * 32 + lane_addr, o);
+        tc::tmem_ld<32>(tO + hf * 64 + q * 32 + lane_addr, o);
         tc::tmem_ld_wait();
         if (valid_row) {
 #pragma unroll
@@ -297,7 +319,14 @@ __global__ void __launch_bounds__(ctxr::kThreads, 1)
                             __uint_as_float(o[e + 2]), __uint_as_float(o[e + 3]));
         }
       }
-      if (valid_row) reinterpret_cast<float2*>(P.ws_ml)[(size_t)gr * P.S + s] = make_float2(m, l);
+      // row sum = both halves' shares, through the exchange slots of parity
+      // u & 1 (last read before the previous tile's barrier; the next write to
+      // them needs the next item's QK, i.e. every warp's q_full arrival)
+      float* const ls = sm_x + (u & 1) * 256;
+      ls[hf * 128 + r] = l;
+      tc::named_bar_sync(1, 256);
+      if (hf == 0 && valid_row)
+        reinterpret_cast<float2*>(P.ws_ml)[(size_t)gr * P.S + s] = make_float2(m, l + ls[128 + r]);
       tc::tc_fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(tc::smem_u32(o_empty));
