@@ -72,9 +72,11 @@ enum {
 #define BA_FLAG_FORCE_FMA 0x1u /* route every branch through the CUDA-core FMA kernel
                                   (tests use it to cover both kernel families)       */
 #define BA_FLAG_NO_PDL 0x2u    /* do not use programmatic dependent launch           */
-#define BA_FLAG_CTX_ROWS 0x4u  /* bf16, d = 128, b*p >= 128: run the context branch on the
-                                  rows-on-M kernel even where the planner would keep
-                                  the single fused launch (tests cover both)          */
+#define BA_FLAG_CTX_ROWS 0x4u  /* bf16, d = 128: run the context branch on the rows-on-M
+                                  kernel also for b*p < 128 (default: b*p >= 128)     */
+#define BA_FLAG_NO_CTX_ROWS 0x8u /* bf16, d = 128: keep the single fused launch (context
+                                  in 32-row passes) also for b*p >= 128 (tests cover
+                                  every path)                                         */
 
 typedef struct {
   int32_t b;        /* samples sharing the context, >= 1                                */

@@ -26,6 +26,7 @@ BA_BF16, BA_FP32 = 0, 1
 BA_FLAG_FORCE_FMA = 0x1
 BA_FLAG_NO_PDL = 0x2
 BA_FLAG_CTX_ROWS = 0x4
+BA_FLAG_NO_CTX_ROWS = 0x8
 
 ERRORS = {0: "BA_OK", -1: "BA_EINVAL", -2: "BA_ENULL", -3: "BA_EALIGN", -4: "BA_EWORKSPACE",
           -5: "BA_EDTYPE", -6: "BA_ENODEV", -7: "BA_ECUDA"}

@@ -258,20 +258,14 @@ int make_plan(const ba_problem_t* pr_in, int sms, bool replicated, Plan* pl) {
     const char* e = getenv("BIFATTN_CTX_ROWS");
     return e ? atoi(e) : 1;
   }();
-  // Rows-on-M context kernel when the swap-AB kernel's 32-row passes would
-  // re-read the context from HBM, or are very many (C4: 192 passes).  Where
-  // the 4-8 passes hit L2 (C3, the 4-token C2b step) the single fused launch
-  // measured faster (round 1: C3 105 vs 125 us; C5 2.7 -> 2.0 ms; C4 163 ->
-  // 127 us).
-  const double ctx_bytes_all = 2.0 * g * (double)pr->mc * pr->d * 2;
-  const int nrc32 = cdiv(R, 32);
-  const long long T32 = (long long)g * nrc32 * cdiv(pr->mc, 128) +
-                        (long long)g * pr->b * cdiv(pr->md_cap, 128);
-  const bool l2_hits32 = ctx_bytes_all <= 64.0 * (1 << 20) ||
-                         1.5 * cdiv(pr->mc, 128) * std::min(sms, ba::bif_max_ctas) >= (double)T32;
-  const bool want_rows = (pr->flags & BA_FLAG_CTX_ROWS) || ctx_rows_env == 2 || !l2_hits32 ||
-                         nrc32 >= 16;
-  if (tcN && !replicated && R >= 128 && ctx_rows_env && want_rows) {
+  // Rows-on-M context kernel for R >= 128 rows per group: measured faster
+  // than the fused kernel's 32-row context passes on every such shape (round
+  // 1: C3 104 -> 90 us, C4 163 -> 86 us, C5 2.7 -> 1.8 ms, 4-token C2b 137 ->
+  // 111 us).  BA_FLAG_CTX_ROWS forces it (any R), BA_FLAG_NO_CTX_ROWS or
+  // BIFATTN_CTX_ROWS=0 keep the single fused launch.
+  const bool want_rows = ((pr->flags & BA_FLAG_CTX_ROWS) || R >= 128) &&
+                         !(pr->flags & BA_FLAG_NO_CTX_ROWS);
+  if (tcN && !replicated && ctx_rows_env && want_rows) {
     // context branch on the rows-on-M kernel; the fused kernel streams only
     // the decode tiles, so its N just has to hold p (smallest legal)
     P.ctx_rows = true;
@@ -282,7 +276,13 @@ int make_plan(const ba_problem_t* pr_in, int sms, bool replicated, Plan* pl) {
       }
     P.cr_nrb = cdiv(R, 128);
     P.cr_ntile = cdiv(pr->mc, 128);
-    int ns = cdiv(2 * sms, g * P.cr_nrb);  // ~2 items per SM
+    // one wave of long items: every item pays a Q load, a pipeline refill and
+    // a 64 KB partial (written here, read by the merge)
+    static const int ns_env = [] {  // experiment override: BIFATTN_ROWS_SPLITS
+      const char* e = getenv("BIFATTN_ROWS_SPLITS");
+      return e ? atoi(e) : 0;
+    }();
+    int ns = ns_env > 0 ? ns_env : std::max(1, sms / (g * P.cr_nrb));
     ns = std::max(1, std::min(ns, P.cr_ntile));
     P.cr_tps = cdiv(P.cr_ntile, ns);
     P.cr_nsplit = cdiv(P.cr_ntile, P.cr_tps);

@@ -37,8 +37,8 @@ def _run(inp, flags=0):
 
 
 @pytest.mark.parametrize("case", CASES, ids=lambda c: f"{c[0].name}_n{c[1]}")
-@pytest.mark.parametrize("flags", [0, ba.BA_FLAG_FORCE_FMA, ba.BA_FLAG_CTX_ROWS],
-                         ids=["auto", "fma", "rows"])
+@pytest.mark.parametrize("flags", [0, ba.BA_FLAG_FORCE_FMA, ba.BA_FLAG_CTX_ROWS,
+                                   ba.BA_FLAG_NO_CTX_ROWS], ids=["auto", "fma", "rows", "fused"])
 @pytest.mark.parametrize("variant", ["ragged", "dec_dom"])
 def test_multi_token_all_rows(case, flags, variant):
     cfg, n = case

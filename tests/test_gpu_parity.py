@@ -45,8 +45,8 @@ SMALL = [
 
 
 @pytest.mark.parametrize("cfg", SMALL, ids=lambda c: c.name)
-@pytest.mark.parametrize("flags", [0, ba.BA_FLAG_FORCE_FMA, ba.BA_FLAG_CTX_ROWS],
-                         ids=["auto", "fma", "rows"])
+@pytest.mark.parametrize("flags", [0, ba.BA_FLAG_FORCE_FMA, ba.BA_FLAG_CTX_ROWS,
+                                   ba.BA_FLAG_NO_CTX_ROWS], ids=["auto", "fma", "rows", "fused"])
 def test_small_all_rows(cfg, flags):
     inp = make_inputs(cfg, seed_for(cfg.name), variant="ragged" if cfg.md > 0 else "normal")
     out, lse = run_gpu(inp, flags)
@@ -57,7 +57,8 @@ def test_small_all_rows(cfg, flags):
 @pytest.mark.parametrize("variant", ["normal", "peaky", "ctx_dom", "dec_dom", "planted_ctx",
                                      "planted_dec", "equal", "ragged"])
 @pytest.mark.parametrize("cfg", [SMALL[2], SMALL[4], SMALL[5], SMALL[13]], ids=lambda c: c.name)
-@pytest.mark.parametrize("flags", [0, ba.BA_FLAG_CTX_ROWS], ids=["auto", "rows"])
+@pytest.mark.parametrize("flags", [0, ba.BA_FLAG_CTX_ROWS, ba.BA_FLAG_NO_CTX_ROWS],
+                         ids=["auto", "rows", "fused"])
 def test_stress_variants(cfg, variant, flags):
     inp = make_inputs(cfg, 7, variant=variant)
     out, lse = run_gpu(inp, flags)
