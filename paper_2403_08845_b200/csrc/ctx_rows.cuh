@@ -17,8 +17,9 @@
 // Two threads own a row (TMEM lane = row, one per half of the positions):
 // the row max is a 2-way exchange, the stale-max test and the O rescale are
 // per row — no vote across the rows of a column as in the swap-AB kernel.  P = P_hi + P_lo
-// (two bf16 parts, ~16 significant bits, reading R13) goes through shared
-// memory; both parts accumulate into the same fp32 O.
+// (two bf16 parts, ~16 significant bits, reading R13) is stored to TMEM and
+// read from there as the PV's A operand; both parts accumulate into the same
+// fp32 O.  TMEM: S x2 (256 cols; P(u) overwrites S(u)), O (128).
 //
 // Warps: 0 / 3 TMA producers of the K / V halves (one lane each), 1 MMA
 // issuer (one lane), 2 TMEM allocator, 4..11 softmax/epilogue: two threads
@@ -44,10 +45,9 @@ struct CtxRowsParams {
 
 namespace ctxr {
 constexpr int kStage = 65536;           // K tile 32 KB + V tile 32 KB
-constexpr int kNst = 2;                 // K/V stages
-constexpr int kQ = 2 * kStage;          // Q block (32 KB)
-constexpr int kP = kQ + 32768;          // P_hi (32 KB), P_lo (32 KB)
-constexpr int kBar = kP + 65536;        // barriers
+constexpr int kNst = 3;                 // K/V stages
+constexpr int kQ = kNst * kStage;       // Q block (32 KB)
+constexpr int kBar = kQ + 32768;        // barriers
 constexpr int kXch = kBar + 256;        // row-max exchange [2 tiles][2 halves][128 rows] floats
 constexpr int kSmem = kXch + 2048;      // 231680 <= 227 KB
 constexpr float kTh = 8.0f;             // stale-max slack (log2 units), as bif_tc.cuh
@@ -67,33 +67,35 @@ __global__ void __launch_bounds__(ctxr::kThreads, 1)
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kBar);
   // K and V halves of a stage have their own barriers: K(u) is released by
   // QK(u), V(u) by PV(u), so the next K load does not wait for the PV
-  uint64_t* k_full = bars;        // [2]
-  uint64_t* k_empty = bars + 2;   // [2]
-  uint64_t* s_full = bars + 4;    // [2]
-  uint64_t* s_free = bars + 6;    // [2]
-  uint64_t* q_full = bars + 8;
-  uint64_t* q_empty = bars + 9;
-  uint64_t* p_full = bars + 10;
-  uint64_t* p_empty = bars + 11;
-  uint64_t* o_full = bars + 12;
-  uint64_t* o_empty = bars + 13;
-  uint64_t* v_full = bars + 14;   // [2]
-  uint64_t* v_empty = bars + 16;  // [2]
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 18);
+  uint64_t* k_full = bars;        // [kNst]
+  uint64_t* k_empty = bars + 3;   // [kNst]
+  uint64_t* s_full = bars + 6;    // [2]
+  uint64_t* s_free = bars + 8;    // [2]
+  uint64_t* q_full = bars + 10;
+  uint64_t* q_empty = bars + 11;
+  uint64_t* p_empty = bars + 13;  // PV(u) done (O quiescent for a rescale)
+  uint64_t* o_full = bars + 14;
+  uint64_t* o_empty = bars + 15;
+  uint64_t* v_full = bars + 16;   // [kNst]
+  uint64_t* v_empty = bars + 19;  // [kNst]
+  uint64_t* p_full = bars + 22;   // [2] P(u) stored over S(u)
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 24);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < kNst; ++s) {
       tc::mbar_init(tc::smem_u32(&k_full[s]), 1);
       tc::mbar_init(tc::smem_u32(&k_empty[s]), 1);
       tc::mbar_init(tc::smem_u32(&v_full[s]), 1);
       tc::mbar_init(tc::smem_u32(&v_empty[s]), 1);
+    }
+    for (int s = 0; s < 2; ++s) {
       tc::mbar_init(tc::smem_u32(&s_full[s]), 1);
-      tc::mbar_init(tc::smem_u32(&s_free[s]), 8);
+      tc::mbar_init(tc::smem_u32(&s_free[s]), 1);  // PV(u) done: slot reusable
+      tc::mbar_init(tc::smem_u32(&p_full[s]), 8);
     }
     tc::mbar_init(tc::smem_u32(q_full), 8);
     tc::mbar_init(tc::smem_u32(q_empty), 1);
-    tc::mbar_init(tc::smem_u32(p_full), 8);
     tc::mbar_init(tc::smem_u32(p_empty), 1);
     tc::mbar_init(tc::smem_u32(o_full), 1);
     tc::mbar_init(tc::smem_u32(o_empty), 8);
@@ -115,6 +117,9 @@ __global__ void __launch_bounds__(ctxr::kThreads, 1)
   const uint32_t tmem = *tmem_holder;
   const uint32_t tS = tmem;        // S buffers at columns [0,128), [128,256)
   const uint32_t tO = tmem + 256;  // O at [256, 384)
+  // P(u) = P_hi | P_lo as bf16 pairs is stored over S(u) (columns [0, 64) and
+  // [64, 128) of its slot) once S(u) is in registers: the S slots double as a
+  // double-buffered P, and a slot is free again when PV(u) completes
 
   // item k -> group c, row block rb, split s; its tiles [t0, t1)
   auto item_of = [&](int k, int& c, int& rb, int& s, int& t0, int& t1) {
@@ -139,8 +144,8 @@ __global__ void __launch_bounds__(ctxr::kThreads, 1)
         int c, rb, s, t0, t1;
         item_of(k, c, rb, s, t0, t1);
         for (int t = t0; t < t1; ++t, ++u) {
-          const int st = u & 1;
-          tc::mbar_wait_sleep(tc::smem_u32(&empty[st]), ((u >> 1) & 1) ^ 1);
+          const int st = u % kNst;
+          tc::mbar_wait_sleep(tc::smem_u32(&empty[st]), ((u / kNst) & 1) ^ 1);
           const uint32_t bar = tc::smem_u32(&full[st]);
           tc::mbar_arrive_expect_tx(bar, kStage / 2);
           const uint32_t dst = tc::smem_u32(smem + st * kStage + (isk ? 0 : 32768));
@@ -155,25 +160,25 @@ __global__ void __launch_bounds__(ctxr::kThreads, 1)
       constexpr uint32_t IDESC_QK = tc::idesc_bf16(128, 128, 0, 0);
       constexpr uint32_t IDESC_PV = tc::idesc_bf16(128, 128, 0, 1);
       const uint32_t qbase = tc::smem_u32(smem + kQ);
-      const uint32_t pbase = tc::smem_u32(smem + kP);
       uint32_t u = 0, it = 0;
       // O += P(v) . V(v): both bf16 parts of P into the same accumulator
       auto pv = [&](uint32_t v, bool first) {
-        tc::mbar_wait_sleep(tc::smem_u32(&v_full[v & 1]), (v >> 1) & 1);
-        tc::mbar_wait_sleep(tc::smem_u32(p_full), v & 1);
+        tc::mbar_wait_sleep(tc::smem_u32(&v_full[v % kNst]), (v / kNst) & 1);
+        tc::mbar_wait_sleep(tc::smem_u32(&p_full[v & 1]), (v >> 1) & 1);
         tc::tc_fence_after();
-        const uint32_t vb = tc::smem_u32(smem + (v & 1) * kStage + 32768);
+        const uint32_t vb = tc::smem_u32(smem + (v % kNst) * kStage + 32768);
 #pragma unroll
         for (int part = 0; part < 2; ++part)
 #pragma unroll
           for (int k = 0; k < 8; ++k) {
-            const uint64_t ad = tc::smem_desc(pbase + part * 32768 + (k >> 2) * 16384 + (k & 3) * 32,
-                                              16, 1024, tc::kSw128);
+            // A = P from TMEM: 16 positions per step = 8 columns of bf16 pairs
             const uint64_t bd = tc::smem_desc(vb + k * 2048, 16384, 1024, tc::kSw128);
-            tc::mma_bf16(tO, ad, bd, IDESC_PV, (first && part == 0 && k == 0) ? 0u : 1u);
+            tc::mma_bf16_ts(tO, tS + (v & 1) * 128 + part * 64 + k * 8, bd, IDESC_PV,
+                            (first && part == 0 && k == 0) ? 0u : 1u);
           }
         tc::mma_commit(tc::smem_u32(p_empty));
-        tc::mma_commit(tc::smem_u32(&v_empty[v & 1]));
+        tc::mma_commit(tc::smem_u32(&s_free[v & 1]));
+        tc::mma_commit(tc::smem_u32(&v_empty[v % kNst]));
       };
       for (int k = blockIdx.x; k < P.items; k += gridDim.x, ++it) {
         int c, rb, s, t0, t1;
@@ -181,10 +186,10 @@ __global__ void __launch_bounds__(ctxr::kThreads, 1)
         tc::mbar_wait_sleep(tc::smem_u32(q_full), it & 1);
         const uint32_t u0 = u;
         for (int t = t0; t < t1; ++t, ++u) {
-          tc::mbar_wait_sleep(tc::smem_u32(&k_full[u & 1]), (u >> 1) & 1);
+          tc::mbar_wait_sleep(tc::smem_u32(&k_full[u % kNst]), (u / kNst) & 1);
           tc::mbar_wait_sleep(tc::smem_u32(&s_free[u & 1]), ((u >> 1) & 1) ^ 1);
           tc::tc_fence_after();
-          const uint32_t kb = tc::smem_u32(smem + (u & 1) * kStage);
+          const uint32_t kb = tc::smem_u32(smem + (u % kNst) * kStage);
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk) {
             const uint64_t ad = tc::smem_desc(qbase + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024,
@@ -194,7 +199,7 @@ __global__ void __launch_bounds__(ctxr::kThreads, 1)
             tc::mma_bf16(tS + (u & 1) * 128, ad, bd, IDESC_QK, kk > 0 ? 1u : 0u);
           }
           tc::mma_commit(tc::smem_u32(&s_full[u & 1]));
-          tc::mma_commit(tc::smem_u32(&k_empty[u & 1]));  // K(u) reusable
+          tc::mma_commit(tc::smem_u32(&k_empty[u % kNst]));  // K(u) reusable
           if (t == t1 - 1) tc::mma_commit(tc::smem_u32(q_empty));  // Q block reusable
           if (u > u0) pv(u - 1, u - 1 == u0);
           else tc::mbar_wait_sleep(tc::smem_u32(o_empty), (it & 1) ^ 1);  // O drained
@@ -215,7 +220,6 @@ __global__ void __launch_bounds__(ctxr::kThreads, 1)
     const uint32_t lane_addr = (uint32_t)(quad * 32) << 16;
     const float sl2 = P.scale_log2;
     uint8_t* const sq = smem + kQ;
-    uint8_t* const sp = smem + kP;
     float* const sm_x = reinterpret_cast<float*>(smem + kXch);
     uint32_t u = 0, it = 0;
     for (int k = blockIdx.x; k < P.items; k += gridDim.x, ++it) {
@@ -245,9 +249,6 @@ __global__ void __launch_bounds__(ctxr::kThreads, 1)
         tc::tmem_ld<32>(tS + (u & 1) * 128 + hf * 64 + lane_addr, reinterpret_cast<uint32_t*>(x));
         tc::tmem_ld<32>(tS + (u & 1) * 128 + hf * 64 + 32 + lane_addr, reinterpret_cast<uint32_t*>(x) + 32);
         tc::tmem_ld_wait();
-        tc::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive(tc::smem_u32(&s_free[u & 1]));
         // logits in log2 units; positions past mc masked (last tile only)
         const int nvalid = min(128, P.mc - t * 128) - hf * 64;
         float mh = kNegInf;
@@ -260,12 +261,11 @@ __global__ void __launch_bounds__(ctxr::kThreads, 1)
         xs[hf * 128 + r] = mh;
         tc::named_bar_sync(1, 256);
         const float mx = fmaxf(mh, xs[(hf ^ 1) * 128 + r]);
-        // PV of the previous tile done: P buffer free and O quiescent
-        tc::mbar_wait(tc::smem_u32(p_empty), (u & 1) ^ 1);
         if (m == kNegInf || mx > m + kTh) {
           // raise the reference to the exact max; rescale l and this half of the O row
           const float mn = mx;
           if (m != kNegInf && t > t0) {
+            tc::mbar_wait(tc::smem_u32(p_empty), (u & 1) ^ 1);  // PV(u-1) done: O quiescent
             const float a = ex2(m - mn);
             l *= a;
             tc::tc_fence_after();
@@ -283,24 +283,24 @@ __global__ void __launch_bounds__(ctxr::kThreads, 1)
           }
           m = mn;
         }
-        // P = 2^(x - m) as P_hi + P_lo (bf16) into shared memory: this half's chunks
+        // P = 2^(x - m) as P_hi + P_lo (bf16 pairs) into TMEM: the PV's A operand
 #pragma unroll
-        for (int cc = 0; cc < 8; ++cc) {
-          uint32_t hk[4], lk[4];
+        for (int j = 0; j < 4; ++j) {
+          uint32_t hk[8], lk[8];
 #pragma unroll
-          for (int e = 0; e < 8; e += 2) {
-            const float p0 = ex2(x[cc * 8 + e] - m), p1 = ex2(x[cc * 8 + e + 1] - m);
+          for (int e = 0; e < 16; e += 2) {
+            const float p0 = ex2(x[j * 16 + e] - m), p1 = ex2(x[j * 16 + e + 1] - m);
             l += p0 + p1;
             hk[e / 2] = pack_bf16x2(p0, p1);
             lk[e / 2] = pack_bf16x2(p0 - bf16lo(hk[e / 2]), p1 - bf16hi(hk[e / 2]));
           }
-          const uint32_t off = sw128_off(r, 8 * hf + cc);
-          *reinterpret_cast<uint4*>(sp + off) = make_uint4(hk[0], hk[1], hk[2], hk[3]);
-          *reinterpret_cast<uint4*>(sp + 32768 + off) = make_uint4(lk[0], lk[1], lk[2], lk[3]);
+          tc::tmem_st<8>(tS + (u & 1) * 128 + hf * 32 + j * 8 + lane_addr, hk);
+          tc::tmem_st<8>(tS + (u & 1) * 128 + 64 + hf * 32 + j * 8 + lane_addr, lk);
         }
-        tc::fence_proxy_async_smem();
+        tc::tmem_st_wait();
+        tc::tc_fence_before();
         __syncwarp();
-        if (lane == 0) tc::mbar_arrive(tc::smem_u32(p_full));
+        if (lane == 0) tc::mbar_arrive(tc::smem_u32(&p_full[u & 1]));
       }
       // ---- the item's partial: O row (relative to 2^m), m, l ----
       tc::mbar_wait(tc::smem_u32(o_full), it & 1);
