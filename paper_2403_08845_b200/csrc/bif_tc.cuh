@@ -1111,8 +1111,8 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
               }
               l_part[n + e] += p0;
               l_part[n + e + 1] += p1;
-              hk[e / 2] = pack_bf16x2(p0, p1);
-              lk[e / 2] = pack_bf16x2(p0 - bf16lo(hk[e / 2]), p1 - bf16hi(hk[e / 2]));
+              hk[e / 2] = pack_bf16x2_trunc(p0, p1);
+              lk[e / 2] = pack_bf16x2_trunc(p0 - bf16lo(hk[e / 2]), p1 - bf16hi(hk[e / 2]));
             }
             const int col = col0 + n;
             uint32_t off = (uint32_t)((col / W) * PLBO + pos * PRB + (col % W) * 2);

@@ -107,6 +107,10 @@ struct Plan {
   // rows-on-M context kernel (ctx_rows.cuh) for R = b*p >= 128 rows per group
   bool ctx_rows = false;
   int cr_nrb = 0, cr_ntile = 0, cr_tps = 0, cr_nsplit = 0, cr_items = 0, cr_grid = 0;
+  // decode branch also in the rows kernel (p >= 32 rows per sample and group);
+  // the second launch is then the light merge kernel, not the fused kernel
+  bool cr_dec = false;
+  int cr_items_ctx = 0;
   long long tc_Tc = 0, tc_T = 0;
   int tc_cs[ba::bif_max_ctas + 1];
   size_t off_cnt = 0;
@@ -287,6 +291,15 @@ int make_plan(const ba_problem_t* pr_in, int sms, bool replicated, Plan* pl) {
     P.cr_tps = cdiv(P.cr_ntile, ns);
     P.cr_nsplit = cdiv(P.cr_ntile, P.cr_tps);
     P.cr_items = g * P.cr_nrb * P.cr_nsplit;
+    P.cr_items_ctx = P.cr_items;
+    static const int rows_dec_env = [] {  // BIFATTN_ROWS_DEC=0: decode stays in the fused kernel
+      const char* e = getenv("BIFATTN_ROWS_DEC");
+      return e ? atoi(e) : 1;
+    }();
+    if (rows_dec_env && p >= 32 && p <= 128 && P.ntok == 1 && pr->md_cap >= 1) {
+      P.cr_dec = true;
+      P.cr_items += b * g;
+    }
     P.cr_grid = std::min(P.cr_items, sms);
   }
   if (tcN) {
@@ -401,6 +414,7 @@ int make_plan(const ba_problem_t* pr_in, int sms, bool replicated, Plan* pl) {
       bw_try = P.tc_ntile_c;  // a unit got split (tiny problem): plain order
     }
     if (P.ctx_rows) sc = P.cr_nsplit;  // context partials written by ctx_rows_kernel
+    if (P.cr_dec) sd = 1;              // one decode partial per row, also from ctx_rows_kernel
     P.tc_Sc = sc;
     P.tc_Sd = sd;
     P.S = sc + sd;
@@ -705,6 +719,17 @@ int run_tc(const ba_problem_t* pr, const Plan& P, const void* q, const void* Kc,
     cp.ntile = P.cr_ntile; cp.tps = P.cr_tps; cp.nsplit = P.cr_nsplit; cp.items = P.cr_items;
     cp.scale_log2 = scale_log2;
     cp.S = P.S;
+    cp.items_ctx = P.cr_items_ctx;
+    cp.dec_slot = P.cr_nsplit;
+    cp.lens = lens;
+    cp.dec_cap = P.dec_cap;
+    cp.lens_add = ap ? ap->n : 0;
+    if (P.cr_dec) {
+      const uint64_t ds = (uint64_t)P.dec_stride, bg = (uint64_t)pr->b * pr->g;
+      rc = make_tmap_3d(&cp.tmKd, Kd, d, ds, bg, d * 2, ds * d * 2, 128, 1);
+      if (!rc) rc = make_tmap_3d(&cp.tmVd, Vd, d, ds, bg, d * 2, ds * d * 2, 128, 1);
+      if (rc) return rc;
+    }
     cp.ws_o = bp.ws_o;
     cp.ws_ml = bp.ws_ml;
     static std::once_flag once;
@@ -736,6 +761,30 @@ int run_tc(const ba_problem_t* pr, const Plan& P, const void* q, const void* Kc,
     }
     rc = rec.end();
     if (rc) return rc;
+    if (P.cr_dec) {
+      // both branches' partials are in the workspace: the light LSE merge
+      ba::MergeParams mp;
+      memset(&mp, 0, sizeof mp);
+      mp.ws_o = bp.ws_o;
+      mp.ws_ml = bp.ws_ml;
+      mp.rows = pr->b * pr->h;
+      mp.S = P.S;
+      mp.h = pr->h;
+      mp.p = p;
+      mp.ctx_mode = 1;
+      mp.nsc = P.cr_nsplit;
+      mp.dec_slot0 = P.cr_nsplit;
+      mp.nsd = 1;
+      mp.out = out;
+      mp.lse = lse;
+      mp.lens_out = ap ? ap->lens : nullptr;
+      mp.b = pr->b;
+      mp.lens_add = ap ? ap->n : 0;
+      mp.dec_cap = P.dec_cap;
+      rec.begin();
+      ba::merge_kernel<__nv_bfloat16, 128><<<cdiv(mp.rows, 8), 256, 0, st>>>(mp);
+      return rec.end();
+    }
   }
   // softmax warpgroups (override for experiments: BIFATTN_SWG=1|2)
   static const int swg_env = [] {
@@ -1061,7 +1110,13 @@ const char* ba_plan_string(const ba_problem_t* prob) {
     snprintf(g_plan_buf, sizeof g_plan_buf, "invalid (%d)", rc);
     return g_plan_buf;
   }
-  if (P.tc && P.ctx_rows)
+  if (P.tc && P.cr_dec)
+    snprintf(g_plan_buf, sizeof g_plan_buf,
+             "ctx_rows(blocks=%d,splits=%d,tiles/split=%d,items=%d+%d dec,ctas=%d) + merge "
+             "launches=2 ws=%zu",
+             P.cr_nrb, P.cr_nsplit, P.cr_tps, P.cr_items_ctx, P.cr_items - P.cr_items_ctx,
+             P.cr_grid, P.ws_bytes);
+  else if (P.tc && P.ctx_rows)
     snprintf(g_plan_buf, sizeof g_plan_buf,
              "ctx_rows(blocks=%d,splits=%d,tiles/split=%d,items=%d,ctas=%d) + "
              "dec_tc(N=%d,dec_tiles=%lld,ctas=%d,stages=%d,slots=%d+%d) launches=2 ws=%zu",
@@ -1088,7 +1143,10 @@ const char* ba_launch_name(const ba_problem_t* prob, int k) {
   if (make_plan(prob, sms, false, &P) != BA_OK) return nullptr;
   const char* names[4];
   int n = 0;
-  if (P.tc && P.ctx_rows) {
+  if (P.tc && P.cr_dec) {
+    names[n++] = "fused_rows";
+    names[n++] = "merge";
+  } else if (P.tc && P.ctx_rows) {
     names[n++] = "ctx_rows";
     names[n++] = "dec_tc_merge";
   } else if (P.tc) {

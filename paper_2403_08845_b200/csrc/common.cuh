@@ -25,6 +25,15 @@ BA_DEVINL uint32_t pack_bf16x2(float lo, float hi) {
   return r;
 }
 
+// Truncate two fp32 to bf16 and pack (lo in the low half): one byte permute
+// on the integer pipe instead of a conversion on the XU pipe, which the ex2 of
+// the softmax already loads.  Used for the split P = P_hi + P_lo (reading
+// R13): P_hi = trunc(P), P_lo = trunc(P - P_hi) (the difference is exact in
+// fp32), so |P - P_hi - P_lo| < 2^-14 |P|.
+BA_DEVINL uint32_t pack_bf16x2_trunc(float lo, float hi) {
+  return __byte_perm(__float_as_uint(lo), __float_as_uint(hi), 0x7632);
+}
+
 BA_DEVINL float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));

@@ -32,6 +32,11 @@ namespace ba {
 
 struct CtxRowsParams {
   CUtensorMap tmKc, tmVc;  // (d, mc, g), box (64, 128, 1), SW128
+  CUtensorMap tmKd, tmVd;  // (d, md_cap, b*g), box (64, 128, 1): decode items (p >= 32)
+  const int32_t* lens;     // decode items: valid length min(clamp(lens[i]) + lens_add, dec_cap)
+  int dec_cap, lens_add;
+  int items_ctx;           // items [0, items_ctx) are context items, then b*g decode items
+  int dec_slot;            // workspace slot of the decode partial
   const void* q;           // [b][h][128] bf16 (rows of group c: (i, c*p + j))
   int b, h, g, p, mc;
   int R, nrb;              // rows per group, 128-row blocks per group
@@ -43,6 +48,12 @@ struct CtxRowsParams {
   float* ws_ml;            // [b*h][S][2]
 };
 
+// Experiment bits (CTXR_EXP, experiment builds only; wrong results): 1 skip
+// the row-max exchange barrier, 2 skip the exp/pack work (P = 0), 4 skip the
+// PV MMAs, 8 skip the QK MMAs.
+#ifndef CTXR_EXP
+#define CTXR_EXP 0
+#endif
 namespace ctxr {
 constexpr int kStage = 65536;           // K tile 32 KB + V tile 32 KB
 constexpr int kNst = 3;                 // K/V stages
@@ -104,6 +115,10 @@ __global__ void __launch_bounds__(ctxr::kThreads, 1)
   if (warp == 0 && lane == 0) {
     tc::prefetch_tmap(&P.tmKc);
     tc::prefetch_tmap(&P.tmVc);
+    if (P.items > P.items_ctx) {
+      tc::prefetch_tmap(&P.tmKd);
+      tc::prefetch_tmap(&P.tmVd);
+    }
   }
   if (warp == 2) {
     tc::tmem_alloc(tc::smem_u32(tmem_holder), 512);
@@ -121,36 +136,64 @@ __global__ void __launch_bounds__(ctxr::kThreads, 1)
   // [64, 128) of its slot) once S(u) is in registers: the S slots double as a
   // double-buffered P, and a slot is free again when PV(u) completes
 
-  // item k -> group c, row block rb, split s; its tiles [t0, t1)
-  auto item_of = [&](int k, int& c, int& rb, int& s, int& t0, int& t1) {
-    s = k % P.nsplit;
-    const int cr = k / P.nsplit;
-    rb = cr % P.nrb;
-    c = cr / P.nrb;
-    t0 = s * P.tps;
-    t1 = min(P.ntile, t0 + P.tps);
+  // item k: a context item (group c, row block rb, split s, tiles [t0, t1) of
+  // Kc[c]) or, for k >= items_ctx, the decode item of (sample i, group c):
+  // the p query rows of sample i against the tiles of Kd[i][c] (p >= 32 rows
+  // fill a useful share of the 128-row block).  L = valid
+  // positions, z = the K/V tensor map's group coordinate.
+  struct Item {
+    bool dec;
+    int c, rb, s, t0, t1, L, z, i;
+  };
+  auto item_of = [&](int k) {
+    Item it;
+    if (k < P.items_ctx) {
+      it.dec = false;
+      it.s = k % P.nsplit;
+      const int cr = k / P.nsplit;
+      it.rb = cr % P.nrb;
+      it.c = cr / P.nrb;
+      it.t0 = it.s * P.tps;
+      it.t1 = min(P.ntile, it.t0 + P.tps);
+      it.L = P.mc;
+      it.z = it.c;
+      it.i = 0;
+    } else {
+      const int j = k - P.items_ctx;
+      it.dec = true;
+      it.i = j / P.g;
+      it.c = j - it.i * P.g;
+      it.rb = 0;
+      it.s = P.dec_slot;
+      int L = P.lens[it.i];
+      L = L < 0 ? 0 : (L > P.dec_cap ? P.dec_cap : L);
+      it.L = min(L + P.lens_add, P.dec_cap);
+      it.t0 = 0;
+      it.t1 = (it.L + 127) >> 7;
+      it.z = it.i * P.g + it.c;
+    }
+    return it;
   };
 
   if (warp == 0 || warp == 3) {
     // ==================== TMA producers: K (warp 0), V (warp 3) ====================
     if (lane == 0) {
       const bool isk = warp == 0;
-      const CUtensorMap* map = isk ? &P.tmKc : &P.tmVc;
       uint64_t* full = isk ? k_full : v_full;
       uint64_t* empty = isk ? k_empty : v_empty;
       const uint64_t pol = tc::policy_evict_last();  // re-read by the other row blocks
       uint32_t u = 0;
       for (int k = blockIdx.x; k < P.items; k += gridDim.x) {
-        int c, rb, s, t0, t1;
-        item_of(k, c, rb, s, t0, t1);
-        for (int t = t0; t < t1; ++t, ++u) {
+        const Item I = item_of(k);
+        const CUtensorMap* map = I.dec ? (isk ? &P.tmKd : &P.tmVd) : (isk ? &P.tmKc : &P.tmVc);
+        for (int t = I.t0; t < I.t1; ++t, ++u) {
           const int st = u % kNst;
           tc::mbar_wait_sleep(tc::smem_u32(&empty[st]), ((u / kNst) & 1) ^ 1);
           const uint32_t bar = tc::smem_u32(&full[st]);
           tc::mbar_arrive_expect_tx(bar, kStage / 2);
           const uint32_t dst = tc::smem_u32(smem + st * kStage + (isk ? 0 : 32768));
-          tc::tma_load_3d_hint(dst, map, bar, 0, t * 128, c, pol);
-          tc::tma_load_3d_hint(dst + 16384, map, bar, 64, t * 128, c, pol);
+          tc::tma_load_3d_hint(dst, map, bar, 0, t * 128, I.z, pol);
+          tc::tma_load_3d_hint(dst + 16384, map, bar, 64, t * 128, I.z, pol);
         }
       }
     }
@@ -173,16 +216,18 @@ __global__ void __launch_bounds__(ctxr::kThreads, 1)
           for (int k = 0; k < 8; ++k) {
             // A = P from TMEM: 16 positions per step = 8 columns of bf16 pairs
             const uint64_t bd = tc::smem_desc(vb + k * 2048, 16384, 1024, tc::kSw128);
-            tc::mma_bf16_ts(tO, tS + (v & 1) * 128 + part * 64 + k * 8, bd, IDESC_PV,
-                            (first && part == 0 && k == 0) ? 0u : 1u);
+            if (!(CTXR_EXP & 4))
+              tc::mma_bf16_ts(tO, tS + (v & 1) * 128 + part * 64 + k * 8, bd, IDESC_PV,
+                              (first && part == 0 && k == 0) ? 0u : 1u);
           }
         tc::mma_commit(tc::smem_u32(p_empty));
         tc::mma_commit(tc::smem_u32(&s_free[v & 1]));
         tc::mma_commit(tc::smem_u32(&v_empty[v % kNst]));
       };
-      for (int k = blockIdx.x; k < P.items; k += gridDim.x, ++it) {
-        int c, rb, s, t0, t1;
-        item_of(k, c, rb, s, t0, t1);
+      for (int k = blockIdx.x; k < P.items; k += gridDim.x) {
+        const Item I = item_of(k);
+        if (I.t1 == I.t0) continue;  // empty decode item: the softmax threads write it
+        const int t0 = I.t0, t1 = I.t1;
         tc::mbar_wait_sleep(tc::smem_u32(q_full), it & 1);
         const uint32_t u0 = u;
         for (int t = t0; t < t1; ++t, ++u) {
@@ -196,7 +241,7 @@ __global__ void __launch_bounds__(ctxr::kThreads, 1)
                                               tc::kSw128);
             const uint64_t bd = tc::smem_desc(kb + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024,
                                               tc::kSw128);
-            tc::mma_bf16(tS + (u & 1) * 128, ad, bd, IDESC_QK, kk > 0 ? 1u : 0u);
+            if (!(CTXR_EXP & 8)) tc::mma_bf16(tS + (u & 1) * 128, ad, bd, IDESC_QK, kk > 0 ? 1u : 0u);
           }
           tc::mma_commit(tc::smem_u32(&s_full[u & 1]));
           tc::mma_commit(tc::smem_u32(&k_empty[u % kNst]));  // K(u) reusable
@@ -206,6 +251,7 @@ __global__ void __launch_bounds__(ctxr::kThreads, 1)
         }
         pv(u - 1, u - 1 == u0);
         tc::mma_commit(tc::smem_u32(o_full));
+        ++it;
       }
     }
   } else if (warp >= 4) {
@@ -222,12 +268,24 @@ __global__ void __launch_bounds__(ctxr::kThreads, 1)
     uint8_t* const sq = smem + kQ;
     float* const sm_x = reinterpret_cast<float*>(smem + kXch);
     uint32_t u = 0, it = 0;
-    for (int k = blockIdx.x; k < P.items; k += gridDim.x, ++it) {
-      int c, rb, s, t0, t1;
-      item_of(k, c, rb, s, t0, t1);
-      const int rg = rb * 128 + r;                      // row within the group
-      const bool valid_row = rg < P.R;
-      const int gr = valid_row ? (rg / P.p) * P.h + c * P.p + rg % P.p : -1;
+    for (int k = blockIdx.x; k < P.items; k += gridDim.x) {
+      const Item I = item_of(k);
+      const int c = I.c, s = I.s, t0 = I.t0, t1 = I.t1;
+      const int rg = I.rb * 128 + r;                    // row within the group (context)
+      const bool valid_row = I.dec ? r < P.p : rg < P.R;
+      const int gr = !valid_row ? -1
+                     : I.dec ? I.i * P.h + c * P.p + r
+                             : (rg / P.p) * P.h + c * P.p + rg % P.p;
+      if (t1 == t0) {
+        // empty decode item (lens = 0): an empty partial (m = -inf, l = 0, o = 0)
+        if (valid_row) {
+          float* wo = P.ws_o + ((size_t)gr * P.S + s) * 128 + hf * 64;
+#pragma unroll
+          for (int e = 0; e < 64; e += 4) *reinterpret_cast<float4*>(wo + e) = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (hf == 0) reinterpret_cast<float2*>(P.ws_ml)[(size_t)gr * P.S + s] = make_float2(kNegInf, 0.f);
+        }
+        continue;
+      }
       // ---- this half of the Q row -> shared memory (SW128, the TMA box layout) ----
       tc::mbar_wait(tc::smem_u32(q_empty), (it & 1) ^ 1);
       {
@@ -250,7 +308,7 @@ __global__ void __launch_bounds__(ctxr::kThreads, 1)
         tc::tmem_ld<32>(tS + (u & 1) * 128 + hf * 64 + 32 + lane_addr, reinterpret_cast<uint32_t*>(x) + 32);
         tc::tmem_ld_wait();
         // logits in log2 units; positions past mc masked (last tile only)
-        const int nvalid = min(128, P.mc - t * 128) - hf * 64;
+        const int nvalid = min(128, I.L - t * 128) - hf * 64;
         float mh = kNegInf;
 #pragma unroll
         for (int i = 0; i < 64; ++i) {
@@ -259,7 +317,7 @@ __global__ void __launch_bounds__(ctxr::kThreads, 1)
         }
         float* const xs = sm_x + (u & 1) * 256;
         xs[hf * 128 + r] = mh;
-        tc::named_bar_sync(1, 256);
+        if (!(CTXR_EXP & 1)) tc::named_bar_sync(1, 256);
         const float mx = fmaxf(mh, xs[(hf ^ 1) * 128 + r]);
         if (m == kNegInf || mx > m + kTh) {
           // raise the reference to the exact max; rescale l and this half of the O row
@@ -285,14 +343,14 @@ __global__ void __launch_bounds__(ctxr::kThreads, 1)
         }
         // P = 2^(x - m) as P_hi + P_lo (bf16 pairs) into TMEM: the PV's A operand
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < ((CTXR_EXP & 2) ? 0 : 4); ++j) {
           uint32_t hk[8], lk[8];
 #pragma unroll
           for (int e = 0; e < 16; e += 2) {
             const float p0 = ex2(x[j * 16 + e] - m), p1 = ex2(x[j * 16 + e + 1] - m);
             l += p0 + p1;
-            hk[e / 2] = pack_bf16x2(p0, p1);
-            lk[e / 2] = pack_bf16x2(p0 - bf16lo(hk[e / 2]), p1 - bf16hi(hk[e / 2]));
+            hk[e / 2] = pack_bf16x2_trunc(p0, p1);
+            lk[e / 2] = pack_bf16x2_trunc(p0 - bf16lo(hk[e / 2]), p1 - bf16hi(hk[e / 2]));
           }
           tc::tmem_st<8>(tS + (u & 1) * 128 + hf * 32 + j * 8 + lane_addr, hk);
           tc::tmem_st<8>(tS + (u & 1) * 128 + 64 + hf * 32 + j * 8 + lane_addr, lk);
@@ -330,6 +388,7 @@ __global__ void __launch_bounds__(ctxr::kThreads, 1)
       tc::tc_fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(tc::smem_u32(o_empty));
+      ++it;
     }
   }
   tc::tc_fence_before();

@@ -34,6 +34,7 @@ CASES = [
     (Config("ap_mha", "bf16", b=16, h=8, g=8, d=128, mc=900, md=70), 1),
     (Config("ap_gqa_n3", "bf16", b=6, h=16, g=4, d=128, mc=400, md=50), 3),
     (Config("ap_fp32", "fp32", b=4, h=4, g=2, d=64, mc=100, md=20), 2),
+    (Config("ap_mqa", "bf16", b=4, h=48, g=1, d=128, mc=300, md=40), 1),  # rows kernel + merge
 ]
 
 

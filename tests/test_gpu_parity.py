@@ -41,6 +41,8 @@ SMALL = [
     Config("rows130", "bf16", b=130, h=2, g=2, d=128, mc=1000, md=20),
     Config("gqa_rows300", "bf16", b=75, h=8, g=2, d=128, mc=700, md=30),
     Config("rows128_md0", "bf16", b=64, h=4, g=2, d=128, mc=129, md=0),
+    # p >= 32: decode items in the rows kernel too, then the light merge
+    Config("p32_rowsdec", "bf16", b=5, h=64, g=2, d=128, mc=300, md=140),
 ]
 
 
@@ -69,8 +71,10 @@ def test_stress_variants(cfg, variant, flags):
         assert torch.equal(o, o[:1].expand_as(o))
 
 
-def test_all_lens_zero_is_context_only():
-    cfg = Config("x", "bf16", b=17, h=4, g=2, d=128, mc=640, md=32)
+@pytest.mark.parametrize("cfg", [Config("x", "bf16", b=17, h=4, g=2, d=128, mc=640, md=32),
+                                 Config("p48", "bf16", b=4, h=48, g=1, d=128, mc=300, md=32)],
+                         ids=["p2", "p48"])
+def test_all_lens_zero_is_context_only(cfg):
     inp = make_inputs(cfg, 8, lens=[0] * cfg.b)
     out, lse = run_gpu(inp)
     ref, ref_lse = oracle_rows(inp)
