@@ -296,7 +296,13 @@ int make_plan(const ba_problem_t* pr_in, int sms, bool replicated, Plan* pl) {
       const char* e = getenv("BIFATTN_ROWS_DEC");
       return e ? atoi(e) : 1;
     }();
-    if (rows_dec_env && p >= 32 && p <= 128 && P.ntok == 1 && pr->md_cap >= 1) {
+    // decode items too when p >= 32 (they fill the row block) or when the
+    // decode part is small (<= 4096 tiles: C3, multi-token C2b), where a second
+    // persistent launch costs more than the half-empty row blocks (measured:
+    // C3 88.8 -> 78 us; C5's 131072 decode tiles stay in the fused kernel)
+    const long long dec_tiles = (long long)b * g * cdiv(pr->md_cap, 128);
+    if (rows_dec_env && (p >= 32 || dec_tiles <= 4096 || rows_dec_env == 2) && p <= 128 &&
+        pr->md_cap >= 1) {
       P.cr_dec = true;
       P.cr_items += b * g;
     }
@@ -724,6 +730,7 @@ int run_tc(const ba_problem_t* pr, const Plan& P, const void* q, const void* Kc,
     cp.lens = lens;
     cp.dec_cap = P.dec_cap;
     cp.lens_add = ap ? ap->n : 0;
+    cp.ntok = P.ntok;
     if (P.cr_dec) {
       const uint64_t ds = (uint64_t)P.dec_stride, bg = (uint64_t)pr->b * pr->g;
       rc = make_tmap_3d(&cp.tmKd, Kd, d, ds, bg, d * 2, ds * d * 2, 128, 1);

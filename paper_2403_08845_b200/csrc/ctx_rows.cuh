@@ -35,6 +35,8 @@ struct CtxRowsParams {
   CUtensorMap tmKd, tmVd;  // (d, md_cap, b*g), box (64, 128, 1): decode items (p >= 32)
   const int32_t* lens;     // decode items: valid length min(clamp(lens[i]) + lens_add, dec_cap)
   int dec_cap, lens_add;
+  int ntok;                // multi-token step: decode row r (token r % ntok) sees
+                           // positions < L - (ntok - 1 - r % ntok)
   int items_ctx;           // items [0, items_ctx) are context items, then b*g decode items
   int dec_slot;            // workspace slot of the decode partial
   const void* q;           // [b][h][128] bf16 (rows of group c: (i, c*p + j))
@@ -308,7 +310,8 @@ __global__ void __launch_bounds__(ctxr::kThreads, 1)
         tc::tmem_ld<32>(tS + (u & 1) * 128 + hf * 64 + 32 + lane_addr, reinterpret_cast<uint32_t*>(x) + 32);
         tc::tmem_ld_wait();
         // logits in log2 units; positions past mc masked (last tile only)
-        const int nvalid = min(128, I.L - t * 128) - hf * 64;
+        const int Lrow = I.dec && P.ntok > 1 ? max(I.L - (P.ntok - 1 - r % P.ntok), 0) : I.L;
+        const int nvalid = min(128, Lrow - t * 128) - hf * 64;
         float mh = kNegInf;
 #pragma unroll
         for (int i = 0; i < 64; ++i) {
@@ -341,13 +344,14 @@ __global__ void __launch_bounds__(ctxr::kThreads, 1)
           }
           m = mn;
         }
+        const float mref = m == kNegInf ? 0.f : m;  // a row with no valid position yet: P = 0
         // P = 2^(x - m) as P_hi + P_lo (bf16 pairs) into TMEM: the PV's A operand
 #pragma unroll
         for (int j = 0; j < ((CTXR_EXP & 2) ? 0 : 4); ++j) {
           uint32_t hk[8], lk[8];
 #pragma unroll
           for (int e = 0; e < 16; e += 2) {
-            const float p0 = ex2(x[j * 16 + e] - m), p1 = ex2(x[j * 16 + e + 1] - m);
+            const float p0 = ex2(x[j * 16 + e] - mref), p1 = ex2(x[j * 16 + e + 1] - mref);
             l += p0 + p1;
             hk[e / 2] = pack_bf16x2_trunc(p0, p1);
             lk[e / 2] = pack_bf16x2_trunc(p0 - bf16lo(hk[e / 2]), p1 - bf16hi(hk[e / 2]));

@@ -136,7 +136,6 @@ def test_split_covers_every_tile_once_and_slots_match(shape):
     if plan.startswith("ctx_rows") and "+ merge" in plan:
         # both branches in the rows kernel (p >= 32): context items + one
         # decode item per (sample, group), then the merge launch
-        assert h // g >= 32, plan
         m = re.search(r"items=(\d+)\+(\d+) dec", plan)
         assert int(m.group(2)) == b * g
         return
