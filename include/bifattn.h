@@ -73,9 +73,9 @@ enum {
                                   (tests use it to cover both kernel families)       */
 #define BA_FLAG_NO_PDL 0x2u    /* do not use programmatic dependent launch           */
 #define BA_FLAG_CTX_ROWS 0x4u  /* bf16, d = 128: run the context branch on the rows-on-M
-                                  kernel also for b*p < 128 (default: b*p >= 128)     */
+                                  kernel also for b*p < 64 (default: b*p >= 64)       */
 #define BA_FLAG_NO_CTX_ROWS 0x8u /* bf16, d = 128: keep the single fused launch (context
-                                  in 32-row passes) also for b*p >= 128 (tests cover
+                                  in 32-row passes) also for b*p >= 64 (tests cover 
                                   every path)                                         */
 
 typedef struct {

@@ -104,7 +104,7 @@ struct Plan {
   int tc_N = 0, tc_nrc = 0, tc_ntile_c = 0, tc_ntile_d = 0, tc_G = 0, tc_nst = 0, tc_npb = 1;
   int tc_Sc = 0, tc_Sd = 0, tc_smem = 0;
   int tc_bw = 0, tc_nband = 0;  // context band width (tiles), bands per group
-  // rows-on-M context kernel (ctx_rows.cuh) for R = b*p >= 128 rows per group
+  // rows-on-M context kernel (ctx_rows.cuh) for R = b*p >= 64 rows per group
   bool ctx_rows = false;
   int cr_nrb = 0, cr_ntile = 0, cr_tps = 0, cr_nsplit = 0, cr_items = 0, cr_grid = 0;
   // decode branch also in the rows kernel (p >= 32 rows per sample and group);
@@ -262,12 +262,13 @@ int make_plan(const ba_problem_t* pr_in, int sms, bool replicated, Plan* pl) {
     const char* e = getenv("BIFATTN_CTX_ROWS");
     return e ? atoi(e) : 1;
   }();
-  // Rows-on-M context kernel for R >= 128 rows per group: measured faster
+  // Rows-on-M context kernel for R >= 64 rows per group: measured faster
   // than the fused kernel's 32-row context passes on every such shape (round
   // 1: C3 104 -> 90 us, C4 163 -> 86 us, C5 2.7 -> 1.8 ms, 4-token C2b 137 ->
-  // 111 us).  BA_FLAG_CTX_ROWS forces it (any R), BA_FLAG_NO_CTX_ROWS or
+  // 111 us, 2-token C2b 86 -> 81 us); at R = 32 (C2b) it is slower (78 vs
+  // 58.7 us: a 128-row pass costs more than a 32-row swap-AB pass).  BA_FLAG_CTX_ROWS forces it (any R), BA_FLAG_NO_CTX_ROWS or
   // BIFATTN_CTX_ROWS=0 keep the single fused launch.
-  const bool want_rows = ((pr->flags & BA_FLAG_CTX_ROWS) || R >= 128) &&
+  const bool want_rows = ((pr->flags & BA_FLAG_CTX_ROWS) || R >= 64 || ctx_rows_env == 2) &&
                          !(pr->flags & BA_FLAG_NO_CTX_ROWS);
   if (tcN && !replicated && ctx_rows_env && want_rows) {
     // context branch on the rows-on-M kernel; the fused kernel streams only

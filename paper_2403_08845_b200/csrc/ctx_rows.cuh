@@ -1,5 +1,5 @@
 // ctx_rows.cuh — the CONTEXT branch of the bifurcated step for wide row sets
-// (R = b*p >= 128 query rows per KV group: C3, C4, C5, multi-token steps),
+// (R = b*p >= 64 query rows per KV group: C3, C4, C5, multi-token steps),
 // rows on the MMA's M dimension (sm_100a tcgen05 + TMEM + TMA).
 //
 // What it computes (Eq. 3-4 context rows; "axis b does

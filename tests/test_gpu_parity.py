@@ -37,7 +37,7 @@ SMALL = [
     Config("fp32_d128", "fp32", b=4, h=4, g=2, d=128, mc=300, md=17),
     Config("mc1", "bf16", b=2, h=2, g=1, d=128, mc=1, md=3),
     Config("md0", "bf16", b=4, h=4, g=4, d=128, mc=333, md=0),
-    # R = b*p >= 128: context branch on the rows-on-M kernel (ctx_rows.cuh)
+    # R = b*p >= 64: context branch on the rows-on-M kernel (ctx_rows.cuh)
     Config("rows130", "bf16", b=130, h=2, g=2, d=128, mc=1000, md=20),
     Config("gqa_rows300", "bf16", b=75, h=8, g=2, d=128, mc=700, md=30),
     Config("rows128_md0", "bf16", b=64, h=4, g=2, d=128, mc=129, md=0),
