@@ -118,8 +118,12 @@ def test_host_entry_point_equals_device_call():
     assert torch.equal(hout, out_dev.cpu())
 
 
-def test_cuda_graph_capture_and_replay():
-    cfg = Config("x", "bf16", b=16, h=8, g=8, d=128, mc=1024, md=64)
+@pytest.mark.parametrize("cfg", [Config("x", "bf16", b=16, h=8, g=8, d=128, mc=1024, md=64),
+                                 Config("rows", "bf16", b=64, h=8, g=4, d=128, mc=1024, md=64),
+                                 Config("rows_c5", "bf16", b=70, h=4, g=4, d=128, mc=1000, md=2000),
+                                 Config("rows_p48", "bf16", b=6, h=48, g=1, d=128, mc=700, md=64)],
+                         ids=["fused", "rows+dec", "rows+fused_dec", "rows_p48"])
+def test_cuda_graph_capture_and_replay(cfg):
     inp = make_inputs(cfg, 12)
     q, Kc, Vc, Kd, Vd, lens = (t.to(DEV) for t in (inp.q, inp.Kc, inp.Vc, inp.Kd, inp.Vd, inp.lens))
     out = torch.empty_like(q)
@@ -147,8 +151,10 @@ def test_cuda_graph_capture_and_replay():
     compare(out, None, ref, None, cfg.torch_dtype, "graph-lens")
 
 
-def test_repeated_calls_deterministic():
-    cfg = Config("x", "bf16", b=32, h=4, g=4, d=128, mc=2048, md=64)
+@pytest.mark.parametrize("cfg", [Config("x", "bf16", b=32, h=4, g=4, d=128, mc=2048, md=64),
+                                 Config("rows", "bf16", b=96, h=4, g=2, d=128, mc=2048, md=64)],
+                         ids=["fused", "rows"])
+def test_repeated_calls_deterministic(cfg):
     inp = make_inputs(cfg, 13)
     a, _ = run_gpu(inp)
     b_, _ = run_gpu(inp)
