@@ -19,7 +19,7 @@
 // per row — no vote across the rows of a column as in the swap-AB kernel.  P = P_hi + P_lo
 // (two bf16 parts, ~16 significant bits, reading R13) is stored to TMEM and
 // read from there as the PV's A operand; both parts accumulate into the same
-// fp32 O.  TMEM: S x2 (256 cols; P(u) overwrites S(u)), O (128).
+// fp32 O.  TMEM: 3 S slots (P(u) overwrites S(u)) + O = 512 columns.
 //
 // Warps: 0 / 3 TMA producers of the K / V halves (one lane each), 1 MMA
 // issuer (one lane), 2 TMEM allocator, 4..11 softmax/epilogue: two threads
@@ -59,6 +59,7 @@ struct CtxRowsParams {
 namespace ctxr {
 constexpr int kStage = 65536;           // K tile 32 KB + V tile 32 KB
 constexpr int kNst = 3;                 // K/V stages
+constexpr int kS = 3;                   // S/P slots in TMEM (3 x 128 columns + O = 512)
 constexpr int kQ = kNst * kStage;       // Q block (32 KB)
 constexpr int kBar = kQ + 32768;        // barriers
 constexpr int kXch = kBar + 256;        // row-max exchange [2 tiles][2 halves][128 rows] floats
@@ -82,17 +83,17 @@ __global__ void __launch_bounds__(ctxr::kThreads, 1)
   // QK(u), V(u) by PV(u), so the next K load does not wait for the PV
   uint64_t* k_full = bars;        // [kNst]
   uint64_t* k_empty = bars + 3;   // [kNst]
-  uint64_t* s_full = bars + 6;    // [2]
-  uint64_t* s_free = bars + 8;    // [2]
-  uint64_t* q_full = bars + 10;
-  uint64_t* q_empty = bars + 11;
-  uint64_t* p_empty = bars + 13;  // PV(u) done (O quiescent for a rescale)
-  uint64_t* o_full = bars + 14;
-  uint64_t* o_empty = bars + 15;
-  uint64_t* v_full = bars + 16;   // [kNst]
-  uint64_t* v_empty = bars + 19;  // [kNst]
-  uint64_t* p_full = bars + 22;   // [2] P(u) stored over S(u)
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 24);
+  uint64_t* s_full = bars + 6;    // [kS]
+  uint64_t* s_free = bars + 9;    // [kS]
+  uint64_t* q_full = bars + 12;
+  uint64_t* q_empty = bars + 13;
+  uint64_t* p_empty = bars + 14;  // PV(u) done (O quiescent for a rescale)
+  uint64_t* o_full = bars + 15;
+  uint64_t* o_empty = bars + 16;
+  uint64_t* v_full = bars + 17;   // [kNst]
+  uint64_t* v_empty = bars + 20;  // [kNst]
+  uint64_t* p_full = bars + 23;   // [kS] P(u) stored over S(u)
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 26);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
@@ -102,7 +103,7 @@ __global__ void __launch_bounds__(ctxr::kThreads, 1)
       tc::mbar_init(tc::smem_u32(&v_full[s]), 1);
       tc::mbar_init(tc::smem_u32(&v_empty[s]), 1);
     }
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < kS; ++s) {
       tc::mbar_init(tc::smem_u32(&s_full[s]), 1);
       tc::mbar_init(tc::smem_u32(&s_free[s]), 1);  // PV(u) done: slot reusable
       tc::mbar_init(tc::smem_u32(&p_full[s]), 8);
@@ -133,7 +134,7 @@ __global__ void __launch_bounds__(ctxr::kThreads, 1)
   pdl_launch_dependents();
   const uint32_t tmem = *tmem_holder;
   const uint32_t tS = tmem;        // S buffers at columns [0,128), [128,256)
-  const uint32_t tO = tmem + 256;  // O at [256, 384)
+  const uint32_t tO = tmem + kS * 128;  // O after the kS S/P slots
   // P(u) = P_hi | P_lo as bf16 pairs is stored over S(u) (columns [0, 64) and
   // [64, 128) of its slot) once S(u) is in registers: the S slots double as a
   // double-buffered P, and a slot is free again when PV(u) completes
@@ -209,7 +210,7 @@ __global__ void __launch_bounds__(ctxr::kThreads, 1)
       // O += P(v) . V(v): both bf16 parts of P into the same accumulator
       auto pv = [&](uint32_t v, bool first) {
         tc::mbar_wait_sleep(tc::smem_u32(&v_full[v % kNst]), (v / kNst) & 1);
-        tc::mbar_wait_sleep(tc::smem_u32(&p_full[v & 1]), (v >> 1) & 1);
+        tc::mbar_wait_sleep(tc::smem_u32(&p_full[v % kS]), (v / kS) & 1);
         tc::tc_fence_after();
         const uint32_t vb = tc::smem_u32(smem + (v % kNst) * kStage + 32768);
 #pragma unroll
@@ -219,11 +220,11 @@ __global__ void __launch_bounds__(ctxr::kThreads, 1)
             // A = P from TMEM: 16 positions per step = 8 columns of bf16 pairs
             const uint64_t bd = tc::smem_desc(vb + k * 2048, 16384, 1024, tc::kSw128);
             if (!(CTXR_EXP & 4))
-              tc::mma_bf16_ts(tO, tS + (v & 1) * 128 + part * 64 + k * 8, bd, IDESC_PV,
+              tc::mma_bf16_ts(tO, tS + (v % kS) * 128 + part * 64 + k * 8, bd, IDESC_PV,
                               (first && part == 0 && k == 0) ? 0u : 1u);
           }
         tc::mma_commit(tc::smem_u32(p_empty));
-        tc::mma_commit(tc::smem_u32(&s_free[v & 1]));
+        tc::mma_commit(tc::smem_u32(&s_free[v % kS]));
         tc::mma_commit(tc::smem_u32(&v_empty[v % kNst]));
       };
       for (int k = blockIdx.x; k < P.items; k += gridDim.x) {
@@ -234,7 +235,7 @@ __global__ void __launch_bounds__(ctxr::kThreads, 1)
         const uint32_t u0 = u;
         for (int t = t0; t < t1; ++t, ++u) {
           tc::mbar_wait_sleep(tc::smem_u32(&k_full[u % kNst]), (u / kNst) & 1);
-          tc::mbar_wait_sleep(tc::smem_u32(&s_free[u & 1]), ((u >> 1) & 1) ^ 1);
+          tc::mbar_wait_sleep(tc::smem_u32(&s_free[u % kS]), ((u / kS) & 1) ^ 1);
           tc::tc_fence_after();
           const uint32_t kb = tc::smem_u32(smem + (u % kNst) * kStage);
 #pragma unroll
@@ -243,9 +244,9 @@ __global__ void __launch_bounds__(ctxr::kThreads, 1)
                                               tc::kSw128);
             const uint64_t bd = tc::smem_desc(kb + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024,
                                               tc::kSw128);
-            if (!(CTXR_EXP & 8)) tc::mma_bf16(tS + (u & 1) * 128, ad, bd, IDESC_QK, kk > 0 ? 1u : 0u);
+            if (!(CTXR_EXP & 8)) tc::mma_bf16(tS + (u % kS) * 128, ad, bd, IDESC_QK, kk > 0 ? 1u : 0u);
           }
-          tc::mma_commit(tc::smem_u32(&s_full[u & 1]));
+          tc::mma_commit(tc::smem_u32(&s_full[u % kS]));
           tc::mma_commit(tc::smem_u32(&k_empty[u % kNst]));  // K(u) reusable
           if (t == t1 - 1) tc::mma_commit(tc::smem_u32(q_empty));  // Q block reusable
           if (u > u0) pv(u - 1, u - 1 == u0);
@@ -303,11 +304,11 @@ __global__ void __launch_bounds__(ctxr::kThreads, 1)
       if (lane == 0) tc::mbar_arrive(tc::smem_u32(q_full));
       float m = kNegInf, l = 0.f;  // l: this half's share of the row sum
       for (int t = t0; t < t1; ++t, ++u) {
-        tc::mbar_wait(tc::smem_u32(&s_full[u & 1]), (u >> 1) & 1);
+        tc::mbar_wait(tc::smem_u32(&s_full[u % kS]), (u / kS) & 1);
         tc::tc_fence_after();
         float x[64];
-        tc::tmem_ld<32>(tS + (u & 1) * 128 + hf * 64 + lane_addr, reinterpret_cast<uint32_t*>(x));
-        tc::tmem_ld<32>(tS + (u & 1) * 128 + hf * 64 + 32 + lane_addr, reinterpret_cast<uint32_t*>(x) + 32);
+        tc::tmem_ld<32>(tS + (u % kS) * 128 + hf * 64 + lane_addr, reinterpret_cast<uint32_t*>(x));
+        tc::tmem_ld<32>(tS + (u % kS) * 128 + hf * 64 + 32 + lane_addr, reinterpret_cast<uint32_t*>(x) + 32);
         tc::tmem_ld_wait();
         // logits in log2 units; positions past mc masked (last tile only)
         const int Lrow = I.dec && P.ntok > 1 ? max(I.L - (P.ntok - 1 - r % P.ntok), 0) : I.L;
@@ -356,13 +357,13 @@ __global__ void __launch_bounds__(ctxr::kThreads, 1)
             hk[e / 2] = pack_bf16x2_trunc(p0, p1);
             lk[e / 2] = pack_bf16x2_trunc(p0 - bf16lo(hk[e / 2]), p1 - bf16hi(hk[e / 2]));
           }
-          tc::tmem_st<8>(tS + (u & 1) * 128 + hf * 32 + j * 8 + lane_addr, hk);
-          tc::tmem_st<8>(tS + (u & 1) * 128 + 64 + hf * 32 + j * 8 + lane_addr, lk);
+          tc::tmem_st<8>(tS + (u % kS) * 128 + hf * 32 + j * 8 + lane_addr, hk);
+          tc::tmem_st<8>(tS + (u % kS) * 128 + 64 + hf * 32 + j * 8 + lane_addr, lk);
         }
         tc::tmem_st_wait();
         tc::tc_fence_before();
         __syncwarp();
-        if (lane == 0) tc::mbar_arrive(tc::smem_u32(&p_full[u & 1]));
+        if (lane == 0) tc::mbar_arrive(tc::smem_u32(&p_full[u % kS]));
       }
       // ---- the item's partial: O row (relative to 2^m), m, l ----
       tc::mbar_wait(tc::smem_u32(o_full), it & 1);
