@@ -202,3 +202,28 @@ def test_full_size_sampled_rows(name):
     assert torch.isfinite(out.float()).all()
     vmax = max(inp.Vc.float().abs().max().item(), inp.Vd.float().abs().max().item())
     assert out.float().abs().max().item() <= vmax * (1 + 1e-2)
+
+
+# ---------------------------------------------------------------------------
+# Seeded random shapes across every plan (fused / rows + decode items / rows +
+# fused decode): odd p, ragged tails, small caps, lens from 0 to the cap
+# ---------------------------------------------------------------------------
+def _random_shapes(n=14, seed=2024):
+    rng = np.random.default_rng(seed)
+    shapes = []
+    for k in range(n):
+        p = int(rng.choice([1, 2, 3, 4, 6, 8, 12, 16, 48]))
+        g = int(rng.choice([1, 2, 3])) if p >= 12 else int(rng.choice([1, 2, 4, 5]))
+        b = int(rng.integers(1, 150 // p + 3))
+        mc = int(rng.integers(1, 1500))
+        md = int(rng.integers(0, 700))
+        shapes.append(Config(f"rand{k}_p{p}", "bf16", b=b, h=g * p, g=g, d=128, mc=mc, md=md))
+    return shapes
+
+
+@pytest.mark.parametrize("cfg", _random_shapes(), ids=lambda c: c.name)
+def test_random_shapes_all_rows(cfg):
+    inp = make_inputs(cfg, 99, variant="ragged" if cfg.md > 0 else "normal")
+    out, lse = run_gpu(inp)
+    ref, ref_lse = oracle_rows(inp)
+    compare(out, lse, ref, ref_lse, cfg.torch_dtype, f"{cfg.name} {ba.ba_plan_string(ba.make_problem(cfg.b, cfg.h, cfg.g, cfg.d, cfg.mc, cfg.md, cfg.torch_dtype))[:40]}")
