@@ -727,6 +727,7 @@ int run_tc(const ba_problem_t* pr, const Plan& P, const void* q, const void* Kc,
     cp.scale_log2 = scale_log2;
     cp.S = P.S;
     cp.items_ctx = P.cr_items_ctx;
+    cp.trace = static_cast<unsigned long long*>(g_trace);
     cp.dec_slot = P.cr_nsplit;
     cp.lens = lens;
     cp.dec_cap = P.dec_cap;

@@ -39,6 +39,7 @@ struct CtxRowsParams {
                            // positions < L - (ntok - 1 - r % ntok)
   int items_ctx;           // items [0, items_ctx) are context items, then b*g decode items
   int dec_slot;            // workspace slot of the decode partial
+  unsigned long long* trace;  // BIFATTN_PROF builds: per-role cycle accounting [grid][1024]
   const void* q;           // [b][h][128] bf16 (rows of group c: (i, c*p + j))
   int b, h, g, p, mc;
   int R, nrb;              // rows per group, 128-row blocks per group
@@ -208,9 +209,13 @@ __global__ void __launch_bounds__(ctxr::kThreads, 1)
       const uint32_t qbase = tc::smem_u32(smem + kQ);
       uint32_t u = 0, it = 0;
       // O += P(v) . V(v): both bf16 parts of P into the same accumulator
+      Prof pf;  // 0 q_full, 1 k_full, 2 s_free, 3 QK issue, 4 v_full, 5 p_full, 6 PV issue, 7 o_empty
       auto pv = [&](uint32_t v, bool first) {
+        pf.mark(3);
         tc::mbar_wait_sleep(tc::smem_u32(&v_full[v % kNst]), (v / kNst) & 1);
+        pf.mark(4);
         tc::mbar_wait_sleep(tc::smem_u32(&p_full[v % kS]), (v / kS) & 1);
+        pf.mark(5);
         tc::tc_fence_after();
         const uint32_t vb = tc::smem_u32(smem + (v % kNst) * kStage + 32768);
 #pragma unroll
@@ -226,16 +231,21 @@ __global__ void __launch_bounds__(ctxr::kThreads, 1)
         tc::mma_commit(tc::smem_u32(p_empty));
         tc::mma_commit(tc::smem_u32(&s_free[v % kS]));
         tc::mma_commit(tc::smem_u32(&v_empty[v % kNst]));
+        pf.mark(6);
       };
       for (int k = blockIdx.x; k < P.items; k += gridDim.x) {
         const Item I = item_of(k);
         if (I.t1 == I.t0) continue;  // empty decode item: the softmax threads write it
         const int t0 = I.t0, t1 = I.t1;
+        pf.mark(3);
         tc::mbar_wait_sleep(tc::smem_u32(q_full), it & 1);
+        pf.mark(0);
         const uint32_t u0 = u;
         for (int t = t0; t < t1; ++t, ++u) {
           tc::mbar_wait_sleep(tc::smem_u32(&k_full[u % kNst]), (u / kNst) & 1);
+          pf.mark(1);
           tc::mbar_wait_sleep(tc::smem_u32(&s_free[u % kS]), ((u / kS) & 1) ^ 1);
+          pf.mark(2);
           tc::tc_fence_after();
           const uint32_t kb = tc::smem_u32(smem + (u % kNst) * kStage);
 #pragma unroll
@@ -250,12 +260,18 @@ __global__ void __launch_bounds__(ctxr::kThreads, 1)
           tc::mma_commit(tc::smem_u32(&k_empty[u % kNst]));  // K(u) reusable
           if (t == t1 - 1) tc::mma_commit(tc::smem_u32(q_empty));  // Q block reusable
           if (u > u0) pv(u - 1, u - 1 == u0);
-          else tc::mbar_wait_sleep(tc::smem_u32(o_empty), (it & 1) ^ 1);  // O drained
+          else {
+            pf.mark(3);
+            tc::mbar_wait_sleep(tc::smem_u32(o_empty), (it & 1) ^ 1);  // O drained
+            pf.mark(7);
+          }
         }
         pv(u - 1, u - 1 == u0);
         tc::mma_commit(tc::smem_u32(o_full));
         ++it;
       }
+      pf.mark(3);
+      pf.dump(P.trace ? P.trace + (size_t)blockIdx.x * 1024 : nullptr, 8);
     }
   } else if (warp >= 4) {
     // ============ softmax + epilogue: two threads per row (one per half) ============
@@ -271,6 +287,7 @@ __global__ void __launch_bounds__(ctxr::kThreads, 1)
     uint8_t* const sq = smem + kQ;
     float* const sm_x = reinterpret_cast<float*>(smem + kXch);
     uint32_t u = 0, it = 0;
+    Prof pf;  // 0 Q load, 1 s_full wait, 2 S load, 3 max, 4 exchange barrier, 5 rescale, 6 P, 7 epilogue
     for (int k = blockIdx.x; k < P.items; k += gridDim.x) {
       const Item I = item_of(k);
       const int c = I.c, s = I.s, t0 = I.t0, t1 = I.t1;
@@ -303,13 +320,16 @@ __global__ void __launch_bounds__(ctxr::kThreads, 1)
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(tc::smem_u32(q_full));
       float m = kNegInf, l = 0.f;  // l: this half's share of the row sum
+      pf.mark(0);
       for (int t = t0; t < t1; ++t, ++u) {
         tc::mbar_wait(tc::smem_u32(&s_full[u % kS]), (u / kS) & 1);
+        pf.mark(1);
         tc::tc_fence_after();
         float x[64];
         tc::tmem_ld<32>(tS + (u % kS) * 128 + hf * 64 + lane_addr, reinterpret_cast<uint32_t*>(x));
         tc::tmem_ld<32>(tS + (u % kS) * 128 + hf * 64 + 32 + lane_addr, reinterpret_cast<uint32_t*>(x) + 32);
         tc::tmem_ld_wait();
+        pf.mark(2);
         // logits in log2 units; positions past mc masked (last tile only)
         const int Lrow = I.dec && P.ntok > 1 ? max(I.L - (P.ntok - 1 - r % P.ntok), 0) : I.L;
         const int nvalid = min(128, Lrow - t * 128) - hf * 64;
@@ -319,10 +339,12 @@ __global__ void __launch_bounds__(ctxr::kThreads, 1)
           x[i] = i < nvalid ? x[i] * sl2 : kNegInf;
           mh = fmaxf(mh, x[i]);
         }
+        pf.mark(3);
         float* const xs = sm_x + (u & 1) * 256;
         xs[hf * 128 + r] = mh;
         if (!(CTXR_EXP & 1)) tc::named_bar_sync(1, 256);
         const float mx = fmaxf(mh, xs[(hf ^ 1) * 128 + r]);
+        pf.mark(4);
         if (m == kNegInf || mx > m + kTh) {
           // raise the reference to the exact max; rescale l and this half of the O row
           const float mn = mx;
@@ -345,6 +367,7 @@ __global__ void __launch_bounds__(ctxr::kThreads, 1)
           }
           m = mn;
         }
+        pf.mark(5);
         const float mref = m == kNegInf ? 0.f : m;  // a row with no valid position yet: P = 0
         // P = 2^(x - m) as P_hi + P_lo (bf16 pairs) into TMEM: the PV's A operand
 #pragma unroll
@@ -364,6 +387,7 @@ __global__ void __launch_bounds__(ctxr::kThreads, 1)
         tc::tc_fence_before();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(tc::smem_u32(&p_full[u % kS]));
+        pf.mark(6);
       }
       // ---- the item's partial: O row (relative to 2^m), m, l ----
       tc::mbar_wait(tc::smem_u32(o_full), it & 1);
@@ -394,7 +418,9 @@ __global__ void __launch_bounds__(ctxr::kThreads, 1)
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(tc::smem_u32(o_empty));
       ++it;
+      pf.mark(7);
     }
+    if (threadIdx.x == 128) pf.dump(P.trace ? P.trace + (size_t)blockIdx.x * 1024 : nullptr, 0);
   }
   tc::tc_fence_before();
   __syncthreads();
