@@ -187,7 +187,10 @@ int ba_lse_merge(int n_parts, int rows, int d, int dtype, const void* out_parts,
 
 /* Number of kernel launches one bifurcated_attn_decode() call makes for this
  * problem on the current device (for the benchmark's launch count): 1 for the
- * tensor-core plan (one cooperative launch), 3 for the CUDA-core plan. */
+ * fused tensor-core plan (one cooperative launch, b*p < 64 rows per group), 2
+ * for the rows-on-M plan (rows kernel + merge, or rows kernel + fused decode
+ * launch), 3 for the CUDA-core plan.  bifurcated_attn_decode_append adds one
+ * (the append kernel). */
 int ba_launches_per_call(const ba_problem_t* prob);
 
 /* Human-readable kernel plan for this problem (static string owned by the
@@ -195,7 +198,8 @@ int ba_launches_per_call(const ba_problem_t* prob);
 const char* ba_plan_string(const ba_problem_t* prob);
 
 /* Name of kernel launch k (0-based, in launch order) of one call for this
- * problem, e.g. "ctx_tc", "dec_fma", "merge" (static string), or NULL. */
+ * problem, e.g. "fused_tc", "fused_rows", "ctx_rows", "dec_tc_merge",
+ * "ctx_fma", "dec_fma", "merge" (static string), or NULL. */
 const char* ba_launch_name(const ba_problem_t* prob, int k);
 
 /* Instrumentation for the benchmark's per-kernel CUDA-event timing.  While
