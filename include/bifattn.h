@@ -148,6 +148,21 @@ int bifurcated_attn_decode_append(const ba_problem_t* prob, const void* q, const
                                   void* Vd, int32_t* lens, void* out, float* lse,
                                   void* workspace, size_t workspace_bytes, void* stream);
 
+/* One serving step with HOST inputs and outputs, the caches resident on the
+ * device: copies this step's q, k_new, v_new (and lens, if hlens != NULL;
+ * otherwise the device lens carries on from the previous step) from host
+ * memory (pinned for async behaviour) into dq, dk_new, dv_new, dlens, runs
+ * bifurcated_attn_decode_append (appends the rows, attends, advances dlens),
+ * and copies out (and lse if hlse and dlse) back.  All on `stream`; returns
+ * after enqueueing. */
+int bifurcated_attn_decode_append_host(const ba_problem_t* prob, const void* hq,
+                                       const void* hk_new, const void* hv_new,
+                                       const int32_t* hlens, void* hout, float* hlse, void* dq,
+                                       void* dk_new, void* dv_new, const void* Kc, const void* Vc,
+                                       void* Kd, void* Vd, int32_t* dlens, void* dout,
+                                       float* dlse, void* workspace, size_t workspace_bytes,
+                                       void* stream);
+
 /* The same step with HOST inputs and outputs (end-to-end entry point): copies
  * q, Kc, Vc, Kd, Vd, lens from host memory (pinned for async behaviour) into
  * the caller-owned device buffers dq..dlens, runs bifurcated_attn_decode, and

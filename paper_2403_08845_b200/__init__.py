@@ -32,7 +32,7 @@ ERRORS = {0: "BA_OK", -1: "BA_EINVAL", -2: "BA_ENULL", -3: "BA_EALIGN", -4: "BA_
           -5: "BA_EDTYPE", -6: "BA_ENODEV", -7: "BA_ECUDA"}
 
 EXPORTED = ["ba_workspace_bytes", "bifurcated_attn_decode", "bifurcated_attn_decode_host",
-            "bifurcated_attn_decode_append", "ba_lse_merge",
+            "bifurcated_attn_decode_append", "bifurcated_attn_decode_append_host", "ba_lse_merge",
             "replicated_attn_decode", "ba_launches_per_call", "ba_plan_string", "ba_strerror",
             "ba_last_cuda_error", "ba_version", "ba_launch_name", "ba_set_launch_events",
             "ba_set_trace_buffer", "ba_plan_ctas"]
@@ -68,6 +68,8 @@ def load_library(path: str = LIB_PATH):
     lib.bifurcated_attn_decode_host.restype = ctypes.c_int
     lib.bifurcated_attn_decode_append.argtypes = [pp] + [P] * 11 + [ctypes.c_size_t, P]
     lib.bifurcated_attn_decode_append.restype = ctypes.c_int
+    lib.bifurcated_attn_decode_append_host.argtypes = [pp] + [P] * 17 + [ctypes.c_size_t, P]
+    lib.bifurcated_attn_decode_append_host.restype = ctypes.c_int
     lib.ba_lse_merge.argtypes = [ctypes.c_int] * 4 + [P] * 5
     lib.ba_lse_merge.restype = ctypes.c_int
     lib.replicated_attn_decode.argtypes = [pp] + [P] * 7 + [ctypes.c_size_t, P]
@@ -305,6 +307,25 @@ def bifurcated_attn_decode_append(q, k_new, v_new, Kc, Vc, Kd, Vd, lens, out=Non
     if rc != 0:
         raise BifAttnError(rc, "bifurcated_attn_decode_append")
     return out
+
+
+def bifurcated_attn_decode_append_host(hq, hk_new, hv_new, hout, dev, *, hlens=None, hlse=None,
+                                       scale=None, stream=None, flags=0):
+    """One serving step with host tensors in and out (include/bifattn.h):
+    ``dev`` holds the resident caches and staging buffers {q, k_new, v_new,
+    Kc, Vc, Kd, Vd, lens, out, lse?, workspace}.  Synchronise before reading
+    ``hout``."""
+    lib = _lib if _lib is not None else load_library()
+    prob = _cached_problem(hq, dev["Kc"], dev["Kd"], scale, flags)
+    ws = dev["workspace"]
+    rc = lib.bifurcated_attn_decode_append_host(
+        ctypes.byref(prob), _ptr(hq), _ptr(hk_new), _ptr(hv_new), _ptr(hlens), _ptr(hout),
+        _ptr(hlse), _ptr(dev["q"]), _ptr(dev["k_new"]), _ptr(dev["v_new"]), _ptr(dev["Kc"]),
+        _ptr(dev["Vc"]), _ptr(dev["Kd"]), _ptr(dev["Vd"]), _ptr(dev["lens"]), _ptr(dev["out"]),
+        _ptr(dev.get("lse")), _ptr(ws), ws.numel(), _stream_handle(stream))
+    if rc != 0:
+        raise BifAttnError(rc, "bifurcated_attn_decode_append_host")
+    return hout
 
 
 def lse_merge(out_parts, lse_parts, out=None, lse=None, *, stream=None):

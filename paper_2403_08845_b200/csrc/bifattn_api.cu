@@ -1007,6 +1007,48 @@ int bifurcated_attn_decode_append(const ba_problem_t* prob, const void* q, const
   return run_d<float>(&E, P, q, Kc, Vc, Kd, Vd, lens, out, lse, workspace, st, &ap);
 }
 
+int bifurcated_attn_decode_append_host(const ba_problem_t* prob, const void* hq,
+                                       const void* hk_new, const void* hv_new,
+                                       const int32_t* hlens, void* hout, float* hlse, void* dq,
+                                       void* dk_new, void* dv_new, const void* Kc, const void* Vc,
+                                       void* Kd, void* Vd, int32_t* dlens, void* dout,
+                                       float* dlse, void* workspace, size_t workspace_bytes,
+                                       void* stream) {
+  int rc = validate(prob);
+  if (rc) return rc;
+  if (!hq || !hk_new || !hv_new || !hout) return BA_ENULL;
+  DevInfo di;
+  rc = device_info(&di);
+  if (rc) return rc;
+  const size_t e = prob->dtype == BA_BF16 ? 2 : 4;
+  const size_t d = prob->d, n = ntok_of(prob);
+  const size_t nq = (size_t)prob->b * prob->h * n * d * e;
+  const size_t nkv = (size_t)prob->b * prob->g * n * d * e;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  auto cp = [&](void* dst, const void* src, size_t bytes, cudaMemcpyKind k) -> int {
+    if (bytes == 0) return BA_OK;
+    if (!dst) return BA_ENULL;
+    const cudaError_t ce = cudaMemcpyAsync(dst, src, bytes, k, st);
+    if (ce != cudaSuccess) {
+      g_last_cuda_error = (int)ce;
+      return BA_ECUDA;
+    }
+    return BA_OK;
+  };
+  if ((rc = cp(dq, hq, nq, cudaMemcpyHostToDevice))) return rc;
+  if ((rc = cp(dk_new, hk_new, nkv, cudaMemcpyHostToDevice))) return rc;
+  if ((rc = cp(dv_new, hv_new, nkv, cudaMemcpyHostToDevice))) return rc;
+  if (hlens && (rc = cp(dlens, hlens, (size_t)prob->b * sizeof(int32_t), cudaMemcpyHostToDevice)))
+    return rc;
+  rc = bifurcated_attn_decode_append(prob, dq, dk_new, dv_new, Kc, Vc, Kd, Vd, dlens, dout, dlse,
+                                     workspace, workspace_bytes, stream);
+  if (rc) return rc;
+  if ((rc = cp(hout, dout, nq, cudaMemcpyDeviceToHost))) return rc;
+  if (hlse && dlse)
+    return cp(hlse, dlse, (size_t)prob->b * prob->h * n * sizeof(float), cudaMemcpyDeviceToHost);
+  return BA_OK;
+}
+
 int replicated_attn_decode(const ba_problem_t* prob, const void* q, const void* K,
                            const void* V, const int32_t* lens, void* out, float* lse,
                            void* workspace, size_t workspace_bytes, void* stream) {

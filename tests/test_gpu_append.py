@@ -99,3 +99,39 @@ def test_append_steps_in_a_cuda_graph():
         assert torch.equal(lens.cpu(), host.lens), it
         ref, _ = oracle_rows(host)
         compare(out, None, ref, None, cfg.torch_dtype, f"graph-step{it}")
+
+
+def test_append_host_entry_equals_device_call():
+    """bifurcated_attn_decode_append_host (host q/k_new/v_new in, host out back,
+    caches resident) gives the device call's result bit for bit, and with
+    hlens = None the device lens carries over between steps."""
+    cfg = Config("x", "bf16", b=8, h=4, g=4, d=128, mc=500, md=30)
+    inp = make_inputs(cfg, 47, lens=[3, 0, 10, 20, 28, 29, 1, 5])
+    gen = torch.Generator().manual_seed(8)
+    kn = torch.randn(cfg.b, cfg.g, 1, cfg.d, generator=gen).to(torch.bfloat16)
+    vn = torch.randn(cfg.b, cfg.g, 1, cfg.d, generator=gen).to(torch.bfloat16)
+    # device reference: two steps
+    Kd, Vd, lens = inp.Kd.to(DEV), inp.Vd.to(DEV), inp.lens.to(DEV)
+    ref = []
+    for _ in range(2):
+        ref.append(ba.bifurcated_attn_decode_append(inp.q.to(DEV), kn.to(DEV), vn.to(DEV),
+                                                    inp.Kc.to(DEV), inp.Vc.to(DEV), Kd, Vd, lens,
+                                                    scale=inp.scale).cpu())
+    # host entry: lens given on the first step only
+    prob = ba.make_problem(cfg.b, cfg.h, cfg.g, cfg.d, cfg.mc, cfg.md, torch.bfloat16, inp.scale)
+    dev = dict(q=torch.empty(inp.q.shape, dtype=torch.bfloat16, device=DEV),
+               k_new=torch.empty(kn.shape, dtype=torch.bfloat16, device=DEV),
+               v_new=torch.empty(vn.shape, dtype=torch.bfloat16, device=DEV),
+               Kc=inp.Kc.to(DEV), Vc=inp.Vc.to(DEV), Kd=inp.Kd.to(DEV), Vd=inp.Vd.to(DEV),
+               lens=torch.empty(cfg.b, dtype=torch.int32, device=DEV),
+               out=torch.empty(inp.q.shape, dtype=torch.bfloat16, device=DEV),
+               workspace=ba.alloc_workspace(prob, DEV))
+    pin = lambda t: t.contiguous().pin_memory()  # noqa: E731
+    hq, hkn, hvn, hl = pin(inp.q), pin(kn), pin(vn), pin(inp.lens)
+    for step in range(2):
+        hout = torch.empty_like(hq).pin_memory()
+        ba.bifurcated_attn_decode_append_host(hq, hkn, hvn, hout, dev,
+                                              hlens=hl if step == 0 else None, scale=inp.scale)
+        torch.cuda.synchronize()
+        assert torch.equal(hout, ref[step]), step
+    assert torch.equal(dev["lens"].cpu(), lens.cpu())
