@@ -292,6 +292,24 @@ def run_ours(args, cfg):
             rep = {"us_per_step": rep_ms * 1e3, "kv_bytes_moved": rep_bytes,
                    "gbs_of_its_bytes": rep_bytes / (rep_ms * 1e-3) / 1e9,
                    "speedup_bifurcated_over_replicated": rep_ms / (t_ms / args.steps)}
+            # library reference on the same replicated cache (SURVEY §8(d)
+            # baseline 2): torch SDPA (its own fused kernels), uniform lens only
+            if bool((s.lens == cfg.md).all()):
+                qs = s.q.unsqueeze(2)  # [b, h, 1, d]
+                sdpa = lambda: torch.nn.functional.scaled_dot_product_attention(  # noqa: E731
+                    qs, K, V, scale=s.scale, enable_gqa=cfg.g != cfg.h)
+                with torch.cuda.stream(stream):
+                    for _ in range(3):
+                        sdpa()
+                    torch.cuda.synchronize()
+                    r0.record(stream)
+                    for _ in range(nrep):
+                        sdpa()
+                    r1.record(stream)
+                torch.cuda.synchronize()
+                sd_ms = r0.elapsed_time(r1) / nrep
+                rep["torch_sdpa_us_per_step"] = sd_ms * 1e3
+                rep["speedup_bifurcated_over_torch_sdpa"] = sd_ms / (t_ms / args.steps)
             del K, V
         except torch.cuda.OutOfMemoryError:
             rep = {"oom": True}
