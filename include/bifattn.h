@@ -235,6 +235,15 @@ void ba_set_launch_events(void* const* events, int n);
  * NULL disables. */
 void ba_set_trace_buffer(void* dev_buf);
 
+/* Measurement instrumentation (not part of the attention step): one launch
+ * of a read-only streaming kernel over `bytes` of device memory at `buf`
+ * (16-byte aligned): 128-bit non-caching loads, 4 per thread in flight,
+ * 4 CTAs of 512 threads per SM, XOR-folded so the loads cannot be elided
+ * (`sink`: device uint32, written only on a magic fold value).  bench.py
+ * times it with CUDA events (best of 10 over 2 GiB) as the read-only HBM
+ * peak of the run.  Returns BA_OK or a BA_E* code. */
+int ba_stream_read_bench(const void* buf, size_t bytes, void* sink, void* stream);
+
 /* Work split of the tensor-core plan for this problem (bf16, d = 128): CTA k
  * streams flat tiles [cs[k], cs[k+1]) of [context tiles | decode tiles]
  * (128 positions each).  Writes min(cap, G + 1) entries to cs (nullable) and

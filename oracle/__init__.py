@@ -32,9 +32,17 @@ OR_BF16, OR_FP32 = 0, 1
 
 def build(force: bool = False) -> str:
     """Compile oracle.c with gcc (-O2, OpenMP over rows, no CUDA)."""
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        subprocess.check_call(
-            ["gcc", "-O2", "-fopenmp", "-shared", "-fPIC", "-Wall", "-o", _LIB, _SRC, "-lm"])
+    import hashlib
+
+    cmd = ["gcc", "-O2", "-fopenmp", "-shared", "-fPIC", "-Wall", "-o", _LIB, _SRC, "-lm"]
+    with open(_SRC, "rb") as f:
+        digest = hashlib.sha256(f.read() + " ".join(cmd).encode()).hexdigest()
+    stamp = _LIB + ".srchash"
+    fresh = os.path.exists(_LIB) and os.path.exists(stamp) and open(stamp).read().strip() == digest
+    if force or not fresh:
+        subprocess.check_call(cmd)
+        with open(stamp, "w") as f:
+            f.write(digest + "\n")
     return _LIB
 
 

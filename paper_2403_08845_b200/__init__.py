@@ -35,7 +35,7 @@ EXPORTED = ["ba_workspace_bytes", "bifurcated_attn_decode", "bifurcated_attn_dec
             "bifurcated_attn_decode_append", "bifurcated_attn_decode_append_host", "ba_lse_merge",
             "replicated_attn_decode", "ba_launches_per_call", "ba_plan_string", "ba_strerror",
             "ba_last_cuda_error", "ba_version", "ba_launch_name", "ba_set_launch_events",
-            "ba_set_trace_buffer", "ba_plan_ctas"]
+            "ba_set_trace_buffer", "ba_plan_ctas", "ba_stream_read_bench"]
 
 
 class BAProblem(ctypes.Structure):
@@ -90,6 +90,8 @@ def load_library(path: str = LIB_PATH):
     lib.ba_plan_ctas.restype = ctypes.c_int
     lib.ba_set_trace_buffer.argtypes = [ctypes.c_void_p]
     lib.ba_set_trace_buffer.restype = None
+    lib.ba_stream_read_bench.argtypes = [P, ctypes.c_size_t, P, P]
+    lib.ba_stream_read_bench.restype = ctypes.c_int
     lib.ba_version.argtypes = []
     lib.ba_version.restype = ctypes.c_int
     _lib = lib
@@ -207,6 +209,22 @@ def ba_plan_ctas(prob: BAProblem):
     return [int(buf[k]) for k in range(G + 1)] if G > 0 else []
 
 
+_ws_cache = {}
+
+
+def _ws_need(prob: BAProblem) -> int:
+    key = bytes(prob)
+    n = _ws_cache.get(key)
+    if n is None:
+        n = ba_workspace_bytes(prob)
+        if n == 0:
+            raise BifAttnError(-1, "ba_workspace_bytes")
+        if len(_ws_cache) > 256:
+            _ws_cache.clear()
+        _ws_cache[key] = n
+    return n
+
+
 def alloc_workspace(prob: BAProblem, device) -> torch.Tensor:
     """Zero-initialised workspace (the completion counters must start at 0)."""
     n = ba_workspace_bytes(prob)
@@ -243,6 +261,54 @@ def _fast_check(ts, dtype, device):
             _check(dict(zip(_NAMES, ts)), dtype, device)
 
 
+_shape_ok = set()
+
+
+def _validate_shapes(q, Kc, Vc, Kd, Vd, lens, out, lse, workspace, ws_need):
+    """Shape / dtype / device agreement of every tensor argument (cached per
+    shape signature): a mismatch is a ValueError here, never an out-of-bounds
+    access in a kernel."""
+    key = (tuple(q.shape), tuple(Kc.shape), tuple(Vc.shape), tuple(Kd.shape), tuple(Vd.shape),
+           tuple(lens.shape), tuple(out.shape), out.dtype, out.device, q.dtype, q.device,
+           None if lse is None else (tuple(lse.shape), lse.dtype, lse.device),
+           workspace.numel(), workspace.device)
+    if key in _shape_ok:
+        if not (out.is_contiguous() and (lse is None or lse.is_contiguous())
+                and workspace.is_contiguous()):
+            raise ValueError("out, lse and workspace must be contiguous")
+        return
+    if q.dim() not in (3, 4):
+        raise ValueError(f"q must be [b,h,d] or [b,h,n,d], got {tuple(q.shape)}")
+    b, h, d = q.shape[0], q.shape[1], q.shape[-1]
+    if Kc.dim() != 3 or Kc.shape[2] != d:
+        raise ValueError(f"Kc must be [g,mc,{d}], got {tuple(Kc.shape)}")
+    g = Kc.shape[0]
+    if tuple(Vc.shape) != tuple(Kc.shape):
+        raise ValueError(f"Vc {tuple(Vc.shape)} must match Kc {tuple(Kc.shape)}")
+    if Kd.dim() != 4 or Kd.shape[0] != b or Kd.shape[1] != g or Kd.shape[3] != d:
+        raise ValueError(f"Kd must be [{b},{g},md_cap,{d}], got {tuple(Kd.shape)}")
+    if tuple(Vd.shape) != tuple(Kd.shape):
+        raise ValueError(f"Vd {tuple(Vd.shape)} must match Kd {tuple(Kd.shape)}")
+    if lens.dim() != 1 or lens.shape[0] != b:
+        raise ValueError(f"lens must be int32 [{b}], got {tuple(lens.shape)}")
+    if tuple(out.shape) != tuple(q.shape) or out.dtype != q.dtype or out.device != q.device:
+        raise ValueError(f"out must be {tuple(q.shape)} {q.dtype} on {q.device}")
+    if not out.is_contiguous():
+        raise ValueError("out must be contiguous")
+    if lse is not None:
+        if (tuple(lse.shape) != tuple(q.shape[:-1]) or lse.dtype != torch.float32
+                or lse.device != q.device or not lse.is_contiguous()):
+            raise ValueError(f"lse must be contiguous float32 {tuple(q.shape[:-1])} on {q.device}")
+    if workspace.device != q.device or not workspace.is_contiguous():
+        raise ValueError(f"workspace must be a contiguous buffer on {q.device}")
+    if workspace.numel() * workspace.element_size() < ws_need:
+        raise ValueError(f"workspace has {workspace.numel() * workspace.element_size()} bytes, "
+                         f"needs {ws_need}")
+    if len(_shape_ok) > 256:
+        _shape_ok.clear()
+    _shape_ok.add(key)
+
+
 def _cached_problem(q, Kc, Kd, scale, flags):
     key = (q.shape, Kc.shape, Kd.shape, q.dtype, scale, flags)
     prob = _prob_cache.get(key)
@@ -269,6 +335,7 @@ def bifurcated_attn_decode(q, Kc, Vc, Kd, Vd, lens, out=None, lse=None, *, scale
         out = torch.empty_like(q)
     if workspace is None:
         workspace = alloc_workspace(prob, q.device)
+    _validate_shapes(q, Kc, Vc, Kd, Vd, lens, out, lse, workspace, _ws_need(prob))
     st = (stream if stream is not None else torch.cuda.current_stream()).cuda_stream
     rc = lib.bifurcated_attn_decode(ctypes.byref(prob), q.data_ptr(), Kc.data_ptr(), Vc.data_ptr(),
                                     Kd.data_ptr(), Vd.data_ptr(), lens.data_ptr(), out.data_ptr(),
@@ -299,6 +366,7 @@ def bifurcated_attn_decode_append(q, k_new, v_new, Kc, Vc, Kd, Vd, lens, out=Non
         out = torch.empty_like(q)
     if workspace is None:
         workspace = alloc_workspace(prob, q.device)
+    _validate_shapes(q, Kc, Vc, Kd, Vd, lens, out, lse, workspace, _ws_need(prob))
     st = (stream if stream is not None else torch.cuda.current_stream()).cuda_stream
     rc = lib.bifurcated_attn_decode_append(
         ctypes.byref(prob), q.data_ptr(), k_new.data_ptr(), v_new.data_ptr(), Kc.data_ptr(),
@@ -393,15 +461,36 @@ def replicated_attn_decode(q, K, V, lens, mc, out=None, lse=None, *, scale=None,
         b, h, n, d = q.shape
     else:
         (b, h, d), n = q.shape, 1
+    if K.dim() != 4 or K.shape[0] != b or K.shape[3] != d or tuple(V.shape) != tuple(K.shape):
+        raise ValueError(f"K, V must be [{b},g,mc+md_cap,{d}], got {tuple(K.shape)}, {tuple(V.shape)}")
     g, M = K.shape[1], K.shape[2]
+    if not 1 <= mc <= M:
+        raise ValueError(f"mc ({mc}) must be in [1, {M}]")
     prob = make_problem(b, h, g, d, mc, M - mc, q.dtype, scale, flags, n)
     if out is None:
         out = torch.empty_like(q)
     if workspace is None:
         workspace = alloc_workspace(prob, q.device)
+    # the replicated cache [b,g,M,d] stands in for both Kd-shaped operands
+    Kc_like = K[0, :, :mc]
+    Kd_like = K[:, :, mc:]
+    _validate_shapes(q, Kc_like, Kc_like, Kd_like, Kd_like, lens, out, lse, workspace,
+                     _ws_need(prob))
     rc = lib.replicated_attn_decode(ctypes.byref(prob), _ptr(q), _ptr(K), _ptr(V), _ptr(lens),
                                     _ptr(out), _ptr(lse), _ptr(workspace), workspace.numel(),
                                     _stream_handle(stream))
     if rc != 0:
         raise BifAttnError(rc, "replicated_attn_decode")
     return out
+
+
+def stream_read_bench(buf: torch.Tensor, sink: torch.Tensor, stream=None) -> None:
+    """One launch of the read-only streaming micro-benchmark kernel over
+    ``buf`` (instrumentation for bench.py; include/bifattn.h)."""
+    lib = _lib if _lib is not None else load_library()
+    if not (buf.is_cuda and buf.is_contiguous() and sink.is_cuda and sink.dtype == torch.int32):
+        raise ValueError("buf: contiguous CUDA tensor; sink: CUDA int32")
+    rc = lib.ba_stream_read_bench(buf.data_ptr(), buf.numel() * buf.element_size(),
+                                  sink.data_ptr(), _stream_handle(stream))
+    if rc != 0:
+        raise BifAttnError(rc, "ba_stream_read_bench")

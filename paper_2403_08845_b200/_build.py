@@ -3,6 +3,7 @@ extension: the .so is a plain C-ABI library loaded with ctypes)."""
 from __future__ import annotations
 
 import glob
+import hashlib
 import os
 import subprocess
 
@@ -23,14 +24,26 @@ NVCC_FLAGS = [
 
 
 def _sources():
-    return glob.glob(os.path.join(HERE, "csrc", "*")) + [os.path.join(ROOT, "include", "bifattn.h")]
+    return sorted(glob.glob(os.path.join(HERE, "csrc", "*"))) + [os.path.join(ROOT, "include", "bifattn.h")]
+
+
+def source_hash(extra=()) -> str:
+    """sha256 over the sources, the nvcc flags and the nvcc path: the library is
+    rebuilt whenever any of them changes (never reused on a newer mtime)."""
+    h = hashlib.sha256()
+    for s in _sources():
+        h.update(os.path.basename(s).encode())
+        with open(s, "rb") as f:
+            h.update(f.read())
+    h.update(" ".join([NVCC, *NVCC_FLAGS, *extra]).encode())
+    return h.hexdigest()
 
 
 def needs_build() -> bool:
-    if not os.path.exists(LIB):
+    if not os.path.exists(LIB) or not os.path.exists(LIB + ".srchash"):
         return True
-    t = os.path.getmtime(LIB)
-    return any(os.path.getmtime(s) > t for s in _sources())
+    with open(LIB + ".srchash") as f:
+        return f.read().strip() != source_hash()
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
@@ -40,6 +53,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
             cmd.insert(1, "-Xptxas=-v")
         subprocess.check_call(cmd)
         os.replace(LIB + ".tmp", LIB)
+        with open(LIB + ".srchash", "w") as f:
+            f.write(source_hash() + "\n")
     return LIB
 
 

@@ -25,8 +25,26 @@
 #include "append.cuh"
 #include "lse_merge.cuh"
 #include "ctx_rows.cuh"
+#include "stream_read.cuh"
 
 namespace {
+
+// Planner / experiment knobs.  Release builds compile every knob to its
+// default (no environment-dependent behaviour on the product path); only
+// BIFATTN_EXPERIMENTS builds (the round-1 sweeps) read the environment.
+#ifdef BIFATTN_EXPERIMENTS
+int knob_i(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+double knob_d(const char* name, double dflt) {
+  const char* e = getenv(name);
+  return e ? atof(e) : dflt;
+}
+#else
+constexpr int knob_i(const char*, int dflt) { return dflt; }
+constexpr double knob_d(const char*, double dflt) { return dflt; }
+#endif
 
 thread_local int g_last_cuda_error = 0;
 thread_local char g_plan_buf[512];
@@ -139,10 +157,7 @@ struct AppendArgs {
 // a chunk end when the leftover budget could not pay for another segment.
 void plan_split(const std::vector<long long>& ends, long long T, long long Tc, int G, int* cs,
                 bool whole_ctx_units, double kDecCost) {
-  static const double kSegPenalty = [] {
-    const char* e = getenv("BIFATTN_SEG_PENALTY");
-    return e ? atof(e) : 2.0;
-  }();
+  static const double kSegPenalty = knob_d("BIFATTN_SEG_PENALTY", 2.0);
   // cost of tiles [a, b)
   auto cost = [&](long long a, long long b) {
     const long long c0 = std::min(b, Tc) - std::min(a, Tc);
@@ -252,16 +267,10 @@ int make_plan(const ba_problem_t* pr_in, int sms, bool replicated, Plan* pl) {
         break;
       }
     }
-    static const int n_env = [] {  // experiment override: BIFATTN_N=16|32|48|64
-      const char* e = getenv("BIFATTN_N");
-      return e ? atoi(e) : 0;
-    }();
+    static const int n_env = knob_i("BIFATTN_N", 0);  // experiment override: BIFATTN_N=16|32|48|64
     if (n_env && n_env % p == 0 && (n_env == 16 || n_env == 32 || n_env == 48 || n_env == 64)) tcN = n_env;
   }
-  static const int ctx_rows_env = [] {  // BIFATTN_CTX_ROWS=0 disables the rows-on-M kernel
-    const char* e = getenv("BIFATTN_CTX_ROWS");
-    return e ? atoi(e) : 1;
-  }();
+  static const int ctx_rows_env = knob_i("BIFATTN_CTX_ROWS", 1);  // BIFATTN_CTX_ROWS=0 disables the rows-on-M kernel
   // Rows-on-M context kernel for R >= 64 rows per group: measured faster
   // than the fused kernel's 32-row context passes on every such shape (round
   // 1: C3 104 -> 90 us, C4 163 -> 86 us, C5 2.7 -> 1.8 ms, 4-token C2b 137 ->
@@ -283,20 +292,14 @@ int make_plan(const ba_problem_t* pr_in, int sms, bool replicated, Plan* pl) {
     P.cr_ntile = cdiv(pr->mc, 128);
     // one wave of long items: every item pays a Q load, a pipeline refill and
     // a 64 KB partial (written here, read by the merge)
-    static const int ns_env = [] {  // experiment override: BIFATTN_ROWS_SPLITS
-      const char* e = getenv("BIFATTN_ROWS_SPLITS");
-      return e ? atoi(e) : 0;
-    }();
+    static const int ns_env = knob_i("BIFATTN_ROWS_SPLITS", 0);  // experiment override: BIFATTN_ROWS_SPLITS
     int ns = ns_env > 0 ? ns_env : std::max(1, sms / (g * P.cr_nrb));
     ns = std::max(1, std::min(ns, P.cr_ntile));
     P.cr_tps = cdiv(P.cr_ntile, ns);
     P.cr_nsplit = cdiv(P.cr_ntile, P.cr_tps);
     P.cr_items = g * P.cr_nrb * P.cr_nsplit;
     P.cr_items_ctx = P.cr_items;
-    static const int rows_dec_env = [] {  // BIFATTN_ROWS_DEC=0: decode stays in the fused kernel
-      const char* e = getenv("BIFATTN_ROWS_DEC");
-      return e ? atoi(e) : 1;
-    }();
+    static const int rows_dec_env = knob_i("BIFATTN_ROWS_DEC", 1);  // BIFATTN_ROWS_DEC=0: decode stays in the fused kernel
     // decode items too when p >= 32 (they fill the row block) or when the
     // decode part is small (<= 4096 tiles: C3, multi-token C2b), where a second
     // persistent launch costs more than the half-empty row blocks (measured:
@@ -329,10 +332,7 @@ int make_plan(const ba_problem_t* pr_in, int sms, bool replicated, Plan* pl) {
     if ((227 * 1024 - ba::bif::smem_fixed(tcN, 2)) / ba::bif::kStageBytes <
         (227 * 1024 - ba::bif::smem_fixed(tcN, 1)) / ba::bif::kStageBytes)
       P.tc_npb = 1;
-    static const int npb_env = [] {  // experiment override: BIFATTN_NPB=1|2
-      const char* e = getenv("BIFATTN_NPB");
-      return e ? atoi(e) : 0;
-    }();
+    static const int npb_env = knob_i("BIFATTN_NPB", 0);  // experiment override: BIFATTN_NPB=1|2
     if (npb_env == 1 || npb_env == 2) P.tc_npb = npb_env;
     const int avail = 227 * 1024 - ba::bif::smem_fixed(tcN, P.tc_npb);  // dynamic smem is 1 KB aligned
     P.tc_nst = avail / ba::bif::kStageBytes;
@@ -343,10 +343,7 @@ int make_plan(const ba_problem_t* pr_in, int sms, bool replicated, Plan* pl) {
     // context bands (ctx_unit, bif_tc.cuh): with several row chunks per group
     // the context is cut into bands of bw tiles whose row-chunk passes follow
     // each other (L2 re-reads instead of HBM); one band when nrc = 1
-    static const int bw_env = [] {  // experiment override: BIFATTN_BAND=<tiles>
-      const char* e = getenv("BIFATTN_BAND");
-      return e ? atoi(e) : 0;
-    }();
+    static const int bw_env = knob_i("BIFATTN_BAND", 0);  // experiment override: BIFATTN_BAND=<tiles>
     // Default: one band.  Measured (round 1, profiles/r01/band_sweep.txt): bands
     // of 8/16/32 tiles were SLOWER on C3, C4, C5 and the 4-token C2b step —
     // the re-reads already hit L2 where the context fits, and a multi-chunk
@@ -360,10 +357,7 @@ int make_plan(const ba_problem_t* pr_in, int sms, bool replicated, Plan* pl) {
     // several row chunks pass an L2-resident context (C3, the 4-token C2b
     // step: the re-reads are L2 hits, cheaper than decode tiles from HBM),
     // more for MQA's 128 passes over a 4 MB context (C4).
-    static const double dc_env = [] {
-      const char* e = getenv("BIFATTN_DEC_COST");
-      return e ? atof(e) : 0.0;
-    }();
+    static const double dc_env = knob_d("BIFATTN_DEC_COST", 0.0);
     // The re-reads hit L2 when the whole context fits in it, or when a chunk
     // is about as long as a CTA's range, so that the nrc passes over a group
     // run concurrently on neighbouring CTAs (not one after another in one CTA).
@@ -477,7 +471,12 @@ int make_plan(const ba_problem_t* pr_in, int sms, bool replicated, Plan* pl) {
   P.S = P.nsc + P.nsd;
   if (P.S < 1) P.S = 1;
   const size_t rows = (size_t)b * h;
-  P.off_o = 0;
+  // bytes [0, 256) stay reserved in EVERY plan: the tensor-core plans keep
+  // their self-resetting grid-barrier words there, and one workspace may serve
+  // FMA and tensor-core problems alternately (e.g. speculative steps of n = 1
+  // and n = 4 sharing a workspace sized for the larger one)
+  P.off_cnt = 0;
+  P.off_o = 256;
   P.off_ml = P.off_o + rows * P.S * P.D * sizeof(float);
   P.ws_bytes = P.off_ml + rows * P.S * 2 * sizeof(float);
   P.ws_bytes = (P.ws_bytes + 255) & ~(size_t)255;
@@ -605,18 +604,30 @@ int make_tmap_3d(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uin
   return BA_OK;
 }
 
-template <int N, int SWG, bool MT>
-int launch_bif_tc_n(const ba::BifTcParams& bp, int smem, uint32_t flags, LaunchRec& rec) {
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [&] {
-    attr_err = cudaFuncSetAttribute(ba::bif_tc_kernel<N, SWG, MT>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-  });
-  if (attr_err != cudaSuccess) {
-    g_last_cuda_error = (int)attr_err;
+// The dynamic-shared-memory opt-in is a per-device attribute of a kernel:
+// set it once per (kernel, device), under the library mutex.
+template <typename Kern>
+int ensure_smem_attr(Kern* fn, int bytes, bool* done) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) {
+    cudaGetLastError();
+    return BA_ENODEV;
+  }
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (done[dev]) return BA_OK;
+  const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e != cudaSuccess) {
+    g_last_cuda_error = (int)e;
     return BA_ECUDA;
   }
+  done[dev] = true;
+  return BA_OK;
+}
+
+template <int N, int SWG, bool MT>
+int launch_bif_tc_n(const ba::BifTcParams& bp, int smem, uint32_t flags, LaunchRec& rec) {
+  static bool attr_done[64];
+  if (int rc = ensure_smem_attr(ba::bif_tc_kernel<N, SWG, MT>, 227 * 1024, attr_done)) return rc;
   // one cooperative launch (all CTAs co-resident: the kernel ends with a grid
   // barrier and the LSE merge); programmatic stream serialisation lets its
   // prologue overlap the previous kernel on the stream
@@ -626,12 +637,9 @@ int launch_bif_tc_n(const ba::BifTcParams& bp, int smem, uint32_t flags, LaunchR
   cfg.dynamicSmemBytes = smem;
   cfg.stream = rec.st;
   cudaLaunchAttribute attr[2];
-  static const int no_coop = [] {  // experiment: plain launch (CTAs are resident anyway)
-    const char* e = getenv("BIFATTN_NO_COOP");
-    return e ? atoi(e) : 0;
-  }();
+  // always cooperative: the kernel's grid barrier needs every CTA resident
   attr[0].id = cudaLaunchAttributeCooperative;
-  attr[0].val.cooperative = no_coop ? 0 : 1;
+  attr[0].val.cooperative = 1;
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[1].val.programmaticStreamSerializationAllowed = (flags & BA_FLAG_NO_PDL) ? 0 : 1;
   cfg.attrs = attr;
@@ -686,15 +694,9 @@ int run_tc(const ba_problem_t* pr, const Plan& P, const void* q, const void* Kc,
   bp.ndc = (pr->g + bp.gpc - 1) / bp.gpc;
   bp.qd_rows = std::min(P.tc_N, pr->h);
   bp.Tc = P.tc_Tc; bp.Td = P.tc_T - P.tc_Tc; bp.G = P.tc_G; bp.nst = P.tc_nst; bp.npb = P.tc_npb;
-  static const int pf_env = [] {  // L2 prefetch distance (tiles; measured slower: off)
-    const char* e = getenv("BIFATTN_PF");
-    return e ? atoi(e) : 0;
-  }();
+  static const int pf_env = knob_i("BIFATTN_PF", 0);  // L2 prefetch distance (tiles; measured slower: off)
   bp.pf_dist = pf_env;
-  static const int rot_env = [] {  // context stream stagger (tiles per CTA index)
-    const char* e = getenv("BIFATTN_ROT");
-    return e ? atoi(e) : 0;
-  }();
+  static const int rot_env = knob_i("BIFATTN_ROT", 0);  // context stream stagger (tiles per CTA index)
   bp.rot = rot_env;
   memcpy(bp.cs, P.tc_cs, sizeof(int) * (P.tc_G + 1));
   bp.ext_ctx = P.ctx_rows ? P.cr_nsplit : 0;
@@ -706,10 +708,7 @@ int run_tc(const ba_problem_t* pr, const Plan& P, const void* q, const void* Kc,
   bp.out = out;
   bp.lse = lse;
   bp.trace = static_cast<unsigned long long*>(g_trace);
-  static const int dbg_skip = [] {
-    const char* e = getenv("BIFATTN_DBG");
-    return e ? atoi(e) : 0;
-  }();
+  static const int dbg_skip = knob_i("BIFATTN_DBG", 0);
   bp.dbg = dbg_skip;
   LaunchRec rec(st);
   if (P.ctx_rows) {
@@ -741,16 +740,8 @@ int run_tc(const ba_problem_t* pr, const Plan& P, const void* q, const void* Kc,
     }
     cp.ws_o = bp.ws_o;
     cp.ws_ml = bp.ws_ml;
-    static std::once_flag once;
-    static cudaError_t attr_err = cudaSuccess;
-    std::call_once(once, [&] {
-      attr_err = cudaFuncSetAttribute(ba::ctx_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      ba::ctxr::kSmem);
-    });
-    if (attr_err != cudaSuccess) {
-      g_last_cuda_error = (int)attr_err;
-      return BA_ECUDA;
-    }
+    static bool attr_done[64];
+    if (int rc2 = ensure_smem_attr(ba::ctx_rows_kernel, ba::ctxr::kSmem, attr_done)) return rc2;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(P.cr_grid);
     cfg.blockDim = dim3(ba::ctxr::kThreads);
@@ -796,10 +787,7 @@ int run_tc(const ba_problem_t* pr, const Plan& P, const void* q, const void* Kc,
     }
   }
   // softmax warpgroups (override for experiments: BIFATTN_SWG=1|2)
-  static const int swg_env = [] {
-    const char* e = getenv("BIFATTN_SWG");
-    return e ? atoi(e) : 0;
-  }();
+  static const int swg_env = knob_i("BIFATTN_SWG", 0);
   const int swg = (swg_env == 1 || swg_env == 2 || (swg_env == 4 && P.tc_N == 32)) ? swg_env : ba::bif::softmax_wgs(P.tc_N);
   if (P.ntok > 1) {  // multi-token kernels (MT): the default warpgroup split only
     switch (P.tc_N) {
@@ -1211,6 +1199,26 @@ const char* ba_launch_name(const ba_problem_t* prob, int k) {
 }
 
 void ba_set_trace_buffer(void* dev_buf) { g_trace = dev_buf; }
+
+int ba_stream_read_bench(const void* buf, size_t bytes, void* sink, void* stream) {
+  if (!buf || !sink) return BA_ENULL;
+  if (!aligned16(buf) || (reinterpret_cast<uintptr_t>(sink) & 3u)) return BA_EALIGN;
+  DevInfo di;
+  const int rc = device_info(&di);
+  if (rc) return rc;
+  const size_t n16 = bytes / 16;
+  if (n16 == 0) return BA_OK;
+  const size_t want = (n16 + 4 * 512 - 1) / (4 * 512);
+  const unsigned grid = (unsigned)std::min<size_t>(want, (size_t)di.sms * 4);
+  ba::stream_read_kernel<<<grid, 512, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const uint4*>(buf), n16, static_cast<unsigned*>(sink));
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    g_last_cuda_error = (int)e;
+    return BA_ECUDA;
+  }
+  return BA_OK;
+}
 
 int ba_plan_ctas(const ba_problem_t* prob, int32_t* cs, int cap) {
   DevInfo di;

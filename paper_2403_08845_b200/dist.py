@@ -12,10 +12,21 @@ over NVLink on GPUs; any torch.distributed backend works for the host logic).
 """
 from __future__ import annotations
 
+import contextlib
 from typing import Optional, Tuple
 
 import torch
 import torch.distributed as dist
+
+
+def _on_stream(stream):
+    """Run a helper's kernels AND its collectives on ``stream``: torch's NCCL
+    collectives order themselves against the CURRENT stream, so the caller's
+    stream is made current for the whole helper (kernel -> all-gather ->
+    merge stay ordered on it)."""
+    if stream is None:
+        return contextlib.nullcontext()
+    return torch.cuda.stream(stream)
 
 
 def shard_bounds(h: int, g: int, world: int, rank: int) -> Tuple[int, int, int, int]:
@@ -62,12 +73,13 @@ def decode_sharded(q_local, Kc_local, Vc_local, Kd_local, Vd_local, lens, *, gat
     Returns the local [b][h/G][d] output, or the full [b][h][d] if gather."""
     from . import bifurcated_attn_decode
 
-    out = bifurcated_attn_decode(q_local, Kc_local, Vc_local, Kd_local, Vd_local, lens, lse=lse,
-                                 scale=scale, workspace=workspace, stream=stream)
-    if not gather:
-        return out
-    world = world or dist.get_world_size(group)
-    return gather_heads(out, world, group)
+    with _on_stream(stream):
+        out = bifurcated_attn_decode(q_local, Kc_local, Vc_local, Kd_local, Vd_local, lens,
+                                     lse=lse, scale=scale, workspace=workspace, stream=stream)
+        if not gather:
+            return out
+        world = world or dist.get_world_size(group)
+        return gather_heads(out, world, group)
 
 
 # ---------------------------------------------------------------------------
@@ -152,9 +164,10 @@ def decode_context_split(q, Kc_r, Vc_r, Kd_r, Vd_r, lens_r, *, world: Optional[i
     from . import bifurcated_attn_decode, lse_merge
 
     world = world or dist.get_world_size(group)
-    lse = torch.empty(q.shape[:-1], dtype=torch.float32, device=q.device)
-    out = bifurcated_attn_decode(q, Kc_r, Vc_r, Kd_r, Vd_r, lens_r, lse=lse, scale=scale,
-                                 workspace=workspace, stream=stream)
-    ob, lb = exchange_partials(out, lse, world, group)
-    full_lse = torch.empty_like(lse)
-    return lse_merge(ob, lb, lse=full_lse, stream=stream), full_lse
+    with _on_stream(stream):
+        lse = torch.empty(q.shape[:-1], dtype=torch.float32, device=q.device)
+        out = bifurcated_attn_decode(q, Kc_r, Vc_r, Kd_r, Vd_r, lens_r, lse=lse, scale=scale,
+                                     workspace=workspace, stream=stream)
+        ob, lb = exchange_partials(out, lse, world, group)
+        full_lse = torch.empty_like(lse)
+        return lse_merge(ob, lb, lse=full_lse, stream=stream), full_lse

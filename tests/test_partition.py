@@ -163,31 +163,3 @@ def test_split_covers_every_tile_once_and_slots_match(shape):
 def test_fma_plan_has_no_cta_table():
     _build.build()
     assert ba.ba_plan_ctas(ba.make_problem(4, 2, 2, 16, 32, 4, 1)) == []
-
-
-def test_banded_context_split_in_subprocess():
-    """The banded context order (BIFATTN_BAND, experiment setting) keeps the
-    same invariants: whole units per CTA, one slot per band, every tile once."""
-    import json
-    import os
-    import subprocess
-    import sys
-    code = (
-        "import json, re, paper_2403_08845_b200 as ba\n"
-        "out = []\n"
-        "for s in [(64, 32, 8, 16384, 512), (256, 64, 64, 4096, 256), (40, 2, 2, 1290, 33)]:\n"
-        "    pr = ba.make_problem(s[0], s[1], s[2], 128, s[3], s[4], 0)\n"
-        "    out.append([list(s), ba.ba_plan_ctas(pr), ba.ba_plan_string(pr)])\n"
-        "print(json.dumps(out))\n")
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, BIFATTN_BAND="8", BIFATTN_CTX_ROWS="0", PYTHONPATH=root)
-    res = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
-                         check=True, cwd=root)
-    for (b, h, g, mc, md), cs, plan in json.loads(res.stdout.strip().splitlines()[-1]):
-        m = re.search(r"N=(\d+).*band=(\d+).*slots=(\d+)\+(\d+)", plan)
-        bw = int(m.group(2))
-        ntc = -(-mc // 128)
-        assert bw in (8, ntc), plan  # tiny problems fall back to one band
-        N, sc, sd, loads, banded = model(b, h, g, mc, md, cs, bw)
-        assert banded == (bw == 8) and (banded or b < 64)
-        assert (int(m.group(1)), int(m.group(3)), int(m.group(4))) == (N, sc, sd)
