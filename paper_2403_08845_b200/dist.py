@@ -171,3 +171,63 @@ def decode_context_split(q, Kc_r, Vc_r, Kd_r, Vd_r, lens_r, *, world: Optional[i
         ob, lb = exchange_partials(out, lse, world, group)
         full_lse = torch.empty_like(lse)
         return lse_merge(ob, lb, lse=full_lse, stream=stream), full_lse
+
+
+# ---------------------------------------------------------------------------
+# One sharded step (bench.py's N > 1 path and tests/test_dist_gloo.py): pick
+# the partition, slice the rank's inputs, run the rank's part through the
+# C ABI, assemble the full output when asked.
+# ---------------------------------------------------------------------------
+def split_mode(b: int, h: int, g: int, mc: int, world: int) -> str:
+    """Partition of one step over ``world`` ranks:
+    'heads'   world | g: the paper's TP partition (h' = h/t, g' = g/t,
+              PAPER.md:1014; Table 8 :1348-1365) — no collective in attention;
+    'batch'   otherwise, when world <= b (MQA, g = 1: "the single head in K
+              and V are duplicated across TP ranks", :1014) — each rank reads
+              the shared context once for its samples, no collective;
+    'context' otherwise: the context positions are split and the ranks
+              exchange (out, lse) once (f3, :701-702)."""
+    if world == 1:
+        return "single"
+    if g % world == 0:
+        return "heads"
+    if world <= b:
+        return "batch"
+    if world <= mc:
+        return "context"
+    raise ValueError(f"cannot partition b={b}, g={g}, mc={mc} over {world} ranks")
+
+
+def shard_step(q, Kc, Vc, Kd, Vd, lens, world: int, rank: int, mode: str):
+    """The rank-local tensors (q, Kc, Vc, Kd, Vd, lens) of ``mode``."""
+    if mode == "single":
+        return q, Kc, Vc, Kd, Vd, lens
+    if mode == "heads":
+        ql, Kcl, Vcl, Kdl, Vdl = shard_inputs(q, Kc, Vc, Kd, Vd, world, rank)
+        return ql, Kcl, Vcl, Kdl, Vdl, lens
+    if mode == "batch":
+        ql, Kdl, Vdl, ll = shard_batch_inputs(q, Kd, Vd, lens, world, rank)
+        return ql, Kc, Vc, Kdl, Vdl, ll
+    if mode == "context":
+        Kcl, Vcl, Kdl, Vdl, ll = split_context_inputs(Kc, Vc, Kd, Vd, lens, world, rank)
+        return q, Kcl, Vcl, Kdl, Vdl, ll
+    raise ValueError(mode)
+
+
+def assemble(out_local, lse_local, b: int, world: int, mode: str, group=None, stream=None):
+    """The full [b][h][d] output from every rank's part: one all-gather of the
+    output heads ('heads') or samples ('batch'), or the (out, lse) exchange +
+    LSE join ('context', needs ``lse_local``; GPU only: ba_lse_merge)."""
+    with _on_stream(stream):
+        if mode == "single":
+            return out_local
+        if mode == "heads":
+            return gather_heads(out_local, world, group)
+        if mode == "batch":
+            return gather_batch(out_local, b, world, group)
+        if mode == "context":
+            from . import lse_merge
+
+            ob, lb = exchange_partials(out_local, lse_local, world, group)
+            return lse_merge(ob, lb, stream=stream)
+        raise ValueError(mode)

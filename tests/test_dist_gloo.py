@@ -168,3 +168,68 @@ def test_split_bounds():
             list(range(8192))
     with pytest.raises(ValueError):
         context_bounds(3, 4, 0)
+
+
+def _step_worker(rank, world, port, cfg_kw, seed, mode, q_out):
+    import oracle
+    from paper_2403_08845_b200.dist import assemble, shard_step, split_mode
+    from synth import Config, make_inputs
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        cfg = Config(**cfg_kw)
+        assert split_mode(cfg.b, cfg.h, cfg.g, cfg.mc, world) == mode
+        inp = make_inputs(cfg, seed, variant="ragged")
+        ql, Kcl, Vcl, Kdl, Vdl, ll = shard_step(inp.q, inp.Kc, inp.Vc, inp.Kd, inp.Vd, inp.lens,
+                                                world, rank, mode)
+        out, _, _ = oracle.attn_decode(ql, Kcl, Vcl, Kdl, Vdl, ll, scale=inp.scale)
+        out_t = torch.from_numpy(out).reshape(ql.shape)
+        full = assemble(out_t, None, cfg.b, world, mode)
+        if rank == 0:
+            q_out.put(full.numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("cfg_kw,mode", [
+    (dict(name="mha", dtype="bf16", b=3, h=8, g=8, d=32, mc=40, md=6), "heads"),
+    (dict(name="mqa", dtype="bf16", b=5, h=6, g=1, d=16, mc=37, md=7), "batch"),
+])
+def test_sharded_step_equals_unsharded(cfg_kw, mode):
+    """bench.py's N > 1 step (dist.split_mode / shard_step / assemble) at world
+    size 2 equals the unsharded step bit for bit (the per-rank compute is the
+    oracle here; on GPUs it is the C ABI)."""
+    import oracle
+    from synth import Config, make_inputs
+
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_step_worker, args=(r, world, port, cfg_kw, 7, mode, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    full = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    cfg = Config(**cfg_kw)
+    inp = make_inputs(cfg, 7, variant="ragged")
+    ref, _, _ = oracle.attn_decode(inp.q, inp.Kc, inp.Vc, inp.Kd, inp.Vd, inp.lens,
+                                   scale=inp.scale)
+    np.testing.assert_array_equal(full.reshape(ref.shape), ref)
+
+
+def test_split_mode_choices():
+    from paper_2403_08845_b200.dist import split_mode
+
+    assert split_mode(32, 32, 32, 8192, 1) == "single"
+    assert split_mode(32, 32, 32, 8192, 8) == "heads"
+    assert split_mode(64, 32, 8, 16384, 8) == "heads"
+    assert split_mode(128, 48, 1, 8192, 8) == "batch"
+    assert split_mode(2, 4, 1, 100, 4) == "context"
+    with pytest.raises(ValueError):
+        split_mode(1, 1, 1, 2, 4)

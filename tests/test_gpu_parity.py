@@ -177,9 +177,19 @@ def test_small_workspace_rejected():
     cfg = Config("x", "bf16", b=2, h=2, g=2, d=128, mc=64, md=4)
     inp = make_inputs(cfg, 15, device=DEV)
     ws = torch.zeros(64, dtype=torch.uint8, device=DEV)
-    with pytest.raises(ba.BifAttnError) as e:
+    # the binding refuses it before the call ...
+    with pytest.raises(ValueError):
         ba.bifurcated_attn_decode(inp.q, inp.Kc, inp.Vc, inp.Kd, inp.Vd, inp.lens, workspace=ws)
-    assert e.value.code == -4
+    # ... and the C ABI itself returns BA_EWORKSPACE
+    import ctypes
+    lib = ba.load_library()
+    prob = ba.make_problem(cfg.b, cfg.h, cfg.g, cfg.d, cfg.mc, cfg.md, cfg.torch_dtype)
+    out = torch.empty_like(inp.q)
+    rc = lib.bifurcated_attn_decode(ctypes.byref(prob), inp.q.data_ptr(), inp.Kc.data_ptr(),
+                                    inp.Vc.data_ptr(), inp.Kd.data_ptr(), inp.Vd.data_ptr(),
+                                    inp.lens.data_ptr(), out.data_ptr(), None, ws.data_ptr(),
+                                    ws.numel(), torch.cuda.current_stream().cuda_stream)
+    assert rc == -4
 
 
 # ---------------------------------------------------------------------------
