@@ -60,6 +60,11 @@ def _load():
         lib.oracle_bifurcated_f64.restype = I
         lib.oracle_attn_decode_multi_f64.argtypes = [I] + args
         lib.oracle_attn_decode_multi_f64.restype = I
+        lib.oracle_attn_decode_kv8_f64.argtypes = [I] * 7 + [ctypes.c_double] * 3 + \
+            [P] * 7 + [I, P, P, P, I]
+        lib.oracle_attn_decode_kv8_f64.restype = I
+        lib.oracle_e4m3_value.argtypes = [I]
+        lib.oracle_e4m3_value.restype = ctypes.c_double
         lib.oracle_kv_read_elements.argtypes = [ctypes.c_int64] * 5 + [I]
         lib.oracle_kv_read_elements.restype = ctypes.c_int64
         _lib = lib
@@ -136,6 +141,46 @@ def attn_decode(q, Kc, Vc, Kd, Vd, lens, *, scale, rows=None, weights=False,
     else:
         fn = _load().oracle_bifurcated_f64 if bifurcated else _load().oracle_attn_decode_f64
         rc = fn(b, h, g, d, mc, md_cap, dtype, *tail)
+    if rc != 0:
+        raise ValueError("oracle: invalid problem")
+    return out, lse, w
+
+
+def e4m3_value(code: int) -> float:
+    """The value of one OCP FP8 E4M3 code (reading R19)."""
+    return float(_load().oracle_e4m3_value(int(code)))
+
+
+def attn_decode_kv8(q, Kc, Vc, Kd, Vd, lens, *, scale, k_scale, v_scale, rows=None,
+                    weights=False, nthreads=1):
+    """The fp64 oracle with an FP8 E4M3 KV cache (oracle_attn_decode_kv8_f64):
+    Kc, Vc [g][mc][d] and Kd, Vd [b][g][md_cap][d] are E4M3 codes (uint8 numpy
+    arrays or torch.float8_e4m3fn / uint8 tensors), dequantised as code value x
+    k_scale (K) or x v_scale (V); q [b][h][d] bf16 or fp32.  Returns (out, lse,
+    weights) like attn_decode."""
+    def codes(t):
+        if isinstance(t, np.ndarray):
+            return np.ascontiguousarray(t.astype(np.uint8, copy=False))
+        t = t.detach().contiguous().cpu()
+        return t.view(__import__("torch").uint8).numpy()
+
+    qn = _as_np(q)
+    Kcn, Vcn, Kdn, Vdn = (codes(t) for t in (Kc, Vc, Kd, Vd))
+    lensn = np.ascontiguousarray(_as_np(lens).astype(np.int32))
+    b, h, d = qn.shape
+    g, mc, _ = Kcn.shape
+    md_cap = Kdn.shape[2]
+    assert Kcn.shape == Vcn.shape and Kdn.shape == Vdn.shape and Kdn.shape[:2] == (b, g)
+    dtype = OR_BF16 if qn.dtype == np.uint16 else OR_FP32
+    rows_np = None if rows is None else np.ascontiguousarray(np.asarray(rows, dtype=np.int32))
+    nrows = b * h if rows is None else int(rows_np.size)
+    out = np.zeros((nrows, d))
+    lse = np.zeros(nrows)
+    w = np.zeros((nrows, mc + md_cap)) if weights else None
+    rc = _load().oracle_attn_decode_kv8_f64(
+        b, h, g, d, mc, md_cap, dtype, float(scale), float(k_scale), float(v_scale), _ptr(qn),
+        _ptr(Kcn), _ptr(Vcn), _ptr(Kdn), _ptr(Vdn), _ptr(lensn), _ptr(rows_np), nrows,
+        _ptr(out), _ptr(lse), _ptr(w), int(nthreads))
     if rc != 0:
         raise ValueError("oracle: invalid problem")
     return out, lse, w

@@ -320,6 +320,104 @@ int oracle_attn_decode_multi_f64(int b, int h, int n, int g, int d, int mc, int 
 }
 
 /*
+ * FP8 (E4M3) KV cache (FAQ 5: "the lower
+ * memory on the attention tensor will effectively reduce the memory I/O for
+ * KV cache by a factor of 2 in the case of int8 quantization"; reading R19):
+ * Kc, Vc, Kd, Vd hold OCP FP8 E4M3 codes (1 sign, 4 exponent bits with bias 7,
+ * 3 mantissa bits; no infinities; S.1111.111 is NaN) with one fp32 scale per
+ * tensor kind shared by the context and decode caches: the cache value is
+ *   K = e4m3(code) * k_scale,   V = e4m3(code) * v_scale.
+ * q is bf16 or fp32 (q_dtype).  The attention is Eq. 1-2 over the replicated
+ * cache exactly as oracle_attn_decode_f64, on those dequantised values
+ * (widened exactly: a 4-bit significand times a 24-bit one fits in fp64), so
+ * the quantisation is input, not error.
+ */
+static double e4m3_value(uint8_t code) {
+  const int s = code >> 7, e = (code >> 3) & 15, m = code & 7;
+  double v;
+  if (e == 15 && m == 7) return NAN;
+  if (e == 0)
+    v = ldexp((double)m, -9); /* subnormal: (m / 8) * 2^-6 */
+  else
+    v = ldexp(1.0 + (double)m / 8.0, e - 7);
+  return s ? -v : v;
+}
+
+/* The value of E4M3 code `code` (exported for the pins: the decode table). */
+double oracle_e4m3_value(int code) { return e4m3_value((uint8_t)(code & 255)); }
+
+int oracle_attn_decode_kv8_f64(int b, int h, int g, int d, int mc, int md_cap, int q_dtype,
+                               double scale, double k_scale, double v_scale, const void *q,
+                               const uint8_t *Kc, const uint8_t *Vc, const uint8_t *Kd,
+                               const uint8_t *Vd, const int32_t *lens, const int32_t *rows,
+                               int nrows, double *out, double *lse, double *weights,
+                               int nthreads) {
+  if (check(b, h, g, d, mc, md_cap, q_dtype)) return -1;
+  if (!rows) nrows = b * h;
+  const int p = h / g;
+  const int Mcap = mc + md_cap;
+  int err = 0;
+  (void)nthreads;
+#pragma omp parallel for schedule(dynamic, 1) num_threads(nthreads > 0 ? nthreads : 1)
+  for (int r = 0; r < nrows; ++r) {
+    const int row = rows ? rows[r] : r;
+    const int i = row / h, j = row % h, c = j / p;
+    const int M = mc + dec_len(lens, i, md_cap);
+    double *Kf = (double *)malloc(sizeof(double) * (size_t)(M > 0 ? M : 1) * d);
+    double *Vf = (double *)malloc(sizeof(double) * (size_t)(M > 0 ? M : 1) * d);
+    double *l = (double *)malloc(sizeof(double) * (size_t)(M > 0 ? M : 1));
+    if (!Kf || !Vf || !l || M < 1) {
+      free(Kf); free(Vf); free(l);
+#pragma omp atomic write
+      err = 1;
+      continue;
+    }
+    /* Step 1: this sample's full cache Kc ⊕ Kd[i] for group c, dequantised. */
+    for (int t = 0; t < M; ++t) {
+      for (int x = 0; x < d; ++x) {
+        size_t src;
+        if (t < mc) {
+          src = ((size_t)c * mc + t) * d + x;
+          Kf[(size_t)t * d + x] = e4m3_value(Kc[src]) * k_scale;
+          Vf[(size_t)t * d + x] = e4m3_value(Vc[src]) * v_scale;
+        } else {
+          src = (((size_t)i * g + c) * md_cap + (t - mc)) * d + x;
+          Kf[(size_t)t * d + x] = e4m3_value(Kd[src]) * k_scale;
+          Vf[(size_t)t * d + x] = e4m3_value(Vd[src]) * v_scale;
+        }
+      }
+    }
+    /* Step 2: logits (Eq. 1). */
+    for (int t = 0; t < M; ++t) {
+      double acc = 0.0;
+      for (int x = 0; x < d; ++x)
+        acc += widen(q, ((size_t)i * h + j) * d + x, q_dtype) * Kf[(size_t)t * d + x];
+      l[t] = scale * acc;
+    }
+    /* Step 3: one softmax over all M positions. */
+    double mx = l[0];
+    for (int t = 1; t < M; ++t)
+      if (l[t] > mx) mx = l[t];
+    double Z = 0.0;
+    for (int t = 0; t < M; ++t) {
+      l[t] = exp(l[t] - mx);
+      Z += l[t];
+    }
+    /* Step 4: out = (sum_t w_t V_t) / Z (Eq. 2). */
+    for (int x = 0; x < d; ++x) {
+      double acc = 0.0;
+      for (int t = 0; t < M; ++t) acc += l[t] * Vf[(size_t)t * d + x];
+      out[(size_t)r * d + x] = acc / Z;
+    }
+    if (lse) lse[r] = mx + log(Z);
+    if (weights)
+      for (int t = 0; t < Mcap; ++t) weights[(size_t)r * Mcap + t] = t < M ? l[t] / Z : 0.0;
+    free(Kf); free(Vf); free(l);
+  }
+  return err ? -1 : 0;
+}
+
+/*
  * KV-read element counts of Eq. 5-6 (§4.3), per K or V
  * tensor, per layer:  naive  g*k*b*(mc+md);  bifurcated  g*k*(mc+b*md).
  */

@@ -31,6 +31,11 @@ class Config:
     d: int
     mc: int
     md: int
+    kv: str = ""  # KV cache storage: "" = the dtype; "e4m3" = FP8 E4M3 codes + fp32 scales (R19)
+
+    @property
+    def kv_bytes(self) -> int:
+        return 1 if self.kv == "e4m3" else self.elem_bytes
 
     @property
     def p(self) -> int:
@@ -56,6 +61,9 @@ CONFIGS = {
     "gqa": Config("gqa", "bf16", b=64, h=32, g=8, d=128, mc=16384, md=512),
     "mqa": Config("mqa", "bf16", b=128, h=48, g=1, d=128, mc=8192, md=256),
     "long": Config("long", "bf16", b=256, h=64, g=64, d=128, mc=32768, md=1024),
+    # f4: the C2b workload with an FP8 (E4M3) KV cache (FAQ 5)
+    "mha7b_b32_fp8": Config("mha7b_b32_fp8", "bf16", b=32, h=32, g=32, d=128, mc=8192, md=256,
+                            kv="e4m3"),
 }
 
 SEED_BASE = 20240313
@@ -74,6 +82,8 @@ class Inputs:
     Vd: torch.Tensor  # [b][g][md_cap][d]
     lens: torch.Tensor  # int32 [b]
     scale: float      # the fp32 logit scale (1/sqrt(d) unless overridden)
+    k_scale: float = 1.0  # FP8 KV (cfg.kv == "e4m3"): K = code value * k_scale (fp32)
+    v_scale: float = 1.0  #                            V = code value * v_scale
 
 
 def make_inputs(cfg: Config, seed: int, device="cpu", variant: str = "normal",
@@ -138,16 +148,33 @@ def make_inputs(cfg: Config, seed: int, device="cpu", variant: str = "normal",
         raise ValueError(variant)
     if scale is None:
         scale = float(torch.tensor(1.0 / cfg.d ** 0.5, dtype=torch.float32))
+    if cfg.kv == "e4m3":
+        # per-tensor-kind scales (one for K, one for V, shared by context and
+        # decode caches): amax / 448 in fp32, then the E4M3 codes of x / scale
+        def amax(a, b_):
+            m = a.float().abs().max()
+            if b_.numel():
+                m = torch.maximum(m, b_.float().abs().max())
+            return m
+
+        ks = amax(Kc, Kd) / 448.0
+        vs = amax(Vc, Vd) / 448.0
+        ks = torch.where(ks > 0, ks, torch.ones_like(ks))
+        vs = torch.where(vs > 0, vs, torch.ones_like(vs))
+        f8 = torch.float8_e4m3fn
+        Kc, Kd = (Kc.float() / ks).to(f8), (Kd.float() / ks).to(f8)
+        Vc, Vd = (Vc.float() / vs).to(f8), (Vd.float() / vs).to(f8)
+        return Inputs(q, Kc, Vc, Kd, Vd, lens_t, scale, float(ks), float(vs))
     return Inputs(q, Kc, Vc, Kd, Vd, lens_t, scale)
 
 
 def alg_bytes(cfg: Config, lens_sum: Optional[int] = None) -> int:
     """Algorithmic bytes of one step (Eq. 6 PAPER.md:287 x 2
     tensors x element bytes, plus the q/out terms of App. E.2):
-      2*e*d*g*(mc + sum_i lens[i]) + 2*e*b*h*d."""
-    e = cfg.elem_bytes
+      2*e_kv*d*g*(mc + sum_i lens[i]) + 2*e*b*h*d   (e_kv = 1 for an FP8 KV cache)."""
+    e, ekv = cfg.elem_bytes, cfg.kv_bytes
     ls = cfg.b * cfg.md if lens_sum is None else lens_sum
-    return 2 * e * cfg.d * cfg.g * (cfg.mc + ls) + 2 * e * cfg.b * cfg.h * cfg.d
+    return 2 * ekv * cfg.d * cfg.g * (cfg.mc + ls) + 2 * e * cfg.b * cfg.h * cfg.d
 
 
 def alg_flops(cfg: Config, lens_sum: Optional[int] = None) -> int:
