@@ -147,4 +147,4 @@ def test_fp8_config_bytes_halve_kv():
     kv16 = 2 * 2 * c16.d * c16.g * (c16.mc + c16.b * c16.md)
     qo = 2 * 2 * c16.b * c16.h * c16.d
     assert alg_bytes(c16) == kv16 + qo == 268959744
-    assert alg_bytes(c8) == kv16 // 2 + qo == 134610944
+    assert alg_bytes(c8) == kv16 // 2 + qo == 134742016
