@@ -55,7 +55,7 @@
 extern "C" {
 #endif
 
-typedef enum { BA_BF16 = 0, BA_FP32 = 1 } ba_dtype_t;
+typedef enum { BA_BF16 = 0, BA_FP32 = 1, BA_FP8_E4M3 = 2 } ba_dtype_t;
 
 enum {
   BA_OK = 0,
@@ -63,7 +63,7 @@ enum {
   BA_ENULL = -2,      /* a required pointer is NULL                                          */
   BA_EALIGN = -3,     /* a tensor pointer is not 16-byte aligned                             */
   BA_EWORKSPACE = -4, /* workspace NULL or smaller than ba_workspace_bytes()                */
-  BA_EDTYPE = -5,     /* dtype not BA_BF16 / BA_FP32                                         */
+  BA_EDTYPE = -5,     /* dtype not BA_BF16 / BA_FP32, or an FP8 cache with a non-bf16 dtype */
   BA_ENODEV = -6,     /* no CUDA device of compute capability 10.x (sm_100a)                 */
   BA_ECUDA = -7       /* a CUDA runtime call or kernel launch failed (see ba_last_cuda_error) */
 };
@@ -91,7 +91,25 @@ typedef struct {
   int32_t n_tok;    /* query tokens per sample in this step (multi-token / speculative
                        verification step, App. G PAPER.md:1219-1226 "with n_g replacing
                        n"); 0 or 1 = the single-token step.  See MULTI-TOKEN below.    */
+  ba_dtype_t kv_dtype; /* storage of Kc, Vc, Kd, Vd: BA_FP8_E4M3 for an FP8 cache (see
+                       FP8 KV below); any other value = stored in `dtype` (0 = default)  */
+  float k_scale;    /* FP8 KV: K = E4M3 code value * k_scale; <= 0 means 1            */
+  float v_scale;    /* FP8 KV: V = E4M3 code value * v_scale; <= 0 means 1            */
 } ba_problem_t;
+
+/* FP8 KV (kv_dtype = BA_FP8_E4M3, FAQ 5:
+ * quantised attention "will effectively reduce the memory I/O for KV cache by
+ * a factor of 2"; reading R19):
+ *   Kc, Vc [g][mc][d] and Kd, Vd [b][g][md_cap][d] hold one-byte OCP FP8 E4M3
+ *   codes (bias 7, no infinities); one fp32 scale per tensor kind, shared by
+ *   the context and decode caches.  q and out stay bf16 (dtype must be
+ *   BA_BF16).  The step is the same attention over the dequantised cache
+ *   (code value x scale); the kernels convert codes to f16 exactly, fold
+ *   k_scale into the logit scale and apply v_scale in the final merge.  The
+ *   tensor-core path converts q to f16 (exact for bf16 values of magnitude in
+ *   [2^-17, 65504]; the caller keeps |q| < 65504), so P enters the PV MMA as
+ *   one f16 operand.  k_new / v_new of the append entry points are codes too.
+ *   Algorithmic bytes: 2*1*d*g*(mc + sum lens) + 2*2*b*h*d. */
 
 /* MULTI-TOKEN STEP (n_tok = n > 1):
  *   q, out [b][h][n][d], lse [b][h][n]: token k of head j of sample i.
@@ -256,7 +274,8 @@ const char* ba_strerror(int code);
 /* The cudaError_t of the last BA_ECUDA on this thread (0 if none). */
 int ba_last_cuda_error(void);
 
-/* ABI version: 2 (2 added ba_problem_t.n_tok, the multi-token step). */
+/* ABI version: 3 (2 added ba_problem_t.n_tok, the multi-token step; 3 added
+ * kv_dtype, k_scale, v_scale: the FP8 KV cache). */
 int ba_version(void);
 
 #ifdef __cplusplus

@@ -22,7 +22,7 @@ import torch
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libbifattn.so")
 
-BA_BF16, BA_FP32 = 0, 1
+BA_BF16, BA_FP32, BA_FP8_E4M3 = 0, 1, 2
 BA_FLAG_FORCE_FMA = 0x1
 BA_FLAG_NO_PDL = 0x2
 BA_FLAG_CTX_ROWS = 0x4
@@ -42,7 +42,8 @@ class BAProblem(ctypes.Structure):
     _fields_ = [("b", ctypes.c_int32), ("h", ctypes.c_int32), ("g", ctypes.c_int32),
                 ("d", ctypes.c_int32), ("mc", ctypes.c_int32), ("md_cap", ctypes.c_int32),
                 ("dtype", ctypes.c_int32), ("scale", ctypes.c_float), ("flags", ctypes.c_uint32),
-                ("n_tok", ctypes.c_int32)]
+                ("n_tok", ctypes.c_int32), ("kv_dtype", ctypes.c_int32),
+                ("k_scale", ctypes.c_float), ("v_scale", ctypes.c_float)]
 
 
 _lib = None
@@ -109,21 +110,30 @@ class BifAttnError(RuntimeError):
         self.code = code
 
 
+FP8_DTYPES = (torch.float8_e4m3fn,)
+
+
 def make_problem(b, h, g, d, mc, md_cap, dtype, scale: Optional[float] = None, flags: int = 0,
-                 n_tok: int = 1):
+                 n_tok: int = 1, kv_dtype=None, k_scale: float = 1.0, v_scale: float = 1.0):
+    """kv_dtype: None / the dtype (cache stored like q), or torch.float8_e4m3fn /
+    BA_FP8_E4M3 (FP8 KV cache with per-tensor k_scale / v_scale, include/bifattn.h)."""
     dt = {torch.bfloat16: BA_BF16, torch.float32: BA_FP32}.get(dtype, dtype)
-    return BAProblem(b, h, g, d, mc, md_cap, dt, float(scale) if scale else 0.0, flags, n_tok)
+    kv = BA_FP8_E4M3 if (kv_dtype in FP8_DTYPES or kv_dtype == BA_FP8_E4M3) else 0
+    return BAProblem(b, h, g, d, mc, md_cap, dt, float(scale) if scale else 0.0, flags, n_tok,
+                     kv, float(k_scale) if kv else 0.0, float(v_scale) if kv else 0.0)
 
 
-def _problem_from(q, Kc, Kd, scale, flags):
-    """q [b,h,d] (one token per sample) or [b,h,n,d] (multi-token step)."""
+def _problem_from(q, Kc, Kd, scale, flags, k_scale=1.0, v_scale=1.0):
+    """q [b,h,d] (one token per sample) or [b,h,n,d] (multi-token step); an FP8
+    cache (Kc dtype float8_e4m3fn) carries its per-tensor scales."""
     if q.dim() == 4:
         b, h, n, d = q.shape
     else:
         (b, h, d), n = q.shape, 1
     g, mc, _ = Kc.shape
     md_cap = Kd.shape[2]
-    return make_problem(b, h, g, d, mc, md_cap, q.dtype, scale, flags, n)
+    return make_problem(b, h, g, d, mc, md_cap, q.dtype, scale, flags, n, Kc.dtype, k_scale,
+                        v_scale)
 
 
 def _ptr(t):
@@ -252,11 +262,19 @@ _prob_cache = {}
 
 
 def _fast_check(ts, dtype, device):
-    """Per-call argument checks (the cheap common case; _check words the error)."""
+    """Per-call argument checks (the cheap common case; _check words the error).
+    The cache (ts[1:5]) is either in q's dtype or, with a bf16 q, FP8 E4M3."""
     for t in ts:
         if not (t.is_cuda and t.device == device and t.is_contiguous()):
             _check(dict(zip(_NAMES, ts)), dtype, device)
-    for t in ts[:5]:
+    if ts[0].dtype != dtype:
+        _check(dict(zip(_NAMES, ts)), dtype, device)
+    kvd = ts[1].dtype
+    if kvd in FP8_DTYPES and dtype == torch.bfloat16:
+        if any(t.dtype != kvd for t in ts[1:5]):
+            raise ValueError("Kc, Vc, Kd, Vd must all be float8_e4m3fn")
+        return
+    for t in ts[1:5]:
         if t.dtype != dtype:
             _check(dict(zip(_NAMES, ts)), dtype, device)
 
@@ -309,28 +327,30 @@ def _validate_shapes(q, Kc, Vc, Kd, Vd, lens, out, lse, workspace, ws_need):
     _shape_ok.add(key)
 
 
-def _cached_problem(q, Kc, Kd, scale, flags):
-    key = (q.shape, Kc.shape, Kd.shape, q.dtype, scale, flags)
+def _cached_problem(q, Kc, Kd, scale, flags, k_scale=1.0, v_scale=1.0):
+    key = (q.shape, Kc.shape, Kd.shape, q.dtype, Kc.dtype, scale, flags, k_scale, v_scale)
     prob = _prob_cache.get(key)
     if prob is None:
         if len(_prob_cache) > 64:
             _prob_cache.clear()
-        prob = _prob_cache[key] = _problem_from(q, Kc, Kd, scale, flags)
+        prob = _prob_cache[key] = _problem_from(q, Kc, Kd, scale, flags, k_scale, v_scale)
     return prob
 
 
 def bifurcated_attn_decode(q, Kc, Vc, Kd, Vd, lens, out=None, lse=None, *, scale=None,
-                           workspace=None, stream=None, flags=0):
+                           workspace=None, stream=None, flags=0, k_scale=1.0, v_scale=1.0):
     """One bifurcated decode step on the GPU.  Shapes: q [b,h,d]; Kc,Vc [g,mc,d];
     Kd,Vd [b,g,md_cap,d]; lens int32 [b].  Returns ``out`` [b,h,d].
     Multi-token step (n draft tokens per sample, include/bifattn.h MULTI-TOKEN):
     q [b,h,n,d], out [b,h,n,d], lse [b,h,n]; token k sees the decode positions
-    t < lens[i] - (n - 1 - k)."""
+    t < lens[i] - (n - 1 - k).
+    FP8 cache: Kc, Vc, Kd, Vd float8_e4m3fn with per-tensor k_scale / v_scale
+    (cache value = code x scale; q and out bf16)."""
     lib = _lib if _lib is not None else load_library()
     _fast_check((q, Kc, Vc, Kd, Vd, lens), q.dtype, q.device)
     if lens.dtype != torch.int32:
         raise ValueError("lens must be int32")
-    prob = _cached_problem(q, Kc, Kd, scale, flags)
+    prob = _cached_problem(q, Kc, Kd, scale, flags, k_scale, v_scale)
     if out is None:
         out = torch.empty_like(q)
     if workspace is None:
@@ -347,17 +367,18 @@ def bifurcated_attn_decode(q, Kc, Vc, Kd, Vd, lens, out=None, lse=None, *, scale
 
 
 def bifurcated_attn_decode_append(q, k_new, v_new, Kc, Vc, Kd, Vd, lens, out=None, lse=None, *,
-                                  scale=None, workspace=None, stream=None, flags=0):
+                                  scale=None, workspace=None, stream=None, flags=0, k_scale=1.0,
+                                  v_scale=1.0):
     """KV append + bifurcated decode step in one call (include/bifattn.h):
     writes k_new/v_new [b,g,n,d] into Kd/Vd at lens[i].., attends with
     lens + n, and advances ``lens`` (device int32) in place.  q [b,h,d]
     (n = 1) or [b,h,n,d]."""
     lib = _lib if _lib is not None else load_library()
     _fast_check((q, Kc, Vc, Kd, Vd, lens), q.dtype, q.device)
-    _check(dict(k_new=k_new, v_new=v_new), q.dtype, q.device)
+    _check(dict(k_new=k_new, v_new=v_new), Kd.dtype, q.device)
     if lens.dtype != torch.int32:
         raise ValueError("lens must be int32")
-    prob = _cached_problem(q, Kc, Kd, scale, flags)
+    prob = _cached_problem(q, Kc, Kd, scale, flags, k_scale, v_scale)
     n = max(prob.n_tok, 1)
     exp = (Kd.shape[0], Kd.shape[1], n, Kd.shape[3])
     if tuple(k_new.shape) != exp or tuple(v_new.shape) != exp:
@@ -378,13 +399,14 @@ def bifurcated_attn_decode_append(q, k_new, v_new, Kc, Vc, Kd, Vd, lens, out=Non
 
 
 def bifurcated_attn_decode_append_host(hq, hk_new, hv_new, hout, dev, *, hlens=None, hlse=None,
-                                       scale=None, stream=None, flags=0):
+                                       scale=None, stream=None, flags=0, k_scale=1.0,
+                                       v_scale=1.0):
     """One serving step with host tensors in and out (include/bifattn.h):
     ``dev`` holds the resident caches and staging buffers {q, k_new, v_new,
     Kc, Vc, Kd, Vd, lens, out, lse?, workspace}.  Synchronise before reading
     ``hout``."""
     lib = _lib if _lib is not None else load_library()
-    prob = _cached_problem(hq, dev["Kc"], dev["Kd"], scale, flags)
+    prob = _cached_problem(hq, dev["Kc"], dev["Kd"], scale, flags, k_scale, v_scale)
     ws = dev["workspace"]
     rc = lib.bifurcated_attn_decode_append_host(
         ctypes.byref(prob), _ptr(hq), _ptr(hk_new), _ptr(hv_new), _ptr(hlens), _ptr(hout),
@@ -418,13 +440,18 @@ def lse_merge(out_parts, lse_parts, out=None, lse=None, *, stream=None):
 
 
 def bifurcated_attn_decode_host(hq, hKc, hVc, hKd, hVd, hlens, hout, dev, *, hlse=None,
-                                scale=None, stream=None, flags=0):
+                                scale=None, stream=None, flags=0, k_scale=1.0, v_scale=1.0):
     """End-to-end call: host (pinned) tensors in, host result out.  ``dev`` is a
     dict of caller-owned device buffers {q,Kc,Vc,Kd,Vd,lens,out,lse,workspace}
     (see make_device_buffers).  Enqueues H2D copies, the kernels and the D2H
     copy on ``stream``; synchronise before reading ``hout``."""
     lib = load_library()
-    prob = _problem_from(hq, hKc, hKd, scale, flags)
+    prob = _problem_from(hq, hKc, hKd, scale, flags, k_scale, v_scale)
+    for name, h in (("q", hq), ("Kc", hKc), ("Vc", hVc), ("Kd", hKd), ("Vd", hVd),
+                    ("lens", hlens), ("out", hout)):
+        dv = dev[name]
+        if dv.numel() * dv.element_size() < h.numel() * h.element_size():
+            raise ValueError(f"device buffer {name} is smaller than its host tensor")
     ws = dev["workspace"]
     rc = lib.bifurcated_attn_decode_host(
         ctypes.byref(prob), _ptr(hq), _ptr(hKc), _ptr(hVc), _ptr(hKd), _ptr(hVd), _ptr(hlens),
@@ -439,10 +466,10 @@ def bifurcated_attn_decode_host(hq, hKc, hVc, hKd, hVd, hlens, hout, dev, *, hls
 def make_device_buffers(hq, hKc, hKd, device, with_lse=False, scale=None, flags=0):
     prob = _problem_from(hq, hKc, hKd, scale, flags)
     e = dict(q=torch.empty(hq.shape, dtype=hq.dtype, device=device),
-             Kc=torch.empty(hKc.shape, dtype=hq.dtype, device=device),
-             Vc=torch.empty(hKc.shape, dtype=hq.dtype, device=device),
-             Kd=torch.empty(hKd.shape, dtype=hq.dtype, device=device),
-             Vd=torch.empty(hKd.shape, dtype=hq.dtype, device=device),
+             Kc=torch.empty(hKc.shape, dtype=hKc.dtype, device=device),
+             Vc=torch.empty(hKc.shape, dtype=hKc.dtype, device=device),
+             Kd=torch.empty(hKd.shape, dtype=hKd.dtype, device=device),
+             Vd=torch.empty(hKd.shape, dtype=hKd.dtype, device=device),
              lens=torch.empty(hq.shape[0], dtype=torch.int32, device=device),
              out=torch.empty(hq.shape, dtype=hq.dtype, device=device),
              workspace=alloc_workspace(prob, device))
@@ -452,11 +479,13 @@ def make_device_buffers(hq, hKc, hKd, device, with_lse=False, scale=None, flags=
 
 
 def replicated_attn_decode(q, K, V, lens, mc, out=None, lse=None, *, scale=None,
-                           workspace=None, stream=None, flags=0):
+                           workspace=None, stream=None, flags=0, k_scale=1.0, v_scale=1.0):
     """Non-bifurcated baseline over the replicated cache K, V [b,g,mc+md_cap,d]:
     sample i attends to positions [0, mc + lens[i])."""
     lib = load_library()
-    _check(dict(q=q, K=K, V=V, lens=lens), q.dtype, q.device)
+    _check(dict(q=q), q.dtype, q.device)
+    _check(dict(K=K, V=V), K.dtype if K.dtype in FP8_DTYPES else q.dtype, q.device)
+    _check(dict(lens=lens), q.dtype, q.device)
     if q.dim() == 4:
         b, h, n, d = q.shape
     else:
@@ -466,7 +495,8 @@ def replicated_attn_decode(q, K, V, lens, mc, out=None, lse=None, *, scale=None,
     g, M = K.shape[1], K.shape[2]
     if not 1 <= mc <= M:
         raise ValueError(f"mc ({mc}) must be in [1, {M}]")
-    prob = make_problem(b, h, g, d, mc, M - mc, q.dtype, scale, flags, n)
+    prob = make_problem(b, h, g, d, mc, M - mc, q.dtype, scale, flags, n, K.dtype, k_scale,
+                        v_scale)
     if out is None:
         out = torch.empty_like(q)
     if workspace is None:

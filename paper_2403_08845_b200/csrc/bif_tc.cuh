@@ -88,6 +88,7 @@ struct BifTcParams {
   int rot;                   // context segments start at tile (blockIdx*rot) mod length (0: in order)
   int cs[bif_max_ctas + 1];  // CTA k streams flat tiles [cs[k], cs[k+1]) of [context | decode]
   float scale_log2;
+  float vscale;              // FP8 KV: out = v_scale * o / l (partials in V-code units); else 1
   int S, Sc;                 // slots per row; decode slots start at Sc
   float* ws_o;               // [b*h][S][128]
   float* ws_ml;              // [b*h][S][2]
@@ -119,11 +120,18 @@ __host__ __device__ constexpr int p_layout(int N) {
 __host__ __device__ constexpr int tmem_cols(int N) {
   return 6 * N <= 32 ? 32 : 6 * N <= 64 ? 64 : 6 * N <= 128 ? 128 : 6 * N <= 256 ? 256 : 512;
 }
-// dynamic smem besides the stages: 2 q + 2 P buffers (256N B each), col-max
-// scratch [4][N], row sums [2][4][N], m_run [2][N], final m [2][N] (floats),
-// lengths [64] ints, barriers (512 B)
-__host__ __device__ constexpr int smem_fixed(int N, int npb) {
-  return (2 + 2 * npb) * 256 * N + 4 * (4 * N + 8 * N + 2 * N + 2 * N) + 256 + 512;
+// FP8 KV (KV8): each tile lands by TMA as E4M3 codes in a raw ring (K 16 KB +
+// V 16 KB, SW128 rows of 128 codes) and the converter warps expand it into the
+// f16 stage the MMAs read.
+constexpr int kRawBytes = 32768;
+constexpr int kNRaw = 2;
+// dynamic smem besides the stages: 2 q + npb P buffers (256N B per q buffer
+// and per P part; P = P_hi | P_lo, or one f16 part with KV8), col-max scratch
+// [4][N], row sums [2][4][N], m_run [2][N], final m [2][N] (floats), lengths
+// [64] ints, barriers (512 B); KV8: the raw ring
+__host__ __device__ constexpr int smem_fixed(int N, int npb, bool kv8 = false) {
+  return (2 + (kv8 ? 1 : 2) * npb) * 256 * N + 4 * (4 * N + 8 * N + 2 * N + 2 * N) + 256 + 512 +
+         (kv8 ? kNRaw * kRawBytes : 0);
 }
 
 // CTA owning flat tile f (the CTA ranges [cs[k], cs[k+1]) are non-empty and
@@ -434,7 +442,7 @@ BA_DEVINL void merge_row(const BifTcParams& P, int gr, int lane, int nctx, int n
     }
     M = Mb;
   }
-  const float inv = 1.f / Lsum;
+  const float inv = P.vscale / Lsum;
   const uint2 packed = make_uint2(pack_bf16x2(acc.x * inv, acc.y * inv),
                                   pack_bf16x2(acc.z * inv, acc.w * inv));
   *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(P.out) + (size_t)gr * bif::kD + lane * 4) = packed;
@@ -491,31 +499,37 @@ struct Prof {
 // MT: multi-token step (P.ntok > 1) — the decode paths carry the per-column
 // intra-step causal bound; compiled out of the single-token kernel (it cost
 // ~1.5 us per C2b step in registers and issue slots).
-template <int N, int SWG, bool MT>
+// KV8: FP8 E4M3 KV cache (f4, reading R19) — the epilogue warps also expand
+// each TMA-landed code tile into an f16 stage and convert q to f16 in place;
+// P enters the PV MMA as ONE f16 operand (11 significant bits, the split is
+// not needed), so O^T has N columns.
+template <int N, int SWG, bool MT, bool KV8 = false>
 __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
     bif_tc_kernel(const __grid_constant__ BifTcParams P) {
   using namespace bif;
   constexpr int NSW = 4 * SWG;               // softmax warps
   constexpr int CPT = N / SWG;               // columns per softmax thread
   constexpr int EPI0 = 4 + NSW;              // first epilogue warp
-  constexpr int NP = 2 * N;                  // P / O^T width: [P_hi | P_lo] columns
+  constexpr int NP = KV8 ? N : 2 * N;        // P / O^T width: [P_hi | P_lo] columns (KV8: P)
   constexpr int W = p_atom(NP);
   constexpr int PRB = 2 * W;
   constexpr int PLBO = kBM * PRB;
   constexpr int PSWM = W == 64 ? 7 : (W == 32 ? 3 : 1);
-  constexpr uint32_t IDESC_QK = tc::idesc_bf16(128, N, 0, 0);
-  constexpr uint32_t IDESC_PV = tc::idesc_bf16(128, NP, 1, 1);
+  constexpr uint32_t IDESC_QK = KV8 ? tc::idesc_f16(128, N, 0, 0) : tc::idesc_bf16(128, N, 0, 0);
+  constexpr uint32_t IDESC_PV = KV8 ? tc::idesc_f16(128, NP, 1, 1) : tc::idesc_bf16(128, NP, 1, 1);
   constexpr uint32_t TMEM_COLS = tmem_cols(N);
-  constexpr int QB = 256 * N;  // bytes of one q buffer / one P buffer
+  constexpr int QB = 256 * N;  // bytes of one q buffer / one P part
+  constexpr int PB = KV8 ? QB : 2 * QB;  // bytes of one P slot
   static_assert(N % 16 == 0 && N >= 16 && N <= 64 && CPT % 8 == 0 && CPT <= 32, "N");
 
   extern __shared__ __align__(1024) uint8_t smem[];
   if (threadIdx.x == 0 && (reinterpret_cast<uintptr_t>(smem) & 1023)) __trap();  // SW128 needs 1 KB
   const int NST = P.nst;
   uint8_t* sm_stage = smem;
-  uint8_t* sm_q = smem + NST * kStageBytes;  // 2 buffers
-  uint8_t* sm_p = sm_q + 2 * QB;             // npb slots of (P_hi, P_lo)
-  float* sm_red = reinterpret_cast<float*>(sm_p + 2 * P.npb * QB);  // [4][N] col max (slow path)
+  uint8_t* sm_raw = smem + NST * kStageBytes;  // KV8: kNRaw code tiles
+  uint8_t* sm_q = sm_raw + (KV8 ? kNRaw * kRawBytes : 0);  // 2 buffers
+  uint8_t* sm_p = sm_q + 2 * QB;             // npb slots of (P_hi, P_lo) / P
+  float* sm_red = reinterpret_cast<float*>(sm_p + P.npb * PB);  // [4][N] col max (slow path)
   float* sm_l = sm_red + 4 * N;                             // [2][4][N] row sums per O buffer
   float* sm_mold = sm_l + 8 * N;                            // [N] running max before a slow path
   float* sm_mfin = sm_mold + 2 * N;                         // [2][N] final max per O buffer
@@ -533,7 +547,10 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
   uint64_t* o_empty = bars + 30;   // [2]  epilogue drained the O buffer
   uint64_t* e_full = bars + 32;    // [2]  softmax wrote row sums / final max
   uint64_t* e_empty = bars + 34;   // [2]  epilogue consumed them
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 36);
+  uint64_t* raw_full = bars + 36;  // [2]  KV8: code tile landed
+  uint64_t* raw_empty = bars + 38; // [2]  KV8: converters read it
+  uint64_t* q_cvt = bars + 40;     // [2]  KV8: q converted to f16
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 44);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   auto tstamp = [&](int slot, unsigned long long tag) {
@@ -546,8 +563,15 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < NST; ++s) {
-      tc::mbar_init(tc::smem_u32(&kv_full[s]), 1);
+      tc::mbar_init(tc::smem_u32(&kv_full[s]), KV8 ? 4 : 1);
       tc::mbar_init(tc::smem_u32(&kv_empty[s]), 1);
+    }
+    if (KV8) {
+      for (int s = 0; s < kNRaw; ++s) {
+        tc::mbar_init(tc::smem_u32(&raw_full[s]), 1);
+        tc::mbar_init(tc::smem_u32(&raw_empty[s]), 4);
+      }
+      for (int s = 0; s < 2; ++s) tc::mbar_init(tc::smem_u32(&q_cvt[s]), 4);
     }
     for (int s = 0; s < 2; ++s) {
       tc::mbar_init(tc::smem_u32(&q_full[s]), 1);
@@ -623,6 +647,17 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
         for (int j = 0; j < s.ntiles; ++j, ++tt) {
           const int z = s.dec ? s.i * P.g + cg : s.c;  // TMA z: group, or sample*g + group
           const int tl = s.dec ? t : ctx_tile(P, s, j);
+          if constexpr (KV8) {
+            // E4M3 codes of the K and V tiles (128 positions x 128 B rows) into
+            // the raw ring; the converter warps fill the f16 stage
+            const int r = tt % kNRaw;
+            tc::mbar_wait_sleep(tc::smem_u32(&raw_empty[r]), ((tt / kNRaw) & 1) ^ 1);
+            const uint32_t bar = tc::smem_u32(&raw_full[r]);
+            tc::mbar_arrive_expect_tx(bar, kRawBytes);
+            const uint32_t dst = tc::smem_u32(sm_raw + r * kRawBytes);
+            tc::tma_load_3d_hint(dst, mk, bar, 0, tl * kBM, z, pol);
+            tc::tma_load_3d_hint(dst + 16384, mv, bar, 0, tl * kBM, z, pol);
+          } else {
           const int st = tt % NST;
           tc::mbar_wait_sleep(tc::smem_u32(&kv_empty[st]), ((tt / NST) & 1) ^ 1, BIF_DBG & 262144);
           pf.mark(2);
@@ -634,6 +669,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
           tc::tma_load_3d_hint(dst + 16384, mk, bar, 64, tl * kBM, z, pol);
           tc::tma_load_3d_hint(dst + 32768, mv, bar, 0, tl * kBM, z, pol);
           tc::tma_load_3d_hint(dst + 49152, mv, bar, 64, tl * kBM, z, pol);
+          }
           // L2 prefetch pf_dist tiles ahead: more bytes in flight than the ring holds
           if (P.pf_dist > 0) {
             const long long wp = (long long)tt + P.pf_dist;
@@ -670,7 +706,8 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
       for (long long w = 0; w < nw; ++sg) {
         const Seg s = seg_at(P, rg, w);
         const uint32_t qbase = q_addr + (sg & 1) * QB;
-        if (BIF_DBG & 16384) tc::mbar_wait_sleep(tc::smem_u32(&q_full[sg & 1]), (sg >> 1) & 1, BIF_DBG & 262144); else tc::mbar_wait(tc::smem_u32(&q_full[sg & 1]), (sg >> 1) & 1);
+        if (KV8) tc::mbar_wait(tc::smem_u32(&q_cvt[sg & 1]), (sg >> 1) & 1);
+        else if (BIF_DBG & 16384) tc::mbar_wait_sleep(tc::smem_u32(&q_full[sg & 1]), (sg >> 1) & 1, BIF_DBG & 262144); else tc::mbar_wait(tc::smem_u32(&q_full[sg & 1]), (sg >> 1) & 1);
         pf.mark(0);
         for (int j = 0; j < s.ntiles; ++j, ++u) {
           const uint32_t st = u % NST;
@@ -724,7 +761,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
           const uint32_t vbase = tc::smem_u32(sm_stage + st * kStageBytes + 32768);
           // P = P_hi + P_lo (two bf16 parts side by side): one MMA per K step
           // gives [O_hi | O_lo]^T += V^T [P_hi | P_lo]^T, V read once
-          const uint32_t pbase = p_addr + 2 * ps * QB;
+          const uint32_t pbase = p_addr + ps * PB;
 #pragma unroll
           for (int k = 0; k < ((BIF_DBG & 32) ? 0 : 8); ++k) {
             const uint64_t ad = tc::smem_desc(vbase + k * 2048, 16384, 1024, tc::kSw128);
@@ -864,14 +901,14 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
 #pragma unroll
               for (int k = 0; k < kNarrowP; ++k) {
                 if (k < P.p && alpha[k] != 1.f) {
-                  uint32_t o1, o2;
+                  uint32_t o1, o2 = 0;
                   tc::tmem_ld<1>(tOb + cv0 + k + lane_addr, &o1);
-                  tc::tmem_ld<1>(tOb + N + cv0 + k + lane_addr, &o2);
+                  if (!KV8) tc::tmem_ld<1>(tOb + N + cv0 + k + lane_addr, &o2);
                   tc::tmem_ld_wait();
                   o1 = __float_as_uint(__uint_as_float(o1) * alpha[k]);
                   o2 = __float_as_uint(__uint_as_float(o2) * alpha[k]);
                   tc::tmem_st<1>(tOb + cv0 + k + lane_addr, &o1);
-                  tc::tmem_st<1>(tOb + N + cv0 + k + lane_addr, &o2);
+                  if (!KV8) tc::tmem_st<1>(tOb + N + cv0 + k + lane_addr, &o2);
                 }
               }
               tc::tmem_st_wait();
@@ -880,7 +917,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
             // P row of this position (hi and lo parts): zeros except the p valid columns
             pf.mark(3);
             if (!(BIF_DBG & 8)) tc::mbar_wait(tc::smem_u32(&p_empty[ps]), (ph & 1) ^ 1);  // PV(u-npb) done
-            uint8_t* const sm_pb = sm_p + 2 * ps * QB;
+            uint8_t* const sm_pb = sm_p + ps * PB;
             pf.mark(4);
 #pragma unroll
             for (int n = 0; n < NP; n += 8) {
@@ -892,15 +929,19 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
             for (int k = 0; k < kNarrowP; ++k) {
               if (k < P.p) {
                 const int col = cv0 + k;
-                const __nv_bfloat16 hi = __float2bfloat16_rn(pv[k]);
-                const __nv_bfloat16 lo = __float2bfloat16_rn(pv[k] - __bfloat162float(hi));
                 l_g[k] += pv[k];
                 uint32_t off = (uint32_t)((col / W) * PLBO + pos * PRB + (col % W) * 2);
                 off ^= ((off >> 7) & PSWM) << 4;
-                uint32_t offl = (uint32_t)(((N + col) / W) * PLBO + pos * PRB + ((N + col) % W) * 2);
-                offl ^= ((offl >> 7) & PSWM) << 4;
-                *reinterpret_cast<__nv_bfloat16*>(sm_pb + off) = hi;
-                *reinterpret_cast<__nv_bfloat16*>(sm_pb + offl) = lo;
+                if constexpr (KV8) {
+                  *reinterpret_cast<__half*>(sm_pb + off) = __float2half_rn(pv[k]);
+                } else {
+                  const __nv_bfloat16 hi = __float2bfloat16_rn(pv[k]);
+                  const __nv_bfloat16 lo = __float2bfloat16_rn(pv[k] - __bfloat162float(hi));
+                  uint32_t offl = (uint32_t)(((N + col) / W) * PLBO + pos * PRB + ((N + col) % W) * 2);
+                  offl ^= ((offl >> 7) & PSWM) << 4;
+                  *reinterpret_cast<__nv_bfloat16*>(sm_pb + off) = hi;
+                  *reinterpret_cast<__nv_bfloat16*>(sm_pb + offl) = lo;
+                }
               }
             }
             tc::fence_proxy_async_smem();
@@ -1077,17 +1118,17 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
               for (int n = 0; n < CPT; n += 8) {
                 uint32_t orr[8], orl[8];
                 tc::tmem_ld<8>(tOb + col0 + n + lane_addr, orr);
-                tc::tmem_ld<8>(tOb + N + col0 + n + lane_addr, orl);
+                if (!KV8) tc::tmem_ld<8>(tOb + N + col0 + n + lane_addr, orl);
                 tc::tmem_ld_wait();
 #pragma unroll
                 for (int e = 0; e < 8; ++e) {
                   const float mo = sm_mold[col0 + n + e];
                   const float a = (mo == kNegInf) ? 1.f : ex2(mo - mr[n + e]);
                   orr[e] = __float_as_uint(__uint_as_float(orr[e]) * a);
-                  orl[e] = __float_as_uint(__uint_as_float(orl[e]) * a);
+                  if (!KV8) orl[e] = __float_as_uint(__uint_as_float(orl[e]) * a);
                 }
                 tc::tmem_st<8>(tOb + col0 + n + lane_addr, orr);
-                tc::tmem_st<8>(tOb + N + col0 + n + lane_addr, orl);
+                if (!KV8) tc::tmem_st<8>(tOb + N + col0 + n + lane_addr, orl);
               }
               tc::tmem_st_wait();
               tc::tc_fence_before();
@@ -1097,10 +1138,25 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
           //      bits) into shared memory; fp32 row sums ----
           pf.mark(3);
           if (!(BIF_DBG & 4)) tc::mbar_wait(tc::smem_u32(&p_empty[ps]), (ph & 1) ^ 1);  // PV(u-npb) done
-          uint8_t* const sm_pb = sm_p + 2 * ps * QB;
+          uint8_t* const sm_pb = sm_p + ps * PB;
           pf.mark(4);
 #pragma unroll
           for (int n = 0; n < CPT; n += 8) {
+            if constexpr (KV8) {  // one f16 part
+              uint32_t hk[4];
+#pragma unroll
+              for (int e = 0; e < 8; e += 2) {
+                const float p0 = ex2(x[n + e]), p1 = ex2(x[n + e + 1]);
+                l_part[n + e] += p0;
+                l_part[n + e + 1] += p1;
+                hk[e / 2] = pack_f16x2(p0, p1);
+              }
+              const int col = col0 + n;
+              uint32_t off = (uint32_t)((col / W) * PLBO + pos * PRB + (col % W) * 2);
+              off ^= ((off >> 7) & PSWM) << 4;
+              *reinterpret_cast<uint4*>(sm_pb + off) = make_uint4(hk[0], hk[1], hk[2], hk[3]);
+              continue;
+            }
             uint32_t hk[4], lk[4];
 #pragma unroll
             for (int e = 0; e < 8; e += 2) {
@@ -1153,16 +1209,15 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
     pf.mark(6);
     if (threadIdx.x == 128 || threadIdx.x == 256)
       pf.dump(P.trace ? P.trace + (size_t)blockIdx.x * kTraceSlots : nullptr, threadIdx.x == 128 ? 0 : 8);
-  } else if (warp >= EPI0) {
+  } else if (warp >= EPI0 && warp < EPI0 + 4) {
     // ===================== epilogue warpgroup (4 warps) =====================
     // O^T lanes are d = 32*(warp%4) + lane; columns are the chunk's rows.
     const int quad = warp & 3;
     const int d = quad * 32 + lane;
     const int et = threadIdx.x - 32 * EPI0;  // 0..127
     const uint32_t lane_addr = (uint32_t)(quad * 32) << 16;
-    uint32_t sg = 0;
-    for (long long w = 0; w < nw; ++sg) {
-      const Seg s = seg_at(P, rg, w);
+    // drain(s, sg): O^T of segment part s (the sg-th of this CTA) -> workspace
+    auto drain = [&](const Seg& s, uint32_t sg) {
       const uint32_t ob = sg & 1;
       if (BIF_DBG & 8192) tc::mbar_wait_sleep(tc::smem_u32(&o_full[ob]), (sg >> 1) & 1, BIF_DBG & 262144);
       else tc::mbar_wait(tc::smem_u32(&o_full[ob]), (sg >> 1) & 1);
@@ -1186,7 +1241,12 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
         uint32_t orr[16], orl[16];
         if (!(BIF_DBG & 2097152)) {
           tc::tmem_ld<16>(tO + ob * NP + n + lane_addr, orr);
-          tc::tmem_ld<16>(tO + ob * NP + N + n + lane_addr, orl);
+          if (KV8) {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) orl[e] = 0u;  // +0.0f
+          } else {
+            tc::tmem_ld<16>(tO + ob * NP + N + n + lane_addr, orl);
+          }
           tc::tmem_ld_wait();
         } else {
 #pragma unroll
@@ -1223,7 +1283,86 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
       }
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(tc::smem_u32(&e_empty[ob]));
-      w = s.next;
+    };
+    if constexpr (!KV8) {
+      uint32_t sg = 0;
+      for (long long w = 0; w < nw; ++sg) {
+        const Seg s = seg_at(P, rg, w);
+        drain(s, sg);
+        w = s.next;
+      }
+    } else {
+      // ---- KV8: these warps are also the converters.  Per segment: q (bf16
+      // -> f16 in place); per tile: the E4M3 codes of the raw ring -> the f16
+      // stage in the layout the MMAs read (two 64-column SW128 halves).  The
+      // previous segment is drained after this segment's first two tiles are
+      // converted (the MMAs work on them meanwhile).  A warp instruction
+      // covers 8 rows x 4 chunks of 16 codes: no bank conflicts. ----
+      const int cw = quad;  // rows [32 cw, 32 cw + 32) of every tile
+      uint32_t u = 0, sg = 0;
+      Seg prev;
+      bool pending = false;
+      for (long long w = 0; w < nw; ++sg) {
+        const Seg s = seg_at(P, rg, w);
+        const uint32_t qbuf = sg & 1;
+        tc::mbar_wait(tc::smem_u32(&q_full[qbuf]), (sg >> 1) & 1);
+        uint4* qv = reinterpret_cast<uint4*>(sm_q + qbuf * QB);
+        for (int i = et; i < QB / 16; i += 128) {
+          uint4 v = qv[i];
+          v.x = pack_f16x2(bf16lo(v.x), bf16hi(v.x));
+          v.y = pack_f16x2(bf16lo(v.y), bf16hi(v.y));
+          v.z = pack_f16x2(bf16lo(v.z), bf16hi(v.z));
+          v.w = pack_f16x2(bf16lo(v.w), bf16hi(v.w));
+          qv[i] = v;
+        }
+        tc::fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(tc::smem_u32(&q_cvt[qbuf]));
+        for (int j = 0; j < s.ntiles; ++j, ++u) {
+          const int r = u % kNRaw, st = u % NST;
+          tc::mbar_wait(tc::smem_u32(&raw_full[r]), (u / kNRaw) & 1);
+          tc::mbar_wait(tc::smem_u32(&kv_empty[st]), ((u / NST) & 1) ^ 1);
+          const uint8_t* src = sm_raw + r * kRawBytes;
+          uint8_t* dst = sm_stage + st * kStageBytes;
+#pragma unroll 4
+          for (int it = 0; it < 16; ++it) {
+            const int kv = it >> 3;              // 0: K, 1: V
+            const int i8 = it & 7;
+            const int R = 32 * cw + 8 * (i8 >> 1) + (lane >> 2);  // position row
+            const int c = 4 * (i8 & 1) + (lane & 3);              // 16-code chunk
+            const uint4 v = *reinterpret_cast<const uint4*>(src + kv * 16384 + R * 128 +
+                                                            ((c ^ (R & 7)) << 4));
+            uint4 a, b;
+            a.x = e4m3x2_to_f16x2(v.x);
+            a.y = e4m3x2_to_f16x2(v.x >> 16);
+            a.z = e4m3x2_to_f16x2(v.y);
+            a.w = e4m3x2_to_f16x2(v.y >> 16);
+            b.x = e4m3x2_to_f16x2(v.z);
+            b.y = e4m3x2_to_f16x2(v.z >> 16);
+            b.z = e4m3x2_to_f16x2(v.w);
+            b.w = e4m3x2_to_f16x2(v.w >> 16);
+            uint8_t* d8 = dst + kv * 32768 + (c >> 2) * 16384 + R * 128;
+            const int cc = 2 * (c & 3);
+            *reinterpret_cast<uint4*>(d8 + ((cc ^ (R & 7)) << 4)) = a;
+            *reinterpret_cast<uint4*>(d8 + (((cc + 1) ^ (R & 7)) << 4)) = b;
+          }
+          tc::fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tc::mbar_arrive(tc::smem_u32(&kv_full[st]));
+            tc::mbar_arrive(tc::smem_u32(&raw_empty[r]));
+          }
+          if (pending && (j == 1 || j == s.ntiles - 1)) {
+            drain(prev, sg - 1);
+            pending = false;
+          }
+        }
+        if (pending) drain(prev, sg - 1);
+        prev = s;
+        pending = true;
+        w = s.next;
+      }
+      if (pending) drain(prev, sg - 1);
     }
   }
   tc::tc_fence_before();

@@ -141,6 +141,8 @@ struct Plan {
   size_t off_o = 0, off_ml = 0, ws_bytes = 0;
   int launches = 0;
   int ntok = 1;  // query tokens per (sample, head) row group (multi-token step)
+  bool kv8 = false;  // FP8 E4M3 KV cache (f4)
+  int kv_elem = 0;   // bytes per KV element
 };
 
 // bifurcated_attn_decode_append: this step's K/V rows and the lens update.
@@ -213,6 +215,8 @@ int pick_rb(int rows) { return rows >= 4 ? 4 : (rows >= 2 ? 2 : 1); }
 int validate(const ba_problem_t* pr) {
   if (!pr) return BA_ENULL;
   if (pr->dtype != BA_BF16 && pr->dtype != BA_FP32) return BA_EDTYPE;
+  // FP8 KV cache (f4, reading R19): q / out stay bf16
+  if (pr->kv_dtype == BA_FP8_E4M3 && pr->dtype != BA_BF16) return BA_EDTYPE;
   if (pr->b < 1 || pr->h < 1 || pr->g < 1 || pr->mc < 1 || pr->md_cap < 0) return BA_EINVAL;
   if (pr->h % pr->g != 0) return BA_EINVAL;
   if (pr->n_tok < 0 || pr->n_tok > 128 || (long long)pr->h * (pr->n_tok > 1 ? pr->n_tok : 1) > (1 << 20))
@@ -246,6 +250,8 @@ int make_plan(const ba_problem_t* pr_in, int sms, bool replicated, Plan* pl) {
   P.D = pr->d;
   P.bf16 = pr->dtype == BA_BF16;
   P.elem = P.bf16 ? 2 : 4;
+  P.kv8 = pr->kv_dtype == BA_FP8_E4M3;
+  P.kv_elem = P.kv8 ? 1 : P.elem;
   P.replicated = replicated;
   const int b = pr->b, h = pr->h, g = pr->g, p = h / g;
   const int target = 4 * sms;  // CTAs of 128 threads per launch (~4 per SM)
@@ -261,6 +267,7 @@ int make_plan(const ba_problem_t* pr_in, int sms, bool replicated, Plan* pl) {
     const int want = R < 32 ? R : 32;
     for (int N : cands) {
       if (N % p) continue;
+      if (P.kv8 && (N > 32 || P.ntok > 1)) continue;  // FP8 tensor-core kernel: N = 16 / 32, n = 1
       if (!tcN) tcN = N;  // smallest legal
       if (N >= want) {
         tcN = N;
@@ -278,7 +285,7 @@ int make_plan(const ba_problem_t* pr_in, int sms, bool replicated, Plan* pl) {
   // 58.7 us: a 128-row pass costs more than a 32-row swap-AB pass).  BA_FLAG_CTX_ROWS forces it (any R), BA_FLAG_NO_CTX_ROWS or
   // BIFATTN_CTX_ROWS=0 keep the single fused launch.
   const bool want_rows = ((pr->flags & BA_FLAG_CTX_ROWS) || R >= 64 || ctx_rows_env == 2) &&
-                         !(pr->flags & BA_FLAG_NO_CTX_ROWS);
+                         !(pr->flags & BA_FLAG_NO_CTX_ROWS) && !P.kv8;
   if (tcN && !replicated && ctx_rows_env && want_rows) {
     // context branch on the rows-on-M kernel; the fused kernel streams only
     // the decode tiles, so its N just has to hold p (smallest legal)
@@ -329,15 +336,15 @@ int make_plan(const ba_problem_t* pr_in, int sms, bool replicated, Plan* pl) {
     if (P.tc_T == 0) P.tc_G = gmax;  // no tiles (ctx_rows, md_cap = 0): the merge only
     // P double-buffered when that keeps the K/V stage count (else one slot)
     P.tc_npb = 2;
-    if ((227 * 1024 - ba::bif::smem_fixed(tcN, 2)) / ba::bif::kStageBytes <
-        (227 * 1024 - ba::bif::smem_fixed(tcN, 1)) / ba::bif::kStageBytes)
+    if ((227 * 1024 - ba::bif::smem_fixed(tcN, 2, P.kv8)) / ba::bif::kStageBytes <
+        (227 * 1024 - ba::bif::smem_fixed(tcN, 1, P.kv8)) / ba::bif::kStageBytes)
       P.tc_npb = 1;
     static const int npb_env = knob_i("BIFATTN_NPB", 0);  // experiment override: BIFATTN_NPB=1|2
     if (npb_env == 1 || npb_env == 2) P.tc_npb = npb_env;
-    const int avail = 227 * 1024 - ba::bif::smem_fixed(tcN, P.tc_npb);  // dynamic smem is 1 KB aligned
+    const int avail = 227 * 1024 - ba::bif::smem_fixed(tcN, P.tc_npb, P.kv8);  // dynamic smem is 1 KB aligned
     P.tc_nst = avail / ba::bif::kStageBytes;
     if (P.tc_nst > 4) P.tc_nst = 4;
-    P.tc_smem = P.tc_nst * ba::bif::kStageBytes + ba::bif::smem_fixed(tcN, P.tc_npb);
+    P.tc_smem = P.tc_nst * ba::bif::kStageBytes + ba::bif::smem_fixed(tcN, P.tc_npb, P.kv8);
     const int gpc = tcN / p;  // groups per decode chunk
     const int ndc = (g + gpc - 1) / gpc;
     // context bands (ctx_unit, bif_tc.cuh): with several row chunks per group
@@ -485,15 +492,15 @@ int make_plan(const ba_problem_t* pr_in, int sms, bool replicated, Plan* pl) {
   return BA_OK;
 }
 
-template <typename T, int D>
+template <typename T, int D, typename TK = T>
 int launch_fma_rb(int rb, int grid, const ba::FmaParams& fp, LaunchRec& rec) {
   if (grid <= 0) return BA_OK;
   cudaStream_t st = rec.st;
   rec.begin();
   switch (rb) {
-    case 1: ba::fma_partial_kernel<T, D, 1><<<grid, 128, 0, st>>>(fp); break;
-    case 2: ba::fma_partial_kernel<T, D, 2><<<grid, 128, 0, st>>>(fp); break;
-    default: ba::fma_partial_kernel<T, D, 4><<<grid, 128, 0, st>>>(fp); break;
+    case 1: ba::fma_partial_kernel<T, D, 1, TK><<<grid, 128, 0, st>>>(fp); break;
+    case 2: ba::fma_partial_kernel<T, D, 2, TK><<<grid, 128, 0, st>>>(fp); break;
+    default: ba::fma_partial_kernel<T, D, 4, TK><<<grid, 128, 0, st>>>(fp); break;
   }
   return rec.end();
 }
@@ -558,15 +565,19 @@ int cached_plan(const ba_problem_t* pr, int sms, bool replicated, const Plan** o
   return BA_OK;
 }
 
+// bf16 maps: box (64, box1, box2) = 128-byte rows; u8 maps (FP8 codes):
+// box (128, box1, box2), also 128-byte rows.  Both 128-byte swizzled.
 int encode_tmap_3d(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64_t d2,
-                 uint64_t stride1_bytes, uint64_t stride2_bytes, uint32_t box1, uint32_t box2) {
+                 uint64_t stride1_bytes, uint64_t stride2_bytes, uint32_t box1, uint32_t box2,
+                 bool u8) {
   EncodeTiledFn fn = get_encode_fn();
   if (!fn) return BA_ECUDA;
   cuuint64_t dims[3] = {d0, d1, d2};
   cuuint64_t strides[2] = {stride1_bytes, stride2_bytes};
-  cuuint32_t box[3] = {64, box1, box2};
+  cuuint32_t box[3] = {u8 ? 128u : 64u, box1, box2};
   cuuint32_t estr[3] = {1, 1, 1};
-  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides,
+  CUresult r = fn(m, u8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3,
+                  const_cast<void*>(base), dims, strides,
                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
@@ -580,27 +591,29 @@ struct TmapEntry {
   const void* base;
   uint64_t d0, d1, d2, s1, s2;
   uint32_t b1, b2;
+  bool u8;
   CUtensorMap map;
 };
 thread_local TmapEntry g_tmap_cache[16];
 thread_local int g_tmap_n = 0, g_tmap_next = 0;
 
 int make_tmap_3d(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64_t d2,
-                 uint64_t stride1_bytes, uint64_t stride2_bytes, uint32_t box1, uint32_t box2) {
+                 uint64_t stride1_bytes, uint64_t stride2_bytes, uint32_t box1, uint32_t box2,
+                 bool u8 = false) {
   for (int k = 0; k < g_tmap_n; ++k) {
     const TmapEntry& e = g_tmap_cache[k];
     if (e.base == base && e.d0 == d0 && e.d1 == d1 && e.d2 == d2 && e.s1 == stride1_bytes &&
-        e.s2 == stride2_bytes && e.b1 == box1 && e.b2 == box2) {
+        e.s2 == stride2_bytes && e.b1 == box1 && e.b2 == box2 && e.u8 == u8) {
       *m = e.map;
       return BA_OK;
     }
   }
-  const int rc = encode_tmap_3d(m, base, d0, d1, d2, stride1_bytes, stride2_bytes, box1, box2);
+  const int rc = encode_tmap_3d(m, base, d0, d1, d2, stride1_bytes, stride2_bytes, box1, box2, u8);
   if (rc) return rc;
   TmapEntry& e = g_tmap_cache[g_tmap_next];
   g_tmap_next = (g_tmap_next + 1) & 15;
   if (g_tmap_n < 16) ++g_tmap_n;
-  e = TmapEntry{base, d0, d1, d2, stride1_bytes, stride2_bytes, box1, box2, *m};
+  e = TmapEntry{base, d0, d1, d2, stride1_bytes, stride2_bytes, box1, box2, u8, *m};
   return BA_OK;
 }
 
@@ -624,10 +637,10 @@ int ensure_smem_attr(Kern* fn, int bytes, bool* done) {
   return BA_OK;
 }
 
-template <int N, int SWG, bool MT>
+template <int N, int SWG, bool MT, bool KV8 = false>
 int launch_bif_tc_n(const ba::BifTcParams& bp, int smem, uint32_t flags, LaunchRec& rec) {
   static bool attr_done[64];
-  if (int rc = ensure_smem_attr(ba::bif_tc_kernel<N, SWG, MT>, 227 * 1024, attr_done)) return rc;
+  if (int rc = ensure_smem_attr(ba::bif_tc_kernel<N, SWG, MT, KV8>, 227 * 1024, attr_done)) return rc;
   // one cooperative launch (all CTAs co-resident: the kernel ends with a grid
   // barrier and the LSE merge); programmatic stream serialisation lets its
   // prologue overlap the previous kernel on the stream
@@ -645,7 +658,7 @@ int launch_bif_tc_n(const ba::BifTcParams& bp, int smem, uint32_t flags, LaunchR
   cfg.attrs = attr;
   cfg.numAttrs = 2;
   rec.begin();
-  cudaError_t e = cudaLaunchKernelEx(&cfg, ba::bif_tc_kernel<N, SWG, MT>, bp);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, ba::bif_tc_kernel<N, SWG, MT, KV8>, bp);
   if (e != cudaSuccess) {
     g_last_cuda_error = (int)e;
     rec.end();
@@ -664,16 +677,17 @@ int run_tc(const ba_problem_t* pr, const Plan& P, const void* q, const void* Kc,
   const int p = pr->h / pr->g;
   const uint64_t d = 128;
   int rc = BA_OK;
+  const uint64_t ek = P.kv8 ? 1 : 2;  // bytes per KV element
   if (P.tc_Tc > 0) {
-    rc = make_tmap_3d(&bp.tmKc, Kc, d, pr->mc, pr->g, d * 2, (uint64_t)pr->mc * d * 2, 128, 1);
-    if (!rc) rc = make_tmap_3d(&bp.tmVc, Vc, d, pr->mc, pr->g, d * 2, (uint64_t)pr->mc * d * 2, 128, 1);
+    rc = make_tmap_3d(&bp.tmKc, Kc, d, pr->mc, pr->g, d * ek, (uint64_t)pr->mc * d * ek, 128, 1, P.kv8);
+    if (!rc) rc = make_tmap_3d(&bp.tmVc, Vc, d, pr->mc, pr->g, d * ek, (uint64_t)pr->mc * d * ek, 128, 1, P.kv8);
     if (!rc) rc = make_tmap_3d(&bp.tmQc, q, d, pr->h, pr->b, d * 2, (uint64_t)pr->h * d * 2, p, P.tc_N / p);
   }
   if (!rc && P.tc_T > P.tc_Tc) {
     const uint64_t ds = (uint64_t)P.dec_stride;
     const uint64_t bg = (uint64_t)pr->b * pr->g;
-    rc = make_tmap_3d(&bp.tmKd, Kd, d, ds, bg, d * 2, ds * d * 2, 128, 1);
-    if (!rc) rc = make_tmap_3d(&bp.tmVd, Vd, d, ds, bg, d * 2, ds * d * 2, 128, 1);
+    rc = make_tmap_3d(&bp.tmKd, Kd, d, ds, bg, d * ek, ds * d * ek, 128, 1, P.kv8);
+    if (!rc) rc = make_tmap_3d(&bp.tmVd, Vd, d, ds, bg, d * ek, ds * d * ek, 128, 1, P.kv8);
     if (!rc)
       rc = make_tmap_3d(&bp.tmQd, q, d, pr->h, pr->b, d * 2, (uint64_t)pr->h * d * 2,
                         std::min(P.tc_N, pr->h), 1);
@@ -701,6 +715,7 @@ int run_tc(const ba_problem_t* pr, const Plan& P, const void* q, const void* Kc,
   memcpy(bp.cs, P.tc_cs, sizeof(int) * (P.tc_G + 1));
   bp.ext_ctx = P.ctx_rows ? P.cr_nsplit : 0;
   bp.scale_log2 = scale_log2;
+  bp.vscale = (P.kv8 && pr->v_scale > 0.f) ? pr->v_scale : 1.f;
   bp.S = P.S; bp.Sc = P.tc_Sc;
   bp.ws_o = reinterpret_cast<float*>(static_cast<char*>(ws) + P.off_o);
   bp.ws_ml = reinterpret_cast<float*>(static_cast<char*>(ws) + P.off_ml);
@@ -781,6 +796,7 @@ int run_tc(const ba_problem_t* pr, const Plan& P, const void* q, const void* Kc,
       mp.b = pr->b;
       mp.lens_add = ap ? ap->n : 0;
       mp.dec_cap = P.dec_cap;
+      mp.vscale = 1.f;
       rec.begin();
       ba::merge_kernel<__nv_bfloat16, 128><<<cdiv(mp.rows, 8), 256, 0, st>>>(mp);
       return rec.end();
@@ -789,6 +805,13 @@ int run_tc(const ba_problem_t* pr, const Plan& P, const void* q, const void* Kc,
   // softmax warpgroups (override for experiments: BIFATTN_SWG=1|2)
   static const int swg_env = knob_i("BIFATTN_SWG", 0);
   const int swg = (swg_env == 1 || swg_env == 2 || (swg_env == 4 && P.tc_N == 32)) ? swg_env : ba::bif::softmax_wgs(P.tc_N);
+  if (P.kv8) {  // FP8 KV cache (single-token step, N = 16 / 32)
+    switch (P.tc_N) {
+      case 16: return launch_bif_tc_n<16, 2, false, true>(bp, P.tc_smem, pr->flags, rec);
+      case 32: return launch_bif_tc_n<32, 2, false, true>(bp, P.tc_smem, pr->flags, rec);
+    }
+    return BA_EINVAL;
+  }
   if (P.ntok > 1) {  // multi-token kernels (MT): the default warpgroup split only
     switch (P.tc_N) {
       case 16: return launch_bif_tc_n<16, 2, true>(bp, P.tc_smem, pr->flags, rec);
@@ -810,7 +833,7 @@ int run_tc(const ba_problem_t* pr, const Plan& P, const void* q, const void* Kc,
   return BA_EINVAL;
 }
 
-template <typename T, int D>
+template <typename T, int D, typename TK = T>
 int run_plan(const ba_problem_t* pr, const Plan& P, const void* q, const void* Kc,
              const void* Vc, const void* Kd, const void* Vd, const int32_t* lens, void* out,
              float* lse, void* ws, cudaStream_t st,
@@ -829,7 +852,7 @@ int run_plan(const ba_problem_t* pr, const Plan& P, const void* q, const void* K
     ba::AppendParams a;
     a.k_new = ap->k_new; a.v_new = ap->v_new; a.Kd = const_cast<void*>(Kd); a.Vd = const_cast<void*>(Vd);
     a.lens = lens; a.b = b; a.g = g; a.n = ap->n; a.md_cap = P.dec_cap;
-    a.vec_per_row = D * (int)sizeof(T) / 16;
+    a.vec_per_row = D * (int)sizeof(TK) / 16;
     const long long tot = (long long)b * g * ap->n * a.vec_per_row;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)std::max(1ll, std::min((tot + 255) / 256, 4ll * 148)));
@@ -846,7 +869,9 @@ int run_plan(const ba_problem_t* pr, const Plan& P, const void* q, const void* K
       return BA_ECUDA;
     }
   }
-  fp.scale_log2 = scale * ba::kLog2e;
+  // FP8 KV: K = code * k_scale, folded into the logit scale (R19)
+  const float kscale = (P.kv8 && pr->k_scale > 0.f) ? pr->k_scale : 1.f;
+  fp.scale_log2 = scale * kscale * ba::kLog2e;
   fp.nsc = P.nsc; fp.nsd = P.nsd;
   fp.ctx_chunk = P.ctx_chunk; fp.dec_chunk = P.dec_chunk;
   fp.nrb_c = P.nrb_c; fp.nrb_d = P.nrb_d;
@@ -864,14 +889,14 @@ int run_plan(const ba_problem_t* pr, const Plan& P, const void* q, const void* K
   if (P.ctx_mode == 1 && P.nsc > 0) {
     ba::FmaParams f = fp;
     f.n_ctx_items = g * P.nsc * P.nrb_c;
-    rc = launch_fma_rb<T, D>(P.rb_c, f.n_ctx_items, f, rec);
+    rc = launch_fma_rb<T, D, TK>(P.rb_c, f.n_ctx_items, f, rec);
     if (rc) return rc;
   }
   // 2. decode branch (FMA): items b * g * nsd * nrb_d
   if (P.nsd > 0) {
     ba::FmaParams f = fp;
     f.n_ctx_items = 0;
-    rc = launch_fma_rb<T, D>(P.rb_d, b * g * P.nsd * P.nrb_d, f, rec);
+    rc = launch_fma_rb<T, D, TK>(P.rb_d, b * g * P.nsd * P.nrb_d, f, rec);
     if (rc) return rc;
   }
   // 3. merge
@@ -892,23 +917,24 @@ int run_plan(const ba_problem_t* pr, const Plan& P, const void* q, const void* K
   mp.b = b;
   mp.lens_add = ap ? ap->n : 0;
   mp.dec_cap = P.dec_cap;
+  mp.vscale = (P.kv8 && pr->v_scale > 0.f) ? pr->v_scale : 1.f;
   const int warps_per_block = 8;
   rec.begin();
   ba::merge_kernel<T, D><<<cdiv(mp.rows, warps_per_block), 32 * warps_per_block, 0, st>>>(mp);
   return rec.end();
 }
 
-template <typename T>
+template <typename T, typename TK = T>
 int run_d(const ba_problem_t* pr, const Plan& P, const void* q, const void* Kc, const void* Vc,
           const void* Kd, const void* Vd, const int32_t* lens, void* out, float* lse, void* ws,
           cudaStream_t st,
           const AppendArgs* ap = nullptr) {
   switch (pr->d) {
-    case 16: return run_plan<T, 16>(pr, P, q, Kc, Vc, Kd, Vd, lens, out, lse, ws, st, ap);
-    case 32: return run_plan<T, 32>(pr, P, q, Kc, Vc, Kd, Vd, lens, out, lse, ws, st, ap);
-    case 64: return run_plan<T, 64>(pr, P, q, Kc, Vc, Kd, Vd, lens, out, lse, ws, st, ap);
-    case 128: return run_plan<T, 128>(pr, P, q, Kc, Vc, Kd, Vd, lens, out, lse, ws, st, ap);
-    case 256: return run_plan<T, 256>(pr, P, q, Kc, Vc, Kd, Vd, lens, out, lse, ws, st, ap);
+    case 16: return run_plan<T, 16, TK>(pr, P, q, Kc, Vc, Kd, Vd, lens, out, lse, ws, st, ap);
+    case 32: return run_plan<T, 32, TK>(pr, P, q, Kc, Vc, Kd, Vd, lens, out, lse, ws, st, ap);
+    case 64: return run_plan<T, 64, TK>(pr, P, q, Kc, Vc, Kd, Vd, lens, out, lse, ws, st, ap);
+    case 128: return run_plan<T, 128, TK>(pr, P, q, Kc, Vc, Kd, Vd, lens, out, lse, ws, st, ap);
+    case 256: return run_plan<T, 256, TK>(pr, P, q, Kc, Vc, Kd, Vd, lens, out, lse, ws, st, ap);
   }
   return BA_EINVAL;
 }
@@ -964,6 +990,8 @@ int bifurcated_attn_decode(const ba_problem_t* prob, const void* q, const void* 
   if (lse && (reinterpret_cast<uintptr_t>(lse) & 3u)) return BA_EALIGN;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const ba_problem_t E = effective(prob);  // h*n query rows per sample
+  if (P.kv8)
+    return run_d<__nv_bfloat16, ba::e4m3_t>(&E, P, q, Kc, Vc, Kd, Vd, lens, out, lse, workspace, st);
   if (P.bf16)
     return run_d<__nv_bfloat16>(&E, P, q, Kc, Vc, Kd, Vd, lens, out, lse, workspace, st);
   return run_d<float>(&E, P, q, Kc, Vc, Kd, Vd, lens, out, lse, workspace, st);
@@ -990,6 +1018,8 @@ int bifurcated_attn_decode_append(const ba_problem_t* prob, const void* q, const
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const ba_problem_t E = effective(prob);
   const AppendArgs ap{k_new, v_new, lens, ntok_of(prob)};
+  if (P.kv8)
+    return run_d<__nv_bfloat16, ba::e4m3_t>(&E, P, q, Kc, Vc, Kd, Vd, lens, out, lse, workspace, st, &ap);
   if (P.bf16)
     return run_d<__nv_bfloat16>(&E, P, q, Kc, Vc, Kd, Vd, lens, out, lse, workspace, st, &ap);
   return run_d<float>(&E, P, q, Kc, Vc, Kd, Vd, lens, out, lse, workspace, st, &ap);
@@ -1009,9 +1039,10 @@ int bifurcated_attn_decode_append_host(const ba_problem_t* prob, const void* hq,
   rc = device_info(&di);
   if (rc) return rc;
   const size_t e = prob->dtype == BA_BF16 ? 2 : 4;
+  const size_t ekv = prob->kv_dtype == BA_FP8_E4M3 ? 1 : e;
   const size_t d = prob->d, n = ntok_of(prob);
   const size_t nq = (size_t)prob->b * prob->h * n * d * e;
-  const size_t nkv = (size_t)prob->b * prob->g * n * d * e;
+  const size_t nkv = (size_t)prob->b * prob->g * n * d * ekv;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   auto cp = [&](void* dst, const void* src, size_t bytes, cudaMemcpyKind k) -> int {
     if (bytes == 0) return BA_OK;
@@ -1055,6 +1086,8 @@ int replicated_attn_decode(const ba_problem_t* prob, const void* q, const void* 
   if (lse && (reinterpret_cast<uintptr_t>(lse) & 3u)) return BA_EALIGN;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const ba_problem_t E = effective(prob);
+  if (P.kv8)
+    return run_d<__nv_bfloat16, ba::e4m3_t>(&E, P, q, nullptr, nullptr, K, V, lens, out, lse, workspace, st);
   if (P.bf16)
     return run_d<__nv_bfloat16>(&E, P, q, nullptr, nullptr, K, V, lens, out, lse, workspace, st);
   return run_d<float>(&E, P, q, nullptr, nullptr, K, V, lens, out, lse, workspace, st);
@@ -1074,10 +1107,11 @@ int bifurcated_attn_decode_host(const ba_problem_t* prob, const void* hq, const 
   rc = device_info(&di);
   if (rc) return rc;
   const size_t e = prob->dtype == BA_BF16 ? 2 : 4;
+  const size_t ekv = prob->kv_dtype == BA_FP8_E4M3 ? 1 : e;
   const size_t d = prob->d;
   const size_t nq = (size_t)prob->b * prob->h * ntok_of(prob) * d * e;
-  const size_t nc = (size_t)prob->g * prob->mc * d * e;
-  const size_t nd = (size_t)prob->b * prob->g * prob->md_cap * d * e;
+  const size_t nc = (size_t)prob->g * prob->mc * d * ekv;
+  const size_t nd = (size_t)prob->b * prob->g * prob->md_cap * d * ekv;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   auto cp = [&](void* dst, const void* src, size_t n, cudaMemcpyKind k) -> int {
     if (n == 0) return BA_OK;
@@ -1172,6 +1206,10 @@ const char* ba_plan_string(const ba_problem_t* prob) {
              "ctx=fma(nsc=%d,chunk=%d,rb=%d) dec=fma(nsd=%d,chunk=%d,rb=%d) S=%d launches=%d "
              "ws=%zu",
              P.nsc, P.ctx_chunk, P.rb_c, P.nsd, P.dec_chunk, P.rb_d, P.S, P.launches, P.ws_bytes);
+  if (P.kv8) {
+    const size_t n = strlen(g_plan_buf);
+    snprintf(g_plan_buf + n, sizeof g_plan_buf - n, " kv=e4m3");
+  }
   return g_plan_buf;
 }
 
@@ -1254,6 +1292,6 @@ const char* ba_strerror(int code) {
 
 int ba_last_cuda_error(void) { return g_last_cuda_error; }
 
-int ba_version(void) { return 2; }
+int ba_version(void) { return 3; }
 
 }  // extern "C"

@@ -1,6 +1,7 @@
 // common.cuh — small device helpers shared by the bifattn kernels (sm_100a).
 #pragma once
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -23,6 +24,23 @@ BA_DEVINL uint32_t pack_bf16x2(float lo, float hi) {
   uint32_t r;
   asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
   return r;
+}
+
+// Round two fp32 to f16 (RNE) and pack (lo in the low half).
+BA_DEVINL uint32_t pack_f16x2(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+
+// Two FP8 E4M3 codes (bits [0,8) and [8,16) of `two`) -> two f16 (exact:
+// every E4M3 value is an f16 normal or zero), packed lo | hi << 16.
+BA_DEVINL uint32_t e4m3x2_to_f16x2(uint32_t two) {
+  uint32_t h2;
+  asm("{\n .reg .b16 a;\n cvt.u16.u32 a, %1;\n cvt.rn.f16x2.e4m3x2 %0, a;\n}"
+      : "=r"(h2)
+      : "r"(two));
+  return h2;
 }
 
 // Truncate two fp32 to bf16 and pack (lo in the low half): one byte permute

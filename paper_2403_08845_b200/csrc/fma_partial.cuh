@@ -92,20 +92,64 @@ struct Vec<float> {
   }
 };
 
-template <typename T, int D, int RB>
+// FP8 E4M3 cache codes (f4, reading R19): loads decode two codes per
+// cvt.rn.f16x2.e4m3x2 (exact: every E4M3 value is an f16 normal or zero)
+// and widen to fp32; the per-tensor scales are applied outside (k_scale in
+// the logit scale, v_scale in the merge).
+struct e4m3_t {
+  uint8_t bits;
+};
+
+BA_DEVINL void e4m3x2_to_f32(uint32_t two_codes, float& lo, float& hi) {
+  const uint32_t h2 = e4m3x2_to_f16x2(two_codes);
+  lo = __half2float(__ushort_as_half((unsigned short)(h2 & 0xffffu)));
+  hi = __half2float(__ushort_as_half((unsigned short)(h2 >> 16)));
+}
+
+template <>
+struct Vec<e4m3_t> {
+  static constexpr int kVecElems = 16;
+  template <int LW>
+  static BA_DEVINL void load(const e4m3_t* p, float* out) {
+    if constexpr (LW == 8) {
+      const uint2 r = ldg_stream8(p);
+      e4m3x2_to_f32(r.x, out[0], out[1]);
+      e4m3x2_to_f32(r.x >> 16, out[2], out[3]);
+      e4m3x2_to_f32(r.y, out[4], out[5]);
+      e4m3x2_to_f32(r.y >> 16, out[6], out[7]);
+    } else if constexpr (LW == 4) {
+      const uint32_t r = ldg_stream4(p);
+      e4m3x2_to_f32(r, out[0], out[1]);
+      e4m3x2_to_f32(r >> 16, out[2], out[3]);
+    } else if constexpr (LW == 2) {
+      const uint32_t r = *reinterpret_cast<const unsigned short*>(p);
+      e4m3x2_to_f32(r, out[0], out[1]);
+    } else {
+      float unused;
+      e4m3x2_to_f32(p->bits, out[0], unused);
+    }
+  }
+};
+
+// T: element type of q (and out); TK: element type of the KV cache.  Lane j
+// owns elements (ch*16 + j)*LW .. +LW of a row in both, so LW is the smaller
+// vector width of the two.
+template <typename T, int D, int RB, typename TK = T>
 struct FmaCfg {
   static constexpr int kThreads = 128;
   static constexpr int kEPL = D / 16;  // elements per lane per row
-  static constexpr int kLW = Vec<T>::kVecElems < kEPL ? Vec<T>::kVecElems : kEPL;
+  static constexpr int kVW = Vec<T>::kVecElems < Vec<TK>::kVecElems ? Vec<T>::kVecElems
+                                                                     : Vec<TK>::kVecElems;
+  static constexpr int kLW = kVW < kEPL ? kVW : kEPL;
   static constexpr int kNCH = kEPL / kLW;  // loads per row per lane
   static constexpr int kU = 4;             // key steps per warp per iteration
   static constexpr int kKeysPerIter = 4 * 2 * kU;
   static_assert(D % 16 == 0, "D must be a multiple of 16");
 };
 
-template <typename T, int D, int RB>
+template <typename T, int D, int RB, typename TK = T>
 __global__ void __launch_bounds__(128) fma_partial_kernel(const FmaParams P) {
-  using C = FmaCfg<T, D, RB>;
+  using C = FmaCfg<T, D, RB, TK>;
   constexpr int EPL = C::kEPL, LW = C::kLW, NCH = C::kNCH, U = C::kU;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int lg = lane >> 4, j = lane & 15;
@@ -114,8 +158,8 @@ __global__ void __launch_bounds__(128) fma_partial_kernel(const FmaParams P) {
   int it = blockIdx.x;
   int c, r_begin, r_end, t0, t1, slot, row_base;  // rows r -> (r/p)*h + c*p + r%p
   int dec_L = -1, dec_r0 = 0;  // decode item: valid length, first row of the sample
-  const T* Kb;
-  const T* Vb;
+  const TK* Kb;
+  const TK* Vb;
   if (it < P.n_ctx_items) {
     const int rb = it % P.nrb_c;
     const int s = (it / P.nrb_c) % P.nsc;
@@ -125,8 +169,8 @@ __global__ void __launch_bounds__(128) fma_partial_kernel(const FmaParams P) {
     r_end = min(R, r_begin + RB);
     t0 = s * P.ctx_chunk;
     t1 = min(P.mc, t0 + P.ctx_chunk);
-    Kb = reinterpret_cast<const T*>(P.Kc) + (size_t)c * P.mc * D;
-    Vb = reinterpret_cast<const T*>(P.Vc) + (size_t)c * P.mc * D;
+    Kb = reinterpret_cast<const TK*>(P.Kc) + (size_t)c * P.mc * D;
+    Vb = reinterpret_cast<const TK*>(P.Vc) + (size_t)c * P.mc * D;
     slot = s;
     row_base = 0;
   } else {
@@ -147,8 +191,8 @@ __global__ void __launch_bounds__(128) fma_partial_kernel(const FmaParams P) {
     t0 = s * P.dec_chunk;
     t1 = min(L, t0 + P.dec_chunk);
     const size_t base = ((size_t)i * P.g + c) * P.dec_stride * D;
-    Kb = reinterpret_cast<const T*>(P.Kd) + base;
-    Vb = reinterpret_cast<const T*>(P.Vd) + base;
+    Kb = reinterpret_cast<const TK*>(P.Kd) + base;
+    Vb = reinterpret_cast<const TK*>(P.Vd) + base;
     slot = P.dec_slot0 + s;
     row_base = 0;
   }
@@ -209,7 +253,7 @@ __global__ void __launch_bounds__(128) fma_partial_kernel(const FmaParams P) {
       if (tk[u] < t1) {
 #pragma unroll
         for (int ch = 0; ch < NCH; ++ch)
-          Vec<T>::template load<LW>(Kb + (size_t)tk[u] * D + (ch * 16 + j) * LW, kv[u][ch]);
+          Vec<TK>::template load<LW>(Kb + (size_t)tk[u] * D + (ch * 16 + j) * LW, kv[u][ch]);
       } else {
 #pragma unroll
         for (int ch = 0; ch < NCH; ++ch)
@@ -222,7 +266,7 @@ __global__ void __launch_bounds__(128) fma_partial_kernel(const FmaParams P) {
       if (tk[u] < t1) {
 #pragma unroll
         for (int ch = 0; ch < NCH; ++ch)
-          Vec<T>::template load<LW>(Vb + (size_t)tk[u] * D + (ch * 16 + j) * LW, vv[u][ch]);
+          Vec<TK>::template load<LW>(Vb + (size_t)tk[u] * D + (ch * 16 + j) * LW, vv[u][ch]);
       } else {
 #pragma unroll
         for (int ch = 0; ch < NCH; ++ch)

@@ -25,6 +25,7 @@ struct MergeParams {
   float* lse;          // [rows] or null
   int32_t* lens_out;   // append+attend: lens[i] <- min(clamp(lens[i]) + lens_add, dec_cap)
   int b, lens_add, dec_cap;
+  float vscale;        // FP8 KV: partials are in V-code units, out = v_scale * o / L (else 1)
 };
 
 // Number of context partials written for output row gr.
@@ -71,7 +72,7 @@ __global__ void __launch_bounds__(256) merge_kernel(const MergeParams P) {
       if (x < D) acc[e] = fmaf(w, o[(size_t)s * D + x], acc[e]);
     }
   }
-  const float invL = 1.f / L;
+  const float invL = P.vscale / L;
 #pragma unroll
   for (int e = 0; e < EPL; ++e) {
     const int x = e * 32 + lane;

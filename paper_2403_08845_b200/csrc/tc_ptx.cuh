@@ -243,6 +243,12 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, int a_mn, int b_
          ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
+// The same with f16 A and B (formats 0): the FP8-KV kernel's converted tiles.
+__host__ __device__ constexpr uint32_t idesc_f16(int M, int N, int a_mn, int b_mn) {
+  return (1u << 4) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
+         ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
 // Shared-memory matrix descriptor (sm_100 "version 1"): start address >> 4
 // (bits 0-13), leading byte offset >> 4 (16-29), stride byte offset >> 4
 // (32-45), version 1 (bits 46-47), base offset 0 (49-51), lbo mode 0 (52),

@@ -151,3 +151,15 @@ def sample_rows(b, h, n=64, seed=0):
     rows = set([0, b * h - 1, h - 1, (b - 1) * h])
     rows.update(int(x) for x in rng.integers(0, b * h, size=n))
     return sorted(rows)
+
+
+def oracle_kv8_all_rows(inp, rows=None):
+    """Every row (or ``rows``) of an FP8-KV problem (synth kv="e4m3") through
+    the FP8 oracle (oracle_attn_decode_kv8_f64) on all host cores."""
+    import oracle as _o
+
+    out, lse, _ = _o.attn_decode_kv8(inp.q.cpu(), inp.Kc.cpu(), inp.Vc.cpu(), inp.Kd.cpu(),
+                                     inp.Vd.cpu(), inp.lens.cpu(), scale=inp.scale,
+                                     k_scale=inp.k_scale, v_scale=inp.v_scale, rows=rows,
+                                     nthreads=host_cores())
+    return out, lse

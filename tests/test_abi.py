@@ -45,7 +45,7 @@ def test_library_is_sm100a_only():
 
 
 def test_version_and_strerror(lib):
-    assert lib.ba_version() == 2
+    assert lib.ba_version() == 3
     assert b"CPU fallback" in lib.ba_strerror(-6)
     for code in range(0, -8, -1):
         assert lib.ba_strerror(code) != b"unknown error"
