@@ -150,7 +150,7 @@ def test_alg_bytes_matches_eq6():
     """bench.py's byte count = Eq. 6 x (K and V) x element bytes + q/out."""
     for cfg in CONFIGS.values():
         kv = oracle.kv_read_elements(cfg.b, cfg.g, cfg.d, cfg.mc, cfg.md, True)
-        assert alg_bytes(cfg) == 2 * kv * cfg.elem_bytes + 2 * cfg.elem_bytes * cfg.b * cfg.h * cfg.d
+        assert alg_bytes(cfg) == 2 * kv * cfg.kv_bytes + 2 * cfg.elem_bytes * cfg.b * cfg.h * cfg.d
     assert alg_bytes(CONFIGS["mha7b_b32"]) == 268_959_744  # SURVEY §8(d)
     assert alg_bytes(CONFIGS["mha7b_b16"]) == 201_588_736
     assert alg_bytes(CONFIGS["tiny"]) == 13_312
