@@ -53,7 +53,7 @@ from synth import CONFIGS, alg_bytes, alg_flops, make_inputs, seed_for  # noqa: 
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FALLBACK_HBM = 6650.0  # B200_PROFILING.md fallback (GB/s)
 FALLBACK_TF = 1590.0
-OTHERS = ["mha7b_b16", "gqa", "mqa", "long"]
+OTHERS = ["mha7b_b16", "gqa", "mqa", "long", "mha7b_b32_fp8"]
 
 
 def peaks():
@@ -207,10 +207,10 @@ def run_reference(args, cfg):
 # ---------------------------------------------------------------------------
 def kernel_alg_bytes(cfg, name):
     """Algorithmic bytes one launch of kernel `name` must move."""
-    e = cfg.elem_bytes
+    e, ekv = cfg.elem_bytes, cfg.kv_bytes
     qo = cfg.b * cfg.h * cfg.d * e
-    ctx = 2 * cfg.g * cfg.mc * cfg.d * e
-    dec = 2 * cfg.b * cfg.g * cfg.md * cfg.d * e
+    ctx = 2 * cfg.g * cfg.mc * cfg.d * ekv
+    dec = 2 * cfg.b * cfg.g * cfg.md * cfg.d * ekv
     if name.startswith("ctx"):
         return ctx + qo
     if name.startswith("dec"):
@@ -235,9 +235,9 @@ def kernel_alg_flops(cfg, name):
 
 def set_bytes(cfg):
     """HBM footprint of one input set (+ its output)."""
-    e = cfg.elem_bytes
-    return e * (2 * cfg.b * cfg.h * cfg.d + 2 * cfg.g * cfg.mc * cfg.d
-                + 2 * cfg.b * cfg.g * cfg.md * cfg.d)
+    e, ekv = cfg.elem_bytes, cfg.kv_bytes
+    return e * 2 * cfg.b * cfg.h * cfg.d + ekv * (2 * cfg.g * cfg.mc * cfg.d
+                                                 + 2 * cfg.b * cfg.g * cfg.md * cfg.d)
 
 
 def l2_bytes(dev):
@@ -257,8 +257,10 @@ class Case:
         self.l2 = l2_bytes(dev)
         self.nsets = max(2, math.ceil(3 * self.l2 / set_bytes(cfg)))
         self.sets = []
+        self.kv_scales = []  # FP8 cache: (k_scale, v_scale) of each set
         for k in range(self.nsets):
             full = make_inputs(cfg, seed_base + k, device=dev)
+            self.kv_scales.append((full.k_scale, full.v_scale))
             loc = bdist.shard_step(full.q, full.Kc, full.Vc, full.Kd, full.Vd, full.lens, world,
                                    rank, mode)
             loc = [t.contiguous() for t in loc]
@@ -270,7 +272,8 @@ class Case:
         self.lses = [torch.empty(s[0].shape[:-1], dtype=torch.float32, device=dev)
                      for s in self.sets] if mode == "context" else [None] * self.nsets
         self.prob = ba.make_problem(q.shape[0], q.shape[1], Kc.shape[0], cfg.d, Kc.shape[1],
-                                    Kd.shape[2], cfg.torch_dtype, self.scale)
+                                    Kd.shape[2], cfg.torch_dtype, self.scale, kv_dtype=Kc.dtype,
+                                    k_scale=self.kv_scales[0][0], v_scale=self.kv_scales[0][1])
         self.ws = ba.alloc_workspace(self.prob, dev)
         self.L = ba.ba_launches_per_call(self.prob)
         self.names = ba.ba_launch_names(self.prob)
@@ -279,9 +282,11 @@ class Case:
 
     def step(self, k, stream, flags=0):
         s = self.sets[k % self.nsets]
+        ks, vs = self.kv_scales[k % self.nsets]
         self.ba.bifurcated_attn_decode(s[0], s[1], s[2], s[3], s[4], s[5], self.outs[k % self.nsets],
                                        self.lses[k % self.nsets], scale=self.scale,
-                                       workspace=self.ws, stream=stream, flags=flags)
+                                       workspace=self.ws, stream=stream, flags=flags,
+                                       k_scale=ks, v_scale=vs)
 
 
 def ev():
@@ -411,22 +416,25 @@ def replicated(ba, cfg, case, stream, steps):
     except torch.cuda.OutOfMemoryError:
         return {"oom": True}
     o = torch.empty_like(q)
+    ks, vs = case.kv_scales[0]
     for _ in range(3):
-        ba.replicated_attn_decode(q, K, V, lens, cfg.mc, o, scale=case.scale, stream=stream)
+        ba.replicated_attn_decode(q, K, V, lens, cfg.mc, o, scale=case.scale, stream=stream,
+                                  k_scale=ks, v_scale=vs)
     torch.cuda.synchronize()
     r0, r1 = ev(), ev()
     nrep = max(3, min(steps, 20))
     r0.record(stream)
     for _ in range(nrep):
-        ba.replicated_attn_decode(q, K, V, lens, cfg.mc, o, scale=case.scale, stream=stream)
+        ba.replicated_attn_decode(q, K, V, lens, cfg.mc, o, scale=case.scale, stream=stream,
+                                  k_scale=ks, v_scale=vs)
     r1.record(stream)
     torch.cuda.synchronize()
     rep_ms = r0.elapsed_time(r1) / nrep
-    rep_bytes = 2 * cfg.elem_bytes * cfg.d * cfg.g * cfg.b * (cfg.mc + cfg.md) \
+    rep_bytes = 2 * cfg.kv_bytes * cfg.d * cfg.g * cfg.b * (cfg.mc + cfg.md) \
         + 2 * cfg.elem_bytes * cfg.b * cfg.h * cfg.d
     rep = {"us_per_step": rep_ms * 1e3, "kv_bytes_moved": rep_bytes,
            "gbs_of_its_bytes": rep_bytes / (rep_ms * 1e-3) / 1e9}
-    if bool((lens == cfg.md).all()):
+    if bool((lens == cfg.md).all()) and not cfg.kv:
         qs = q.unsqueeze(2)
 
         def sdpa():
@@ -451,13 +459,14 @@ def e2e_runs(ba, cfg, case, dev, stream, barrier, steps):
     """The contract's e2e (all inputs copied from pinned host memory each
     step) and the decode-loop serving view."""
     q, Kc, Vc, Kd, Vd, lens = case.sets[0]
+    ks, vs = case.kv_scales[0]
     pin = lambda t: t.cpu().pin_memory()  # noqa: E731
     hq, hKc, hVc, hKd, hVd, hl = map(pin, (q, Kc, Vc, Kd, Vd, lens))
     hout = torch.empty_like(hq).pin_memory()
     dbuf = ba.make_device_buffers(hq, hKc, hKd, dev, scale=case.scale)
     for _ in range(2):
         ba.bifurcated_attn_decode_host(hq, hKc, hVc, hKd, hVd, hl, hout, dbuf, scale=case.scale,
-                                       stream=stream)
+                                       stream=stream, k_scale=ks, v_scale=vs)
     torch.cuda.synchronize()
     ne = max(2, min(steps, 10))
     barrier()
@@ -466,7 +475,7 @@ def e2e_runs(ba, cfg, case, dev, stream, barrier, steps):
     a0.record(stream)
     for _ in range(ne):
         ba.bifurcated_attn_decode_host(hq, hKc, hVc, hKd, hVd, hl, hout, dbuf, scale=case.scale,
-                                       stream=stream)
+                                       stream=stream, k_scale=ks, v_scale=vs)
     a1.record(stream)
     torch.cuda.synchronize()
     barrier()
@@ -477,8 +486,8 @@ def e2e_runs(ba, cfg, case, dev, stream, barrier, steps):
     # decode loop: caches resident; q, this step's K/V rows and lens copied in,
     # append + attend in one C-ABI call, out copied back
     b, g = Kd.shape[0], Kd.shape[1]
-    hkn = torch.randn(b, g, 1, cfg.d).to(q.dtype).pin_memory()
-    hvn = torch.randn(b, g, 1, cfg.d).to(q.dtype).pin_memory()
+    hkn = torch.randn(b, g, 1, cfg.d).to(Kd.dtype).pin_memory()
+    hvn = torch.randn(b, g, 1, cfg.d).to(Kd.dtype).pin_memory()
     hl1 = (lens.cpu() - 1).clamp_min(0).to(torch.int32).pin_memory()
     cs = torch.cuda.Stream()
     loop_dev = dict(q=torch.empty_like(q), k_new=torch.empty_like(hkn, device=dev),
@@ -488,7 +497,8 @@ def e2e_runs(ba, cfg, case, dev, stream, barrier, steps):
 
     def loop_step():
         ba.bifurcated_attn_decode_append_host(hq, hkn, hvn, hout, loop_dev, hlens=hl1,
-                                              scale=case.scale, stream=cs)
+                                              scale=case.scale, stream=cs, k_scale=ks,
+                                              v_scale=vs)
     for _ in range(2):
         loop_step()
     torch.cuda.synchronize()
@@ -603,7 +613,7 @@ def run_ours(args, cfg):
         torch.distributed.all_reduce(vals, op=torch.distributed.ReduceOp.MAX)
     ms_step, e2e_ms, loop_ms, gather_us, graph_us, p50, p10, p90 = [float(x) for x in vals]
 
-    names, nsets = case.names, case.nsets
+    names, nsets, plan = case.names, case.nsets, case.plan
     others = {}
     if ws == 1 and rank == 0 and not args.no_others and cfg.name == "mha7b_b32":
         del case
@@ -628,7 +638,8 @@ def run_ours(args, cfg):
             "us_per_step": ms_step * 1e3, "us_p10": p10, "us_p50": p50, "us_p90": p90,
             "graph_us_per_step": graph_us if graph_us > 0 else t["graph_us"],
             "higher_is_better": True, "scaling": "strong" if ws > 1 else "weak",
-            "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic",
+            "vs_baseline": None, "dtype": cfg.dtype + ("/e4m3-kv" if cfg.kv else ""),
+            "data": "synthetic",
             "config": {"workload": cfg.name, "b": cfg.b, "h": cfg.h, "g": cfg.g, "d": cfg.d,
                        "mc": cfg.mc, "md": cfg.md, "alg_bytes_per_step": bytes_step,
                        "alg_flops_per_step": alg_flops(cfg),
@@ -636,9 +647,7 @@ def run_ours(args, cfg):
                        "l2": (f"{nsets} rotating input sets of "
                               f"{set_bytes(local_cfg) / 1e6:.1f} MB (>= 3x the "
                               f"{l2_bytes(dev) / 2 ** 20:.0f} MiB L2 between re-reads)"),
-                       "plan": ba.ba_plan_string(ba.make_problem(
-                           local_cfg.b, local_cfg.h, local_cfg.g, cfg.d, local_cfg.mc, cfg.md,
-                           cfg.torch_dtype))},
+                       "plan": plan},
             "frac_of_hbm_peak": value / ws / peak_gbs, "frac_of_8tbs": value / ws / 8000.0,
             "peak_kind": peak_kind,
             "gpu_launches": len(shares) * args.steps,

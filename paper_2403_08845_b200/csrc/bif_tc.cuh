@@ -120,18 +120,16 @@ __host__ __device__ constexpr int p_layout(int N) {
 __host__ __device__ constexpr int tmem_cols(int N) {
   return 6 * N <= 32 ? 32 : 6 * N <= 64 ? 64 : 6 * N <= 128 ? 128 : 6 * N <= 256 ? 256 : 512;
 }
-// FP8 KV (KV8): each tile lands by TMA as E4M3 codes in a raw ring (K 16 KB +
-// V 16 KB, SW128 rows of 128 codes) and the converter warps expand it into the
-// f16 stage the MMAs read.
-constexpr int kRawBytes = 32768;
-constexpr int kNRaw = 2;
+// FP8 KV (KV8): each tile lands by TMA as E4M3 codes (K 16 KB, V 16 KB, SW128
+// rows of 128 codes) in the upper half of its own f16 stage region (K codes
+// at +16 KB, V codes at +48 KB) and the converter warps expand it IN PLACE
+// into the f16 layout the MMAs read: a stage holds codes, then f16.
 // dynamic smem besides the stages: 2 q + npb P buffers (256N B per q buffer
 // and per P part; P = P_hi | P_lo, or one f16 part with KV8), col-max scratch
 // [4][N], row sums [2][4][N], m_run [2][N], final m [2][N] (floats), lengths
-// [64] ints, barriers (512 B); KV8: the raw ring
+// [64] ints, barriers (512 B)
 __host__ __device__ constexpr int smem_fixed(int N, int npb, bool kv8 = false) {
-  return (2 + (kv8 ? 1 : 2) * npb) * 256 * N + 4 * (4 * N + 8 * N + 2 * N + 2 * N) + 256 + 512 +
-         (kv8 ? kNRaw * kRawBytes : 0);
+  return (2 + (kv8 ? 1 : 2) * npb) * 256 * N + 4 * (4 * N + 8 * N + 2 * N + 2 * N) + 256 + 512;
 }
 
 // CTA owning flat tile f (the CTA ranges [cs[k], cs[k+1]) are non-empty and
@@ -526,8 +524,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
   if (threadIdx.x == 0 && (reinterpret_cast<uintptr_t>(smem) & 1023)) __trap();  // SW128 needs 1 KB
   const int NST = P.nst;
   uint8_t* sm_stage = smem;
-  uint8_t* sm_raw = smem + NST * kStageBytes;  // KV8: kNRaw code tiles
-  uint8_t* sm_q = sm_raw + (KV8 ? kNRaw * kRawBytes : 0);  // 2 buffers
+  uint8_t* sm_q = smem + NST * kStageBytes;  // 2 buffers
   uint8_t* sm_p = sm_q + 2 * QB;             // npb slots of (P_hi, P_lo) / P
   float* sm_red = reinterpret_cast<float*>(sm_p + P.npb * PB);  // [4][N] col max (slow path)
   float* sm_l = sm_red + 4 * N;                             // [2][4][N] row sums per O buffer
@@ -547,10 +544,10 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
   uint64_t* o_empty = bars + 30;   // [2]  epilogue drained the O buffer
   uint64_t* e_full = bars + 32;    // [2]  softmax wrote row sums / final max
   uint64_t* e_empty = bars + 34;   // [2]  epilogue consumed them
-  uint64_t* raw_full = bars + 36;  // [2]  KV8: code tile landed
-  uint64_t* raw_empty = bars + 38; // [2]  KV8: converters read it
-  uint64_t* q_cvt = bars + 40;     // [2]  KV8: q converted to f16
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 44);
+  uint64_t* k_cvt = bars + 36;     // [4]  KV8: K of the stage converted to f16
+  uint64_t* v_cvt = bars + 40;     // [4]  KV8: V of the stage converted to f16
+  uint64_t* q_cvt = bars + 44;     // [2]  KV8: q converted to f16
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 48);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   auto tstamp = [&](int slot, unsigned long long tag) {
@@ -563,16 +560,15 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < NST; ++s) {
-      tc::mbar_init(tc::smem_u32(&kv_full[s]), KV8 ? 4 : 1);
+      tc::mbar_init(tc::smem_u32(&kv_full[s]), 1);
       tc::mbar_init(tc::smem_u32(&kv_empty[s]), 1);
-    }
-    if (KV8) {
-      for (int s = 0; s < kNRaw; ++s) {
-        tc::mbar_init(tc::smem_u32(&raw_full[s]), 1);
-        tc::mbar_init(tc::smem_u32(&raw_empty[s]), 4);
+      if (KV8) {
+        tc::mbar_init(tc::smem_u32(&k_cvt[s]), 4);
+        tc::mbar_init(tc::smem_u32(&v_cvt[s]), 4);
       }
-      for (int s = 0; s < 2; ++s) tc::mbar_init(tc::smem_u32(&q_cvt[s]), 4);
     }
+    if (KV8)
+      for (int s = 0; s < 2; ++s) tc::mbar_init(tc::smem_u32(&q_cvt[s]), 4);
     for (int s = 0; s < 2; ++s) {
       tc::mbar_init(tc::smem_u32(&q_full[s]), 1);
       tc::mbar_init(tc::smem_u32(&q_empty[s]), 1);
@@ -649,14 +645,14 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
           const int tl = s.dec ? t : ctx_tile(P, s, j);
           if constexpr (KV8) {
             // E4M3 codes of the K and V tiles (128 positions x 128 B rows) into
-            // the raw ring; the converter warps fill the f16 stage
-            const int r = tt % kNRaw;
-            tc::mbar_wait_sleep(tc::smem_u32(&raw_empty[r]), ((tt / kNRaw) & 1) ^ 1);
-            const uint32_t bar = tc::smem_u32(&raw_full[r]);
-            tc::mbar_arrive_expect_tx(bar, kRawBytes);
-            const uint32_t dst = tc::smem_u32(sm_raw + r * kRawBytes);
-            tc::tma_load_3d_hint(dst, mk, bar, 0, tl * kBM, z, pol);
-            tc::tma_load_3d_hint(dst + 16384, mv, bar, 0, tl * kBM, z, pol);
+            // the upper halves of the stage; the converter warps expand in place
+            const int st = tt % NST;
+            tc::mbar_wait_sleep(tc::smem_u32(&kv_empty[st]), ((tt / NST) & 1) ^ 1);
+            const uint32_t bar = tc::smem_u32(&kv_full[st]);
+            tc::mbar_arrive_expect_tx(bar, 32768);
+            const uint32_t dst = tc::smem_u32(sm_stage + st * kStageBytes);
+            tc::tma_load_3d_hint(dst + 16384, mk, bar, 0, tl * kBM, z, pol);
+            tc::tma_load_3d_hint(dst + 49152, mv, bar, 0, tl * kBM, z, pol);
           } else {
           const int st = tt % NST;
           tc::mbar_wait_sleep(tc::smem_u32(&kv_empty[st]), ((tt / NST) & 1) ^ 1, BIF_DBG & 262144);
@@ -712,7 +708,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
         for (int j = 0; j < s.ntiles; ++j, ++u) {
           const uint32_t st = u % NST;
           const uint32_t slot = u & 1;
-          tc::mbar_wait_sleep(tc::smem_u32(&kv_full[st]), (u / NST) & 1, BIF_DBG & 262144);
+          tc::mbar_wait_sleep(tc::smem_u32(KV8 ? &k_cvt[st] : &kv_full[st]), (u / NST) & 1, BIF_DBG & 262144);
           pf.mark(1);
           if (kStamp && P.trace && u < 128)
             P.trace[(size_t)blockIdx.x * kTraceSlots + 256 + 128 + u] = (gtimer() & 0x00ffffffffffffffull) | (33ull << 56);
@@ -756,6 +752,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
           const uint32_t st = u % NST;
           const uint32_t ps = P.npb == 2 ? (u & 1) : 0, ph = P.npb == 2 ? (u >> 1) : u;
           tc::mbar_wait_sleep(tc::smem_u32(&p_full[ps]), ph & 1, BIF_DBG & 262144);
+          if (KV8) tc::mbar_wait_sleep(tc::smem_u32(&v_cvt[st]), (u / NST) & 1);
           pf.mark(1);
           tc::tc_fence_after();
           const uint32_t vbase = tc::smem_u32(sm_stage + st * kStageBytes + 32768);
@@ -1319,38 +1316,40 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(tc::smem_u32(&q_cvt[qbuf]));
         for (int j = 0; j < s.ntiles; ++j, ++u) {
-          const int r = u % kNRaw, st = u % NST;
-          tc::mbar_wait(tc::smem_u32(&raw_full[r]), (u / kNRaw) & 1);
-          tc::mbar_wait(tc::smem_u32(&kv_empty[st]), ((u / NST) & 1) ^ 1);
-          const uint8_t* src = sm_raw + r * kRawBytes;
-          uint8_t* dst = sm_stage + st * kStageBytes;
-#pragma unroll 4
-          for (int it = 0; it < 16; ++it) {
-            const int kv = it >> 3;              // 0: K, 1: V
-            const int i8 = it & 7;
-            const int R = 32 * cw + 8 * (i8 >> 1) + (lane >> 2);  // position row
-            const int c = 4 * (i8 & 1) + (lane & 3);              // 16-code chunk
-            const uint4 v = *reinterpret_cast<const uint4*>(src + kv * 16384 + R * 128 +
-                                                            ((c ^ (R & 7)) << 4));
-            uint4 a, b;
-            a.x = e4m3x2_to_f16x2(v.x);
-            a.y = e4m3x2_to_f16x2(v.x >> 16);
-            a.z = e4m3x2_to_f16x2(v.y);
-            a.w = e4m3x2_to_f16x2(v.y >> 16);
-            b.x = e4m3x2_to_f16x2(v.z);
-            b.y = e4m3x2_to_f16x2(v.z >> 16);
-            b.z = e4m3x2_to_f16x2(v.w);
-            b.w = e4m3x2_to_f16x2(v.w >> 16);
-            uint8_t* d8 = dst + kv * 32768 + (c >> 2) * 16384 + R * 128;
-            const int cc = 2 * (c & 3);
-            *reinterpret_cast<uint4*>(d8 + ((cc ^ (R & 7)) << 4)) = a;
-            *reinterpret_cast<uint4*>(d8 + (((cc + 1) ^ (R & 7)) << 4)) = b;
-          }
-          tc::fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0) {
-            tc::mbar_arrive(tc::smem_u32(&kv_full[st]));
-            tc::mbar_arrive(tc::smem_u32(&raw_empty[r]));
+          const int st = u % NST;
+          tc::mbar_wait(tc::smem_u32(&kv_full[st]), (u / NST) & 1);
+          uint8_t* const stage = sm_stage + st * kStageBytes;
+          // K (kv = 0) then V (kv = 1): codes of row R at region + 16 KB + R*128
+          // expand to f16 row R of both 64-column halves.  The odd iteration of
+          // a row pair overwrites the code row it read (all 8 chunks: the even
+          // iteration read chunks 0-3, this LDS reads 4-7 before the dependent
+          // STS issue) — in place, one warp per row.
+#pragma unroll
+          for (int kv = 0; kv < 2; ++kv) {
+            uint8_t* const reg = stage + kv * 32768;
+#pragma unroll 2
+            for (int i8 = 0; i8 < 8; ++i8) {
+              const int R = 32 * cw + 8 * (i8 >> 1) + (lane >> 2);  // position row
+              const int c = 4 * (i8 & 1) + (lane & 3);              // 16-code chunk
+              const uint4 v = lds128(reg + 16384 + R * 128 + ((c ^ (R & 7)) << 4));
+              uint4 a, b;
+              a.x = e4m3x2_to_f16x2(v.x);
+              a.y = e4m3x2_to_f16x2(v.x >> 16);
+              a.z = e4m3x2_to_f16x2(v.y);
+              a.w = e4m3x2_to_f16x2(v.y >> 16);
+              b.x = e4m3x2_to_f16x2(v.z);
+              b.y = e4m3x2_to_f16x2(v.z >> 16);
+              b.z = e4m3x2_to_f16x2(v.w);
+              b.w = e4m3x2_to_f16x2(v.w >> 16);
+              uint8_t* d8 = reg + (c >> 2) * 16384 + R * 128;
+              const int cc = 2 * (c & 3);
+              __syncwarp();  // every lane's code load of this row precedes the overwrite
+              sts128(d8 + ((cc ^ (R & 7)) << 4), a);
+              sts128(d8 + (((cc + 1) ^ (R & 7)) << 4), b);
+            }
+            tc::fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(tc::smem_u32(kv == 0 ? &k_cvt[st] : &v_cvt[st]));
           }
           if (pending && (j == 1 || j == s.ntiles - 1)) {
             drain(prev, sg - 1);

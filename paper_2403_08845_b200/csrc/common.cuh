@@ -43,6 +43,24 @@ BA_DEVINL uint32_t e4m3x2_to_f16x2(uint32_t two) {
   return h2;
 }
 
+// 16-byte shared-memory load / store that the compiler keeps in program order
+// with other memory operations (in-place conversions).
+BA_DEVINL uint4 lds128(const void* p) {
+  uint4 v;
+  const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(p));
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(a)
+               : "memory");
+  return v;
+}
+BA_DEVINL void sts128(void* p, uint4 v) {
+  const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(p));
+  asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
+}
+
 // Truncate two fp32 to bf16 and pack (lo in the low half): one byte permute
 // on the integer pipe instead of a conversion on the XU pipe, which the ex2 of
 // the softmax already loads.  Used for the split P = P_hi + P_lo (reading
