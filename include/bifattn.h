@@ -158,9 +158,13 @@ int bifurcated_attn_decode(const ba_problem_t* prob, const void* q, const void* 
  *   3. stores lens[i] <- min(lens[i] + n, md_cap) on the device after every
  *      read of lens, so the next step's call (or a CUDA-graph replay) needs
  *      no host work.
- * Two launches (append kernel, then the attention kernels chained by
- * programmatic dependent launch).  Kd, Vd and lens are modified; k_new/v_new
- * 16-byte aligned; md_cap >= 1.  Errors as bifurcated_attn_decode. */
+ * The append is FUSED into the attention launch(es): the CTA that will read
+ * the tile (or decode item) holding a new row stores it first — generic
+ * stores, then a proxy fence, then its TMA loads; the CUDA-core kernel reads
+ * the new rows from k_new / v_new directly — so the call launches exactly
+ * what bifurcated_attn_decode launches (ba_launches_per_call).  Kd, Vd and
+ * lens are modified; k_new/v_new 16-byte aligned; md_cap >= 1.  Errors as
+ * bifurcated_attn_decode. */
 int bifurcated_attn_decode_append(const ba_problem_t* prob, const void* q, const void* k_new,
                                   const void* v_new, const void* Kc, const void* Vc, void* Kd,
                                   void* Vd, int32_t* lens, void* out, float* lse,
@@ -222,8 +226,8 @@ int ba_lse_merge(int n_parts, int rows, int d, int dtype, const void* out_parts,
  * problem on the current device (for the benchmark's launch count): 1 for the
  * fused tensor-core plan (one cooperative launch, b*p < 64 rows per group), 2
  * for the rows-on-M plan (rows kernel + merge, or rows kernel + fused decode
- * launch), 3 for the CUDA-core plan.  bifurcated_attn_decode_append adds one
- * (the append kernel). */
+ * launch), 3 for the CUDA-core plan.  bifurcated_attn_decode_append launches
+ * the same kernels (the append is fused into them). */
 int ba_launches_per_call(const ba_problem_t* prob);
 
 /* Human-readable kernel plan for this problem (static string owned by the

@@ -53,6 +53,7 @@
 // of its chunk to its workspace slot (context slots [0, Sc), decode slots
 // [Sc, S)).
 #pragma once
+#include "append.cuh"
 #include "common.cuh"
 #include "tc_ptx.cuh"
 
@@ -71,6 +72,8 @@ struct BifTcParams {
   int lens_add;              // append+attend: lens[i] counts the cache BEFORE this step's n
                              // appended rows; the step sees min(lens[i] + lens_add, dec_cap)
   int32_t* lens_out;         // append+attend: lens updated in place after the step (or null)
+  AppendSrc app;             // append+attend: this step's K/V rows (app.n = 0: none), stored
+                             // by the CTA owning the decode tile that holds them (append.cuh)
   int ntok;                  // tokens per head (multi-token step): in-group row k sees decode
                              // positions < max(L - (ntok - 1 - k % ntok), lens_offset)
   int N;                     // rows per chunk (== template N)
@@ -578,8 +581,8 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
       tc::mbar_init(tc::smem_u32(&p_empty[s]), 1);
       tc::mbar_init(tc::smem_u32(&o_full[s]), 1);
       tc::mbar_init(tc::smem_u32(&o_empty[s]), 4);
-      tc::mbar_init(tc::smem_u32(&e_full[s]), NSW);
-      tc::mbar_init(tc::smem_u32(&e_empty[s]), 4);
+      tc::mbar_init(tc::smem_u32(&e_full[s]), 32 * NSW);  // every softmax thread (once per segment)
+      tc::mbar_init(tc::smem_u32(&e_empty[s]), 128);      // every epilogue thread
     }
     tc::fence_mbar_init();
   }
@@ -612,6 +615,20 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
   const long long nw = rg.n();
 
   if (warp == 0) {
+    // append+attend: store this step's K/V rows that fall in this CTA's decode
+    // tiles before any TMA of them (same CTA: generic stores, then a proxy fence)
+    if (P.app.n > 0 && P.Td > 0) {
+      for (long long f = max(rg.f0, P.Tc); f < rg.f1; ++f) {
+        const long long fd = f - P.Tc;
+        const long long ic = fd / P.ntile_d;
+        const int t = (int)(fd - ic * P.ntile_d);
+        const int i = (int)(ic / P.g), c = (int)(ic - (long long)i * P.g);
+        append_rows_warp(P.app, i, c, clamp_len(P.lens, i, P.dec_cap), t * kBM, t * kBM + kBM, lane);
+      }
+      fence_proxy_async_global();
+      __syncwarp();
+      fence_proxy_async_global();
+    }
     // ============================ TMA producer ============================
     if (lane == 0) {
       Prof pf;
@@ -989,8 +1006,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
           }
         }
         stamp(4);
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive(tc::smem_u32(&e_full[ob]));
+        tc::mbar_arrive(tc::smem_u32(&e_full[ob]));
       } else {
         // ====== general path: every column of the tile may be valid ======
         float l_part[CPT], mr[CPT];  // per-position row sums; running max per column
@@ -1152,8 +1168,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
               uint32_t off = (uint32_t)((col / W) * PLBO + pos * PRB + (col % W) * 2);
               off ^= ((off >> 7) & PSWM) << 4;
               *reinterpret_cast<uint4*>(sm_pb + off) = make_uint4(hk[0], hk[1], hk[2], hk[3]);
-              continue;
-            }
+            } else {
             uint32_t hk[4], lk[4];
 #pragma unroll
             for (int e = 0; e < 8; e += 2) {
@@ -1176,6 +1191,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
               *reinterpret_cast<uint4*>(sm_pb + off) = make_uint4(hk[0], hk[1], hk[2], hk[3]);
               *reinterpret_cast<uint4*>(sm_pb + offl) = make_uint4(lk[0], lk[1], lk[2], lk[3]);
             }
+            }
           }
           tc::fence_proxy_async_smem();
           __syncwarp();
@@ -1196,8 +1212,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
 #pragma unroll
           for (int n = 0; n < CPT; ++n) sm_mfin[ob * N + col0 + n] = mr[n];
         }
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive(tc::smem_u32(&e_full[ob]));
+        tc::mbar_arrive(tc::smem_u32(&e_full[ob]));
       }
       w = s.next;
       L = Ln;
@@ -1278,8 +1293,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
           reinterpret_cast<float2*>(P.ws_ml)[(size_t)gr * P.S + s.slot] = make_float2(sm_mfin[ob * N + et], Lr);
         }
       }
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(tc::smem_u32(&e_empty[ob]));
+      tc::mbar_arrive(tc::smem_u32(&e_empty[ob]));
     };
     if constexpr (!KV8) {
       uint32_t sg = 0;
@@ -1319,33 +1333,50 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
           const int st = u % NST;
           tc::mbar_wait(tc::smem_u32(&kv_full[st]), (u / NST) & 1);
           uint8_t* const stage = sm_stage + st * kStageBytes;
-          // K (kv = 0) then V (kv = 1): codes of row R at region + 16 KB + R*128
-          // expand to f16 row R of both 64-column halves.  The odd iteration of
-          // a row pair overwrites the code row it read (all 8 chunks: the even
-          // iteration read chunks 0-3, this LDS reads 4-7 before the dependent
-          // STS issue) — in place, one warp per row.
+          // K (kv = 0) then V (kv = 1): the codes of row R (region + 16 KB +
+          // R*128) expand to f16 row R of both 64-column halves.  Lane: row R
+          // of an 8-row block, code chunks c0 and c0 + 4 (-> half 0 and half 1).
+          // Half-1 rows overwrite the code rows they come from: a block's
+          // stores follow a __syncwarp after all its loads (and the next
+          // block's prefetch, which reads other rows).
 #pragma unroll
           for (int kv = 0; kv < 2; ++kv) {
             uint8_t* const reg = stage + kv * 32768;
-#pragma unroll 2
-            for (int i8 = 0; i8 < 8; ++i8) {
-              const int R = 32 * cw + 8 * (i8 >> 1) + (lane >> 2);  // position row
-              const int c = 4 * (i8 & 1) + (lane & 3);              // 16-code chunk
-              const uint4 v = lds128(reg + 16384 + R * 128 + ((c ^ (R & 7)) << 4));
-              uint4 a, b;
-              a.x = e4m3x2_to_f16x2(v.x);
-              a.y = e4m3x2_to_f16x2(v.x >> 16);
-              a.z = e4m3x2_to_f16x2(v.y);
-              a.w = e4m3x2_to_f16x2(v.y >> 16);
-              b.x = e4m3x2_to_f16x2(v.z);
-              b.y = e4m3x2_to_f16x2(v.z >> 16);
-              b.z = e4m3x2_to_f16x2(v.w);
-              b.w = e4m3x2_to_f16x2(v.w >> 16);
-              uint8_t* d8 = reg + (c >> 2) * 16384 + R * 128;
-              const int cc = 2 * (c & 3);
-              __syncwarp();  // every lane's code load of this row precedes the overwrite
-              sts128(d8 + ((cc ^ (R & 7)) << 4), a);
-              sts128(d8 + (((cc + 1) ^ (R & 7)) << 4), b);
+            const int c0 = lane & 3;
+            auto code_at = [&](int blk, int c) {
+              const int R = 32 * cw + 8 * blk + (lane >> 2);
+              return lds128(reg + 16384 + R * 128 + ((c ^ (R & 7)) << 4));
+            };
+            uint4 a0 = code_at(0, c0), a1 = code_at(0, c0 + 4);
+#pragma unroll
+            for (int blk = 0; blk < 4; ++blk) {
+              uint4 n0, n1;
+              if (blk < 3) {
+                n0 = code_at(blk + 1, c0);
+                n1 = code_at(blk + 1, c0 + 4);
+              }
+              uint4 h0a, h0b, h1a, h1b;
+              h0a.x = e4m3x2_to_f16x2(a0.x); h0a.y = e4m3x2_to_f16x2(a0.x >> 16);
+              h0a.z = e4m3x2_to_f16x2(a0.y); h0a.w = e4m3x2_to_f16x2(a0.y >> 16);
+              h0b.x = e4m3x2_to_f16x2(a0.z); h0b.y = e4m3x2_to_f16x2(a0.z >> 16);
+              h0b.z = e4m3x2_to_f16x2(a0.w); h0b.w = e4m3x2_to_f16x2(a0.w >> 16);
+              h1a.x = e4m3x2_to_f16x2(a1.x); h1a.y = e4m3x2_to_f16x2(a1.x >> 16);
+              h1a.z = e4m3x2_to_f16x2(a1.y); h1a.w = e4m3x2_to_f16x2(a1.y >> 16);
+              h1b.x = e4m3x2_to_f16x2(a1.z); h1b.y = e4m3x2_to_f16x2(a1.z >> 16);
+              h1b.z = e4m3x2_to_f16x2(a1.w); h1b.w = e4m3x2_to_f16x2(a1.w >> 16);
+              const int R = 32 * cw + 8 * blk + (lane >> 2);
+              const int cc = 2 * c0, x = R & 7;
+              __syncwarp();  // every lane's loads of this block precede the overwrite
+              uint8_t* const d0 = reg + R * 128;
+              uint8_t* const d1 = reg + 16384 + R * 128;
+              sts128(d0 + ((cc ^ x) << 4), h0a);
+              sts128(d0 + (((cc + 1) ^ x) << 4), h0b);
+              sts128(d1 + ((cc ^ x) << 4), h1a);
+              sts128(d1 + (((cc + 1) ^ x) << 4), h1b);
+              if (blk < 3) {
+                a0 = n0;
+                a1 = n1;
+              }
             }
             tc::fence_proxy_async_smem();
             __syncwarp();

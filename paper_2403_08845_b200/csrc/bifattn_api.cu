@@ -671,7 +671,7 @@ int launch_bif_tc_n(const ba::BifTcParams& bp, int smem, uint32_t flags, LaunchR
 // Kc = Vc = nullptr, Kd/Vd are the replicated caches [b][g][mc+md_cap][d].
 int run_tc(const ba_problem_t* pr, const Plan& P, const void* q, const void* Kc, const void* Vc,
            const void* Kd, const void* Vd, const int32_t* lens, void* out, float* lse, void* ws,
-           float scale_log2, cudaStream_t st, const AppendArgs* ap) {
+           float scale_log2, cudaStream_t st, const AppendArgs* ap, const ba::AppendSrc& app) {
   ba::BifTcParams bp;
   memset(&bp, 0, sizeof bp);
   const int p = pr->h / pr->g;
@@ -698,6 +698,7 @@ int run_tc(const ba_problem_t* pr, const Plan& P, const void* q, const void* Kc,
   bp.lens = lens;
   bp.lens_add = ap ? ap->n : 0;
   bp.lens_out = ap ? ap->lens : nullptr;
+  bp.app = app;
   bp.b = pr->b; bp.h = pr->h; bp.g = pr->g; bp.p = p; bp.mc = pr->mc;
   bp.dec_cap = P.dec_cap; bp.lens_offset = P.lens_offset; bp.ntok = P.ntok;
   bp.N = P.tc_N;
@@ -746,6 +747,7 @@ int run_tc(const ba_problem_t* pr, const Plan& P, const void* q, const void* Kc,
     cp.lens = lens;
     cp.dec_cap = P.dec_cap;
     cp.lens_add = ap ? ap->n : 0;
+    cp.app = app;
     cp.ntok = P.ntok;
     if (P.cr_dec) {
       const uint64_t ds = (uint64_t)P.dec_stride, bg = (uint64_t)pr->b * pr->g;
@@ -847,27 +849,17 @@ int run_plan(const ba_problem_t* pr, const Plan& P, const void* q, const void* K
   fp.dec_stride = P.dec_stride; fp.dec_cap = P.dec_cap; fp.lens_offset = P.lens_offset;
   fp.ntok = P.ntok;
   fp.lens_add = ap ? ap->n : 0;
+  // append+attend: the rows are stored by the attention kernels themselves
+  // (append.cuh), no separate launch
   if (ap) {
-    // KV append (append.cuh) first; the next launch depends on it
-    ba::AppendParams a;
-    a.k_new = ap->k_new; a.v_new = ap->v_new; a.Kd = const_cast<void*>(Kd); a.Vd = const_cast<void*>(Vd);
-    a.lens = lens; a.b = b; a.g = g; a.n = ap->n; a.md_cap = P.dec_cap;
-    a.vec_per_row = D * (int)sizeof(TK) / 16;
-    const long long tot = (long long)b * g * ap->n * a.vec_per_row;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)std::max(1ll, std::min((tot + 255) / 256, 4ll * 148)));
-    cfg.blockDim = dim3(256);
-    cfg.stream = st;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = (pr->flags & BA_FLAG_NO_PDL) ? 0 : 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, ba::kv_append_kernel, a);
-    if (e != cudaSuccess) {
-      g_last_cuda_error = (int)e;
-      return BA_ECUDA;
-    }
+    fp.app.k_new = ap->k_new;
+    fp.app.v_new = ap->v_new;
+    fp.app.Kd = const_cast<void*>(Kd);
+    fp.app.Vd = const_cast<void*>(Vd);
+    fp.app.n = ap->n;
+    fp.app.row_bytes = D * (int)sizeof(TK);
+    fp.app.dec_cap = P.dec_cap;
+    fp.app.g = g;
   }
   // FP8 KV: K = code * k_scale, folded into the logit scale (R19)
   const float kscale = (P.kv8 && pr->k_scale > 0.f) ? pr->k_scale : 1.f;
@@ -881,7 +873,7 @@ int run_plan(const ba_problem_t* pr, const Plan& P, const void* q, const void* K
   int rc;
   if (P.tc) {
     if constexpr (sizeof(T) == 2 && D == 128)
-      return run_tc(pr, P, q, Kc, Vc, Kd, Vd, lens, out, lse, ws, fp.scale_log2, st, ap);
+      return run_tc(pr, P, q, Kc, Vc, Kd, Vd, lens, out, lse, ws, fp.scale_log2, st, ap, fp.app);
     return BA_EINVAL;
   }
   LaunchRec rec(st);

@@ -25,6 +25,7 @@
 // issuer (one lane), 2 TMEM allocator, 4..11 softmax/epilogue: two threads
 // per row, each taking half of the tile's positions and of the O columns.
 #pragma once
+#include "append.cuh"
 #include "common.cuh"
 #include "tc_ptx.cuh"
 
@@ -35,6 +36,7 @@ struct CtxRowsParams {
   CUtensorMap tmKd, tmVd;  // (d, md_cap, b*g), box (64, 128, 1): decode items (p >= 32)
   const int32_t* lens;     // decode items: valid length min(clamp(lens[i]) + lens_add, dec_cap)
   int dec_cap, lens_add;
+  AppendSrc app;           // append+attend: this step's rows, stored by the decode item's CTA
   int ntok;                // multi-token step: decode row r (token r % ntok) sees
                            // positions < L - (ntok - 1 - r % ntok)
   int items_ctx;           // items [0, items_ctx) are context items, then b*g decode items
@@ -64,7 +66,8 @@ constexpr int kS = 3;                   // S/P slots in TMEM (3 x 128 columns + 
 constexpr int kQ = kNst * kStage;       // Q block (32 KB)
 constexpr int kBar = kQ + 32768;        // barriers
 constexpr int kXch = kBar + 256;        // row-max exchange [2 tiles][2 halves][128 rows] floats
-constexpr int kSmem = kXch + 2048;      // 231680 <= 227 KB
+constexpr int kLsx = kXch + 2048;       // item-end row-sum exchange [128 rows] floats (own slot)
+constexpr int kSmem = kLsx + 512;       // 232192 <= 227 KB
 constexpr float kTh = 8.0f;             // stale-max slack (log2 units), as bif_tc.cuh
 constexpr int kThreads = 384;
 
@@ -180,6 +183,19 @@ __global__ void __launch_bounds__(ctxr::kThreads, 1)
   };
 
   if (warp == 0 || warp == 3) {
+    // append+attend: the K (warp 0) / V (warp 3) rows of this CTA's decode items
+    // before any TMA of them (same CTA: generic stores, then a proxy fence)
+    if (P.app.n > 0) {
+      for (int k = blockIdx.x; k < P.items; k += gridDim.x) {
+        if (k < P.items_ctx) continue;
+        const int j = k - P.items_ctx, i = j / P.g, c = j - (j / P.g) * P.g;
+        append_rows_warp(P.app, i, c, clamp_len(P.lens, i, P.dec_cap), 0, P.dec_cap, lane,
+                         warp == 0 ? 1 : 2);
+      }
+      fence_proxy_async_global();
+      __syncwarp();
+      fence_proxy_async_global();
+    }
     // ==================== TMA producers: K (warp 0), V (warp 3) ====================
     if (lane == 0) {
       const bool isk = warp == 0;
@@ -228,7 +244,6 @@ __global__ void __launch_bounds__(ctxr::kThreads, 1)
               tc::mma_bf16_ts(tO, tS + (v % kS) * 128 + part * 64 + k * 8, bd, IDESC_PV,
                               (first && part == 0 && k == 0) ? 0u : 1u);
           }
-        tc::mma_commit(tc::smem_u32(p_empty));
         tc::mma_commit(tc::smem_u32(&s_free[v % kS]));
         tc::mma_commit(tc::smem_u32(&v_empty[v % kNst]));
         pf.mark(6);
@@ -349,7 +364,8 @@ __global__ void __launch_bounds__(ctxr::kThreads, 1)
           // raise the reference to the exact max; rescale l and this half of the O row
           const float mn = mx;
           if (m != kNegInf && t > t0) {
-            tc::mbar_wait(tc::smem_u32(p_empty), (u & 1) ^ 1);  // PV(u-1) done: O quiescent
+            // PV(u-1) done (O quiescent): the commit that frees S slot (u-1) % kS
+            tc::mbar_wait(tc::smem_u32(&s_free[(u - 1) % kS]), ((u - 1) / kS) & 1);
             const float a = ex2(m - mn);
             l *= a;
             tc::tc_fence_after();
@@ -406,14 +422,14 @@ __global__ void __launch_bounds__(ctxr::kThreads, 1)
                             __uint_as_float(o[e + 2]), __uint_as_float(o[e + 3]));
         }
       }
-      // row sum = both halves' shares, through the exchange slots of parity
-      // u & 1 (last read before the previous tile's barrier; the next write to
-      // them needs the next item's QK, i.e. every warp's q_full arrival)
-      float* const ls = sm_x + (u & 1) * 256;
-      ls[hf * 128 + r] = l;
+      // row sum = both halves' shares, through its own exchange slot (written
+      // by the hf = 1 half, read by hf = 0 between this barrier and the next
+      // item's first tile barrier)
+      float* const ls = reinterpret_cast<float*>(smem + kLsx);
+      if (hf == 1) ls[r] = l;
       tc::named_bar_sync(1, 256);
       if (hf == 0 && valid_row)
-        reinterpret_cast<float2*>(P.ws_ml)[(size_t)gr * P.S + s] = make_float2(m, l + ls[128 + r]);
+        reinterpret_cast<float2*>(P.ws_ml)[(size_t)gr * P.S + s] = make_float2(m, l + ls[r]);
       tc::tc_fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(tc::smem_u32(o_empty));

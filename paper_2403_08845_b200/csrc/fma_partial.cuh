@@ -20,6 +20,7 @@
 // own running (m, l, o) for its keys; the 8 streams are merged in shared
 // memory at the end of the item.
 #pragma once
+#include "append.cuh"
 #include "common.cuh"
 
 namespace ba {
@@ -47,6 +48,8 @@ struct FmaParams {
   int dec_slot0;             // first slot index of the decode splits
   float* ws_o;               // [b*h][S][D]
   float* ws_ml;              // [b*h][S][2]  (m in log2 units, l)
+  AppendSrc app;             // append+attend (app.n > 0): decode items read positions >= the
+                             // old length from k_new / v_new; row block 0 stores them
 };
 
 template <typename T>
@@ -158,6 +161,9 @@ __global__ void __launch_bounds__(128) fma_partial_kernel(const FmaParams P) {
   int it = blockIdx.x;
   int c, r_begin, r_end, t0, t1, slot, row_base;  // rows r -> (r/p)*h + c*p + r%p
   int dec_L = -1, dec_r0 = 0;  // decode item: valid length, first row of the sample
+  int app_L0 = 1 << 30;        // append+attend: keys >= app_L0 come from k_new / v_new
+  const TK* Kn = nullptr;
+  const TK* Vn = nullptr;
   const TK* Kb;
   const TK* Vb;
   if (it < P.n_ctx_items) {
@@ -194,6 +200,16 @@ __global__ void __launch_bounds__(128) fma_partial_kernel(const FmaParams P) {
     Kb = reinterpret_cast<const TK*>(P.Kd) + base;
     Vb = reinterpret_cast<const TK*>(P.Vd) + base;
     slot = P.dec_slot0 + s;
+    if (P.app.n > 0) {
+      const int L0 = clamp_len(P.lens, i, P.dec_cap);
+      app_L0 = P.lens_offset + L0;
+      const size_t nb = ((size_t)i * P.g + c) * P.app.n * D;
+      Kn = reinterpret_cast<const TK*>(P.app.k_new) + nb - (size_t)app_L0 * D;
+      Vn = reinterpret_cast<const TK*>(P.app.v_new) + nb - (size_t)app_L0 * D;
+      // the row-block-0 item of the split holding a new row stores it (for the
+      // next steps; nobody reads it from Kd / Vd in this one)
+      if (rb == 0 && warp == 0) append_rows_warp(P.app, i, c, L0, t0, t1, lane);
+    }
     row_base = 0;
   }
   (void)row_base;
@@ -253,7 +269,8 @@ __global__ void __launch_bounds__(128) fma_partial_kernel(const FmaParams P) {
       if (tk[u] < t1) {
 #pragma unroll
         for (int ch = 0; ch < NCH; ++ch)
-          Vec<TK>::template load<LW>(Kb + (size_t)tk[u] * D + (ch * 16 + j) * LW, kv[u][ch]);
+          Vec<TK>::template load<LW>((tk[u] >= app_L0 ? Kn : Kb) + (size_t)tk[u] * D + (ch * 16 + j) * LW,
+                                     kv[u][ch]);
       } else {
 #pragma unroll
         for (int ch = 0; ch < NCH; ++ch)
@@ -266,7 +283,8 @@ __global__ void __launch_bounds__(128) fma_partial_kernel(const FmaParams P) {
       if (tk[u] < t1) {
 #pragma unroll
         for (int ch = 0; ch < NCH; ++ch)
-          Vec<TK>::template load<LW>(Vb + (size_t)tk[u] * D + (ch * 16 + j) * LW, vv[u][ch]);
+          Vec<TK>::template load<LW>((tk[u] >= app_L0 ? Vn : Vb) + (size_t)tk[u] * D + (ch * 16 + j) * LW,
+                                     vv[u][ch]);
       } else {
 #pragma unroll
         for (int ch = 0; ch < NCH; ++ch)
