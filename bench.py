@@ -483,36 +483,43 @@ def e2e_runs(ba, cfg, case, dev, stream, barrier, steps):
            "h2d_bytes_per_step": sum(t.numel() * t.element_size() for t in (hq, hKc, hVc, hKd, hVd, hl)),
            "d2h_bytes_per_step": hout.numel() * hout.element_size()}
     del dbuf
-    # decode loop: caches resident; q, this step's K/V rows and lens copied in,
-    # append + attend in one C-ABI call, out copied back
+    # decode loop: caches resident; ONE H2D of the packed [q | k_new | v_new |
+    # lens], append + attend, ONE D2H of out (bifurcated_attn_decode_step_packed),
+    # the whole step replayed from a CUDA graph
     b, g = Kd.shape[0], Kd.shape[1]
-    hkn = torch.randn(b, g, 1, cfg.d).to(Kd.dtype).pin_memory()
-    hvn = torch.randn(b, g, 1, cfg.d).to(Kd.dtype).pin_memory()
-    hl1 = (lens.cpu() - 1).clamp_min(0).to(torch.int32).pin_memory()
+    hkn = torch.randn(b, g, 1, cfg.d).to(Kd.dtype)
+    hvn = torch.randn(b, g, 1, cfg.d).to(Kd.dtype)
+    hl1 = (lens.cpu() - 1).clamp_min(0).to(torch.int32)
+    step = ba.PackedStep(case.prob, Kc, Vc, Kd.clone(), Vd.clone(), dev)
+    step.pack(q.cpu(), hkn, hvn, hl1)
     cs = torch.cuda.Stream()
-    loop_dev = dict(q=torch.empty_like(q), k_new=torch.empty_like(hkn, device=dev),
-                    v_new=torch.empty_like(hvn, device=dev), Kc=Kc, Vc=Vc, Kd=Kd.clone(),
-                    Vd=Vd.clone(), lens=torch.empty_like(lens), out=torch.empty_like(q),
-                    workspace=ba.alloc_workspace(case.prob, dev))
-
-    def loop_step():
-        ba.bifurcated_attn_decode_append_host(hq, hkn, hvn, hout, loop_dev, hlens=hl1,
-                                              scale=case.scale, stream=cs, k_scale=ks,
-                                              v_scale=vs)
-    for _ in range(2):
-        loop_step()
+    step.run(stream=cs)
     torch.cuda.synchronize()
-    barrier()
-    torch.cuda.synchronize()
-    a0.record(cs)
-    for _ in range(ne):
-        loop_step()
-    a1.record(cs)
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=cs):
+        for _ in range(ne):
+            step.run(stream=cs)
+    with torch.cuda.stream(cs):
+        graph.replay()
+        torch.cuda.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        a0.record(cs)
+        graph.replay()
+        a1.record(cs)
     torch.cuda.synchronize()
     barrier()
     res["loop_ms"] = a0.elapsed_time(a1) / ne
-    res["loop_h2d"] = sum(t.numel() * t.element_size() for t in (hq, hkn, hvn, hl1))
-    res["loop_d2h"] = hout.numel() * hout.element_size()
+    res["loop_h2d"] = step.h_in.numel()
+    res["loop_d2h"] = step.nq
+    # the same steps without the graph (one C-ABI call per step)
+    torch.cuda.synchronize()
+    a0.record(cs)
+    for _ in range(ne):
+        step.run(stream=cs)
+    a1.record(cs)
+    torch.cuda.synchronize()
+    res["loop_nograph_ms"] = a0.elapsed_time(a1) / ne
     return res
 
 
@@ -675,8 +682,10 @@ def run_ours(args, cfg):
                 "value": bytes_step / (loop_ms * 1e-3) / 1e9, "unit": "GB/s",
                 "ms_per_step": loop_ms, "h2d_bytes_per_step": e2e["loop_h2d"],
                 "d2h_bytes_per_step": e2e["loop_d2h"],
-                "api": "bifurcated_attn_decode_append_host: one call per step (caches resident; "
-                       "q, K/V rows, lens copied in, out copied back)"}
+                "ms_per_step_without_graph": e2e.get("loop_nograph_ms"),
+                "api": "bifurcated_attn_decode_step_packed: caches resident; one H2D of "
+                       "[q | k_new | v_new | lens], append + attend fused, one D2H of out; "
+                       "steps replayed from a CUDA graph"}
         if others:
             line["other_configs"] = others
         if ws == 1 and not args.no_cpu_baseline:

@@ -185,6 +185,27 @@ int bifurcated_attn_decode_append_host(const ba_problem_t* prob, const void* hq,
                                        float* dlse, void* workspace, size_t workspace_bytes,
                                        void* stream);
 
+/* One serving step with ONE host->device and ONE device->host copy (SURVEY
+ * §8(f) row f2; the decode loop of PAPER.md Table 5's per-step accounting):
+ * the caches stay resident; the host packs this step's inputs into one pinned
+ * buffer and gets the result back in one:
+ *   h_in / d_in  [ q | k_new | v_new | lens ]   ba_step_in_bytes(prob) bytes
+ *   h_out / d_out[ out | lse ]                   ba_step_out_bytes(prob) bytes
+ * each part starting at a 256-byte boundary (q [b][h][n][d], k_new / v_new
+ * [b][g][n][d] in the cache type, lens int32 [b] = each cache's length BEFORE
+ * this step; out [b][h][n][d], lse float32 [b][h][n], copied back only when
+ * with_lse != 0).  Runs H2D(in), bifurcated_attn_decode_append (rows appended
+ * into Kd, Vd; lens advanced inside d_in), D2H(out) on `stream` and returns
+ * after enqueueing — the whole step is CUDA-graph capturable.  d_in / d_out
+ * are caller-owned device buffers (16-byte aligned), h_in / h_out pinned host
+ * memory for asynchronous copies. */
+size_t ba_step_in_bytes(const ba_problem_t* prob);
+size_t ba_step_out_bytes(const ba_problem_t* prob);
+int bifurcated_attn_decode_step_packed(const ba_problem_t* prob, const void* h_in, void* h_out,
+                                       void* d_in, void* d_out, int with_lse, const void* Kc,
+                                       const void* Vc, void* Kd, void* Vd, void* workspace,
+                                       size_t workspace_bytes, void* stream);
+
 /* The same step with HOST inputs and outputs (end-to-end entry point): copies
  * q, Kc, Vc, Kd, Vd, lens from host memory (pinned for async behaviour) into
  * the caller-owned device buffers dq..dlens, runs bifurcated_attn_decode, and
@@ -271,6 +292,21 @@ int ba_stream_read_bench(const void* buf, size_t bytes, void* sink, void* stream
  * (128 positions each).  Writes min(cap, G + 1) entries to cs (nullable) and
  * returns G, or 0 if the problem takes the CUDA-core plan, or a BA_E* code. */
 int ba_plan_ctas(const ba_problem_t* prob, int32_t* cs, int cap);
+
+/* Workload-based switch (PAPER.md FAQ 4 :688-689: "one
+ * can get the best of both worlds ... by triggering bifurcated attention under
+ * high workload scenarios and using normal attention otherwise"; SPEC.md:257-
+ * 258, :284-287 select_path):
+ *   policy BA_PATH_BIFURCATED / BA_PATH_NAIVE force the choice; BA_PATH_AUTO
+ *   returns bifurcated iff b * mc > threshold (threshold <= 0: the library's
+ *   measured default, BA_AUTO_THRESHOLD).  A caller keeps the
+ *   replicated cache [b][g][mc + md_cap][d] and calls replicated_attn_decode
+ *   for BA_PATH_NAIVE, the bifurcated cache and bifurcated_attn_decode
+ *   otherwise.  Returns BA_PATH_BIFURCATED or BA_PATH_NAIVE, or a BA_E* code
+ *   for an invalid problem / policy. */
+enum { BA_PATH_AUTO = 0, BA_PATH_BIFURCATED = 1, BA_PATH_NAIVE = 2 };
+#define BA_AUTO_THRESHOLD 16384LL /* b*mc elements (SPEC.md:303 placeholder 2^14) */
+int ba_select_path(const ba_problem_t* prob, int policy, long long threshold);
 
 /* Message for a BA_* code (static string). */
 const char* ba_strerror(int code);

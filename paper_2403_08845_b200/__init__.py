@@ -35,7 +35,8 @@ EXPORTED = ["ba_workspace_bytes", "bifurcated_attn_decode", "bifurcated_attn_dec
             "bifurcated_attn_decode_append", "bifurcated_attn_decode_append_host", "ba_lse_merge",
             "replicated_attn_decode", "ba_launches_per_call", "ba_plan_string", "ba_strerror",
             "ba_last_cuda_error", "ba_version", "ba_launch_name", "ba_set_launch_events",
-            "ba_set_trace_buffer", "ba_plan_ctas", "ba_stream_read_bench"]
+            "ba_set_trace_buffer", "ba_plan_ctas", "ba_stream_read_bench", "ba_step_in_bytes",
+            "ba_step_out_bytes", "bifurcated_attn_decode_step_packed", "ba_select_path"]
 
 
 class BAProblem(ctypes.Structure):
@@ -91,6 +92,15 @@ def load_library(path: str = LIB_PATH):
     lib.ba_plan_ctas.restype = ctypes.c_int
     lib.ba_set_trace_buffer.argtypes = [ctypes.c_void_p]
     lib.ba_set_trace_buffer.restype = None
+    lib.ba_select_path.argtypes = [pp, ctypes.c_int, ctypes.c_longlong]
+    lib.ba_select_path.restype = ctypes.c_int
+    lib.ba_step_in_bytes.argtypes = [pp]
+    lib.ba_step_in_bytes.restype = ctypes.c_size_t
+    lib.ba_step_out_bytes.argtypes = [pp]
+    lib.ba_step_out_bytes.restype = ctypes.c_size_t
+    lib.bifurcated_attn_decode_step_packed.argtypes = [pp, P, P, P, P, ctypes.c_int] + [P] * 5 + \
+        [ctypes.c_size_t, P]
+    lib.bifurcated_attn_decode_step_packed.restype = ctypes.c_int
     lib.ba_stream_read_bench.argtypes = [P, ctypes.c_size_t, P, P]
     lib.ba_stream_read_bench.restype = ctypes.c_int
     lib.ba_version.argtypes = []
@@ -524,3 +534,82 @@ def stream_read_bench(buf: torch.Tensor, sink: torch.Tensor, stream=None) -> Non
                                   sink.data_ptr(), _stream_handle(stream))
     if rc != 0:
         raise BifAttnError(rc, "ba_stream_read_bench")
+
+
+def _up256(x: int) -> int:
+    return (x + 255) & ~255
+
+
+class PackedStep:
+    """One serving step with one H2D and one D2H copy (include/bifattn.h
+    bifurcated_attn_decode_step_packed).  Holds the pinned host buffers and
+    device staging buffers of the packed layout [q | k_new | v_new | lens] ->
+    [out | lse]; ``pack`` fills the host input, ``run`` enqueues the step,
+    ``unpack`` views the host result.  The caches (Kc, Vc, Kd, Vd) stay
+    resident; lens is this step's cache length before the append."""
+
+    def __init__(self, prob: BAProblem, Kc, Vc, Kd, Vd, device, with_lse=False):
+        lib = load_library()
+        self.prob, self.lib = prob, lib
+        self.Kc, self.Vc, self.Kd, self.Vd = Kc, Vc, Kd, Vd
+        self.with_lse = with_lse
+        nin = int(lib.ba_step_in_bytes(ctypes.byref(prob)))
+        nout = int(lib.ba_step_out_bytes(ctypes.byref(prob)))
+        if nin == 0 or nout == 0:
+            raise BifAttnError(-1, "ba_step_in_bytes")
+        self.h_in = torch.empty(nin, dtype=torch.uint8).pin_memory()
+        self.h_out = torch.empty(nout, dtype=torch.uint8).pin_memory()
+        self.d_in = torch.empty(nin, dtype=torch.uint8, device=device)
+        self.d_out = torch.empty(nout, dtype=torch.uint8, device=device)
+        self.ws = alloc_workspace(prob, device)
+        n = max(prob.n_tok, 1)
+        e = 2 if prob.dtype == BA_BF16 else 4
+        ekv = 1 if prob.kv_dtype == BA_FP8_E4M3 else e
+        b, h, g, d = prob.b, prob.h, prob.g, prob.d
+        self.nq = b * h * n * d * e
+        self.nkv = b * g * n * d * ekv
+        self.off_k = _up256(self.nq)
+        self.off_v = self.off_k + _up256(self.nkv)
+        self.off_lens = self.off_v + _up256(self.nkv)
+        self.off_lse = _up256(self.nq)
+        self.q_shape = (b, h, n, d) if n > 1 else (b, h, d)
+        self.q_dtype = torch.bfloat16 if prob.dtype == BA_BF16 else torch.float32
+
+    def pack(self, q, k_new, v_new, lens):
+        hb = self.h_in
+        hb[:self.nq].copy_(q.contiguous().view(torch.uint8).reshape(-1))
+        hb[self.off_k:self.off_k + self.nkv].copy_(k_new.contiguous().view(torch.uint8).reshape(-1))
+        hb[self.off_v:self.off_v + self.nkv].copy_(v_new.contiguous().view(torch.uint8).reshape(-1))
+        lb = torch.as_tensor(lens, dtype=torch.int32).contiguous().view(torch.uint8).reshape(-1)
+        hb[self.off_lens:self.off_lens + lb.numel()].copy_(lb)
+
+    def run(self, stream=None):
+        rc = self.lib.bifurcated_attn_decode_step_packed(
+            ctypes.byref(self.prob), self.h_in.data_ptr(), self.h_out.data_ptr(),
+            self.d_in.data_ptr(), self.d_out.data_ptr(), 1 if self.with_lse else 0,
+            self.Kc.data_ptr(), self.Vc.data_ptr(), self.Kd.data_ptr(), self.Vd.data_ptr(),
+            self.ws.data_ptr(), self.ws.numel(), _stream_handle(stream))
+        if rc != 0:
+            raise BifAttnError(rc, "bifurcated_attn_decode_step_packed")
+
+    def out(self):
+        return self.h_out[:self.nq].view(self.q_dtype).view(self.q_shape)
+
+    def lse(self):
+        nl = self.nq // (self.q_shape[-1] * (2 if self.q_dtype == torch.bfloat16 else 4))
+        return self.h_out[self.off_lse:self.off_lse + 4 * nl].view(torch.float32)
+
+
+BA_PATH_AUTO, BA_PATH_BIFURCATED, BA_PATH_NAIVE = 0, 1, 2
+_POLICIES = {"auto": BA_PATH_AUTO, "always_bifurcated": BA_PATH_BIFURCATED,
+             "always_naive": BA_PATH_NAIVE}
+
+
+def select_path(prob: BAProblem, policy="auto", threshold: int = 0) -> str:
+    """FAQ 4 workload switch (include/bifattn.h ba_select_path): 'bifurcated'
+    or 'naive' for this problem; policy 'auto' | 'always_bifurcated' |
+    'always_naive'; threshold on b*mc (0: the library's measured default)."""
+    rc = load_library().ba_select_path(ctypes.byref(prob), _POLICIES[policy], int(threshold))
+    if rc < 0:
+        raise BifAttnError(rc, "ba_select_path")
+    return "bifurcated" if rc == BA_PATH_BIFURCATED else "naive"

@@ -945,6 +945,28 @@ int common_checks(const ba_problem_t* pr, const void* const* ptrs, int nptr, voi
   return BA_OK;
 }
 
+// Packed serving-step layout: [q | k_new | v_new | lens] in, [out | lse] out,
+// each part starting at a 256-byte boundary.
+struct StepLayout {
+  size_t q, k, v, lens, in_bytes, out, lse, out_bytes;
+};
+StepLayout step_layout(const ba_problem_t* pr) {
+  auto up = [](size_t x) { return (x + 255) & ~(size_t)255; };
+  const size_t e = pr->dtype == BA_BF16 ? 2 : 4;
+  const size_t ekv = pr->kv_dtype == BA_FP8_E4M3 ? 1 : e;
+  const size_t n = ntok_of(pr), d = pr->d;
+  StepLayout L;
+  L.q = 0;
+  L.k = up((size_t)pr->b * pr->h * n * d * e);
+  L.v = L.k + up((size_t)pr->b * pr->g * n * d * ekv);
+  L.lens = L.v + up((size_t)pr->b * pr->g * n * d * ekv);
+  L.in_bytes = L.lens + up((size_t)pr->b * 4);
+  L.out = 0;
+  L.lse = up((size_t)pr->b * pr->h * n * d * e);
+  L.out_bytes = L.lse + up((size_t)pr->b * pr->h * n * 4);
+  return L;
+}
+
 }  // namespace
 
 extern "C" {
@@ -1057,6 +1079,43 @@ int bifurcated_attn_decode_append_host(const ba_problem_t* prob, const void* hq,
   if ((rc = cp(hout, dout, nq, cudaMemcpyDeviceToHost))) return rc;
   if (hlse && dlse)
     return cp(hlse, dlse, (size_t)prob->b * prob->h * n * sizeof(float), cudaMemcpyDeviceToHost);
+  return BA_OK;
+}
+
+size_t ba_step_in_bytes(const ba_problem_t* prob) {
+  return validate(prob) == BA_OK ? step_layout(prob).in_bytes : 0;
+}
+size_t ba_step_out_bytes(const ba_problem_t* prob) {
+  return validate(prob) == BA_OK ? step_layout(prob).out_bytes : 0;
+}
+
+int bifurcated_attn_decode_step_packed(const ba_problem_t* prob, const void* h_in, void* h_out,
+                                       void* d_in, void* d_out, int with_lse, const void* Kc,
+                                       const void* Vc, void* Kd, void* Vd, void* workspace,
+                                       size_t workspace_bytes, void* stream) {
+  int rc = validate(prob);
+  if (rc) return rc;
+  if (!h_in || !h_out || !d_in || !d_out) return BA_ENULL;
+  if (!aligned16(d_in) || !aligned16(d_out)) return BA_EALIGN;
+  const StepLayout L = step_layout(prob);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaError_t ce = cudaMemcpyAsync(d_in, h_in, L.in_bytes, cudaMemcpyHostToDevice, st);
+  if (ce != cudaSuccess) {
+    g_last_cuda_error = (int)ce;
+    return BA_ECUDA;
+  }
+  char* di = static_cast<char*>(d_in);
+  char* dout = static_cast<char*>(d_out);
+  rc = bifurcated_attn_decode_append(prob, di + L.q, di + L.k, di + L.v, Kc, Vc, Kd, Vd,
+                                     reinterpret_cast<int32_t*>(di + L.lens), dout + L.out,
+                                     with_lse ? reinterpret_cast<float*>(dout + L.lse) : nullptr,
+                                     workspace, workspace_bytes, stream);
+  if (rc) return rc;
+  ce = cudaMemcpyAsync(h_out, d_out, with_lse ? L.out_bytes : L.lse, cudaMemcpyDeviceToHost, st);
+  if (ce != cudaSuccess) {
+    g_last_cuda_error = (int)ce;
+    return BA_ECUDA;
+  }
   return BA_OK;
 }
 
@@ -1266,6 +1325,15 @@ int ba_plan_ctas(const ba_problem_t* prob, int32_t* cs, int cap) {
 void ba_set_launch_events(void* const* events, int n) {
   g_events = n > 0 ? events : nullptr;
   g_nevents = n > 0 ? n : 0;
+}
+
+int ba_select_path(const ba_problem_t* prob, int policy, long long threshold) {
+  const int rc = validate(prob);
+  if (rc) return rc;
+  if (policy == BA_PATH_BIFURCATED || policy == BA_PATH_NAIVE) return policy;
+  if (policy != BA_PATH_AUTO) return BA_EINVAL;
+  const long long th = threshold > 0 ? threshold : BA_AUTO_THRESHOLD;
+  return (long long)prob->b * prob->mc > th ? BA_PATH_BIFURCATED : BA_PATH_NAIVE;
 }
 
 const char* ba_strerror(int code) {

@@ -135,3 +135,41 @@ def test_append_host_entry_equals_device_call():
         torch.cuda.synchronize()
         assert torch.equal(hout, ref[step]), step
     assert torch.equal(dev["lens"].cpu(), lens.cpu())
+
+
+def test_packed_step_one_copy_each_way_and_graph():
+    """bifurcated_attn_decode_step_packed: one H2D of [q | k_new | v_new | lens],
+    append + attend, one D2H of [out | lse]; two steps, the second replayed
+    from a CUDA graph of the whole step, each equal to the oracle on the
+    host-side appended cache."""
+    cfg = Config("packed", "bf16", b=32, h=8, g=4, d=128, mc=700, md=64)
+    inp = make_inputs(cfg, 61, lens=[3 + (5 * i) % 50 for i in range(cfg.b)])
+    prob = ba.make_problem(cfg.b, cfg.h, cfg.g, cfg.d, cfg.mc, cfg.md, cfg.torch_dtype, inp.scale)
+    Kc, Vc = inp.Kc.to(DEV), inp.Vc.to(DEV)
+    Kd, Vd = inp.Kd.to(DEV).clone(), inp.Vd.to(DEV).clone()
+    step = ba.PackedStep(prob, Kc, Vc, Kd, Vd, DEV, with_lse=True)
+    host = inp
+    lens = inp.lens.clone()
+    g = torch.cuda.CUDAGraph()
+    for k in range(2):
+        kn = torch.randn(cfg.b, cfg.g, 1, cfg.d).to(cfg.torch_dtype)
+        vn = torch.randn(cfg.b, cfg.g, 1, cfg.d).to(cfg.torch_dtype)
+        q = torch.randn(cfg.b, cfg.h, cfg.d).to(cfg.torch_dtype)
+        step.pack(q, kn, vn, lens)
+        if k == 0:
+            step.run()
+        else:
+            s = torch.cuda.Stream()
+            with torch.cuda.graph(g, stream=s):
+                step.run(stream=s)
+            step.pack(q, kn, vn, lens)  # capture does not execute; the replay does
+            Kd.copy_(host.Kd.to(DEV))
+            Vd.copy_(host.Vd.to(DEV))
+            with torch.cuda.stream(s):
+                g.replay()
+        torch.cuda.synchronize()
+        host = host_append(type(inp)(q, host.Kc, host.Vc, host.Kd, host.Vd, lens, inp.scale),
+                           kn, vn, 1)
+        ref, ref_lse = oracle_rows(host)
+        compare(step.out().clone(), step.lse().clone(), ref, ref_lse, cfg.torch_dtype, f"packed{k}")
+        lens = host.lens.clone()
