@@ -58,5 +58,22 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+
+def build_variant(name: str, defines, force: bool = False) -> str:
+    """An instrumented build of the same sources (e.g. -DBIFATTN_TRACE: the
+    %globaltimer timeline of scripts/timeline.py) next to the product
+    library: libbifattn_<name>.so.  Never loaded by the product binding."""
+    out = os.path.join(HERE, f"libbifattn_{name}.so")
+    stamp = out + ".srchash"
+    h = source_hash(tuple(defines))
+    if force or not os.path.exists(out) or not os.path.exists(stamp) or open(stamp).read().strip() != h:
+        cmd = [NVCC, *NVCC_FLAGS, *defines, "-I", os.path.join(ROOT, "include"), "-o", out + ".tmp", SRC]
+        subprocess.check_call(cmd)
+        os.replace(out + ".tmp", out)
+        with open(stamp, "w") as f:
+            f.write(h + "\n")
+    return out
+
+
 if __name__ == "__main__":
     print(build(force=True, verbose=True))

@@ -1,0 +1,106 @@
+"""Per-CTA phase timeline of the fused kernel from %globaltimer stamps
+(-DBIFATTN_TRACE build of the same sources, _build.build_variant("trace")).
+
+usage: python scripts/timeline.py [config ...]   (default: mha7b_b32 mha7b_b32_fp8)
+
+Stamps (include/bifattn.h ba_set_trace_buffer; bif_tc.cuh): per CTA slot 250
+kernel start, 254 after the PDL wait, 251 main loop end, 252 out of the grid
+barrier, 253 merge done; softmax thread 128: 20 S ready, 21/22 fast/slow path
+after the vote, 23 P handed to the MMA, 2/3 first tile of a context/decode
+segment, 4 segment end; producer 30 (TMA issue of tile u); QK 33 (K landed),
+31 (QK issued); PV 32 (PV issued).  Prints one JSON line per config: the
+phase split of the step (median / max over CTAs, us) and the per-tile
+softmax intervals."""
+import json
+import os
+import statistics
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+from paper_2403_08845_b200 import _build  # noqa: E402
+
+LIB = _build.build_variant("trace", ["-DBIFATTN_TRACE"])
+import paper_2403_08845_b200 as ba  # noqa: E402
+
+ba.load_library(LIB)
+from synth import CONFIGS, make_inputs, seed_for  # noqa: E402
+
+
+def med(v):
+    return round(statistics.median(v), 3) if v else None
+
+
+def run(name):
+    cfg = CONFIGS[name]
+    inp = make_inputs(cfg, seed_for(name), device="cuda")
+    prob = ba.make_problem(cfg.b, cfg.h, cfg.g, cfg.d, cfg.mc, cfg.md, cfg.torch_dtype, inp.scale,
+                           kv_dtype=inp.Kc.dtype, k_scale=inp.k_scale, v_scale=inp.v_scale)
+    G = len(ba.ba_plan_ctas(prob)) - 1
+    buf = torch.zeros(G * 1024, dtype=torch.int64, device="cuda")
+    out = torch.empty_like(inp.q)
+    ws = ba.alloc_workspace(prob, "cuda")
+
+    def step():
+        ba.bifurcated_attn_decode(inp.q, inp.Kc, inp.Vc, inp.Kd, inp.Vd, inp.lens, out,
+                                  scale=inp.scale, workspace=ws, k_scale=inp.k_scale,
+                                  v_scale=inp.v_scale)
+    for _ in range(5):
+        step()
+    torch.cuda.synchronize()
+    lib = ba.load_library()
+    lib.ba_set_trace_buffer(buf.data_ptr())
+    step()
+    torch.cuda.synchronize()
+    lib.ba_set_trace_buffer(None)
+    tr = buf.view(G, 1024).cpu().tolist()
+    mask = (1 << 56) - 1
+
+    def t(v):
+        return (v & mask) / 1e3 if v else None  # us
+
+    t0 = min(t(r[250]) for r in tr if r[250])
+    ph = {k: [] for k in ("pdl_wait", "to_first_S", "stream", "main_end", "barrier_wait", "merge",
+                          "total")}
+    sm_gap, sm_busy, vote, p_write, qk_lat = [], [], [], [], []
+    for r in tr:
+        start, pdl, mend, bout, mdone = (t(r[s]) for s in (250, 254, 251, 252, 253))
+        if not (start and mend and bout and mdone):
+            continue
+        sm = [(r[k] >> 56, t(r[k])) for k in range(256) if r[k]]
+        s_ready = [x for tag, x in sm if tag == 20]
+        voted = [x for tag, x in sm if tag in (21, 22)]
+        handed = [x for tag, x in sm if tag == 23]
+        ph["pdl_wait"].append(pdl - start)
+        if s_ready:
+            ph["to_first_S"].append(s_ready[0] - pdl)
+            ph["stream"].append(mend - s_ready[0])
+        ph["main_end"].append(mend - t0)
+        ph["barrier_wait"].append(bout - mend)
+        ph["merge"].append(mdone - bout)
+        ph["total"].append(mdone - t0)
+        n = min(len(s_ready), len(voted), len(handed))
+        for k in range(n):
+            vote.append(voted[k] - s_ready[k])
+            p_write.append(handed[k] - voted[k])
+            sm_busy.append(handed[k] - s_ready[k])
+            if k + 1 < len(s_ready):
+                sm_gap.append(s_ready[k + 1] - handed[k])
+        qk_issued = [t(r[512 + u]) for u in range(256) if r[512 + u]]
+        for u in range(min(len(qk_issued), len(s_ready))):
+            qk_lat.append(s_ready[u] - qk_issued[u])
+    res = {"config": name, "plan": ba.ba_plan_string(prob), "ctas": G,
+           "phases_us_median": {k: med(v) for k, v in ph.items()},
+           "phases_us_max": {k: round(max(v), 3) if v else None for k, v in ph.items()},
+           "per_tile_us_median": {"S_ready_to_vote": med(vote), "vote_to_P_handed": med(p_write),
+                                  "softmax_busy": med(sm_busy), "P_handed_to_next_S": med(sm_gap),
+                                  "QK_issue_to_S_ready": med(qk_lat)},
+           "tiles_per_cta_median": med([len([1 for k in range(256) if r[k] and r[k] >> 56 == 20])
+                                        for r in tr])}
+    print(json.dumps(res), flush=True)
+
+
+if __name__ == "__main__":
+    for nm in sys.argv[1:] or ["mha7b_b32", "mha7b_b32_fp8"]:
+        run(nm)
