@@ -1334,17 +1334,23 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
           tc::mbar_wait(tc::smem_u32(&kv_full[st]), (u / NST) & 1);
           uint8_t* const stage = sm_stage + st * kStageBytes;
           // K (kv = 0) then V (kv = 1): the codes of row R (region + 16 KB +
-          // R*128) expand to f16 row R of both 64-column halves.  Lane: row R
-          // of an 8-row block, code chunks c0 and c0 + 4 (-> half 0 and half 1).
+          // R*128) expand to f16 row R of both 64-column halves.  Lane: code
+          // chunks c0 and c0 + 4 (-> half 0 and half 1) of row r8 of an 8-row
+          // block; an 8-lane shared-memory phase covers rows k and k + 4, whose
+          // swizzled chunk sets are complementary (conflict-free loads), and
+          // the second row of a phase stores its odd f16 chunk first (the two
+          // rows then hit even and odd chunk sets: conflict-free stores).
           // Half-1 rows overwrite the code rows they come from: a block's
           // stores follow a __syncwarp after all its loads (and the next
           // block's prefetch, which reads other rows).
+          const int r8 = ((lane >> 2) & 1) * 4 + (lane >> 3);
+          const bool odd_first = (lane >> 2) & 1;
 #pragma unroll
           for (int kv = 0; kv < 2; ++kv) {
             uint8_t* const reg = stage + kv * 32768;
             const int c0 = lane & 3;
             auto code_at = [&](int blk, int c) {
-              const int R = 32 * cw + 8 * blk + (lane >> 2);
+              const int R = 32 * cw + 8 * blk + r8;
               return lds128(reg + 16384 + R * 128 + ((c ^ (R & 7)) << 4));
             };
             uint4 a0 = code_at(0, c0), a1 = code_at(0, c0 + 4);
@@ -1364,15 +1370,16 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
               h1a.z = e4m3x2_to_f16x2(a1.y); h1a.w = e4m3x2_to_f16x2(a1.y >> 16);
               h1b.x = e4m3x2_to_f16x2(a1.z); h1b.y = e4m3x2_to_f16x2(a1.z >> 16);
               h1b.z = e4m3x2_to_f16x2(a1.w); h1b.w = e4m3x2_to_f16x2(a1.w >> 16);
-              const int R = 32 * cw + 8 * blk + (lane >> 2);
-              const int cc = 2 * c0, x = R & 7;
+              const int R = 32 * cw + 8 * blk + r8;
+              const int x = R & 7;
+              const int ca = 2 * c0 + (odd_first ? 1 : 0), cb = 2 * c0 + (odd_first ? 0 : 1);
               __syncwarp();  // every lane's loads of this block precede the overwrite
               uint8_t* const d0 = reg + R * 128;
               uint8_t* const d1 = reg + 16384 + R * 128;
-              sts128(d0 + ((cc ^ x) << 4), h0a);
-              sts128(d0 + (((cc + 1) ^ x) << 4), h0b);
-              sts128(d1 + ((cc ^ x) << 4), h1a);
-              sts128(d1 + (((cc + 1) ^ x) << 4), h1b);
+              sts128(d0 + ((ca ^ x) << 4), odd_first ? h0b : h0a);
+              sts128(d0 + ((cb ^ x) << 4), odd_first ? h0a : h0b);
+              sts128(d1 + ((ca ^ x) << 4), odd_first ? h1b : h1a);
+              sts128(d1 + ((cb ^ x) << 4), odd_first ? h1a : h1b);
               if (blk < 3) {
                 a0 = n0;
                 a1 = n1;
@@ -1417,12 +1424,14 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
     my_ndec = dec_parts(P, i, c / P.gpc);
   }
   if (threadIdx.x == 0) {
+    tstamp(249, 49);
     // generation barrier: grid_ctr[0] counts arrivals (reset by the last
     // arriver), grid_ctr[1] is the generation it then advances
     unsigned gen;
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(gen) : "l"(P.grid_ctr + 1) : "memory");
     unsigned old;
     asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(P.grid_ctr) : "memory");
+    tstamp(248, 48);
     if (old == (unsigned)P.G - 1u) {
       asm volatile("st.relaxed.gpu.global.u32 [%0], 0;" ::"l"(P.grid_ctr) : "memory");
       asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(P.grid_ctr + 1) : "memory");

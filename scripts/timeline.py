@@ -64,6 +64,7 @@ def run(name):
     ph = {k: [] for k in ("pdl_wait", "to_first_S", "stream", "main_end", "barrier_wait", "merge",
                           "total")}
     sm_gap, sm_busy, vote, p_write, qk_lat = [], [], [], [], []
+    abs_t = {"first_S": [], "main_end": [], "barrier_out": [], "merge_done": [], "segments": []}
     for r in tr:
         start, pdl, mend, bout, mdone = (t(r[s]) for s in (250, 254, 251, 252, 253))
         if not (start and mend and bout and mdone):
@@ -72,6 +73,12 @@ def run(name):
         s_ready = [x for tag, x in sm if tag == 20]
         voted = [x for tag, x in sm if tag in (21, 22)]
         handed = [x for tag, x in sm if tag == 23]
+        abs_t["main_end"].append(mend - t0)
+        abs_t["barrier_out"].append(bout - t0)
+        abs_t["merge_done"].append(mdone - t0)
+        abs_t["segments"].append(sum(1 for tag, _ in sm if tag == 4))
+        if s_ready:
+            abs_t["first_S"].append(s_ready[0] - t0)
         ph["pdl_wait"].append(pdl - start)
         if s_ready:
             ph["to_first_S"].append(s_ready[0] - pdl)
@@ -90,12 +97,31 @@ def run(name):
         qk_issued = [t(r[512 + u]) for u in range(256) if r[512 + u]]
         for u in range(min(len(qk_issued), len(s_ready))):
             qk_lat.append(s_ready[u] - qk_issued[u])
-    res = {"config": name, "plan": ba.ba_plan_string(prob), "ctas": G,
+    # per-CTA regression of the main-loop end on its context / decode tile counts
+    cs = ba.ba_plan_ctas(prob)
+    Tc = cfg.g * (-(-cfg.b * cfg.p // 32)) * (-(-cfg.mc // 128)) if cfg.b * cfg.p < 64 else 0
+    import numpy as np
+    X, y = [], []
+    for k, r in enumerate(tr):
+        if r[251] and r[250]:
+            nc = max(0, min(cs[k + 1], Tc) - cs[k])
+            nd = (cs[k + 1] - cs[k]) - nc
+            X.append([1.0, nc, nd])
+            y.append(t(r[251]) - t0)
+    coef = np.linalg.lstsq(np.array(X), np.array(y), rcond=None)[0].tolist() if len(X) > 3 else None
+    before = [t(r[249]) - t0 for r in tr if r[249]]
+    after = [t(r[248]) - t0 for r in tr if r[248]]
+    res = {"config": name, "main_end_fit_us": {"const": coef[0], "per_ctx_tile": coef[1],
+                                               "per_dec_tile": coef[2]} if coef else None,
+           "barrier_atomic_issue_min_med_max": [round(min(before), 2), med(before), round(max(before), 2)] if before else None,
+           "barrier_atomic_return_min_med_max": [round(min(after), 2), med(after), round(max(after), 2)] if after else None, "plan": ba.ba_plan_string(prob), "ctas": G,
            "phases_us_median": {k: med(v) for k, v in ph.items()},
            "phases_us_max": {k: round(max(v), 3) if v else None for k, v in ph.items()},
            "per_tile_us_median": {"S_ready_to_vote": med(vote), "vote_to_P_handed": med(p_write),
                                   "softmax_busy": med(sm_busy), "P_handed_to_next_S": med(sm_gap),
                                   "QK_issue_to_S_ready": med(qk_lat)},
+           "abs_us_min_med_max": {k: [round(min(v), 2), med(v), round(max(v), 2)] if v else None
+                                  for k, v in abs_t.items()},
            "tiles_per_cta_median": med([len([1 for k in range(256) if r[k] and r[k] >> 56 == 20])
                                         for r in tr])}
     print(json.dumps(res), flush=True)
