@@ -81,6 +81,9 @@ struct BifTcParams {
   int bw, nband;             // context band width (tiles) and bands per group (see seg_at)
   int ext_ctx;               // > 0: the context branch ran in ctx_rows_kernel (ctx_rows.cuh),
                              // which wrote ext_ctx context partials per row (slots [0, ext_ctx))
+  int late_wait;             // 1: launched right behind ctx_rows_kernel (PDL) to stream the
+                             // decode tiles on the SMs it leaves free, concurrently with it:
+                             // wait for it (griddepcontrol.wait) only before the merge
   int spc;                   // samples per context row chunk = N / p
   int gpc, ndc;              // groups per decode chunk = N / p; decode chunks per sample
   int qd_rows;               // rows of the decode q box = min(N, h)
@@ -131,8 +134,9 @@ __host__ __device__ constexpr int tmem_cols(int N) {
 // and per P part; P = P_hi | P_lo, or one f16 part with KV8), col-max scratch
 // [4][N], row sums [2][4][N], m_run [2][N], final m [2][N] (floats), lengths
 // [64] ints, barriers (512 B)
+// + 128 B: the merge part counts of each warp's first output row
 __host__ __device__ constexpr int smem_fixed(int N, int npb, bool kv8 = false) {
-  return (2 + (kv8 ? 1 : 2) * npb) * 256 * N + 4 * (4 * N + 8 * N + 2 * N + 2 * N) + 256 + 512;
+  return (2 + (kv8 ? 1 : 2) * npb) * 256 * N + 4 * (4 * N + 8 * N + 2 * N + 2 * N) + 256 + 512 + 128;
 }
 
 // CTA owning flat tile f (the CTA ranges [cs[k], cs[k+1]) are non-empty and
@@ -551,6 +555,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
   uint64_t* v_cvt = bars + 40;     // [4]  KV8: V of the stage converted to f16
   uint64_t* q_cvt = bars + 44;     // [2]  KV8: q converted to f16
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 48);
+  int* sm_mcnt = reinterpret_cast<int*>(bars + 64);  // [16 warps][2]: merge part counts
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   auto tstamp = [&](int slot, unsigned long long tag) {
@@ -560,6 +565,9 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
 #endif
   };
   if (threadIdx.x == 0) tstamp(250, 50);
+  const int rows = P.b * P.h;
+  const int r0 = (int)((long long)blockIdx.x * rows / P.G);
+  const int r1 = (int)((long long)(blockIdx.x + 1) * rows / P.G);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < NST; ++s) {
@@ -604,7 +612,9 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
   // programmatic dependent launch: the prologue above overlapped the previous
   // kernel; wait for it before touching any global memory, and let the next
   // launch start its own prologue
-  pdl_wait();
+  // (concurrent decode launch: ctx_rows_kernel triggered this launch after its
+  // own wait, so every earlier kernel is complete; only its partials are not)
+  if (!P.late_wait) pdl_wait();
   pdl_launch_dependents();
   if (threadIdx.x == 0) tstamp(254, 54);
   const uint32_t tmem = *tmem_holder;
@@ -1221,6 +1231,22 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
     pf.mark(6);
     if (threadIdx.x == 128 || threadIdx.x == 256)
       pf.dump(P.trace ? P.trace + (size_t)blockIdx.x * kTraceSlots : nullptr, threadIdx.x == 128 ? 0 : 8);
+  } else if (warp == 2) {
+    // ===== merge bookkeeping, off the critical path (this warp is otherwise
+    // idle after the TMEM allocation): part counts of every warp's first
+    // merge row (binary searches of the CTA table) =====
+    if (lane < (int)(blockDim.x >> 5)) {
+      const int gr = r0 + lane;
+      int nc = 0, nd = 0;
+      if (gr < r1) {
+        const int i = gr / P.h, j = gr - i * P.h;
+        const int c = j / P.p;
+        nc = ctx_parts(P, c, (i * P.p + (j - c * P.p)) / P.N);
+        nd = dec_parts(P, i, c / P.gpc);
+      }
+      sm_mcnt[2 * lane] = nc;
+      sm_mcnt[2 * lane + 1] = nd;
+    }
   } else if (warp >= EPI0 && warp < EPI0 + 4) {
     // ===================== epilogue warpgroup (4 warps) =====================
     // O^T lanes are d = 32*(warp%4) + lane; columns are the chunk's rows.
@@ -1403,6 +1429,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
     }
   }
   tc::tc_fence_before();
+  if (P.late_wait) pdl_wait();  // the context partials of ctx_rows_kernel are complete
   __syncthreads();
   if (threadIdx.x == 0) tstamp(251, 51);
   if (warp == 2) {
@@ -1412,17 +1439,9 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
   // ---- grid-wide barrier (cooperative launch: all CTAs are resident), then
   //      every CTA joins the partials of its share of the output rows ----
   // part counts of this CTA's merge rows (computed while waiting)
-  const int rows = P.b * P.h;
-  const int r0 = (int)((long long)blockIdx.x * rows / P.G);
-  const int r1 = (int)((long long)(blockIdx.x + 1) * rows / P.G);
   const int nwarps = (int)(blockDim.x >> 5);
-  int my_gr = r0 + warp, my_nctx = 0, my_ndec = 0;
-  if (my_gr < r1) {
-    const int i = my_gr / P.h, j = my_gr - i * P.h;
-    const int c = j / P.p;
-    my_nctx = ctx_parts(P, c, (i * P.p + (j - c * P.p)) / P.N);
-    my_ndec = dec_parts(P, i, c / P.gpc);
-  }
+  const int my_gr = r0 + warp;
+  int my_nctx = sm_mcnt[2 * warp], my_ndec = sm_mcnt[2 * warp + 1];
   if (threadIdx.x == 0) {
     tstamp(249, 49);
     // generation barrier: grid_ctr[0] counts arrivals (reset by the last

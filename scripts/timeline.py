@@ -108,11 +108,13 @@ def run(name):
             nd = (cs[k + 1] - cs[k]) - nc
             X.append([1.0, nc, nd])
             y.append(t(r[251]) - t0)
+    per_cta = [[int(X[k][1]), int(X[k][2]), round(y[k], 2)] for k in range(len(X))]
     coef = np.linalg.lstsq(np.array(X), np.array(y), rcond=None)[0].tolist() if len(X) > 3 else None
     before = [t(r[249]) - t0 for r in tr if r[249]]
     after = [t(r[248]) - t0 for r in tr if r[248]]
     res = {"config": name, "main_end_fit_us": {"const": coef[0], "per_ctx_tile": coef[1],
                                                "per_dec_tile": coef[2]} if coef else None,
+           "per_cta_ctx_dec_mainend": per_cta,
            "barrier_atomic_issue_min_med_max": [round(min(before), 2), med(before), round(max(before), 2)] if before else None,
            "barrier_atomic_return_min_med_max": [round(min(after), 2), med(after), round(max(after), 2)] if after else None, "plan": ba.ba_plan_string(prob), "ctas": G,
            "phases_us_median": {k: med(v) for k, v in ph.items()},
