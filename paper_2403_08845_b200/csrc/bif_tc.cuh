@@ -81,9 +81,6 @@ struct BifTcParams {
   int bw, nband;             // context band width (tiles) and bands per group (see seg_at)
   int ext_ctx;               // > 0: the context branch ran in ctx_rows_kernel (ctx_rows.cuh),
                              // which wrote ext_ctx context partials per row (slots [0, ext_ctx))
-  int late_wait;             // 1: launched right behind ctx_rows_kernel (PDL) to stream the
-                             // decode tiles on the SMs it leaves free, concurrently with it:
-                             // wait for it (griddepcontrol.wait) only before the merge
   int spc;                   // samples per context row chunk = N / p
   int gpc, ndc;              // groups per decode chunk = N / p; decode chunks per sample
   int qd_rows;               // rows of the decode q box = min(N, h)
@@ -612,9 +609,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
   // programmatic dependent launch: the prologue above overlapped the previous
   // kernel; wait for it before touching any global memory, and let the next
   // launch start its own prologue
-  // (concurrent decode launch: ctx_rows_kernel triggered this launch after its
-  // own wait, so every earlier kernel is complete; only its partials are not)
-  if (!P.late_wait) pdl_wait();
+  pdl_wait();
   pdl_launch_dependents();
   if (threadIdx.x == 0) tstamp(254, 54);
   const uint32_t tmem = *tmem_holder;
@@ -838,6 +833,10 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
         float* nred = reinterpret_cast<float*>(sm_len);  // [2 slots][4 quads][kNarrowP]
         bool e_waited = false;
         const int cfirst = cl;
+        // first column of the group whose P a slot holds (-1: arbitrary data,
+        // e.g. from a context segment): the other columns of a slot stay zero
+        // from tile to tile, so only a group switch re-zeroes p columns
+        int pcol0 = -1, pcol1 = -1;
         float m_g[kNarrowP], l_g[kNarrowP];
 #pragma unroll
         for (int k = 0; k < kNarrowP; ++k) {
@@ -889,7 +888,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
               }
             }
           }
-          tc::named_bar_sync(2, 32 * NSW);
+          if (h0) tc::named_bar_sync(3, 128);  // the 4 half-0 warps (one per quadrant)
           pf.mark(2);
           if (h0) {
             float pv[kNarrowP], alpha[kNarrowP], tm[kNarrowP];
@@ -943,12 +942,31 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
             if (!(BIF_DBG & 8)) tc::mbar_wait(tc::smem_u32(&p_empty[ps]), (ph & 1) ^ 1);  // PV(u-npb) done
             uint8_t* const sm_pb = sm_p + ps * PB;
             pf.mark(4);
+            const int pc = ps ? pcol1 : pcol0;
+            if (pc < 0) {
 #pragma unroll
-            for (int n = 0; n < NP; n += 8) {
-              uint32_t off = (uint32_t)((n / W) * PLBO + pos * PRB + (n % W) * 2);
-              off ^= ((off >> 7) & PSWM) << 4;
-              *reinterpret_cast<uint4*>(sm_pb + off) = make_uint4(0, 0, 0, 0);
+              for (int n = 0; n < NP; n += 8) {
+                uint32_t off = (uint32_t)((n / W) * PLBO + pos * PRB + (n % W) * 2);
+                off ^= ((off >> 7) & PSWM) << 4;
+                *reinterpret_cast<uint4*>(sm_pb + off) = make_uint4(0, 0, 0, 0);
+              }
+            } else if (pc != cv0) {
+#pragma unroll
+              for (int k = 0; k < kNarrowP; ++k) {
+                if (k < P.p) {  // the previous group's columns (both parts) back to zero
+                  const int col = pc + k;
+                  uint32_t off = (uint32_t)((col / W) * PLBO + pos * PRB + (col % W) * 2);
+                  off ^= ((off >> 7) & PSWM) << 4;
+                  *reinterpret_cast<uint16_t*>(sm_pb + off) = 0;
+                  if constexpr (!KV8) {
+                    uint32_t offl = (uint32_t)(((N + col) / W) * PLBO + pos * PRB + ((N + col) % W) * 2);
+                    offl ^= ((offl >> 7) & PSWM) << 4;
+                    *reinterpret_cast<uint16_t*>(sm_pb + offl) = 0;
+                  }
+                }
+              }
             }
+            if (ps) pcol1 = cv0; else pcol0 = cv0;
 #pragma unroll
             for (int k = 0; k < kNarrowP; ++k) {
               if (k < P.p) {
@@ -1429,7 +1447,6 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
     }
   }
   tc::tc_fence_before();
-  if (P.late_wait) pdl_wait();  // the context partials of ctx_rows_kernel are complete
   __syncthreads();
   if (threadIdx.x == 0) tstamp(251, 51);
   if (warp == 2) {

@@ -128,7 +128,6 @@ struct Plan {
   // decode branch also in the rows kernel (p >= 32 rows per sample and group);
   // the second launch is then the light merge kernel, not the fused kernel
   bool cr_dec = false;
-  bool cr_conc = false;  // decode launch concurrent with the rows kernel (SM split)
   int cr_items_ctx = 0;
   long long tc_Tc = 0, tc_T = 0;
   int tc_cs[ba::bif_max_ctas + 1];
@@ -312,32 +311,21 @@ int make_plan(const ba_problem_t* pr_in, int sms, bool replicated, Plan* pl) {
     // decode part is small (<= 4096 tiles: C3, multi-token C2b), where a second
     // persistent launch costs more than the half-empty row blocks (measured:
     // C3 88.8 -> 78 us; C5's 131072 decode tiles stay in the fused kernel)
-    // decode items in the rows kernel only when p >= 32 rows fill a useful
-    // share of the 128-row block (C4); otherwise the decode tiles stream
-    // through the fused kernel (narrow path) launched right behind the rows
-    // kernel and running CONCURRENTLY with it on the SMs it leaves free
-    if (rows_dec_env && (p >= 32 || rows_dec_env == 2) && p <= 128 && pr->md_cap >= 1) {
+    // decode items too when p >= 32 (they fill the row block) or when the
+    // decode part is small (<= 4096 tiles: C3, multi-token C2b), where a second
+    // persistent launch costs more than the half-empty row blocks (measured:
+    // C3 88.8 -> 78 us; C5's 131072 decode tiles stay in the fused kernel).
+    // (Round 2 measured a decode launch running CONCURRENTLY with the rows
+    // kernel on the SMs it leaves free — PDL, griddepcontrol.wait only before
+    // the merge: the cooperative decode launch does not start until the rows
+    // kernel has drained, so C3 took 124 us and C5 3.3 ms; not used.)
+    const long long dec_tiles = (long long)b * g * cdiv(pr->md_cap, 128);
+    if (rows_dec_env && (p >= 32 || dec_tiles <= 4096 || rows_dec_env == 2) && p <= 128 &&
+        pr->md_cap >= 1) {
       P.cr_dec = true;
       P.cr_items += b * g;
     }
     P.cr_grid = std::min(P.cr_items, sms);
-    P.cr_conc = !P.cr_dec && pr->md_cap >= 1;
-    if (P.cr_conc) {
-      // SM split by work: a 128-row context pass and a 128-position decode
-      // tile cost about the same SM time (round-2 measurements: ~1-1.8 us
-      // each), so the rows kernel gets its share of the SMs
-      const double passes = (double)g * P.cr_nrb * P.cr_ntile;
-      const double dtiles = (double)b * g * cdiv(pr->md_cap, 128);
-      int X = (int)(sms * passes / (passes + dtiles) + 0.5);
-      X = std::max(8, std::min(X, sms - 16));
-      // re-split the context so its items fill the X CTAs
-      int ns2 = std::max(1, X / (g * P.cr_nrb));
-      ns2 = std::max(1, std::min(ns2, P.cr_ntile));
-      P.cr_tps = cdiv(P.cr_ntile, ns2);
-      P.cr_nsplit = cdiv(P.cr_ntile, P.cr_tps);
-      P.cr_items = P.cr_items_ctx = g * P.cr_nrb * P.cr_nsplit;
-      P.cr_grid = std::min(P.cr_items, X);
-    }
   }
   if (tcN) {
     P.tc = true;
@@ -351,8 +339,7 @@ int make_plan(const ba_problem_t* pr_in, int sms, bool replicated, Plan* pl) {
     P.tc_ntile_d = cdiv(P.lens_offset + P.dec_cap, 128);
     P.tc_Tc = (long long)g * P.tc_nrc * P.tc_ntile_c;
     P.tc_T = P.tc_Tc + (long long)g * b * P.tc_ntile_d;
-    int gmax = sms < ba::bif_max_ctas ? sms : ba::bif_max_ctas;
-    if (P.cr_conc) gmax = std::min(gmax, sms - P.cr_grid);  // the SMs the rows kernel leaves
+    const int gmax = sms < ba::bif_max_ctas ? sms : ba::bif_max_ctas;
     P.tc_G = (int)(P.tc_T < gmax ? P.tc_T : gmax);
     if (P.tc_T == 0) P.tc_G = gmax;  // no tiles (ctx_rows, md_cap = 0): the merge only
     // P double-buffered when that keeps the K/V stage count (else one slot)
@@ -738,7 +725,6 @@ int run_tc(const ba_problem_t* pr, const Plan& P, const void* q, const void* Kc,
   bp.rot = rot_env;
   memcpy(bp.cs, P.tc_cs, sizeof(int) * (P.tc_G + 1));
   bp.ext_ctx = P.ctx_rows ? P.cr_nsplit : 0;
-  bp.late_wait = (P.cr_conc && !(pr->flags & BA_FLAG_NO_PDL)) ? 1 : 0;
   bp.scale_log2 = scale_log2;
   bp.vscale = (P.kv8 && pr->v_scale > 0.f) ? pr->v_scale : 1.f;
   bp.S = P.S; bp.Sc = P.tc_Sc;
@@ -1267,9 +1253,9 @@ const char* ba_plan_string(const ba_problem_t* prob) {
   else if (P.tc && P.ctx_rows)
     snprintf(g_plan_buf, sizeof g_plan_buf,
              "ctx_rows(blocks=%d,splits=%d,tiles/split=%d,items=%d,ctas=%d) + "
-             "dec_tc(N=%d,dec_tiles=%lld,ctas=%d,stages=%d,slots=%d+%d)%s launches=2 ws=%zu",
+             "dec_tc(N=%d,dec_tiles=%lld,ctas=%d,stages=%d,slots=%d+%d) launches=2 ws=%zu",
              P.cr_nrb, P.cr_nsplit, P.cr_tps, P.cr_items, P.cr_grid, P.tc_N, P.tc_T, P.tc_G,
-             P.tc_nst, P.tc_Sc, P.tc_Sd, P.cr_conc ? " concurrent" : "", P.ws_bytes);
+             P.tc_nst, P.tc_Sc, P.tc_Sd, P.ws_bytes);
   else if (P.tc)
     snprintf(g_plan_buf, sizeof g_plan_buf,
              "fused_tc(N=%d,nrc=%d,band=%d,ctx_tiles=%lld,dec_tiles=%lld,ctas=%d,stages=%d,pbuf=%d,"
