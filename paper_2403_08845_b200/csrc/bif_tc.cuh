@@ -611,6 +611,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
   // HBM is nearly idle).  Only L2 is touched — the TMA loads below still read
   // after the wait, and L2 is the coherence point, so a line the previous
   // kernel writes later is simply re-read.
+#ifndef BIFATTN_NO_L2PF
   if (warp == 0 && lane == 0) {
     const Range r0g = my_range(P);
     const long long npf = r0g.n() < NST ? r0g.n() : NST;
@@ -628,6 +629,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
       }
     }
   }
+#endif
   // programmatic dependent launch: the prologue above overlapped the previous
   // kernel; wait for it before touching any global memory, and let the next
   // launch start its own prologue
