@@ -606,30 +606,6 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
-  // L2 prefetch of this CTA's first tiles (one per K/V stage) BEFORE the PDL
-  // wait: it overlaps the previous kernel's tail (its barrier and merge, when
-  // HBM is nearly idle).  Only L2 is touched — the TMA loads below still read
-  // after the wait, and L2 is the coherence point, so a line the previous
-  // kernel writes later is simply re-read.
-#ifndef BIFATTN_NO_L2PF
-  if (warp == 0 && lane == 0) {
-    const Range r0g = my_range(P);
-    const long long npf = r0g.n() < NST ? r0g.n() : NST;
-    for (long long w = 0; w < npf; ++w) {
-      bool dec;
-      int z, t;
-      tile_at(P, r0g, w, dec, z, t);
-      const CUtensorMap* mk = dec ? &P.tmKd : &P.tmKc;
-      const CUtensorMap* mv = dec ? &P.tmVd : &P.tmVc;
-      tc::tma_prefetch_3d(mk, 0, t * kBM, z);
-      tc::tma_prefetch_3d(mv, 0, t * kBM, z);
-      if (!KV8) {
-        tc::tma_prefetch_3d(mk, 64, t * kBM, z);
-        tc::tma_prefetch_3d(mv, 64, t * kBM, z);
-      }
-    }
-  }
-#endif
   // programmatic dependent launch: the prologue above overlapped the previous
   // kernel; wait for it before touching any global memory, and let the next
   // launch start its own prologue

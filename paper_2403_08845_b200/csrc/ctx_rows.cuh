@@ -13,17 +13,21 @@
 //
 // Tile math (rows on M):
 //   S[128 rows x 128 pos]  = Q_blk[128 x d] . K_tile^T       (A = Q, B = K, both K-major)
-//   O[128 rows x d]       += P_hi . V_tile + P_lo . V_tile   (A = P K-major, B = V MN-major)
+//   O[128 rows x d]       += P . V16_tile                     (A = P K-major, B = V MN-major)
 // Two threads own a row (TMEM lane = row, one per half of the positions):
 // the row max is a 2-way exchange, the stale-max test and the O rescale are
-// per row — no vote across the rows of a column as in the swap-AB kernel.  P = P_hi + P_lo
-// (two bf16 parts, ~16 significant bits, reading R13) is stored to TMEM and
-// read from there as the PV's A operand; both parts accumulate into the same
-// fp32 O.  TMEM: 3 S slots (P(u) overwrites S(u)) + O = 512 columns.
+// per row — no vote across the rows of a column as in the swap-AB kernel.
+// Round 2 (reading R23): the V tile is converted in place to f16 x 2^-8 by two
+// converter warps once it lands, so P = 2^(x - m) enters the PV MMA as ONE
+// f16 operand (11 significant bits; the bf16 pair P_hi + P_lo of round 1 cost
+// twice the PV MMAs), stored to TMEM over its S slot and read from there as
+// the A operand; the epilogue scales O back by 2^8 (exact).  TMEM: 3 S slots
+// (P(u) overwrites S(u)) + O = 512 columns.
 //
 // Warps: 0 / 3 TMA producers of the K / V halves (one lane each), 1 MMA
-// issuer (one lane), 2 TMEM allocator, 4..11 softmax/epilogue: two threads
-// per row, each taking half of the tile's positions and of the O columns.
+// issuer (one lane), 2 TMEM allocator and (with 12) V converter, 4..11
+// softmax/epilogue: two threads per row, each taking half of the tile's
+// positions and of the O columns.
 #pragma once
 #include "append.cuh"
 #include "common.cuh"
@@ -69,7 +73,8 @@ constexpr int kXch = kBar + 256;        // row-max exchange [2 tiles][2 halves][
 constexpr int kLsx = kXch + 2048;       // item-end row-sum exchange [128 rows] floats (own slot)
 constexpr int kSmem = kLsx + 512;       // 232192 <= 227 KB
 constexpr float kTh = 8.0f;             // stale-max slack (log2 units), as bif_tc.cuh
-constexpr int kThreads = 384;
+constexpr int kThreads = 416;        // 13 warps: + warp 12, the second V converter
+constexpr float kVScale = 0.00390625f;  // V is converted to f16 as V * 2^-8 (reading R23)
 
 // byte offset of 16-byte chunk `ch` (0..15) of row r in a 128-row x 128-col
 // bf16 K-major SW128 tile stored as two 64-column halves (the TMA box layout)
@@ -97,7 +102,8 @@ __global__ void __launch_bounds__(ctxr::kThreads, 1)
   uint64_t* v_full = bars + 17;   // [kNst]
   uint64_t* v_empty = bars + 20;  // [kNst]
   uint64_t* p_full = bars + 23;   // [kS] P(u) stored over S(u)
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 26);
+  uint64_t* v_cvt = bars + 26;    // [kNst] V(u) converted to f16 in place
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 30);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
@@ -117,6 +123,7 @@ __global__ void __launch_bounds__(ctxr::kThreads, 1)
     tc::mbar_init(tc::smem_u32(p_empty), 1);
     tc::mbar_init(tc::smem_u32(o_full), 1);
     tc::mbar_init(tc::smem_u32(o_empty), 8);
+    for (int s = 0; s < kNst; ++s) tc::mbar_init(tc::smem_u32(&v_cvt[s]), 64);
     tc::fence_mbar_init();
   }
   if (warp == 0 && lane == 0) {
@@ -221,29 +228,27 @@ __global__ void __launch_bounds__(ctxr::kThreads, 1)
     // ============================ MMA issuer ==============================
     if (lane == 0) {
       constexpr uint32_t IDESC_QK = tc::idesc_bf16(128, 128, 0, 0);
-      constexpr uint32_t IDESC_PV = tc::idesc_bf16(128, 128, 0, 1);
+      constexpr uint32_t IDESC_PV = tc::idesc_f16(128, 128, 0, 1);  // f16 P (TMEM) x f16 V
       const uint32_t qbase = tc::smem_u32(smem + kQ);
       uint32_t u = 0, it = 0;
       // O += P(v) . V(v): both bf16 parts of P into the same accumulator
       Prof pf;  // 0 q_full, 1 k_full, 2 s_free, 3 QK issue, 4 v_full, 5 p_full, 6 PV issue, 7 o_empty
       auto pv = [&](uint32_t v, bool first) {
         pf.mark(3);
-        tc::mbar_wait_sleep(tc::smem_u32(&v_full[v % kNst]), (v / kNst) & 1);
+        tc::mbar_wait_sleep(tc::smem_u32(&v_cvt[v % kNst]), (v / kNst) & 1);
         pf.mark(4);
         tc::mbar_wait_sleep(tc::smem_u32(&p_full[v % kS]), (v / kS) & 1);
         pf.mark(5);
         tc::tc_fence_after();
         const uint32_t vb = tc::smem_u32(smem + (v % kNst) * kStage + 32768);
 #pragma unroll
-        for (int part = 0; part < 2; ++part)
-#pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            // A = P from TMEM: 16 positions per step = 8 columns of bf16 pairs
-            const uint64_t bd = tc::smem_desc(vb + k * 2048, 16384, 1024, tc::kSw128);
-            if (!(CTXR_EXP & 4))
-              tc::mma_bf16_ts(tO, tS + (v % kS) * 128 + part * 64 + k * 8, bd, IDESC_PV,
-                              (first && part == 0 && k == 0) ? 0u : 1u);
-          }
+        for (int k = 0; k < 8; ++k) {
+          // A = P from TMEM: 16 positions per step = 8 columns of f16 pairs
+          const uint64_t bd = tc::smem_desc(vb + k * 2048, 16384, 1024, tc::kSw128);
+          if (!(CTXR_EXP & 4))
+            tc::mma_bf16_ts(tO, tS + (v % kS) * 128 + k * 8, bd, IDESC_PV,
+                            (first && k == 0) ? 0u : 1u);
+        }
         tc::mma_commit(tc::smem_u32(&s_free[v % kS]));
         tc::mma_commit(tc::smem_u32(&v_empty[v % kNst]));
         pf.mark(6);
@@ -288,7 +293,33 @@ __global__ void __launch_bounds__(ctxr::kThreads, 1)
       pf.mark(3);
       pf.dump(P.trace ? P.trace + (size_t)blockIdx.x * 1024 : nullptr, 8);
     }
-  } else if (warp >= 4) {
+  } else if (warp == 2 || warp == 12) {
+    // ============ V converters (warps 2 and 12): bf16 V tile -> f16 * 2^-8 in place ============
+    // (element-wise and in place, so the TMA's SW128 layout is kept; each warp
+    // takes half of the tile's 2048 16-byte chunks, consecutive lanes on
+    // consecutive chunks: conflict-free)
+    const int half = warp == 2 ? 0 : 1;
+    uint32_t u = 0;
+    for (int k = blockIdx.x; k < P.items; k += gridDim.x) {
+      const Item I = item_of(k);
+      for (int t = I.t0; t < I.t1; ++t, ++u) {
+        const int st = u % kNst;
+        tc::mbar_wait(tc::smem_u32(&v_full[st]), (u / kNst) & 1);
+        uint8_t* const vt = smem + st * kStage + 32768;
+#pragma unroll 4
+        for (int ch = half * 1024 + lane; ch < half * 1024 + 1024; ch += 32) {
+          uint4 v = lds128(vt + ch * 16);
+          v.x = pack_f16x2(bf16lo(v.x) * kVScale, bf16hi(v.x) * kVScale);
+          v.y = pack_f16x2(bf16lo(v.y) * kVScale, bf16hi(v.y) * kVScale);
+          v.z = pack_f16x2(bf16lo(v.z) * kVScale, bf16hi(v.z) * kVScale);
+          v.w = pack_f16x2(bf16lo(v.w) * kVScale, bf16hi(v.w) * kVScale);
+          sts128(vt + ch * 16, v);
+        }
+        tc::fence_proxy_async_smem();
+        tc::mbar_arrive(tc::smem_u32(&v_cvt[st]));
+      }
+    }
+  } else if (warp >= 4 && warp < 12) {
     // ============ softmax + epilogue: two threads per row (one per half) ============
     // warps 4..7 (hf = 0) take positions [0, 64) and O columns [0, 64) of their
     // rows, warps 8..11 (hf = 1) positions [64, 128) and O columns [64, 128);
@@ -385,19 +416,18 @@ __global__ void __launch_bounds__(ctxr::kThreads, 1)
         }
         pf.mark(5);
         const float mref = m == kNegInf ? 0.f : m;  // a row with no valid position yet: P = 0
-        // P = 2^(x - m) as P_hi + P_lo (bf16 pairs) into TMEM: the PV's A operand
+        // P = 2^(x - m) as ONE f16 operand (reading R23; V is f16 * 2^-8) into
+        // TMEM over S: the PV's A operand
 #pragma unroll
         for (int j = 0; j < ((CTXR_EXP & 2) ? 0 : 4); ++j) {
-          uint32_t hk[8], lk[8];
+          uint32_t hk[8];
 #pragma unroll
           for (int e = 0; e < 16; e += 2) {
             const float p0 = ex2(x[j * 16 + e] - mref), p1 = ex2(x[j * 16 + e + 1] - mref);
             l += p0 + p1;
-            hk[e / 2] = pack_bf16x2_trunc(p0, p1);
-            lk[e / 2] = pack_bf16x2_trunc(p0 - bf16lo(hk[e / 2]), p1 - bf16hi(hk[e / 2]));
+            hk[e / 2] = pack_f16x2(p0, p1);
           }
           tc::tmem_st<8>(tS + (u % kS) * 128 + hf * 32 + j * 8 + lane_addr, hk);
-          tc::tmem_st<8>(tS + (u % kS) * 128 + 64 + hf * 32 + j * 8 + lane_addr, lk);
         }
         tc::tmem_st_wait();
         tc::tc_fence_before();
@@ -417,9 +447,9 @@ __global__ void __launch_bounds__(ctxr::kThreads, 1)
         if (valid_row) {
 #pragma unroll
           for (int e = 0; e < 32; e += 4)
-            *reinterpret_cast<float4*>(wo + q * 32 + e) =
-                make_float4(__uint_as_float(o[e]), __uint_as_float(o[e + 1]),
-                            __uint_as_float(o[e + 2]), __uint_as_float(o[e + 3]));
+            *reinterpret_cast<float4*>(wo + q * 32 + e) =  // undo V * 2^-8 (exact)
+                make_float4(__uint_as_float(o[e]) * 256.f, __uint_as_float(o[e + 1]) * 256.f,
+                            __uint_as_float(o[e + 2]) * 256.f, __uint_as_float(o[e + 3]) * 256.f);
         }
       }
       // row sum = both halves' shares, through its own exchange slot (written
