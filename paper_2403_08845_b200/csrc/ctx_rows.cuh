@@ -365,6 +365,17 @@ __global__ void __launch_bounds__(ctxr::kThreads, 1)
       tc::fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(tc::smem_u32(q_full));
+      // L2 prefetch of this thread's half Q row of the NEXT item (its load is
+      // on the item-switch path; the item's tiles take microseconds)
+      if (k + (int)gridDim.x < P.items) {
+        const Item In = item_of(k + gridDim.x);
+        const int rgn = In.rb * 128 + r;
+        const bool vn = In.dec ? r < P.p : rgn < P.R;
+        if (vn) {
+          const int grn = In.dec ? In.i * P.h + In.c * P.p + r : (rgn / P.p) * P.h + In.c * P.p + rgn % P.p;
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const uint4*>(P.q) + (size_t)grn * 16 + 8 * hf));
+        }
+      }
       float m = kNegInf, l = 0.f;  // l: this half's share of the row sum
       pf.mark(0);
       for (int t = t0; t < t1; ++t, ++u) {
@@ -379,12 +390,26 @@ __global__ void __launch_bounds__(ctxr::kThreads, 1)
         // logits in log2 units; positions past mc masked (last tile only)
         const int Lrow = I.dec && P.ntok > 1 ? max(I.L - (P.ntok - 1 - r % P.ntok), 0) : I.L;
         const int nvalid = min(128, Lrow - t * 128) - hf * 64;
-        float mh = kNegInf;
+        // row max over this half's 64 positions: 8 independent chains (a
+        // single running fmax was a 64-deep dependency chain, ~1k cycles/pass)
+        float mq[8];
 #pragma unroll
-        for (int i = 0; i < 64; ++i) {
-          x[i] = i < nvalid ? x[i] * sl2 : kNegInf;
-          mh = fmaxf(mh, x[i]);
+        for (int k = 0; k < 8; ++k) mq[k] = kNegInf;
+        if (nvalid >= 64) {
+#pragma unroll
+          for (int i = 0; i < 64; ++i) {
+            x[i] *= sl2;
+            mq[i & 7] = fmaxf(mq[i & 7], x[i]);
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 64; ++i) {
+            x[i] = i < nvalid ? x[i] * sl2 : kNegInf;
+            mq[i & 7] = fmaxf(mq[i & 7], x[i]);
+          }
         }
+        const float mh = fmaxf(fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3])),
+                               fmaxf(fmaxf(mq[4], mq[5]), fmaxf(mq[6], mq[7])));
         pf.mark(3);
         float* const xs = sm_x + (u & 1) * 256;
         xs[hf * 128 + r] = mh;
@@ -418,17 +443,19 @@ __global__ void __launch_bounds__(ctxr::kThreads, 1)
         const float mref = m == kNegInf ? 0.f : m;  // a row with no valid position yet: P = 0
         // P = 2^(x - m) as ONE f16 operand (reading R23; V is f16 * 2^-8) into
         // TMEM over S: the PV's A operand
+        float lq[4] = {0.f, 0.f, 0.f, 0.f};  // independent partial row sums
 #pragma unroll
         for (int j = 0; j < ((CTXR_EXP & 2) ? 0 : 4); ++j) {
           uint32_t hk[8];
 #pragma unroll
           for (int e = 0; e < 16; e += 2) {
             const float p0 = ex2(x[j * 16 + e] - mref), p1 = ex2(x[j * 16 + e + 1] - mref);
-            l += p0 + p1;
+            lq[(e >> 1) & 3] += p0 + p1;
             hk[e / 2] = pack_f16x2(p0, p1);
           }
           tc::tmem_st<8>(tS + (u % kS) * 128 + hf * 32 + j * 8 + lane_addr, hk);
         }
+        l += (lq[0] + lq[1]) + (lq[2] + lq[3]);
         tc::tmem_st_wait();
         tc::tc_fence_before();
         __syncwarp();
