@@ -14,13 +14,18 @@ import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-TAG2CFG = {"b32": "mha7b_b32", "b16": "mha7b_b16", "gqa": "gqa"}
+TAG2CFG = {"b32": "mha7b_b32", "b16": "mha7b_b16", "gqa": "gqa", "mqa": "mqa", "long": "long",
+           "fp8": "mha7b_b32_fp8"}
 KEYS = ["Duration", "DRAM Throughput", "Memory Throughput", "Compute (SM) Throughput",
         "Executed Ipc Active", "Issue Slots Busy", "L1/TEX Hit Rate", "L2 Hit Rate",
         "No Eligible", "Warp Cycles Per Issued Instruction", "Registers Per Thread",
         "Dynamic Shared Memory Per Block", "Achieved Occupancy"]
 RAW = ["dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum",
-       "smsp__inst_executed.sum", "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum"]
+       "smsp__inst_executed.sum", "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
+       "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
+       "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
+       "sm__inst_executed_pipe_tc.sum", "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
+       "dram__throughput.avg.pct_of_peak_sustained_elapsed"]
 
 
 def ncu_csv(rep, page, extra=()):
@@ -36,7 +41,8 @@ def launches(path):
     agg = {}
     for r in rows[1:]:
         name = r[ix["Kernel Name"]]
-        name = name.split("(")[0][:60] if "bif" in name or "merge" in name or "fma" in name else name[:40]
+        name = (name.split("(")[0][:60] if any(k in name for k in ("bif", "merge", "fma", "ctx_rows"))
+                else name[:40])
         v = float(r[ix["Metric Value"]].replace(",", ""))
         agg.setdefault(name, {}).setdefault(r[ix["Metric Name"]], []).append(v)
     return agg
