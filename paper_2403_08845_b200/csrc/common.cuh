@@ -76,25 +76,6 @@ BA_DEVINL float ex2(float x) {
   return y;
 }
 
-// 2^x on the FMA / integer pipes, to take part of the exponentials off the
-// MUFU pipe where it binds (the rows kernel: 16K exponentials per 128x128
-// pass).  x = i + f with i = round(x) (magic-number add) and f in [-0.5, 0.5];
-// 2^f by a degree-4 polynomial (least-squares on Chebyshev nodes, relative
-// error <= 2.7e-6, far below the f16 rounding of P, 2^-12); 2^i by an exponent
-// add.  Valid for x <= 128; returns 0 for x < -125 (incl. -inf).
-BA_DEVINL float ex2_fma(float x) {
-  const float xc = fmaxf(x, -125.f);
-  const float t = xc + 12582912.f;  // 1.5 * 2^23: round(xc) in the low mantissa bits
-  const float f = xc - (t - 12582912.f);
-  float p = fmaf(0.009560510516f, f, 0.05591703951f);
-  p = fmaf(p, f, 0.2402498126f);
-  p = fmaf(p, f, 0.6931219697f);
-  p = fmaf(p, f, 0.9999991655f);
-  const int i = __float_as_int(t) - 0x4B400000;
-  const float r = __int_as_float(__float_as_int(p) + (i << 23));
-  return x < -125.f ? 0.f : r;
-}
-
 BA_DEVINL float lg2(float x) {
   float y;
   asm("lg2.approx.f32 %0, %1;" : "=f"(y) : "f"(x));

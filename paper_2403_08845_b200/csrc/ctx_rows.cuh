@@ -449,11 +449,9 @@ __global__ void __launch_bounds__(ctxr::kThreads, 1)
           uint32_t hk[8];
 #pragma unroll
           for (int e = 0; e < 16; e += 2) {
-            // 6 of every 16 exponentials on the FMA pipe (ex2_fma), the rest on
-            // MUFU: the pass was MUFU-bound (16K ex2 per 128x128 pass)
-            const float a0 = x[j * 16 + e] - mref, a1 = x[j * 16 + e + 1] - mref;
-            const float p0 = e < 6 ? ex2_fma(a0) : ex2(a0);
-            const float p1 = e < 6 ? ex2_fma(a1) : ex2(a1);
+            // (moving 6 of 16 exponentials to an FMA-pipe polynomial was
+            // measured slower, C4 50.9 -> 56.0 us: the pass is issue-bound)
+            const float p0 = ex2(x[j * 16 + e] - mref), p1 = ex2(x[j * 16 + e + 1] - mref);
             lq[(e >> 1) & 3] += p0 + p1;
             hk[e / 2] = pack_f16x2(p0, p1);
           }

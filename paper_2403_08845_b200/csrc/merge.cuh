@@ -52,8 +52,15 @@ __global__ void __launch_bounds__(256) merge_kernel(const MergeParams P) {
   // slot index of the k-th live partial
   auto slot_of = [&](int k) { return k < nctx ? k : P.dec_slot0 + (k - nctx); };
   const float* ml = P.ws_ml + (size_t)warp * P.S * 2;
+  const float* o = P.ws_o + (size_t)warp * P.S * D;
+  // (m, l) of up to 32 partials per round, one per lane: the row max and the
+  // weights take one load round trip instead of one per partial
   float M = kNegInf;
-  for (int k = lane; k < ntot; k += 32) M = fmaxf(M, ml[2 * slot_of(k)]);
+  for (int k0 = 0; k0 < ntot; k0 += 32) {
+    const int k = k0 + lane;
+    const float mk = k < ntot ? ml[2 * slot_of(k)] : kNegInf;
+    M = fmaxf(M, mk);
+  }
 #pragma unroll
   for (int off = 16; off >= 1; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
   const float Ms = (M == kNegInf) ? 0.f : M;
@@ -61,17 +68,38 @@ __global__ void __launch_bounds__(256) merge_kernel(const MergeParams P) {
 #pragma unroll
   for (int e = 0; e < EPL; ++e) acc[e] = 0.f;
   float L = 0.f;
-  const float* o = P.ws_o + (size_t)warp * P.S * D;
-  for (int k = 0; k < ntot; ++k) {
-    const int s = slot_of(k);
-    const float w = ex2(ml[2 * s] - Ms);
-    L = fmaf(w, ml[2 * s + 1], L);
+  for (int k0 = 0; k0 < ntot; k0 += 32) {
+    const int kl = k0 + lane;
+    float wl = 0.f;
+    if (kl < ntot) {
+      const int s = slot_of(kl);
+      wl = ex2(ml[2 * s] - Ms);
+      L = fmaf(wl, ml[2 * s + 1], L);
+    }
+    const int nk = min(32, ntot - k0);
+    // value rows 4 partials at a time: all loads of a batch before any use
+    for (int kb = 0; kb < nk; kb += 4) {
+      float ov[4][EPL];
+      float wk[4];
 #pragma unroll
-    for (int e = 0; e < EPL; ++e) {
-      const int x = e * 32 + lane;
-      if (x < D) acc[e] = fmaf(w, o[(size_t)s * D + x], acc[e]);
+      for (int q = 0; q < 4; ++q) {
+        wk[q] = __shfl_sync(0xffffffffu, wl, (kb + q) & 31);
+        const int k = k0 + kb + q;
+        const float* os = o + (size_t)slot_of(k < ntot ? k : k0) * D;
+#pragma unroll
+        for (int e = 0; e < EPL; ++e) {
+          const int x = e * 32 + lane;
+          ov[q][e] = (kb + q < nk && x < D) ? __ldcg(os + x) : 0.f;
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int e = 0; e < EPL; ++e) acc[e] = fmaf(kb + q < nk ? wk[q] : 0.f, ov[q][e], acc[e]);
     }
   }
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) L += __shfl_xor_sync(0xffffffffu, L, off);
   const float invL = P.vscale / L;
 #pragma unroll
   for (int e = 0; e < EPL; ++e) {
