@@ -677,6 +677,29 @@ int launch_bif_tc_n(const ba::BifTcParams& bp, int smem, uint32_t flags, LaunchR
   return rec.end();
 }
 
+// The merge launch, programmatically dependent on the partial kernel before it
+// (PDL: it launches while that kernel drains; merge_kernel waits with
+// griddepcontrol.wait before reading the partials).  Already begun with rec.
+template <typename T, int D>
+int launch_merge(const ba::MergeParams& mp, uint32_t flags, LaunchRec& rec) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(cdiv(mp.rows, 8));
+  cfg.blockDim = dim3(256);
+  cfg.stream = rec.st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = (flags & BA_FLAG_NO_PDL) ? 0 : 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, ba::merge_kernel<T, D>, mp);
+  if (e != cudaSuccess) {
+    g_last_cuda_error = (int)e;
+    rec.end();
+    return BA_ECUDA;
+  }
+  return rec.end();
+}
+
 // tcgen05 step: streaming kernel + PDL-chained merge.  Replicated baseline:
 // Kc = Vc = nullptr, Kd/Vd are the replicated caches [b][g][mc+md_cap][d].
 int run_tc(const ba_problem_t* pr, const Plan& P, const void* q, const void* Kc, const void* Vc,
@@ -810,8 +833,7 @@ int run_tc(const ba_problem_t* pr, const Plan& P, const void* q, const void* Kc,
       mp.dec_cap = P.dec_cap;
       mp.vscale = 1.f;
       rec.begin();
-      ba::merge_kernel<__nv_bfloat16, 128><<<cdiv(mp.rows, 8), 256, 0, st>>>(mp);
-      return rec.end();
+      return launch_merge<__nv_bfloat16, 128>(mp, pr->flags, rec);
     }
   }
   // softmax warpgroups (override for experiments: BIFATTN_SWG=1|2)
@@ -922,8 +944,8 @@ int run_plan(const ba_problem_t* pr, const Plan& P, const void* q, const void* K
   mp.vscale = (P.kv8 && pr->v_scale > 0.f) ? pr->v_scale : 1.f;
   const int warps_per_block = 8;
   rec.begin();
-  ba::merge_kernel<T, D><<<cdiv(mp.rows, warps_per_block), 32 * warps_per_block, 0, st>>>(mp);
-  return rec.end();
+  (void)warps_per_block;
+  return launch_merge<T, D>(mp, pr->flags, rec);
 }
 
 template <typename T, typename TK = T>

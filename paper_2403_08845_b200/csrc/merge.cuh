@@ -39,6 +39,8 @@ __global__ void __launch_bounds__(256) merge_kernel(const MergeParams P) {
   constexpr int EPL = (D + 31) / 32;
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
+  pdl_wait();  // launched programmatically dependent on the partial kernel
+  pdl_launch_dependents();
   // append+attend: the partial kernels (earlier launches) have read lens
   if (P.lens_out && blockIdx.x == 0)
     for (int i = threadIdx.x; i < P.b; i += blockDim.x) {
