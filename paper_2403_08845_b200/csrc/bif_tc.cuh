@@ -519,7 +519,9 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
   constexpr int PSWM = W == 64 ? 7 : (W == 32 ? 3 : 1);
   constexpr uint32_t IDESC_QK = KV8 ? tc::idesc_f16(128, N, 0, 0) : tc::idesc_bf16(128, N, 0, 0);
   constexpr uint32_t IDESC_PV = KV8 ? tc::idesc_f16(128, NP, 1, 1) : tc::idesc_bf16(128, NP, 1, 1);
-  constexpr uint32_t TMEM_COLS = tmem_cols(N);
+  // KV8: + the f16 K tiles of the NST stages in TMEM (64 columns each), the
+  // QK MMA's A operand
+  constexpr uint32_t TMEM_COLS = KV8 ? 512 : tmem_cols(N);
   constexpr int QB = 256 * N;  // bytes of one q buffer / one P part
   constexpr int PB = KV8 ? QB : 2 * QB;  // bytes of one P slot
   static_assert(N % 16 == 0 && N >= 16 && N <= 64 && CPT % 8 == 0 && CPT <= 32, "N");
@@ -615,6 +617,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
   const uint32_t tmem = *tmem_holder;
   const uint32_t tS = tmem;          // S^T slots at columns [0,N), [N,2N)
   const uint32_t tO = tmem + 2 * N;  // O^T buffers at [2N,4N), [4N,6N): O_hi | O_lo halves
+  const uint32_t tK = tmem + 4 * N;  // KV8: f16 K tile of stage st at [tK + 64 st, +64)
 
   const Range rg = my_range(P);
   const long long nw = rg.n();
@@ -740,9 +743,13 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
           const uint32_t kbase = tc::smem_u32(sm_stage + st * kStageBytes);
 #pragma unroll
           for (int k = 0; k < 8; ++k) {
-            const uint64_t ad = tc::smem_desc(kbase + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024, tc::kSw128);
             const uint64_t bd = tc::smem_desc(qbase + (k >> 2) * (N * 128) + (k & 3) * 32, 16, 1024, tc::kSw128);
-            tc::mma_bf16(tS + slot * N, ad, bd, IDESC_QK, k > 0 ? 1u : 0u);
+            if constexpr (KV8) {  // A = the f16 K tile in TMEM (8 columns per K step)
+              tc::mma_bf16_ts(tS + slot * N, tK + st * 64 + k * 8, bd, IDESC_QK, k > 0 ? 1u : 0u);
+            } else {
+              const uint64_t ad = tc::smem_desc(kbase + (k >> 2) * 16384 + (k & 3) * 32, 16, 1024, tc::kSw128);
+              tc::mma_bf16(tS + slot * N, ad, bd, IDESC_QK, k > 0 ? 1u : 0u);
+            }
           }
           tc::mma_commit(tc::smem_u32(&s_full[slot]));
           if (BIF_DBG & 1024) tc::mma_commit(tc::smem_u32(&kv_empty[st]));  // experiment: release at QK
@@ -1382,21 +1389,52 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
           const int st = u % NST;
           tc::mbar_wait(tc::smem_u32(&kv_full[st]), (u / NST) & 1);
           uint8_t* const stage = sm_stage + st * kStageBytes;
-          // K (kv = 0) then V (kv = 1): the codes of row R (region + 16 KB +
-          // R*128) expand to f16 row R of both 64-column halves.  Lane: code
-          // chunks c0 and c0 + 4 (-> half 0 and half 1) of row r8 of an 8-row
-          // block; an 8-lane shared-memory phase covers rows k and k + 4, whose
-          // swizzled chunk sets are complementary (conflict-free loads), and
-          // the second row of a phase stores its odd f16 chunk first (the two
-          // rows then hit even and odd chunk sets: conflict-free stores).
-          // Half-1 rows overwrite the code rows they come from: a block's
-          // stores follow a __syncwarp after all its loads (and the next
-          // block's prefetch, which reads other rows).
+          // K: each thread expands the 128 codes of ITS position row (its TMEM
+          // lane, R = 32 cw + lane) into f16 pairs and stores them into the
+          // stage's K slot in TMEM (64 columns, d = 2j, 2j + 1 in column j):
+          // the QK MMA reads A from there, so the f16 K never touches smem.
+          // An 8-lane phase reads 8 consecutive rows' chunks at distinct
+          // swizzled positions: conflict-free.
+          {
+            const int R = 32 * cw + lane;
+            const uint8_t* const krow = stage + 16384 + R * 128;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              uint32_t kv[32];
+#pragma unroll
+              for (int c4 = 0; c4 < 4; ++c4) {
+                const int c = 4 * h + c4;
+                const uint4 v = lds128(krow + ((c ^ (R & 7)) << 4));
+                kv[8 * c4 + 0] = e4m3x2_to_f16x2(v.x);
+                kv[8 * c4 + 1] = e4m3x2_to_f16x2(v.x >> 16);
+                kv[8 * c4 + 2] = e4m3x2_to_f16x2(v.y);
+                kv[8 * c4 + 3] = e4m3x2_to_f16x2(v.y >> 16);
+                kv[8 * c4 + 4] = e4m3x2_to_f16x2(v.z);
+                kv[8 * c4 + 5] = e4m3x2_to_f16x2(v.z >> 16);
+                kv[8 * c4 + 6] = e4m3x2_to_f16x2(v.w);
+                kv[8 * c4 + 7] = e4m3x2_to_f16x2(v.w >> 16);
+              }
+              tc::tmem_st<32>(tK + st * 64 + h * 32 + lane_addr, kv);
+            }
+            tc::tmem_st_wait();
+            tc::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(tc::smem_u32(&k_cvt[st]));
+          }
+          // V: the codes of row R (region + 16 KB + R*128) expand in place to
+          // f16 row R of both 64-column halves.  Lane: code chunks c0 and
+          // c0 + 4 (-> half 0 and half 1) of row r8 of an 8-row block; an 8-lane
+          // shared-memory phase covers rows k and k + 4, whose swizzled chunk
+          // sets are complementary (conflict-free loads), and the second row
+          // of a phase stores its odd f16 chunk first (the two rows then hit
+          // even and odd chunk sets: conflict-free stores).  Half-1 rows
+          // overwrite the code rows they come from: a block's stores follow a
+          // __syncwarp after all its loads (and the next block's prefetch,
+          // which reads other rows).
           const int r8 = ((lane >> 2) & 1) * 4 + (lane >> 3);
           const bool odd_first = (lane >> 2) & 1;
-#pragma unroll
-          for (int kv = 0; kv < 2; ++kv) {
-            uint8_t* const reg = stage + kv * 32768;
+          {
+            uint8_t* const reg = stage + 32768;
             const int c0 = lane & 3;
             auto code_at = [&](int blk, int c) {
               const int R = 32 * cw + 8 * blk + r8;
@@ -1436,7 +1474,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
             }
             tc::fence_proxy_async_smem();
             __syncwarp();
-            if (lane == 0) tc::mbar_arrive(tc::smem_u32(kv == 0 ? &k_cvt[st] : &v_cvt[st]));
+            if (lane == 0) tc::mbar_arrive(tc::smem_u32(&v_cvt[st]));
           }
           if (pending && (j == 1 || j == s.ntiles - 1)) {
             drain(prev, sg - 1);
