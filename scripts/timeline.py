@@ -64,6 +64,9 @@ def run(name):
     ph = {k: [] for k in ("pdl_wait", "to_first_S", "stream", "main_end", "barrier_wait", "merge",
                           "total")}
     sm_gap, sm_busy, vote, p_write, qk_lat = [], [], [], [], []
+    by_kind = {"ctx": {"busy": [], "gap": [], "tile": []}, "dec": {"busy": [], "gap": [], "tile": []}}
+    cs_tab = ba.ba_plan_ctas(prob)
+    Tc_ = cfg.g * (-(-cfg.b * cfg.p // 32)) * (-(-cfg.mc // 128)) if cfg.b * cfg.p < 64 else 0
     abs_t = {"first_S": [], "main_end": [], "barrier_out": [], "merge_done": [], "segments": []}
     for r in tr:
         start, pdl, mend, bout, mdone = (t(r[s]) for s in (250, 254, 251, 252, 253))
@@ -88,6 +91,17 @@ def run(name):
         ph["merge"].append(mdone - bout)
         ph["total"].append(mdone - t0)
         n = min(len(s_ready), len(voted), len(handed))
+        kidx = tr.index(r)
+        kind = None
+        if cs_tab[kidx + 1] <= Tc_:
+            kind = "ctx"
+        elif cs_tab[kidx] >= Tc_:
+            kind = "dec"
+        if kind:
+            for k in range(1, n - 1):
+                by_kind[kind]["busy"].append(handed[k] - s_ready[k])
+                by_kind[kind]["gap"].append(s_ready[k + 1] - handed[k])
+                by_kind[kind]["tile"].append(s_ready[k + 1] - s_ready[k])
         for k in range(n):
             vote.append(voted[k] - s_ready[k])
             p_write.append(handed[k] - voted[k])
@@ -115,6 +129,7 @@ def run(name):
     res = {"config": name, "main_end_fit_us": {"const": coef[0], "per_ctx_tile": coef[1],
                                                "per_dec_tile": coef[2]} if coef else None,
            "per_cta_ctx_dec_mainend": per_cta,
+           "pure_cta_tile_us_median": {k: {q: med(v) for q, v in d.items()} for k, d in by_kind.items()},
            "barrier_atomic_issue_min_med_max": [round(min(before), 2), med(before), round(max(before), 2)] if before else None,
            "barrier_atomic_return_min_med_max": [round(min(after), 2), med(after), round(max(after), 2)] if after else None, "plan": ba.ba_plan_string(prob), "ctas": G,
            "phases_us_median": {k: med(v) for k, v in ph.items()},
