@@ -287,13 +287,10 @@ void ba_set_trace_buffer(void* dev_buf);
  * peak of the run.  Returns BA_OK or a BA_E* code. */
 int ba_stream_read_bench(const void* buf, size_t bytes, void* sink, void* stream);
 
-/* Work split of the tensor-core plan for this problem (bf16, d = 128): range k
- * covers flat tiles [cs[k], cs[k+1]) of [context tiles | decode tiles] (128
- * positions each).  The first `pool` ranges (ba_plan_string "pool=") are the
- * dynamic tail pool that CTAs take from an atomic counter; each later range
- * is one CTA's static range.  Writes min(cap, R + 1) entries to cs (nullable)
- * and returns the number of ranges R, or 0 if the problem takes the CUDA-core
- * plan, or a BA_E* code. */
+/* Work split of the tensor-core plan for this problem (bf16, d = 128): CTA k
+ * streams flat tiles [cs[k], cs[k+1]) of [context tiles | decode tiles]
+ * (128 positions each).  Writes min(cap, G + 1) entries to cs (nullable) and
+ * returns G, or 0 if the problem takes the CUDA-core plan, or a BA_E* code. */
 int ba_plan_ctas(const ba_problem_t* prob, int32_t* cs, int cap);
 
 /* Workload-based switch (PAPER.md FAQ 4 :688-689: "one

@@ -60,7 +60,6 @@
 namespace ba {
 
 constexpr int bif_max_ctas = 160;
-constexpr int bif_max_ranges = 448;  // CTA ranges + the dynamic tail pool
 
 struct BifTcParams {
   CUtensorMap tmKc, tmVc;  // Kc/Vc as 3D (d, mc, g), box (64, 128, 1), SW128
@@ -86,14 +85,11 @@ struct BifTcParams {
   int gpc, ndc;              // groups per decode chunk = N / p; decode chunks per sample
   int qd_rows;               // rows of the decode q box = min(N, h)
   long long Tc, Td;          // context tiles, decode tiles
-  int G, nst;                // G = ranges (npool + CTAs)
+  int G, nst;
   int npb;                   // P buffer slots (1 or 2; each a P_hi, P_lo pair)
   int pf_dist;               // L2 prefetch distance in tiles beyond the one being loaded (0: off)
   int rot;                   // context segments start at tile (blockIdx*rot) mod length (0: in order)
-  int cs[bif_max_ranges + 1];  // range k covers flat tiles [cs[k], cs[k+1]) of [context | decode]
-  int npool;                 // ranges [0, npool): the dynamic tail pool; CTA k starts with range
-                             // npool + k and then takes pool ranges (atomic counter) until empty
-  unsigned* dyn_ctr;         // the pool counter (workspace; reset by CTA 0 after the grid barrier)
+  int cs[bif_max_ctas + 1];  // CTA k streams flat tiles [cs[k], cs[k+1]) of [context | decode]
   float scale_log2;
   float vscale;              // FP8 KV: out = v_scale * o / l (partials in V-code units); else 1
   int S, Sc;                 // slots per row; decode slots start at Sc
@@ -172,18 +168,16 @@ BA_DEVINL int dec_len(const BifTcParams& P, int i) {
   return P.lens_offset + L;
 }
 
-// A range of work: flat tiles [f0, f1) of [context tiles | decode tiles];
-// work index w = f - f0; id = its index in the CTA-range table.
+// This CTA's work: flat tiles [f0, f1) of [context tiles | decode tiles];
+// work index w = f - f0.
 struct Range {
   long long f0, f1;
-  int id;
   BA_DEVINL long long n() const { return f1 - f0; }
 };
-BA_DEVINL Range range_of(const BifTcParams& P, int id) {
+BA_DEVINL Range my_range(const BifTcParams& P) {
   Range r;
-  r.f0 = P.cs[id];
-  r.f1 = P.cs[id + 1];
-  r.id = id;
+  r.f0 = P.cs[blockIdx.x];
+  r.f1 = P.cs[blockIdx.x + 1];
   return r;
 }
 
@@ -246,7 +240,7 @@ BA_DEVINL Seg seg_at(const BifTcParams& P, const Range& rg, long long w) {
     s.t0 = (int)(f - seg * P.ntile_c);
     s.c0 = s.c;
     s.ntiles = (int)(fend - f);
-    s.slot = rg.id - owner(P.cs, P.G, seg * P.ntile_c);
+    s.slot = (int)blockIdx.x - owner(P.cs, P.G, seg * P.ntile_c);
     s.next = w + (fend - f);
   } else if (f < P.Tc) {
     int c, band, rc, tg, wb;
@@ -261,7 +255,7 @@ BA_DEVINL Seg seg_at(const BifTcParams& P, const Range& rg, long long w) {
     s.ntiles = (int)(fend - f);
     // banded: the planner never splits a unit, slot = band; else the CTA's
     // index among the CTAs that share the chunk
-    s.slot = P.nband > 1 ? band : rg.id - owner(P.cs, P.G, u0);
+    s.slot = P.nband > 1 ? band : (int)blockIdx.x - owner(P.cs, P.G, u0);
     s.next = w + (fend - f);
   } else {
     const long long fd = f - P.Tc;
@@ -275,7 +269,7 @@ BA_DEVINL Seg seg_at(const BifTcParams& P, const Range& rg, long long w) {
     const long long a = P.Tc + dec_chunk_begin(P.g, P.gpc, P.ntile_d, s.i, s.cb);
     const long long fend = min(P.Tc + dec_chunk_end(P.g, P.gpc, P.ntile_d, s.i, s.cb), rg.f1);
     s.ntiles = (int)(fend - f);
-    s.slot = P.Sc + rg.id - owner(P.cs, P.G, a);
+    s.slot = P.Sc + (int)blockIdx.x - owner(P.cs, P.G, a);
     s.next = w + (fend - f);
   }
   return s;
@@ -560,8 +554,6 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
   uint64_t* v_cvt = bars + 40;     // [4]  KV8: V of the stage converted to f16
   uint64_t* q_cvt = bars + 44;     // [2]  KV8: q converted to f16
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 48);
-  uint64_t* ring_full = bars + 52;                        // [8] next range id published
-  int* ring_id = reinterpret_cast<int*>(bars + 60);       // [8]
   int* sm_mcnt = reinterpret_cast<int*>(bars + 64);  // [16 warps][2]: merge part counts
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -573,8 +565,8 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
   };
   if (threadIdx.x == 0) tstamp(250, 50);
   const int rows = P.b * P.h;
-  const int r0 = (int)((long long)blockIdx.x * rows / gridDim.x);
-  const int r1 = (int)((long long)(blockIdx.x + 1) * rows / gridDim.x);
+  const int r0 = (int)((long long)blockIdx.x * rows / P.G);
+  const int r1 = (int)((long long)(blockIdx.x + 1) * rows / P.G);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < NST; ++s) {
@@ -587,7 +579,6 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
     }
     if (KV8)
       for (int s = 0; s < 2; ++s) tc::mbar_init(tc::smem_u32(&q_cvt[s]), 4);
-    for (int s = 0; s < 8; ++s) tc::mbar_init(tc::smem_u32(&ring_full[s]), 1);
     for (int s = 0; s < 2; ++s) {
       tc::mbar_init(tc::smem_u32(&q_full[s]), 1);
       tc::mbar_init(tc::smem_u32(&q_empty[s]), 1);
@@ -628,22 +619,11 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
   const uint32_t tO = tmem + 2 * N;  // O^T buffers at [2N,4N), [4N,6N): O_hi | O_lo halves
   const uint32_t tK = tmem + 4 * N;  // KV8: f16 K tile of stage st at [tK + 64 st, +64)
 
-  // this CTA's ranges: its static range first, then pool ranges the producer
-  // takes from the counter; every role walks the same sequence (the producer
-  // publishes each next id through ring_id / ring_full)
-  Range rg = range_of(P, P.npool + (int)blockIdx.x);
-  long long nw = rg.n();
-  auto next_range = [&](uint32_t ri) {  // consumer roles: the id after range ri (-1: done)
-    const uint32_t k = (ri + 1) & 7;
-    tc::mbar_wait(tc::smem_u32(&ring_full[k]), ((ri + 1) >> 3) & 1);
-    return ring_id[k];
-  };
+  const Range rg = my_range(P);
+  const long long nw = rg.n();
 
   if (warp == 0) {
-    Prof pf;
-    uint32_t tt = 0, sg = 0;
-    for (uint32_t ri = 0;; ++ri) {
-    // append+attend: store this step's K/V rows that fall in this range's decode
+    // append+attend: store this step's K/V rows that fall in this CTA's decode
     // tiles before any TMA of them (same CTA: generic stores, then a proxy fence)
     if (P.app.n > 0 && P.Td > 0) {
       for (long long f = max(rg.f0, P.Tc); f < rg.f1; ++f) {
@@ -659,6 +639,8 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
     }
     // ============================ TMA producer ============================
     if (lane == 0) {
+      Prof pf;
+      uint32_t tt = 0, sg = 0;
       const uint64_t pol_c = P.nrc == 1 ? tc::policy_evict_first() : tc::policy_evict_last();
       const uint64_t pol_d = tc::policy_evict_first();
       for (long long w = 0; w < nw; ++sg) {
@@ -732,24 +714,8 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
         }
         w = s.next;
       }
+      pf.dump(P.trace ? P.trace + (size_t)blockIdx.x * kTraceSlots : nullptr, 16);
     }
-    // the next range: a pool range while any is left (one atomic per range)
-    int nid = -1;
-    if (lane == 0) {
-      if (P.npool > 0) {
-        const unsigned v = atomicAdd(P.dyn_ctr, 1u);
-        nid = v < (unsigned)P.npool ? (int)v : -1;
-      }
-      const uint32_t k = (ri + 1) & 7;
-      ring_id[k] = nid;
-      tc::mbar_arrive(tc::smem_u32(&ring_full[k]));
-    }
-    nid = __shfl_sync(0xffffffffu, nid, 0);
-    if (nid < 0) break;
-    rg = range_of(P, nid);
-    nw = rg.n();
-    }
-    if (lane == 0) pf.dump(P.trace ? P.trace + (size_t)blockIdx.x * kTraceSlots : nullptr, 16);
   } else if (warp == 1) {
     // ========================== QK issuer (one lane) ==========================
     // S^T(u) = K_tile(u) . q^T once the tile has landed and the softmax has
@@ -758,7 +724,6 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
       const uint32_t q_addr = tc::smem_u32(sm_q);
       Prof pf;
       uint32_t u = 0, sg = 0;
-      for (uint32_t ri = 0;; ++ri) {
       for (long long w = 0; w < nw; ++sg) {
         const Seg s = seg_at(P, rg, w);
         const uint32_t qbase = q_addr + (sg & 1) * QB;
@@ -795,11 +760,6 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
         tc::mma_commit(tc::smem_u32(&q_empty[sg & 1]));  // q buffer reusable
         w = s.next;
       }
-      const int nid = next_range(ri);
-      if (nid < 0) break;
-      rg = range_of(P, nid);
-      nw = rg.n();
-      }
       pf.dump(P.trace ? P.trace + (size_t)blockIdx.x * kTraceSlots : nullptr, 24);
     }
   } else if (warp == 3) {
@@ -812,7 +772,6 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
       const uint32_t p_addr = tc::smem_u32(sm_p);
       Prof pf;
       uint32_t u = 0, sg = 0;
-      for (uint32_t ri = 0;; ++ri) {
       for (long long w = 0; w < nw; ++sg) {
         const Seg s = seg_at(P, rg, w);
         const uint32_t ob = sg & 1;
@@ -844,11 +803,6 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
         tc::mma_commit(tc::smem_u32(&o_full[ob]));
         w = s.next;
       }
-      const int nid = next_range(ri);
-      if (nid < 0) break;
-      rg = range_of(P, nid);
-      nw = rg.n();
-      }
       pf.dump(P.trace ? P.trace + (size_t)blockIdx.x * kTraceSlots : nullptr, 32);
     }
   } else if (warp >= 4 && warp < EPI0) {
@@ -870,7 +824,6 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
     // valid positions of a segment's sequence; decode lengths are prefetched one
     // segment ahead so no global-load latency sits on a segment boundary
     auto seg_len = [&](const Seg& q) { return q.dec ? dec_len(P, q.i) : P.mc; };
-    for (uint32_t ri = 0;; ++ri) {
     int L = nw > 0 ? seg_len(seg_at(P, rg, 0)) : 0;
     for (long long w = 0; w < nw; ++sg) {
       const Seg s = seg_at(P, rg, w);
@@ -1304,11 +1257,6 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
       w = s.next;
       L = Ln;
     }
-    const int nid = next_range(ri);
-    if (nid < 0) break;
-    rg = range_of(P, nid);
-    nw = rg.n();
-    }
     stamp(7);
     pf.mark(6);
     if (threadIdx.x == 128 || threadIdx.x == 256)
@@ -1405,16 +1353,10 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
     };
     if constexpr (!KV8) {
       uint32_t sg = 0;
-      for (uint32_t ri = 0;; ++ri) {
-        for (long long w = 0; w < nw; ++sg) {
-          const Seg s = seg_at(P, rg, w);
-          drain(s, sg);
-          w = s.next;
-        }
-        const int nid = next_range(ri);
-        if (nid < 0) break;
-        rg = range_of(P, nid);
-        nw = rg.n();
+      for (long long w = 0; w < nw; ++sg) {
+        const Seg s = seg_at(P, rg, w);
+        drain(s, sg);
+        w = s.next;
       }
     } else {
       // ---- KV8: these warps are also the converters.  Per segment: q (bf16
@@ -1427,7 +1369,6 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
       uint32_t u = 0, sg = 0;
       Seg prev;
       bool pending = false;
-      for (uint32_t ri = 0;; ++ri) {
       for (long long w = 0; w < nw; ++sg) {
         const Seg s = seg_at(P, rg, w);
         const uint32_t qbuf = sg & 1;
@@ -1545,11 +1486,6 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
         pending = true;
         w = s.next;
       }
-      const int nid = next_range(ri);
-      if (nid < 0) break;
-      rg = range_of(P, nid);
-      nw = rg.n();
-      }
       if (pending) drain(prev, sg - 1);
     }
   }
@@ -1575,7 +1511,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
     unsigned old;
     asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(P.grid_ctr) : "memory");
     tstamp(248, 48);
-    if (old == gridDim.x - 1u) {
+    if (old == (unsigned)P.G - 1u) {
       asm volatile("st.relaxed.gpu.global.u32 [%0], 0;" ::"l"(P.grid_ctr) : "memory");
       asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(P.grid_ctr + 1) : "memory");
     } else {
@@ -1587,8 +1523,6 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
   }
   __syncthreads();
   if (threadIdx.x == 0) tstamp(252, 52);
-  // every CTA took its last range before the barrier: re-arm the pool counter
-  if (P.npool > 0 && blockIdx.x == 0 && threadIdx.x == 0) *P.dyn_ctr = 0u;
   // append+attend: every CTA has read lens (before the barrier); advance it
   if (P.lens_out && blockIdx.x == 0)
     for (int i = threadIdx.x; i < P.b; i += blockDim.x) P.lens_out[i] = dec_len(P, i) - P.lens_offset;

@@ -130,8 +130,7 @@ struct Plan {
   bool cr_dec = false;
   int cr_items_ctx = 0;
   long long tc_Tc = 0, tc_T = 0;
-  int tc_cs[ba::bif_max_ranges + 1];  // ranges: [0, tc_npool) the dynamic pool, then one per CTA
-  int tc_R = 0, tc_npool = 0;          // ranges in tc_cs; pool ranges
+  int tc_cs[ba::bif_max_ctas + 1];
   size_t off_cnt = 0;
   // FMA context branch
   int nsc = 0, ctx_chunk = 0, rb_c = 1, nrb_c = 0;
@@ -388,8 +387,6 @@ int make_plan(const ba_problem_t* pr_in, int sms, bool replicated, Plan* pl) {
     int sc = 0, sd = 0;
     for (; P.tc_T == 0;) {  // nothing to stream: empty ranges, merge only
       for (int k = 0; k <= P.tc_G; ++k) P.tc_cs[k] = 0;
-      P.tc_R = P.tc_G;
-      P.tc_npool = 0;
       P.tc_bw = 1;
       P.tc_nband = 0;
       break;
@@ -413,53 +410,12 @@ int make_plan(const ba_problem_t* pr_in, int sms, bool replicated, Plan* pl) {
       for (int i = 0; P.tc_ntile_d && i < b; ++i)
         for (int cb = 0; cb < ndc; ++cb)
           ends.push_back(P.tc_Tc + ba::bif::dec_chunk_end(g, gpc, P.tc_ntile_d, i, cb));
-      // Dynamic tail pool (round 2): the first ~12% of the flat tiles are cut
-      // into small units (<= usz tiles, never across a chunk end) that CTAs
-      // take from an atomic counter after their static range, so the CTAs
-      // that stream slowest (DRAM placement, decode-heavy ranges) take fewer;
-      // the rest is split into one static range per CTA by plan_split.  Slot
-      // numbering stays static (a unit is a range with its own partial slot).
-#ifdef BIFATTN_NO_POOL
-      static const double pool_frac = 0.0;  // A/B variant: static ranges only
-#else
-      static const double pool_frac = knob_d("BIFATTN_POOL", 0.12);
-#endif
-      std::vector<int> pc;  // pool unit starts
-      long long Tp = 0;
-      if (!banded && pool_frac > 0 && P.tc_T >= 8LL * P.tc_G) {
-        Tp = (long long)(pool_frac * (double)P.tc_T);
-        const long long usz = std::max(2LL, (Tp + 191) / 192);
-        long long cur = 0;
-        size_t ci = 0;
-        while (cur < Tp) {
-          pc.push_back((int)cur);
-          long long nxt = std::min(cur + usz, Tp);
-          while (ci < ends.size() && ends[ci] <= cur) ++ci;
-          if (ci < ends.size() && ends[ci] < nxt) nxt = ends[ci];
-          cur = nxt;
-        }
-        if ((int)pc.size() + P.tc_G > ba::bif_max_ranges) {
-          pc.clear();
-          Tp = 0;
-        }
-      }
-      P.tc_npool = (int)pc.size();
-      {
-        std::vector<long long> ends2;
-        for (long long e : ends)
-          if (e > Tp) ends2.push_back(e - Tp);
-        std::vector<int> cs2(P.tc_G + 1);
-        plan_split(ends2, P.tc_T - Tp, std::max(0LL, P.tc_Tc - Tp), P.tc_G, cs2.data(), banded,
-                   dec_cost);
-        for (int k = 0; k < P.tc_npool; ++k) P.tc_cs[k] = pc[k];
-        for (int k = 0; k <= P.tc_G; ++k) P.tc_cs[P.tc_npool + k] = cs2[k] + (int)Tp;
-        P.tc_R = P.tc_npool + P.tc_G;
-      }
+      plan_split(ends, P.tc_T, P.tc_Tc, P.tc_G, P.tc_cs, banded, dec_cost);
       sc = sd = 0;
       bool whole = true;
       long long prev = 0;
       for (size_t k = 0; k < ends.size(); ++k) {
-        const int n = ba::bif::parts_of(P.tc_cs, P.tc_R, prev, ends[k]);
+        const int n = ba::bif::parts_of(P.tc_cs, P.tc_G, prev, ends[k]);
         if (prev < P.tc_Tc) {
           whole = whole && n == 1;
           sc = std::max(sc, n);
@@ -699,7 +655,7 @@ int launch_bif_tc_n(const ba::BifTcParams& bp, int smem, uint32_t flags, LaunchR
   // barrier and the LSE merge); programmatic stream serialisation lets its
   // prologue overlap the previous kernel on the stream
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(bp.G - bp.npool);  // one CTA per static range
+  cfg.gridDim = dim3(bp.G);
   cfg.blockDim = dim3(ba::bif::threads(SWG));
   cfg.dynamicSmemBytes = smem;
   cfg.stream = rec.st;
@@ -785,13 +741,12 @@ int run_tc(const ba_problem_t* pr, const Plan& P, const void* q, const void* Kc,
   bp.gpc = P.tc_N / p;
   bp.ndc = (pr->g + bp.gpc - 1) / bp.gpc;
   bp.qd_rows = std::min(P.tc_N, pr->h);
-  bp.Tc = P.tc_Tc; bp.Td = P.tc_T - P.tc_Tc; bp.G = P.tc_R; bp.nst = P.tc_nst; bp.npb = P.tc_npb;
-  bp.npool = P.tc_npool;
+  bp.Tc = P.tc_Tc; bp.Td = P.tc_T - P.tc_Tc; bp.G = P.tc_G; bp.nst = P.tc_nst; bp.npb = P.tc_npb;
   static const int pf_env = knob_i("BIFATTN_PF", 0);  // L2 prefetch distance (tiles; measured slower: off)
   bp.pf_dist = pf_env;
   static const int rot_env = knob_i("BIFATTN_ROT", 0);  // context stream stagger (tiles per CTA index)
   bp.rot = rot_env;
-  memcpy(bp.cs, P.tc_cs, sizeof(int) * (P.tc_R + 1));
+  memcpy(bp.cs, P.tc_cs, sizeof(int) * (P.tc_G + 1));
   bp.ext_ctx = P.ctx_rows ? P.cr_nsplit : 0;
   bp.scale_log2 = scale_log2;
   bp.vscale = (P.kv8 && pr->v_scale > 0.f) ? pr->v_scale : 1.f;
@@ -799,7 +754,6 @@ int run_tc(const ba_problem_t* pr, const Plan& P, const void* q, const void* Kc,
   bp.ws_o = reinterpret_cast<float*>(static_cast<char*>(ws) + P.off_o);
   bp.ws_ml = reinterpret_cast<float*>(static_cast<char*>(ws) + P.off_ml);
   bp.grid_ctr = reinterpret_cast<unsigned*>(static_cast<char*>(ws) + P.off_cnt);
-  bp.dyn_ctr = bp.grid_ctr + 2;  // in the reserved bytes [0, 256)
   bp.out = out;
   bp.lse = lse;
   bp.trace = static_cast<unsigned long long*>(g_trace);
@@ -1321,15 +1275,15 @@ const char* ba_plan_string(const ba_problem_t* prob) {
   else if (P.tc && P.ctx_rows)
     snprintf(g_plan_buf, sizeof g_plan_buf,
              "ctx_rows(blocks=%d,splits=%d,tiles/split=%d,items=%d,ctas=%d) + "
-             "dec_tc(N=%d,dec_tiles=%lld,ctas=%d,pool=%d,stages=%d,slots=%d+%d) launches=2 ws=%zu",
+             "dec_tc(N=%d,dec_tiles=%lld,ctas=%d,stages=%d,slots=%d+%d) launches=2 ws=%zu",
              P.cr_nrb, P.cr_nsplit, P.cr_tps, P.cr_items, P.cr_grid, P.tc_N, P.tc_T, P.tc_G,
-             P.tc_npool, P.tc_nst, P.tc_Sc, P.tc_Sd, P.ws_bytes);
+             P.tc_nst, P.tc_Sc, P.tc_Sd, P.ws_bytes);
   else if (P.tc)
     snprintf(g_plan_buf, sizeof g_plan_buf,
-             "fused_tc(N=%d,nrc=%d,band=%d,ctx_tiles=%lld,dec_tiles=%lld,ctas=%d,pool=%d,stages=%d,"
-             "pbuf=%d,slots=%d+%d,smem=%d) launches=1 ws=%zu",
-             P.tc_N, P.tc_nrc, P.tc_bw, P.tc_Tc, P.tc_T - P.tc_Tc, P.tc_G, P.tc_npool, P.tc_nst,
-             P.tc_npb, P.tc_Sc, P.tc_Sd, P.tc_smem, P.ws_bytes);
+             "fused_tc(N=%d,nrc=%d,band=%d,ctx_tiles=%lld,dec_tiles=%lld,ctas=%d,stages=%d,pbuf=%d,"
+             "slots=%d+%d,smem=%d) launches=1 ws=%zu",
+             P.tc_N, P.tc_nrc, P.tc_bw, P.tc_Tc, P.tc_T - P.tc_Tc, P.tc_G, P.tc_nst, P.tc_npb, P.tc_Sc,
+             P.tc_Sd, P.tc_smem, P.ws_bytes);
   else
     snprintf(g_plan_buf, sizeof g_plan_buf,
              "ctx=fma(nsc=%d,chunk=%d,rb=%d) dec=fma(nsd=%d,chunk=%d,rb=%d) S=%d launches=%d "
@@ -1395,9 +1349,9 @@ int ba_plan_ctas(const ba_problem_t* prob, int32_t* cs, int cap) {
   if (rc) return rc;
   if (!P.tc) return 0;
   if (cs) {
-    for (int k = 0; k <= P.tc_R && k < cap; ++k) cs[k] = P.tc_cs[k];
+    for (int k = 0; k <= P.tc_G && k < cap; ++k) cs[k] = P.tc_cs[k];
   }
-  return P.tc_R;
+  return P.tc_G;
 }
 
 void ba_set_launch_events(void* const* events, int n) {

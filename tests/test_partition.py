@@ -17,7 +17,7 @@ from paper_2403_08845_b200 import _build
 
 def dec_cost(N, nrc, g, mc, ntc, G, T):
     """The planner's decode-tile weight (bifattn_api.cu, make_plan)."""
-    dc = 1.7 if N == 16 else 1.4
+    dc = 1.7 if N == 16 else 1.25
     if nrc > 1 and (2 * g * mc * 128 * 2 <= 64 * 2 ** 20 or 1.5 * ntc * G >= T):
         dc *= 2.4 if nrc >= 32 else 1.6
     return dc
@@ -154,19 +154,10 @@ def test_split_covers_every_tile_once_and_slots_match(shape):
     assert m, plan
     N, sc, sd, loads, banded = model(b, h, g, mc, md, cs, int(m.group(2)))
     assert (int(m.group(1)), int(m.group(3)), int(m.group(4))) == (N, sc, sd)
-    # the first `pool` ranges are the dynamic tail pool (small units, never
-    # across a chunk end); the rest are the static per-CTA ranges
-    npool = int(re.search(r"pool=(\d+)", plan).group(1))
-    ctas = int(re.search(r"ctas=(\d+)", plan).group(1))
-    assert len(cs) - 1 == npool + ctas
-    pool, static = loads[:npool], loads[npool:]
-    if npool:
-        assert max(cs[k + 1] - cs[k] for k in range(npool)) <= max(2, -(-cs[npool] // 192))
-        assert cs[npool] <= 0.13 * cs[-1]
-    mean = sum(static) / len(static)
+    mean = sum(loads) / len(loads)
     # the segment penalty only trims loads; whole banded units (8 tiles) add
     # at most half a unit
-    assert max(static) <= mean + 3 + 0.1 * mean + (4 if banded else 0)
+    assert max(loads) <= mean + 3 + 0.1 * mean + (4 if banded else 0)
 
 
 def test_fma_plan_has_no_cta_table():
