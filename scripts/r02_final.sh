@@ -1,7 +1,8 @@
 # round-2 evidence: default bench line, GPU tests, smoke, sanitizers, ncu launch list of the
-# bench command, ncu full-set captures of the dominant kernels, timelines
+# bench command, ncu full-set captures of the dominant kernels (exported to CSV pages on the
+# box: the reports themselves exceed gpurun's copy-back limit), timelines
 set -x
-mkdir -p gpurun_out/final gpurun_out/san
+mkdir -p gpurun_out/final
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/final/build.txt 2>&1
 timeout -k 10 900 python bench.py > gpurun_out/final/bench.json 2> gpurun_out/final/bench.err
 timeout -k 10 900 python -m pytest tests -m gpu -q -x --timeout 120 -rA > gpurun_out/final/pytest_gpu.txt 2>&1
@@ -15,9 +16,12 @@ timeout -k 10 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram
   python bench.py --steps 5 --warmup 3 --no-e2e --no-replicated --no-cpu-baseline --no-stream-peak --no-others --soak 0 > gpurun_out/final/launches.csv 2>&1
 for c in mha7b_b32:bif_tc:b32 mha7b_b32_fp8:bif_tc:fp8 mqa:ctx_rows:mqa gqa:ctx_rows:gqa long:bif_tc:long; do
   cfg=${c%%:*}; rest=${c#*:}; k=${rest%%:*}; tag=${rest#*:}
-  timeout -k 10 600 ncu --set full --clock-control none --import-source on -k regex:$k --launch-skip 6 --launch-count 1 -o gpurun_out/final/prof_$tag \
+  timeout -k 10 600 ncu --set full --clock-control none --import-source on -k regex:$k --launch-skip 6 --launch-count 1 -o /tmp/prof_$tag \
     python bench.py --config $cfg --steps 3 --warmup 3 --no-e2e --no-replicated --no-cpu-baseline --no-stream-peak --no-others --soak 0 > gpurun_out/final/ncu_$tag.log 2>&1
+  for page in details raw; do ncu -i /tmp/prof_$tag.ncu-rep --page $page --csv > gpurun_out/final/prof_$tag.$page.csv 2>/dev/null; done
+  rm -f /tmp/prof_$tag.ncu-rep
 done
 timeout -k 10 600 python scripts/timeline.py mha7b_b32 mha7b_b32_fp8 mha7b_b16 > gpurun_out/final/timeline.jsonl 2> gpurun_out/final/timeline.err
 timeout -k 10 600 python scripts/role_cycles_rows.py mqa gqa > gpurun_out/final/role_cycles_rows.jsonl 2> gpurun_out/final/role_cycles_rows.err
 MT_CFG=mha7b_b32 timeout -k 10 300 python scripts/bench_multitoken.py > gpurun_out/final/multitoken.jsonl 2> gpurun_out/final/multitoken.err
+du -sh gpurun_out

@@ -29,6 +29,12 @@ RAW = ["dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum"
 
 
 def ncu_csv(rep, page, extra=()):
+    """Rows of one ncu page: from a report (.ncu-rep) or from its exported
+    CSV pages <stem>.<page>.csv (written on the GPU box, where the reports
+    are too large to bring back)."""
+    if not rep.endswith(".ncu-rep"):
+        with open(f"{rep}.{page}.csv") as f:
+            return [r for r in csv.reader(f) if r and not r[0].startswith("==")]
     out = subprocess.run(["ncu", "-i", rep, "--page", page, "--csv", *extra],
                          capture_output=True, text=True, check=True).stdout
     return list(csv.reader(out.splitlines()))
