@@ -97,8 +97,9 @@ def run(name):
             kind = "ctx"
         elif cs_tab[kidx] >= Tc_:
             kind = "dec"
-        if kind:
-            for k in range(1, n - 1):
+        if kind:  # (the narrow decode path stamps no vote: pair S-ready with P-handed)
+            n2 = min(len(s_ready), len(handed))
+            for k in range(1, n2 - 1):
                 by_kind[kind]["busy"].append(handed[k] - s_ready[k])
                 by_kind[kind]["gap"].append(s_ready[k + 1] - handed[k])
                 by_kind[kind]["tile"].append(s_ready[k + 1] - s_ready[k])
