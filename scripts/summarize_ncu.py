@@ -41,7 +41,9 @@ def ncu_csv(rep, page, extra=()):
 
 
 def launches(path):
-    rows = [r for r in csv.reader(open(path)) if len(r) > 10]
+    rows = list(csv.reader(open(path)))
+    start = next(k for k, r in enumerate(rows) if r and r[0] == "ID")
+    rows = [r for r in rows[start:] if len(r) > 10]
     h = rows[0]
     ix = {k: i for i, k in enumerate(h)}
     agg = {}
