@@ -832,7 +832,11 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
       const uint32_t tOb = tO + ob * NP;
       int t = s.t0, cl = s.c0 - s.cb * P.gpc;  // tile index, group within the decode chunk
       const int ntl = s.dec ? P.ntile_d : P.ntile_c;
+#ifdef BIFATTN_NO_NARROW
+      if (false) {  // A/B variant: decode tiles through the general path
+#else
       if (s.dec && P.p <= kNarrowP) {
+#endif
         // ====== narrow decode path: a tile of group c feeds only its p columns ======
         // Half-0 warps (one per TMEM lane quadrant) handle the p valid columns
         // with an exact per-tile max; half-1 warps only keep the barriers.
@@ -897,6 +901,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
           }
           if (h0) tc::named_bar_sync(3, 128);  // the 4 half-0 warps (one per quadrant)
           pf.mark(2);
+          stamp(21);
           if (h0) {
             float pv[kNarrowP], alpha[kNarrowP], tm[kNarrowP];
             bool resc = false;
@@ -946,7 +951,9 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
             }
             // P row of this position (hi and lo parts): zeros except the p valid columns
             pf.mark(3);
+            stamp(27);
             if (!(BIF_DBG & 8)) tc::mbar_wait(tc::smem_u32(&p_empty[ps]), (ph & 1) ^ 1);  // PV(u-npb) done
+            stamp(28);
             uint8_t* const sm_pb = sm_p + ps * PB;
             pf.mark(4);
             const int pc = ps ? pcol1 : pcol0;
@@ -1190,7 +1197,9 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
           // ---- P = 2^x as two bf16 parts (P_hi + P_lo carries ~16 mantissa
           //      bits) into shared memory; fp32 row sums ----
           pf.mark(3);
+          stamp(27);
           if (!(BIF_DBG & 4)) tc::mbar_wait(tc::smem_u32(&p_empty[ps]), (ph & 1) ^ 1);  // PV(u-npb) done
+          stamp(28);
           uint8_t* const sm_pb = sm_p + ps * PB;
           pf.mark(4);
 #pragma unroll

@@ -97,12 +97,18 @@ def run(name):
             kind = "ctx"
         elif cs_tab[kidx] >= Tc_:
             kind = "dec"
-        if kind:  # (the narrow decode path stamps no vote: pair S-ready with P-handed)
-            n2 = min(len(s_ready), len(handed))
+        if kind:
+            pw0 = [x for tag, x in sm if tag == 27]  # before the P-slot wait (PV(u-npb) done)
+            pw1 = [x for tag, x in sm if tag == 28]  # after it
+            n2 = min(len(s_ready), len(handed), len(voted), len(pw0), len(pw1))
             for k in range(1, n2 - 1):
                 by_kind[kind]["busy"].append(handed[k] - s_ready[k])
                 by_kind[kind]["gap"].append(s_ready[k + 1] - handed[k])
                 by_kind[kind]["tile"].append(s_ready[k + 1] - s_ready[k])
+                by_kind[kind].setdefault("to_vote", []).append(voted[k] - s_ready[k])
+                by_kind[kind].setdefault("vote_to_pwait", []).append(pw0[k] - voted[k])
+                by_kind[kind].setdefault("pslot_wait", []).append(pw1[k] - pw0[k])
+                by_kind[kind].setdefault("pwrite_to_handed", []).append(handed[k] - pw1[k])
         for k in range(n):
             vote.append(voted[k] - s_ready[k])
             p_write.append(handed[k] - voted[k])
