@@ -66,7 +66,15 @@ struct BifTcParams {
   CUtensorMap tmQc;        // q as 3D (d, h, b), box (64, p, N/p), SW128
   CUtensorMap tmKd, tmVd;  // Kd/Vd as 3D (d, dec_stride, b*g), box (64, 128, 1)
   CUtensorMap tmQd;        // q as 3D (d, h, b), box (64, min(N, h), 1), SW128
+  CUtensorMap tmQ1;        // dyn: q as 3D (d, h, b), box (64, 1, 1) — one query row
   const int32_t* lens;
+  // dyn = 1: the decode branch is NOT in the static tile ranges; after its
+  // static (context) range every CTA takes decode columns (sample i, group c),
+  // col = i*g + c < ncol = b*g, from the grid-wide counter *col_ctr and its
+  // softmax warps compute them on the CUDA cores (p = 1: one query row per
+  // column — a GEMV, not an MMA tile).  One decode partial per row (slot Sc).
+  int dyn, ncol;
+  unsigned* col_ctr;       // grid_ctr + 2 (reset to 0 by the grid barrier's last arriver)
   int b, h, g, p, mc;
   int dec_cap, lens_offset;  // decode length = lens_offset + clamp(lens[i], 0, dec_cap)
   int lens_add;              // append+attend: lens[i] counts the cache BEFORE this step's n
@@ -309,6 +317,7 @@ __host__ __device__ inline int ctx_parts(const BifTcParams& P, int c, int rc) {
   return parts_of(P.cs, P.G, ff, ff + P.ntile_c);
 }
 __host__ __device__ inline int dec_parts(const BifTcParams& P, int i, int cb) {
+  if (P.dyn) return P.ncol > 0 ? 1 : 0;  // each column is computed whole by one CTA
   if (P.Td == 0) return 0;
   const long long a = P.Tc + dec_chunk_begin(P.g, P.gpc, P.ntile_d, i, cb);
   const long long e = P.Tc + dec_chunk_end(P.g, P.gpc, P.ntile_d, i, cb);
@@ -337,6 +346,18 @@ BA_DEVINL void tmem_ld_cols(uint32_t taddr, uint32_t* r) {
   for (; c + 16 <= CPT; c += 16) tc::tmem_ld<16>(taddr + c, r + c);
 #pragma unroll
   for (; c + 8 <= CPT; c += 8) tc::tmem_ld<8>(taddr + c, r + c);
+}
+
+// two bf16 (lo, hi halves of a word) -> float2 (exact)
+BA_DEVINL float2 bf16x2_f2(uint32_t w) { return make_float2(bf16lo(w), bf16hi(w)); }
+// acc += a * b on both lanes of a pair (one packed FFMA2 on sm_100)
+BA_DEVINL void ffma2(float2& acc, float2 a, float2 b) {
+  unsigned long long A, X, Y;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(A) : "f"(acc.x), "f"(acc.y));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(X) : "f"(a.x), "f"(a.y));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(Y) : "f"(b.x), "f"(b.y));
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(A) : "l"(X), "l"(Y));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(acc.x), "=f"(acc.y) : "l"(A));
 }
 
 BA_DEVINL unsigned long long gtimer() {
@@ -571,7 +592,9 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < NST; ++s) {
       tc::mbar_init(tc::smem_u32(&kv_full[s]), 1);
-      tc::mbar_init(tc::smem_u32(&kv_empty[s]), 1);
+      // released by the PV commit (+ NSW - 1 plain arrivals) after an MMA tile,
+      // by the NSW softmax warps after a CUDA-core decode tile (dyn)
+      tc::mbar_init(tc::smem_u32(&kv_empty[s]), KV8 ? 1 : NSW);
       if (KV8) {
         tc::mbar_init(tc::smem_u32(&k_cvt[s]), 4);
         tc::mbar_init(tc::smem_u32(&v_cvt[s]), 4);
@@ -600,6 +623,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
     tc::prefetch_tmap(&P.tmKd);
     tc::prefetch_tmap(&P.tmVd);
     tc::prefetch_tmap(&P.tmQd);
+    if (P.dyn) tc::prefetch_tmap(&P.tmQ1);
   }
   if (warp == 2) {
     tc::tmem_alloc(tc::smem_u32(tmem_holder), TMEM_COLS);
@@ -638,6 +662,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
       fence_proxy_async_global();
     }
     // ============================ TMA producer ============================
+    uint32_t p_tt = 0, p_sg = 0;  // tiles / segments issued by the static range
     if (lane == 0) {
       Prof pf;
       uint32_t tt = 0, sg = 0;
@@ -715,6 +740,69 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
         w = s.next;
       }
       pf.dump(P.trace ? P.trace + (size_t)blockIdx.x * kTraceSlots : nullptr, 16);
+      p_tt = tt;
+      p_sg = sg;
+    }
+    if constexpr (!KV8 && !MT && NSW == 8) {
+      if (P.dyn) {
+        // ===== dynamic decode columns (whole warp: lane 0 drives the TMA, the
+        // warp stores this step's appended rows) =====
+        uint32_t tt = __shfl_sync(0xffffffffu, p_tt, 0), sg = __shfl_sync(0xffffffffu, p_sg, 0);
+        int2* const ring = reinterpret_cast<int2*>(bars + 56);  // [2] (column, length) per q buffer
+        const uint64_t pol_d = tc::policy_evict_first();
+        const unsigned ncol = (unsigned)P.ncol;
+        // the next column's id and length are fetched one column ahead
+        unsigned nxt = 0;
+        int nxtL = 0;
+        if (lane == 0) {
+          nxt = atomicAdd(P.col_ctr, 1u);
+          if (nxt < ncol) nxtL = dec_len(P, (int)(nxt / (unsigned)P.g));
+        }
+        for (;; ++sg) {
+          const unsigned col = __shfl_sync(0xffffffffu, nxt, 0);
+          const int L = __shfl_sync(0xffffffffu, nxtL, 0);
+          if (lane == 0 && col < ncol) nxt = atomicAdd(P.col_ctr, 1u);
+          const uint32_t qbuf = sg & 1;
+          if (lane == 0) tc::mbar_wait_sleep(tc::smem_u32(&q_empty[qbuf]), ((sg >> 1) & 1) ^ 1);
+          if (col >= ncol) {  // queue drained: tell the softmax warps
+            if (lane == 0) {
+              ring[qbuf] = make_int2(-1, 0);
+              tc::mbar_arrive(tc::smem_u32(&q_full[qbuf]));
+            }
+            break;
+          }
+          const int i = (int)(col / (unsigned)P.g), c = (int)(col - (unsigned)i * (unsigned)P.g);
+          if (P.app.n > 0) {  // append+attend: this column's new rows before its TMA
+            append_rows_warp(P.app, i, c, clamp_len(P.lens, i, P.dec_cap), 0, P.dec_cap, lane);
+            fence_proxy_async_global();
+            __syncwarp();
+            fence_proxy_async_global();
+          }
+          if (lane == 0) {
+            ring[qbuf] = make_int2((int)col, L);
+            const uint32_t qb = tc::smem_u32(&q_full[qbuf]);
+            const uint32_t qdst = tc::smem_u32(sm_q + qbuf * QB);
+            tc::mbar_arrive_expect_tx(qb, 256);
+            tc::tma_load_3d(qdst, &P.tmQ1, qb, 0, c, i);
+            tc::tma_load_3d(qdst + N * 128, &P.tmQ1, qb, 64, c, i);
+            const int z = i * P.g + c;
+            const int nt = (L + kBM - 1) / kBM;
+            for (int t = 0; t < nt; ++t, ++tt) {
+              const int st = tt % NST;
+              tc::mbar_wait_sleep(tc::smem_u32(&kv_empty[st]), ((tt / NST) & 1) ^ 1);
+              const uint32_t bar = tc::smem_u32(&kv_full[st]);
+              tc::mbar_arrive_expect_tx(bar, kStageBytes);
+              const uint32_t dst = tc::smem_u32(sm_stage + st * kStageBytes);
+              tc::tma_load_3d_hint(dst, &P.tmKd, bar, 0, t * kBM, z, pol_d);
+              tc::tma_load_3d_hint(dst + 16384, &P.tmKd, bar, 64, t * kBM, z, pol_d);
+              tc::tma_load_3d_hint(dst + 32768, &P.tmVd, bar, 0, t * kBM, z, pol_d);
+              tc::tma_load_3d_hint(dst + 49152, &P.tmVd, bar, 64, t * kBM, z, pol_d);
+            }
+            if (nxt < ncol) nxtL = dec_len(P, (int)(nxt / (unsigned)P.g));
+          }
+          __syncwarp();
+        }
+      }
     }
   } else if (warp == 1) {
     // ========================== QK issuer (one lane) ==========================
@@ -796,6 +884,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
           }
           tc::mma_commit(tc::smem_u32(&p_empty[ps]));
           if (!(BIF_DBG & 1024)) tc::mma_commit(tc::smem_u32(&kv_empty[st]));
+          if (!KV8) tc::mbar_arrive_cnt(tc::smem_u32(&kv_empty[st]), NSW - 1);
           pf.mark(2);
           if (kStamp && P.trace && u < 256)
             P.trace[(size_t)blockIdx.x * kTraceSlots + 768 + u] = (gtimer() & 0x00ffffffffffffffull) | (32ull << 56);
@@ -1266,6 +1355,140 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
       w = s.next;
       L = Ln;
     }
+    if constexpr (!KV8 && !MT && NSW == 8) {
+      if (P.dyn) {
+        // ====== dynamic decode columns on the CUDA cores (p = 1) ======
+        // Column (i, c): one query row against Kd[i][c] / Vd[i][c], a GEMV.
+        // Warp sw owns tile positions [16 sw, 16 sw + 16): QK with 2 lanes per
+        // position (lane half hf = d half), then PV over the same positions with
+        // lane l holding d = 4l .. 4l + 3.  Each warp keeps its own exact online
+        // softmax (m, l, o) over the column's tiles; at the column's end the
+        // NSW partials are joined through shared memory into ONE partial of row
+        // i*h + c (workspace slot Sc).  fp32 throughout (bf16 products are exact).
+        const int2* const ring = reinterpret_cast<const int2*>(bars + 56);
+        float* const scr_o = reinterpret_cast<float*>(sm_p);  // [2][NSW][128] (the idle P buffer)
+        float* const scr_ml = sm_red;                         // [2][NSW][2]
+        // the last PV of the static range has read the P buffer
+        if (u > 0) tc::mbar_wait(tc::smem_u32(&p_empty[(u - 1) % P.npb]), ((u - 1) / P.npb) & 1);
+        const int hf = lane >> 4;
+        const int pp = 16 * sw + (lane & 15);        // QK: this lane's tile position
+        const int vch = (lane & 15) >> 1;            // PV: 16-byte chunk of d = 4 lane ..
+        const int vsub = (lane & 1) * 8;             //     and the 8-byte half of it
+        const float sl2 = P.scale_log2;
+        int cb = 0;
+        stamp(39);  // static range done
+        for (;; ++sg) {
+          const uint32_t qb = sg & 1;
+          tc::mbar_wait(tc::smem_u32(&q_full[qb]), (sg >> 1) & 1);
+          stamp(40);  // column's q (and id) in shared memory
+          const int col = reinterpret_cast<const volatile int*>(ring + qb)[0];
+          if (col < 0) break;
+          const int Lc = reinterpret_cast<const volatile int*>(ring + qb)[1];
+          // this lane's half of the query row, fp32 (row 0 of the SW128 q box: unswizzled)
+          float qf[64];
+          {
+            const uint8_t* const qrow = sm_q + qb * QB + hf * (N * 128);
+#pragma unroll
+            for (int ch = 0; ch < 8; ++ch) {
+              const uint4 v = *reinterpret_cast<const uint4*>(qrow + ch * 16);
+              qf[8 * ch + 0] = bf16lo(v.x); qf[8 * ch + 1] = bf16hi(v.x);
+              qf[8 * ch + 2] = bf16lo(v.y); qf[8 * ch + 3] = bf16hi(v.y);
+              qf[8 * ch + 4] = bf16lo(v.z); qf[8 * ch + 5] = bf16hi(v.z);
+              qf[8 * ch + 6] = bf16lo(v.w); qf[8 * ch + 7] = bf16hi(v.w);
+            }
+          }
+          float m_w = kNegInf, l_w = 0.f;
+          float2 oa = make_float2(0.f, 0.f), ob2 = make_float2(0.f, 0.f);
+          const int nt = (Lc + kBM - 1) / kBM;
+          for (int t = 0; t < nt; ++t, ++u) {
+            const uint32_t st = u % NST;
+            tc::mbar_wait(tc::smem_u32(&kv_full[st]), (u / NST) & 1);
+            stamp(41);  // tile landed
+            const uint8_t* const stage = sm_stage + st * kStageBytes;
+            // ---- logit of position pp: this lane's 64 products, + the other half ----
+            const uint8_t* const krow = stage + hf * 16384 + pp * 128;
+            float2 a0 = make_float2(0.f, 0.f), a1 = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int ch = 0; ch < 8; ++ch) {
+              const uint4 v = *reinterpret_cast<const uint4*>(krow + ((ch ^ (pp & 7)) << 4));
+              ffma2(a0, bf16x2_f2(v.x), make_float2(qf[8 * ch + 0], qf[8 * ch + 1]));
+              ffma2(a1, bf16x2_f2(v.y), make_float2(qf[8 * ch + 2], qf[8 * ch + 3]));
+              ffma2(a0, bf16x2_f2(v.z), make_float2(qf[8 * ch + 4], qf[8 * ch + 5]));
+              ffma2(a1, bf16x2_f2(v.w), make_float2(qf[8 * ch + 6], qf[8 * ch + 7]));
+            }
+            float sdot = (a0.x + a0.y) + (a1.x + a1.y);
+            sdot += __shfl_xor_sync(0xffffffffu, sdot, 16);
+            const int tpos = t * kBM + pp;
+            const float x = tpos < Lc ? sdot * sl2 : kNegInf;
+            // ---- exact online softmax over this warp's positions ----
+            float mt = x;
+#pragma unroll
+            for (int off = 8; off >= 1; off >>= 1) mt = fmaxf(mt, __shfl_xor_sync(0xffffffffu, mt, off));
+            const float mn = fmaxf(m_w, mt);
+            const float mref = (mn == kNegInf) ? 0.f : mn;
+            const float alpha = ex2(m_w - mref);  // 0 while m_w is unset (l, o are 0)
+            l_w *= alpha;
+            oa.x *= alpha; oa.y *= alpha; ob2.x *= alpha; ob2.y *= alpha;
+            m_w = mn;
+            const float pe = ex2(x - mref);  // 0 at masked positions
+            l_w += hf ? 0.f : pe;
+            // ---- o += p . V over the warp's valid positions (lane: d = 4 lane ..) ----
+            const uint8_t* const vb = stage + 32768 + hf * 16384 + vsub;
+            const int nv = min(max(Lc - (t * kBM + 16 * sw), 0), 16);
+            if (nv == 16) {
+#pragma unroll
+              for (int k = 0; k < 16; ++k) {
+                const float pk = __shfl_sync(0xffffffffu, pe, k);
+                const int r = 16 * sw + k;
+                const uint2 v = *reinterpret_cast<const uint2*>(vb + r * 128 + ((vch ^ (r & 7)) << 4));
+                ffma2(oa, bf16x2_f2(v.x), make_float2(pk, pk));
+                ffma2(ob2, bf16x2_f2(v.y), make_float2(pk, pk));
+              }
+            } else {
+              for (int k = 0; k < nv; ++k) {  // positions past the length are never read
+                const float pk = __shfl_sync(0xffffffffu, pe, k);
+                const int r = 16 * sw + k;
+                const uint2 v = *reinterpret_cast<const uint2*>(vb + r * 128 + ((vch ^ (r & 7)) << 4));
+                ffma2(oa, bf16x2_f2(v.x), make_float2(pk, pk));
+                ffma2(ob2, bf16x2_f2(v.y), make_float2(pk, pk));
+              }
+            }
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(tc::smem_u32(&kv_empty[st]));  // 1 of NSW
+            stamp(42);  // tile done
+          }
+          // ---- join the NSW warp partials of the column: one (m, l, o) ----
+#pragma unroll
+          for (int off = 16; off >= 1; off >>= 1) l_w += __shfl_xor_sync(0xffffffffu, l_w, off);
+          *reinterpret_cast<float4*>(scr_o + (cb * NSW + sw) * kD + 4 * lane) = make_float4(oa.x, oa.y, ob2.x, ob2.y);
+          if (lane == 0) *reinterpret_cast<float2*>(scr_ml + (cb * NSW + sw) * 2) = make_float2(m_w, l_w);
+          tc::named_bar_sync(2, 32 * NSW);
+          if (sw < 4) {
+            const int d = sw * 32 + lane;
+            const float2* const ml = reinterpret_cast<const float2*>(scr_ml + cb * NSW * 2);
+            float M = kNegInf;
+#pragma unroll
+            for (int w2 = 0; w2 < NSW; ++w2) M = fmaxf(M, ml[w2].x);
+            const float Ms = (M == kNegInf) ? 0.f : M;
+            float od = 0.f, ls = 0.f;
+#pragma unroll
+            for (int w2 = 0; w2 < NSW; ++w2) {
+              const float wt = ex2(ml[w2].x - Ms);
+              od = fmaf(wt, scr_o[(cb * NSW + w2) * kD + d], od);
+              ls = fmaf(wt, ml[w2].y, ls);
+            }
+            const int i = col / P.g, c = col - i * P.g;
+            const size_t gr = (size_t)i * P.h + c;  // p = 1
+            P.ws_o[(gr * P.S + P.Sc) * kD + d] = od;
+            if (d == 0) reinterpret_cast<float2*>(P.ws_ml)[gr * P.S + P.Sc] = make_float2(M, ls);
+          }
+          // every warp loaded q before the barrier: the buffer goes back
+          if (sw == 0 && lane == 0) tc::mbar_arrive(tc::smem_u32(&q_empty[qb]));
+          stamp(43);  // column joined and written
+          cb ^= 1;
+        }
+      }
+    }
     stamp(7);
     pf.mark(6);
     if (threadIdx.x == 128 || threadIdx.x == 256)
@@ -1522,6 +1745,8 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
     tstamp(248, 48);
     if (old == (unsigned)P.G - 1u) {
       asm volatile("st.relaxed.gpu.global.u32 [%0], 0;" ::"l"(P.grid_ctr) : "memory");
+      // every CTA has taken its last decode column: the queue starts at 0 next launch
+      if (P.dyn) asm volatile("st.relaxed.gpu.global.u32 [%0], 0;" ::"l"(P.col_ctr) : "memory");
       asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(P.grid_ctr + 1) : "memory");
     } else {
       unsigned g2;

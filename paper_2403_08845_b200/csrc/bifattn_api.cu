@@ -140,6 +140,10 @@ struct Plan {
   int S = 0, dec_slot0 = 0;
   size_t off_o = 0, off_ml = 0, ws_bytes = 0;
   int launches = 0;
+  // decode columns taken dynamically by the fused kernel's CTAs after their
+  // static (context) range and computed on the CUDA cores (p = 1, bf16,
+  // single-token, no FP8): the static table covers the context tiles only
+  bool dyn = false;
   int ntok = 1;  // query tokens per (sample, head) row group (multi-token step)
   bool kv8 = false;  // FP8 E4M3 KV cache (f4)
   int kv_elem = 0;   // bytes per KV element
@@ -338,10 +342,20 @@ int make_plan(const ba_problem_t* pr_in, int sms, bool replicated, Plan* pl) {
     P.tc_ntile_c = (replicated || P.ctx_rows) ? 0 : cdiv(pr->mc, 128);
     P.tc_ntile_d = cdiv(P.lens_offset + P.dec_cap, 128);
     P.tc_Tc = (long long)g * P.tc_nrc * P.tc_ntile_c;
-    P.tc_T = P.tc_Tc + (long long)g * b * P.tc_ntile_d;
+    // p = 1 decode columns (one query row against Kd[i][c]: a GEMV) on the
+    // CUDA cores, taken dynamically after the static context range (round 3:
+    // the narrow tensor-core decode tile cost ~1.6 us against ~1.0 for a
+    // context tile and set the tail; a CUDA-core column tile is well under the
+    // per-SM HBM time of a 64 KB tile)
+#ifdef BIFATTN_NO_DYN
+    P.dyn = false;  // A/B variant build: decode tiles in the static ranges (narrow path)
+#else
+    P.dyn = p == 1 && !P.kv8 && P.ntok == 1 && !P.cr_dec && P.tc_ntile_d > 0;
+#endif
+    P.tc_T = P.tc_Tc + (P.dyn ? 0 : (long long)g * b * P.tc_ntile_d);
     const int gmax = sms < ba::bif_max_ctas ? sms : ba::bif_max_ctas;
     P.tc_G = (int)(P.tc_T < gmax ? P.tc_T : gmax);
-    if (P.tc_T == 0) P.tc_G = gmax;  // no tiles (ctx_rows, md_cap = 0): the merge only
+    if (P.tc_T == 0 || P.dyn) P.tc_G = gmax;  // no tiles (ctx_rows, md_cap = 0): the merge only; dyn: every SM
     // P double-buffered when that keeps the K/V stage count (else one slot)
     P.tc_npb = 2;
     if ((227 * 1024 - ba::bif::smem_fixed(tcN, 2, P.kv8)) / ba::bif::kStageBytes <
@@ -407,10 +421,15 @@ int make_plan(const ba_problem_t* pr_in, int sms, bool replicated, Plan* pl) {
           }
         }
       }
-      for (int i = 0; P.tc_ntile_d && i < b; ++i)
+      for (int i = 0; P.tc_ntile_d && !P.dyn && i < b; ++i)
         for (int cb = 0; cb < ndc; ++cb)
           ends.push_back(P.tc_Tc + ba::bif::dec_chunk_end(g, gpc, P.tc_ntile_d, i, cb));
-      plan_split(ends, P.tc_T, P.tc_Tc, P.tc_G, P.tc_cs, banded, dec_cost);
+      // fewer static tiles than CTAs (dyn, tiny context): one tile per CTA,
+      // the remaining CTAs' static ranges empty (at the END of the table, so
+      // owner() / parts_of() still count only CTAs that write partials)
+      const int Gs = P.tc_T < P.tc_G ? (int)P.tc_T : P.tc_G;
+      plan_split(ends, P.tc_T, P.tc_Tc, Gs, P.tc_cs, banded, dec_cost);
+      for (int k = Gs + 1; k <= P.tc_G; ++k) P.tc_cs[k] = (int)P.tc_T;
       sc = sd = 0;
       bool whole = true;
       long long prev = 0;
@@ -433,6 +452,7 @@ int make_plan(const ba_problem_t* pr_in, int sms, bool replicated, Plan* pl) {
     }
     if (P.ctx_rows) sc = P.cr_nsplit;  // context partials written by ctx_rows_kernel
     if (P.cr_dec) sd = 1;              // one decode partial per row, also from ctx_rows_kernel
+    if (P.dyn) sd = 1;                 // one decode partial per row: a column is one CTA's
     P.tc_Sc = sc;
     P.tc_Sd = sd;
     P.S = sc + sd;
@@ -716,7 +736,7 @@ int run_tc(const ba_problem_t* pr, const Plan& P, const void* q, const void* Kc,
     if (!rc) rc = make_tmap_3d(&bp.tmVc, Vc, d, pr->mc, pr->g, d * ek, (uint64_t)pr->mc * d * ek, 128, 1, P.kv8);
     if (!rc) rc = make_tmap_3d(&bp.tmQc, q, d, pr->h, pr->b, d * 2, (uint64_t)pr->h * d * 2, p, P.tc_N / p);
   }
-  if (!rc && P.tc_T > P.tc_Tc) {
+  if (!rc && (P.tc_T > P.tc_Tc || P.dyn)) {
     const uint64_t ds = (uint64_t)P.dec_stride;
     const uint64_t bg = (uint64_t)pr->b * pr->g;
     rc = make_tmap_3d(&bp.tmKd, Kd, d, ds, bg, d * ek, ds * d * ek, 128, 1, P.kv8);
@@ -724,6 +744,7 @@ int run_tc(const ba_problem_t* pr, const Plan& P, const void* q, const void* Kc,
     if (!rc)
       rc = make_tmap_3d(&bp.tmQd, q, d, pr->h, pr->b, d * 2, (uint64_t)pr->h * d * 2,
                         std::min(P.tc_N, pr->h), 1);
+    if (!rc && P.dyn) rc = make_tmap_3d(&bp.tmQ1, q, d, pr->h, pr->b, d * 2, (uint64_t)pr->h * d * 2, 1, 1);
   }
   if (!rc && P.tc_Tc == 0)  // replicated baseline: q map for the decode chunks
     rc = make_tmap_3d(&bp.tmQc, q, d, pr->h, pr->b, d * 2, (uint64_t)pr->h * d * 2, p, P.tc_N / p);
@@ -754,6 +775,9 @@ int run_tc(const ba_problem_t* pr, const Plan& P, const void* q, const void* Kc,
   bp.ws_o = reinterpret_cast<float*>(static_cast<char*>(ws) + P.off_o);
   bp.ws_ml = reinterpret_cast<float*>(static_cast<char*>(ws) + P.off_ml);
   bp.grid_ctr = reinterpret_cast<unsigned*>(static_cast<char*>(ws) + P.off_cnt);
+  bp.dyn = P.dyn ? 1 : 0;
+  bp.ncol = P.dyn ? pr->b * pr->g : 0;
+  bp.col_ctr = bp.grid_ctr + 2;
   bp.out = out;
   bp.lse = lse;
   bp.trace = static_cast<unsigned long long*>(g_trace);
@@ -838,7 +862,8 @@ int run_tc(const ba_problem_t* pr, const Plan& P, const void* q, const void* Kc,
   }
   // softmax warpgroups (override for experiments: BIFATTN_SWG=1|2)
   static const int swg_env = knob_i("BIFATTN_SWG", 0);
-  const int swg = (swg_env == 1 || swg_env == 2 || (swg_env == 4 && P.tc_N == 32)) ? swg_env : ba::bif::softmax_wgs(P.tc_N);
+  int swg = (swg_env == 1 || swg_env == 2 || (swg_env == 4 && P.tc_N == 32)) ? swg_env : ba::bif::softmax_wgs(P.tc_N);
+  if (P.dyn) swg = 2;  // the CUDA-core decode columns are written for 8 softmax warps
   if (P.kv8) {  // FP8 KV cache (single-token step, N = 16 / 32)
     switch (P.tc_N) {
       case 16: return launch_bif_tc_n<16, 2, false, true>(bp, P.tc_smem, pr->flags, rec);
@@ -1275,14 +1300,17 @@ const char* ba_plan_string(const ba_problem_t* prob) {
   else if (P.tc && P.ctx_rows)
     snprintf(g_plan_buf, sizeof g_plan_buf,
              "ctx_rows(blocks=%d,splits=%d,tiles/split=%d,items=%d,ctas=%d) + "
-             "dec_tc(N=%d,dec_tiles=%lld,ctas=%d,stages=%d,slots=%d+%d) launches=2 ws=%zu",
-             P.cr_nrb, P.cr_nsplit, P.cr_tps, P.cr_items, P.cr_grid, P.tc_N, P.tc_T, P.tc_G,
-             P.tc_nst, P.tc_Sc, P.tc_Sd, P.ws_bytes);
+             "dec_tc(N=%d,dec_tiles=%lld%s,ctas=%d,stages=%d,slots=%d+%d) launches=2 ws=%zu",
+             P.cr_nrb, P.cr_nsplit, P.cr_tps, P.cr_items, P.cr_grid, P.tc_N,
+             P.dyn ? (long long)prob->b * prob->g * P.tc_ntile_d : P.tc_T, P.dyn ? ",dec=cuda_core_dyn" : "",
+             P.tc_G, P.tc_nst, P.tc_Sc, P.tc_Sd, P.ws_bytes);
   else if (P.tc)
     snprintf(g_plan_buf, sizeof g_plan_buf,
-             "fused_tc(N=%d,nrc=%d,band=%d,ctx_tiles=%lld,dec_tiles=%lld,ctas=%d,stages=%d,pbuf=%d,"
+             "fused_tc(N=%d,nrc=%d,band=%d,ctx_tiles=%lld,dec_tiles=%lld%s,ctas=%d,stages=%d,pbuf=%d,"
              "slots=%d+%d,smem=%d) launches=1 ws=%zu",
-             P.tc_N, P.tc_nrc, P.tc_bw, P.tc_Tc, P.tc_T - P.tc_Tc, P.tc_G, P.tc_nst, P.tc_npb, P.tc_Sc,
+             P.tc_N, P.tc_nrc, P.tc_bw, P.tc_Tc,
+             P.dyn ? (long long)prob->b * prob->g * P.tc_ntile_d : P.tc_T - P.tc_Tc,
+             P.dyn ? ",dec=cuda_core_dyn" : "", P.tc_G, P.tc_nst, P.tc_npb, P.tc_Sc,
              P.tc_Sd, P.tc_smem, P.ws_bytes);
   else
     snprintf(g_plan_buf, sizeof g_plan_buf,

@@ -30,6 +30,13 @@ BA_DEVINL void mbar_arrive(uint32_t bar) {
       "{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}" ::"r"(bar)
       : "memory");
 }
+// `count` arrivals at once (a barrier released by one async MMA commit on some
+// phases and by `count + 1` threads on others)
+BA_DEVINL void mbar_arrive_cnt(uint32_t bar, uint32_t count) {
+  asm volatile(
+      "{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0], %1;\n}" ::"r"(bar), "r"(count)
+      : "memory");
+}
 BA_DEVINL void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
   asm volatile(
       "{\n .reg .b64 st;\n mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}" ::"r"(bar),

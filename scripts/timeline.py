@@ -131,6 +131,49 @@ def run(name):
             y.append(t(r[251]) - t0)
     per_cta = [[int(X[k][1]), int(X[k][2]), round(y[k], 2)] for k in range(len(X))]
     coef = np.linalg.lstsq(np.array(X), np.array(y), rcond=None)[0].tolist() if len(X) > 3 else None
+    # dynamic CUDA-core decode columns (tags 39-43 of softmax thread 128)
+    dyn = {"static_end": [], "cols": [], "tile_compute": [], "tile_wait": [], "col_head": [],
+           "col_tail": [], "first_col": [], "last_col_end": []}
+    for r in tr:
+        sm = [(r[k] >> 56, t(r[k])) for k in range(256) if r[k]]
+        se = [x for tag, x in sm if tag == 39]
+        if not se:
+            continue
+        dyn["static_end"].append(se[0] - t0)
+        dyn["cols"].append(sum(1 for tag, _ in sm if tag == 40))
+        prev, prev_tag = None, None
+        for tag, x in sm:
+            if tag == 40 and prev_tag is not None:
+                dyn.setdefault("col_gap", []).append(x - prev)
+            if tag == 41 and prev is not None:
+                (dyn["col_head"] if prev_tag == 40 else dyn["tile_wait"]).append(x - prev)
+            if tag == 42 and prev_tag == 41:
+                dyn["tile_compute"].append(x - prev)
+            if tag == 43 and prev_tag == 42:
+                dyn["col_tail"].append(x - prev)
+            if tag == 40 and not dyn["first_col"] or (tag == 40 and prev_tag == 39):
+                dyn["first_col"].append(x - t0)
+            if tag == 43:
+                last = x
+            if tag in (39, 40, 41, 42, 43):
+                prev, prev_tag = x, tag
+        if any(tag == 43 for tag, _ in sm):
+            dyn["last_col_end"].append(last - t0)
+    dyn_sum = {k: [round(min(v), 3), med(v), round(max(v), 3), len(v)] for k, v in dyn.items() if v}
+    # pipeline start: first TMA issue (producer slot 256), first K landed (QK slot 384),
+    # first QK issued (512), first S ready (softmax tag 20); second/third TMA issue
+    ramp = {"tma0": [], "tma1": [], "tma2": [], "k0_landed": [], "k1_landed": [], "qk0": [], "s0": []}
+    for r in tr:
+        if not r[250]:
+            continue
+        for key, slot in (("tma0", 256), ("tma1", 257), ("tma2", 258), ("k0_landed", 384),
+                          ("k1_landed", 385), ("qk0", 512)):
+            if r[slot]:
+                ramp[key].append(t(r[slot]) - t0)
+        s20 = [t(r[k]) for k in range(256) if r[k] and r[k] >> 56 == 20]
+        if s20:
+            ramp["s0"].append(s20[0] - t0)
+    ramp_sum = {k: [round(min(v), 3), med(v), round(max(v), 3)] for k, v in ramp.items() if v}
     before = [t(r[249]) - t0 for r in tr if r[249]]
     after = [t(r[248]) - t0 for r in tr if r[248]]
     res = {"config": name, "main_end_fit_us": {"const": coef[0], "per_ctx_tile": coef[1],
@@ -146,6 +189,8 @@ def run(name):
                                   "QK_issue_to_S_ready": med(qk_lat)},
            "abs_us_min_med_max": {k: [round(min(v), 2), med(v), round(max(v), 2)] if v else None
                                   for k, v in abs_t.items()},
+           "dyn_min_med_max_n": dyn_sum,
+           "ramp_min_med_max": ramp_sum,
            "tiles_per_cta_median": med([len([1 for k in range(256) if r[k] and r[k] >> 56 == 20])
                                         for r in tr])}
     print(json.dumps(res), flush=True)

@@ -232,11 +232,18 @@ def _long_rows(cfg):
     p = cfg.p
     rows = set()
     for k in range(len(cs) - 1):
+        if cs[k + 1] <= cs[k]:
+            continue  # empty static range (decode columns taken dynamically)
         for f in (cs[k], cs[k + 1] - 1):
             ic = f // ntd
             i, c = divmod(ic, cfg.g)
             if i < cfg.b:
                 rows.add(i * cfg.h + c * p)
+    # dynamic decode columns (any CTA may take any (sample, group)): the first
+    # and last group of every sample
+    for i in range(cfg.b):
+        rows.add(i * cfg.h)
+        rows.add(i * cfg.h + (cfg.g - 1) * p)
     R = cfg.b * p
     for c in range(cfg.g):
         for rb in range((R + 127) // 128):

@@ -44,10 +44,13 @@ def pick_n(b, h, g):
     return fit[0] if fit else cands[-1]
 
 
-def model(b, h, g, mc, md, cs, bw, N=None, with_ctx=True):
+def model(b, h, g, mc, md, cs, bw, N=None, with_ctx=True, dyn=False):
     """Python model of seg_at / ctx_unit / ctx_parts / dec_parts (bif_tc.cuh)
     over the planner's CTA table; bw = the plan's context band width.  With
-    with_ctx=False (the context ran in ctx_rows_kernel) only decode tiles."""
+    with_ctx=False (the context ran in ctx_rows_kernel) only decode tiles.
+    dyn=True: the decode columns are taken dynamically (not in the table; one
+    decode partial per row), and CTAs beyond the static tiles have empty
+    ranges at the end of the table."""
     p = h // g
     N = N or pick_n(b, h, g)
     R = b * p
@@ -55,6 +58,9 @@ def model(b, h, g, mc, md, cs, bw, N=None, with_ctx=True):
     ntc = -(-mc // 128) if with_ctx else 0
     bw = bw if with_ctx else 1
     ntd = -(-md // 128) if md else 0
+    if dyn:
+        sd_dyn = 1 if ntd else 0
+        ntd = 0
     gpc = N // p
     ndc = -(-g // gpc)
     Tc = g * nrc * ntc
@@ -65,6 +71,11 @@ def model(b, h, g, mc, md, cs, bw, N=None, with_ctx=True):
     banded = nband > 1
     assert not banded or nrc > 1
     assert cs[0] == 0 and cs[-1] == T
+    if dyn and T < G:
+        # one static tile per CTA, then empty ranges only at the end
+        assert cs == [min(k, T) for k in range(G + 1)], cs
+        G = T
+        cs = cs[:T + 1]
     assert all(cs[k] < cs[k + 1] for k in range(G)), "empty CTA range"
     # units: (kind, chunk id, slot base, begin, end) in flat order (c, band, rc, tile)
     chunks = []
@@ -109,10 +120,12 @@ def model(b, h, g, mc, md, cs, bw, N=None, with_ctx=True):
             sc = max(sc, parts)
         else:
             sd = max(sd, parts)
+    if dyn:
+        sd = sd_dyn
     # planner cost: decode tiles weigh DEC_COST (bifattn_api.cu, plan_split)
     DEC_COST = dec_cost(N, nrc, g, mc, ntc, G, T)
     loads = [(min(cs[k + 1], Tc) - min(cs[k], Tc)) + DEC_COST * (max(cs[k + 1], Tc) - max(cs[k], Tc))
-             for k in range(G)]
+             for k in range(max(G, 1))] if T else [0]
     return N, sc, sd, loads, banded
 
 
@@ -146,13 +159,17 @@ def test_split_covers_every_tile_once_and_slots_match(shape):
         N = int(m.group(2))
         assert N == min(n for n in (16, 32, 48, 64) if n % (h // g) == 0)
         assert int(m.group(3)) == int(m.group(1))
+        dyn = "cuda_core_dyn" in plan
+        assert dyn == (h == g), plan  # p = 1 decode columns are dynamic
         if md:
-            _, _, sd, _, _ = model(b, h, g, mc, md, cs, 1, N=N, with_ctx=False)
+            _, _, sd, _, _ = model(b, h, g, mc, md, cs, 1, N=N, with_ctx=False, dyn=dyn)
             assert sd == int(m.group(4))
         return
     m = re.search(r"N=(\d+).*band=(\d+).*slots=(\d+)\+(\d+)", plan)
     assert m, plan
-    N, sc, sd, loads, banded = model(b, h, g, mc, md, cs, int(m.group(2)))
+    dyn = "cuda_core_dyn" in plan
+    assert dyn == (h == g and md > 0), plan
+    N, sc, sd, loads, banded = model(b, h, g, mc, md, cs, int(m.group(2)), dyn=dyn)
     assert (int(m.group(1)), int(m.group(3)), int(m.group(4))) == (N, sc, sd)
     mean = sum(loads) / len(loads)
     # the segment penalty only trims loads; whole banded units (8 tiles) add
