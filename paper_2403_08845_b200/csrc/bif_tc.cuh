@@ -98,6 +98,11 @@ struct BifTcParams {
   int pf_dist;               // L2 prefetch distance in tiles beyond the one being loaded (0: off)
   int rot;                   // context segments start at tile (blockIdx*rot) mod length (0: in order)
   int cs[bif_max_ctas + 1];  // CTA k streams flat tiles [cs[k], cs[k+1]) of [context | decode]
+  // workspace slot (index among the CTAs sharing the chunk) of CTA k's FIRST
+  // segment part; every later segment part of a CTA starts a chunk (slot 0).
+  // Planned on the host: a binary search of cs[] in parameter space at the
+  // start costs ~8 dependent constant-cache misses before the first TMA.
+  int slot0[bif_max_ctas];
   float scale_log2;
   float vscale;              // FP8 KV: out = v_scale * o / l (partials in V-code units); else 1
   int S, Sc;                 // slots per row; decode slots start at Sc
@@ -248,7 +253,7 @@ BA_DEVINL Seg seg_at(const BifTcParams& P, const Range& rg, long long w) {
     s.t0 = (int)(f - seg * P.ntile_c);
     s.c0 = s.c;
     s.ntiles = (int)(fend - f);
-    s.slot = (int)blockIdx.x - owner(P.cs, P.G, seg * P.ntile_c);
+    s.slot = w == 0 ? P.slot0[blockIdx.x] : 0;
     s.next = w + (fend - f);
   } else if (f < P.Tc) {
     int c, band, rc, tg, wb;
@@ -263,7 +268,7 @@ BA_DEVINL Seg seg_at(const BifTcParams& P, const Range& rg, long long w) {
     s.ntiles = (int)(fend - f);
     // banded: the planner never splits a unit, slot = band; else the CTA's
     // index among the CTAs that share the chunk
-    s.slot = P.nband > 1 ? band : (int)blockIdx.x - owner(P.cs, P.G, u0);
+    s.slot = P.nband > 1 ? band : (w == 0 ? P.slot0[blockIdx.x] : 0);
     s.next = w + (fend - f);
   } else {
     const long long fd = f - P.Tc;
@@ -274,10 +279,9 @@ BA_DEVINL Seg seg_at(const BifTcParams& P, const Range& rg, long long w) {
     s.cb = s.c0 / P.gpc;
     s.c = s.rc = 0;
     s.t0 = (int)(fd - ic * P.ntile_d);
-    const long long a = P.Tc + dec_chunk_begin(P.g, P.gpc, P.ntile_d, s.i, s.cb);
     const long long fend = min(P.Tc + dec_chunk_end(P.g, P.gpc, P.ntile_d, s.i, s.cb), rg.f1);
     s.ntiles = (int)(fend - f);
-    s.slot = P.Sc + (int)blockIdx.x - owner(P.cs, P.G, a);
+    s.slot = P.Sc + (w == 0 ? P.slot0[blockIdx.x] : 0);
     s.next = w + (fend - f);
   }
   return s;
@@ -633,9 +637,11 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
   __syncthreads();
   tc::tc_fence_after();
   // programmatic dependent launch: the prologue above overlapped the previous
-  // kernel; wait for it before touching any global memory, and let the next
-  // launch start its own prologue
-  pdl_wait();
+  // kernel; wait for it before touching any global memory (the producer warp
+  // first plans its first segment from the parameters while the previous
+  // kernel drains; measured neutral), and let the next launch start its own
+  // prologue
+  if (warp != 0) pdl_wait();
   pdl_launch_dependents();
   if (threadIdx.x == 0) tstamp(254, 54);
   const uint32_t tmem = *tmem_holder;
@@ -647,6 +653,12 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
   const long long nw = rg.n();
 
   if (warp == 0) {
+    // parameter-only planning of the first segment, before the PDL wait
+    Seg s_first;
+    if (lane == 0 && nw > 0) s_first = seg_at(P, rg, 0);
+    const uint64_t pol_c = P.nrc == 1 ? tc::policy_evict_first() : tc::policy_evict_last();
+    const uint64_t pol_d = tc::policy_evict_first();
+    pdl_wait();
     // append+attend: store this step's K/V rows that fall in this CTA's decode
     // tiles before any TMA of them (same CTA: generic stores, then a proxy fence)
     if (P.app.n > 0 && P.Td > 0) {
@@ -666,10 +678,10 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
     if (lane == 0) {
       Prof pf;
       uint32_t tt = 0, sg = 0;
-      const uint64_t pol_c = P.nrc == 1 ? tc::policy_evict_first() : tc::policy_evict_last();
-      const uint64_t pol_d = tc::policy_evict_first();
+      tstamp(240, 60);
       for (long long w = 0; w < nw; ++sg) {
-        const Seg s = seg_at(P, rg, w);
+        const Seg s = w == 0 ? s_first : seg_at(P, rg, w);
+        if (sg == 0) tstamp(241, 61);
         const uint32_t qbuf = sg & 1;
         if (BIF_DBG & 16384) tc::mbar_wait_sleep(tc::smem_u32(&q_empty[qbuf]), ((sg >> 1) & 1) ^ 1, BIF_DBG & 262144); else tc::mbar_wait(tc::smem_u32(&q_empty[qbuf]), ((sg >> 1) & 1) ^ 1);
         pf.mark(0);
@@ -685,6 +697,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
           tc::tma_load_3d(qdst + N * 128, &P.tmQd, qb, 64, s.cb * P.gpc * P.p, s.i);
         }
         pf.mark(1);
+        if (sg == 0) tstamp(242, 62);
         const CUtensorMap* mk = s.dec ? &P.tmKd : &P.tmKc;
         const CUtensorMap* mv = s.dec ? &P.tmVd : &P.tmVc;
         const uint64_t pol = s.dec ? pol_d : pol_c;
@@ -749,7 +762,6 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
         // warp stores this step's appended rows) =====
         uint32_t tt = __shfl_sync(0xffffffffu, p_tt, 0), sg = __shfl_sync(0xffffffffu, p_sg, 0);
         int2* const ring = reinterpret_cast<int2*>(bars + 56);  // [2] (column, length) per q buffer
-        const uint64_t pol_d = tc::policy_evict_first();
         const unsigned ncol = (unsigned)P.ncol;
         // the next column's id and length are fetched one column ahead
         unsigned nxt = 0;

@@ -131,6 +131,7 @@ struct Plan {
   int cr_items_ctx = 0;
   long long tc_Tc = 0, tc_T = 0;
   int tc_cs[ba::bif_max_ctas + 1];
+  int tc_slot0[ba::bif_max_ctas];  // slot of each CTA's first segment part (bif_tc.cuh)
   size_t off_cnt = 0;
   // FMA context branch
   int nsc = 0, ctx_chunk = 0, rb_c = 1, nrb_c = 0;
@@ -450,6 +451,24 @@ int make_plan(const ba_problem_t* pr_in, int sms, bool replicated, Plan* pl) {
       }
       bw_try = P.tc_ntile_c;  // a unit got split (tiny problem): plain order
     }
+    // slot of each CTA's first segment part: its index among the CTAs sharing
+    // the chunk that holds its first tile (banded context: the band, set in-kernel)
+    for (int k = 0; k < P.tc_G; ++k) {
+      const long long f = P.tc_cs[k];
+      long long a = 0;
+      if (f >= P.tc_T || P.tc_cs[k + 1] <= f) {
+        P.tc_slot0[k] = 0;  // empty range
+        continue;
+      }
+      if (f < P.tc_Tc) {
+        a = (f / P.tc_ntile_c) * P.tc_ntile_c;
+      } else {
+        const long long ic = (f - P.tc_Tc) / P.tc_ntile_d;
+        const int i = (int)(ic / g), cb = (int)(ic % g) / gpc;
+        a = P.tc_Tc + ba::bif::dec_chunk_begin(g, gpc, P.tc_ntile_d, i, cb);
+      }
+      P.tc_slot0[k] = k - ba::bif::owner(P.tc_cs, P.tc_G, a);
+    }
     if (P.ctx_rows) sc = P.cr_nsplit;  // context partials written by ctx_rows_kernel
     if (P.cr_dec) sd = 1;              // one decode partial per row, also from ctx_rows_kernel
     if (P.dyn) sd = 1;                 // one decode partial per row: a column is one CTA's
@@ -768,6 +787,7 @@ int run_tc(const ba_problem_t* pr, const Plan& P, const void* q, const void* Kc,
   static const int rot_env = knob_i("BIFATTN_ROT", 0);  // context stream stagger (tiles per CTA index)
   bp.rot = rot_env;
   memcpy(bp.cs, P.tc_cs, sizeof(int) * (P.tc_G + 1));
+  memcpy(bp.slot0, P.tc_slot0, sizeof(int) * P.tc_G);
   bp.ext_ctx = P.ctx_rows ? P.cr_nsplit : 0;
   bp.scale_log2 = scale_log2;
   bp.vscale = (P.kv8 && pr->v_scale > 0.f) ? pr->v_scale : 1.f;

@@ -15,6 +15,7 @@ from tests.parity import compare, oracle_kv8_all_rows, oracle_rows  # noqa: E402
 DEV = "cuda:0"
 CASES = {
     "fused_tc": (Config("s1", "bf16", b=24, h=8, g=4, d=128, mc=700, md=45), 0, 1),
+    "fused_dyn": (Config("s9", "bf16", b=16, h=4, g=4, d=128, mc=700, md=300), 0, 1),
     "rows_merge": (Config("s2", "bf16", b=66, h=8, g=4, d=128, mc=600, md=40), 0, 1),
     "rows_dec_tc": (Config("s3", "bf16", b=64, h=8, g=8, d=128, mc=130, md=1152), 0, 1),
     "fma_fp32": (Config("s4", "fp32", b=4, h=2, g=2, d=16, mc=32, md=4), 0, 1),

@@ -162,11 +162,13 @@ def run(name):
     dyn_sum = {k: [round(min(v), 3), med(v), round(max(v), 3), len(v)] for k, v in dyn.items() if v}
     # pipeline start: first TMA issue (producer slot 256), first K landed (QK slot 384),
     # first QK issued (512), first S ready (softmax tag 20); second/third TMA issue
-    ramp = {"tma0": [], "tma1": [], "tma2": [], "k0_landed": [], "k1_landed": [], "qk0": [], "s0": []}
+    ramp = {"p_range": [], "p_seg0": [], "p_q_issued": [], "pdl": [], "tma0": [], "tma1": [], "tma2": [],
+            "k0_landed": [], "k1_landed": [], "qk0": [], "s0": []}
     for r in tr:
         if not r[250]:
             continue
-        for key, slot in (("tma0", 256), ("tma1", 257), ("tma2", 258), ("k0_landed", 384),
+        for key, slot in (("p_range", 240), ("p_seg0", 241), ("p_q_issued", 242), ("pdl", 254),
+                          ("tma0", 256), ("tma1", 257), ("tma2", 258), ("k0_landed", 384),
                           ("k1_landed", 385), ("qk0", 512)):
             if r[slot]:
                 ramp[key].append(t(r[slot]) - t0)

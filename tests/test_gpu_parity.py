@@ -320,6 +320,36 @@ def test_fma_and_tc_plans_share_one_workspace():
         compare(o4, None, ref4, None, cfg.torch_dtype, "tc-on-shared-ws")
 
 
+def test_two_fused_plans_share_one_workspace():
+    """Two fused tensor-core plans with different row counts (n = 1: 64 rows,
+    dynamic CUDA-core decode columns; n = 2: 128 rows, multi-token kernel)
+    alternate on one workspace (the grid-barrier words and the column queue
+    are left at 0 by every completed call)."""
+    cfg = Config("alt", "bf16", b=16, h=4, g=4, d=128, mc=900, md=70)
+    one = make_inputs(cfg, 41, device=DEV)
+    two = make_inputs(cfg, 42, device=DEV, n_tok=2)
+    p1 = ba.make_problem(cfg.b, cfg.h, cfg.g, cfg.d, cfg.mc, cfg.md, cfg.torch_dtype, n_tok=1)
+    p2 = ba.make_problem(cfg.b, cfg.h, cfg.g, cfg.d, cfg.mc, cfg.md, cfg.torch_dtype, n_tok=2)
+    assert "fused_tc" in ba.ba_plan_string(p1) and "fused_tc" in ba.ba_plan_string(p2)
+    ws = torch.zeros(max(ba.ba_workspace_bytes(p1), ba.ba_workspace_bytes(p2)), dtype=torch.uint8,
+                     device=DEV)
+    ref1, _ = oracle_rows(one)
+    ref2, _ = oracle_rows(type(two)(*(t.cpu() if torch.is_tensor(t) else t for t in
+                                      (two.q, two.Kc, two.Vc, two.Kd, two.Vd, two.lens,
+                                       two.scale))))
+    for _ in range(3):
+        o1 = ba.bifurcated_attn_decode(one.q, one.Kc, one.Vc, one.Kd, one.Vd, one.lens,
+                                       scale=one.scale, workspace=ws)
+        o1b = ba.bifurcated_attn_decode(one.q, one.Kc, one.Vc, one.Kd, one.Vd, one.lens,
+                                        scale=one.scale, workspace=ws)
+        o2 = ba.bifurcated_attn_decode(two.q, two.Kc, two.Vc, two.Kd, two.Vd, two.lens,
+                                       scale=two.scale, workspace=ws)
+        torch.cuda.synchronize()
+        compare(o1, None, ref1, None, cfg.torch_dtype, "plan1-on-shared-ws")
+        compare(o1b, None, ref1, None, cfg.torch_dtype, "plan1-again")
+        compare(o2, None, ref2, None, cfg.torch_dtype, "plan2-on-shared-ws")
+
+
 def test_binding_rejects_mismatched_shapes():
     cfg = Config("x", "bf16", b=3, h=4, g=2, d=128, mc=64, md=8)
     inp = make_inputs(cfg, 16, device=DEV)
