@@ -66,14 +66,19 @@ struct BifTcParams {
   CUtensorMap tmQc;        // q as 3D (d, h, b), box (64, p, N/p), SW128
   CUtensorMap tmKd, tmVd;  // Kd/Vd as 3D (d, dec_stride, b*g), box (64, 128, 1)
   CUtensorMap tmQd;        // q as 3D (d, h, b), box (64, min(N, h), 1), SW128
-  CUtensorMap tmQ1;        // dyn: q as 3D (d, h, b), box (64, 1, 1) — one query row
+  CUtensorMap tmQ1;        // dyn: q as 3D (d, h, b), box (64, p, 1) — the p query rows of a column
   const int32_t* lens;
   // dyn = 1: the decode branch is NOT in the static tile ranges; after its
   // static (context) range every CTA takes decode columns (sample i, group c),
   // col = i*g + c < ncol = b*g, from the grid-wide counter *col_ctr and its
-  // softmax warps compute them on the CUDA cores (p = 1: one query row per
+  // softmax warps compute them on the CUDA cores (p = 1, 2 or 4 query rows per
   // column — a GEMV, not an MMA tile).  One decode partial per row (slot Sc).
   int dyn, ncol;
+  // a column's tiles are cut into dparts parts of dunit tiles (the queue hands
+  // out (column, part) units, unit = col * dparts + part; part k writes decode
+  // slot Sc + k, an empty partial when it starts past the column's length):
+  // enough units to balance the CTAs when columns are few or long
+  int dparts, dunit;
   unsigned* col_ctr;       // grid_ctr + 2 (reset to 0 by the grid barrier's last arriver)
   int b, h, g, p, mc;
   int dec_cap, lens_offset;  // decode length = lens_offset + clamp(lens[i], 0, dec_cap)
@@ -321,7 +326,7 @@ __host__ __device__ inline int ctx_parts(const BifTcParams& P, int c, int rc) {
   return parts_of(P.cs, P.G, ff, ff + P.ntile_c);
 }
 __host__ __device__ inline int dec_parts(const BifTcParams& P, int i, int cb) {
-  if (P.dyn) return P.ncol > 0 ? 1 : 0;  // each column is computed whole by one CTA
+  if (P.dyn) return P.ncol > 0 ? P.dparts : 0;  // one partial per (column, part) unit
   if (P.Td == 0) return 0;
   const long long a = P.Tc + dec_chunk_begin(P.g, P.gpc, P.ntile_d, i, cb);
   const long long e = P.Tc + dec_chunk_end(P.g, P.gpc, P.ntile_d, i, cb);
@@ -362,6 +367,185 @@ BA_DEVINL void ffma2(float2& acc, float2 a, float2 b) {
   asm("mov.b64 %0, {%1, %2};" : "=l"(Y) : "f"(b.x), "f"(b.y));
   asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(A) : "l"(X), "l"(Y));
   asm("mov.b64 {%0, %1}, %2;" : "=f"(acc.x), "=f"(acc.y) : "l"(A));
+}
+
+// ---------------------------------------------------------------------------
+// Dynamic decode columns with PQ = p = 2 or 4 query rows (GQA), CUDA cores.
+// Same division of a tile as the p = 1 path (warp sw: positions 16 sw ..
+// 16 sw + 15; QK with 2 lanes per position, PV with lane l on d = 4l .. 4l+3),
+// but the PQ query rows are read from shared memory as fp32 (converted from
+// the column's bf16 q box once per column: broadcast reads, the two d halves
+// 16 B apart in bank) and each position's PQ probabilities go through a
+// per-warp shared-memory row to the PV lanes.  Per warp and row an exact
+// online softmax; at the column's end warps 0..PQ-1 join the NSW partials of
+// rows c*p .. c*p + PQ - 1 of sample i (workspace slot Sc).
+// ---------------------------------------------------------------------------
+namespace bif {
+constexpr int kQHalf = 68;  // floats per (row, d half) of the fp32 q: 64 + 16 B of bank padding
+__host__ __device__ constexpr int cc_extra_bytes(int pq) {
+  return pq > 1 ? (2 * pq * kQHalf * 4 + 8 * 16 * pq * 4 + 127) / 128 * 128 : 0;
+}
+}  // namespace bif
+
+struct DynSmem {
+  uint8_t* stage;        // NST x 64 KB K/V stages
+  const uint8_t* q;      // 2 bf16 q buffers of QB bytes (d halves at +0 and +Nq*128)
+  int QB, Nq, nst;
+  uint64_t *kv_full, *kv_empty, *q_full, *q_empty;
+  const int2* ring;      // (column, length) per q buffer
+  float* scr_o;          // [NSW][PQ][128] warp partials (the idle P buffer)
+  float* scr_ml;         // [NSW][PQ][2]
+  float* qf;             // [PQ][2][kQHalf] fp32 query rows
+  float* pex;            // [NSW][16][PQ] probabilities of the warp's positions
+};
+
+template <int PQ, int NSW>
+BA_DEVINL void dyn_cc_multi(const BifTcParams& P, const DynSmem& S, int sw, int lane, uint32_t& u,
+                            uint32_t& sg) {
+  constexpr int kD = bif::kD, kBM = bif::kBM;
+  const int hf = lane >> 4;
+  const int pp = 16 * sw + (lane & 15);
+  const int vch = (lane & 15) >> 1, vsub = (lane & 1) * 8;
+  const float sl2 = P.scale_log2;
+  const int tid = sw * 32 + lane;  // 0 .. 32 NSW - 1
+  for (;; ++sg) {
+    const uint32_t qb = sg & 1;
+    tc::mbar_wait(tc::smem_u32(&S.q_full[qb]), (sg >> 1) & 1);
+    const int unit = reinterpret_cast<const volatile int*>(S.ring + qb)[0];
+    if (unit < 0) break;
+    const int Lc = reinterpret_cast<const volatile int*>(S.ring + qb)[1];
+    const int col = unit / P.dparts, part = unit - col * P.dparts;
+    const int t0 = part * P.dunit;
+    // q rows (bf16, SW128 box rows) -> fp32 [r][half][kQHalf]: one 16-byte chunk per thread
+    if (tid < PQ * 16) {
+      const int r = tid >> 4, h2 = (tid >> 3) & 1, ch = tid & 7;
+      const uint4 v = *reinterpret_cast<const uint4*>(S.q + qb * S.QB + h2 * (S.Nq * 128) + r * 128 +
+                                                      ((ch ^ (r & 7)) << 4));
+      float* const dst = S.qf + (r * 2 + h2) * bif::kQHalf + ch * 8;
+      *reinterpret_cast<float4*>(dst) = make_float4(bf16lo(v.x), bf16hi(v.x), bf16lo(v.y), bf16hi(v.y));
+      *reinterpret_cast<float4*>(dst + 4) = make_float4(bf16lo(v.z), bf16hi(v.z), bf16lo(v.w), bf16hi(v.w));
+    }
+    // (also orders the previous column's joins before this column's partial writes)
+    tc::named_bar_sync(2, 32 * NSW);
+    if (tid == 0) tc::mbar_arrive(tc::smem_u32(&S.q_empty[qb]));  // bf16 q no longer read
+    float m_w[PQ], l_w[PQ];
+    float4 o[PQ];
+#pragma unroll
+    for (int r = 0; r < PQ; ++r) {
+      m_w[r] = kNegInf;
+      l_w[r] = 0.f;
+      o[r] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    float* const pw = S.pex + sw * 16 * PQ;
+    const int nt = min((Lc + kBM - 1) / kBM, t0 + P.dunit);
+    for (int t = t0; t < nt; ++t, ++u) {
+      const uint32_t st = u % S.nst;
+      tc::mbar_wait(tc::smem_u32(&S.kv_full[st]), (u / S.nst) & 1);
+      const uint8_t* const stage = S.stage + st * bif::kStageBytes;
+      // ---- PQ logits of position pp (this lane's d half, then the other) ----
+      const uint8_t* const krow = stage + hf * 16384 + pp * 128;
+      float2 a[PQ];
+#pragma unroll
+      for (int r = 0; r < PQ; ++r) a[r] = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int ch = 0; ch < 8; ++ch) {
+        const uint4 kv = *reinterpret_cast<const uint4*>(krow + ((ch ^ (pp & 7)) << 4));
+        const float2 k0 = bf16x2_f2(kv.x), k1 = bf16x2_f2(kv.y), k2 = bf16x2_f2(kv.z), k3 = bf16x2_f2(kv.w);
+#pragma unroll
+        for (int r = 0; r < PQ; ++r) {
+          const float* const qr = S.qf + (r * 2 + hf) * bif::kQHalf + ch * 8;
+          const float4 qa = *reinterpret_cast<const float4*>(qr);
+          const float4 qc = *reinterpret_cast<const float4*>(qr + 4);
+          ffma2(a[r], k0, make_float2(qa.x, qa.y));
+          ffma2(a[r], k1, make_float2(qa.z, qa.w));
+          ffma2(a[r], k2, make_float2(qc.x, qc.y));
+          ffma2(a[r], k3, make_float2(qc.z, qc.w));
+        }
+      }
+      const bool valid = t * kBM + pp < Lc;
+      float pe[PQ];
+#pragma unroll
+      for (int r = 0; r < PQ; ++r) {
+        float sdot = a[r].x + a[r].y;
+        sdot += __shfl_xor_sync(0xffffffffu, sdot, 16);
+        const float x = valid ? sdot * sl2 : kNegInf;
+        float mt = x;
+#pragma unroll
+        for (int off = 8; off >= 1; off >>= 1) mt = fmaxf(mt, __shfl_xor_sync(0xffffffffu, mt, off));
+        const float mn = fmaxf(m_w[r], mt);
+        const float mref = (mn == kNegInf) ? 0.f : mn;
+        const float alpha = ex2(m_w[r] - mref);
+        l_w[r] *= alpha;
+        o[r].x *= alpha; o[r].y *= alpha; o[r].z *= alpha; o[r].w *= alpha;
+        m_w[r] = mn;
+        pe[r] = ex2(x - mref);
+        l_w[r] += hf ? 0.f : pe[r];
+      }
+      // this warp's probabilities [position][row] for the PV lanes
+      if (hf == 0) {
+        if constexpr (PQ == 4)
+          *reinterpret_cast<float4*>(pw + (lane & 15) * 4) = make_float4(pe[0], pe[1], pe[2], pe[3]);
+        else
+          *reinterpret_cast<float2*>(pw + (lane & 15) * 2) = make_float2(pe[0], pe[1]);
+      }
+      __syncwarp();
+      // ---- o[r] += p[r] . V over the warp's valid positions (lane: d = 4 lane ..) ----
+      const uint8_t* const vb = stage + 32768 + hf * 16384 + vsub;
+      const int nv = min(max(Lc - (t * kBM + 16 * sw), 0), 16);
+      for (int k = 0; k < nv; ++k) {
+        const int rr = 16 * sw + k;
+        const uint2 v = *reinterpret_cast<const uint2*>(vb + rr * 128 + ((vch ^ (rr & 7)) << 4));
+        const float2 v0 = bf16x2_f2(v.x), v1 = bf16x2_f2(v.y);
+        float pk[PQ];
+        if constexpr (PQ == 4) {
+          const float4 p4 = *reinterpret_cast<const float4*>(pw + k * 4);
+          pk[0] = p4.x; pk[1] = p4.y; pk[2] = p4.z; pk[3] = p4.w;
+        } else {
+          const float2 p2 = *reinterpret_cast<const float2*>(pw + k * 2);
+          pk[0] = p2.x; pk[1] = p2.y;
+        }
+#pragma unroll
+        for (int r = 0; r < PQ; ++r) {
+          float2 lo = make_float2(o[r].x, o[r].y), hi = make_float2(o[r].z, o[r].w);
+          ffma2(lo, v0, make_float2(pk[r], pk[r]));
+          ffma2(hi, v1, make_float2(pk[r], pk[r]));
+          o[r] = make_float4(lo.x, lo.y, hi.x, hi.y);
+        }
+      }
+      __syncwarp();  // every lane's stage and pex reads are done
+      if (lane == 0) tc::mbar_arrive(tc::smem_u32(&S.kv_empty[st]));  // 1 of NSW
+    }
+    // ---- join the NSW warp partials of each of the PQ rows ----
+#pragma unroll
+    for (int r = 0; r < PQ; ++r) {
+#pragma unroll
+      for (int off = 16; off >= 1; off >>= 1) l_w[r] += __shfl_xor_sync(0xffffffffu, l_w[r], off);
+      *reinterpret_cast<float4*>(S.scr_o + (sw * PQ + r) * kD + 4 * lane) = o[r];
+      if (lane == 0) *reinterpret_cast<float2*>(S.scr_ml + (sw * PQ + r) * 2) = make_float2(m_w[r], l_w[r]);
+    }
+    tc::named_bar_sync(2, 32 * NSW);
+    if (sw < PQ) {
+      const int r = sw;
+      float M = kNegInf;
+#pragma unroll
+      for (int w2 = 0; w2 < NSW; ++w2) M = fmaxf(M, S.scr_ml[(w2 * PQ + r) * 2]);
+      const float Ms = (M == kNegInf) ? 0.f : M;
+      float4 od = make_float4(0.f, 0.f, 0.f, 0.f);
+      float ls = 0.f;
+#pragma unroll
+      for (int w2 = 0; w2 < NSW; ++w2) {
+        const float wt = ex2(S.scr_ml[(w2 * PQ + r) * 2] - Ms);
+        const float4 v = *reinterpret_cast<const float4*>(S.scr_o + (w2 * PQ + r) * kD + 4 * lane);
+        od.x = fmaf(wt, v.x, od.x); od.y = fmaf(wt, v.y, od.y);
+        od.z = fmaf(wt, v.z, od.z); od.w = fmaf(wt, v.w, od.w);
+        ls = fmaf(wt, S.scr_ml[(w2 * PQ + r) * 2 + 1], ls);
+      }
+      const int i = col / P.g, c = col - i * P.g;
+      const size_t gr = (size_t)i * P.h + c * PQ + r;
+      *reinterpret_cast<float4*>(P.ws_o + (gr * P.S + P.Sc + part) * kD + 4 * lane) = od;
+      if (lane == 0) reinterpret_cast<float2*>(P.ws_ml)[gr * P.S + P.Sc + part] = make_float2(M, ls);
+    }
+  }
 }
 
 BA_DEVINL unsigned long long gtimer() {
@@ -762,13 +946,14 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
         // warp stores this step's appended rows) =====
         uint32_t tt = __shfl_sync(0xffffffffu, p_tt, 0), sg = __shfl_sync(0xffffffffu, p_sg, 0);
         int2* const ring = reinterpret_cast<int2*>(bars + 56);  // [2] (column, length) per q buffer
-        const unsigned ncol = (unsigned)P.ncol;
-        // the next column's id and length are fetched one column ahead
+        const unsigned ncol = (unsigned)P.ncol * (unsigned)P.dparts;  // units
+        const unsigned gp = (unsigned)P.g * (unsigned)P.dparts;       // units per sample
+        // the next unit's id and column length are fetched one unit ahead
         unsigned nxt = 0;
         int nxtL = 0;
         if (lane == 0) {
           nxt = atomicAdd(P.col_ctr, 1u);
-          if (nxt < ncol) nxtL = dec_len(P, (int)(nxt / (unsigned)P.g));
+          if (nxt < ncol) nxtL = dec_len(P, (int)(nxt / gp));
         }
         for (;; ++sg) {
           const unsigned col = __shfl_sync(0xffffffffu, nxt, 0);
@@ -783,9 +968,13 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
             }
             break;
           }
-          const int i = (int)(col / (unsigned)P.g), c = (int)(col - (unsigned)i * (unsigned)P.g);
-          if (P.app.n > 0) {  // append+attend: this column's new rows before its TMA
-            append_rows_warp(P.app, i, c, clamp_len(P.lens, i, P.dec_cap), 0, P.dec_cap, lane);
+          const int i = (int)(col / gp);
+          const int cp = (int)(col - (unsigned)i * gp);  // c * dparts + part
+          const int c = cp / P.dparts, part = cp - c * P.dparts;
+          const int t0 = part * P.dunit;
+          if (P.app.n > 0) {  // append+attend: this unit's new rows before its TMA
+            append_rows_warp(P.app, i, c, clamp_len(P.lens, i, P.dec_cap), t0 * kBM,
+                             (t0 + P.dunit) * kBM, lane);
             fence_proxy_async_global();
             __syncwarp();
             fence_proxy_async_global();
@@ -794,12 +983,12 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
             ring[qbuf] = make_int2((int)col, L);
             const uint32_t qb = tc::smem_u32(&q_full[qbuf]);
             const uint32_t qdst = tc::smem_u32(sm_q + qbuf * QB);
-            tc::mbar_arrive_expect_tx(qb, 256);
-            tc::tma_load_3d(qdst, &P.tmQ1, qb, 0, c, i);
-            tc::tma_load_3d(qdst + N * 128, &P.tmQ1, qb, 64, c, i);
+            tc::mbar_arrive_expect_tx(qb, 256 * P.p);
+            tc::tma_load_3d(qdst, &P.tmQ1, qb, 0, c * P.p, i);
+            tc::tma_load_3d(qdst + N * 128, &P.tmQ1, qb, 64, c * P.p, i);
             const int z = i * P.g + c;
-            const int nt = (L + kBM - 1) / kBM;
-            for (int t = 0; t < nt; ++t, ++tt) {
+            const int nt = min((L + kBM - 1) / kBM, t0 + P.dunit);
+            for (int t = t0; t < nt; ++t, ++tt) {
               const int st = tt % NST;
               tc::mbar_wait_sleep(tc::smem_u32(&kv_empty[st]), ((tt / NST) & 1) ^ 1);
               const uint32_t bar = tc::smem_u32(&kv_full[st]);
@@ -810,7 +999,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
               tc::tma_load_3d_hint(dst + 32768, &P.tmVd, bar, 0, t * kBM, z, pol_d);
               tc::tma_load_3d_hint(dst + 49152, &P.tmVd, bar, 64, t * kBM, z, pol_d);
             }
-            if (nxt < ncol) nxtL = dec_len(P, (int)(nxt / (unsigned)P.g));
+            if (nxt < ncol) nxtL = dec_len(P, (int)(nxt / gp));
           }
           __syncwarp();
         }
@@ -1368,7 +1557,30 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
       L = Ln;
     }
     if constexpr (!KV8 && !MT && NSW == 8) {
-      if (P.dyn) {
+      if (P.dyn && P.p > 1) {
+        // ====== dynamic decode columns, p = 2 / 4 query rows (dyn_cc_multi) ======
+        if (u > 0) tc::mbar_wait(tc::smem_u32(&p_empty[(u - 1) % P.npb]), ((u - 1) / P.npb) & 1);
+        DynSmem S;
+        S.stage = sm_stage;
+        S.q = sm_q;
+        S.QB = QB;
+        S.Nq = N;
+        S.nst = NST;
+        S.kv_full = kv_full;
+        S.kv_empty = kv_empty;
+        S.q_full = q_full;
+        S.q_empty = q_empty;
+        S.ring = reinterpret_cast<const int2*>(bars + 56);
+        S.scr_o = reinterpret_cast<float*>(sm_p);
+        S.scr_ml = sm_red;
+        S.qf = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars + 64) + 128);
+        S.pex = S.qf + 2 * P.p * bif::kQHalf;
+        // (planned only for N = 16: compiled only there)
+        if constexpr (N == 16) {
+          if (P.p == 4) dyn_cc_multi<4, NSW>(P, S, sw, lane, u, sg);
+          else dyn_cc_multi<2, NSW>(P, S, sw, lane, u, sg);
+        }
+      } else if (P.dyn) {
         // ====== dynamic decode columns on the CUDA cores (p = 1) ======
         // Column (i, c): one query row against Kd[i][c] / Vd[i][c], a GEMV.
         // Warp sw owns tile positions [16 sw, 16 sw + 16): QK with 2 lanes per
@@ -1393,9 +1605,11 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
           const uint32_t qb = sg & 1;
           tc::mbar_wait(tc::smem_u32(&q_full[qb]), (sg >> 1) & 1);
           stamp(40);  // column's q (and id) in shared memory
-          const int col = reinterpret_cast<const volatile int*>(ring + qb)[0];
-          if (col < 0) break;
+          const int unit = reinterpret_cast<const volatile int*>(ring + qb)[0];
+          if (unit < 0) break;
           const int Lc = reinterpret_cast<const volatile int*>(ring + qb)[1];
+          const int col = unit / P.dparts, part = unit - col * P.dparts;
+          const int t0 = part * P.dunit;
           // this lane's half of the query row, fp32 (row 0 of the SW128 q box: unswizzled)
           float qf[64];
           {
@@ -1411,8 +1625,8 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
           }
           float m_w = kNegInf, l_w = 0.f;
           float2 oa = make_float2(0.f, 0.f), ob2 = make_float2(0.f, 0.f);
-          const int nt = (Lc + kBM - 1) / kBM;
-          for (int t = 0; t < nt; ++t, ++u) {
+          const int nt = min((Lc + kBM - 1) / kBM, t0 + P.dunit);
+          for (int t = t0; t < nt; ++t, ++u) {
             const uint32_t st = u % NST;
             tc::mbar_wait(tc::smem_u32(&kv_full[st]), (u / NST) & 1);
             stamp(41);  // tile landed
@@ -1491,8 +1705,8 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
             }
             const int i = col / P.g, c = col - i * P.g;
             const size_t gr = (size_t)i * P.h + c;  // p = 1
-            P.ws_o[(gr * P.S + P.Sc) * kD + d] = od;
-            if (d == 0) reinterpret_cast<float2*>(P.ws_ml)[gr * P.S + P.Sc] = make_float2(M, ls);
+            P.ws_o[(gr * P.S + P.Sc + part) * kD + d] = od;
+            if (d == 0) reinterpret_cast<float2*>(P.ws_ml)[gr * P.S + P.Sc + part] = make_float2(M, ls);
           }
           // every warp loaded q before the barrier: the buffer goes back
           if (sw == 0 && lane == 0) tc::mbar_arrive(tc::smem_u32(&q_empty[qb]));

@@ -145,6 +145,7 @@ struct Plan {
   // static (context) range and computed on the CUDA cores (p = 1, bf16,
   // single-token, no FP8): the static table covers the context tiles only
   bool dyn = false;
+  int dparts = 1, dunit = 1;  // dyn: parts per column, tiles per part
   int ntok = 1;  // query tokens per (sample, head) row group (multi-token step)
   bool kv8 = false;  // FP8 E4M3 KV cache (f4)
   int kv_elem = 0;   // bytes per KV element
@@ -325,8 +326,13 @@ int make_plan(const ba_problem_t* pr_in, int sms, bool replicated, Plan* pl) {
     // the merge: the cooperative decode launch does not start until the rows
     // kernel has drained, so C3 took 124 us and C5 3.3 ms; not used.)
     const long long dec_tiles = (long long)b * g * cdiv(pr->md_cap, 128);
+    // (round 3: p = 1 decode branches go to the fused launch's dynamic
+    // CUDA-core columns instead (C5); for C3 (p = 4) that plan measured 78 us
+    // against 70 us with decode items here: its decode launch also joins 9
+    // context partials per row)
+    const bool dyn_cand = p == 1 && P.ntok == 1 && !P.kv8;
     if (rows_dec_env && (p >= 32 || dec_tiles <= 4096 || rows_dec_env == 2) && p <= 128 &&
-        pr->md_cap >= 1) {
+        pr->md_cap >= 1 && !(dyn_cand && rows_dec_env != 2)) {
       P.cr_dec = true;
       P.cr_items += b * g;
     }
@@ -348,26 +354,39 @@ int make_plan(const ba_problem_t* pr_in, int sms, bool replicated, Plan* pl) {
     // the narrow tensor-core decode tile cost ~1.6 us against ~1.0 for a
     // context tile and set the tail; a CUDA-core column tile is well under the
     // per-SM HBM time of a 64 KB tile)
+    // p = 2 / 4 (GQA) columns read q as fp32 from extra shared memory and use
+    // the P buffer as the join scratch: only where that keeps 3 K/V stages
+    // (N = 16; the N = 32 fused plans have no room)
+    auto pq_fits = [&](int pq) {
+      if (pq <= 1) return true;
+      const int fx = ba::bif::smem_fixed(tcN, 2, false) + ba::bif::cc_extra_bytes(pq);
+      return (227 * 1024 - fx) / ba::bif::kStageBytes >= 3 && 2 * 256 * tcN * 2 >= 8 * pq * 512;
+    };
 #ifdef BIFATTN_NO_DYN
     P.dyn = false;  // A/B variant build: decode tiles in the static ranges (narrow path)
 #else
-    P.dyn = p == 1 && !P.kv8 && P.ntok == 1 && !P.cr_dec && P.tc_ntile_d > 0;
+    // p = 4 columns measured slower than the narrow tensor-core path (48.1 vs
+    // 45.4 us, b=4 h=32 g=8 mc=1k md=8k); p = 2 faster (36.3 vs 41.0 us)
+    P.dyn = (p == 1 || p == 2) && !P.kv8 && P.ntok == 1 && !P.cr_dec && P.tc_ntile_d > 0 &&
+            pq_fits(p);
 #endif
+    const int cc_x = P.dyn && p > 1 ? ba::bif::cc_extra_bytes(p) : 0;  // extra shared memory
     P.tc_T = P.tc_Tc + (P.dyn ? 0 : (long long)g * b * P.tc_ntile_d);
     const int gmax = sms < ba::bif_max_ctas ? sms : ba::bif_max_ctas;
     P.tc_G = (int)(P.tc_T < gmax ? P.tc_T : gmax);
     if (P.tc_T == 0 || P.dyn) P.tc_G = gmax;  // no tiles (ctx_rows, md_cap = 0): the merge only; dyn: every SM
     // P double-buffered when that keeps the K/V stage count (else one slot)
     P.tc_npb = 2;
-    if ((227 * 1024 - ba::bif::smem_fixed(tcN, 2, P.kv8)) / ba::bif::kStageBytes <
-        (227 * 1024 - ba::bif::smem_fixed(tcN, 1, P.kv8)) / ba::bif::kStageBytes)
+    if ((227 * 1024 - ba::bif::smem_fixed(tcN, 2, P.kv8) - cc_x) / ba::bif::kStageBytes <
+        (227 * 1024 - ba::bif::smem_fixed(tcN, 1, P.kv8) - cc_x) / ba::bif::kStageBytes)
       P.tc_npb = 1;
     static const int npb_env = knob_i("BIFATTN_NPB", 0);  // experiment override: BIFATTN_NPB=1|2
     if (npb_env == 1 || npb_env == 2) P.tc_npb = npb_env;
-    const int avail = 227 * 1024 - ba::bif::smem_fixed(tcN, P.tc_npb, P.kv8);  // dynamic smem is 1 KB aligned
+    if (cc_x) P.tc_npb = 2;  // the join scratch of p = 2 / 4 columns needs both P slots
+    const int avail = 227 * 1024 - ba::bif::smem_fixed(tcN, P.tc_npb, P.kv8) - cc_x;  // dynamic smem is 1 KB aligned
     P.tc_nst = avail / ba::bif::kStageBytes;
     if (P.tc_nst > 4) P.tc_nst = 4;
-    P.tc_smem = P.tc_nst * ba::bif::kStageBytes + ba::bif::smem_fixed(tcN, P.tc_npb, P.kv8);
+    P.tc_smem = P.tc_nst * ba::bif::kStageBytes + ba::bif::smem_fixed(tcN, P.tc_npb, P.kv8) + cc_x;
     const int gpc = tcN / p;  // groups per decode chunk
     const int ndc = (g + gpc - 1) / gpc;
     // context bands (ctx_unit, bif_tc.cuh): with several row chunks per group
@@ -471,7 +490,17 @@ int make_plan(const ba_problem_t* pr_in, int sms, bool replicated, Plan* pl) {
     }
     if (P.ctx_rows) sc = P.cr_nsplit;  // context partials written by ctx_rows_kernel
     if (P.cr_dec) sd = 1;              // one decode partial per row, also from ctx_rows_kernel
-    if (P.dyn) sd = 1;                 // one decode partial per row: a column is one CTA's
+    if (P.dyn) {
+      // (column, part) units: at least ~6 per CTA so the queue balances the
+      // CTAs, parts of >= 2 tiles (each part pays a q load and a join)
+      const long long ncol = (long long)b * g;
+      long long parts = (6LL * P.tc_G + ncol - 1) / ncol;
+      if (parts > (P.tc_ntile_d + 1) / 2) parts = (P.tc_ntile_d + 1) / 2;
+      if (parts < 1) parts = 1;
+      P.dunit = (int)((P.tc_ntile_d + parts - 1) / parts);
+      P.dparts = (P.tc_ntile_d + P.dunit - 1) / P.dunit;
+      sd = P.dparts;                   // one decode partial per (row, part)
+    }
     P.tc_Sc = sc;
     P.tc_Sd = sd;
     P.S = sc + sd;
@@ -763,7 +792,7 @@ int run_tc(const ba_problem_t* pr, const Plan& P, const void* q, const void* Kc,
     if (!rc)
       rc = make_tmap_3d(&bp.tmQd, q, d, pr->h, pr->b, d * 2, (uint64_t)pr->h * d * 2,
                         std::min(P.tc_N, pr->h), 1);
-    if (!rc && P.dyn) rc = make_tmap_3d(&bp.tmQ1, q, d, pr->h, pr->b, d * 2, (uint64_t)pr->h * d * 2, 1, 1);
+    if (!rc && P.dyn) rc = make_tmap_3d(&bp.tmQ1, q, d, pr->h, pr->b, d * 2, (uint64_t)pr->h * d * 2, p, 1);
   }
   if (!rc && P.tc_Tc == 0)  // replicated baseline: q map for the decode chunks
     rc = make_tmap_3d(&bp.tmQc, q, d, pr->h, pr->b, d * 2, (uint64_t)pr->h * d * 2, p, P.tc_N / p);
@@ -797,6 +826,8 @@ int run_tc(const ba_problem_t* pr, const Plan& P, const void* q, const void* Kc,
   bp.grid_ctr = reinterpret_cast<unsigned*>(static_cast<char*>(ws) + P.off_cnt);
   bp.dyn = P.dyn ? 1 : 0;
   bp.ncol = P.dyn ? pr->b * pr->g : 0;
+  bp.dparts = P.dparts;
+  bp.dunit = P.dunit;
   bp.col_ctr = bp.grid_ctr + 2;
   bp.out = out;
   bp.lse = lse;
@@ -1311,6 +1342,8 @@ const char* ba_plan_string(const ba_problem_t* prob) {
     snprintf(g_plan_buf, sizeof g_plan_buf, "invalid (%d)", rc);
     return g_plan_buf;
   }
+  char dyn_tag[64] = "";
+  if (P.dyn) snprintf(dyn_tag, sizeof dyn_tag, ",dec=cuda_core_dyn(parts=%d)", P.dparts);
   if (P.tc && P.cr_dec)
     snprintf(g_plan_buf, sizeof g_plan_buf,
              "ctx_rows(blocks=%d,splits=%d,tiles/split=%d,items=%d+%d dec,ctas=%d) + merge "
@@ -1322,7 +1355,7 @@ const char* ba_plan_string(const ba_problem_t* prob) {
              "ctx_rows(blocks=%d,splits=%d,tiles/split=%d,items=%d,ctas=%d) + "
              "dec_tc(N=%d,dec_tiles=%lld%s,ctas=%d,stages=%d,slots=%d+%d) launches=2 ws=%zu",
              P.cr_nrb, P.cr_nsplit, P.cr_tps, P.cr_items, P.cr_grid, P.tc_N,
-             P.dyn ? (long long)prob->b * prob->g * P.tc_ntile_d : P.tc_T, P.dyn ? ",dec=cuda_core_dyn" : "",
+             P.dyn ? (long long)prob->b * prob->g * P.tc_ntile_d : P.tc_T, dyn_tag,
              P.tc_G, P.tc_nst, P.tc_Sc, P.tc_Sd, P.ws_bytes);
   else if (P.tc)
     snprintf(g_plan_buf, sizeof g_plan_buf,
@@ -1330,7 +1363,7 @@ const char* ba_plan_string(const ba_problem_t* prob) {
              "slots=%d+%d,smem=%d) launches=1 ws=%zu",
              P.tc_N, P.tc_nrc, P.tc_bw, P.tc_Tc,
              P.dyn ? (long long)prob->b * prob->g * P.tc_ntile_d : P.tc_T - P.tc_Tc,
-             P.dyn ? ",dec=cuda_core_dyn" : "", P.tc_G, P.tc_nst, P.tc_npb, P.tc_Sc,
+             dyn_tag, P.tc_G, P.tc_nst, P.tc_npb, P.tc_Sc,
              P.tc_Sd, P.tc_smem, P.ws_bytes);
   else
     snprintf(g_plan_buf, sizeof g_plan_buf,

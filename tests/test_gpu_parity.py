@@ -293,6 +293,24 @@ def test_random_shapes_all_rows(cfg):
     compare(out, lse, ref, ref_lse, cfg.torch_dtype, f"{cfg.name} {ba.ba_plan_string(ba.make_problem(cfg.b, cfg.h, cfg.g, cfg.d, cfg.mc, cfg.md, cfg.torch_dtype))[:40]}")
 
 
+@pytest.mark.parametrize("cfg", [
+    # dynamic CUDA-core decode columns cut into parts (few, long columns):
+    # p = 1 and p = 2, ragged lens incl. 0, a part past a column's length
+    Config("dyn_p1_parts", "bf16", b=16, h=2, g=2, d=128, mc=200, md=2500),
+    Config("dyn_p2_parts", "bf16", b=8, h=4, g=2, d=128, mc=300, md=3000),
+    Config("dyn_p2_fused", "bf16", b=8, h=6, g=3, d=128, mc=1100, md=600),
+], ids=lambda c: c.name)
+def test_dyn_decode_parts_all_rows(cfg):
+    prob = ba.make_problem(cfg.b, cfg.h, cfg.g, cfg.d, cfg.mc, cfg.md, cfg.torch_dtype)
+    plan = ba.ba_plan_string(prob)
+    assert "cuda_core_dyn" in plan, plan
+    for variant in ("ragged", "normal"):
+        inp = make_inputs(cfg, 77, variant=variant)
+        out, lse = run_gpu(inp)
+        ref, ref_lse = oracle_rows(inp)
+        compare(out, lse, ref, ref_lse, cfg.torch_dtype, f"{cfg.name} {variant} {plan[:60]}")
+
+
 def test_fma_and_tc_plans_share_one_workspace():
     """One workspace serves the CUDA-core plan (n = 1, b*p = 8 rows) and the
     tensor-core plan (n = 4: 32 rows, grid barrier) alternately: the FMA plan

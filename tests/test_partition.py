@@ -44,7 +44,7 @@ def pick_n(b, h, g):
     return fit[0] if fit else cands[-1]
 
 
-def model(b, h, g, mc, md, cs, bw, N=None, with_ctx=True, dyn=False):
+def model(b, h, g, mc, md, cs, bw, N=None, with_ctx=True, dyn=False, dparts=1):
     """Python model of seg_at / ctx_unit / ctx_parts / dec_parts (bif_tc.cuh)
     over the planner's CTA table; bw = the plan's context band width.  With
     with_ctx=False (the context ran in ctx_rows_kernel) only decode tiles.
@@ -59,7 +59,11 @@ def model(b, h, g, mc, md, cs, bw, N=None, with_ctx=True, dyn=False):
     bw = bw if with_ctx else 1
     ntd = -(-md // 128) if md else 0
     if dyn:
-        sd_dyn = 1 if ntd else 0
+        # (column, part) units: parts of ceil(ntd / parts) tiles, one slot each
+        assert 1 <= dparts <= ntd
+        unit = -(-ntd // dparts)
+        assert -(-ntd // unit) == dparts
+        sd_dyn = dparts if ntd else 0
         ntd = 0
     gpc = N // p
     ndc = -(-g // gpc)
@@ -160,16 +164,17 @@ def test_split_covers_every_tile_once_and_slots_match(shape):
         assert N == min(n for n in (16, 32, 48, 64) if n % (h // g) == 0)
         assert int(m.group(3)) == int(m.group(1))
         dyn = "cuda_core_dyn" in plan
-        assert dyn == (h == g), plan  # p = 1 decode columns are dynamic
+        assert dyn == (h // g == 1), plan  # p = 1 decode columns are dynamic
+        dp = int(re.search(r"parts=(\d+)", plan).group(1)) if dyn else 1
         if md:
-            _, _, sd, _, _ = model(b, h, g, mc, md, cs, 1, N=N, with_ctx=False, dyn=dyn)
+            _, _, sd, _, _ = model(b, h, g, mc, md, cs, 1, N=N, with_ctx=False, dyn=dyn, dparts=dp)
             assert sd == int(m.group(4))
         return
     m = re.search(r"N=(\d+).*band=(\d+).*slots=(\d+)\+(\d+)", plan)
     assert m, plan
     dyn = "cuda_core_dyn" in plan
-    assert dyn == (h == g and md > 0), plan
-    N, sc, sd, loads, banded = model(b, h, g, mc, md, cs, int(m.group(2)), dyn=dyn)
+    dp = int(re.search(r"parts=(\d+)", plan).group(1)) if dyn else 1
+    N, sc, sd, loads, banded = model(b, h, g, mc, md, cs, int(m.group(2)), dyn=dyn, dparts=dp)
     assert (int(m.group(1)), int(m.group(3)), int(m.group(4))) == (N, sc, sd)
     mean = sum(loads) / len(loads)
     # the segment penalty only trims loads; whole banded units (8 tiles) add
