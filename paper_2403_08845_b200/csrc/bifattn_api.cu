@@ -845,6 +845,19 @@ int run_tc(const ba_problem_t* pr, const Plan& P, const void* q, const void* Kc,
     if (rc) return rc;
     cp.q = q;
     cp.b = pr->b; cp.h = pr->h; cp.g = pr->g; cp.p = p; cp.mc = pr->mc;
+    // Q blocks by TMA where a block is one box (rows on M = (sample, head j))
+#ifdef BIFATTN_NO_QTMA
+    if (false) {  // A/B variant: the softmax threads load Q
+#else
+    if (pr->g == 1) {
+#endif
+      cp.q_mode = 2;
+      rc = make_tmap_3d(&cp.tmQ, q, d, (uint64_t)pr->b * pr->h, 1, d * 2, (uint64_t)pr->b * pr->h * d * 2, 128, 1);
+    } else if (128 % p == 0) {
+      cp.q_mode = 1;
+      rc = make_tmap_3d(&cp.tmQ, q, d, pr->h, pr->b, d * 2, (uint64_t)pr->h * d * 2, p, 128 / p);
+    }
+    if (rc) return rc;
     cp.R = pr->b * p; cp.nrb = P.cr_nrb;
     cp.ntile = P.cr_ntile; cp.tps = P.cr_tps; cp.nsplit = P.cr_nsplit; cp.items = P.cr_items;
     cp.scale_log2 = scale_log2;

@@ -38,6 +38,12 @@ namespace ba {
 struct CtxRowsParams {
   CUtensorMap tmKc, tmVc;  // (d, mc, g), box (64, 128, 1), SW128
   CUtensorMap tmKd, tmVd;  // (d, md_cap, b*g), box (64, 128, 1): decode items (p >= 32)
+  // Q block by TMA (round 3; the softmax threads' global loads cost ~4k cycles
+  // per item): q_mode 1 = q as (d, h, b), box (64, p, 128/p) at (., c*p,
+  // rb*128/p) (p divides 128); 2 = q as (d, b*h) rows, box (64, 128) at
+  // (., rb*128) (g = 1: a block's rows are consecutive); 0 = thread loads
+  CUtensorMap tmQ;
+  int q_mode;
   const int32_t* lens;     // decode items: valid length min(clamp(lens[i]) + lens_add, dec_cap)
   int dec_cap, lens_add;
   AppendSrc app;           // append+attend: this step's rows, stored by the decode item's CTA
@@ -118,7 +124,7 @@ __global__ void __launch_bounds__(ctxr::kThreads, 1)
       tc::mbar_init(tc::smem_u32(&s_free[s]), 1);  // PV(u) done: slot reusable
       tc::mbar_init(tc::smem_u32(&p_full[s]), 8);
     }
-    tc::mbar_init(tc::smem_u32(q_full), 8);
+    tc::mbar_init(tc::smem_u32(q_full), P.q_mode ? 1 : 8);
     tc::mbar_init(tc::smem_u32(q_empty), 1);
     tc::mbar_init(tc::smem_u32(p_empty), 1);
     tc::mbar_init(tc::smem_u32(o_full), 1);
@@ -129,6 +135,7 @@ __global__ void __launch_bounds__(ctxr::kThreads, 1)
   if (warp == 0 && lane == 0) {
     tc::prefetch_tmap(&P.tmKc);
     tc::prefetch_tmap(&P.tmVc);
+    if (P.q_mode) tc::prefetch_tmap(&P.tmQ);
     if (P.items > P.items_ctx) {
       tc::prefetch_tmap(&P.tmKd);
       tc::prefetch_tmap(&P.tmVd);
@@ -203,8 +210,31 @@ __global__ void __launch_bounds__(ctxr::kThreads, 1)
       __syncwarp();
       fence_proxy_async_global();
     }
-    // ==================== TMA producers: K (warp 0), V (warp 3) ====================
-    if (lane == 0) {
+    // ============ TMA producers: K (warp 0), V (warp 3), Q (warp 0 lane 1) ============
+    if (lane == 1 && warp == 0 && P.q_mode) {
+      // the Q block of every non-empty item, as soon as the previous item's
+      // last QK has read the single Q buffer
+      uint32_t it = 0;
+      for (int k = blockIdx.x; k < P.items; k += gridDim.x) {
+        const Item I = item_of(k);
+        if (I.t1 == I.t0) continue;
+        tc::mbar_wait_sleep(tc::smem_u32(q_empty), (it & 1) ^ 1);
+        const uint32_t bar = tc::smem_u32(q_full);
+        tc::mbar_arrive_expect_tx(bar, 32768);
+        const uint32_t dst = tc::smem_u32(smem + kQ);
+        int y, z;
+        if (P.q_mode == 1) {  // (head c*p + j, sample): rows of the block are (sample, j)
+          y = I.c * P.p;
+          z = I.dec ? I.i : I.rb * (128 / P.p);
+        } else {              // g = 1: row gr = i*h + j = the row within the group
+          y = I.dec ? I.i * P.h : I.rb * 128;
+          z = 0;
+        }
+        tc::tma_load_3d(dst, &P.tmQ, bar, 0, y, z);
+        tc::tma_load_3d(dst + 16384, &P.tmQ, bar, 64, y, z);
+        ++it;
+      }
+    } else if (lane == 0) {
       const bool isk = warp == 0;
       uint64_t* full = isk ? k_full : v_full;
       uint64_t* empty = isk ? k_empty : v_empty;
@@ -353,6 +383,7 @@ __global__ void __launch_bounds__(ctxr::kThreads, 1)
         continue;
       }
       // ---- this half of the Q row -> shared memory (SW128, the TMA box layout) ----
+      if (!P.q_mode) {
       tc::mbar_wait(tc::smem_u32(q_empty), (it & 1) ^ 1);
       {
         const uint4* src = reinterpret_cast<const uint4*>(P.q) + (size_t)(valid_row ? gr : 0) * 16;
@@ -376,6 +407,7 @@ __global__ void __launch_bounds__(ctxr::kThreads, 1)
           asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const uint4*>(P.q) + (size_t)grn * 16 + 8 * hf));
         }
       }
+      }  // !q_mode
       float m = kNegInf, l = 0.f;  // l: this half's share of the row sum
       pf.mark(0);
       for (int t = t0; t < t1; ++t, ++u) {
