@@ -359,15 +359,6 @@ BA_DEVINL void tmem_ld_cols(uint32_t taddr, uint32_t* r) {
 
 // two bf16 (lo, hi halves of a word) -> float2 (exact)
 BA_DEVINL float2 bf16x2_f2(uint32_t w) { return make_float2(bf16lo(w), bf16hi(w)); }
-// acc += a * b on both lanes of a pair (one packed FFMA2 on sm_100)
-BA_DEVINL void ffma2(float2& acc, float2 a, float2 b) {
-  unsigned long long A, X, Y;
-  asm("mov.b64 %0, {%1, %2};" : "=l"(A) : "f"(acc.x), "f"(acc.y));
-  asm("mov.b64 %0, {%1, %2};" : "=l"(X) : "f"(a.x), "f"(a.y));
-  asm("mov.b64 %0, {%1, %2};" : "=l"(Y) : "f"(b.x), "f"(b.y));
-  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(A) : "l"(X), "l"(Y));
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(acc.x), "=f"(acc.y) : "l"(A));
-}
 
 // ---------------------------------------------------------------------------
 // Dynamic decode columns with PQ = p = 2 or 4 query rows (GQA), CUDA cores.

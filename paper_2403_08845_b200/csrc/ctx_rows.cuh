@@ -423,25 +423,24 @@ __global__ void __launch_bounds__(ctxr::kThreads, 1)
         const int Lrow = I.dec && P.ntok > 1 ? max(I.L - (P.ntok - 1 - r % P.ntok), 0) : I.L;
         const int nvalid = min(128, Lrow - t * 128) - hf * 64;
         // row max over this half's 64 positions: 8 independent chains (a
-        // single running fmax was a 64-deep dependency chain, ~1k cycles/pass)
+        // single running fmax was a 64-deep dependency chain, ~1k cycles/pass),
+        // on the raw logits (the scale is positive: max commutes with it, and
+        // the scaling folds into the exponent's FFMA2 below)
         float mq[8];
 #pragma unroll
         for (int k = 0; k < 8; ++k) mq[k] = kNegInf;
         if (nvalid >= 64) {
 #pragma unroll
-          for (int i = 0; i < 64; ++i) {
-            x[i] *= sl2;
-            mq[i & 7] = fmaxf(mq[i & 7], x[i]);
-          }
+          for (int i = 0; i < 64; ++i) mq[i & 7] = fmaxf(mq[i & 7], x[i]);
         } else {
 #pragma unroll
           for (int i = 0; i < 64; ++i) {
-            x[i] = i < nvalid ? x[i] * sl2 : kNegInf;
+            x[i] = i < nvalid ? x[i] : kNegInf;
             mq[i & 7] = fmaxf(mq[i & 7], x[i]);
           }
         }
         const float mh = fmaxf(fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3])),
-                               fmaxf(fmaxf(mq[4], mq[5]), fmaxf(mq[6], mq[7])));
+                               fmaxf(fmaxf(mq[4], mq[5]), fmaxf(mq[6], mq[7]))) * sl2;
         pf.mark(3);
         float* const xs = sm_x + (u & 1) * 256;
         xs[hf * 128 + r] = mh;
@@ -475,7 +474,9 @@ __global__ void __launch_bounds__(ctxr::kThreads, 1)
         const float mref = m == kNegInf ? 0.f : m;  // a row with no valid position yet: P = 0
         // P = 2^(x - m) as ONE f16 operand (reading R23; V is f16 * 2^-8) into
         // TMEM over S: the PV's A operand
-        float lq[4] = {0.f, 0.f, 0.f, 0.f};  // independent partial row sums
+        // exponent x * scale - m as one FFMA2 per pair; partial row sums as FADD2
+        const float2 sl2v = make_float2(sl2, sl2), nmv = make_float2(-mref, -mref);
+        float2 lq[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};  // independent partial row sums
 #pragma unroll
         for (int j = 0; j < ((CTXR_EXP & 2) ? 0 : 4); ++j) {
           uint32_t hk[8];
@@ -483,13 +484,14 @@ __global__ void __launch_bounds__(ctxr::kThreads, 1)
           for (int e = 0; e < 16; e += 2) {
             // (moving 6 of 16 exponentials to an FMA-pipe polynomial was
             // measured slower, C4 50.9 -> 56.0 us: the pass is issue-bound)
-            const float p0 = ex2(x[j * 16 + e] - mref), p1 = ex2(x[j * 16 + e + 1] - mref);
-            lq[(e >> 1) & 3] += p0 + p1;
-            hk[e / 2] = pack_f16x2(p0, p1);
+            const float2 z = fma2(make_float2(x[j * 16 + e], x[j * 16 + e + 1]), sl2v, nmv);
+            const float2 pz = make_float2(ex2(z.x), ex2(z.y));
+            lq[(e >> 1) & 1] = add2(lq[(e >> 1) & 1], pz);
+            hk[e / 2] = pack_f16x2(pz.x, pz.y);
           }
           tc::tmem_st<8>(tS + (u % kS) * 128 + hf * 32 + j * 8 + lane_addr, hk);
         }
-        l += (lq[0] + lq[1]) + (lq[2] + lq[3]);
+        l += (lq[0].x + lq[0].y) + (lq[1].x + lq[1].y);
         tc::tmem_st_wait();
         tc::tc_fence_before();
         __syncwarp();

@@ -3,7 +3,8 @@ the same sources (_build.build_variant) on one config: each round runs
 bench.py once per library in a fresh process; medians of us_per_step and the
 CUDA-graph replay over the rounds.
 
-usage: python scripts/ab.py CONFIG ROUNDS NAME -DFLAG [-DFLAG ...]"""
+usage: python scripts/ab.py CONFIG ROUNDS NAME -DFLAG [-DFLAG ...]
+       python scripts/ab.py CONFIG ROUNDS NAME --lib PATH   (a prebuilt library, e.g. scripts/build_rev.py)"""
 import json
 import os
 import statistics
@@ -15,7 +16,10 @@ sys.path.insert(0, ROOT)
 from paper_2403_08845_b200 import _build  # noqa: E402
 
 cfg, rounds, name, defines = sys.argv[1], int(sys.argv[2]), sys.argv[3], sys.argv[4:]
-libs = {"product": _build.build(), name: _build.build_variant(name, defines)}
+if defines[:1] == ["--lib"]:
+    libs = {"product": _build.build(), name: os.path.join(ROOT, defines[1])}
+else:
+    libs = {"product": _build.build(), name: _build.build_variant(name, defines)}
 RUN = ("import sys; sys.path.insert(0, %r); import paper_2403_08845_b200 as ba; "
        "ba.load_library(%r); import bench; sys.argv = ['bench.py', '--config', %r, '--steps', '30', "
        "'--no-e2e', '--no-replicated', '--no-cpu-baseline', '--no-stream-peak', '--no-others', "
