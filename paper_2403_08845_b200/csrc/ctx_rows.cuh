@@ -82,6 +82,7 @@ constexpr float kTh = 8.0f;             // stale-max slack (log2 units), as bif_
 constexpr int kThreads = 416;        // 13 warps: + warp 12, the second V converter
 constexpr float kVScale = 0.00390625f;  // V is converted to f16 as V * 2^-8 (reading R23)
 
+
 // byte offset of 16-byte chunk `ch` (0..15) of row r in a 128-row x 128-col
 // bf16 K-major SW128 tile stored as two 64-column halves (the TMA box layout)
 BA_DEVINL uint32_t sw128_off(int r, int ch) {
@@ -482,8 +483,9 @@ __global__ void __launch_bounds__(ctxr::kThreads, 1)
           uint32_t hk[8];
 #pragma unroll
           for (int e = 0; e < 16; e += 2) {
-            // (moving 6 of 16 exponentials to an FMA-pipe polynomial was
-            // measured slower, C4 50.9 -> 56.0 us: the pass is issue-bound)
+            // (round 3 again moved 3 of 8 pairs to a packed degree-3 FMA-pipe
+            // polynomial: C4 48.6 vs 45.9 us, C3 70.4 vs 68.1 us without it —
+            // the pass is bound by issue and latency, not by MUFU)
             const float2 z = fma2(make_float2(x[j * 16 + e], x[j * 16 + e + 1]), sl2v, nmv);
             const float2 pz = make_float2(ex2(z.x), ex2(z.y));
             lq[(e >> 1) & 1] = add2(lq[(e >> 1) & 1], pz);
