@@ -359,6 +359,12 @@ BA_DEVINL void tmem_ld_cols(uint32_t taddr, uint32_t* r) {
 
 // two bf16 (lo, hi halves of a word) -> float2 (exact)
 BA_DEVINL float2 bf16x2_f2(uint32_t w) { return make_float2(bf16lo(w), bf16hi(w)); }
+// two f16 (lo, hi) -> float2 (exact)
+BA_DEVINL float2 f16x2_f2(uint32_t w) {
+  __half2 h;
+  h = *reinterpret_cast<const __half2*>(&w);
+  return __half22float2(h);
+}
 
 // ---------------------------------------------------------------------------
 // Dynamic decode columns with PQ = p = 2 or 4 query rows (GQA), CUDA cores.
@@ -773,7 +779,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
       tc::mbar_init(tc::smem_u32(&kv_full[s]), 1);
       // released by the PV commit (+ NSW - 1 plain arrivals) after an MMA tile,
       // by the NSW softmax warps after a CUDA-core decode tile (dyn)
-      tc::mbar_init(tc::smem_u32(&kv_empty[s]), KV8 ? 1 : NSW);
+      tc::mbar_init(tc::smem_u32(&kv_empty[s]), NSW);
       if (KV8) {
         tc::mbar_init(tc::smem_u32(&k_cvt[s]), 4);
         tc::mbar_init(tc::smem_u32(&v_cvt[s]), 4);
@@ -931,7 +937,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
       p_tt = tt;
       p_sg = sg;
     }
-    if constexpr (!KV8 && !MT && NSW == 8) {
+    if constexpr (!MT && NSW == 8) {
       if (P.dyn) {
         // ===== dynamic decode columns (whole warp: lane 0 drives the TMA, the
         // warp stores this step's appended rows) =====
@@ -983,12 +989,18 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
               const int st = tt % NST;
               tc::mbar_wait_sleep(tc::smem_u32(&kv_empty[st]), ((tt / NST) & 1) ^ 1);
               const uint32_t bar = tc::smem_u32(&kv_full[st]);
-              tc::mbar_arrive_expect_tx(bar, kStageBytes);
               const uint32_t dst = tc::smem_u32(sm_stage + st * kStageBytes);
-              tc::tma_load_3d_hint(dst, &P.tmKd, bar, 0, t * kBM, z, pol_d);
-              tc::tma_load_3d_hint(dst + 16384, &P.tmKd, bar, 64, t * kBM, z, pol_d);
-              tc::tma_load_3d_hint(dst + 32768, &P.tmVd, bar, 0, t * kBM, z, pol_d);
-              tc::tma_load_3d_hint(dst + 49152, &P.tmVd, bar, 64, t * kBM, z, pol_d);
+              if constexpr (KV8) {  // code tiles into the stage's code slots (as the static path)
+                tc::mbar_arrive_expect_tx(bar, 32768);
+                tc::tma_load_3d_hint(dst + 16384, &P.tmKd, bar, 0, t * kBM, z, pol_d);
+                tc::tma_load_3d_hint(dst + 49152, &P.tmVd, bar, 0, t * kBM, z, pol_d);
+              } else {
+                tc::mbar_arrive_expect_tx(bar, kStageBytes);
+                tc::tma_load_3d_hint(dst, &P.tmKd, bar, 0, t * kBM, z, pol_d);
+                tc::tma_load_3d_hint(dst + 16384, &P.tmKd, bar, 64, t * kBM, z, pol_d);
+                tc::tma_load_3d_hint(dst + 32768, &P.tmVd, bar, 0, t * kBM, z, pol_d);
+                tc::tma_load_3d_hint(dst + 49152, &P.tmVd, bar, 64, t * kBM, z, pol_d);
+              }
             }
             if (nxt < ncol) nxtL = dec_len(P, (int)(nxt / gp));
           }
@@ -1076,7 +1088,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
           }
           tc::mma_commit(tc::smem_u32(&p_empty[ps]));
           if (!(BIF_DBG & 1024)) tc::mma_commit(tc::smem_u32(&kv_empty[st]));
-          if (!KV8) tc::mbar_arrive_cnt(tc::smem_u32(&kv_empty[st]), NSW - 1);
+          tc::mbar_arrive_cnt(tc::smem_u32(&kv_empty[st]), NSW - 1);
           pf.mark(2);
           if (kStamp && P.trace && u < 256)
             P.trace[(size_t)blockIdx.x * kTraceSlots + 768 + u] = (gtimer() & 0x00ffffffffffffffull) | (32ull << 56);
@@ -1547,8 +1559,8 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
       w = s.next;
       L = Ln;
     }
-    if constexpr (!KV8 && !MT && NSW == 8) {
-      if (P.dyn && P.p > 1) {
+    if constexpr (!MT && NSW == 8) {
+      if (!KV8 && P.dyn && P.p > 1) {
         // ====== dynamic decode columns, p = 2 / 4 query rows (dyn_cc_multi) ======
         if (u > 0) tc::mbar_wait(tc::smem_u32(&p_empty[(u - 1) % P.npb]), ((u - 1) / P.npb) & 1);
         DynSmem S;
@@ -1566,8 +1578,8 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
         S.scr_ml = sm_red;
         S.qf = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(bars + 64) + 128);
         S.pex = S.qf + 2 * P.p * bif::kQHalf;
-        // (planned only for N = 16: compiled only there)
-        if constexpr (N == 16) {
+        // (planned only for N = 16, bf16 cache: compiled only there)
+        if constexpr (N == 16 && !KV8) {
           if (P.p == 4) dyn_cc_multi<4, NSW>(P, S, sw, lane, u, sg);
           else dyn_cc_multi<2, NSW>(P, S, sw, lane, u, sg);
         }
@@ -1623,15 +1635,33 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
             stamp(41);  // tile landed
             const uint8_t* const stage = sm_stage + st * kStageBytes;
             // ---- logit of position pp: this lane's 64 products, + the other half ----
-            const uint8_t* const krow = stage + hf * 16384 + pp * 128;
             float2 a0 = make_float2(0.f, 0.f), a1 = make_float2(0.f, 0.f);
+            if constexpr (KV8) {
+              // E4M3 codes of row pp (128 B, SW128 chunks of 16 codes; the stage's
+              // K code slot at +16 KB): this lane's 64 codes = chunks 4 hf .. 4 hf + 3,
+              // exact via f16 (R20); k_scale is in the logit scale
+              const uint8_t* const krow = stage + 16384 + pp * 128;
 #pragma unroll
-            for (int ch = 0; ch < 8; ++ch) {
-              const uint4 v = *reinterpret_cast<const uint4*>(krow + ((ch ^ (pp & 7)) << 4));
-              ffma2(a0, bf16x2_f2(v.x), make_float2(qf[8 * ch + 0], qf[8 * ch + 1]));
-              ffma2(a1, bf16x2_f2(v.y), make_float2(qf[8 * ch + 2], qf[8 * ch + 3]));
-              ffma2(a0, bf16x2_f2(v.z), make_float2(qf[8 * ch + 4], qf[8 * ch + 5]));
-              ffma2(a1, bf16x2_f2(v.w), make_float2(qf[8 * ch + 6], qf[8 * ch + 7]));
+              for (int cc = 0; cc < 4; ++cc) {
+                const uint4 v = *reinterpret_cast<const uint4*>(krow + (((4 * hf + cc) ^ (pp & 7)) << 4));
+                const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  const float2 k0 = f16x2_f2(e4m3x2_to_f16x2(w[e])), k1 = f16x2_f2(e4m3x2_to_f16x2(w[e] >> 16));
+                  ffma2(a0, k0, make_float2(qf[16 * cc + 4 * e + 0], qf[16 * cc + 4 * e + 1]));
+                  ffma2(a1, k1, make_float2(qf[16 * cc + 4 * e + 2], qf[16 * cc + 4 * e + 3]));
+                }
+              }
+            } else {
+              const uint8_t* const krow = stage + hf * 16384 + pp * 128;
+#pragma unroll
+              for (int ch = 0; ch < 8; ++ch) {
+                const uint4 v = *reinterpret_cast<const uint4*>(krow + ((ch ^ (pp & 7)) << 4));
+                ffma2(a0, bf16x2_f2(v.x), make_float2(qf[8 * ch + 0], qf[8 * ch + 1]));
+                ffma2(a1, bf16x2_f2(v.y), make_float2(qf[8 * ch + 2], qf[8 * ch + 3]));
+                ffma2(a0, bf16x2_f2(v.z), make_float2(qf[8 * ch + 4], qf[8 * ch + 5]));
+                ffma2(a1, bf16x2_f2(v.w), make_float2(qf[8 * ch + 6], qf[8 * ch + 7]));
+              }
             }
             float sdot = (a0.x + a0.y) + (a1.x + a1.y);
             sdot += __shfl_xor_sync(0xffffffffu, sdot, 16);
@@ -1652,7 +1682,17 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
             // ---- o += p . V over the warp's valid positions (lane: d = 4 lane ..) ----
             const uint8_t* const vb = stage + 32768 + hf * 16384 + vsub;
             const int nv = min(max(Lc - (t * kBM + 16 * sw), 0), 16);
-            if (nv == 16) {
+            if constexpr (KV8) {
+              // V codes (the stage's V code slot at +48 KB): 4 codes = d 4 lane .. per row
+              const uint8_t* const vc = stage + 49152 + (lane & 3) * 4;
+              for (int k = 0; k < nv; ++k) {
+                const float pk = __shfl_sync(0xffffffffu, pe, k);
+                const int r = 16 * sw + k;
+                const uint32_t w = *reinterpret_cast<const uint32_t*>(vc + r * 128 + (((lane >> 2) ^ (r & 7)) << 4));
+                ffma2(oa, f16x2_f2(e4m3x2_to_f16x2(w)), make_float2(pk, pk));
+                ffma2(ob2, f16x2_f2(e4m3x2_to_f16x2(w >> 16)), make_float2(pk, pk));
+              }
+            } else if (nv == 16) {
 #pragma unroll
               for (int k = 0; k < 16; ++k) {
                 const float pk = __shfl_sync(0xffffffffu, pe, k);

@@ -367,7 +367,7 @@ int make_plan(const ba_problem_t* pr_in, int sms, bool replicated, Plan* pl) {
 #else
     // p = 4 columns measured slower than the narrow tensor-core path (48.1 vs
     // 45.4 us, b=4 h=32 g=8 mc=1k md=8k); p = 2 faster (36.3 vs 41.0 us)
-    P.dyn = (p == 1 || p == 2) && !P.kv8 && P.ntok == 1 && !P.cr_dec && P.tc_ntile_d > 0 &&
+    P.dyn = (p == 1 || (p == 2 && !P.kv8)) && P.ntok == 1 && !P.cr_dec && P.tc_ntile_d > 0 &&
             pq_fits(p);
 #endif
     const int cc_x = P.dyn && p > 1 ? ba::bif::cc_extra_bytes(p) : 0;  // extra shared memory
