@@ -822,7 +822,13 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
   // first plans its first segment from the parameters while the previous
   // kernel drains; measured neutral), and let the next launch start its own
   // prologue
-  if (warp != 0) pdl_wait();
+  // decode-only launch after the rows kernel (ext_ctx, no context tiles): it
+  // reads nothing the rows kernel writes until the merge, and the rows kernel
+  // waited for the previous step before letting this launch start, so its
+  // CTAs stream decode columns on the SMs the rows kernel leaves free (a
+  // non-cooperative launch) and wait for it only before the grid barrier
+  const bool early = P.ext_ctx > 0 && P.Tc == 0;
+  if (warp != 0 && !early) pdl_wait();
   pdl_launch_dependents();
   if (threadIdx.x == 0) tstamp(254, 54);
   const uint32_t tmem = *tmem_holder;
@@ -839,7 +845,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
     if (lane == 0 && nw > 0) s_first = seg_at(P, rg, 0);
     const uint64_t pol_c = P.nrc == 1 ? tc::policy_evict_first() : tc::policy_evict_last();
     const uint64_t pol_d = tc::policy_evict_first();
-    pdl_wait();
+    if (!early) pdl_wait();
     // append+attend: store this step's K/V rows that fall in this CTA's decode
     // tiles before any TMA of them (same CTA: generic stores, then a proxy fence)
     if (P.app.n > 0 && P.Td > 0) {
@@ -1992,6 +1998,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
   const int my_gr = r0 + warp;
   int my_nctx = sm_mcnt[2 * warp], my_ndec = sm_mcnt[2 * warp + 1];
   if (threadIdx.x == 0) {
+    if (early) pdl_wait();  // the rows kernel's context partials are complete
     tstamp(249, 49);
     // generation barrier: grid_ctr[0] counts arrivals (reset by the last
     // arriver), grid_ctr[1] is the generation it then advances

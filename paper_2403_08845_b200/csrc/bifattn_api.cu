@@ -717,6 +717,11 @@ int ensure_smem_attr(Kern* fn, int bytes, bool* done) {
 
 template <int N, int SWG, bool MT, bool KV8 = false>
 int launch_bif_tc_n(const ba::BifTcParams& bp, int smem, uint32_t flags, LaunchRec& rec) {
+  // the decode-only launch after the rows kernel starts on the SMs the rows
+  // kernel leaves free: not cooperative (its grid barrier still completes —
+  // the rows kernel ends on its own and frees the rest); every other launch
+  // is cooperative (all CTAs co-resident before the grid barrier)
+  const bool coop = !(bp.ext_ctx > 0 && bp.Tc == 0);
   static bool attr_done[64];
   if (int rc = ensure_smem_attr(ba::bif_tc_kernel<N, SWG, MT, KV8>, 227 * 1024, attr_done)) return rc;
   // one cooperative launch (all CTAs co-resident: the kernel ends with a grid
@@ -728,9 +733,9 @@ int launch_bif_tc_n(const ba::BifTcParams& bp, int smem, uint32_t flags, LaunchR
   cfg.dynamicSmemBytes = smem;
   cfg.stream = rec.st;
   cudaLaunchAttribute attr[2];
-  // always cooperative: the kernel's grid barrier needs every CTA resident
+  // cooperative unless this is the early-start decode launch (see coop above)
   attr[0].id = cudaLaunchAttributeCooperative;
-  attr[0].val.cooperative = 1;
+  attr[0].val.cooperative = coop ? 1 : 0;
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[1].val.programmaticStreamSerializationAllowed = (flags & BA_FLAG_NO_PDL) ? 0 : 1;
   cfg.attrs = attr;
