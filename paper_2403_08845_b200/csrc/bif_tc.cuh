@@ -113,7 +113,7 @@ struct BifTcParams {
   int S, Sc;                 // slots per row; decode slots start at Sc
   float* ws_o;               // [b*h][S][128]
   float* ws_ml;              // [b*h][S][2]
-  unsigned* grid_ctr;        // grid barrier [count, generation] (self-resetting; zeroed once)
+  unsigned* grid_ctr;        // grid barrier: 64-bit arrival count at [0, 1] (+256 per launch; zeroed once), [2] col_ctr
   void* out;                 // [b][h][128] bf16
   float* lse;                // [b][h] or null
   unsigned long long* trace; // optional [G][kTraceSlots] globaltimer stamps (instrumentation)
@@ -2000,23 +2000,29 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
   if (threadIdx.x == 0) {
     if (early) pdl_wait();  // the rows kernel's context partials are complete
     tstamp(249, 49);
-    // generation barrier: grid_ctr[0] counts arrivals (reset by the last
-    // arriver), grid_ctr[1] is the generation it then advances
-    unsigned gen;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(gen) : "l"(P.grid_ctr + 1) : "memory");
-    unsigned old;
-    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(P.grid_ctr) : "memory");
+    // monotonic barrier: the 64-bit word grid_ctr[0..1] grows by exactly
+    // kLaunchStride per launch (G arrivals + the last arriver's pad), so a
+    // launch starts at a multiple of the stride whatever G the plans on this
+    // workspace use; the CTAs poll the counter itself — no reset and no
+    // generation flip (one dependent round trip fewer after the last arrival
+    // than round 2's count + generation pair)
+    constexpr unsigned long long kLaunchStride = 256;  // > bif_max_ctas
+    unsigned long long* const ctr = reinterpret_cast<unsigned long long*>(P.grid_ctr);
+    unsigned long long old;
+    asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], 1;" : "=l"(old) : "l"(ctr) : "memory");
     tstamp(248, 48);
-    if (old == (unsigned)P.G - 1u) {
-      asm volatile("st.relaxed.gpu.global.u32 [%0], 0;" ::"l"(P.grid_ctr) : "memory");
-      // every CTA has taken its last decode column: the queue starts at 0 next launch
+    const unsigned long long target = old / kLaunchStride * kLaunchStride + (unsigned long long)P.G;
+    if (old + 1ull == target) {
+      // the last arrival: every CTA has taken its last decode column — the
+      // queue starts at 0 next launch; pad the count to the next stride (no
+      // CTA of the next launch arrives before this grid has completed)
       if (P.dyn) asm volatile("st.relaxed.gpu.global.u32 [%0], 0;" ::"l"(P.col_ctr) : "memory");
-      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(P.grid_ctr + 1) : "memory");
+      asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(ctr), "l"(kLaunchStride - (unsigned long long)P.G) : "memory");
     } else {
-      unsigned g2;
+      unsigned long long cur;
       do {
-        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(g2) : "l"(P.grid_ctr + 1) : "memory");
-      } while (g2 == gen);
+        asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(cur) : "l"(ctr) : "memory");
+      } while (cur < target);
     }
   }
   __syncthreads();
