@@ -20,6 +20,7 @@
 #include "../../include/bifattn.h"
 #include "common.cuh"
 #include "bif_tc.cuh"
+#include "ctx_rows2.cuh"
 #include "fma_partial.cuh"
 #include "merge.cuh"
 #include "append.cuh"
@@ -128,6 +129,9 @@ struct Plan {
   // decode branch also in the rows kernel (p >= 32 rows per sample and group);
   // the second launch is then the light merge kernel, not the fused kernel
   bool cr_dec = false;
+  // two 128-row blocks per item in ping-pong (ctx_rows2.cuh; Q by TMA only)
+  bool cr_v2 = false;
+  int cr_nrp = 0;
   int cr_items_ctx = 0;
   long long tc_Tc = 0, tc_T = 0;
   int tc_cs[ba::bif_max_ctas + 1];
@@ -303,16 +307,37 @@ int make_plan(const ba_problem_t* pr_in, int sms, bool replicated, Plan* pl) {
       }
     P.cr_nrb = cdiv(R, 128);
     P.cr_ntile = cdiv(pr->mc, 128);
+    // decode items in the rows kernel?  (see below; decided first: the
+    // two-block kernel runs them one block at a time, slower than the
+    // one-block kernel's two threads per row)
+    static const int rows_dec_env = knob_i("BIFATTN_ROWS_DEC", 1);  // BIFATTN_ROWS_DEC=0: decode stays in the fused kernel
+    const long long dec_tiles = (long long)b * g * cdiv(pr->md_cap, 128);
+    // (round 3: p = 1 decode branches go to the fused launch's dynamic
+    // CUDA-core columns instead (C5); for C3 (p = 4) that plan measured 78 us
+    // against 70 us with decode items here: its decode launch also joins 9
+    // context partials per row)
+    const bool dyn_cand = p == 1 && P.ntok == 1 && !P.kv8;
+    const bool will_cr_dec = rows_dec_env && (p >= 32 || dec_tiles <= 4096 || rows_dec_env == 2) &&
+                             p <= 128 && pr->md_cap >= 1 && !(dyn_cand && rows_dec_env != 2);
+    // two-block ping-pong kernel (ctx_rows2.cuh) for context-only launches
+    // whose Q blocks are TMA boxes (g = 1, or p divides 128), >= 2 row blocks
+    // per group: C5's context 432 -> 360 us; with decode items (C3, C4) the
+    // one-block kernel stays faster (C4 46.2 vs 48.6, C3 69.5 vs 75.4 us)
+#ifdef BIFATTN_ROWS1
+    P.cr_v2 = false;  // A/B variant: the one-block rows kernel
+#else
+    P.cr_v2 = (g == 1 || 128 % p == 0) && P.cr_nrb >= 2 && !will_cr_dec;
+#endif
+    P.cr_nrp = P.cr_v2 ? cdiv(P.cr_nrb, 2) : P.cr_nrb;
     // one wave of long items: every item pays a Q load, a pipeline refill and
     // a 64 KB partial (written here, read by the merge)
     static const int ns_env = knob_i("BIFATTN_ROWS_SPLITS", 0);  // experiment override: BIFATTN_ROWS_SPLITS
-    int ns = ns_env > 0 ? ns_env : std::max(1, sms / (g * P.cr_nrb));
+    int ns = ns_env > 0 ? ns_env : std::max(1, sms / (g * P.cr_nrp));
     ns = std::max(1, std::min(ns, P.cr_ntile));
     P.cr_tps = cdiv(P.cr_ntile, ns);
     P.cr_nsplit = cdiv(P.cr_ntile, P.cr_tps);
-    P.cr_items = g * P.cr_nrb * P.cr_nsplit;
+    P.cr_items = g * P.cr_nrp * P.cr_nsplit;
     P.cr_items_ctx = P.cr_items;
-    static const int rows_dec_env = knob_i("BIFATTN_ROWS_DEC", 1);  // BIFATTN_ROWS_DEC=0: decode stays in the fused kernel
     // decode items too when p >= 32 (they fill the row block) or when the
     // decode part is small (<= 4096 tiles: C3, multi-token C2b), where a second
     // persistent launch costs more than the half-empty row blocks (measured:
@@ -325,14 +350,7 @@ int make_plan(const ba_problem_t* pr_in, int sms, bool replicated, Plan* pl) {
     // kernel on the SMs it leaves free — PDL, griddepcontrol.wait only before
     // the merge: the cooperative decode launch does not start until the rows
     // kernel has drained, so C3 took 124 us and C5 3.3 ms; not used.)
-    const long long dec_tiles = (long long)b * g * cdiv(pr->md_cap, 128);
-    // (round 3: p = 1 decode branches go to the fused launch's dynamic
-    // CUDA-core columns instead (C5); for C3 (p = 4) that plan measured 78 us
-    // against 70 us with decode items here: its decode launch also joins 9
-    // context partials per row)
-    const bool dyn_cand = p == 1 && P.ntok == 1 && !P.kv8;
-    if (rows_dec_env && (p >= 32 || dec_tiles <= 4096 || rows_dec_env == 2) && p <= 128 &&
-        pr->md_cap >= 1 && !(dyn_cand && rows_dec_env != 2)) {
+    if (will_cr_dec) {
       P.cr_dec = true;
       P.cr_items += b * g;
     }
@@ -863,7 +881,7 @@ int run_tc(const ba_problem_t* pr, const Plan& P, const void* q, const void* Kc,
       rc = make_tmap_3d(&cp.tmQ, q, d, pr->h, pr->b, d * 2, (uint64_t)pr->h * d * 2, p, 128 / p);
     }
     if (rc) return rc;
-    cp.R = pr->b * p; cp.nrb = P.cr_nrb;
+    cp.R = pr->b * p; cp.nrb = P.cr_nrb; cp.nrp = P.cr_nrp;
     cp.ntile = P.cr_ntile; cp.tps = P.cr_tps; cp.nsplit = P.cr_nsplit; cp.items = P.cr_items;
     cp.scale_log2 = scale_log2;
     cp.S = P.S;
@@ -883,12 +901,16 @@ int run_tc(const ba_problem_t* pr, const Plan& P, const void* q, const void* Kc,
     }
     cp.ws_o = bp.ws_o;
     cp.ws_ml = bp.ws_ml;
-    static bool attr_done[64];
-    if (int rc2 = ensure_smem_attr(ba::ctx_rows_kernel, ba::ctxr::kSmem, attr_done)) return rc2;
+    static bool attr_done[64], attr_done2[64];
+    if (P.cr_v2) {
+      if (int rc2 = ensure_smem_attr(ba::ctx_rows2_kernel, ba::ctxr2::kSmem, attr_done2)) return rc2;
+    } else if (int rc2 = ensure_smem_attr(ba::ctx_rows_kernel, ba::ctxr::kSmem, attr_done)) {
+      return rc2;
+    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(P.cr_grid);
-    cfg.blockDim = dim3(ba::ctxr::kThreads);
-    cfg.dynamicSmemBytes = ba::ctxr::kSmem;
+    cfg.blockDim = dim3(P.cr_v2 ? ba::ctxr2::kThreads : ba::ctxr::kThreads);
+    cfg.dynamicSmemBytes = P.cr_v2 ? ba::ctxr2::kSmem : ba::ctxr::kSmem;
     cfg.stream = st;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -896,7 +918,8 @@ int run_tc(const ba_problem_t* pr, const Plan& P, const void* q, const void* Kc,
     cfg.attrs = at;
     cfg.numAttrs = 1;
     rec.begin();
-    const cudaError_t e = cudaLaunchKernelEx(&cfg, ba::ctx_rows_kernel, cp);
+    const cudaError_t e = P.cr_v2 ? cudaLaunchKernelEx(&cfg, ba::ctx_rows2_kernel, cp)
+                                  : cudaLaunchKernelEx(&cfg, ba::ctx_rows_kernel, cp);
     if (e != cudaSuccess) {
       g_last_cuda_error = (int)e;
       rec.end();
@@ -1364,15 +1387,15 @@ const char* ba_plan_string(const ba_problem_t* prob) {
   if (P.dyn) snprintf(dyn_tag, sizeof dyn_tag, ",dec=cuda_core_dyn(parts=%d)", P.dparts);
   if (P.tc && P.cr_dec)
     snprintf(g_plan_buf, sizeof g_plan_buf,
-             "ctx_rows(blocks=%d,splits=%d,tiles/split=%d,items=%d+%d dec,ctas=%d) + merge "
+             "ctx_rows%s(blocks=%d,splits=%d,tiles/split=%d,items=%d+%d dec,ctas=%d) + merge "
              "launches=2 ws=%zu",
-             P.cr_nrb, P.cr_nsplit, P.cr_tps, P.cr_items_ctx, P.cr_items - P.cr_items_ctx,
+             P.cr_v2 ? "2" : "", P.cr_nrb, P.cr_nsplit, P.cr_tps, P.cr_items_ctx, P.cr_items - P.cr_items_ctx,
              P.cr_grid, P.ws_bytes);
   else if (P.tc && P.ctx_rows)
     snprintf(g_plan_buf, sizeof g_plan_buf,
-             "ctx_rows(blocks=%d,splits=%d,tiles/split=%d,items=%d,ctas=%d) + "
+             "ctx_rows%s(blocks=%d,splits=%d,tiles/split=%d,items=%d,ctas=%d) + "
              "dec_tc(N=%d,dec_tiles=%lld%s,ctas=%d,stages=%d,slots=%d+%d) launches=2 ws=%zu",
-             P.cr_nrb, P.cr_nsplit, P.cr_tps, P.cr_items, P.cr_grid, P.tc_N,
+             P.cr_v2 ? "2" : "", P.cr_nrb, P.cr_nsplit, P.cr_tps, P.cr_items, P.cr_grid, P.tc_N,
              P.dyn ? (long long)prob->b * prob->g * P.tc_ntile_d : P.tc_T, dyn_tag,
              P.tc_G, P.tc_nst, P.tc_Sc, P.tc_Sd, P.ws_bytes);
   else if (P.tc)

@@ -44,6 +44,7 @@ struct CtxRowsParams {
   // (., rb*128) (g = 1: a block's rows are consecutive); 0 = thread loads
   CUtensorMap tmQ;
   int q_mode;
+  int nrp;                 // ctx_rows2_kernel: row-block pairs per group (items pair blocks 2rp, 2rp+1)
   const int32_t* lens;     // decode items: valid length min(clamp(lens[i]) + lens_add, dec_cap)
   int dec_cap, lens_add;
   AppendSrc app;           // append+attend: this step's rows, stored by the decode item's CTA

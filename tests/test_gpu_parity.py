@@ -311,6 +311,24 @@ def test_dyn_decode_parts_all_rows(cfg):
         compare(out, lse, ref, ref_lse, cfg.torch_dtype, f"{cfg.name} {variant} {plan[:60]}")
 
 
+@pytest.mark.parametrize("cfg", [
+    # two-block ping-pong rows kernel (context-only launch): a partly filled
+    # block B, an odd block count (last pair without B), g = 1 (Q rows by a
+    # 2-D box), ragged decode lengths in the dynamic decode launch
+    Config("rows2_b200", "bf16", b=200, h=2, g=2, d=128, mc=1500, md=700),
+    Config("rows2_b130", "bf16", b=130, h=4, g=4, d=128, mc=900, md=300),
+    Config("rows2_mqa_odd", "bf16", b=300, h=1, g=1, d=128, mc=1000, md=2000),
+], ids=lambda c: c.name)
+def test_rows2_kernel_all_rows(cfg):
+    prob = ba.make_problem(cfg.b, cfg.h, cfg.g, cfg.d, cfg.mc, cfg.md, cfg.torch_dtype)
+    plan = ba.ba_plan_string(prob)
+    assert plan.startswith("ctx_rows2"), plan
+    inp = make_inputs(cfg, 88, variant="ragged")
+    out, lse = run_gpu(inp)
+    ref, ref_lse = oracle_rows(inp)
+    compare(out, lse, ref, ref_lse, cfg.torch_dtype, f"{cfg.name} {plan[:60]}")
+
+
 def test_fma_and_tc_plans_share_one_workspace():
     """One workspace serves the CUDA-core plan (n = 1, b*p = 8 rows) and the
     tensor-core plan (n = 4: 32 rows, grid barrier) alternately: the FMA plan
