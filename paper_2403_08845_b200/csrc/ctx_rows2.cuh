@@ -210,8 +210,11 @@ __global__ void __launch_bounds__(ctxr2::kThreads, 1)
       bool pendB = false;
       uint32_t pendB_u = 0;
       bool pendB_first = false;
+      Prof pf;
       auto qk = [&](int x, uint32_t st) {
+        pf.mark(6);
         if (nP[x] > 0) tc::mbar_wait_sleep(tc::smem_u32(&pv_done[x]), (nP[x] - 1) & 1);  // S/P slot free
+        pf.mark(2);
         tc::tc_fence_after();
         const uint32_t qbase = tc::smem_u32(smem + kQ + x * 32768);
         const uint32_t kb = tc::smem_u32(smem + st * kStage);
@@ -222,11 +225,16 @@ __global__ void __launch_bounds__(ctxr2::kThreads, 1)
           tc::mma_bf16(tS + x * 128, ad, bd, IDESC_QK, kk > 0 ? 1u : 0u);
         }
         tc::mma_commit(tc::smem_u32(&s_full[x]));
+        pf.mark(3);
       };
       auto pv = [&](int x, uint32_t v, bool first, bool release_v) {
+        pf.mark(6);
         if (first) tc::mbar_wait_sleep(tc::smem_u32(&o_empty[x]), (nIt[x] & 1) ^ 1);  // O drained
+        pf.mark(7);
         tc::mbar_wait_sleep(tc::smem_u32(&v_cvt[v % kNst]), (v / kNst) & 1);
+        pf.mark(4);
         tc::mbar_wait_sleep(tc::smem_u32(&p_full[x]), nP[x] & 1);
+        pf.mark(5);
         tc::tc_fence_after();
         const uint32_t vb = tc::smem_u32(smem + (v % kNst) * kStage + 32768);
 #pragma unroll
@@ -241,10 +249,14 @@ __global__ void __launch_bounds__(ctxr2::kThreads, 1)
       for (int k = blockIdx.x; k < P.items; k += gridDim.x) {
         const Item I = item_of(k);
         if (I.t1 == I.t0) continue;
+        pf.mark(6);
         tc::mbar_wait_sleep(tc::smem_u32(q_full), it & 1);
+        pf.mark(0);
         for (int t = I.t0; t < I.t1; ++t, ++u) {
           const uint32_t st = u % kNst;
+          pf.mark(6);
           tc::mbar_wait_sleep(tc::smem_u32(&k_full[st]), (u / kNst) & 1);
+          pf.mark(1);
           qk(0, st);                                     // QK_A(u)
           if (pendB) {                                   // PV_B(u-1): releases V(u-1)
             pv(1, pendB_u, pendB_first, true);
@@ -271,6 +283,8 @@ __global__ void __launch_bounds__(ctxr2::kThreads, 1)
         }
         ++it;
       }
+      pf.mark(6);
+      pf.dump(P.trace ? P.trace + (size_t)blockIdx.x * 1024 : nullptr, 520);  // (0..40: the fused kernel's)
     }
   } else if (warp == 2 || warp == 3) {
     // ============ V converters: bf16 V tile -> f16 * 2^-8 in place (R23) ============
@@ -304,6 +318,7 @@ __global__ void __launch_bounds__(ctxr2::kThreads, 1)
     const uint32_t tSx = tS + x * 128, tOx = tO + x * 128;
     const float sl2 = P.scale_log2;
     uint32_t n = 0, nit = 0;  // this block's tiles / items
+    Prof pf;
     for (int k = blockIdx.x; k < P.items; k += gridDim.x) {
       const Item I = item_of(k);
       const int rb = 2 * I.rp + x;
@@ -325,14 +340,17 @@ __global__ void __launch_bounds__(ctxr2::kThreads, 1)
       }
       const int Lrow = I.dec && P.ntok > 1 ? max(I.L - (P.ntok - 1 - r % P.ntok), 0) : I.L;
       float m = kNegInf, l = 0.f;
+      pf.mark(0);
       for (int t = I.t0; t < I.t1; ++t, ++n) {
         tc::mbar_wait(tc::smem_u32(&s_full[x]), n & 1);
+        pf.mark(1);
         tc::tc_fence_after();
         float xs[128];
 #pragma unroll
         for (int q = 0; q < 4; ++q)
           tc::tmem_ld<32>(tSx + q * 32 + lane_addr, reinterpret_cast<uint32_t*>(xs) + q * 32);
         tc::tmem_ld_wait();
+        pf.mark(2);
         // row max on the raw logits (the scale is positive), 8 chains
         const int nvalid = min(128, Lrow - t * 128);
         float mq[8];
@@ -350,6 +368,7 @@ __global__ void __launch_bounds__(ctxr2::kThreads, 1)
         }
         const float mx = fmaxf(fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3])),
                                fmaxf(fmaxf(mq[4], mq[5]), fmaxf(mq[6], mq[7]))) * sl2;
+        pf.mark(3);
         if (m == kNegInf || mx > m + kTh) {
           // raise the reference to the exact max; rescale l and the O row (PV(u-1)
           // of this block completed before QK(u) was issued: O is quiescent)
@@ -369,6 +388,7 @@ __global__ void __launch_bounds__(ctxr2::kThreads, 1)
           }
           m = mx;
         }
+        pf.mark(5);
         const float mref = m == kNegInf ? 0.f : m;
         const float2 sl2v = make_float2(sl2, sl2), nmv = make_float2(-mref, -mref);
         float2 lq[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
@@ -389,6 +409,7 @@ __global__ void __launch_bounds__(ctxr2::kThreads, 1)
         tc::tc_fence_before();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(tc::smem_u32(&p_full[x]));
+        pf.mark(6);
       }
       // ---- the item's partial: O row (relative to 2^m), m, l ----
       tc::mbar_wait(tc::smem_u32(&pv_done[x]), (n - 1) & 1);  // this block's last PV
@@ -412,7 +433,9 @@ __global__ void __launch_bounds__(ctxr2::kThreads, 1)
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(tc::smem_u32(&o_empty[x]));
       ++nit;
+      pf.mark(7);
     }
+    if (threadIdx.x == 128) pf.dump(P.trace ? P.trace + (size_t)blockIdx.x * 1024 : nullptr, 512);
   }
   tc::tc_fence_before();
   __syncthreads();

@@ -26,8 +26,17 @@ MMA = ["q_full_wait", "k_full_wait", "s_free_wait", "QK_issue", "v_cvt_wait", "p
 
 
 def run(name):
-    cfg = CONFIGS[name]
-    inp = make_inputs(cfg, seed_for(name), device="cuda")
+    base = 0
+    if name.startswith("v2:"):
+        # the two-block kernel (ctx_rows2.cuh) dumps at slots 512 / 520; shape
+        # "v2:b,h,g,mc,md" (a context-only rows launch)
+        from synth import Config
+        b, h, g, mc, md = map(int, name[3:].split(","))
+        cfg = Config(name, "bf16", b=b, h=h, g=g, d=128, mc=mc, md=md)
+        base = 512
+    else:
+        cfg = CONFIGS[name]
+    inp = make_inputs(cfg, seed_for(name) if name in CONFIGS else 5, device="cuda")
     out = torch.empty_like(inp.q)
     prob = ba.make_problem(cfg.b, cfg.h, cfg.g, cfg.d, cfg.mc, cfg.md, cfg.torch_dtype, inp.scale)
     ws = ba.alloc_workspace(prob, "cuda")
@@ -45,10 +54,10 @@ def run(name):
     torch.cuda.synchronize()
     lib.ba_set_trace_buffer(None)
     tr = buf.view(160, 1024).cpu()
-    rows = [r for r in tr.tolist() if any(r[:16])]
+    rows = [r for r in tr.tolist() if any(r[base:base + 16])]
     n = len(rows)
-    sm = {k: sum(r[i] for r in rows) / n / 1e3 for i, k in enumerate(SM)}
-    mma = {k: sum(r[8 + i] for r in rows) / n / 1e3 for i, k in enumerate(MMA)}
+    sm = {k: sum(r[base + i] for r in rows) / n / 1e3 for i, k in enumerate(SM)}
+    mma = {k: sum(r[base + 8 + i] for r in rows) / n / 1e3 for i, k in enumerate(MMA)}
     print(json.dumps({"config": name, "plan": ba.ba_plan_string(prob), "ctas": n,
                       "softmax_thread_kcycles": {k: round(v, 1) for k, v in sm.items()},
                       "mma_lane_kcycles": {k: round(v, 1) for k, v in mma.items()}}), flush=True)
