@@ -55,6 +55,55 @@ __global__ void __launch_bounds__(256) merge_kernel(const MergeParams P) {
   auto slot_of = [&](int k) { return k < nctx ? k : P.dec_slot0 + (k - nctx); };
   const float* ml = P.ws_ml + (size_t)warp * P.S * 2;
   const float* o = P.ws_o + (size_t)warp * P.S * D;
+  if constexpr (D == 128) {
+    if (ntot <= 32) {
+      // one load round trip: every lane's (m, l) of partial `lane` AND the
+      // float4 slices (d = 4 lane ..) of the first 8 partials' rows go out
+      // together; later batches of 8 (rare) follow
+      const float2 mlk = lane < ntot ? __ldcg(reinterpret_cast<const float2*>(ml) + slot_of(lane))
+                                     : make_float2(kNegInf, 0.f);
+      float4 ov[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        ov[q] = q < ntot ? __ldcg(reinterpret_cast<const float4*>(o + (size_t)slot_of(q) * D) + lane)
+                         : make_float4(0.f, 0.f, 0.f, 0.f);
+      float M = mlk.x;
+#pragma unroll
+      for (int off = 16; off >= 1; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
+      const float Ms = (M == kNegInf) ? 0.f : M;
+      const float wl = lane < ntot ? ex2(mlk.x - Ms) : 0.f;
+      float L = wl * mlk.y;
+#pragma unroll
+      for (int off = 16; off >= 1; off >>= 1) L += __shfl_xor_sync(0xffffffffu, L, off);
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int k0 = 0; k0 < ntot; k0 += 8) {
+        if (k0 > 0) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            ov[q] = k0 + q < ntot ? __ldcg(reinterpret_cast<const float4*>(o + (size_t)slot_of(k0 + q) * D) + lane)
+                                  : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const float wq = __shfl_sync(0xffffffffu, wl, (k0 + q) & 31);
+          if (k0 + q < ntot) {
+            acc.x = fmaf(wq, ov[q].x, acc.x); acc.y = fmaf(wq, ov[q].y, acc.y);
+            acc.z = fmaf(wq, ov[q].z, acc.z); acc.w = fmaf(wq, ov[q].w, acc.w);
+          }
+        }
+      }
+      const float invL = P.vscale / L;
+      if constexpr (sizeof(T) == 2) {
+        const uint2 packed = make_uint2(pack_bf16x2(acc.x * invL, acc.y * invL), pack_bf16x2(acc.z * invL, acc.w * invL));
+        *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(P.out) + (size_t)warp * D + 4 * lane) = packed;
+      } else {
+        *reinterpret_cast<float4*>(reinterpret_cast<float*>(P.out) + (size_t)warp * D + 4 * lane) =
+            make_float4(acc.x * invL, acc.y * invL, acc.z * invL, acc.w * invL);
+      }
+      if (P.lse && lane == 0) P.lse[warp] = (M + lg2(L)) * kLn2;
+      return;
+    }
+  }
   // (m, l) of up to 32 partials per round, one per lane: the row max and the
   // weights take one load round trip instead of one per partial
   float M = kNegInf;
