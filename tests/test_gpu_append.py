@@ -35,6 +35,12 @@ CASES = [
     (Config("ap_gqa_n3", "bf16", b=6, h=16, g=4, d=128, mc=400, md=50), 3),
     (Config("ap_fp32", "fp32", b=4, h=4, g=2, d=64, mc=100, md=20), 2),
     (Config("ap_mqa", "bf16", b=4, h=48, g=1, d=128, mc=300, md=40), 1),  # rows kernel + merge
+    # rows kernel (context) + the early-start dynamic decode launch (p = 1)
+    (Config("ap_rows_dyn", "bf16", b=80, h=4, g=4, d=128, mc=300, md=700), 1),
+    # the same with the two-block rows kernel (>= 2 row blocks) and decode parts
+    (Config("ap_rows2_dyn", "bf16", b=200, h=2, g=2, d=128, mc=500, md=1400), 1),
+    # fused kernel, dynamic columns cut into parts (few long columns)
+    (Config("ap_dyn_parts", "bf16", b=16, h=2, g=2, d=128, mc=200, md=2500), 1),
 ]
 
 
