@@ -774,31 +774,22 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
   const int r0 = (int)((long long)blockIdx.x * rows / P.G);
   const int r1 = (int)((long long)(blockIdx.x + 1) * rows / P.G);
 
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < NST; ++s) {
-      tc::mbar_init(tc::smem_u32(&kv_full[s]), 1);
-      // released by the PV commit (+ NSW - 1 plain arrivals) after an MMA tile,
-      // by the NSW softmax warps after a CUDA-core decode tile (dyn)
-      tc::mbar_init(tc::smem_u32(&kv_empty[s]), NSW);
-      if (KV8) {
-        tc::mbar_init(tc::smem_u32(&k_cvt[s]), 4);
-        tc::mbar_init(tc::smem_u32(&v_cvt[s]), 4);
-      }
-    }
-    if (KV8)
-      for (int s = 0; s < 2; ++s) tc::mbar_init(tc::smem_u32(&q_cvt[s]), 4);
-    for (int s = 0; s < 2; ++s) {
-      tc::mbar_init(tc::smem_u32(&q_full[s]), 1);
-      tc::mbar_init(tc::smem_u32(&q_empty[s]), 1);
-      tc::mbar_init(tc::smem_u32(&s_full[s]), 1);
-      tc::mbar_init(tc::smem_u32(&s_free[s]), NSW);
-      tc::mbar_init(tc::smem_u32(&p_full[s]), NSW);
-      tc::mbar_init(tc::smem_u32(&p_empty[s]), 1);
-      tc::mbar_init(tc::smem_u32(&o_full[s]), 1);
-      tc::mbar_init(tc::smem_u32(&o_empty[s]), 4);
-      tc::mbar_init(tc::smem_u32(&e_full[s]), 32 * NSW);  // every softmax thread (once per segment)
-      tc::mbar_init(tc::smem_u32(&e_empty[s]), 128);      // every epilogue thread
-    }
+  if (threadIdx.x < 46) {
+    // one mbarrier per thread (bars[t]; a serial init of ~40 barriers by one
+    // thread cost ~0.5 us of the prologue): arrival counts by role
+    const int t = threadIdx.x;
+    uint32_t cnt = 0;
+    if (t < 8) cnt = t < NST ? 1 : 0;                              // kv_full
+    else if (t < 16) cnt = t - 8 < NST ? NSW : 0;                  // kv_empty: PV commit + NSW-1, or NSW warps (dyn)
+    else if (t < 22) cnt = 1;                                      // q_full, q_empty, s_full
+    else if (t < 26) cnt = NSW;                                    // s_free, p_full
+    else if (t < 30) cnt = 1;                                      // p_empty, o_full
+    else if (t < 32) cnt = 4;                                      // o_empty
+    else if (t < 34) cnt = 32 * NSW;                               // e_full: every softmax thread
+    else if (t < 36) cnt = 128;                                    // e_empty: every epilogue thread
+    else if (t < 44) cnt = KV8 && ((t - 36) & 3) < NST ? 4 : 0;    // k_cvt, v_cvt
+    else cnt = KV8 ? 4 : 0;                                        // q_cvt
+    if (cnt) tc::mbar_init(tc::smem_u32(&bars[t]), cnt);
     tc::fence_mbar_init();
   }
   if (warp == 0 && lane == 0) {

@@ -739,7 +739,11 @@ int launch_bif_tc_n(const ba::BifTcParams& bp, int smem, uint32_t flags, LaunchR
   // kernel leaves free: not cooperative (its grid barrier still completes —
   // the rows kernel ends on its own and frees the rest); every other launch
   // is cooperative (all CTAs co-resident before the grid barrier)
+#ifdef BIFATTN_NONCOOP
+  const bool coop = false;  // experiment: every fused launch non-cooperative
+#else
   const bool coop = !(bp.ext_ctx > 0 && bp.Tc == 0);
+#endif
   static bool attr_done[64];
   if (int rc = ensure_smem_attr(ba::bif_tc_kernel<N, SWG, MT, KV8>, 227 * 1024, attr_done)) return rc;
   // one cooperative launch (all CTAs co-resident: the kernel ends with a grid
