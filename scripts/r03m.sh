@@ -2,7 +2,7 @@ set -x
 OUT=gpurun_out/${TAG:-r03m}
 mkdir -p $OUT
 python -c "import __graft_entry__ as g; g.build()" > $OUT/build.txt 2>&1
-for c in mqa gqa; do PROBE_STEPS=3 timeout -k 5 90 python scripts/hang_probe.py $c 20 >> $OUT/probe.txt 2>&1; echo "exit $?" >> $OUT/probe.txt; done
+for c in ${PROBE_CFGS:-mqa gqa}; do PROBE_STEPS=3 timeout -k 5 90 python scripts/hang_probe.py $c 20 >> $OUT/probe.txt 2>&1; echo "exit $?" >> $OUT/probe.txt; done
 cut -c1-200 $OUT/probe.txt
 grep -q '"finished": false' $OUT/probe.txt && exit 1
 timeout -k 10 900 python -m pytest tests -m gpu -q -x --timeout 120 -rA > $OUT/pytest_gpu.txt 2>&1
