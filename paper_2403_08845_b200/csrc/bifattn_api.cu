@@ -512,8 +512,15 @@ int make_plan(const ba_problem_t* pr_in, int sms, bool replicated, Plan* pl) {
       // (column, part) units: at least ~6 per CTA so the queue balances the
       // CTAs, parts of >= 2 tiles (each part pays a q load and a join)
       const long long ncol = (long long)b * g;
-      long long parts = (6LL * P.tc_G + ncol - 1) / ncol;
-      if (parts > (P.tc_ntile_d + 1) / 2) parts = (P.tc_ntile_d + 1) / 2;
+#ifndef BIFATTN_DYN_UNITS
+#define BIFATTN_DYN_UNITS 6
+#endif
+#ifndef BIFATTN_DYN_MIN_TILES
+#define BIFATTN_DYN_MIN_TILES 2
+#endif
+      long long parts = ((long long)BIFATTN_DYN_UNITS * P.tc_G + ncol - 1) / ncol;
+      if (parts > (P.tc_ntile_d + BIFATTN_DYN_MIN_TILES - 1) / BIFATTN_DYN_MIN_TILES)
+        parts = (P.tc_ntile_d + BIFATTN_DYN_MIN_TILES - 1) / BIFATTN_DYN_MIN_TILES;
       if (parts < 1) parts = 1;
       P.dunit = (int)((P.tc_ntile_d + parts - 1) / parts);
       P.dparts = (P.tc_ntile_d + P.dunit - 1) / P.dunit;
