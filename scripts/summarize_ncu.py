@@ -15,7 +15,7 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 TAG2CFG = {"b32": "mha7b_b32", "b16": "mha7b_b16", "gqa": "gqa", "mqa": "mqa", "long": "long",
-           "fp8": "mha7b_b32_fp8"}
+           "fp8": "mha7b_b32_fp8", "long_rows2": "long_rows2"}
 KEYS = ["Duration", "DRAM Throughput", "Memory Throughput", "Compute (SM) Throughput",
         "Executed Ipc Active", "Issue Slots Busy", "L1/TEX Hit Rate", "L2 Hit Rate",
         "No Eligible", "Warp Cycles Per Issued Instruction", "Registers Per Thread",
