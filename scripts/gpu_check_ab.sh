@@ -1,3 +1,4 @@
+# GPU check of a change: hang probe of PROBE_CFGS, pytest -m gpu, and interleaved A/Bs (scripts/ab.py) of AB_CFGS against AB_DEFS (-D flags or --lib PATH); results under gpurun_out/$TAG
 set -x
 OUT=gpurun_out/${TAG:-r03m}
 mkdir -p $OUT
