@@ -123,12 +123,20 @@ typedef struct {
  *   n = 1 is exactly the single-token step. */
 
 /* Bytes of device workspace bifurcated_attn_decode() / replicated_attn_decode()
- * need: a grid-barrier word pair at offset 0, then fp32 partials (m, l, o[d])
- * per output row and split.  Returns 0 for an invalid problem.  The workspace
- * must be 16-byte aligned and ZEROED ONCE before its first use (cudaMemset);
- * every completed call leaves the barrier word reset, so one workspace serves
- * any number of back-to-back calls (and CUDA graph replays) on one stream.
- * Calls that may run concurrently need separate workspaces. */
+ * need: a 256-byte header (the fused kernel's grid barrier: a 64-bit arrival
+ * count that grows by 256 per launch; the dynamic decode-unit queue counter,
+ * left at 0 by every completed launch), then fp32 partials (m, l, o[d]) per
+ * output row and split.  Returns 0 for an invalid problem.  The workspace must
+ * be 16-byte aligned and ZEROED ONCE before its first use (cudaMemset); one
+ * workspace then serves any number of back-to-back calls of any problems (and
+ * CUDA graph replays) on one stream.  Calls that may run concurrently need
+ * separate workspaces.
+ * Concurrency note: the fused launch is cooperative (its grid barrier needs
+ * every CTA resident); the decode-only launch that follows the rows kernel
+ * (long contexts with many samples) is not, so that it can start on the SMs
+ * the rows kernel leaves free — it needs every SM of the device to become
+ * available to it eventually (no other kernel may occupy SMs indefinitely
+ * while it runs, e.g. one waiting on this step's output). */
 size_t ba_workspace_bytes(const ba_problem_t* prob);
 
 /* One decode step of bifurcated attention (see above).  Kc/Vc are read from
