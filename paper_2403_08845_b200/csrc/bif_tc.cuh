@@ -539,6 +539,7 @@ BA_DEVINL void dyn_cc_multi(const BifTcParams& P, const DynSmem& S, int sw, int 
       }
       const int i = col / P.g, c = col - i * P.g;
       const size_t gr = (size_t)i * P.h + c * PQ + r;
+      BA_CHECK(gr < (size_t)P.b * P.h && P.Sc + part < P.S && (c + 1) * PQ <= P.h);
       *reinterpret_cast<float4*>(P.ws_o + (gr * P.S + P.Sc + part) * kD + 4 * lane) = od;
       if (lane == 0) reinterpret_cast<float2*>(P.ws_ml)[gr * P.S + P.Sc + part] = make_float2(M, ls);
     }
@@ -611,6 +612,7 @@ BA_DEVINL void warp_col_reduce(float* v, int lane) {
 // ----------------------------------------------------------------------------
 BA_DEVINL void merge_row(const BifTcParams& P, int gr, int lane, int nctx, int ndec) {
   const int n = nctx + ndec;
+  BA_CHECK(gr >= 0 && gr < P.b * P.h && nctx <= P.Sc && P.Sc + ndec <= P.S);
   const float2* ml = reinterpret_cast<const float2*>(P.ws_ml) + (size_t)gr * P.S;
   const float* obuf = P.ws_o + (size_t)gr * P.S * bif::kD;
   float M = kNegInf, Lsum = 0.f;
@@ -763,6 +765,10 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
   int* sm_mcnt = reinterpret_cast<int*>(bars + 64);  // [16 warps][2]: merge part counts
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // every shared-memory region this plan uses lies inside the launch's allocation
+  BA_CHECK(threadIdx.x != 0 ||
+           (uint32_t)(reinterpret_cast<uint8_t*>(bars + 64) + 128 - smem) +
+                   (uint32_t)(P.dyn && P.p > 1 ? bif::cc_extra_bytes(P.p) : 0) <= dyn_smem_bytes());
   auto tstamp = [&](int slot, unsigned long long tag) {
     if (kStamp && P.trace) P.trace[(size_t)blockIdx.x * kTraceSlots + slot] = (gtimer() & 0x00ffffffffffffffull) | (tag << 56);
 #ifdef BIFATTN_PROF
@@ -966,6 +972,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
           const int cp = (int)(col - (unsigned)i * gp);  // c * dparts + part
           const int c = cp / P.dparts, part = cp - c * P.dparts;
           const int t0 = part * P.dunit;
+          BA_CHECK(i < P.b && c < P.g && part < P.dparts && L >= 0 && L <= P.lens_offset + P.dec_cap);
           if (P.app.n > 0) {  // append+attend: this unit's new rows before its TMA
             append_rows_warp(P.app, i, c, clamp_len(P.lens, i, P.dec_cap), t0 * kBM,
                              (t0 + P.dunit) * kBM, lane);
@@ -1733,6 +1740,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
             }
             const int i = col / P.g, c = col - i * P.g;
             const size_t gr = (size_t)i * P.h + c;  // p = 1
+            BA_CHECK(gr < (size_t)P.b * P.h && P.Sc + part < P.S);
             P.ws_o[(gr * P.S + P.Sc + part) * kD + d] = od;
             if (d == 0) reinterpret_cast<float2*>(P.ws_ml)[gr * P.S + P.Sc + part] = make_float2(M, ls);
           }
@@ -1788,6 +1796,7 @@ __global__ void __launch_bounds__(32 * (8 + 4 * SWG), 1)
         ri = r0 / P.p;
         rj = r0 - ri * P.p;
       }
+      BA_CHECK(s.slot >= 0 && s.slot < P.S);
       float* const wo = P.ws_o + (size_t)s.slot * kD + d;
       const size_t row_stride = (size_t)P.S * kD;
 #pragma unroll

@@ -7,7 +7,32 @@
 
 #define BA_DEVINL __device__ __forceinline__
 
+// Device-side bounds checks of a -DBIFATTN_CHECKS variant build (the GPU test
+// suite runs against it: BIFATTN_TEST_LIB, tests/conftest.py; a failed check
+// prints its line and traps).  Compiled out of the product library.
+#ifdef BIFATTN_CHECKS
+#include <cstdio>
+#define BA_CHECK(c)                                                               \
+  do {                                                                            \
+    if (!(c)) {                                                                   \
+      printf("BA_CHECK failed: %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, #c, \
+             (int)blockIdx.x, (int)threadIdx.x);                                  \
+      __trap();                                                                   \
+    }                                                                             \
+  } while (0)
+#else
+#define BA_CHECK(c) \
+  do {              \
+  } while (0)
+#endif
+
 namespace ba {
+
+BA_DEVINL uint32_t dyn_smem_bytes() {
+  uint32_t v;
+  asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(v));
+  return v;
+}
 
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;

@@ -371,6 +371,7 @@ __global__ void __launch_bounds__(ctxr::kThreads, 1)
       const int c = I.c, s = I.s, t0 = I.t0, t1 = I.t1;
       const int rg = I.rb * 128 + r;                    // row within the group (context)
       const bool valid_row = I.dec ? r < P.p : rg < P.R;
+      BA_CHECK(I.s >= 0 && I.s < P.S && I.c < P.g && (!I.dec || I.i < P.b));
       const int gr = !valid_row ? -1
                      : I.dec ? I.i * P.h + c * P.p + r
                              : (rg / P.p) * P.h + c * P.p + rg % P.p;

@@ -324,6 +324,7 @@ __global__ void __launch_bounds__(ctxr2::kThreads, 1)
       const int rb = 2 * I.rp + x;
       const int rg = rb * 128 + r;
       const bool valid_row = I.dec ? r < P.p : rg < P.R;
+      BA_CHECK(I.s >= 0 && I.s < P.S && I.c < P.g && (!I.dec || I.i < P.b));
       const int gr = !valid_row ? -1
                      : I.dec ? I.i * P.h + I.c * P.p + r
                              : (rg / P.p) * P.h + I.c * P.p + rg % P.p;

@@ -11,6 +11,13 @@ if ROOT not in sys.path:
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a B200 (sm_100a) GPU")
     config.addinivalue_line("markers", "slow: long-running")
+    # BIFATTN_TEST_LIB=<path>: run the suite against a variant build of the same
+    # sources (e.g. the -DBIFATTN_CHECKS device-bounds-check build)
+    lib = os.environ.get("BIFATTN_TEST_LIB")
+    if lib:
+        import paper_2403_08845_b200 as ba
+
+        ba.load_library(lib)
 
 
 def pytest_collection_modifyitems(config, items):
